@@ -1,0 +1,278 @@
+/*
+ * bagpipe_b200.h -- C ABI of the B200-native BagPipe embedding-access path.
+ *
+ * The reference (embcache 0.1.0, a pure Python/numpy package) has no FFI:
+ * its "plugin API" is the Python module API.  Each entry point below replaces
+ * the numpy/dict body of one reference function; the Python package
+ * paper_2202_12429_b200 keeps the reference's names and binds these symbols
+ * with ctypes (see INTEGRATION.md for the binding a maintainer would add to
+ * the reference itself).
+ *
+ * Conventions
+ *   - Every function returns a status: BP_OK or one BP_ERR_* code.  Codes map
+ *     1:1 to the reference exception classes (reference errors.py:6-77).
+ *     Nothing throws across the ABI.
+ *   - Pointers named d_* are device pointers (cudaMalloc / torch CUDA
+ *     tensors); h_* are host pointers.  Streams are cudaStream_t passed as
+ *     void*.  All work is asynchronous on the given stream unless the comment
+ *     says "synchronises".
+ *   - Counts that a previous kernel produced may be passed as a device
+ *     pointer (d_n, int64); the matching host ``n`` is then an upper bound.
+ *     Pass d_n = NULL to use ``n`` as the exact count.
+ *   - Device-side contract violations (cache miss, duplicate insert, ...) are
+ *     recorded in the context's bp_error_t (first error in (iteration, index)
+ *     order wins) and surfaced by bp_ctx_check, which synchronises.
+ *   - Keys are packed u64: (table_id << 44) | row_id (reference engine.py:117-121).
+ */
+#ifndef BAGPIPE_B200_H
+#define BAGPIPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BP_OK 0
+#define BP_ERR_CONFIG 1         /* ConfigurationError   */
+#define BP_ERR_CACHE_MISS 2     /* CacheMissError(key, iteration) */
+#define BP_ERR_CACHE_CAPACITY 3 /* CacheCapacityError   */
+#define BP_ERR_CACHE_ORDERING 4 /* CacheOrderingError   */
+#define BP_ERR_STORE_KEY 5      /* StoreKeyError        */
+#define BP_ERR_STORE 6          /* StoreError           */
+#define BP_ERR_ENGINE 7         /* EngineError          */
+#define BP_ERR_CUDA 100         /* CUDA runtime failure */
+#define BP_ERR_OOM 101          /* allocation failure   */
+#define BP_ERR_INVALID 102      /* bad argument at the ABI (ConfigurationError) */
+
+typedef void* bp_stream_t; /* cudaStream_t */
+
+typedef struct bp_error_t {
+  int32_t code; /* BP_ERR_* or 0 */
+  int32_t lock;
+  int64_t iteration;
+  int64_t index; /* position of the offending key in the call's key order */
+  uint64_t key;  /* packed key */
+} bp_error_t;
+
+typedef struct bp_ctx bp_ctx;
+typedef struct bp_schema bp_schema;
+typedef struct bp_prep bp_prep;
+typedef struct bp_planner bp_planner;
+typedef struct bp_cache bp_cache;
+typedef struct bp_store bp_store;
+
+/* ---------------------------------------------------------------- context */
+const char* bp_version(void);
+const char* bp_last_error_message(void);
+int bp_ctx_create(bp_ctx** out);
+int bp_ctx_destroy(bp_ctx* ctx);
+/* Synchronises the stream, copies the error record out and clears it. */
+int bp_ctx_check(bp_ctx* ctx, bp_stream_t stream, bp_error_t* h_out);
+
+/* ----------------------------------------------------------------- schema
+ * Schema = table cardinalities; dense id g = table_base[t] + row is monotone
+ * in (table, row) and indexes every per-row array (store rows, cache slot map,
+ * planner tracker).  Replaces reference traces.py:42-71 (Schema). */
+int bp_schema_create(int32_t num_tables, const int64_t* h_rows_per_table, int32_t emb_dim, bp_schema** out);
+int bp_schema_destroy(bp_schema* schema);
+int64_t bp_schema_total_rows(const bp_schema* schema);
+
+/* ------------------------------------------------------------ batch prep
+ * Replaces Batch.unique_keys (reference traces.py:91-103) and _prep_batch
+ * (reference engine.py:142-182): dedupe in first-occurrence order, key-sorted
+ * unique order, per-key occurrence lists in occurrence order (the order of
+ * np.add.at), per-occurrence labels and trainer-rank bounds.
+ * schema may be NULL (registry mode: keys of any table/row; ids are then
+ * assigned by the consumer objects).  d_keys/d_labels: n_occ entries, device.
+ * h_rank_bounds: num_ranks+1 occurrence positions (rank r owns
+ * [b[r], b[r+1])).  flags: BP_PREP_OCC_INDEX also materialises the
+ * occurrence -> unique (first-occurrence index) map.  row_bits/table_bits
+ * (registry mode only): bit widths of the largest row / table id, so the
+ * sort runs only over live key bits. */
+#define BP_PREP_OCC_INDEX 1
+int bp_prep_create(bp_ctx* ctx, const bp_schema* schema, const uint64_t* d_keys, const uint8_t* d_labels,
+                   int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks, int64_t iteration,
+                   int32_t flags, int32_t row_bits, int32_t table_bits, bp_stream_t stream, bp_prep** out);
+int bp_prep_destroy(bp_prep* prep);
+
+typedef struct bp_prep_view {
+  int64_t n_occ;
+  int64_t iteration;
+  int32_t num_ranks;
+  int32_t pad;
+  const int64_t* d_num_unique;   /* device scalar U */
+  const uint64_t* d_uniq_key_s;  /* [U] unique keys, key-sorted        */
+  const uint32_t* d_uniq_id_s;   /* [U] dense ids g (schema mode)      */
+  const uint64_t* d_uniq_key_k;  /* [U] unique keys, first-occurrence order */
+  const uint32_t* d_perm_s2k;    /* [U] sorted index -> first-occurrence index */
+  const uint32_t* d_perm_k2s;    /* [U] first-occurrence index -> sorted index */
+  const uint32_t* d_seg_start;   /* [U+1] CSR offsets (sorted order) into d_occ_pos */
+  const uint32_t* d_occ_pos;     /* [n_occ] occurrence positions grouped by key, ascending */
+  const uint8_t* d_occ_label;    /* [n_occ] label of d_occ_pos[j] */
+  const uint32_t* d_occ_k;       /* [n_occ] occurrence -> first-occurrence unique index (flag) */
+  const int64_t* d_rank_bounds;  /* [num_ranks+1] */
+} bp_prep_view;
+int bp_prep_get_view(const bp_prep* prep, bp_prep_view* out);
+/* Synchronises; host copy of U. */
+int bp_prep_num_unique(bp_prep* prep, bp_stream_t stream, int64_t* h_out);
+
+/* ---------------------------------------------------------------- planner
+ * Oracle Cacher state (reference lookahead.py:38-123).  The window queue and
+ * lookahead/halving decisions stay on the host (they are scalar); per-key
+ * state (latest_tracker, in_cache mirror) is device-resident.
+ * schema NULL => registry mode (GPU hash map key -> dense id). */
+int bp_planner_create(bp_ctx* ctx, const bp_schema* schema, int64_t capacity, bp_planner** out);
+int bp_planner_destroy(bp_planner* planner);
+/* emit_next_plan refill step for one appended batch: tracker[e] = iteration
+ * for every unique key (reference lookahead.py:75-82). */
+int bp_planner_refill(bp_planner* planner, bp_prep* prep, bp_stream_t stream);
+
+typedef struct bp_plan_buffers {
+  /* caller-allocated device buffers with room for U entries each */
+  uint64_t* d_prefetch_keys;  /* sorted by key */
+  uint32_t* d_prefetch_ids;   /* dense ids of the above (schema mode) */
+  int64_t* d_prefetch_ttls;   /* ttl of each prefetched key */
+  int64_t* d_ttl_k;           /* ttl per unique key, first-occurrence order */
+  uint64_t* d_evict_keys;     /* planner's evict set {e : ttl == iteration}, sorted */
+  int64_t* d_counts;          /* [4]: n_prefetch, n_evict, projected, resident_before */
+} bp_plan_buffers;
+
+typedef struct bp_planner_stats {
+  int64_t tracked;          /* len(latest_tracker) == projected occupancy */
+  int64_t in_cache;         /* len(in_cache) */
+  int64_t insertions;
+  int64_t removals;
+  int64_t peak_occupancy;
+  int64_t peak_projected;
+  int64_t last_projected;   /* projected occupancy recorded by the last pop */
+  int64_t last_prefetch;
+  int64_t last_evict;
+  int64_t registry_size;
+} bp_planner_stats;
+
+/* Pop step of emit_next_plan for the front batch (reference lookahead.py:84-110):
+ * records projected occupancy, assigns TTLs, prefetch/mirror, erases keys whose
+ * last windowed use is this batch.  Writes the plan into *bufs. */
+int bp_planner_pop(bp_planner* planner, bp_prep* prep, const bp_plan_buffers* bufs, bp_stream_t stream);
+/* Synchronises. */
+int bp_planner_get_stats(bp_planner* planner, bp_stream_t stream, bp_planner_stats* h_out);
+
+/* ------------------------------------------------------------------ cache
+ * Trainer TTL cache in HBM (reference cache.py:31-286): dense id -> slot map,
+ * row arena [capacity, dim] f32, ttl/dirty/used per slot, LIFO free list
+ * (lowest freed slot reused first, like reference cache.py:209-210). */
+int bp_cache_create(bp_ctx* ctx, const bp_schema* schema, int64_t capacity, int32_t dim, bp_cache** out);
+int bp_cache_destroy(bp_cache* cache);
+
+typedef struct bp_cache_stats {
+  int64_t occupancy;
+  int64_t insertions;
+  int64_t evictions;
+  int64_t peak_occupancy;
+  int64_t capacity;
+  int64_t registry_size;
+} bp_cache_stats;
+int bp_cache_get_stats(bp_cache* cache, bp_stream_t stream, bp_cache_stats* h_out); /* synchronises */
+
+/* apply_prefetch (reference cache.py:99-136): insert clean rows with TTLs.
+ * d_ids may be NULL (ids derived from keys).  Duplicate -> CACHE_ORDERING.
+ * Capacity is checked on the device too (CACHE_CAPACITY). */
+int bp_cache_insert(bp_cache* cache, const uint64_t* d_keys, const uint32_t* d_ids, const float* d_rows,
+                    const int64_t* d_ttls, int64_t n, const int64_t* d_n, int64_t iteration, bp_stream_t stream);
+/* apply_ttl_updates (reference cache.py:138-149); absent key -> CACHE_ORDERING. */
+int bp_cache_set_ttl(bp_cache* cache, const uint64_t* d_keys, const uint32_t* d_ids, const int64_t* d_ttls,
+                     int64_t n, const int64_t* d_n, int64_t iteration, bp_stream_t stream);
+/* resolve_slots (reference cache.py:151-164); miss -> CACHE_MISS(key, iteration),
+ * first missing key in the given order.  Missing entries get slot -1. */
+int bp_cache_resolve(bp_cache* cache, const uint64_t* d_keys, const uint32_t* d_ids, int64_t n,
+                     const int64_t* d_n, int64_t iteration, int32_t* d_slots, bp_stream_t stream);
+/* values_at (copy) and update_rows (reference cache.py:166-184). d_dirty may be NULL. */
+int bp_cache_gather(bp_cache* cache, const int32_t* d_slots, int64_t n, const int64_t* d_n, float* d_out,
+                    bp_stream_t stream);
+int bp_cache_update(bp_cache* cache, const int32_t* d_slots, const float* d_rows, const uint8_t* d_dirty,
+                    int64_t n, const int64_t* d_n, bp_stream_t stream);
+/* evict_expired_arrays / drain_arrays (reference cache.py:214-242): every used
+ * slot with ttl <= completed (drain: all).  Output in slot order; sorting by
+ * key is bp_sort_keys.  Outputs need room for ``capacity`` entries. */
+typedef struct bp_evict_buffers {
+  uint64_t* d_keys;
+  uint32_t* d_ids;
+  float* d_rows;
+  uint8_t* d_dirty;
+  int64_t* d_count;  /* [2]: evicted, evicted dirty */
+} bp_evict_buffers;
+int bp_cache_evict(bp_cache* cache, int64_t completed, int32_t drain, const bp_evict_buffers* out,
+                   bp_stream_t stream);
+/* content_checksum (reference cache.py:249-272) into a device u64. */
+int bp_cache_checksum(bp_cache* cache, uint64_t* d_out, bp_stream_t stream);
+/* Raw views for inspection (device pointers). */
+typedef struct bp_cache_view {
+  int64_t capacity;
+  int32_t dim;
+  int32_t pad;
+  float* d_values;
+  int64_t* d_ttl;
+  uint8_t* d_dirty;
+  uint8_t* d_used;
+  uint64_t* d_slot_key;
+} bp_cache_view;
+int bp_cache_get_view(const bp_cache* cache, bp_cache_view* out);
+
+/* ------------------------------------------------------------------ store
+ * Embedding Server (reference store.py:65-201): the full table lives in
+ * pinned host memory, row-major in (table, row, component) order -- the
+ * digest order of reference store.py:179-185.  Initial values are computed on
+ * the GPU (reference store.py:29-42) and streamed to the host table. */
+int bp_store_create(bp_ctx* ctx, const bp_schema* schema, uint64_t seed, bp_stream_t stream, bp_store** out);
+int bp_store_destroy(bp_store* store);
+float* bp_store_host_table(bp_store* store);
+uint8_t* bp_store_written_bitmap(bp_store* store); /* device, 1 bit per row */
+/* fetch (reference store.py:106-129): zero-copy gather of rows g from the
+ * pinned table over the host link into d_out[n, dim]. */
+int bp_store_fetch(bp_store* store, const uint32_t* d_ids, int64_t n, const int64_t* d_n, float* d_out,
+                   bp_stream_t stream);
+/* write_back (reference store.py:131-155): zero-copy scatter into the
+ * pinned table; ids must be unique within one call. */
+int bp_store_write(bp_store* store, const uint32_t* d_ids, const float* d_rows, int64_t n,
+                   const int64_t* d_n, bp_stream_t stream);
+/* initial_values (reference store.py:29-42) for arbitrary packed keys. */
+int bp_init_values(uint64_t seed, int32_t dim, const uint64_t* d_keys, int64_t n, float* d_out,
+                   bp_stream_t stream);
+/* dense ids for packed keys (schema mode); out-of-schema -> STORE_KEY. */
+int bp_schema_ids(bp_ctx* ctx, const bp_schema* schema, const uint64_t* d_keys, int64_t n, uint32_t* d_ids,
+                  bp_stream_t stream);
+
+/* ---------------------------------------------------------------- trainer
+ * Fused stub backward + rank-ordered combine + SGD (reference trainer.py:37-53,
+ * 92-105, 140-146; engine.py:545-579).  For every unique key (sorted order s)
+ * the kernel walks the key's occurrences in occurrence order: per rank
+ * G_r = ((0 + g_1) + g_2) + ... with g = c_value*v + c_label*(label - 0.5),
+ * then combined = ((0 + G_r0) + G_r1) + ... in ascending rank, exactly the
+ * association of np.add.at.  mode BP_STUB_SGD updates rows in place
+ * (v - lr*combined) and sets dirty where combined != 0; mode BP_STUB_GRAD
+ * writes combined to d_grad_out[s] instead.
+ * d_rows: row arena; d_row_index: row of sorted unique s (NULL = s itself).
+ * d_next_ids/n_next: optional (sorted) dense ids of the next batch: counts
+ * critical keys (reference engine.py:560-569) into d_stats[0]. */
+#define BP_STUB_SGD 0
+#define BP_STUB_GRAD 1
+int bp_stub_step(bp_ctx* ctx, bp_prep* prep, float* d_rows, const int32_t* d_row_index, uint8_t* d_dirty,
+                 int32_t dim, float c_value, float c_label, float lr, int32_t mode, float* d_grad_out,
+                 const uint32_t* d_next_ids, const int64_t* d_n_next, int64_t n_next_max, int64_t* d_stats,
+                 bp_stream_t stream);
+/* sgd_step (reference trainer.py:140-146): out = v - lr*g, single precision. */
+int bp_sgd(const float* d_values, const float* d_grads, float lr, int64_t count, float* d_out, bp_stream_t stream);
+
+/* ------------------------------------------------------------ utilities */
+/* Sort packed keys ascending with a u32 payload (stable); n host-known. */
+int bp_sort_keys_u64(uint64_t* d_keys, uint32_t* d_vals, int64_t n, int32_t key_bits, bp_stream_t stream);
+/* Order-independent digest helpers for parity tests. */
+int bp_xor_checksum_rows(const float* d_rows, int64_t n, int32_t dim, uint64_t* d_out, bp_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BAGPIPE_B200_H */

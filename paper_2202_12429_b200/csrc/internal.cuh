@@ -1,0 +1,104 @@
+// Internal object layouts shared by the translation units of libbagpipe_b200.
+#pragma once
+
+#include "sort.cuh"
+
+struct bp_ctx {
+  bp::ErrorRecord* d_err;
+  bp::ErrorRecord* h_err;  // pinned
+};
+
+struct bp_schema {
+  int32_t num_tables;
+  int32_t emb_dim;
+  int64_t total_rows;
+  int32_t id_bits;         // bit width of total_rows - 1 (sort key width)
+  int64_t* d_table_base;   // [num_tables + 1]
+  int64_t* d_rows;         // [num_tables]
+  int64_t* h_table_base;
+};
+
+namespace bp {
+
+constexpr uint32_t kNoId = 0xFFFFFFFFu;
+constexpr uint64_t kEmptyKey = ~0ull;
+
+// Memory from the device's stream-ordered pool (release threshold raised at
+// context creation so steady-state iterations never hit cudaMalloc).
+template <typename T>
+inline cudaError_t pool_alloc(T** p, size_t count, cudaStream_t s) {
+  return cudaMallocAsync((void**)p, (count ? count : 1) * sizeof(T), s);
+}
+
+// GPU hash map packed key -> dense id for schema-less objects (the planner
+// and cache API accept keys of any table/row without a schema).  Insert-only,
+// linear probing; ids are assigned densely in call order via a scan over the
+// CAS winners, so every per-key array of the owner can be indexed by id.
+struct Registry {
+  uint64_t* d_keys = nullptr;  // [slots]
+  uint32_t* d_ids = nullptr;   // [slots]
+  long long* d_count = nullptr;
+  uint32_t* d_claim = nullptr;  // scratch [claim_cap]
+  uint32_t* d_claim_scan = nullptr;
+  uint32_t* d_partials = nullptr;
+  long long claim_cap = 0;
+  long long slots = 0;
+  long long id_capacity = 0;
+  long long count_upper = 0;
+};
+
+int registry_init(Registry* r, long long id_capacity, cudaStream_t s);
+void registry_free(Registry* r, cudaStream_t s);
+// Makes room for n more ids; returns 1 in *grown when id_capacity changed.
+int registry_reserve(Registry* r, long long n, cudaStream_t s, int* grown);
+// ids for unique keys; insert=1 registers unknown keys, insert=0 yields kNoId.
+int registry_map(Registry* r, const uint64_t* d_keys, long long n, const long long* d_n, uint32_t* d_ids,
+                 int insert, cudaStream_t s);
+
+__device__ __forceinline__ uint64_t registry_hash(uint64_t key) { return splitmix64(key); }
+
+__device__ __forceinline__ uint32_t registry_find(const uint64_t* keys, const uint32_t* ids, long long slots,
+                                                  uint64_t key) {
+  const uint64_t mask = (uint64_t)slots - 1;
+  uint64_t h = registry_hash(key) & mask;
+  for (long long probe = 0; probe < slots; ++probe) {
+    const uint64_t k = keys[h];
+    if (k == key) return ids[h];
+    if (k == kEmptyKey) return kNoId;
+    h = (h + 1) & mask;
+  }
+  return kNoId;
+}
+
+// Dense id of a packed key in schema mode; kNoId if out of schema.
+__device__ __forceinline__ uint32_t schema_id(const int64_t* base, const int64_t* rows, int num_tables,
+                                              uint64_t key) {
+  const uint32_t t = table_of(key);
+  const uint64_t r = row_of(key);
+  if (t >= (uint32_t)num_tables || r >= (uint64_t)rows[t]) return kNoId;
+  return (uint32_t)(base[t] + (long long)r);
+}
+
+}  // namespace bp
+
+struct bp_prep {
+  bp_ctx* ctx;
+  long long n_occ;
+  long long iteration;
+  int num_ranks;
+  int flags;
+  int schema_mode;
+  long long* d_num_unique;
+  uint64_t* d_uniq_key_s;
+  uint32_t* d_uniq_id_s;
+  uint64_t* d_uniq_key_k;
+  uint32_t* d_perm_s2k;
+  uint32_t* d_perm_k2s;
+  uint32_t* d_seg_start;
+  uint32_t* d_occ_pos;
+  uint8_t* d_occ_label;
+  uint32_t* d_occ_k;
+  long long* d_rank_bounds;
+  long long h_num_unique;  // -1 until read back
+  cudaStream_t stream;
+};

@@ -1,0 +1,259 @@
+// Batch prep: dedupe + grouping of one batch's occurrences on the device.
+//
+// Replaces Batch.unique_keys (reference traces.py:91-103) and _prep_batch
+// (reference engine.py:142-182).  One stable LSD radix sort of
+// (sort key, occurrence position) yields, for free:
+//   * key-sorted unique keys (segment heads) -- the order of plan.prefetch
+//     and of every store call (reference lookahead.py:108, engine.py:150),
+//   * each key's occurrences in occurrence order (stability) -- the order in
+//     which np.add.at accumulates (reference trainer.py:48-53),
+// and one scan over "first occurrence" flags scattered back to occurrence
+// positions gives the first-occurrence order of ttl_updates.
+//
+// Sort key: schema mode -> dense id g = table_base[t] + row (u32, monotone in
+// (table,row)); registry mode -> the packed u64 key sorted on its two live
+// bit ranges (rows: [0,row_bits), tables: [44, 44+table_bits)).
+#include "internal.cuh"
+
+namespace bp {
+
+__global__ void k_prep_keys_schema(const uint64_t* __restrict__ keys, long long n, const int64_t* base,
+                                   const int64_t* rows, int num_tables, uint32_t* __restrict__ sk,
+                                   uint32_t* __restrict__ val, ErrorRecord* err, long long iteration) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    uint32_t id = schema_id(base, rows, num_tables, keys[i]);
+    if (id == kNoId) {
+      raise_error(err, BP_ERR_STORE_KEY, iteration, i, keys[i]);
+      id = 0;
+    }
+    sk[i] = id;
+    val[i] = (uint32_t)i;
+  }
+}
+
+__global__ void k_prep_keys_packed(const uint64_t* __restrict__ keys, long long n, uint64_t* __restrict__ sk,
+                                   uint32_t* __restrict__ val) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    sk[i] = keys[i];
+    val[i] = (uint32_t)i;
+  }
+}
+
+template <typename K>
+__global__ void k_prep_heads(const K* __restrict__ sk, long long n, uint32_t* __restrict__ head) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
+    head[j] = (j == 0 || sk[j] != sk[j - 1]) ? 1u : 0u;
+}
+
+// Segment heads: CSR start, unique key/id (sorted order), first-occurrence
+// flag at the head's position (the smallest position of the key: stable sort).
+template <typename K>
+__global__ void k_prep_segments(const K* __restrict__ sk, const uint32_t* __restrict__ pos,
+                                const uint32_t* __restrict__ head, const uint32_t* __restrict__ segx, long long n,
+                                const uint64_t* __restrict__ keys, const uint8_t* __restrict__ labels,
+                                int schema_mode, uint32_t* __restrict__ seg_start, uint64_t* __restrict__ uniq_key_s,
+                                uint32_t* __restrict__ uniq_id_s, uint32_t* __restrict__ first_flag,
+                                uint8_t* __restrict__ occ_label, const long long* d_num_unique) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const uint32_t p = pos[j];
+    occ_label[j] = labels[p];
+    if (head[j]) {
+      const uint32_t s = segx[j];
+      seg_start[s] = (uint32_t)j;
+      uniq_key_s[s] = keys[p];
+      uniq_id_s[s] = schema_mode ? (uint32_t)sk[j] : kNoId;
+      first_flag[p] = 1u;
+    }
+    if (j == n - 1) seg_start[*d_num_unique] = (uint32_t)n;
+  }
+}
+
+__global__ void k_prep_perm(const uint32_t* __restrict__ pos, const uint32_t* __restrict__ head,
+                            const uint32_t* __restrict__ segx, const uint32_t* __restrict__ first_rank, long long n,
+                            const uint64_t* __restrict__ uniq_key_s, uint32_t* __restrict__ perm_s2k,
+                            uint32_t* __restrict__ perm_k2s, uint64_t* __restrict__ uniq_key_k) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    if (!head[j]) continue;
+    const uint32_t s = segx[j];
+    const uint32_t k = first_rank[pos[j]];
+    perm_s2k[s] = k;
+    perm_k2s[k] = s;
+    uniq_key_k[k] = uniq_key_s[s];
+  }
+}
+
+__global__ void k_prep_occ_k(const uint32_t* __restrict__ pos, const uint32_t* __restrict__ head,
+                             const uint32_t* __restrict__ segx, long long n, const uint32_t* __restrict__ perm_s2k,
+                             uint32_t* __restrict__ occ_k) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const uint32_t s = segx[j] + head[j] - 1u;  // inclusive segment index
+    occ_k[pos[j]] = perm_s2k[s];
+  }
+}
+
+template <typename K>
+static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, const uint8_t* d_labels,
+                      int row_bits, int table_bits, cudaStream_t s) {
+  const long long n = P->n_occ;
+  K *ka, *kb;
+  uint32_t *va, *vb, *hist, *head, *segx, *first_flag, *first_rank, *partials;
+  BP_CUDA_TRY(pool_alloc(&ka, n, s));
+  BP_CUDA_TRY(pool_alloc(&kb, n, s));
+  BP_CUDA_TRY(pool_alloc(&va, n, s));
+  BP_CUDA_TRY(pool_alloc(&vb, n, s));
+  BP_CUDA_TRY(pool_alloc(&hist, sort_hist_words(n), s));
+  BP_CUDA_TRY(pool_alloc(&head, n, s));
+  BP_CUDA_TRY(pool_alloc(&segx, n, s));
+  BP_CUDA_TRY(pool_alloc(&first_flag, n, s));
+  BP_CUDA_TRY(pool_alloc(&first_rank, n, s));
+  BP_CUDA_TRY(pool_alloc(&partials, scan_tiles(n) + 1, s));
+  const int g = grid_for(n, 256);
+  int which = 0;
+  if (P->schema_mode) {
+    k_prep_keys_schema<<<g, 256, 0, s>>>(d_keys, n, sc->d_table_base, sc->d_rows, sc->num_tables,
+                                         (uint32_t*)ka, va, P->ctx ? P->ctx->d_err : nullptr, P->iteration);
+    BP_CUDA_TRY(radix_sort_pairs<K>(ka, va, kb, vb, n, nullptr, 0, sc->id_bits, hist, &which, s));
+  } else {
+    k_prep_keys_packed<<<g, 256, 0, s>>>(d_keys, n, (uint64_t*)ka, va);
+    int w1 = 0, w2 = 0;
+    BP_CUDA_TRY(radix_sort_pairs<K>(ka, va, kb, vb, n, nullptr, 0, row_bits, hist, &w1, s));
+    K* k1 = w1 ? kb : ka;
+    uint32_t* v1 = w1 ? vb : va;
+    K* k2 = w1 ? ka : kb;
+    uint32_t* v2 = w1 ? va : vb;
+    BP_CUDA_TRY(radix_sort_pairs<K>(k1, v1, k2, v2, n, nullptr, kKeyTableShift, kKeyTableShift + table_bits, hist,
+                                    &w2, s));
+    which = w1 ^ w2;
+  }
+  const K* skey = which ? kb : ka;
+  const uint32_t* spos = which ? vb : va;
+  BP_CUDA_TRY(cudaMemcpyAsync(P->d_occ_pos, spos, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+
+  k_prep_heads<K><<<g, 256, 0, s>>>(skey, n, head);
+  BP_CUDA_TRY(exclusive_scan(head, segx, n, nullptr, partials, nullptr, P->d_num_unique, s));
+  BP_CUDA_TRY(cudaMemsetAsync(first_flag, 0, n * sizeof(uint32_t), s));
+  k_prep_segments<K><<<g, 256, 0, s>>>(skey, P->d_occ_pos, head, segx, n, d_keys, d_labels, P->schema_mode,
+                                       P->d_seg_start, P->d_uniq_key_s, P->d_uniq_id_s, first_flag,
+                                       P->d_occ_label, P->d_num_unique);
+  BP_CUDA_TRY(exclusive_scan(first_flag, first_rank, n, nullptr, partials, nullptr, nullptr, s));
+  k_prep_perm<<<g, 256, 0, s>>>(P->d_occ_pos, head, segx, first_rank, n, P->d_uniq_key_s, P->d_perm_s2k,
+                                P->d_perm_k2s, P->d_uniq_key_k);
+  if (P->flags & BP_PREP_OCC_INDEX)
+    k_prep_occ_k<<<g, 256, 0, s>>>(P->d_occ_pos, head, segx, n, P->d_perm_s2k, P->d_occ_k);
+  BP_LAUNCH_CHECK();
+  cudaFreeAsync(ka, s);
+  cudaFreeAsync(kb, s);
+  cudaFreeAsync(va, s);
+  cudaFreeAsync(vb, s);
+  cudaFreeAsync(hist, s);
+  cudaFreeAsync(head, s);
+  cudaFreeAsync(segx, s);
+  cudaFreeAsync(first_flag, s);
+  cudaFreeAsync(first_rank, s);
+  cudaFreeAsync(partials, s);
+  return BP_OK;
+}
+
+}  // namespace bp
+
+extern "C" int bp_prep_create(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_keys, const uint8_t* d_labels,
+                              int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks, int64_t iteration,
+                              int32_t flags, int32_t row_bits, int32_t table_bits, bp_stream_t stream,
+                              bp_prep** out) {
+  using namespace bp;
+  if (n_occ < 0 || num_ranks < 1 || n_occ >= (int64_t)kNoId) return BP_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  bp_prep* P = new bp_prep();
+  P->ctx = ctx;
+  P->n_occ = n_occ;
+  P->iteration = iteration;
+  P->num_ranks = num_ranks;
+  P->flags = flags;
+  P->schema_mode = sc != nullptr;
+  P->stream = s;
+  P->h_num_unique = n_occ == 0 ? 0 : -1;
+  const long long n = n_occ > 0 ? n_occ : 1;
+  BP_CUDA_TRY(pool_alloc(&P->d_num_unique, 1, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_uniq_key_s, n, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_uniq_id_s, n, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_uniq_key_k, n, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_perm_s2k, n, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_perm_k2s, n, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_seg_start, n + 1, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_occ_pos, n, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_occ_label, n, s));
+  P->d_occ_k = nullptr;
+  if (flags & BP_PREP_OCC_INDEX) BP_CUDA_TRY(pool_alloc(&P->d_occ_k, n, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_rank_bounds, num_ranks + 1, s));
+  BP_CUDA_TRY(cudaMemcpyAsync(P->d_rank_bounds, h_rank_bounds, sizeof(long long) * (num_ranks + 1),
+                              cudaMemcpyHostToDevice, s));
+  // The pageable H2D copy above is staged by the driver before returning, so
+  // the caller's rank-bounds array may be released immediately.
+  if (n_occ == 0) {
+    BP_CUDA_TRY(cudaMemsetAsync(P->d_num_unique, 0, sizeof(long long), s));
+    BP_CUDA_TRY(cudaMemsetAsync(P->d_seg_start, 0, sizeof(uint32_t), s));
+    *out = P;
+    return BP_OK;
+  }
+  int rc;
+  if (sc) {
+    rc = prep_build<uint32_t>(P, sc, d_keys, d_labels, 0, 0, s);
+  } else {
+    if (row_bits < 1) row_bits = 1;
+    if (table_bits < 1) table_bits = 1;
+    if (row_bits > kKeyTableShift || table_bits > 64 - kKeyTableShift) return BP_ERR_INVALID;
+    rc = prep_build<uint64_t>(P, nullptr, d_keys, d_labels, row_bits, table_bits, s);
+  }
+  if (rc != BP_OK) return rc;
+  *out = P;
+  return BP_OK;
+}
+
+extern "C" int bp_prep_destroy(bp_prep* P) {
+  if (!P) return BP_OK;
+  cudaStream_t s = P->stream;
+  cudaFreeAsync(P->d_num_unique, s);
+  cudaFreeAsync(P->d_uniq_key_s, s);
+  cudaFreeAsync(P->d_uniq_id_s, s);
+  cudaFreeAsync(P->d_uniq_key_k, s);
+  cudaFreeAsync(P->d_perm_s2k, s);
+  cudaFreeAsync(P->d_perm_k2s, s);
+  cudaFreeAsync(P->d_seg_start, s);
+  cudaFreeAsync(P->d_occ_pos, s);
+  cudaFreeAsync(P->d_occ_label, s);
+  if (P->d_occ_k) cudaFreeAsync(P->d_occ_k, s);
+  cudaFreeAsync(P->d_rank_bounds, s);
+  delete P;
+  return BP_OK;
+}
+
+extern "C" int bp_prep_get_view(const bp_prep* P, bp_prep_view* v) {
+  v->n_occ = P->n_occ;
+  v->iteration = P->iteration;
+  v->num_ranks = P->num_ranks;
+  v->pad = 0;
+  v->d_num_unique = (const int64_t*)P->d_num_unique;
+  v->d_uniq_key_s = P->d_uniq_key_s;
+  v->d_uniq_id_s = P->d_uniq_id_s;
+  v->d_uniq_key_k = P->d_uniq_key_k;
+  v->d_perm_s2k = P->d_perm_s2k;
+  v->d_perm_k2s = P->d_perm_k2s;
+  v->d_seg_start = P->d_seg_start;
+  v->d_occ_pos = P->d_occ_pos;
+  v->d_occ_label = P->d_occ_label;
+  v->d_occ_k = P->d_occ_k;
+  v->d_rank_bounds = (const int64_t*)P->d_rank_bounds;
+  return BP_OK;
+}
+
+extern "C" int bp_prep_num_unique(bp_prep* P, bp_stream_t stream, int64_t* h_out) {
+  if (P->h_num_unique < 0) {
+    long long u = 0;
+    BP_CUDA_TRY(cudaMemcpyAsync(&u, P->d_num_unique, sizeof(long long), cudaMemcpyDeviceToHost,
+                                (cudaStream_t)stream));
+    BP_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    P->h_num_unique = u;
+  }
+  *h_out = P->h_num_unique;
+  return BP_OK;
+}
