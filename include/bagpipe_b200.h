@@ -156,6 +156,16 @@ typedef struct bp_planner_stats {
  * records projected occupancy, assigns TTLs, prefetch/mirror, erases keys whose
  * last windowed use is this batch.  Writes the plan into *bufs. */
 int bp_planner_pop(bp_planner* planner, bp_prep* prep, const bp_plan_buffers* bufs, bp_stream_t stream);
+/* Enumerate keys with planner state (tracked and/or mirrored), arbitrary
+ * order: flags bit0 = in latest_tracker, bit1 = in the in_cache mirror.
+ * *d_count receives the total (entries beyond cap are dropped). */
+typedef struct bp_planner_dump_t {
+  uint64_t* d_keys;
+  int64_t* d_last;
+  uint8_t* d_flags;
+  int64_t* d_count;
+} bp_planner_dump_t;
+int bp_planner_dump(bp_planner* planner, const bp_planner_dump_t* out, int64_t cap, bp_stream_t stream);
 /* Synchronises. */
 int bp_planner_get_stats(bp_planner* planner, bp_stream_t stream, bp_planner_stats* h_out);
 
@@ -204,7 +214,14 @@ typedef struct bp_evict_buffers {
   int64_t* d_count;  /* [2]: evicted, evicted dirty */
 } bp_evict_buffers;
 int bp_cache_evict(bp_cache* cache, int64_t completed, int32_t drain, const bp_evict_buffers* out,
-                   bp_stream_t stream);
+                   int64_t out_capacity, bp_stream_t stream);
+/* Engine step of reference engine.py:525-543 over a schema-mode prep: TTL
+ * updates for every batch key (except skip_key when has_skip, the
+ * drop_prefetch fault) then slot resolution into d_slots_s (key-sorted
+ * order).  Absent TTL key -> CACHE_ORDERING; absent skipped key ->
+ * CACHE_MISS (index | 1<<40 marks the resolve phase). */
+int bp_cache_apply_resolve(bp_cache* cache, bp_prep* prep, const int64_t* d_ttl_k, uint64_t skip_key,
+                           int32_t has_skip, int32_t* d_slots_s, bp_stream_t stream);
 /* content_checksum (reference cache.py:249-272) into a device u64. */
 int bp_cache_checksum(bp_cache* cache, uint64_t* d_out, bp_stream_t stream);
 /* Raw views for inspection (device pointers). */
@@ -237,6 +254,9 @@ int bp_store_fetch(bp_store* store, const uint32_t* d_ids, int64_t n, const int6
  * pinned table; ids must be unique within one call. */
 int bp_store_write(bp_store* store, const uint32_t* d_ids, const float* d_rows, int64_t n,
                    const int64_t* d_n, bp_stream_t stream);
+/* write_back of only the masked (dirty) rows of an eviction chunk. */
+int bp_store_write_masked(bp_store* store, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_mask,
+                          int64_t n, const int64_t* d_n, bp_stream_t stream);
 /* initial_values (reference store.py:29-42) for arbitrary packed keys. */
 int bp_init_values(uint64_t seed, int32_t dim, const uint64_t* d_keys, int64_t n, float* d_out,
                    bp_stream_t stream);
@@ -262,6 +282,12 @@ int bp_stub_step(bp_ctx* ctx, bp_prep* prep, float* d_rows, const int32_t* d_row
                  int32_t dim, float c_value, float c_label, float lr, int32_t mode, float* d_grad_out,
                  const uint32_t* d_next_ids, const int64_t* d_n_next, int64_t n_next_max, int64_t* d_stats,
                  bp_stream_t stream);
+/* np.add.at(out, idx, vals) row-wise in input order, over a registry-mode
+ * prep built from keys = idx (combine_core, reference trainer.py:92-105).
+ * d_out rows absent from idx are left untouched. */
+int bp_add_at_rows(bp_prep* prep, const float* d_vals, int32_t dim, float* d_out, bp_stream_t stream);
+/* row index (low 44 bits) of each key-sorted unique key, as int32. */
+int bp_prep_key_rows(bp_prep* prep, int32_t* d_out, bp_stream_t stream);
 /* sgd_step (reference trainer.py:140-146): out = v - lr*g, single precision. */
 int bp_sgd(const float* d_values, const float* d_grads, float lr, int64_t count, float* d_out, bp_stream_t stream);
 

@@ -64,7 +64,7 @@ struct ErrorRecord {
 // Error path only: a short critical section keeps (code, iteration, index,
 // key) consistent; the fast pre-check avoids the lock once an earlier error
 // is recorded.
-__device__ __noinline__ void raise_error(ErrorRecord* err, int code, long long iteration, long long index,
+static __device__ __noinline__ void raise_error(ErrorRecord* err, int code, long long iteration, long long index,
                                          uint64_t key) {
   if (err == nullptr) return;
   volatile ErrorRecord* v = err;

@@ -56,7 +56,7 @@ __device__ __forceinline__ uint32_t block_inclusive_scan_256(uint32_t v, uint32_
   return v + add;
 }
 
-__global__ void k_scan_reduce(const uint32_t* __restrict__ in, long long n, const long long* d_n,
+static __global__ void k_scan_reduce(const uint32_t* __restrict__ in, long long n, const long long* d_n,
                               uint32_t* __restrict__ partials) {
   n = load_count(n, d_n);
   const long long base = (long long)blockIdx.x * kScanTile;
@@ -79,7 +79,7 @@ __global__ void k_scan_reduce(const uint32_t* __restrict__ in, long long n, cons
 
 // Single CTA: exclusive scan of ``tiles`` partials in place; writes the grand
 // total to *total (u32) and optionally *total64.
-__global__ void k_scan_partials(uint32_t* partials, int tiles, uint32_t* total, long long* total64) {
+static __global__ void k_scan_partials(uint32_t* partials, int tiles, uint32_t* total, long long* total64) {
   __shared__ uint32_t sh[kScanThreads / 32];
   uint32_t carry = 0;
   for (int base = 0; base < tiles; base += kScanThreads) {
@@ -96,7 +96,7 @@ __global__ void k_scan_partials(uint32_t* partials, int tiles, uint32_t* total, 
   }
 }
 
-__global__ void k_scan_down(const uint32_t* __restrict__ in, long long n, const long long* d_n,
+static __global__ void k_scan_down(const uint32_t* __restrict__ in, long long n, const long long* d_n,
                             const uint32_t* __restrict__ partials, uint32_t* __restrict__ out) {
   n = load_count(n, d_n);
   __shared__ uint32_t sh[kScanThreads / 32];
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_upsweep(const K* __restr
 }
 
 // Exclusive scan over the digit-major histogram [radix][tiles] (single CTA).
-__global__ void k_radix_scan(uint32_t* hist, int len) {
+static __global__ void k_radix_scan(uint32_t* hist, int len) {
   __shared__ uint32_t sh[kScanThreads / 32];
   uint32_t carry = 0;
   for (int base = 0; base < len; base += kScanThreads) {

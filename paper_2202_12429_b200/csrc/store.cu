@@ -1,0 +1,198 @@
+// Embedding Server: the full table in pinned host memory, served over the
+// host link by zero-copy kernels (reference store.py:65-201).
+//
+// Layout: one row-major float32 matrix [total_rows, dim] in (table, row,
+// component) order -- byte-for-byte the stream the reference digests
+// (store.py:179-185) -- so the digest is a single blake2b pass over host
+// memory and no per-shard dictionaries exist.  Hash sharding (store.py:80-104)
+// never changes values (reference tests/test_store.py:42-45); it is kept as
+// metadata only (num_shards is echoed in reports).
+//
+// Initial values are the functional init of store.py:29-42 evaluated on the
+// GPU and written straight into the mapped host table, so creating a 2.2 GB
+// Criteo-Kaggle store costs one PCIe pass instead of 113 s of numpy.
+#include "internal.cuh"
+
+struct bp_store {
+  bp_ctx* ctx;
+  const bp_schema* sc;
+  uint64_t seed;
+  int dim;
+  float* h_table;       // pinned, mapped
+  float* d_table;       // device alias of h_table (UVA)
+  uint32_t* d_written;  // bitmap, 1 bit per row
+};
+
+namespace bp {
+
+// One thread per (row, 4-component chunk); dims not divisible by 4 use a
+// scalar tail.  FNV over (t, r) is shared by all components of a row.
+__global__ void k_store_init(float* __restrict__ out, long long row0, long long nrows, uint32_t table,
+                             uint64_t seed, int dim) {
+  const int chunks = (dim + 3) >> 2;
+  const long long total = nrows * chunks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / chunks;
+    const int c = (int)(i - r * chunks);
+    const uint64_t h_tr = fnv_u64(fnv_u64(kFnvOffset, table), (uint64_t)r);
+    float v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = c * 4 + q;
+      v[q] = j < dim ? init_component(seed, h_tr, (uint64_t)j) : 0.f;
+    }
+    float* dst = out + (row0 + r) * dim + c * 4;
+    if ((dim & 3) == 0) {
+      *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      for (int q = 0; q < 4 && c * 4 + q < dim; ++q) dst[q] = v[q];
+    }
+  }
+}
+
+__global__ void k_init_values(uint64_t seed, int dim, const uint64_t* __restrict__ keys, long long n,
+                              float* __restrict__ out) {
+  const long long total = n * dim;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long k = i / dim;
+    const int j = (int)(i - k * dim);
+    const uint64_t key = keys[k];
+    const uint64_t h_tr = fnv_u64(fnv_u64(kFnvOffset, (uint64_t)table_of(key)), row_of(key));
+    out[i] = init_component(seed, h_tr, (uint64_t)j);
+  }
+}
+
+// Row gather from the mapped host table: 16-byte lanes, one row per
+// (dim/4)-lane group, so each row is one contiguous PCIe read burst.
+__global__ void k_store_fetch_v4(const float4* __restrict__ table, const uint32_t* __restrict__ ids, long long n,
+                                 const long long* d_n, int q, float4* __restrict__ out) {
+  n = load_count(n, d_n);
+  const long long total = n * q;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / q;
+    const int c = (int)(i - r * q);
+    out[i] = table[(long long)ids[r] * q + c];
+  }
+}
+
+__global__ void k_store_fetch_scalar(const float* __restrict__ table, const uint32_t* __restrict__ ids, long long n,
+                                     const long long* d_n, int dim, float* __restrict__ out) {
+  n = load_count(n, d_n);
+  const long long total = n * dim;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / dim;
+    out[i] = table[(long long)ids[r] * dim + (i - r * dim)];
+  }
+}
+
+// Scatter rows into the host table; ``mask`` (optional) skips clean rows, the
+// write-back of only dirty evictions (reference engine.py:403-413).
+__global__ void k_store_write(float* __restrict__ table, uint32_t* __restrict__ written,
+                              const uint32_t* __restrict__ ids, const float* __restrict__ rows,
+                              const uint8_t* __restrict__ mask, long long n, const long long* d_n, int dim) {
+  n = load_count(n, d_n);
+  const bool v4 = (dim & 3) == 0;
+  const int q = v4 ? dim >> 2 : dim;
+  const long long total = n * q;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / q;
+    const int c = (int)(i - r * q);
+    if (mask && !mask[r]) continue;
+    const long long g = ids[r];
+    if (v4) {
+      reinterpret_cast<float4*>(table)[g * q + c] = reinterpret_cast<const float4*>(rows)[r * q + c];
+    } else {
+      table[g * dim + c] = rows[r * dim + c];
+    }
+    if (c == 0) atomicOr(&written[g >> 5], 1u << (g & 31));
+  }
+}
+
+}  // namespace bp
+
+extern "C" int bp_store_create(bp_ctx* ctx, const bp_schema* sc, uint64_t seed, bp_stream_t stream, bp_store** out) {
+  using namespace bp;
+  cudaStream_t s = (cudaStream_t)stream;
+  bp_store* st = new bp_store();
+  st->ctx = ctx;
+  st->sc = sc;
+  st->seed = seed;
+  st->dim = sc->emb_dim;
+  const size_t bytes = (size_t)sc->total_rows * sc->emb_dim * sizeof(float);
+  BP_CUDA_TRY(cudaHostAlloc((void**)&st->h_table, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  BP_CUDA_TRY(cudaHostGetDevicePointer((void**)&st->d_table, st->h_table, 0));
+  const long long words = (sc->total_rows + 31) / 32;
+  BP_CUDA_TRY(cudaMalloc(&st->d_written, words * sizeof(uint32_t)));
+  BP_CUDA_TRY(cudaMemsetAsync(st->d_written, 0, words * sizeof(uint32_t), s));
+  const int chunks = (sc->emb_dim + 3) / 4;
+  for (int t = 0; t < sc->num_tables; ++t) {
+    const long long rows = sc->h_table_base[t + 1] - sc->h_table_base[t];
+    k_store_init<<<grid_for(rows * chunks, 256, kNumSMs * 32), 256, 0, s>>>(st->d_table, sc->h_table_base[t], rows,
+                                                                            (uint32_t)t, seed, sc->emb_dim);
+  }
+  BP_LAUNCH_CHECK();
+  BP_CUDA_TRY(cudaStreamSynchronize(s));
+  *out = st;
+  return BP_OK;
+}
+
+extern "C" int bp_store_destroy(bp_store* st) {
+  if (!st) return BP_OK;
+  cudaFreeHost(st->h_table);
+  cudaFree(st->d_written);
+  delete st;
+  return BP_OK;
+}
+
+extern "C" float* bp_store_host_table(bp_store* st) { return st->h_table; }
+extern "C" uint8_t* bp_store_written_bitmap(bp_store* st) { return (uint8_t*)st->d_written; }
+
+extern "C" int bp_store_fetch(bp_store* st, const uint32_t* d_ids, int64_t n, const int64_t* d_n, float* d_out,
+                              bp_stream_t stream) {
+  using namespace bp;
+  if (n <= 0) return BP_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int dim = st->dim;
+  if ((dim & 3) == 0) {
+    const int q = dim >> 2;
+    k_store_fetch_v4<<<grid_for(n * q, 256, kNumSMs * 32), 256, 0, s>>>(
+        reinterpret_cast<const float4*>(st->d_table), d_ids, n, (const long long*)d_n, q,
+        reinterpret_cast<float4*>(d_out));
+  } else {
+    k_store_fetch_scalar<<<grid_for(n * dim, 256, kNumSMs * 32), 256, 0, s>>>(st->d_table, d_ids, n,
+                                                                             (const long long*)d_n, dim, d_out);
+  }
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_store_write(bp_store* st, const uint32_t* d_ids, const float* d_rows, int64_t n, const int64_t* d_n,
+                              bp_stream_t stream) {
+  using namespace bp;
+  if (n <= 0) return BP_OK;
+  const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
+  k_store_write<<<grid_for(n * q, 256, kNumSMs * 32), 256, 0, (cudaStream_t)stream>>>(
+      st->d_table, st->d_written, d_ids, d_rows, nullptr, n, (const long long*)d_n, st->dim);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_store_write_masked(bp_store* st, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_mask,
+                                     int64_t n, const int64_t* d_n, bp_stream_t stream) {
+  using namespace bp;
+  if (n <= 0) return BP_OK;
+  const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
+  k_store_write<<<grid_for(n * q, 256, kNumSMs * 32), 256, 0, (cudaStream_t)stream>>>(
+      st->d_table, st->d_written, d_ids, d_rows, d_mask, n, (const long long*)d_n, st->dim);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_init_values(uint64_t seed, int32_t dim, const uint64_t* d_keys, int64_t n, float* d_out,
+                              bp_stream_t stream) {
+  using namespace bp;
+  if (n <= 0) return BP_OK;
+  k_init_values<<<grid_for(n * dim, 256), 256, 0, (cudaStream_t)stream>>>(seed, dim, d_keys, n, d_out);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}

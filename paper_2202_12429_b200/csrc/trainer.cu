@@ -1,0 +1,246 @@
+// Fused stub backward + rank-ordered combine + SGD (the reference's whole
+// "EmbeddingBag backward + sparse optimizer": trainer.py:37-53, 92-105,
+// 140-146, driven by engine.py:545-579 / 706-718).
+//
+// Bit-exactness: np.add.at accumulates sequentially, per key, in occurrence
+// order, starting from +0.0; the cross-rank combine is a second sequential
+// sum in ascending rank.  A tree or warp reduction would change the float32
+// rounding, so each (key, component) is one sequential chain here: a group of
+// G lanes owns a key (lane = component), walks the key's occurrence list (the
+// stable sort in prep.cu keeps it in occurrence order) rank by rank, and
+// applies SGD in place.  Parallelism comes from the ~75K keys x 16 components
+// of a Criteo-Kaggle batch; the longest chain (a 3-row table's hot key,
+// ~9K occurrences per batch) bounds the kernel at a few tens of microseconds.
+// Every multiply/add uses an explicit _rn intrinsic: no FMA contraction.
+#include "internal.cuh"
+
+namespace bp {
+
+template <int G, int DPL>
+__global__ void __launch_bounds__(256) k_stub_step(
+    const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ occ_pos,
+    const uint8_t* __restrict__ occ_label, const long long* __restrict__ rank_bounds, int num_ranks,
+    const long long* __restrict__ d_U, float* __restrict__ rows, const int32_t* __restrict__ row_index,
+    uint8_t* __restrict__ dirty, int dim, float c_value, float c_label, float lr, int mode,
+    float* __restrict__ grad_out, const uint32_t* __restrict__ my_ids, const uint32_t* __restrict__ next_ids,
+    const long long* __restrict__ d_n_next, long long n_next_max, unsigned long long* __restrict__ stats) {
+  const long long U = *d_U;
+  const unsigned lane = threadIdx.x & 31u;
+  const int lane_g = (int)(lane & (G - 1));
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(unsigned)(G - 1)));
+  const long long groups_per_block = blockDim.x / G;
+  const long long groups_total = (long long)gridDim.x * groups_per_block;
+  const long long warp_first = (long long)blockIdx.x * groups_per_block + (threadIdx.x >> 5) * (32 / G);
+  const long long n_next = next_ids ? load_count(n_next_max, d_n_next) : 0;
+
+  for (long long base = warp_first; base < U; base += groups_total) {
+    const long long s = base + (long long)(lane / G);
+    bool active = s < U;
+    int32_t row = 0;
+    if (active) {
+      row = row_index ? row_index[s] : (int32_t)s;
+      active = row >= 0;
+    }
+    bool nonzero = false;
+    if (active) {
+      uint32_t j = seg_start[s];
+      const uint32_t b = seg_start[s + 1];
+      float v[DPL], sc[DPL], comb[DPL];
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) {
+        const int d = lane_g + q * G;
+        v[q] = d < dim ? rows[(long long)row * dim + d] : 0.f;
+        sc[q] = __fmul_rn(c_value, v[q]);
+        comb[q] = 0.f;
+      }
+      for (int r = 0; r < num_ranks && j < b; ++r) {
+        const long long hi = rank_bounds[r + 1];
+        uint32_t lo = j, up = b;  // first index in [j, b) whose position is >= hi
+        while (lo < up) {
+          const uint32_t mid = (lo + up) >> 1;
+          if ((long long)occ_pos[mid] < hi) lo = mid + 1;
+          else up = mid;
+        }
+        if (lo == j) continue;  // key absent from this rank: rank not in the combine
+        float acc[DPL];
+#pragma unroll
+        for (int q = 0; q < DPL; ++q) acc[q] = 0.f;
+        constexpr int kU = 8;
+        for (; j + kU <= lo; j += kU) {
+          float bias[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) bias[u] = __fmul_rn(c_label, __fsub_rn((float)occ_label[j + u], 0.5f));
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+#pragma unroll
+            for (int q = 0; q < DPL; ++q) acc[q] = __fadd_rn(acc[q], __fadd_rn(sc[q], bias[u]));
+          }
+        }
+        for (; j < lo; ++j) {
+          const float bias = __fmul_rn(c_label, __fsub_rn((float)occ_label[j], 0.5f));
+#pragma unroll
+          for (int q = 0; q < DPL; ++q) acc[q] = __fadd_rn(acc[q], __fadd_rn(sc[q], bias));
+        }
+#pragma unroll
+        for (int q = 0; q < DPL; ++q) comb[q] = __fadd_rn(comb[q], acc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) {
+        const int d = lane_g + q * G;
+        if (d < dim) {
+          nonzero |= comb[q] != 0.f;
+          if (mode == BP_STUB_SGD) rows[(long long)row * dim + d] = __fsub_rn(v[q], __fmul_rn(lr, comb[q]));
+          else grad_out[s * dim + d] = comb[q];
+        }
+      }
+    }
+    const unsigned nz = __ballot_sync(0xffffffffu, nonzero) & gmask;
+    bool crit = false;
+    if (active && lane_g == 0) {
+      if (nz && dirty && mode == BP_STUB_SGD) dirty[row] = 1;
+      if (n_next > 0) {
+        const uint32_t id = my_ids[s];
+        long long lo = 0, up = n_next;
+        while (lo < up) {
+          const long long mid = (lo + up) >> 1;
+          if (next_ids[mid] < id) lo = mid + 1;
+          else up = mid;
+        }
+        crit = lo < n_next && next_ids[lo] == id;
+      }
+    }
+    if (stats) {
+      const unsigned cm = __ballot_sync(0xffffffffu, crit);
+      const unsigned dm = __ballot_sync(0xffffffffu, active && lane_g == 0 && nz != 0);
+      if (lane == 0) {
+        if (cm) atomicAdd(&stats[0], (unsigned long long)__popc(cm));
+        if (dm) atomicAdd(&stats[1], (unsigned long long)__popc(dm));
+      }
+    }
+  }
+}
+
+// np.add.at(out, idx, vals) for row blocks, sequential per index in input
+// order (combine_core, reference trainer.py:92-105).  Groups over the CSR of
+// a registry-mode prep whose keys are the indices.
+template <int G, int DPL>
+__global__ void __launch_bounds__(256) k_add_at_rows(const uint32_t* __restrict__ seg_start,
+                                                     const uint32_t* __restrict__ occ_pos,
+                                                     const uint64_t* __restrict__ uniq_key_s,
+                                                     const long long* __restrict__ d_U, const float* __restrict__ vals,
+                                                     int dim, float* __restrict__ out) {
+  const long long U = *d_U;
+  const int lane_g = (int)(threadIdx.x & (G - 1));
+  const long long groups_total = (long long)gridDim.x * (blockDim.x / G);
+  for (long long s = (long long)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; s < U; s += groups_total) {
+    const uint32_t a = seg_start[s], b = seg_start[s + 1];
+    const long long dst = (long long)row_of(uniq_key_s[s]);
+    float acc[DPL];
+#pragma unroll
+    for (int q = 0; q < DPL; ++q) acc[q] = 0.f;
+    for (uint32_t j = a; j < b; ++j) {
+      const long long src = occ_pos[j];
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) {
+        const int d = lane_g + q * G;
+        if (d < dim) acc[q] = __fadd_rn(acc[q], vals[src * dim + d]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < DPL; ++q) {
+      const int d = lane_g + q * G;
+      if (d < dim) out[dst * dim + d] = acc[q];
+    }
+  }
+}
+
+__global__ void k_sgd(const float* __restrict__ v, const float* __restrict__ g, float lr, long long n,
+                      float* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = __fsub_rn(v[i], __fmul_rn(lr, g[i]));
+}
+
+__global__ void k_key_rows(const uint64_t* __restrict__ keys, const long long* d_U, int32_t* __restrict__ out) {
+  const long long U = *d_U;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < U; i += (long long)gridDim.x * blockDim.x)
+    out[i] = (int32_t)row_of(keys[i]);
+}
+
+static inline void group_shape(int dim, int* G, int* dpl) {
+  int g = 1;
+  while (g < dim && g < 32) g <<= 1;
+  *G = g;
+  *dpl = (dim + g - 1) / g;
+}
+
+}  // namespace bp
+
+#define BP_DISPATCH_GD(G, DPL, CALL)                      \
+  switch (G * 16 + DPL) {                                 \
+    case 1 * 16 + 1: { constexpr int g_ = 1, d_ = 1; CALL; break; }   \
+    case 2 * 16 + 1: { constexpr int g_ = 2, d_ = 1; CALL; break; }   \
+    case 4 * 16 + 1: { constexpr int g_ = 4, d_ = 1; CALL; break; }   \
+    case 8 * 16 + 1: { constexpr int g_ = 8, d_ = 1; CALL; break; }   \
+    case 16 * 16 + 1: { constexpr int g_ = 16, d_ = 1; CALL; break; } \
+    case 32 * 16 + 1: { constexpr int g_ = 32, d_ = 1; CALL; break; } \
+    case 32 * 16 + 2: { constexpr int g_ = 32, d_ = 2; CALL; break; } \
+    case 32 * 16 + 3: { constexpr int g_ = 32, d_ = 3; CALL; break; } \
+    case 32 * 16 + 4: { constexpr int g_ = 32, d_ = 4; CALL; break; } \
+    default: return BP_ERR_INVALID;                       \
+  }
+
+extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_t* d_row_index, uint8_t* d_dirty,
+                            int32_t dim, float c_value, float c_label, float lr, int32_t mode, float* d_grad_out,
+                            const uint32_t* d_next_ids, const int64_t* d_n_next, int64_t n_next_max, int64_t* d_stats,
+                            bp_stream_t stream) {
+  using namespace bp;
+  (void)ctx;
+  if (dim < 1 || dim > 128) return BP_ERR_INVALID;
+  if (P->n_occ == 0) return BP_OK;
+  int G, dpl;
+  group_shape(dim, &G, &dpl);
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long groups = P->n_occ;  // upper bound on U
+  const int threads = 256;
+  const int blocks = grid_for(groups * G, threads, kNumSMs * 8);
+  BP_DISPATCH_GD(G, dpl,
+                 (k_stub_step<g_, d_><<<blocks, threads, 0, s>>>(
+                     P->d_seg_start, P->d_occ_pos, P->d_occ_label, P->d_rank_bounds, P->num_ranks,
+                     P->d_num_unique, d_rows, d_row_index, d_dirty, dim, c_value, c_label, lr, mode, d_grad_out,
+                     P->d_uniq_id_s, d_next_ids, (const long long*)d_n_next, n_next_max,
+                     (unsigned long long*)d_stats)));
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_add_at_rows(bp_prep* P, const float* d_vals, int32_t dim, float* d_out, bp_stream_t stream) {
+  using namespace bp;
+  if (dim < 1 || dim > 128) return BP_ERR_INVALID;
+  if (P->n_occ == 0) return BP_OK;
+  int G, dpl;
+  group_shape(dim, &G, &dpl);
+  const int blocks = grid_for(P->n_occ * G, 256, kNumSMs * 8);
+  cudaStream_t s = (cudaStream_t)stream;
+  BP_DISPATCH_GD(G, dpl,
+                 (k_add_at_rows<g_, d_><<<blocks, 256, 0, s>>>(P->d_seg_start, P->d_occ_pos, P->d_uniq_key_s,
+                                                                P->d_num_unique, d_vals, dim, d_out)));
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_prep_key_rows(bp_prep* P, int32_t* d_out, bp_stream_t stream) {
+  using namespace bp;
+  if (P->n_occ == 0) return BP_OK;
+  k_key_rows<<<grid_for(P->n_occ, 256), 256, 0, (cudaStream_t)stream>>>(P->d_uniq_key_s, P->d_num_unique, d_out);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_sgd(const float* d_values, const float* d_grads, float lr, int64_t count, float* d_out,
+                      bp_stream_t stream) {
+  using namespace bp;
+  if (count <= 0) return BP_OK;
+  k_sgd<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(d_values, d_grads, lr, count, d_out);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}

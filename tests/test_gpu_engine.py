@@ -1,0 +1,133 @@
+"""GPU engine vs the reference: byte-identical reports, bit-exact digests,
+fault detection (reference tests/test_engine.py, tests/test_acceptance.py
+criteria 2, 3, 6).  Golden reports were produced by the reference."""
+
+from __future__ import annotations
+
+import json
+
+import pytest
+
+from conftest import golden, unpack
+from oracle import bagpipe_oracle as O
+from paper_2202_12429_b200.traces import Schema, ZipfSpec, batchify_columns, generate_columns
+
+pytestmark = pytest.mark.gpu
+
+SMALL_CASES = ["L8_T1", "L4_T3_rpc1", "L32_cap550_halving", "auto_cap900", "L8_nosplit", "L16_T2", "L1_T2_rpc1",
+               "L8_T1_events"]
+
+
+def _engine():
+    from paper_2202_12429_b200 import engine
+
+    return engine
+
+
+def _cfg(d):
+    return _engine().EngineConfig.from_dict(d)
+
+
+def _assert_report(report, blob):
+    assert report.to_json_bytes().decode() == blob["json"]
+    assert report.to_csv_bytes().decode() == blob["csv"]
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_pipeline_report_byte_identical(small_schema, small_batches, case):
+    blob = golden("reports_small.json")[case]
+    report = _engine().run_pipeline(_cfg(blob["config"]), small_schema, small_batches)
+    _assert_report(report, blob)
+    if "events" in blob:
+        got = [{"iteration": e["iteration"], "prefetch": [(k[0] << 44) | k[1] for k in e["prefetch"]],
+                "ttl_updates": [[(k[0] << 44) | k[1], t] for k, t in e["ttl_updates"]],
+                "evicted": [(k[0] << 44) | k[1] for k in e["evicted"]]} for e in report.events]
+        assert got == blob["events"]
+
+
+@pytest.mark.parametrize("trainers", [1, 2, 3])
+def test_baseline_report_byte_identical(small_schema, small_batches, trainers):
+    blob = golden("reports_small.json")[f"baseline_T{trainers}"]
+    report = _engine().run_synchronous_baseline(_cfg(blob["config"]), small_schema, small_batches)
+    _assert_report(report, blob)
+
+
+def test_object_batches_same_digest(small_schema, small_object_batches):
+    blob = golden("reports_small.json")["L8_T1"]
+    report = _engine().run_pipeline(_cfg(blob["config"]), small_schema, small_object_batches)
+    assert report.final_store_digest == json.loads(blob["json"])["final_store_digest"]
+
+
+def test_worked_example_event_log(worked_trace):
+    blob = golden("reports_small.json")["worked"]
+    report = _engine().run_pipeline(_cfg(blob["config"]), Schema(1, (10,), 0, 4), worked_trace)
+    _assert_report(report, blob)
+    assert [[(k[0] << 44) | k[1] for k in e["evicted"]] for e in report.events] == blob["evicted"]
+    assert [[k.row_id for k in e["evicted"]] for e in report.events] == [[9], [4], [3], [1, 6]]
+
+
+def test_dropped_prefetch_is_a_miss_at_the_reference_key(small_schema, small_batches):
+    from paper_2202_12429_b200.errors import CacheMissError
+
+    want = golden("reports_small.json")["fault_drop_prefetch"]
+    cfg = _cfg(golden("reports_small.json")["L8_T1"]["config"])
+    with pytest.raises(CacheMissError) as err:
+        _engine().run_pipeline(cfg, small_schema, small_batches, fault="drop_prefetch")
+    assert err.value.iteration == want["iteration"]
+    assert err.value.key == unpack(want["key"])
+
+
+def test_ungated_run_reproduces_reference_staleness(small_schema, small_batches):
+    """fault=no_gate: the stale digest equals the reference's stale digest bit
+    for bit, and differs from the baseline with a non-empty diff."""
+    eng = _engine()
+    blob = golden("reports_small.json")["fault_no_gate"]
+    cfg = _cfg(blob["config"])
+    stale = eng.run_pipeline(cfg, small_schema, small_batches, fault="no_gate")
+    _assert_report(stale, blob)
+    base = eng.run_synchronous_baseline(cfg, small_schema, small_batches)
+    result = eng.verify_equivalence(stale, base)
+    assert not result.equal and result.diffs
+
+
+@pytest.fixture(scope="module")
+def acceptance_batches():
+    schema = Schema(2, (60_000, 40_000), 2, 4)
+    rows, labels, dense = generate_columns(ZipfSpec(schema, 1.05, 500 * 512, seed=1337))
+    return schema, batchify_columns(rows, labels, dense, 512)
+
+
+@pytest.mark.parametrize("trainers", [1, 2, 4])
+def test_acceptance_baseline_digests(acceptance_batches, trainers):
+    schema, batches = acceptance_batches
+    eng = _engine()
+    cfg = eng.EngineConfig(cache_capacity=50_000, batch_size=512, lookahead=1, num_trainers=trainers, num_shards=4,
+                           seed=11)
+    rep = eng.run_synchronous_baseline(cfg, schema, batches, trace_fingerprint="zipf1337/512x500")
+    assert rep.final_store_digest == golden("acceptance.json")["baseline"][str(trainers)]
+
+
+@pytest.mark.parametrize("case", ["T2_L64_rpc0.25_cap16000", "T4_L200_rpc1.0_cap16000", "T1_L8_rpc0.25_cap50000"])
+def test_acceptance_pipeline_reports(acceptance_batches, case):
+    schema, batches = acceptance_batches
+    blob = golden("acceptance.json")["pipeline"][case]
+    rep = _engine().run_pipeline(_cfg(blob["config"]), schema, batches, trace_fingerprint="zipf1337/512x500")
+    _assert_report(rep, blob)
+
+
+def test_ck12_pipeline_report_and_baseline_t8():
+    """Criteo-Kaggle shape (config 2: cache 1% of rows, auto lookahead -> 7),
+    12 iterations: report and final digest byte-identical to the reference;
+    the T=8 synchronous baseline digest too."""
+    eng = _engine()
+    g = golden("ck12.json")
+    gen = golden("generator.json")["ck12"]
+    nt, rpt, nd, dim = gen["schema"]
+    schema = Schema(nt, rpt, nd, dim)
+    rows, labels, dense = generate_columns(ZipfSpec(schema, gen["exponent"], gen["n"], gen["seed"]))
+    batches = batchify_columns(rows, labels, dense, 16384)
+    rep = eng.run_pipeline(_cfg(g["pipeline_T1"]["config"]), schema, batches)
+    _assert_report(rep, g["pipeline_T1"])
+    cfg8 = eng.EngineConfig(cache_capacity=g["capacity"], batch_size=16384, lookahead=0, num_trainers=8,
+                            num_shards=1, seed=11)
+    assert eng.run_synchronous_baseline(cfg8, schema, batches).final_store_digest == g["baseline_T8_digest"]
