@@ -192,7 +192,7 @@ def test_combine_rank_order_and_sgd():
     from paper_2202_12429_b200.trainer import combine_core, sgd_step
 
     rng = np.random.default_rng(1)
-    blocks = [rng.standard_normal((4, 3)).astype(np.float32) * 10 ** rng.integers(-4, 4) for _ in range(3)]
+    blocks = [rng.standard_normal((4, 3)).astype(np.float32) * np.float32(10.0) ** int(rng.integers(-4, 4)) for _ in range(3)]
     idx = [np.asarray([0, 1, 2, 3]), np.asarray([2, 0, 1, 3]), np.asarray([3, 2, 1, 0])]
     want = np.zeros((4, 3), np.float32)
     np.add.at(want, np.concatenate(idx), np.concatenate(blocks))
