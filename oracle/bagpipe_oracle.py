@@ -280,107 +280,129 @@ def baseline(batches, rows_per_table, dim: int, seed: int, num_trainers: int, lr
 
 
 # ------------------------------------------------------ pipeline data path
-def pipeline(batches, rows_per_table, dim: int, seed: int, num_trainers: int, capacity: int, lookahead: int,
-             rpc: float, lr=0.01, c_value=0.01, c_label=0.001):
+class OraclePipeline:
     """The pipelined engine's data path (engine.py:302-452) without the clock.
 
-    Returns (store, per-iteration counters dict list).  Dispatch position of
-    plan x: min(first flush boundary >= x - L_x, x - 1) (-1 before
-    iteration 0); forced flush when an unflushed dirty eviction has
+    Dispatch position of plan x: min(first flush boundary >= x - L_x, x - 1)
+    (-1 before iteration 0); forced flush when an unflushed dirty eviction has
     ttl <= x - L_x; flush on (pos+1) % interval == 0; final drain + flush.
+    ``step(pos)`` runs one iteration; ``stats`` collects per-iteration counters.
     """
-    base = batches[0].iteration
-    n = len(batches)
-    L0 = lookahead or auto_lookahead(batches, capacity)
-    interval = max(1, math.ceil(rpc * L0))
-    store = Store(rows_per_table, dim, seed)
-    planner = Planner(L0, capacity)
-    src = ((b.iteration, first_order_unique(batch_occurrences(b)[0])[0]) for b in batches)
-    cache: dict = {}  # key -> [row f32[dim], ttl, dirty]
-    pending, staged, buffered = [], {}, []
-    state = {"exhausted": False, "min_unflushed": None}
-    stats = []
 
-    def dispatch_pos(plan):
-        pos = plan[0] - base
+    def __init__(self, batches, rows_per_table, dim: int, seed: int, num_trainers: int, capacity: int,
+                 lookahead: int, rpc: float, lr=0.01, c_value=0.01, c_label=0.001):
+        self.batches, self.dim, self.T = batches, dim, num_trainers
+        self.capacity, self.lr, self.c_value, self.c_label = capacity, lr, c_value, c_label
+        self.base = batches[0].iteration
+        self.n = len(batches)
+        self.L0 = lookahead or auto_lookahead(batches, capacity)
+        self.interval = max(1, math.ceil(rpc * self.L0))
+        self.store = Store(rows_per_table, dim, seed)
+        self.planner = Planner(self.L0, capacity)
+        self.src = ((b.iteration, first_order_unique(batch_occurrences(b)[0])[0]) for b in batches)
+        self.cache: dict = {}  # key -> [row f32[dim], ttl, dirty]
+        self.pending, self.staged, self.buffered = [], {}, []
+        self.exhausted = False
+        self.min_unflushed = None
+        self.stats: list = []
+
+    def _dispatch_pos(self, plan) -> int:
+        pos = plan[0] - self.base
         s = pos - plan[5]
         if s < 0:
             return -1
-        return min(((s + interval) // interval) * interval - 1, pos - 1)
+        p = self.interval
+        return min(((s + p) // p) * p - 1, pos - 1)
 
-    def flush():
+    def _flush(self) -> None:
         merged: dict = {}
-        for keys, rows in buffered:
+        for keys, rows in self.buffered:
             for k, v in zip(keys, rows):
                 merged[k] = v
         if merged:
             ks = np.asarray(sorted(merged), dtype=np.uint64)
-            store.write(ks, np.stack([merged[k] for k in ks.tolist()]))
-        buffered.clear()
-        state["min_unflushed"] = None
+            self.store.write(ks, np.stack([merged[k] for k in ks.tolist()]))
+        self.buffered.clear()
+        self.min_unflushed = None
 
-    def dispatch_until(cur):
+    def _dispatch_until(self, cur: int) -> None:
         while True:
-            if not pending:
-                if state["exhausted"]:
+            if not self.pending:
+                if self.exhausted:
                     return
-                plan = planner.emit(src)
+                plan = self.planner.emit(self.src)
                 if plan is None:
-                    state["exhausted"] = True
+                    self.exhausted = True
                     return
-                planner.adapt()
-                pending.append(plan)
-            plan = pending[0]
-            if dispatch_pos(plan) > cur:
+                self.planner.adapt()
+                self.pending.append(plan)
+            plan = self.pending[0]
+            if self._dispatch_pos(plan) > cur:
                 return
-            pending.pop(0)
-            theta = plan[0] - plan[5]
-            if state["min_unflushed"] is not None and state["min_unflushed"] <= theta:
-                flush()
-            staged[plan[0] - base] = (plan, store.fetch(plan[1]))
+            self.pending.pop(0)
+            if self.min_unflushed is not None and self.min_unflushed <= plan[0] - plan[5]:
+                self._flush()
+            self.staged[plan[0] - self.base] = (plan, self.store.fetch(plan[1]))
 
-    def evict(pred):
-        gone = sorted(k for k, e in cache.items() if pred(e))
-        rows = [cache.pop(k) for k in gone]
-        return gone, rows
+    def _evict(self, pred):
+        gone = sorted(k for k, e in self.cache.items() if pred(e))
+        return gone, [self.cache.pop(k) for k in gone]
 
-    dispatch_until(-1)
-    for pos, b in enumerate(batches):
+    def _buffer(self, gone, ent, iteration) -> int:
+        dirty = [(k, e[0]) for k, e in zip(gone, ent) if e[2]]
+        if dirty:
+            self.buffered.append(([k for k, _ in dirty], [v for _, v in dirty]))
+            if self.min_unflushed is None:
+                self.min_unflushed = iteration
+        return len(dirty)
+
+    def begin(self) -> None:
+        self._dispatch_until(-1)
+
+    def step(self, pos: int) -> None:
+        cache = self.cache
         if pos > 0:
-            dispatch_until(pos - 1)
-        (iteration, pf, uniq, ttl, _, _), pf_rows = staged.pop(pos)
+            self._dispatch_until(pos - 1)
+        (iteration, pf, uniq, ttl, _, _), pf_rows = self.staged.pop(pos)
         ttl_of = dict(zip(uniq.tolist(), ttl.tolist()))
-        if len(cache) + len(pf) > capacity:
+        if len(cache) + len(pf) > self.capacity:
             raise RuntimeError(f"capacity exceeded at {iteration}")
         for k, v in zip(pf.tolist(), pf_rows):
             cache[k] = [v.copy(), ttl_of[k], False]
         for k, t in ttl_of.items():
             cache[k][1] = t
         occ_peak = len(cache)
-        vals = np.stack([cache[k][0] for k in uniq.tolist()]) if uniq.size else np.zeros((0, dim), np.float32)
-        _, g = batch_gradients(b, vals, num_trainers, c_value, c_label)
-        new = sgd(vals, g, lr)
+        keys = uniq.tolist()
+        vals = np.stack([cache[k][0] for k in keys]) if keys else np.zeros((0, self.dim), np.float32)
+        _, g = batch_gradients(self.batches[pos], vals, self.T, self.c_value, self.c_label)
+        new = sgd(vals, g, self.lr)
         dirty = (g != 0).any(axis=1)
-        for i, k in enumerate(uniq.tolist()):
-            cache[k][0] = new[i]
-            cache[k][2] = cache[k][2] or bool(dirty[i])
-        gone, ent = evict(lambda e: e[1] <= iteration)
-        n_dirty = sum(e[2] for e in ent)
-        if n_dirty:
-            buffered.append(([k for k, e in zip(gone, ent) if e[2]], [e[0] for e in ent if e[2]]))
-            if state["min_unflushed"] is None:
-                state["min_unflushed"] = iteration
-        if pos == n - 1:
-            gone2, ent2 = evict(lambda e: True)
-            if any(e[2] for e in ent2):
-                buffered.append(([k for k, e in zip(gone2, ent2) if e[2]], [e[0] for e in ent2 if e[2]]))
-            flush()
+        for i, k in enumerate(keys):
+            e = cache[k]
+            e[0] = new[i]
+            e[2] = e[2] or bool(dirty[i])
+        gone, ent = self._evict(lambda e: e[1] <= iteration)
+        n_dirty = self._buffer(gone, ent, iteration)
+        if pos == self.n - 1:
+            gone2, ent2 = self._evict(lambda e: True)
+            self._buffer(gone2, ent2, iteration)
+            self._flush()
             gone = gone + gone2
-        elif (pos + 1) % interval == 0 and buffered:
-            flush()
-        stats.append({"prefetch": len(pf), "evicted": len(gone), "dirty": n_dirty, "occupancy_peak": occ_peak,
-                      "occupancy_end": len(cache), "unique": int(uniq.size)})
-    return store, stats
+        elif (pos + 1) % self.interval == 0 and self.buffered:
+            self._flush()
+        self.stats.append({"prefetch": len(pf), "evicted": len(gone), "dirty": n_dirty, "occupancy_peak": occ_peak,
+                           "occupancy_end": len(cache), "unique": len(keys)})
+
+
+def pipeline(batches, rows_per_table, dim: int, seed: int, num_trainers: int, capacity: int, lookahead: int,
+             rpc: float, lr=0.01, c_value=0.01, c_label=0.001):
+    """Run the whole pipeline data path; returns (store, per-iteration counters)."""
+    run = OraclePipeline(batches, rows_per_table, dim, seed, num_trainers, capacity, lookahead, rpc, lr, c_value,
+                         c_label)
+    run.begin()
+    for pos in range(run.n):
+        run.step(pos)
+    return run.store, run.stats
 
 
 def plan_sha(plan) -> str:

@@ -25,6 +25,7 @@ report and the gate need.
 
 from __future__ import annotations
 
+import ctypes as C
 import hashlib
 import json
 import math
@@ -40,7 +41,7 @@ from . import _lib as L
 from .cache import DynamicCache
 from .device import DevicePrep
 from .errors import CacheCapacityError, ConfigurationError, EngineError, IncomparableRunsError
-from .lookahead import adapt_on_pressure, auto_lookahead, emit_next_plan, new_state
+from .lookahead import CachePlan, DevicePlan, adapt_on_pressure, auto_lookahead, new_state
 from .report import IterationRecord, RunReport
 from .store import ShardedStore
 from .trainer import BP_STUB_SGD, StubModelConfig, f32
@@ -152,19 +153,44 @@ _METADATA = {
 
 
 class _Chunk:
-    """Dirty evictions of one iteration, still in HBM, awaiting a flush."""
+    """Evictions of one iteration, still in HBM, awaiting a flush."""
 
     __slots__ = ("ids", "rows", "dirty", "count", "n", "n_dirty", "keys")
 
-    def __init__(self, ids, rows, dirty, count, n, n_dirty, keys=None):
-        self.ids, self.rows, self.dirty, self.count = ids, rows, dirty, count
-        self.n, self.n_dirty, self.keys = n, n_dirty, keys
+    def __init__(self, ids, rows, dirty, count, keys=None):
+        self.ids, self.rows, self.dirty, self.count, self.keys = ids, rows, dirty, count, keys
+        self.n = self.n_dirty = 0
+
+
+class _PendingPlan:
+    """An emitted plan whose device counters are read lazily (the next host
+    synchronisation makes them final), so emission never blocks the host."""
+
+    __slots__ = ("plan", "h_counts", "done")
+
+    def __init__(self, plan, stream):
+        self.plan = plan
+        self.h_counts = torch.empty(4, dtype=torch.int64, pin_memory=True)
+        self.h_counts.copy_(plan.device.counts, non_blocking=True)
+        self.done = torch.cuda.Event()
+        self.done.record(stream)
+
+    def counts(self):
+        if not self.done.query():
+            self.done.synchronize()
+        return self.h_counts
 
 
 class _Pipeline:
-    """One pipelined run (reference engine.py:239-649) driving the GPU."""
+    """One pipelined run (reference engine.py:239-649) driving the GPU.
 
-    def __init__(self, cfg: EngineConfig, schema: Schema, batches: list, fingerprint, fault):
+    ``begin`` / ``step(pos)`` / ``end`` split the reference's run loop so a
+    benchmark can time single iterations.  Each step enqueues its kernels
+    with device-side counts and synchronises exactly once, at the end, to
+    read the counters the simulated clock, the gate and the report need.
+    """
+
+    def __init__(self, cfg: EngineConfig, schema: Schema, batches: list, fingerprint, fault, device_inputs=None):
         if fault not in (None, FAULT_NO_GATE, FAULT_DROP_PREFETCH):
             raise ConfigurationError(f"unknown fault {fault!r}")
         self.cfg, self.schema, self.batches = cfg, schema, batches
@@ -173,9 +199,11 @@ class _Pipeline:
         self.n = len(batches)
         self.T = cfg.num_trainers
         self.stream = torch.cuda.current_stream()
+        self.device_inputs = device_inputs  # optional {pos: (d_keys, d_labels)} already in HBM
         self._preps: dict = {}
         stub = cfg.stub()
         self.c_value, self.c_label, self.lr = f32(stub.c_value), f32(stub.c_label), f32(stub.lr)
+        self.probe = None  # optional callable(name, phase) for kernel timing
 
         self.L0 = cfg.lookahead or auto_lookahead(iter(batches), cfg.cache_capacity, schema=schema,
                                                   prep_provider=self._prep_of_batch)
@@ -187,6 +215,7 @@ class _Pipeline:
                                prep_provider=self._prep_of_batch)
         self.source = iter(batches)
         self.snapshots = {} if cfg.check_mirror else None
+        self._adapt_pending = None
 
         self.pending: deque = deque()
         self.exhausted = False
@@ -209,27 +238,57 @@ class _Pipeline:
         self.peak_occupancy = 0
         self.drop_done = False
         self.stats = torch.zeros(2, dtype=torch.int64, device="cuda")
-        self.h_stats = torch.zeros(4, dtype=torch.int64).pin_memory()
+        self.h_step = torch.zeros(8, dtype=torch.int64, pin_memory=True)
+        self.kernel_launches = 0
 
     # -- batch preps (device) ------------------------------------------------------
     def _prep_of_batch(self, batch: Batch) -> DevicePrep:
         pos = batch.iteration - self.base
         prep = self._preps.get(pos)
         if prep is None:
-            prep = DevicePrep.from_batch(batch, self.T, self.schema, stream=self.stream)
+            dev = self.device_inputs.get(pos) if self.device_inputs else None
+            if dev is not None:
+                keys, labels = dev
+                n = keys.numel()
+                prep = DevicePrep(None, None, batch.rank_bounds(self.T), batch.iteration, self.schema,
+                                  stream=self.stream, d_keys=keys, d_labels=labels)
+            else:
+                prep = DevicePrep.from_batch(batch, self.T, self.schema, stream=self.stream)
             self._preps[pos] = prep
         return prep
 
     def _prep(self, pos: int) -> DevicePrep:
         return self._prep_of_batch(self.batches[pos])
 
-    # -- plan dispatch (reference engine.py:302-346) ------------------------------
+    # -- plan emission (reference engine.py:198-236, lookahead.py:64-123) --------
     def _next_plan(self):
-        plan = emit_next_plan(self.state, self.source)
-        if plan is not None:
-            if self.snapshots is not None:
-                self.snapshots[plan.iteration - self.base] = self.state.mirror_keys_u64()
-            adapt_on_pressure(self.state)
+        st = self.state
+        if self._adapt_pending is not None:
+            # The reference adapts lazily, when the next plan is requested.
+            st.projected_occupancy = int(self._adapt_pending.counts()[2])
+            adapt_on_pressure(st)
+            self._adapt_pending = None
+        lib = L.lib()
+        sp = L.stream_ptr(self.stream)
+        while len(st.batch_queue) < st.lookahead:
+            batch = next(self.source, None)
+            if batch is None:
+                break
+            prep = self._prep_of_batch(batch)
+            st.batch_queue.append(batch)
+            st._preps.append(prep)
+            L.check(lib.bp_planner_refill(st.handle, prep.handle, sp), "bp_planner_refill")
+        if not st.batch_queue:
+            return None
+        batch = st.batch_queue.popleft()
+        prep = st._preps.popleft()
+        dev = DevicePlan(prep, exact=False)
+        L.check(lib.bp_planner_pop(st.handle, prep.handle, C.byref(dev.buffers()), sp), "bp_planner_pop")
+        plan = CachePlan(batch.iteration, None, None, st.lookahead, device=dev)
+        self._adapt_pending = _PendingPlan(plan, self.stream)
+        dev.h_pending = self._adapt_pending
+        if self.snapshots is not None:
+            self.snapshots[plan.iteration - self.base] = st.mirror_keys_u64()
         return plan
 
     def _dispatch_pos(self, plan) -> int:
@@ -253,10 +312,9 @@ class _Pipeline:
             self.forced_flushes += 1
         arrival = self._gate_time(theta) + self.cfg.fetch_latency
         dev = plan.device
-        n_pf = dev.n_prefetch
-        rows = self.store.fetch_ids_async(dev.prefetch_ids, n_pf, stream=self.stream)
-        if n_pf:
-            self.store.fetch_calls += 1
+        self._probe("store_fetch", 0)
+        rows = self.store.fetch_ids_async(dev.prefetch_ids, dev.cap, d_n=dev.counts[0:1], stream=self.stream)
+        self._probe("store_fetch", 1)
         self.staged[plan.iteration - self.base] = (plan, rows, arrival)
 
     def _dispatch_until(self, cur: int) -> None:
@@ -275,13 +333,19 @@ class _Pipeline:
             self.pending.popleft()
             self._dispatch(plan, cur)
 
+    def _probe(self, name: str, phase: int) -> None:
+        if self.probe is not None:
+            self.probe(name, phase, self.stream)
+
     # -- write-back (reference engine.py:350-377) ---------------------------------
     def _flush(self, kind: str, pos: int) -> None:
         flusher = self.flush_counter % self.T
         count = 0
         if self.chunks:
+            self._probe("store_write", 0)
             for ch in self.chunks:  # in eviction order: the last write wins
                 self.store.write_ids_async(ch.ids, ch.rows, ch.n, d_mask=ch.dirty, stream=self.stream)
+            self._probe("store_write", 1)
             count = self._merged_count()
             self.store.write_calls += 1
             self.store.entries_written += count
@@ -299,30 +363,22 @@ class _Pipeline:
             # window (its re-prefetch waits for the flush of the first
             # eviction), so chunk key sets are disjoint.
             return sum(ch.n_dirty for ch in self.chunks)
-        keys = np.concatenate([self._chunk_dirty_ids(ch) for ch in self.chunks])
-        return int(np.unique(keys).size)
-
-    @staticmethod
-    def _chunk_dirty_ids(ch) -> np.ndarray:
-        ids = L.to_host(ch.ids, ch.n)
-        dirty = L.to_host(ch.dirty, ch.n).astype(bool)
-        return ids[dirty]
+        ids = [L.to_host(ch.ids, ch.n)[L.to_host(ch.dirty, ch.n).astype(bool)] for ch in self.chunks]
+        return int(np.unique(np.concatenate(ids)).size)
 
     # -- per iteration ---------------------------------------------------------------
     def _evict(self, completed: int, drain: bool, out_cap: int) -> _Chunk:
         cap = max(1, out_cap)
         dim = self.schema.emb_dim
-        ids = torch.empty(cap, dtype=torch.uint32, device="cuda")
-        rows = torch.empty((cap, dim), dtype=torch.float32, device="cuda")
-        dirty = torch.empty(cap, dtype=torch.uint8, device="cuda")
-        keys = torch.empty(cap, dtype=torch.uint64, device="cuda") if self.events is not None else None
-        count = torch.zeros(2, dtype=torch.int64, device="cuda")
-        buf = L.EvictBuffers(L.ptr(keys), L.ptr(ids), L.ptr(rows), L.ptr(dirty), L.ptr(count))
-        import ctypes as C
-
+        ch = _Chunk(torch.empty(cap, dtype=torch.uint32, device="cuda"),
+                    torch.empty((cap, dim), dtype=torch.float32, device="cuda"),
+                    torch.empty(cap, dtype=torch.uint8, device="cuda"),
+                    torch.zeros(2, dtype=torch.int64, device="cuda"),
+                    torch.empty(cap, dtype=torch.uint64, device="cuda") if self.events is not None else None)
+        buf = L.EvictBuffers(L.ptr(ch.keys), L.ptr(ch.ids), L.ptr(ch.rows), L.ptr(ch.dirty), L.ptr(ch.count))
         L.check(L.lib().bp_cache_evict(self.cache.handle, completed, 1 if drain else 0, C.byref(buf), cap,
                                        L.stream_ptr(self.stream)), "bp_cache_evict")
-        return _Chunk(ids, rows, dirty, count, 0, 0, keys)
+        return ch
 
     def _buffer(self, ch: _Chunk, iteration: int) -> None:
         self.clean_evictions += ch.n - ch.n_dirty
@@ -337,104 +393,116 @@ class _Pipeline:
             return []
         return unpack_keys(np.sort(L.to_host(ch.keys, ch.n)))
 
-    def run(self) -> RunReport:
-        import ctypes as C
+    def begin(self) -> None:
+        self._dispatch_until(-1)
 
+    def step(self, pos: int) -> None:
         cfg, lib, ctx = self.cfg, L.lib(), L.Context.get()
         sp = L.stream_ptr(self.stream)
         bw = cfg.sync_bandwidth
-        self._dispatch_until(-1)
-        for pos, batch in enumerate(self.batches):
-            if pos > 0:
-                self._dispatch_until(pos - 1)
-            iteration = batch.iteration
-            staged = self.staged.pop(pos, None)
-            if staged is None:
-                raise EngineError(f"no staged prefetch for position {pos}")
-            plan, rows, arrival = staged
-            if plan.iteration != iteration:
-                raise EngineError(f"plan {plan.iteration} misaligned with batch {iteration}")
-            dev = plan.device
-            prep = self._prep(pos)
-            n_pf = dev.n_prefetch
-            off = 0
-            skip_key, has_skip = 0, 0
-            if self.fault == FAULT_DROP_PREFETCH and not self.drop_done and pos >= self.n // 2 and n_pf:
-                # Drop the first (smallest) prefetched key from the plan: it is
-                # neither inserted nor TTL-updated, so the lookup must miss.
-                skip_key = int(L.to_host(dev.prefetch_keys, 1)[0])
-                has_skip, off = 1, 1
-                self.drop_done = True
-            n_ins = n_pf - off
-            if self.occupancy + n_ins > cfg.cache_capacity:
-                raise CacheCapacityError(f"inserting {n_ins} entries into {self.occupancy}/{cfg.cache_capacity}")
-            if n_ins:
-                dim = self.schema.emb_dim
-                L.check(lib.bp_cache_insert(
-                    self.cache.handle, L.ptr(dev.prefetch_keys) + 8 * off, L.ptr(dev.prefetch_ids) + 4 * off,
-                    L.ptr(rows) + 4 * dim * off, L.ptr(dev.prefetch_ttls) + 8 * off, n_ins, None, iteration, sp),
-                    "bp_cache_insert")
-            self.occupancy += n_ins
-            occupancy_peak = self.occupancy
-            self.peak_occupancy = max(self.peak_occupancy, occupancy_peak)
-            self.total_prefetched += n_ins
+        batch = self.batches[pos]
+        if pos > 0:
+            self._dispatch_until(pos - 1)
+        iteration = batch.iteration
+        staged = self.staged.pop(pos, None)
+        if staged is None:
+            raise EngineError(f"no staged prefetch for position {pos}")
+        plan, rows, arrival = staged
+        if plan.iteration != iteration:
+            raise EngineError(f"plan {plan.iteration} misaligned with batch {iteration}")
+        dev = plan.device
+        prep = self._prep(pos)
+        off, skip_key, has_skip = 0, 0, 0
+        if self.fault == FAULT_DROP_PREFETCH and not self.drop_done and pos >= self.n // 2 and dev.n_prefetch:
+            # Drop the first (smallest) prefetched key: it is neither inserted
+            # nor TTL-updated, so the lookup must miss (reference engine.py:512-523).
+            skip_key = int(L.to_host(dev.prefetch_keys, 1)[0])
+            has_skip, off = 1, 1
+            self.drop_done = True
+        dim = self.schema.emb_dim
+        # apply_prefetch: device count (minus the dropped key), device-side capacity check
+        if off:
+            n_ins_dev = dev.counts[0:1] - off
+        else:
+            n_ins_dev = dev.counts[0:1]
+        self._probe("cache_insert", 0)
+        L.check(lib.bp_cache_insert(
+            self.cache.handle, L.ptr(dev.prefetch_keys) + 8 * off, L.ptr(dev.prefetch_ids) + 4 * off,
+            L.ptr(rows) + 4 * dim * off, L.ptr(dev.prefetch_ttls) + 8 * off, max(dev.cap - off, 0),
+            L.ptr(n_ins_dev), iteration, sp), "bp_cache_insert")
+        slots = torch.empty(max(prep.n_occ, 1), dtype=torch.int32, device="cuda")
+        L.check(lib.bp_cache_apply_resolve(self.cache.handle, prep.handle, L.ptr(dev.ttl_k), skip_key, has_skip,
+                                           L.ptr(slots), sp), "bp_cache_apply_resolve")
+        self._probe("cache_insert", 1)
+        nxt = self._prep(pos + 1) if pos + 1 < self.n else None
+        self.stats.zero_()
+        self._probe("stub_step", 0)
+        L.check(lib.bp_stub_step(ctx.handle, prep.handle, L.ptr(self.cache.values), L.ptr(slots),
+                                 L.ptr(self.cache.dirty), dim, self.c_value, self.c_label, self.lr, BP_STUB_SGD, None,
+                                 nxt.view.d_uniq_id_s if nxt is not None else None,
+                                 nxt.view.d_num_unique if nxt is not None else None,
+                                 nxt.n_occ if nxt is not None else 0, L.ptr(self.stats), sp), "bp_stub_step")
+        self._probe("stub_step", 1)
+        self._probe("cache_evict", 0)
+        ch = self._evict(iteration, False, min(cfg.cache_capacity, max(prep.n_occ, 1)))
+        self._probe("cache_evict", 1)
+        # one host synchronisation: counters for the clock, gate and report
+        h = self.h_step
+        h[0:1].copy_(prep.tensor("d_num_unique", torch.int64, 1), non_blocking=True)
+        h[1:2].copy_(n_ins_dev, non_blocking=True)
+        h[2:4].copy_(self.stats, non_blocking=True)
+        h[4:6].copy_(ch.count, non_blocking=True)
+        ctx.raise_pending(self.stream)
+        u, n_ins, crit_count, _, n_ev, n_ev_dirty = (int(v) for v in h[:6].tolist())
+        ch.n, ch.n_dirty = n_ev, n_ev_dirty
+        self.occupancy += n_ins
+        occupancy_peak = self.occupancy
+        self.occupancy -= n_ev
+        self.peak_occupancy = max(self.peak_occupancy, occupancy_peak)
+        self.total_prefetched += n_ins
+        if n_ins:
+            self.store.fetch_calls += 1
 
-            stall = max(0.0, arrival - self.crit_end)
-            blocked_prefetch = min(stall, max(0.0, cfg.fetch_latency - self.crit_end))
-            blocked_eviction = stall - blocked_prefetch
-            compute_end = self.crit_end + stall + cfg.compute_latency
+        stall = max(0.0, arrival - self.crit_end)
+        blocked_prefetch = min(stall, max(0.0, cfg.fetch_latency - self.crit_end))
+        blocked_eviction = stall - blocked_prefetch
+        compute_end = self.crit_end + stall + cfg.compute_latency
+        if cfg.split_sync:
+            critical_size = crit_count if nxt is not None else 0
+            background_size = u - critical_size
+        else:
+            critical_size, background_size = u, 0
+        sync_start = max(compute_end, self.bg_end)
+        blocked_background = sync_start - compute_end
+        self.crit_end = sync_start + critical_size / bw
+        self.bg_end = self.crit_end + background_size / bw
+        partial = {
+            "iteration": iteration, "warmup": pos < self.L0, "compute": cfg.compute_latency,
+            "critical_sync": critical_size / bw, "blocked_on_prefetch": blocked_prefetch,
+            "blocked_on_eviction": blocked_eviction, "blocked_on_background": blocked_background,
+            "occupancy_peak": occupancy_peak, "prefetch_count": n_ins, "critical_size": critical_size,
+            "background_size": background_size, "lookahead": plan.lookahead,
+        }
+        if self.events is not None:
+            ttl = plan.ttl_updates
+            if has_skip:
+                lost = unpack_key(skip_key)
+                ttl = [(k, t) for k, t in ttl if k != lost]
+            partial["prefetch_keys"] = list(plan.prefetch[off:])
+            partial["ttl_updates"] = list(ttl)
+        self._maintenance(pos, ch, partial)
+        self._preps.pop(pos, None)
 
-            u = prep.num_unique
-            slots = torch.empty(max(u, 1), dtype=torch.int32, device="cuda")
-            L.check(lib.bp_cache_apply_resolve(self.cache.handle, prep.handle, L.ptr(dev.ttl_k), skip_key, has_skip,
-                                               L.ptr(slots), sp), "bp_cache_apply_resolve")
-            nxt = self._prep(pos + 1) if pos + 1 < self.n else None
-            self.stats.zero_()
-            nxt_ids = nxt.view.d_uniq_id_s if nxt is not None else None
-            nxt_n = nxt.view.d_num_unique if nxt is not None else None
-            L.check(lib.bp_stub_step(ctx.handle, prep.handle, L.ptr(self.cache.values), L.ptr(slots),
-                                     L.ptr(self.cache.dirty), self.schema.emb_dim, self.c_value, self.c_label,
-                                     self.lr, BP_STUB_SGD, None, nxt_ids, nxt_n,
-                                     nxt.n_occ if nxt is not None else 0, L.ptr(self.stats), sp), "bp_stub_step")
-            # maintenance: evict ttl <= iteration into a flush chunk
-            ch = self._evict(iteration, False, min(cfg.cache_capacity, max(u, 1)))
-            self.h_stats[:2].copy_(self.stats, non_blocking=True)
-            self.h_stats[2:].copy_(ch.count, non_blocking=True)
-            ctx.raise_pending(self.stream)  # synchronises; raises the first device error
-            crit_count, _, n_ev, n_ev_dirty = (int(v) for v in self.h_stats.tolist())
-            ch.n, ch.n_dirty = n_ev, n_ev_dirty
-            self.occupancy -= n_ev
-
-            if cfg.split_sync:
-                critical_size = crit_count if nxt is not None else 0
-                background_size = u - critical_size
-            else:
-                critical_size, background_size = u, 0
-            sync_start = max(compute_end, self.bg_end)
-            blocked_background = sync_start - compute_end
-            self.crit_end = sync_start + critical_size / bw
-            self.bg_end = self.crit_end + background_size / bw
-            partial = {
-                "iteration": iteration, "warmup": pos < self.L0, "compute": cfg.compute_latency,
-                "critical_sync": critical_size / bw, "blocked_on_prefetch": blocked_prefetch,
-                "blocked_on_eviction": blocked_eviction, "blocked_on_background": blocked_background,
-                "occupancy_peak": occupancy_peak, "prefetch_count": n_ins, "critical_size": critical_size,
-                "background_size": background_size, "lookahead": plan.lookahead,
-            }
-            if self.events is not None:
-                pf = plan.prefetch[off:]
-                ttl = plan.ttl_updates
-                if has_skip:
-                    lost = unpack_key(skip_key)
-                    ttl = [(k, t) for k, t in ttl if k != lost]
-                partial["prefetch_keys"] = list(pf)
-                partial["ttl_updates"] = list(ttl)
-            self._maintenance(pos, ch, partial)
-            self._preps.pop(pos, None)
-            del rows, slots
+    def end(self) -> RunReport:
         if not self.exhausted and (self.pending or self._next_plan() is not None):
             raise EngineError("planner emitted more plans than batches")
         return self._report()
+
+    def run(self) -> RunReport:
+        self.begin()
+        for pos in range(self.n):
+            self.step(pos)
+        return self.end()
 
     def _maintenance(self, pos: int, ch: _Chunk, partial: dict) -> None:
         iteration = self.base + pos
@@ -444,9 +512,9 @@ class _Pipeline:
         last = pos == self.n - 1
         if last:
             drain = self._evict(iteration, True, max(1, self.occupancy))
-            self.h_stats[2:].copy_(drain.count, non_blocking=True)
+            self.h_step[4:6].copy_(drain.count, non_blocking=True)
             L.Context.get().raise_pending(self.stream)
-            drain.n, drain.n_dirty = (int(v) for v in self.h_stats[2:].tolist())
+            drain.n, drain.n_dirty = (int(v) for v in self.h_step[4:6].tolist())
             self.occupancy -= drain.n
             self._buffer(drain, iteration)
             if self.chunks:

@@ -31,9 +31,12 @@ _MIRRORED = 2
 class DevicePlan:
     """Plan buffers of one emission, resident in HBM."""
 
-    def __init__(self, prep: DevicePrep):
-        u = prep.num_unique
+    def __init__(self, prep: DevicePrep, exact: bool = True):
+        # exact: size buffers by U (one sync); else by the occurrence count,
+        # an upper bound known on the host, so emission never blocks.
+        u = prep.num_unique if exact else prep.n_occ
         self.prep = prep
+        self.h_pending = None
         self.cap = u
         dev = "cuda"
         self.prefetch_keys = torch.empty(max(u, 1), dtype=torch.uint64, device=dev)
@@ -48,9 +51,12 @@ class DevicePlan:
         return L.PlanBuffers(L.ptr(self.prefetch_keys), L.ptr(self.prefetch_ids), L.ptr(self.prefetch_ttls),
                              L.ptr(self.ttl_k), L.ptr(self.evict_keys), L.ptr(self.counts))
 
-    def read_counts(self, stream=None) -> np.ndarray:
+    def read_counts(self) -> np.ndarray:
         if self.h_counts is None:
-            self.h_counts = self.counts.cpu().numpy()
+            if self.h_pending is not None:
+                self.h_counts = self.h_pending.counts().numpy().copy()
+            else:
+                self.h_counts = self.counts.cpu().numpy()
         return self.h_counts
 
     @property
@@ -93,7 +99,7 @@ class CachePlan:
     def ttl_updates(self) -> list:
         if self._ttl_updates is None:
             d = self.device
-            u = d.cap
+            u = d.prep.num_unique
             if u == 0:
                 self._ttl_updates = []
             else:
