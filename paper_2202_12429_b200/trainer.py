@@ -85,8 +85,9 @@ def combine_core(rank_batch_idx, rank_grads, num_unique: int, emb_dim: int) -> n
     grads = np.ascontiguousarray(np.concatenate([rank_grads[i] for i in nonempty]), dtype=np.float32)
     prep = _index_prep(idx, np.zeros(len(idx), dtype=np.uint8))
     d_out = L.to_device(out)
-    L.check(L.lib().bp_add_at_rows(prep.handle, L.ptr(L.to_device(grads)), emb_dim, L.ptr(d_out),
-                                   L.stream_ptr()), "bp_add_at_rows")
+    d_grads = L.to_device(grads)  # keep alive until the kernel is enqueued after every upload
+    L.check(L.lib().bp_add_at_rows(prep.handle, L.ptr(d_grads), emb_dim, L.ptr(d_out), L.stream_ptr()),
+            "bp_add_at_rows")
     return d_out.cpu().numpy()
 
 
@@ -97,8 +98,8 @@ def sgd_step(values, grads, lr: float) -> np.ndarray:
     if v.size == 0:
         return v.copy()
     d_out = torch.empty(v.shape, dtype=torch.float32, device="cuda")
-    L.check(L.lib().bp_sgd(L.ptr(L.to_device(v)), L.ptr(L.to_device(g)), f32(lr), v.size, L.ptr(d_out),
-                           L.stream_ptr()), "bp_sgd")
+    d_v, d_g = L.to_device(v), L.to_device(g)
+    L.check(L.lib().bp_sgd(L.ptr(d_v), L.ptr(d_g), f32(lr), v.size, L.ptr(d_out), L.stream_ptr()), "bp_sgd")
     return d_out.cpu().numpy()
 
 

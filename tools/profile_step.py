@@ -1,0 +1,71 @@
+"""Profile engine steps at the Criteo-Kaggle bench shape.
+
+  python tools/profile_step.py [--steps 3] [--nvtx] [--torch-prof]
+
+--nvtx wraps each profiled step in an NVTX range "timed_step" so that
+  ncu --nvtx --nvtx-include "timed_step/" ... captures only those launches.
+--torch-prof prints a per-kernel device-time table (torch profiler / CUPTI).
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2202_12429_b200.engine import EngineConfig, _Pipeline  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--nvtx", action="store_true")
+    ap.add_argument("--torch-prof", action="store_true")
+    ap.add_argument("--host-inputs", action="store_true")
+    args = ap.parse_args()
+    sc = bench.schema()
+    n = args.warmup + args.steps + 12
+    batches = bench.make_batches(n, 1)
+    cfg = EngineConfig(cache_capacity=sc.total_rows // 100, batch_size=bench.BATCH, lookahead=0, num_shards=1,
+                       seed=11)
+    dev = None
+    if not args.host_inputs:
+        dev = {}
+        for i, b in enumerate(batches):
+            k, lab, _ = b.packed_occurrences()
+            dev[i] = (torch.from_numpy(k).cuda(), torch.from_numpy(lab).cuda())
+    pipe = _Pipeline(cfg, sc, batches, None, None, device_inputs=dev)
+    pipe.begin()
+    for pos in range(args.warmup):
+        pipe.step(pos)
+    torch.cuda.synchronize()
+    if args.torch_prof:
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+            for i in range(args.steps):
+                pipe.step(args.warmup + i)
+            torch.cuda.synchronize()
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=40))
+        print(prof.key_averages().table(sort_by="cpu_time_total", row_limit=25))
+        return
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        if args.nvtx:
+            torch.cuda.nvtx.range_push("timed_step")
+        pipe.step(args.warmup + i)
+        if args.nvtx:
+            torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
+    print(f"{args.steps} steps in {(time.perf_counter() - t0) * 1e3:.2f} ms")
+
+
+if __name__ == "__main__":
+    main()
