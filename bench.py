@@ -141,6 +141,9 @@ class Probe:
             self.spans.setdefault(name, []).append((self.open.pop(name), ev))
 
     def totals_ms(self) -> dict:
+        for v in self.spans.values():
+            for _, b in v:
+                b.synchronize()
         return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.spans.items()}
 
     def counts(self) -> dict:

@@ -291,12 +291,14 @@ extern "C" int bp_sort_keys_u64(uint64_t* d_keys, uint32_t* d_vals, int64_t n, i
   cudaStream_t s = (cudaStream_t)stream;
   uint64_t* kb;
   uint32_t* vb;
-  uint32_t* hist;
+  uint32_t *hist, *partials;
   BP_CUDA_TRY(bp::pool_alloc(&kb, n, s));
   BP_CUDA_TRY(bp::pool_alloc(&vb, n, s));
   BP_CUDA_TRY(bp::pool_alloc(&hist, bp::sort_hist_words(n), s));
+  BP_CUDA_TRY(bp::pool_alloc(&partials, bp::sort_partials_words(n), s));
   int which = 0;
-  BP_CUDA_TRY(bp::radix_sort_pairs<uint64_t>(d_keys, d_vals, kb, vb, n, nullptr, 0, key_bits, hist, &which, s));
+  BP_CUDA_TRY(bp::radix_sort_pairs<uint64_t>(d_keys, d_vals, kb, vb, n, nullptr, 0, key_bits, hist, partials, &which,
+                                             s));
   if (which) {
     BP_CUDA_TRY(cudaMemcpyAsync(d_keys, kb, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     BP_CUDA_TRY(cudaMemcpyAsync(d_vals, vb, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
@@ -304,6 +306,7 @@ extern "C" int bp_sort_keys_u64(uint64_t* d_keys, uint32_t* d_vals, int64_t n, i
   cudaFreeAsync(kb, s);
   cudaFreeAsync(vb, s);
   cudaFreeAsync(hist, s);
+  cudaFreeAsync(partials, s);
   return BP_OK;
 }
 

@@ -45,18 +45,34 @@ __global__ void k_prep_heads(const K* __restrict__ sk, long long n, uint32_t* __
     head[j] = (j == 0 || sk[j] != sk[j - 1]) ? 1u : 0u;
 }
 
+__device__ __forceinline__ int rank_of(long long p, const long long* __restrict__ rb, int num_ranks) {
+  int r = 0;
+  while (r + 1 < num_ranks && p >= rb[r + 1]) ++r;
+  return r;
+}
+
 // Segment heads: CSR start, unique key/id (sorted order), first-occurrence
 // flag at the head's position (the smallest position of the key: stable sort).
+// Every occurrence's label byte carries bit 7 = "first occurrence of this key
+// in its trainer rank", so the trainer streams one byte per occurrence and
+// closes a rank partial on the flag (reference combine order, trainer.py:92-105).
 template <typename K>
 __global__ void k_prep_segments(const K* __restrict__ sk, const uint32_t* __restrict__ pos,
                                 const uint32_t* __restrict__ head, const uint32_t* __restrict__ segx, long long n,
                                 const uint64_t* __restrict__ keys, const uint8_t* __restrict__ labels,
                                 int schema_mode, uint32_t* __restrict__ seg_start, uint64_t* __restrict__ uniq_key_s,
                                 uint32_t* __restrict__ uniq_id_s, uint32_t* __restrict__ first_flag,
-                                uint8_t* __restrict__ occ_label, const long long* d_num_unique) {
+                                uint8_t* __restrict__ occ_label, const long long* d_num_unique,
+                                const long long* __restrict__ rank_bounds, int num_ranks, ErrorRecord* err,
+                                long long iteration) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
     const uint32_t p = pos[j];
-    occ_label[j] = labels[p];
+    const uint8_t lab = labels[p];
+    if (lab > 127) raise_error(err, BP_ERR_CONFIG, iteration, p, 0);
+    bool rank_start = head[j] != 0;
+    if (!rank_start && num_ranks > 1)
+      rank_start = rank_of(p, rank_bounds, num_ranks) != rank_of(pos[j - 1], rank_bounds, num_ranks);
+    occ_label[j] = (uint8_t)((lab & 0x7f) | (rank_start ? 0x80 : 0));
     if (head[j]) {
       const uint32_t s = segx[j];
       seg_start[s] = (uint32_t)j;
@@ -106,23 +122,23 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
   BP_CUDA_TRY(pool_alloc(&segx, n, s));
   BP_CUDA_TRY(pool_alloc(&first_flag, n, s));
   BP_CUDA_TRY(pool_alloc(&first_rank, n, s));
-  BP_CUDA_TRY(pool_alloc(&partials, scan_tiles(n) + 1, s));
+  BP_CUDA_TRY(pool_alloc(&partials, (long long)sort_partials_words(n) + scan_tiles(n) + 1, s));
   const int g = grid_for(n, 256);
   int which = 0;
   if (P->schema_mode) {
     k_prep_keys_schema<<<g, 256, 0, s>>>(d_keys, n, sc->d_table_base, sc->d_rows, sc->num_tables,
                                          (uint32_t*)ka, va, P->ctx ? P->ctx->d_err : nullptr, P->iteration);
-    BP_CUDA_TRY(radix_sort_pairs<K>(ka, va, kb, vb, n, nullptr, 0, sc->id_bits, hist, &which, s));
+    BP_CUDA_TRY(radix_sort_pairs<K>(ka, va, kb, vb, n, nullptr, 0, sc->id_bits, hist, partials, &which, s));
   } else {
     k_prep_keys_packed<<<g, 256, 0, s>>>(d_keys, n, (uint64_t*)ka, va);
     int w1 = 0, w2 = 0;
-    BP_CUDA_TRY(radix_sort_pairs<K>(ka, va, kb, vb, n, nullptr, 0, row_bits, hist, &w1, s));
+    BP_CUDA_TRY(radix_sort_pairs<K>(ka, va, kb, vb, n, nullptr, 0, row_bits, hist, partials, &w1, s));
     K* k1 = w1 ? kb : ka;
     uint32_t* v1 = w1 ? vb : va;
     K* k2 = w1 ? ka : kb;
     uint32_t* v2 = w1 ? va : vb;
     BP_CUDA_TRY(radix_sort_pairs<K>(k1, v1, k2, v2, n, nullptr, kKeyTableShift, kKeyTableShift + table_bits, hist,
-                                    &w2, s));
+                                    partials, &w2, s));
     which = w1 ^ w2;
   }
   const K* skey = which ? kb : ka;
@@ -134,7 +150,8 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
   BP_CUDA_TRY(cudaMemsetAsync(first_flag, 0, n * sizeof(uint32_t), s));
   k_prep_segments<K><<<g, 256, 0, s>>>(skey, P->d_occ_pos, head, segx, n, d_keys, d_labels, P->schema_mode,
                                        P->d_seg_start, P->d_uniq_key_s, P->d_uniq_id_s, first_flag,
-                                       P->d_occ_label, P->d_num_unique);
+                                       P->d_occ_label, P->d_num_unique, P->d_rank_bounds, P->num_ranks,
+                                       P->ctx ? P->ctx->d_err : nullptr, P->iteration);
   BP_CUDA_TRY(exclusive_scan(first_flag, first_rank, n, nullptr, partials, nullptr, nullptr, s));
   k_prep_perm<<<g, 256, 0, s>>>(P->d_occ_pos, head, segx, first_rank, n, P->d_uniq_key_s, P->d_perm_s2k,
                                 P->d_perm_k2s, P->d_uniq_key_k);
@@ -181,7 +198,7 @@ extern "C" int bp_prep_create(bp_ctx* ctx, const bp_schema* sc, const uint64_t* 
   BP_CUDA_TRY(pool_alloc(&P->d_perm_k2s, n, s));
   BP_CUDA_TRY(pool_alloc(&P->d_seg_start, n + 1, s));
   BP_CUDA_TRY(pool_alloc(&P->d_occ_pos, n, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_occ_label, n, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_occ_label, n + 16, s));  // read as 16-byte chunks
   P->d_occ_k = nullptr;
   if (flags & BP_PREP_OCC_INDEX) BP_CUDA_TRY(pool_alloc(&P->d_occ_k, n, s));
   BP_CUDA_TRY(pool_alloc(&P->d_rank_bounds, num_ranks + 1, s));

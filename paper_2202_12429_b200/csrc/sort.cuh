@@ -155,20 +155,6 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_upsweep(const K* __restr
   for (int d = threadIdx.x; d < radix; d += kSortThreads) hist[(long long)d * tiles + blockIdx.x] = cnt[d];
 }
 
-// Exclusive scan over the digit-major histogram [radix][tiles] (single CTA).
-static __global__ void k_radix_scan(uint32_t* hist, int len) {
-  __shared__ uint32_t sh[kScanThreads / 32];
-  uint32_t carry = 0;
-  for (int base = 0; base < len; base += kScanThreads) {
-    const int i = base + threadIdx.x;
-    const uint32_t v = i < len ? hist[i] : 0;
-    uint32_t tot;
-    const uint32_t inc = block_inclusive_scan_256(v, sh, &tot);
-    if (i < len) hist[i] = carry + inc - v;
-    carry += tot;
-  }
-}
-
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads) k_radix_downsweep(const K* __restrict__ keys_in,
                                                                   const uint32_t* __restrict__ vals_in,
@@ -230,11 +216,13 @@ inline size_t sort_hist_words(long long n) { return (size_t)kSortMaxRadix * (siz
 
 // Stable sort of (key, value) pairs on bits [begin_bit, end_bit).  Ping-pongs
 // between the a/b buffers; returns in *which the buffer holding the result
-// (0 = a, 1 = b).  ``hist`` must hold sort_hist_words(n_max) u32.
+// (0 = a, 1 = b).  ``hist`` must hold sort_hist_words(n_max) u32 and
+// ``partials`` scan_tiles(sort_hist_words(n_max)) + 1 u32.  The digit-major
+// histogram [radix][tiles] is scanned by the multi-CTA exclusive scan.
 template <typename K>
 cudaError_t radix_sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b, long long n_max,
-                             const long long* d_n, int begin_bit, int end_bit, uint32_t* hist, int* which,
-                             cudaStream_t s) {
+                             const long long* d_n, int begin_bit, int end_bit, uint32_t* hist, uint32_t* partials,
+                             int* which, cudaStream_t s) {
   *which = 0;
   if (n_max <= 0 || end_bit <= begin_bit) return cudaSuccess;
   const int tiles = sort_tiles(n_max);
@@ -244,8 +232,10 @@ cudaError_t radix_sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* v
   uint32_t* vout = vals_b;
   for (int shift = begin_bit; shift < end_bit; shift += kSortMaxBits) {
     const int bits = (end_bit - shift) < kSortMaxBits ? (end_bit - shift) : kSortMaxBits;
+    const long long len = (long long)(1 << bits) * tiles;
     k_radix_upsweep<K><<<tiles, kSortThreads, 0, s>>>(kin, n_max, d_n, shift, bits, hist, tiles);
-    k_radix_scan<<<1, kScanThreads, 0, s>>>(hist, (1 << bits) * tiles);
+    cudaError_t e = exclusive_scan(hist, hist, len, nullptr, partials, nullptr, nullptr, s);
+    if (e != cudaSuccess) return e;
     k_radix_downsweep<K><<<tiles, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_max, d_n, shift, bits, hist,
                                                          tiles);
     K* tk = kin;
@@ -258,6 +248,8 @@ cudaError_t radix_sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* v
   }
   return cudaGetLastError();
 }
+
+inline size_t sort_partials_words(long long n) { return (size_t)scan_tiles((long long)sort_hist_words(n)) + 1; }
 
 inline int bit_width_u64(unsigned long long x) {
   int b = 0;

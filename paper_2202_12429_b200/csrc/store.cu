@@ -62,16 +62,32 @@ __global__ void k_init_values(uint64_t seed, int dim, const uint64_t* __restrict
   }
 }
 
-// Row gather from the mapped host table: 16-byte lanes, one row per
-// (dim/4)-lane group, so each row is one contiguous PCIe read burst.
+// Row gather from the mapped host table: 16-byte lanes, (dim/4) lanes per row
+// so each row is one contiguous PCIe read; every thread issues kIlp
+// independent loads before its stores to keep enough host-link reads in
+// flight (random 64 B rows are latency-bound on PCIe).
+constexpr int kIlp = 4;
+
 __global__ void k_store_fetch_v4(const float4* __restrict__ table, const uint32_t* __restrict__ ids, long long n,
                                  const long long* d_n, int q, float4* __restrict__ out) {
   n = load_count(n, d_n);
   const long long total = n * q;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / q;
-    const int c = (int)(i - r * q);
-    out[i] = table[(long long)ids[r] * q + c];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += stride * kIlp) {
+    float4 v[kIlp];
+#pragma unroll
+    for (int r = 0; r < kIlp; ++r) {
+      const long long i = i0 + r * stride;
+      if (i < total) {
+        const long long row = i / q;
+        v[r] = table[(long long)ids[row] * q + (i - row * q)];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kIlp; ++r) {
+      const long long i = i0 + r * stride;
+      if (i < total) out[i] = v[r];
+    }
   }
 }
 
@@ -86,7 +102,8 @@ __global__ void k_store_fetch_scalar(const float* __restrict__ table, const uint
 }
 
 // Scatter rows into the host table; ``mask`` (optional) skips clean rows, the
-// write-back of only dirty evictions (reference engine.py:403-413).
+// write-back of only dirty evictions (reference engine.py:403-413).  Reads of
+// the (device) source rows are batched kIlp deep before the posted PCIe writes.
 __global__ void k_store_write(float* __restrict__ table, uint32_t* __restrict__ written,
                               const uint32_t* __restrict__ ids, const float* __restrict__ rows,
                               const uint8_t* __restrict__ mask, long long n, const long long* d_n, int dim) {
@@ -94,17 +111,31 @@ __global__ void k_store_write(float* __restrict__ table, uint32_t* __restrict__ 
   const bool v4 = (dim & 3) == 0;
   const int q = v4 ? dim >> 2 : dim;
   const long long total = n * q;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / q;
-    const int c = (int)(i - r * q);
-    if (mask && !mask[r]) continue;
-    const long long g = ids[r];
-    if (v4) {
-      reinterpret_cast<float4*>(table)[g * q + c] = reinterpret_cast<const float4*>(rows)[r * q + c];
-    } else {
-      table[g * dim + c] = rows[r * dim + c];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += stride * kIlp) {
+    float4 v[kIlp];
+    long long dst[kIlp];
+#pragma unroll
+    for (int r = 0; r < kIlp; ++r) {
+      const long long i = i0 + r * stride;
+      dst[r] = -1;
+      if (i < total) {
+        const long long row = i / q;
+        const int c = (int)(i - row * q);
+        if (mask && !mask[row]) continue;
+        const long long g = ids[row];
+        dst[r] = g * q + c;
+        if (v4) v[r] = reinterpret_cast<const float4*>(rows)[i];
+        else v[r].x = rows[i];
+        if (c == 0) atomicOr(&written[g >> 5], 1u << (g & 31));
+      }
     }
-    if (c == 0) atomicOr(&written[g >> 5], 1u << (g & 31));
+#pragma unroll
+    for (int r = 0; r < kIlp; ++r) {
+      if (dst[r] < 0) continue;
+      if (v4) reinterpret_cast<float4*>(table)[dst[r]] = v[r];
+      else table[dst[r]] = v[r].x;
+    }
   }
 }
 

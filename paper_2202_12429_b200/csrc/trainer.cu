@@ -16,10 +16,16 @@
 
 namespace bp {
 
+// One group of G lanes per unique key; lane = embedding component (DPL
+// components per lane when dim > 32).  The key's occurrence bytes (label |
+// rank-start flag, see prep.cu) are streamed as aligned 16-byte chunks: each
+// lane loads one chunk per round, two rounds are kept in flight (the Zipf-hot
+// keys of tiny tables have ~9K occurrences per batch, so the chain must not
+// wait on memory), and chunks are broadcast to the group by shuffles.  The
+// dependent chain per lane is one float add per occurrence.
 template <int G, int DPL>
 __global__ void __launch_bounds__(256) k_stub_step(
-    const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ occ_pos,
-    const uint8_t* __restrict__ occ_label, const long long* __restrict__ rank_bounds, int num_ranks,
+    const uint32_t* __restrict__ seg_start, const uint8_t* __restrict__ occ_label,
     const long long* __restrict__ d_U, float* __restrict__ rows, const int32_t* __restrict__ row_index,
     uint8_t* __restrict__ dirty, int dim, float c_value, float c_label, float lr, int mode,
     float* __restrict__ grad_out, const uint32_t* __restrict__ my_ids, const uint32_t* __restrict__ next_ids,
@@ -27,11 +33,14 @@ __global__ void __launch_bounds__(256) k_stub_step(
   const long long U = *d_U;
   const unsigned lane = threadIdx.x & 31u;
   const int lane_g = (int)(lane & (G - 1));
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(unsigned)(G - 1)));
+  const unsigned gbase = lane & ~(unsigned)(G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const long long groups_per_block = blockDim.x / G;
   const long long groups_total = (long long)gridDim.x * groups_per_block;
   const long long warp_first = (long long)blockIdx.x * groups_per_block + (threadIdx.x >> 5) * (32 / G);
   const long long n_next = next_ids ? load_count(n_next_max, d_n_next) : 0;
+  const uint4* __restrict__ chunks = reinterpret_cast<const uint4*>(occ_label);
+  const float b0 = __fmul_rn(c_label, -0.5f), b1 = __fmul_rn(c_label, 0.5f);
 
   for (long long base = warp_first; base < U; base += groups_total) {
     const long long s = base + (long long)(lane / G);
@@ -43,49 +52,61 @@ __global__ void __launch_bounds__(256) k_stub_step(
     }
     bool nonzero = false;
     if (active) {
-      uint32_t j = seg_start[s];
-      const uint32_t b = seg_start[s + 1];
-      float v[DPL], sc[DPL], comb[DPL];
+      const uint32_t a = seg_start[s], b = seg_start[s + 1];
+      float v[DPL], t0[DPL], t1[DPL], sc[DPL], acc[DPL], comb[DPL];
 #pragma unroll
       for (int q = 0; q < DPL; ++q) {
         const int d = lane_g + q * G;
         v[q] = d < dim ? rows[(long long)row * dim + d] : 0.f;
         sc[q] = __fmul_rn(c_value, v[q]);
+        t0[q] = __fadd_rn(sc[q], b0);  // occurrence gradient for label 0
+        t1[q] = __fadd_rn(sc[q], b1);  // ... and label 1
+        acc[q] = 0.f;
         comb[q] = 0.f;
       }
-      for (int r = 0; r < num_ranks && j < b; ++r) {
-        const long long hi = rank_bounds[r + 1];
-        uint32_t lo = j, up = b;  // first index in [j, b) whose position is >= hi
-        while (lo < up) {
-          const uint32_t mid = (lo + up) >> 1;
-          if ((long long)occ_pos[mid] < hi) lo = mid + 1;
-          else up = mid;
-        }
-        if (lo == j) continue;  // key absent from this rank: rank not in the combine
-        float acc[DPL];
+      const uint32_t c_first = a >> 4;
+      const uint32_t n_chunks = ((b - 1) >> 4) - c_first + 1;
+      const uint4 zero4 = make_uint4(0, 0, 0, 0);
+      uint4 w0 = lane_g < (int)n_chunks ? chunks[c_first + lane_g] : zero4;
+      uint4 w1 = lane_g + G < (int)n_chunks ? chunks[c_first + G + lane_g] : zero4;
+      for (uint32_t r0 = 0; r0 < n_chunks; r0 += G) {
+        const uint32_t nxt = r0 + 2 * G + lane_g;
+        const uint4 w2 = nxt < n_chunks ? chunks[c_first + nxt] : zero4;
+        const uint32_t in_round = min((uint32_t)G, n_chunks - r0);
+        for (uint32_t i = 0; i < in_round; ++i) {
+          uint32_t word[4];
+          word[0] = __shfl_sync(gmask, w0.x, (int)i, G);
+          word[1] = __shfl_sync(gmask, w0.y, (int)i, G);
+          word[2] = __shfl_sync(gmask, w0.z, (int)i, G);
+          word[3] = __shfl_sync(gmask, w0.w, (int)i, G);
+          const uint32_t cbase = (c_first + r0 + i) << 4;
+          const uint32_t lo = a > cbase ? a - cbase : 0u;
+          const uint32_t hi = b - cbase < 16u ? b - cbase : 16u;
+          for (uint32_t q8 = lo; q8 < hi; ++q8) {
+            const uint32_t byte = (word[q8 >> 2] >> ((q8 & 3) * 8)) & 0xFFu;
+            const uint32_t lab = byte & 0x7Fu;
+            if ((byte & 0x80u) && cbase + q8 != a) {  // a new trainer rank starts: close the partial
 #pragma unroll
-        for (int q = 0; q < DPL; ++q) acc[q] = 0.f;
-        constexpr int kU = 8;
-        for (; j + kU <= lo; j += kU) {
-          float bias[kU];
+              for (int q = 0; q < DPL; ++q) {
+                comb[q] = __fadd_rn(comb[q], acc[q]);
+                acc[q] = 0.f;
+              }
+            }
 #pragma unroll
-          for (int u = 0; u < kU; ++u) bias[u] = __fmul_rn(c_label, __fsub_rn((float)occ_label[j + u], 0.5f));
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-#pragma unroll
-            for (int q = 0; q < DPL; ++q) acc[q] = __fadd_rn(acc[q], __fadd_rn(sc[q], bias[u]));
+            for (int q = 0; q < DPL; ++q) {
+              const float t = lab == 0 ? t0[q]
+                            : lab == 1 ? t1[q]
+                                       : __fadd_rn(sc[q], __fmul_rn(c_label, __fsub_rn((float)lab, 0.5f)));
+              acc[q] = __fadd_rn(acc[q], t);
+            }
           }
         }
-        for (; j < lo; ++j) {
-          const float bias = __fmul_rn(c_label, __fsub_rn((float)occ_label[j], 0.5f));
-#pragma unroll
-          for (int q = 0; q < DPL; ++q) acc[q] = __fadd_rn(acc[q], __fadd_rn(sc[q], bias));
-        }
-#pragma unroll
-        for (int q = 0; q < DPL; ++q) comb[q] = __fadd_rn(comb[q], acc[q]);
+        w0 = w1;
+        w1 = w2;
       }
 #pragma unroll
       for (int q = 0; q < DPL; ++q) {
+        comb[q] = __fadd_rn(comb[q], acc[q]);
         const int d = lane_g + q * G;
         if (d < dim) {
           nonzero |= comb[q] != 0.f;
@@ -205,8 +226,8 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   const int blocks = grid_for(groups * G, threads, kNumSMs * 8);
   BP_DISPATCH_GD(G, dpl,
                  (k_stub_step<g_, d_><<<blocks, threads, 0, s>>>(
-                     P->d_seg_start, P->d_occ_pos, P->d_occ_label, P->d_rank_bounds, P->num_ranks,
-                     P->d_num_unique, d_rows, d_row_index, d_dirty, dim, c_value, c_label, lr, mode, d_grad_out,
+                     P->d_seg_start, P->d_occ_label, P->d_num_unique, d_rows, d_row_index, d_dirty, dim, c_value,
+                     c_label, lr, mode, d_grad_out,
                      P->d_uniq_id_s, d_next_ids, (const long long*)d_n_next, n_next_max,
                      (unsigned long long*)d_stats)));
   BP_LAUNCH_CHECK();

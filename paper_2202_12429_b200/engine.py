@@ -199,6 +199,11 @@ class _Pipeline:
         self.n = len(batches)
         self.T = cfg.num_trainers
         self.stream = torch.cuda.current_stream()
+        # Host-link traffic (prefetch gathers, write-back scatters) runs on its
+        # own stream so it overlaps the compute of the current iteration; the
+        # gate order of reference engine.py:302-377 is kept by issuing both in
+        # dispatch order on that one stream, fenced by events.
+        self.link = torch.cuda.Stream()
         self.device_inputs = device_inputs  # optional {pos: (d_keys, d_labels)} already in HBM
         self._preps: dict = {}
         stub = cfg.stub()
@@ -312,10 +317,15 @@ class _Pipeline:
             self.forced_flushes += 1
         arrival = self._gate_time(theta) + self.cfg.fetch_latency
         dev = plan.device
-        self._probe("store_fetch", 0)
-        rows = self.store.fetch_ids_async(dev.prefetch_ids, dev.cap, d_n=dev.counts[0:1], stream=self.stream)
-        self._probe("store_fetch", 1)
-        self.staged[plan.iteration - self.base] = (plan, rows, arrival)
+        self.link.wait_event(dev.h_pending.done)  # the plan's pop has run
+        self._probe("store_fetch", 0, self.link)
+        rows = self.store.fetch_ids_async(dev.prefetch_ids, dev.cap, d_n=dev.counts[0:1], stream=self.link)
+        self._probe("store_fetch", 1, self.link)
+        for t in (rows, dev.prefetch_ids, dev.counts):
+            t.record_stream(self.link)
+        fetched = torch.cuda.Event()
+        fetched.record(self.link)
+        self.staged[plan.iteration - self.base] = (plan, rows, arrival, fetched)
 
     def _dispatch_until(self, cur: int) -> None:
         while True:
@@ -333,19 +343,23 @@ class _Pipeline:
             self.pending.popleft()
             self._dispatch(plan, cur)
 
-    def _probe(self, name: str, phase: int) -> None:
+    def _probe(self, name: str, phase: int, stream=None) -> None:
         if self.probe is not None:
-            self.probe(name, phase, self.stream)
+            self.probe(name, phase, stream or self.stream)
 
     # -- write-back (reference engine.py:350-377) ---------------------------------
     def _flush(self, kind: str, pos: int) -> None:
         flusher = self.flush_counter % self.T
         count = 0
         if self.chunks:
-            self._probe("store_write", 0)
+            # Chunks were produced on the compute stream, which the host has
+            # synchronised since; the scatter runs on the link stream.
+            self._probe("store_write", 0, self.link)
             for ch in self.chunks:  # in eviction order: the last write wins
-                self.store.write_ids_async(ch.ids, ch.rows, ch.n, d_mask=ch.dirty, stream=self.stream)
-            self._probe("store_write", 1)
+                self.store.write_ids_async(ch.ids, ch.rows, ch.n, d_mask=ch.dirty, stream=self.link)
+                for t in (ch.ids, ch.rows, ch.dirty):
+                    t.record_stream(self.link)
+            self._probe("store_write", 1, self.link)
             count = self._merged_count()
             self.store.write_calls += 1
             self.store.entries_written += count
@@ -407,11 +421,12 @@ class _Pipeline:
         staged = self.staged.pop(pos, None)
         if staged is None:
             raise EngineError(f"no staged prefetch for position {pos}")
-        plan, rows, arrival = staged
+        plan, rows, arrival, fetched = staged
         if plan.iteration != iteration:
             raise EngineError(f"plan {plan.iteration} misaligned with batch {iteration}")
         dev = plan.device
         prep = self._prep(pos)
+        self.stream.wait_event(fetched)
         off, skip_key, has_skip = 0, 0, 0
         if self.fault == FAULT_DROP_PREFETCH and not self.drop_done and pos >= self.n // 2 and dev.n_prefetch:
             # Drop the first (smallest) prefetched key: it is neither inserted

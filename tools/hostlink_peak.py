@@ -1,0 +1,58 @@
+"""Host-link (PCIe) peaks on the GPU box: pinned memcpy H2D/D2H and the
+zero-copy row gather/scatter kernels of the store at 64 B rows.
+
+  python tools/hostlink_peak.py   -> one JSON line
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2202_12429_b200.store import ShardedStore  # noqa: E402
+
+
+def timed(fn, reps=20):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / reps * 1e-3
+
+
+def main():
+    out = {}
+    nbytes = 256 << 20
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    out["memcpy_h2d_gbs"] = nbytes / timed(lambda: d.copy_(h, non_blocking=True)) / 1e9
+    out["memcpy_d2h_gbs"] = nbytes / timed(lambda: h.copy_(d, non_blocking=True)) / 1e9
+    sc = bench.schema()
+    store = ShardedStore(sc, 1, 11)
+    rng = np.random.default_rng(0)
+    for n in (35_000, 1_000_000):
+        for kind in ("random", "sequential"):
+            ids = rng.integers(0, sc.total_rows, n) if kind == "random" else np.arange(n)
+            ids = np.sort(ids).astype(np.uint32)
+            d_ids = torch.from_numpy(ids).cuda()
+            rows = torch.empty((n, sc.emb_dim), dtype=torch.float32, device="cuda")
+            t = timed(lambda: store.fetch_ids_async(d_ids, n))
+            out[f"zero_copy_gather_{kind}_{n}_gbs"] = n * 64 / t / 1e9
+            t = timed(lambda: store.write_ids_async(d_ids, rows, n))
+            out[f"zero_copy_scatter_{kind}_{n}_gbs"] = n * 64 / t / 1e9
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
