@@ -274,14 +274,18 @@ int bp_schema_ids(bp_ctx* ctx, const bp_schema* schema, const uint64_t* d_keys, 
  * (v - lr*combined) and sets dirty where combined != 0; mode BP_STUB_GRAD
  * writes combined to d_grad_out[s] instead.
  * d_rows: row arena; d_row_index: row of sorted unique s (NULL = s itself).
- * d_next_ids/n_next: optional (sorted) dense ids of the next batch: counts
- * critical keys (reference engine.py:560-569) into d_stats[0]. */
+ * d_next_mark/next_tag: optional dense per-id array in which bp_mark_ids
+ * stamped the next batch's ids with next_tag: keys found there are counted
+ * as critical (reference engine.py:560-569) into d_stats[0]; keys whose
+ * combined gradient is non-zero are counted into d_stats[1].  Labels must
+ * be < 128 (bit 7 of the prep's label bytes flags trainer-rank starts). */
 #define BP_STUB_SGD 0
 #define BP_STUB_GRAD 1
 int bp_stub_step(bp_ctx* ctx, bp_prep* prep, float* d_rows, const int32_t* d_row_index, uint8_t* d_dirty,
                  int32_t dim, float c_value, float c_label, float lr, int32_t mode, float* d_grad_out,
-                 const uint32_t* d_next_ids, const int64_t* d_n_next, int64_t n_next_max, int64_t* d_stats,
-                 bp_stream_t stream);
+                 const int64_t* d_next_mark, int64_t next_tag, int64_t* d_stats, bp_stream_t stream);
+/* mark[id] = tag for every unique key of a schema-mode prep. */
+int bp_mark_ids(bp_prep* prep, int64_t* d_mark, int64_t tag, bp_stream_t stream);
 /* np.add.at(out, idx, vals) row-wise in input order, over a registry-mode
  * prep built from keys = idx (combine_core, reference trainer.py:92-105).
  * d_out rows absent from idx are left untouched. */

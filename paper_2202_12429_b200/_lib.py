@@ -117,8 +117,9 @@ _SIGS = {
     "bp_store_write": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bp_store_write_masked": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bp_init_values": (c_i32, [c_u64, c_i32, c_vp, c_i64, c_vp, c_vp]),
-    "bp_stub_step": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_f32, c_f32, c_f32, c_i32, c_vp, c_vp, c_vp,
-                             c_i64, c_vp, c_vp]),
+    "bp_stub_step": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_f32, c_f32, c_f32, c_i32, c_vp, c_vp, c_i64,
+                             c_vp, c_vp]),
+    "bp_mark_ids": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "bp_add_at_rows": (c_i32, [c_vp, c_vp, c_i32, c_vp, c_vp]),
     "bp_sgd": (c_i32, [c_vp, c_vp, c_f32, c_i64, c_vp, c_vp]),
     "bp_sort_keys_u64": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp]),

@@ -28,8 +28,8 @@ __global__ void __launch_bounds__(256) k_stub_step(
     const uint32_t* __restrict__ seg_start, const uint8_t* __restrict__ occ_label,
     const long long* __restrict__ d_U, float* __restrict__ rows, const int32_t* __restrict__ row_index,
     uint8_t* __restrict__ dirty, int dim, float c_value, float c_label, float lr, int mode,
-    float* __restrict__ grad_out, const uint32_t* __restrict__ my_ids, const uint32_t* __restrict__ next_ids,
-    const long long* __restrict__ d_n_next, long long n_next_max, unsigned long long* __restrict__ stats) {
+    float* __restrict__ grad_out, const uint32_t* __restrict__ my_ids, const int64_t* __restrict__ next_mark,
+    long long next_tag, unsigned long long* __restrict__ stats) {
   const long long U = *d_U;
   const unsigned lane = threadIdx.x & 31u;
   const int lane_g = (int)(lane & (G - 1));
@@ -38,7 +38,6 @@ __global__ void __launch_bounds__(256) k_stub_step(
   const long long groups_per_block = blockDim.x / G;
   const long long groups_total = (long long)gridDim.x * groups_per_block;
   const long long warp_first = (long long)blockIdx.x * groups_per_block + (threadIdx.x >> 5) * (32 / G);
-  const long long n_next = next_ids ? load_count(n_next_max, d_n_next) : 0;
   const uint4* __restrict__ chunks = reinterpret_cast<const uint4*>(occ_label);
   const float b0 = __fmul_rn(c_label, -0.5f), b1 = __fmul_rn(c_label, 0.5f);
 
@@ -82,22 +81,41 @@ __global__ void __launch_bounds__(256) k_stub_step(
           const uint32_t cbase = (c_first + r0 + i) << 4;
           const uint32_t lo = a > cbase ? a - cbase : 0u;
           const uint32_t hi = b - cbase < 16u ? b - cbase : 16u;
-          for (uint32_t q8 = lo; q8 < hi; ++q8) {
-            const uint32_t byte = (word[q8 >> 2] >> ((q8 & 3) * 8)) & 0xFFu;
-            const uint32_t lab = byte & 0x7Fu;
-            if ((byte & 0x80u) && cbase + q8 != a) {  // a new trainer rank starts: close the partial
+          const bool full = lo == 0 && hi == 16;
+          const uint32_t big = (word[0] | word[1] | word[2] | word[3]) & 0x7E7E7E7Eu;
+          const uint32_t flags_hi = (word[1] | word[2] | word[3]) & 0x80808080u;
+          const uint32_t flags_lo = word[0] & 0x80808080u;
+          if (full && !big && !flags_hi && (flags_lo == 0 || (cbase == a && flags_lo == 0x80u))) {
+            // Fast path: 16 occurrences, labels 0/1, no rank change inside
+            // the chunk (a rank-start flag on the key's first byte is the
+            // start of the chain itself): one select + one add each.
 #pragma unroll
-              for (int q = 0; q < DPL; ++q) {
-                comb[q] = __fadd_rn(comb[q], acc[q]);
-                acc[q] = 0.f;
+            for (int wi = 0; wi < 4; ++wi) {
+#pragma unroll
+              for (int bi = 0; bi < 4; ++bi) {
+                const bool one = (word[wi] >> (bi * 8)) & 1u;
+#pragma unroll
+                for (int q = 0; q < DPL; ++q) acc[q] = __fadd_rn(acc[q], one ? t1[q] : t0[q]);
               }
             }
+          } else {
+            for (uint32_t q8 = lo; q8 < hi; ++q8) {
+              const uint32_t byte = (word[q8 >> 2] >> ((q8 & 3) * 8)) & 0xFFu;
+              const uint32_t lab = byte & 0x7Fu;
+              if ((byte & 0x80u) && cbase + q8 != a) {  // a new trainer rank starts: close the partial
 #pragma unroll
-            for (int q = 0; q < DPL; ++q) {
-              const float t = lab == 0 ? t0[q]
-                            : lab == 1 ? t1[q]
-                                       : __fadd_rn(sc[q], __fmul_rn(c_label, __fsub_rn((float)lab, 0.5f)));
-              acc[q] = __fadd_rn(acc[q], t);
+                for (int q = 0; q < DPL; ++q) {
+                  comb[q] = __fadd_rn(comb[q], acc[q]);
+                  acc[q] = 0.f;
+                }
+              }
+#pragma unroll
+              for (int q = 0; q < DPL; ++q) {
+                const float t = lab == 0 ? t0[q]
+                              : lab == 1 ? t1[q]
+                                         : __fadd_rn(sc[q], __fmul_rn(c_label, __fsub_rn((float)lab, 0.5f)));
+                acc[q] = __fadd_rn(acc[q], t);
+              }
             }
           }
         }
@@ -119,16 +137,9 @@ __global__ void __launch_bounds__(256) k_stub_step(
     bool crit = false;
     if (active && lane_g == 0) {
       if (nz && dirty && mode == BP_STUB_SGD) dirty[row] = 1;
-      if (n_next > 0) {
-        const uint32_t id = my_ids[s];
-        long long lo = 0, up = n_next;
-        while (lo < up) {
-          const long long mid = (lo + up) >> 1;
-          if (next_ids[mid] < id) lo = mid + 1;
-          else up = mid;
-        }
-        crit = lo < n_next && next_ids[lo] == id;
-      }
+      // critical = needed by the next batch (reference engine.py:560-564):
+      // the next batch's ids carry its iteration tag in a dense mark array.
+      if (next_mark) crit = next_mark[my_ids[s]] == next_tag;
     }
     if (stats) {
       const unsigned cm = __ballot_sync(0xffffffffu, crit);
@@ -187,6 +198,13 @@ __global__ void k_key_rows(const uint64_t* __restrict__ keys, const long long* d
     out[i] = (int32_t)row_of(keys[i]);
 }
 
+__global__ void k_mark_ids(const uint32_t* __restrict__ ids, const long long* __restrict__ d_U, int64_t* mark,
+                           long long tag) {
+  const long long U = *d_U;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < U; i += (long long)gridDim.x * blockDim.x)
+    mark[ids[i]] = tag;
+}
+
 static inline void group_shape(int dim, int* G, int* dpl) {
   int g = 1;
   while (g < dim && g < 32) g <<= 1;
@@ -210,10 +228,18 @@ static inline void group_shape(int dim, int* G, int* dpl) {
     default: return BP_ERR_INVALID;                       \
   }
 
+extern "C" int bp_mark_ids(bp_prep* P, int64_t* d_mark, int64_t tag, bp_stream_t stream) {
+  using namespace bp;
+  if (P->n_occ == 0 || !P->schema_mode) return P->schema_mode ? BP_OK : BP_ERR_INVALID;
+  k_mark_ids<<<grid_for(P->n_occ, 256), 256, 0, (cudaStream_t)stream>>>(P->d_uniq_id_s, P->d_num_unique, d_mark,
+                                                                         tag);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
 extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_t* d_row_index, uint8_t* d_dirty,
                             int32_t dim, float c_value, float c_label, float lr, int32_t mode, float* d_grad_out,
-                            const uint32_t* d_next_ids, const int64_t* d_n_next, int64_t n_next_max, int64_t* d_stats,
-                            bp_stream_t stream) {
+                            const int64_t* d_next_mark, int64_t next_tag, int64_t* d_stats, bp_stream_t stream) {
   using namespace bp;
   (void)ctx;
   if (dim < 1 || dim > 128) return BP_ERR_INVALID;
@@ -227,8 +253,7 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   BP_DISPATCH_GD(G, dpl,
                  (k_stub_step<g_, d_><<<blocks, threads, 0, s>>>(
                      P->d_seg_start, P->d_occ_label, P->d_num_unique, d_rows, d_row_index, d_dirty, dim, c_value,
-                     c_label, lr, mode, d_grad_out,
-                     P->d_uniq_id_s, d_next_ids, (const long long*)d_n_next, n_next_max,
+                     c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark, next_tag,
                      (unsigned long long*)d_stats)));
   BP_LAUNCH_CHECK();
   return BP_OK;

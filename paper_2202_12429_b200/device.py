@@ -48,6 +48,44 @@ class DeviceSchema:
             pass
 
 
+class Uploader:
+    """Host -> HBM batch uploads through a ring of reusable pinned buffers.
+
+    ``tensor.pin_memory()`` per batch costs a pinned allocation each time; the
+    ring copies the numpy batch into a pre-pinned slot (waiting only for that
+    slot's previous DMA) and issues one asynchronous H2D copy.
+    """
+
+    def __init__(self, slot_bytes: int, slots: int = 4):
+        self.slot_bytes = slot_bytes
+        self.bufs = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(slots)]
+        self.views = [b.numpy() for b in self.bufs]
+        self.events = [None] * slots
+        self.i = 0
+
+    def upload(self, arr: np.ndarray, stream) -> torch.Tensor:
+        arr = np.ascontiguousarray(arr)
+        nbytes = arr.nbytes
+        if nbytes > self.slot_bytes:
+            return L.to_device(arr, stream)
+        k = self.i
+        self.i = (self.i + 1) % len(self.bufs)
+        if self.events[k] is not None:
+            self.events[k].synchronize()
+        view = self.views[k][:nbytes]
+        view[:] = arr.view(np.uint8).reshape(-1)
+        out = torch.empty(arr.shape, dtype=_TORCH_OF[arr.dtype.str], device="cuda")
+        with torch.cuda.stream(stream):
+            out.view(torch.uint8).reshape(-1).copy_(self.bufs[k][:nbytes], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self.events[k] = ev
+        return out
+
+
+_TORCH_OF = {"<u8": torch.uint64, "|u1": torch.uint8, "<i8": torch.int64, "<u4": torch.uint32, "<f4": torch.float32}
+
+
 def _bits(x: int) -> int:
     return max(1, int(x).bit_length())
 
@@ -58,16 +96,16 @@ class DevicePrep:
 
     def __init__(self, keys: np.ndarray, labels: np.ndarray, rank_bounds: np.ndarray, iteration: int,
                  schema: Schema | None = None, occ_index: bool = False, stream=None,
-                 d_keys: torch.Tensor | None = None, d_labels: torch.Tensor | None = None):
+                 d_keys: torch.Tensor | None = None, d_labels: torch.Tensor | None = None, uploader=None):
         lib = L.lib()
         self.stream = stream or torch.cuda.current_stream()
         self.n_occ = int(len(keys)) if d_keys is None else int(d_keys.numel())
         self.iteration = int(iteration)
         self.num_ranks = len(rank_bounds) - 1
         self.schema = schema
-        self.d_keys = d_keys if d_keys is not None else L.to_device(np.asarray(keys, dtype=np.uint64), self.stream)
-        self.d_labels = d_labels if d_labels is not None else L.to_device(np.asarray(labels, dtype=np.uint8),
-                                                                          self.stream)
+        up = uploader.upload if uploader is not None else L.to_device
+        self.d_keys = d_keys if d_keys is not None else up(np.asarray(keys, dtype=np.uint64), self.stream)
+        self.d_labels = d_labels if d_labels is not None else up(np.asarray(labels, dtype=np.uint8), self.stream)
         rb = np.ascontiguousarray(rank_bounds, dtype=np.int64)
         row_bits = table_bits = 1
         if schema is None and self.n_occ:
@@ -88,9 +126,10 @@ class DevicePrep:
 
     @classmethod
     def from_batch(cls, batch: Batch, num_ranks: int = 1, schema: Schema | None = None, occ_index: bool = False,
-                   stream=None) -> "DevicePrep":
+                   stream=None, uploader=None) -> "DevicePrep":
         keys, labels, _ = batch.packed_occurrences()
-        return cls(keys, labels, batch.rank_bounds(num_ranks), batch.iteration, schema, occ_index, stream)
+        return cls(keys, labels, batch.rank_bounds(num_ranks), batch.iteration, schema, occ_index, stream,
+                   uploader=uploader)
 
     @property
     def num_unique(self) -> int:

@@ -39,7 +39,7 @@ import torch
 
 from . import _lib as L
 from .cache import DynamicCache
-from .device import DevicePrep
+from .device import DevicePrep, Uploader
 from .errors import CacheCapacityError, ConfigurationError, EngineError, IncomparableRunsError
 from .lookahead import CachePlan, DevicePlan, adapt_on_pressure, auto_lookahead, new_state
 from .report import IterationRecord, RunReport
@@ -206,6 +206,7 @@ class _Pipeline:
         self.link = torch.cuda.Stream()
         self.device_inputs = device_inputs  # optional {pos: (d_keys, d_labels)} already in HBM
         self._preps: dict = {}
+        self._uploader = None
         stub = cfg.stub()
         self.c_value, self.c_label, self.lr = f32(stub.c_value), f32(stub.c_label), f32(stub.lr)
         self.probe = None  # optional callable(name, phase) for kernel timing
@@ -243,6 +244,8 @@ class _Pipeline:
         self.peak_occupancy = 0
         self.drop_done = False
         self.stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+        # dense per-row stamp of the next batch's keys (critical-set test)
+        self.mark = torch.full((schema.total_rows,), -(1 << 62), dtype=torch.int64, device="cuda")
         self.h_step = torch.zeros(8, dtype=torch.int64, pin_memory=True)
         self.kernel_launches = 0
 
@@ -258,7 +261,10 @@ class _Pipeline:
                 prep = DevicePrep(None, None, batch.rank_bounds(self.T), batch.iteration, self.schema,
                                   stream=self.stream, d_keys=keys, d_labels=labels)
             else:
-                prep = DevicePrep.from_batch(batch, self.T, self.schema, stream=self.stream)
+                if self._uploader is None:
+                    occ = batch.packed_occurrences()[0].size
+                    self._uploader = Uploader(max(1 << 20, 16 * occ), slots=8)
+                prep = DevicePrep.from_batch(batch, self.T, self.schema, stream=self.stream, uploader=self._uploader)
             self._preps[pos] = prep
         return prep
 
@@ -450,13 +456,14 @@ class _Pipeline:
                                            L.ptr(slots), sp), "bp_cache_apply_resolve")
         self._probe("cache_insert", 1)
         nxt = self._prep(pos + 1) if pos + 1 < self.n else None
+        if nxt is not None:
+            L.check(lib.bp_mark_ids(nxt.handle, L.ptr(self.mark), nxt.iteration, sp), "bp_mark_ids")
         self.stats.zero_()
         self._probe("stub_step", 0)
         L.check(lib.bp_stub_step(ctx.handle, prep.handle, L.ptr(self.cache.values), L.ptr(slots),
                                  L.ptr(self.cache.dirty), dim, self.c_value, self.c_label, self.lr, BP_STUB_SGD, None,
-                                 nxt.view.d_uniq_id_s if nxt is not None else None,
-                                 nxt.view.d_num_unique if nxt is not None else None,
-                                 nxt.n_occ if nxt is not None else 0, L.ptr(self.stats), sp), "bp_stub_step")
+                                 L.ptr(self.mark) if nxt is not None else None,
+                                 nxt.iteration if nxt is not None else 0, L.ptr(self.stats), sp), "bp_stub_step")
         self._probe("stub_step", 1)
         self._probe("cache_evict", 0)
         ch = self._evict(iteration, False, min(cfg.cache_capacity, max(prep.n_occ, 1)))
@@ -618,7 +625,7 @@ def run_synchronous_baseline(cfg: EngineConfig, schema: Schema, trace: Iterable[
             rows = store.fetch_ids_async(ids, u, stream=stream)
             store.fetch_calls += 1
             L.check(lib.bp_stub_step(ctx.handle, prep.handle, L.ptr(rows), None, None, schema.emb_dim, c_value,
-                                     c_label, lr, BP_STUB_SGD, None, None, None, 0, None, sp), "bp_stub_step")
+                                     c_label, lr, BP_STUB_SGD, None, 0, None, sp), "bp_stub_step")
             store.write_ids_async(ids, rows, u, stream=stream)
             store.write_calls += 1
             store.entries_written += u

@@ -69,7 +69,7 @@ def gradient_core(occ_unique_idx, occ_labels, unique_values, cfg: StubModelConfi
     grad = torch.empty((nu, dim), dtype=torch.float32, device="cuda")
     L.check(L.lib().bp_stub_step(L.Context.get().handle, prep.handle, L.ptr(d_rows), L.ptr(row_index), None, dim,
                                  f32(cfg.c_value), f32(cfg.c_label), f32(cfg.lr), BP_STUB_GRAD, L.ptr(grad),
-                                 None, None, 0, None, L.stream_ptr()), "bp_stub_step")
+                                 None, 0, None, L.stream_ptr()), "bp_stub_step")
     rows = row_index.cpu().numpy()
     out[rows] = grad.cpu().numpy()
     return out

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--nvtx", action="store_true")
     ap.add_argument("--torch-prof", action="store_true")
     ap.add_argument("--host-inputs", action="store_true")
+    ap.add_argument("--cprofile", action="store_true")
     args = ap.parse_args()
     sc = bench.schema()
     n = args.warmup + args.steps + 12
@@ -55,6 +56,18 @@ def main():
             torch.cuda.synchronize()
         print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=40))
         print(prof.key_averages().table(sort_by="cpu_time_total", row_limit=25))
+        return
+    if args.cprofile:
+        import cProfile
+        import pstats
+
+        pr = cProfile.Profile()
+        pr.enable()
+        for i in range(args.steps):
+            pipe.step(args.warmup + i)
+        torch.cuda.synchronize()
+        pr.disable()
+        pstats.Stats(pr).sort_stats("tottime").print_stats(30)
         return
     t0 = time.perf_counter()
     for i in range(args.steps):
