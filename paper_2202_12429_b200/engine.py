@@ -625,7 +625,7 @@ def run_synchronous_baseline(cfg: EngineConfig, schema: Schema, trace: Iterable[
             rows = store.fetch_ids_async(ids, u, stream=stream)
             store.fetch_calls += 1
             L.check(lib.bp_stub_step(ctx.handle, prep.handle, L.ptr(rows), None, None, schema.emb_dim, c_value,
-                                     c_label, lr, BP_STUB_SGD, None, 0, None, sp), "bp_stub_step")
+                                     c_label, lr, BP_STUB_SGD, None, None, 0, None, sp), "bp_stub_step")
             store.write_ids_async(ids, rows, u, stream=stream)
             store.write_calls += 1
             store.entries_written += u
