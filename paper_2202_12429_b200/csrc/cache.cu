@@ -339,7 +339,7 @@ extern "C" int bp_cache_create(bp_ctx* ctx, const bp_schema* sc, int64_t capacit
   BP_CUDA_TRY(cudaMalloc(&c->d_free, C * sizeof(uint32_t)));
   BP_CUDA_TRY(cudaMalloc(&c->d_flag, C * sizeof(uint32_t)));
   BP_CUDA_TRY(cudaMalloc(&c->d_pos, C * sizeof(uint32_t)));
-  BP_CUDA_TRY(cudaMalloc(&c->d_partials, (scan_tiles(C) + 1) * sizeof(uint32_t)));
+  BP_CUDA_TRY(cudaMalloc(&c->d_partials, scan_state_words(C) * sizeof(uint32_t)));
   BP_CUDA_TRY(cudaMalloc(&c->d_ctr, sizeof(CacheCounters)));
   BP_CUDA_TRY(cudaMallocHost(&c->h_ctr, sizeof(CacheCounters)));
   BP_CUDA_TRY(cudaMemset(c->d_dirty, 0, C));

@@ -246,7 +246,7 @@ int registry_map(Registry* r, const uint64_t* d_keys, long long n, const long lo
       r->claim_cap = pow2_at_least(n);
       BP_CUDA_TRY(pool_alloc(&r->d_claim, r->claim_cap, s));
       BP_CUDA_TRY(pool_alloc(&r->d_claim_scan, r->claim_cap + 1, s));
-      BP_CUDA_TRY(pool_alloc(&r->d_partials, scan_tiles(r->claim_cap) + 1, s));
+      BP_CUDA_TRY(pool_alloc(&r->d_partials, scan_state_words(r->claim_cap), s));
     }
     long long* slot_of_input;
     BP_CUDA_TRY(pool_alloc(&slot_of_input, n, s));

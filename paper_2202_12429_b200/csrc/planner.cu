@@ -145,7 +145,7 @@ static int planner_scratch(bp_planner* p, long long n, cudaStream_t s) {
   BP_CUDA_TRY(pool_alloc(&p->d_ev_flag, cap, s));
   BP_CUDA_TRY(pool_alloc(&p->d_pf_pos, cap, s));
   BP_CUDA_TRY(pool_alloc(&p->d_ev_pos, cap, s));
-  BP_CUDA_TRY(pool_alloc(&p->d_partials, scan_tiles(cap) + 1, s));
+  BP_CUDA_TRY(pool_alloc(&p->d_partials, scan_state_words(cap), s));
   return BP_OK;
 }
 

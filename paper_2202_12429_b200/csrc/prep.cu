@@ -122,7 +122,7 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
   BP_CUDA_TRY(pool_alloc(&segx, n, s));
   BP_CUDA_TRY(pool_alloc(&first_flag, n, s));
   BP_CUDA_TRY(pool_alloc(&first_rank, n, s));
-  BP_CUDA_TRY(pool_alloc(&partials, (long long)sort_partials_words(n) + scan_tiles(n) + 1, s));
+  BP_CUDA_TRY(pool_alloc(&partials, (long long)sort_partials_words(n) + scan_state_words(n), s));
   const int g = grid_for(n, 256);
   int which = 0;
   if (P->schema_mode) {

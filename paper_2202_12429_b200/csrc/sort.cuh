@@ -56,77 +56,111 @@ __device__ __forceinline__ uint32_t block_inclusive_scan_256(uint32_t v, uint32_
   return v + add;
 }
 
-static __global__ void k_scan_reduce(const uint32_t* __restrict__ in, long long n, const long long* d_n,
-                              uint32_t* __restrict__ partials) {
+// Single-pass exclusive scan with decoupled look-back.  Each CTA scans a
+// 4096-element tile (16 consecutive elements per thread, vector loads),
+// publishes its aggregate, then thread 0 walks back over predecessor tiles
+// until it meets an inclusive prefix.  Tile status words pack
+// (epoch:30 | flag:2 | value:32), so the state array never needs clearing:
+// entries from earlier calls carry another epoch and read as "not ready".
+constexpr unsigned long long kFlagAgg = 1ull, kFlagPrefix = 2ull;
+
+__device__ __forceinline__ unsigned long long scan_pack(uint32_t epoch, unsigned long long flag, uint32_t v) {
+  return ((unsigned long long)(epoch & 0x3FFFFFFFu) << 34) | (flag << 32) | v;
+}
+
+static __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(const uint32_t* in, uint32_t* out, long long n,
+                                                                      const long long* d_n,
+                                                                      unsigned long long* state, uint32_t epoch,
+                                                                      uint32_t* total, long long* total64) {
   n = load_count(n, d_n);
-  const long long base = (long long)blockIdx.x * kScanTile;
-  uint32_t s = 0;
-#pragma unroll 4
-  for (int r = 0; r < kScanIpt; ++r) {
-    const long long i = base + r * kScanThreads + threadIdx.x;
-    if (i < n) s += in[i];
+  const long long tile = blockIdx.x;
+  const long long base = tile * kScanTile;
+  if (base >= n && tile > 0) return;
+  __shared__ uint32_t sh_warp[kScanThreads / 32];
+  __shared__ uint32_t sh_prefix;
+  const long long i0 = base + (long long)threadIdx.x * kScanIpt;
+  uint32_t v[kScanIpt];
+  if (i0 + kScanIpt <= n && ((reinterpret_cast<uintptr_t>(in + i0) & 15) == 0)) {
+    const uint4* p = reinterpret_cast<const uint4*>(in + i0);
+#pragma unroll
+    for (int q = 0; q < kScanIpt / 4; ++q) {
+      const uint4 w = p[q];
+      v[4 * q] = w.x;
+      v[4 * q + 1] = w.y;
+      v[4 * q + 2] = w.z;
+      v[4 * q + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kScanIpt; ++q) v[q] = i0 + q < n ? in[i0 + q] : 0u;
   }
-  s = warp_sum(s);
-  __shared__ uint32_t sh[kScanThreads / 32];
-  if (lane_id() == 0) sh[threadIdx.x >> 5] = s;
+  uint32_t run = 0;
+#pragma unroll
+  for (int q = 0; q < kScanIpt; ++q) {
+    const uint32_t x = v[q];
+    v[q] = run;  // exclusive within the thread
+    run += x;
+  }
+  uint32_t block_total;
+  const uint32_t thread_excl = block_inclusive_scan_256(run, sh_warp, &block_total) - run;
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* st = state;
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      st[0] = scan_pack(epoch, kFlagPrefix, block_total);
+    } else {
+      st[tile] = scan_pack(epoch, kFlagAgg, block_total);
+      for (long long j = tile - 1; j >= 0; --j) {
+        unsigned long long w;
+        do {
+          w = st[j];
+        } while ((uint32_t)(w >> 34) != (epoch & 0x3FFFFFFFu) || ((w >> 32) & 3ull) == 0);
+        prefix += (uint32_t)w;
+        if (((w >> 32) & 3ull) == kFlagPrefix) break;
+      }
+      st[tile] = scan_pack(epoch, kFlagPrefix, prefix + block_total);
+    }
+    sh_prefix = prefix;
+    if (base + kScanTile >= n) {
+      if (total) *total = prefix + block_total;
+      if (total64) *total64 = (long long)(prefix + block_total);
+    }
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t t = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) t += sh[w];
-    partials[blockIdx.x] = t;
+  const uint32_t add = sh_prefix + thread_excl;
+  if (i0 + kScanIpt <= n && ((reinterpret_cast<uintptr_t>(out + i0) & 15) == 0)) {
+    uint4* p = reinterpret_cast<uint4*>(out + i0);
+#pragma unroll
+    for (int q = 0; q < kScanIpt / 4; ++q)
+      p[q] = make_uint4(v[4 * q] + add, v[4 * q + 1] + add, v[4 * q + 2] + add, v[4 * q + 3] + add);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kScanIpt; ++q)
+      if (i0 + q < n) out[i0 + q] = v[q] + add;
   }
 }
-
-// Single CTA: exclusive scan of ``tiles`` partials in place; writes the grand
-// total to *total (u32) and optionally *total64.
-static __global__ void k_scan_partials(uint32_t* partials, int tiles, uint32_t* total, long long* total64) {
-  __shared__ uint32_t sh[kScanThreads / 32];
-  uint32_t carry = 0;
-  for (int base = 0; base < tiles; base += kScanThreads) {
-    const int i = base + threadIdx.x;
-    const uint32_t v = i < tiles ? partials[i] : 0;
-    uint32_t tot;
-    const uint32_t inc = block_inclusive_scan_256(v, sh, &tot);
-    if (i < tiles) partials[i] = carry + inc - v;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) {
-    if (total) *total = carry;
-    if (total64) *total64 = (long long)carry;
-  }
-}
-
-static __global__ void k_scan_down(const uint32_t* __restrict__ in, long long n, const long long* d_n,
-                            const uint32_t* __restrict__ partials, uint32_t* __restrict__ out) {
-  n = load_count(n, d_n);
-  __shared__ uint32_t sh[kScanThreads / 32];
-  const long long base = (long long)blockIdx.x * kScanTile;
-  if (base >= n) return;  // whole CTA exits together
-  uint32_t carry = partials[blockIdx.x];
-  for (int r = 0; r < kScanIpt; ++r) {
-    const long long i = base + r * kScanThreads + threadIdx.x;
-    const uint32_t v = i < n ? in[i] : 0;
-    uint32_t tot;
-    const uint32_t inc = block_inclusive_scan_256(v, sh, &tot);
-    if (i < n) out[i] = carry + inc - v;
-    carry += tot;
-  }
-}
-
-struct ScanTemp {
-  uint32_t* partials;  // >= tiles_for(n_max)
-};
 
 inline int scan_tiles(long long n) { return (int)((n + kScanTile - 1) / kScanTile); }
+// u32 words of tile state an exclusive_scan over n elements needs.
+inline long long scan_state_words(long long n) { return 2ll * (scan_tiles(n > 0 ? n : 1) + 1); }
 
-// Exclusive scan; *d_total (u32) and *d_total64 receive the sum.  in and out may alias.
+inline uint32_t next_scan_epoch() {
+  static unsigned int counter = 0;
+  return __atomic_add_fetch(&counter, 1u, __ATOMIC_RELAXED);
+}
+
+// Exclusive scan; *d_total (u32) and *d_total64 receive the sum.  in and out
+// may alias.  ``state`` needs scan_state_words(n_max) u32 (8-byte aligned).
 inline cudaError_t exclusive_scan(const uint32_t* in, uint32_t* out, long long n_max, const long long* d_n,
-                                  uint32_t* partials, uint32_t* d_total, long long* d_total64,
-                                  cudaStream_t s) {
+                                  uint32_t* state, uint32_t* d_total, long long* d_total64, cudaStream_t s) {
   const int tiles = scan_tiles(n_max > 0 ? n_max : 1);
-  k_scan_reduce<<<tiles, kScanThreads, 0, s>>>(in, n_max, d_n, partials);
-  k_scan_partials<<<1, kScanThreads, 0, s>>>(partials, tiles, d_total, d_total64);
-  k_scan_down<<<tiles, kScanThreads, 0, s>>>(in, n_max, d_n, partials, out);
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(state) + 7) & ~uintptr_t(7));
+  // Epoch tags already separate calls; clearing the (tiny) state as well
+  // rules out a recycled pool buffer whose garbage happens to match an epoch.
+  cudaError_t e = cudaMemsetAsync(st, 0, sizeof(unsigned long long) * tiles, s);
+  if (e != cudaSuccess) return e;
+  k_scan_onepass<<<tiles, kScanThreads, 0, s>>>(in, out, n_max, d_n, st, next_scan_epoch(), d_total, d_total64);
   return cudaGetLastError();
 }
 
@@ -249,7 +283,7 @@ cudaError_t radix_sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* v
   return cudaGetLastError();
 }
 
-inline size_t sort_partials_words(long long n) { return (size_t)scan_tiles((long long)sort_hist_words(n)) + 1; }
+inline size_t sort_partials_words(long long n) { return (size_t)scan_state_words((long long)sort_hist_words(n)); }
 
 inline int bit_width_u64(unsigned long long x) {
   int b = 0;

@@ -24,7 +24,7 @@ namespace bp {
 // wait on memory), and chunks are broadcast to the group by shuffles.  The
 // dependent chain per lane is one float add per occurrence.
 template <int G, int DPL>
-__global__ void __launch_bounds__(256) k_stub_step(
+__global__ void __launch_bounds__(256, 6) k_stub_step(
     const uint32_t* __restrict__ seg_start, const uint8_t* __restrict__ occ_label,
     const long long* __restrict__ d_U, float* __restrict__ rows, const int32_t* __restrict__ row_index,
     uint8_t* __restrict__ dirty, int dim, float c_value, float c_label, float lr, int mode,
@@ -44,14 +44,21 @@ __global__ void __launch_bounds__(256) k_stub_step(
   for (long long base = warp_first; base < U; base += groups_total) {
     const long long s = base + (long long)(lane / G);
     bool active = s < U;
+    // Issue every per-key load that does not depend on another one up front
+    // (segment bounds, slot, next-batch stamp), then the dependent ones (row,
+    // label chunks): two memory latencies per key instead of four in series.
+    uint32_t a = 0, b = 0;
     int32_t row = 0;
+    bool crit = false;
     if (active) {
+      a = seg_start[s];
+      b = seg_start[s + 1];
       row = row_index ? row_index[s] : (int32_t)s;
+      if (next_mark && lane_g == 0) crit = next_mark[my_ids[s]] == next_tag;
       active = row >= 0;
     }
     bool nonzero = false;
     if (active) {
-      const uint32_t a = seg_start[s], b = seg_start[s + 1];
       float v[DPL], t0[DPL], t1[DPL], sc[DPL], acc[DPL], comb[DPL];
 #pragma unroll
       for (int q = 0; q < DPL; ++q) {
@@ -134,13 +141,10 @@ __global__ void __launch_bounds__(256) k_stub_step(
       }
     }
     const unsigned nz = __ballot_sync(0xffffffffu, nonzero) & gmask;
-    bool crit = false;
-    if (active && lane_g == 0) {
-      if (nz && dirty && mode == BP_STUB_SGD) dirty[row] = 1;
-      // critical = needed by the next batch (reference engine.py:560-564):
-      // the next batch's ids carry its iteration tag in a dense mark array.
-      if (next_mark) crit = next_mark[my_ids[s]] == next_tag;
-    }
+    // critical = needed by the next batch (reference engine.py:560-564): the
+    // next batch's ids carry its iteration tag in a dense mark array.
+    crit = crit && active;
+    if (active && lane_g == 0 && nz && dirty && mode == BP_STUB_SGD) dirty[row] = 1;
     if (stats) {
       const unsigned cm = __ballot_sync(0xffffffffu, crit);
       const unsigned dm = __ballot_sync(0xffffffffu, active && lane_g == 0 && nz != 0);
