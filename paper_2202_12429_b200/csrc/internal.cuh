@@ -21,6 +21,9 @@ struct bp_schema {
 namespace bp {
 
 constexpr uint32_t kNoId = 0xFFFFFFFFu;
+// Segments at least this long (occurrences of one key in one batch) take the
+// shared-memory path of the trainer kernel (trainer.cu).
+constexpr uint32_t kLongSeg = 512;
 constexpr uint64_t kEmptyKey = ~0ull;
 
 // Memory from the device's stream-ordered pool (release threshold raised at
@@ -99,6 +102,8 @@ struct bp_prep {
   uint8_t* d_occ_label;
   uint32_t* d_occ_k;
   long long* d_rank_bounds;
+  uint32_t* d_long;        // key-sorted indices of segments with >= kLongSeg occurrences
+  long long* d_num_long;
   long long h_num_unique;  // -1 until read back
   cudaStream_t stream;
 };

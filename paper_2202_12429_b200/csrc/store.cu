@@ -186,7 +186,7 @@ extern "C" int bp_store_fetch(bp_store* st, const uint32_t* d_ids, int64_t n, co
   const int dim = st->dim;
   if ((dim & 3) == 0) {
     const int q = dim >> 2;
-    k_store_fetch_v4<<<grid_for(n * q, 256, kNumSMs * 32), 256, 0, s>>>(
+    k_store_fetch_v4<<<grid_for(n * q, 256 * kIlp, kNumSMs), 256, 0, s>>>(
         reinterpret_cast<const float4*>(st->d_table), d_ids, n, (const long long*)d_n, q,
         reinterpret_cast<float4*>(d_out));
   } else {
@@ -202,7 +202,7 @@ extern "C" int bp_store_write(bp_store* st, const uint32_t* d_ids, const float* 
   using namespace bp;
   if (n <= 0) return BP_OK;
   const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
-  k_store_write<<<grid_for(n * q, 256, kNumSMs * 32), 256, 0, (cudaStream_t)stream>>>(
+  k_store_write<<<grid_for(n * q, 256 * kIlp, kNumSMs), 256, 0, (cudaStream_t)stream>>>(
       st->d_table, st->d_written, d_ids, d_rows, nullptr, n, (const long long*)d_n, st->dim);
   BP_LAUNCH_CHECK();
   return BP_OK;
@@ -213,7 +213,7 @@ extern "C" int bp_store_write_masked(bp_store* st, const uint32_t* d_ids, const 
   using namespace bp;
   if (n <= 0) return BP_OK;
   const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
-  k_store_write<<<grid_for(n * q, 256, kNumSMs * 32), 256, 0, (cudaStream_t)stream>>>(
+  k_store_write<<<grid_for(n * q, 256 * kIlp, kNumSMs), 256, 0, (cudaStream_t)stream>>>(
       st->d_table, st->d_written, d_ids, d_rows, d_mask, n, (const long long*)d_n, st->dim);
   BP_LAUNCH_CHECK();
   return BP_OK;

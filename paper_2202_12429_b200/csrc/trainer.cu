@@ -16,37 +16,151 @@
 
 namespace bp {
 
-// One group of G lanes per unique key; lane = embedding component (DPL
-// components per lane when dim > 32).  The key's occurrence bytes (label |
-// rank-start flag, see prep.cu) are streamed as aligned 16-byte chunks: each
-// lane loads one chunk per round, two rounds are kept in flight (the Zipf-hot
-// keys of tiny tables have ~9K occurrences per batch, so the chain must not
-// wait on memory), and chunks are broadcast to the group by shuffles.  The
-// dependent chain per lane is one float add per occurrence.
+// Accumulate the occurrence bytes [lo, hi) of one 16-byte chunk into the
+// per-component chains.  Byte = label (7 bits) | rank-start flag (bit 7);
+// ``first_q`` is the chunk offset of the key's first occurrence (16 if the
+// key does not start in this chunk): its flag opens the chain, every other
+// flag closes the running rank partial into ``comb``.
+template <int DPL>
+__device__ __forceinline__ void chain_chunk(const uint32_t (&word)[4], uint32_t lo, uint32_t hi, uint32_t first_q,
+                                            float (&acc)[DPL], float (&comb)[DPL], const float (&t0)[DPL],
+                                            const float (&t1)[DPL], const float (&sc)[DPL], float c_label) {
+  const uint32_t big = (word[0] | word[1] | word[2] | word[3]) & 0x7E7E7E7Eu;
+  const uint32_t flags_hi = (word[1] | word[2] | word[3]) & 0x80808080u;
+  const uint32_t flags_lo = word[0] & 0x80808080u;
+  if (lo == 0 && hi == 16 && !big && !flags_hi && (flags_lo == 0 || (first_q == 0 && flags_lo == 0x80u))) {
+    // 16 occurrences, labels 0/1, no rank change: one select + one add each.
+#pragma unroll
+    for (int wi = 0; wi < 4; ++wi) {
+#pragma unroll
+      for (int bi = 0; bi < 4; ++bi) {
+        const bool one = (word[wi] >> (bi * 8)) & 1u;
+#pragma unroll
+        for (int q = 0; q < DPL; ++q) acc[q] = __fadd_rn(acc[q], one ? t1[q] : t0[q]);
+      }
+    }
+    return;
+  }
+  for (uint32_t q8 = lo; q8 < hi; ++q8) {
+    const uint32_t byte = (word[q8 >> 2] >> ((q8 & 3) * 8)) & 0xFFu;
+    const uint32_t lab = byte & 0x7Fu;
+    if ((byte & 0x80u) && q8 != first_q) {
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) {
+        comb[q] = __fadd_rn(comb[q], acc[q]);
+        acc[q] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < DPL; ++q) {
+      const float t = lab == 0 ? t0[q]
+                    : lab == 1 ? t1[q]
+                               : __fadd_rn(sc[q], __fmul_rn(c_label, __fsub_rn((float)lab, 0.5f)));
+      acc[q] = __fadd_rn(acc[q], t);
+    }
+  }
+}
+
+constexpr int kLongBlocks = 64;        // CTAs reserved for long segments
+constexpr int kLongWindowChunks = 1024;  // 16 KB of occurrence bytes staged in smem
+
+// Fused trainer kernel.  CTAs [0, kLongBlocks) take the keys whose segment
+// has >= kLongSeg occurrences (the Zipf-hot rows of tiny tables, up to ~9K
+// per batch at Criteo-Kaggle): the whole CTA stages the key's occurrence
+// bytes in shared memory with coalesced 16-byte loads, then one warp runs the
+// per-component chains from shared memory (broadcast reads, no global
+// latency inside the chain).  All other CTAs handle short segments with one
+// group of G lanes per key (lane = component, DPL components per lane when
+// dim > 32): every per-key load that does not depend on another is issued
+// up front, and the label chunks are prefetched two rounds ahead.
 template <int G, int DPL>
 __global__ void __launch_bounds__(256, 6) k_stub_step(
     const uint32_t* __restrict__ seg_start, const uint8_t* __restrict__ occ_label,
-    const long long* __restrict__ d_U, float* __restrict__ rows, const int32_t* __restrict__ row_index,
+    const long long* __restrict__ d_U, const uint32_t* __restrict__ long_list,
+    const long long* __restrict__ d_num_long, float* __restrict__ rows, const int32_t* __restrict__ row_index,
     uint8_t* __restrict__ dirty, int dim, float c_value, float c_label, float lr, int mode,
     float* __restrict__ grad_out, const uint32_t* __restrict__ my_ids, const int64_t* __restrict__ next_mark,
     long long next_tag, unsigned long long* __restrict__ stats) {
-  const long long U = *d_U;
   const unsigned lane = threadIdx.x & 31u;
+  const uint4* __restrict__ chunks = reinterpret_cast<const uint4*>(occ_label);
+  const float b0 = __fmul_rn(c_label, -0.5f), b1 = __fmul_rn(c_label, 0.5f);
+
+  if (blockIdx.x < kLongBlocks) {
+    __shared__ uint4 win[kLongWindowChunks];
+    const long long n_long = *d_num_long;
+    const bool chain_lane = threadIdx.x < G;  // warp 0, lanes [0, G)
+    for (long long li = blockIdx.x; li < n_long; li += kLongBlocks) {
+      const uint32_t s = long_list[li];
+      const uint32_t a = seg_start[s], b = seg_start[s + 1];
+      const int32_t row = row_index ? row_index[s] : (int32_t)s;
+      if (row < 0) continue;  // block-uniform: the miss is already recorded
+      float v[DPL], t0[DPL], t1[DPL], sc[DPL], acc[DPL], comb[DPL];
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) {
+        const int d = (int)threadIdx.x + q * G;
+        v[q] = (chain_lane && d < dim) ? rows[(long long)row * dim + d] : 0.f;
+        sc[q] = __fmul_rn(c_value, v[q]);
+        t0[q] = __fadd_rn(sc[q], b0);
+        t1[q] = __fadd_rn(sc[q], b1);
+        acc[q] = 0.f;
+        comb[q] = 0.f;
+      }
+      const uint32_t c0 = a >> 4, c_end = ((b - 1) >> 4) + 1;
+      for (uint32_t wc = c0; wc < c_end; wc += kLongWindowChunks) {
+        const uint32_t nchunk = min((uint32_t)kLongWindowChunks, c_end - wc);
+        for (uint32_t k = threadIdx.x; k < nchunk; k += blockDim.x) win[k] = chunks[wc + k];
+        __syncthreads();
+        if (chain_lane) {
+#pragma unroll 2
+          for (uint32_t k = 0; k < nchunk; ++k) {
+            const uint4 w4 = win[k];
+            const uint32_t word[4] = {w4.x, w4.y, w4.z, w4.w};
+            const uint32_t cbase = (wc + k) << 4;
+            const uint32_t lo = a > cbase ? a - cbase : 0u;
+            const uint32_t hi = b - cbase < 16u ? b - cbase : 16u;
+            const uint32_t first_q = (a >= cbase && a < cbase + 16) ? a - cbase : 16u;
+            chain_chunk<DPL>(word, lo, hi, first_q, acc, comb, t0, t1, sc, c_label);
+          }
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x < 32) {
+        bool nonzero = false;
+#pragma unroll
+        for (int q = 0; q < DPL; ++q) {
+          comb[q] = __fadd_rn(comb[q], acc[q]);
+          const int d = (int)threadIdx.x + q * G;
+          if (chain_lane && d < dim) {
+            nonzero |= comb[q] != 0.f;
+            if (mode == BP_STUB_SGD) rows[(long long)row * dim + d] = __fsub_rn(v[q], __fmul_rn(lr, comb[q]));
+            else grad_out[(long long)s * dim + d] = comb[q];
+          }
+        }
+        const bool nz = __ballot_sync(0xffffffffu, nonzero) != 0;
+        if (threadIdx.x == 0) {
+          if (nz && dirty && mode == BP_STUB_SGD) dirty[row] = 1;
+          if (stats) {
+            if (next_mark && next_mark[my_ids[s]] == next_tag) atomicAdd(&stats[0], 1ull);
+            if (nz) atomicAdd(&stats[1], 1ull);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  const long long U = *d_U;
   const int lane_g = (int)(lane & (G - 1));
   const unsigned gbase = lane & ~(unsigned)(G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const long long groups_per_block = blockDim.x / G;
-  const long long groups_total = (long long)gridDim.x * groups_per_block;
-  const long long warp_first = (long long)blockIdx.x * groups_per_block + (threadIdx.x >> 5) * (32 / G);
-  const uint4* __restrict__ chunks = reinterpret_cast<const uint4*>(occ_label);
-  const float b0 = __fmul_rn(c_label, -0.5f), b1 = __fmul_rn(c_label, 0.5f);
+  const long long groups_total = (long long)(gridDim.x - kLongBlocks) * groups_per_block;
+  const long long warp_first =
+      (long long)(blockIdx.x - kLongBlocks) * groups_per_block + (threadIdx.x >> 5) * (32 / G);
 
   for (long long base = warp_first; base < U; base += groups_total) {
     const long long s = base + (long long)(lane / G);
     bool active = s < U;
-    // Issue every per-key load that does not depend on another one up front
-    // (segment bounds, slot, next-batch stamp), then the dependent ones (row,
-    // label chunks): two memory latencies per key instead of four in series.
     uint32_t a = 0, b = 0;
     int32_t row = 0;
     bool crit = false;
@@ -55,7 +169,7 @@ __global__ void __launch_bounds__(256, 6) k_stub_step(
       b = seg_start[s + 1];
       row = row_index ? row_index[s] : (int32_t)s;
       if (next_mark && lane_g == 0) crit = next_mark[my_ids[s]] == next_tag;
-      active = row >= 0;
+      active = row >= 0 && b - a < kLongSeg;  // long segments belong to the long CTAs
     }
     bool nonzero = false;
     if (active) {
@@ -65,8 +179,8 @@ __global__ void __launch_bounds__(256, 6) k_stub_step(
         const int d = lane_g + q * G;
         v[q] = d < dim ? rows[(long long)row * dim + d] : 0.f;
         sc[q] = __fmul_rn(c_value, v[q]);
-        t0[q] = __fadd_rn(sc[q], b0);  // occurrence gradient for label 0
-        t1[q] = __fadd_rn(sc[q], b1);  // ... and label 1
+        t0[q] = __fadd_rn(sc[q], b0);
+        t1[q] = __fadd_rn(sc[q], b1);
         acc[q] = 0.f;
         comb[q] = 0.f;
       }
@@ -88,43 +202,8 @@ __global__ void __launch_bounds__(256, 6) k_stub_step(
           const uint32_t cbase = (c_first + r0 + i) << 4;
           const uint32_t lo = a > cbase ? a - cbase : 0u;
           const uint32_t hi = b - cbase < 16u ? b - cbase : 16u;
-          const bool full = lo == 0 && hi == 16;
-          const uint32_t big = (word[0] | word[1] | word[2] | word[3]) & 0x7E7E7E7Eu;
-          const uint32_t flags_hi = (word[1] | word[2] | word[3]) & 0x80808080u;
-          const uint32_t flags_lo = word[0] & 0x80808080u;
-          if (full && !big && !flags_hi && (flags_lo == 0 || (cbase == a && flags_lo == 0x80u))) {
-            // Fast path: 16 occurrences, labels 0/1, no rank change inside
-            // the chunk (a rank-start flag on the key's first byte is the
-            // start of the chain itself): one select + one add each.
-#pragma unroll
-            for (int wi = 0; wi < 4; ++wi) {
-#pragma unroll
-              for (int bi = 0; bi < 4; ++bi) {
-                const bool one = (word[wi] >> (bi * 8)) & 1u;
-#pragma unroll
-                for (int q = 0; q < DPL; ++q) acc[q] = __fadd_rn(acc[q], one ? t1[q] : t0[q]);
-              }
-            }
-          } else {
-            for (uint32_t q8 = lo; q8 < hi; ++q8) {
-              const uint32_t byte = (word[q8 >> 2] >> ((q8 & 3) * 8)) & 0xFFu;
-              const uint32_t lab = byte & 0x7Fu;
-              if ((byte & 0x80u) && cbase + q8 != a) {  // a new trainer rank starts: close the partial
-#pragma unroll
-                for (int q = 0; q < DPL; ++q) {
-                  comb[q] = __fadd_rn(comb[q], acc[q]);
-                  acc[q] = 0.f;
-                }
-              }
-#pragma unroll
-              for (int q = 0; q < DPL; ++q) {
-                const float t = lab == 0 ? t0[q]
-                              : lab == 1 ? t1[q]
-                                         : __fadd_rn(sc[q], __fmul_rn(c_label, __fsub_rn((float)lab, 0.5f)));
-                acc[q] = __fadd_rn(acc[q], t);
-              }
-            }
-          }
+          const uint32_t first_q = (a >= cbase && a < cbase + 16) ? a - cbase : 16u;
+          chain_chunk<DPL>(word, lo, hi, first_q, acc, comb, t0, t1, sc, c_label);
         }
         w0 = w1;
         w1 = w2;
@@ -253,10 +332,11 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   cudaStream_t s = (cudaStream_t)stream;
   const long long groups = P->n_occ;  // upper bound on U
   const int threads = 256;
-  const int blocks = grid_for(groups * G, threads, kNumSMs * 8);
+  const int blocks = kLongBlocks + grid_for(groups * G, threads, kNumSMs * 6);
   BP_DISPATCH_GD(G, dpl,
                  (k_stub_step<g_, d_><<<blocks, threads, 0, s>>>(
-                     P->d_seg_start, P->d_occ_label, P->d_num_unique, d_rows, d_row_index, d_dirty, dim, c_value,
+                     P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, d_rows,
+                     d_row_index, d_dirty, dim, c_value,
                      c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark, next_tag,
                      (unsigned long long*)d_stats)));
   BP_LAUNCH_CHECK();
