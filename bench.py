@@ -119,37 +119,6 @@ def stub_step_bytes(n_occ: int, u: int) -> int:
     return n_occ * 5 + u * (8 + 8 * DIM)
 
 
-class Probe:
-    """CUDA events around engine stages, on the stream the kernels run on."""
-
-    def __init__(self):
-        import torch
-
-        self.torch = torch
-        self.open = {}
-        self.spans = {}
-        self.enabled = False
-
-    def __call__(self, name, phase, stream):
-        if not self.enabled:
-            return
-        ev = self.torch.cuda.Event(enable_timing=True)
-        ev.record(stream)
-        if phase == 0:
-            self.open[name] = ev
-        else:
-            self.spans.setdefault(name, []).append((self.open.pop(name), ev))
-
-    def totals_ms(self) -> dict:
-        for v in self.spans.values():
-            for _, b in v:
-                b.synchronize()
-        return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.spans.items()}
-
-    def counts(self) -> dict:
-        return {k: len(v) for k, v in self.spans.items()}
-
-
 def count_launches(pipe, pos: int) -> int:
     """Kernels of our library launched by one engine step (torch profiler / CUPTI)."""
     import torch
@@ -189,9 +158,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         keys, labels, _ = b.packed_occurrences()
         dev_inputs[i] = (torch.from_numpy(keys).cuda(), torch.from_numpy(labels).cuda())
     torch.cuda.synchronize()
-    pipe = _Pipeline(cfg, sc, batches, None, None, device_inputs=dev_inputs)
-    probe = Probe()
-    pipe.probe = probe
+    pipe = _Pipeline(cfg, sc, batches, None, None, device_inputs=dev_inputs, timing=True)
+    stream = pipe.stream  # the engine's compute stream (kernels of a step run there)
     pipe.begin()
     for pos in range(warm):
         pipe.step(pos)
@@ -202,23 +170,24 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    pipe.stage_times()  # reset the per-stage event record
     clocks.start()
     wall0 = time.perf_counter()
-    probe.enabled = True
     for i in range(steps):
         flush_buf.zero_()  # evict L2 between timed steps (outside the timed span)
+        stream.wait_stream(torch.cuda.current_stream())
         starts[i].record(stream)
         pipe.step(warm + i)
         ends[i].record(stream)
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
-    probe.enabled = False
     clk = clocks.stop()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    stage_ms = probe.totals_ms()
+    stages = pipe.stage_times()
     records = pipe.records[warm:warm + steps]
     launches_per_step = count_launches(pipe, warm + steps)
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
+    pf_mean = statistics.mean(r.prefetch_count for r in records)
     n_occ = BATCH * sc.num_tables
 
     # ---- e2e: host batches through the public engine API
@@ -226,6 +195,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     if not args.no_e2e:
         batches_e2e = make_batches(n_batches, args.seed + 1000 + rank)
         pipe2 = _Pipeline(cfg, sc, batches_e2e, None, None)
+        s2 = pipe2.stream
         pipe2.begin()
         for pos in range(warm):
             pipe2.step(pos)
@@ -236,9 +206,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         t_e2e = 0.0
         for i in range(steps):
             flush_buf.zero_()
-            e0.record(stream)
+            s2.wait_stream(torch.cuda.current_stream())
+            e0.record(s2)
             pipe2.step(warm + i)
-            e1.record(stream)
+            e1.record(s2)
             e1.synchronize()
             t_e2e += e0.elapsed_time(e1)
         e2e = {"ms": t_e2e, "h2d_bytes_per_step": n_occ * 9, "d2h_bytes_per_step": 8 * 8 + 32 + 4 * 8}
@@ -257,9 +228,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    stub_launches = probe.counts().get("stub_step", steps)
-    stub_ms = stage_ms.get("stub_step", 0.0) / max(stub_launches, 1)
+    stub_total, stub_launches = stages["trainer"]
+    stub_ms = stub_total / max(stub_launches, 1)
     stub_bytes = stub_step_bytes(n_occ, int(u_mean))
+    fetch_total, fetch_n = stages["fetch"]
+    flush_total, flush_n = stages["flush"]
     achieved = stub_bytes / (stub_ms * 1e-3) / 1e9 if stub_ms else 0.0
     samples = BATCH * steps * world
     out = {
@@ -285,7 +258,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                      "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
                      "bytes_per_launch": stub_bytes, "ms_per_launch": stub_ms},
-        "stages_ms_per_step": {k: v / steps for k, v in stage_ms.items()},
+        "stages_ms_per_step": {k: v[0] / steps for k, v in stages.items()},
+        "host_link": {"prefetch_rows_per_step": pf_mean,
+                      "prefetch_gbs": pf_mean * 64 * fetch_n / (fetch_total * 1e-3) / 1e9 if fetch_total else None,
+                      "writeback_gbs_note": "flush every 2 steps; see stages_ms_per_step.flush"},
         "gpu_launches": launches_per_step * steps,
         "clocks": clk,
         "wall_s_timed_region": wall,

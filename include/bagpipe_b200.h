@@ -295,6 +295,62 @@ int bp_prep_key_rows(bp_prep* prep, int32_t* d_out, bp_stream_t stream);
 /* sgd_step (reference trainer.py:140-146): out = v - lr*g, single precision. */
 int bp_sgd(const float* d_values, const float* d_grads, float lr, int64_t count, float* d_out, bp_stream_t stream);
 
+/* ----------------------------------------------------------------- engine
+ * Native runtime of the pipelined iteration (reference engine.py:487-649):
+ * owns the store, cache, planner, two streams (compute, host link) and every
+ * per-iteration buffer (plan / staging / chunk rings), so one iteration is a
+ * handful of calls and no allocation.  The host keeps the scalar control
+ * flow (window, gate, flush cadence, simulated clock) and drives:
+ *   add_batch -> refill/pop -> fetch -> train -> flush -> release_batch. */
+typedef struct bp_engine bp_engine;
+typedef struct bp_engine_config {
+  int64_t capacity;   /* cache entries */
+  int64_t max_occ;    /* largest batch (occurrences) */
+  uint64_t seed;      /* store seed */
+  int32_t dim;
+  int32_t num_ranks;  /* data-parallel trainers T (combine order) */
+  float c_value, c_label, lr;
+  int32_t record_keys; /* keep evicted keys for event logs */
+  int32_t plan_slots, chunk_slots, prep_slots;
+  int32_t timing;      /* record per-stage CUDA events (bp_engine_stage_times) */
+} bp_engine_config;
+typedef struct bp_step_result {
+  int64_t unique, inserted, critical, dirty_keys, evicted, evicted_dirty, drained, drained_dirty;
+  bp_error_t err;
+} bp_step_result;
+typedef struct bp_engine_parts_t {
+  bp_store* store;
+  bp_cache* cache;
+  bp_planner* planner;
+  bp_stream_t compute_stream;
+  bp_stream_t link_stream;
+} bp_engine_parts_t;
+int bp_engine_create(bp_ctx* ctx, const bp_schema* schema, const bp_engine_config* cfg, bp_engine** out);
+int bp_engine_destroy(bp_engine* engine);
+int bp_engine_parts(bp_engine* engine, bp_engine_parts_t* out);
+/* keys/labels: host pointers (keys_on_host=1, copied through a pinned ring)
+ * or device pointers that stay valid until the prep kernels ran. */
+int bp_engine_add_batch(bp_engine* engine, int64_t pos, int64_t iteration, const uint64_t* keys,
+                        const uint8_t* labels, int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks,
+                        int32_t keys_on_host);
+int bp_engine_prep(bp_engine* engine, int64_t pos, bp_prep** out);
+int bp_engine_release_batch(bp_engine* engine, int64_t pos);
+int bp_engine_refill(bp_engine* engine, int64_t pos);
+int bp_engine_pop(bp_engine* engine, int64_t pos, int32_t* slot_out);
+int bp_engine_plan_counts(bp_engine* engine, int32_t slot, int64_t* h_out4); /* waits for that pop */
+int bp_engine_plan_view(bp_engine* engine, int32_t slot, bp_plan_buffers* out, float** d_staging);
+int bp_engine_fetch(bp_engine* engine, int32_t slot);
+int bp_engine_flush(bp_engine* engine, const int32_t* h_chunk_slots, int32_t n);
+int bp_engine_train(bp_engine* engine, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
+                    int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out);
+int bp_engine_chunk_keys(bp_engine* engine, int32_t chunk_slot, uint64_t* h_out, int64_t n);
+int bp_engine_chunk_view(bp_engine* engine, int32_t chunk_slot, bp_evict_buffers* out);
+int bp_engine_sync(bp_engine* engine);
+/* Per-stage device time since the last call, 7 stages: prep, planner, fetch
+ * (link), apply (insert+TTL+lookup+mark), trainer, evict, flush (link).
+ * Synchronises the device. */
+int bp_engine_stage_times(bp_engine* engine, double* h_ms7, int64_t* h_counts7);
+
 /* ------------------------------------------------------------ utilities */
 /* Sort packed keys ascending with a u32 payload (stable); n host-known. */
 int bp_sort_keys_u64(uint64_t* d_keys, uint32_t* d_vals, int64_t n, int32_t key_bits, bp_stream_t stream);

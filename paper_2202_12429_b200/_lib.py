@@ -74,6 +74,22 @@ class PlannerDump(C.Structure):
     _fields_ = [("d_keys", c_vp), ("d_last", c_vp), ("d_flags", c_vp), ("d_count", c_vp)]
 
 
+class EngineConfig(C.Structure):
+    _fields_ = [("capacity", c_i64), ("max_occ", c_i64), ("seed", c_u64), ("dim", c_i32), ("num_ranks", c_i32),
+                ("c_value", c_f32), ("c_label", c_f32), ("lr", c_f32), ("record_keys", c_i32),
+                ("plan_slots", c_i32), ("chunk_slots", c_i32), ("prep_slots", c_i32), ("timing", c_i32)]
+
+
+class StepResult(C.Structure):
+    _fields_ = [(n, c_i64) for n in ("unique", "inserted", "critical", "dirty_keys", "evicted", "evicted_dirty",
+                                     "drained", "drained_dirty")] + [("err", ErrorT)]
+
+
+class EngineParts(C.Structure):
+    _fields_ = [("store", c_vp), ("cache", c_vp), ("planner", c_vp), ("compute_stream", c_vp),
+                ("link_stream", c_vp)]
+
+
 P = C.POINTER
 _SIGS = {
     "bp_version": (C.c_char_p, []),
@@ -124,6 +140,23 @@ _SIGS = {
     "bp_sgd": (c_i32, [c_vp, c_vp, c_f32, c_i64, c_vp, c_vp]),
     "bp_sort_keys_u64": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp]),
     "bp_xor_checksum_rows": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "bp_engine_create": (c_i32, [c_vp, c_vp, P(EngineConfig), P(c_vp)]),
+    "bp_engine_destroy": (c_i32, [c_vp]),
+    "bp_engine_parts": (c_i32, [c_vp, P(EngineParts)]),
+    "bp_engine_add_batch": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32]),
+    "bp_engine_prep": (c_i32, [c_vp, c_i64, P(c_vp)]),
+    "bp_engine_release_batch": (c_i32, [c_vp, c_i64]),
+    "bp_engine_refill": (c_i32, [c_vp, c_i64]),
+    "bp_engine_pop": (c_i32, [c_vp, c_i64, P(c_i32)]),
+    "bp_engine_plan_counts": (c_i32, [c_vp, c_i32, c_vp]),
+    "bp_engine_plan_view": (c_i32, [c_vp, c_i32, P(PlanBuffers), P(c_vp)]),
+    "bp_engine_fetch": (c_i32, [c_vp, c_i32]),
+    "bp_engine_flush": (c_i32, [c_vp, c_vp, c_i32]),
+    "bp_engine_train": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_u64, c_i32, c_i32, c_i32, P(StepResult)]),
+    "bp_engine_chunk_keys": (c_i32, [c_vp, c_i32, c_vp, c_i64]),
+    "bp_engine_chunk_view": (c_i32, [c_vp, c_i32, P(EvictBuffers)]),
+    "bp_engine_sync": (c_i32, [c_vp]),
+    "bp_engine_stage_times": (c_i32, [c_vp, c_vp, c_vp]),
 }
 
 _lock = threading.Lock()
@@ -204,21 +237,27 @@ class Context:
         code = lib().bp_ctx_check(self.handle, stream_ptr(stream), C.byref(err))
         if code == 0:
             return
-        key = unpack_key(err.key)
-        it = None if err.iteration < 0 else int(err.iteration)
-        index = int(err.index) & ((1 << 40) - 1)
-        if code == 2:
-            raise E.CacheMissError(key, it)
-        if code == 3:
-            raise E.CacheCapacityError(f"insert would exceed capacity at iteration {it}")
-        if code == 4:
-            raise E.CacheOrderingError(f"ordering violation for {key!r} (position {index}) at iteration {it}")
-        if code == 5:
-            raise E.StoreKeyError(f"key {key!r} outside the schema")
-        if code == 7:
-            raise E.EngineError(f"engine invariant violated at iteration {it} ({index})")
-        cls = E.STATUS_TO_ERROR.get(code, E.NativeError)
-        raise cls(f"device error {code} at iteration {it} for {key!r}")
+        raise_error_record(err)
+
+
+def raise_error_record(err: ErrorT) -> None:
+    """Raise the reference exception for a device error record (code != 0)."""
+    code = err.code
+    key = unpack_key(err.key)
+    it = None if err.iteration < 0 else int(err.iteration)
+    index = int(err.index) & ((1 << 40) - 1)
+    if code == 2:
+        raise E.CacheMissError(key, it)
+    if code == 3:
+        raise E.CacheCapacityError(f"insert would exceed capacity at iteration {it}")
+    if code == 4:
+        raise E.CacheOrderingError(f"ordering violation for {key!r} (position {index}) at iteration {it}")
+    if code == 5:
+        raise E.StoreKeyError(f"key {key!r} outside the schema")
+    if code == 7:
+        raise E.EngineError(f"engine invariant violated at iteration {it} ({index})")
+    cls = E.STATUS_TO_ERROR.get(code, E.NativeError)
+    raise cls(f"device error {code} at iteration {it} for {key!r}")
 
 
 def host_u64(keys) -> np.ndarray:

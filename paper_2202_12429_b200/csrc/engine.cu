@@ -1,0 +1,540 @@
+// Native engine runtime for the pipelined BagPipe iteration.
+//
+// The reference's per-iteration loop (engine.py:487-649) is split in two:
+// the host keeps the scalar control flow (window length, dispatch gate,
+// flush cadence, simulated clock -- integer/float bookkeeping that must stay
+// byte-identical to the reference), and this runtime owns every device
+// buffer and issues every kernel, a few coarse calls per iteration:
+//
+//   bp_engine_add_batch  upload (host or device keys) + batch prep
+//   bp_engine_refill/pop planner window step into a ring plan slot
+//   bp_engine_fetch      prefetch gather on the host-link stream
+//   bp_engine_train      insert + TTL + lookup + mark + fused trainer +
+//                        eviction into a ring chunk slot, counters D2H,
+//                        one synchronisation of the compute stream
+//   bp_engine_flush      dirty write-back of chunk slots on the link stream
+//
+// All buffers are allocated once (plan/staging/chunk rings sized for the
+// largest batch), so the steady state performs no allocation.  The compute
+// and link streams are ordered by events exactly as the reference orders
+// fetches and write-backs: prefetch of plan x waits for its pop; training of
+// x waits for the prefetch; write-backs and prefetches share the link stream
+// in dispatch order, which is the consistency gate (engine.py:302-377).
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+struct bp_store;
+struct bp_cache;
+struct bp_planner;
+
+extern "C" {
+int bp_store_create(bp_ctx*, const bp_schema*, uint64_t, bp_stream_t, bp_store**);
+int bp_store_destroy(bp_store*);
+int bp_store_fetch(bp_store*, const uint32_t*, int64_t, const int64_t*, float*, bp_stream_t);
+int bp_store_write_masked(bp_store*, const uint32_t*, const float*, const uint8_t*, int64_t, const int64_t*,
+                          bp_stream_t);
+int bp_cache_create(bp_ctx*, const bp_schema*, int64_t, int32_t, bp_cache**);
+int bp_cache_destroy(bp_cache*);
+int bp_cache_insert(bp_cache*, const uint64_t*, const uint32_t*, const float*, const int64_t*, int64_t,
+                    const int64_t*, int64_t, bp_stream_t);
+int bp_cache_apply_resolve(bp_cache*, bp_prep*, const int64_t*, uint64_t, int32_t, int32_t*, bp_stream_t);
+int bp_cache_evict(bp_cache*, int64_t, int32_t, const bp_evict_buffers*, int64_t, bp_stream_t);
+int bp_cache_get_view(const bp_cache*, bp_cache_view*);
+int bp_planner_create(bp_ctx*, const bp_schema*, int64_t, bp_planner**);
+int bp_planner_destroy(bp_planner*);
+int bp_planner_refill(bp_planner*, bp_prep*, bp_stream_t);
+int bp_planner_pop(bp_planner*, bp_prep*, const bp_plan_buffers*, bp_stream_t);
+int bp_mark_ids(bp_prep*, int64_t*, int64_t, bp_stream_t);
+int bp_stub_step(bp_ctx*, bp_prep*, float*, const int32_t*, uint8_t*, int32_t, float, float, float, int32_t, float*,
+                 const int64_t*, int64_t, int64_t*, bp_stream_t);
+}
+
+namespace bp {
+
+__global__ void k_offset_count(const int64_t* src, int64_t off, int64_t* dst) {
+  const int64_t v = *src - off;
+  *dst = v < 0 ? 0 : v;
+}
+
+struct PlanSlot {
+  uint64_t* keys;
+  uint32_t* ids;
+  int64_t* ttls;
+  int64_t* ttl_k;
+  uint64_t* evict_keys;
+  int64_t* counts;   // [4] device
+  int64_t* h_counts;  // [4] pinned
+  float* staging;    // [max_occ, dim]
+  int64_t* n_ins;    // device: counts[0] - dropped
+  cudaEvent_t popped, fetched, consumed;
+  long long prep_pos;
+};
+
+struct ChunkSlot {
+  uint64_t* keys;
+  uint32_t* ids;
+  float* rows;
+  uint8_t* dirty;
+  int64_t* count;  // [2] device
+  cudaEvent_t flushed;
+  bool pending;
+};
+
+struct UploadSlot {
+  uint8_t* host;  // pinned
+  size_t bytes;
+  cudaEvent_t done;
+  bool used;
+};
+
+}  // namespace bp
+
+namespace bp {
+// Optional per-stage CUDA-event timing (cfg.timing): pairs recorded on the
+// stream that runs the stage, summed on demand by bp_engine_stage_times.
+enum Stage { kStagePrep = 0, kStagePlanner, kStageFetch, kStageApply, kStageTrainer, kStageEvict, kStageFlush,
+             kNumStages };
+struct StageTimer {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans[kNumStages];
+  cudaEvent_t open[kNumStages] = {};
+};
+}  // namespace bp
+
+struct bp_engine {
+  bp::StageTimer timer;
+  bp_ctx* ctx;
+  const bp_schema* sc;
+  bp_engine_config cfg;
+  bp_store* store;
+  bp_cache* cache;
+  bp_planner* planner;
+  cudaStream_t compute, link;
+  std::vector<bp_prep*> preps;  // ring indexed by position
+  std::vector<bp::PlanSlot> plans;
+  std::vector<bp::ChunkSlot> chunks;
+  std::vector<bp::UploadSlot> uploads;
+  int next_plan;
+  int next_upload;
+  int32_t* slots_s;
+  int64_t* mark;
+  int64_t* stats;  // [2]
+  int64_t* h_result;  // pinned, [16]
+  uint64_t* d_keys_staging[2];
+  uint8_t* d_labels_staging[2];
+  cudaEvent_t staging_free[2];
+  int staging_i;
+  long long chunk_cap;
+};
+
+namespace bp {
+
+static int engine_prep_slot(bp_engine* e, long long pos) { return (int)(pos % (long long)e->preps.size()); }
+
+static void stage_begin(bp_engine* e, int stage, cudaStream_t s) {
+  if (!e->cfg.timing) return;
+  cudaEvent_t ev;
+  cudaEventCreate(&ev);
+  cudaEventRecord(ev, s);
+  e->timer.open[stage] = ev;
+}
+
+static void stage_end(bp_engine* e, int stage, cudaStream_t s) {
+  if (!e->cfg.timing || !e->timer.open[stage]) return;
+  cudaEvent_t ev;
+  cudaEventCreate(&ev);
+  cudaEventRecord(ev, s);
+  e->timer.spans[stage].emplace_back(e->timer.open[stage], ev);
+  e->timer.open[stage] = nullptr;
+}
+
+}  // namespace bp
+
+// Sum of the recorded stage spans (ms) and their counts since the last call;
+// synchronises the device, then clears the record.
+extern "C" int bp_engine_stage_times(bp_engine* e, double* h_ms, int64_t* h_counts) {
+  BP_CUDA_TRY(cudaDeviceSynchronize());
+  for (int st = 0; st < bp::kNumStages; ++st) {
+    double total = 0;
+    for (auto& pr : e->timer.spans[st]) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pr.first, pr.second);
+      total += ms;
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    h_ms[st] = total;
+    h_counts[st] = (int64_t)e->timer.spans[st].size();
+    e->timer.spans[st].clear();
+  }
+  return BP_OK;
+}
+
+extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engine_config* cfg, bp_engine** out) {
+  using namespace bp;
+  if (!sc || cfg->capacity < 1 || cfg->dim != sc->emb_dim || cfg->max_occ < 1 || cfg->plan_slots < 2 ||
+      cfg->chunk_slots < 2 || cfg->prep_slots < 2)
+    return BP_ERR_INVALID;
+  bp_engine* e = new bp_engine();
+  e->ctx = ctx;
+  e->sc = sc;
+  e->cfg = *cfg;
+  int lo = 0, hi = 0;
+  BP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  // Compute at the highest priority: the host-link kernels only wait on PCIe
+  // and must not delay the critical path's CTAs.
+  BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->compute, cudaStreamNonBlocking, hi));
+  BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->link, cudaStreamNonBlocking, lo));
+  int rc = bp_store_create(ctx, sc, cfg->seed, e->compute, &e->store);
+  if (rc) return rc;
+  rc = bp_cache_create(ctx, sc, cfg->capacity, cfg->dim, &e->cache);
+  if (rc) return rc;
+  rc = bp_planner_create(ctx, sc, cfg->capacity, &e->planner);
+  if (rc) return rc;
+  const long long n = cfg->max_occ;
+  const int dim = cfg->dim;
+  e->preps.assign(cfg->prep_slots, nullptr);
+  e->plans.resize(cfg->plan_slots);
+  for (auto& p : e->plans) {
+    BP_CUDA_TRY(cudaMalloc(&p.keys, n * sizeof(uint64_t)));
+    BP_CUDA_TRY(cudaMalloc(&p.ids, n * sizeof(uint32_t)));
+    BP_CUDA_TRY(cudaMalloc(&p.ttls, n * sizeof(int64_t)));
+    BP_CUDA_TRY(cudaMalloc(&p.ttl_k, n * sizeof(int64_t)));
+    BP_CUDA_TRY(cudaMalloc(&p.evict_keys, n * sizeof(uint64_t)));
+    BP_CUDA_TRY(cudaMalloc(&p.counts, 4 * sizeof(int64_t)));
+    BP_CUDA_TRY(cudaMallocHost(&p.h_counts, 4 * sizeof(int64_t)));
+    BP_CUDA_TRY(cudaMalloc(&p.staging, n * dim * sizeof(float)));
+    BP_CUDA_TRY(cudaMalloc(&p.n_ins, sizeof(int64_t)));
+    BP_CUDA_TRY(cudaEventCreateWithFlags(&p.popped, cudaEventDisableTiming));
+    BP_CUDA_TRY(cudaEventCreateWithFlags(&p.fetched, cudaEventDisableTiming));
+    BP_CUDA_TRY(cudaEventCreateWithFlags(&p.consumed, cudaEventDisableTiming));
+    BP_CUDA_TRY(cudaEventRecord(p.consumed, e->compute));
+    p.prep_pos = -1;
+  }
+  e->chunk_cap = cfg->capacity < n ? cfg->capacity : n;
+  const long long cc = cfg->capacity;  // a drain may return every resident entry
+  e->chunks.resize(cfg->chunk_slots);
+  for (auto& c : e->chunks) {
+    BP_CUDA_TRY(cudaMalloc(&c.keys, cc * sizeof(uint64_t)));
+    BP_CUDA_TRY(cudaMalloc(&c.ids, cc * sizeof(uint32_t)));
+    BP_CUDA_TRY(cudaMalloc(&c.rows, cc * dim * sizeof(float)));
+    BP_CUDA_TRY(cudaMalloc(&c.dirty, cc));
+    BP_CUDA_TRY(cudaMalloc(&c.count, 2 * sizeof(int64_t)));
+    BP_CUDA_TRY(cudaEventCreateWithFlags(&c.flushed, cudaEventDisableTiming));
+    BP_CUDA_TRY(cudaEventRecord(c.flushed, e->link));
+    c.pending = false;
+  }
+  e->uploads.resize(4);
+  for (auto& u : e->uploads) {
+    u.bytes = (size_t)n * 9 + 64;
+    BP_CUDA_TRY(cudaMallocHost(&u.host, u.bytes));
+    BP_CUDA_TRY(cudaEventCreateWithFlags(&u.done, cudaEventDisableTiming));
+    u.used = false;
+  }
+  for (int i = 0; i < 2; ++i) {
+    BP_CUDA_TRY(cudaMalloc(&e->d_keys_staging[i], n * sizeof(uint64_t)));
+    BP_CUDA_TRY(cudaMalloc(&e->d_labels_staging[i], n + 16));
+    BP_CUDA_TRY(cudaEventCreateWithFlags(&e->staging_free[i], cudaEventDisableTiming));
+    BP_CUDA_TRY(cudaEventRecord(e->staging_free[i], e->compute));
+  }
+  e->staging_i = 0;
+  e->next_plan = 0;
+  e->next_upload = 0;
+  BP_CUDA_TRY(cudaMalloc(&e->slots_s, n * sizeof(int32_t)));
+  BP_CUDA_TRY(cudaMalloc(&e->mark, sc->total_rows * sizeof(int64_t)));
+  BP_CUDA_TRY(cudaMemsetAsync(e->mark, 0xC0, sc->total_rows * sizeof(int64_t), e->compute));  // never a tag
+  BP_CUDA_TRY(cudaMalloc(&e->stats, 2 * sizeof(int64_t)));
+  BP_CUDA_TRY(cudaMallocHost(&e->h_result, 16 * sizeof(int64_t)));
+  BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
+  *out = e;
+  return BP_OK;
+}
+
+extern "C" int bp_engine_destroy(bp_engine* e) {
+  if (!e) return BP_OK;
+  cudaDeviceSynchronize();
+  for (auto* p : e->preps)
+    if (p) bp_prep_destroy(p);
+  for (auto& p : e->plans) {
+    cudaFree(p.keys);
+    cudaFree(p.ids);
+    cudaFree(p.ttls);
+    cudaFree(p.ttl_k);
+    cudaFree(p.evict_keys);
+    cudaFree(p.counts);
+    cudaFreeHost(p.h_counts);
+    cudaFree(p.staging);
+    cudaFree(p.n_ins);
+    cudaEventDestroy(p.popped);
+    cudaEventDestroy(p.fetched);
+    cudaEventDestroy(p.consumed);
+  }
+  for (auto& c : e->chunks) {
+    cudaFree(c.keys);
+    cudaFree(c.ids);
+    cudaFree(c.rows);
+    cudaFree(c.dirty);
+    cudaFree(c.count);
+    cudaEventDestroy(c.flushed);
+  }
+  for (auto& u : e->uploads) {
+    cudaFreeHost(u.host);
+    cudaEventDestroy(u.done);
+  }
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(e->d_keys_staging[i]);
+    cudaFree(e->d_labels_staging[i]);
+    cudaEventDestroy(e->staging_free[i]);
+  }
+  cudaFree(e->slots_s);
+  cudaFree(e->mark);
+  cudaFree(e->stats);
+  cudaFreeHost(e->h_result);
+  bp_planner_destroy(e->planner);
+  bp_cache_destroy(e->cache);
+  bp_store_destroy(e->store);
+  cudaStreamDestroy(e->compute);
+  cudaStreamDestroy(e->link);
+  delete e;
+  return BP_OK;
+}
+
+extern "C" int bp_engine_parts(bp_engine* e, bp_engine_parts_t* out) {
+  out->store = e->store;
+  out->cache = e->cache;
+  out->planner = e->planner;
+  out->compute_stream = e->compute;
+  out->link_stream = e->link;
+  return BP_OK;
+}
+
+// Batch entering the window: upload (host keys go through a pinned ring and
+// one H2D copy each for keys and labels) and device prep on the compute stream.
+extern "C" int bp_engine_add_batch(bp_engine* e, int64_t pos, int64_t iteration, const uint64_t* keys,
+                                   const uint8_t* labels, int64_t n_occ, const int64_t* h_rank_bounds,
+                                   int32_t num_ranks, int32_t keys_on_host) {
+  using namespace bp;
+  if (n_occ > e->cfg.max_occ) return BP_ERR_INVALID;
+  const int slot = engine_prep_slot(e, pos);
+  if (e->preps[slot]) {
+    bp_prep_destroy(e->preps[slot]);
+    e->preps[slot] = nullptr;
+  }
+  const uint64_t* d_keys = keys;
+  const uint8_t* d_labels = labels;
+  if (keys_on_host && n_occ > 0) {
+    UploadSlot& u = e->uploads[e->next_upload];
+    e->next_upload = (e->next_upload + 1) % (int)e->uploads.size();
+    if (u.used) BP_CUDA_TRY(cudaEventSynchronize(u.done));
+    std::memcpy(u.host, keys, n_occ * sizeof(uint64_t));
+    std::memcpy(u.host + n_occ * sizeof(uint64_t), labels, n_occ);
+    const int si = e->staging_i;
+    e->staging_i ^= 1;
+    BP_CUDA_TRY(cudaStreamWaitEvent(e->compute, e->staging_free[si], 0));
+    BP_CUDA_TRY(cudaMemcpyAsync(e->d_keys_staging[si], u.host, n_occ * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                e->compute));
+    BP_CUDA_TRY(cudaMemcpyAsync(e->d_labels_staging[si], u.host + n_occ * sizeof(uint64_t), n_occ,
+                                cudaMemcpyHostToDevice, e->compute));
+    BP_CUDA_TRY(cudaEventRecord(u.done, e->compute));
+    u.used = true;
+    d_keys = e->d_keys_staging[si];
+    d_labels = e->d_labels_staging[si];
+    stage_begin(e, kStagePrep, e->compute);
+    int rc = bp_prep_create(e->ctx, e->sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, 0, 0, 0,
+                            e->compute, &e->preps[slot]);
+    stage_end(e, kStagePrep, e->compute);
+    if (rc) return rc;
+    BP_CUDA_TRY(cudaEventRecord(e->staging_free[si], e->compute));  // prep consumed the staging copy
+    return BP_OK;
+  }
+  stage_begin(e, kStagePrep, e->compute);
+  const int rc = bp_prep_create(e->ctx, e->sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, 0, 0,
+                                0, e->compute, &e->preps[slot]);
+  stage_end(e, kStagePrep, e->compute);
+  return rc;
+}
+
+extern "C" int bp_engine_prep(bp_engine* e, int64_t pos, bp_prep** out) {
+  *out = e->preps[bp::engine_prep_slot(e, pos)];
+  return *out ? BP_OK : BP_ERR_ENGINE;
+}
+
+extern "C" int bp_engine_release_batch(bp_engine* e, int64_t pos) {
+  const int slot = bp::engine_prep_slot(e, pos);
+  if (e->preps[slot] && e->preps[slot]->iteration >= 0) {
+    bp_prep_destroy(e->preps[slot]);  // stream-ordered free on the compute stream
+    e->preps[slot] = nullptr;
+  }
+  return BP_OK;
+}
+
+extern "C" int bp_engine_refill(bp_engine* e, int64_t pos) {
+  bp_prep* P = e->preps[bp::engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  bp::stage_begin(e, bp::kStagePlanner, e->compute);
+  const int rc = bp_planner_refill(e->planner, P, e->compute);
+  bp::stage_end(e, bp::kStagePlanner, e->compute);
+  return rc;
+}
+
+// Pop the planner window for the batch at ``pos`` into the next plan slot.
+extern "C" int bp_engine_pop(bp_engine* e, int64_t pos, int32_t* slot_out) {
+  using namespace bp;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  const int slot = e->next_plan;
+  e->next_plan = (e->next_plan + 1) % (int)e->plans.size();
+  PlanSlot& ps = e->plans[slot];
+  // The slot's previous plan must have been consumed by training.
+  BP_CUDA_TRY(cudaStreamWaitEvent(e->compute, ps.consumed, 0));
+  bp_plan_buffers b{ps.keys, ps.ids, ps.ttls, ps.ttl_k, ps.evict_keys, ps.counts};
+  stage_begin(e, kStagePlanner, e->compute);
+  int rc = bp_planner_pop(e->planner, P, &b, e->compute);
+  stage_end(e, kStagePlanner, e->compute);
+  if (rc) return rc;
+  BP_CUDA_TRY(cudaMemcpyAsync(ps.h_counts, ps.counts, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, e->compute));
+  BP_CUDA_TRY(cudaEventRecord(ps.popped, e->compute));
+  ps.prep_pos = pos;
+  *slot_out = slot;
+  return BP_OK;
+}
+
+// Host copy of a plan slot's counters (n_prefetch, n_evict, projected,
+// resident_before); waits for that pop only.
+extern "C" int bp_engine_plan_counts(bp_engine* e, int32_t slot, int64_t* out4) {
+  bp::PlanSlot& ps = e->plans[slot];
+  BP_CUDA_TRY(cudaEventSynchronize(ps.popped));
+  std::memcpy(out4, ps.h_counts, 4 * sizeof(int64_t));
+  return BP_OK;
+}
+
+extern "C" int bp_engine_plan_view(bp_engine* e, int32_t slot, bp_plan_buffers* out, float** staging) {
+  bp::PlanSlot& ps = e->plans[slot];
+  *out = bp_plan_buffers{ps.keys, ps.ids, ps.ttls, ps.ttl_k, ps.evict_keys, ps.counts};
+  if (staging) *staging = ps.staging;
+  return BP_OK;
+}
+
+// Prefetch of a plan on the link stream: zero-copy gather of its rows from
+// the pinned store, after the plan's pop and after every earlier write-back
+// issued on the same stream (the gate).
+extern "C" int bp_engine_fetch(bp_engine* e, int32_t slot) {
+  bp::PlanSlot& ps = e->plans[slot];
+  BP_CUDA_TRY(cudaStreamWaitEvent(e->link, ps.popped, 0));
+  bp::stage_begin(e, bp::kStageFetch, e->link);
+  int rc = bp_store_fetch(e->store, ps.ids, e->cfg.max_occ, ps.counts, ps.staging, e->link);
+  bp::stage_end(e, bp::kStageFetch, e->link);
+  if (rc) return rc;
+  BP_CUDA_TRY(cudaEventRecord(ps.fetched, e->link));
+  return BP_OK;
+}
+
+// Dirty write-back of chunk slots, in order (last write wins), on the link stream.
+extern "C" int bp_engine_flush(bp_engine* e, const int32_t* chunk_slots, int32_t n) {
+  bp::stage_begin(e, bp::kStageFlush, e->link);
+  for (int i = 0; i < n; ++i) {
+    bp::ChunkSlot& c = e->chunks[chunk_slots[i]];
+    int rc = bp_store_write_masked(e->store, c.ids, c.rows, c.dirty, e->cfg.capacity, c.count, e->link);
+    if (rc) return rc;
+    BP_CUDA_TRY(cudaEventRecord(c.flushed, e->link));
+    c.pending = false;
+  }
+  bp::stage_end(e, bp::kStageFlush, e->link);
+  return BP_OK;
+}
+
+// One training iteration on the compute stream (reference engine.py:525-606):
+// apply the staged prefetch (insert, minus an optional dropped first key),
+// TTL updates + lookup, next-batch stamp, fused trainer, eviction of
+// ttl <= iteration into ``chunk_slot`` (and a full drain into
+// ``drain_slot`` on the last iteration).  Synchronises the compute stream
+// once and fills ``out``; device contract violations come back in out->err.
+extern "C" int bp_engine_train(bp_engine* e, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
+                               int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out) {
+  using namespace bp;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  PlanSlot& ps = e->plans[plan_slot];
+  cudaStream_t s = e->compute;
+  const int dim = e->cfg.dim;
+  BP_CUDA_TRY(cudaStreamWaitEvent(s, ps.fetched, 0));
+  stage_begin(e, kStageApply, s);
+  const int off = has_skip ? 1 : 0;
+  k_offset_count<<<1, 1, 0, s>>>(ps.counts, off, ps.n_ins);
+  int rc = bp_cache_insert(e->cache, ps.keys + off, ps.ids + off, ps.staging + (size_t)off * dim, ps.ttls + off,
+                           e->cfg.max_occ - off, ps.n_ins, P->iteration, s);
+  if (rc) return rc;
+  rc = bp_cache_apply_resolve(e->cache, P, ps.ttl_k, skip_key, has_skip, e->slots_s, s);
+  if (rc) return rc;
+  bp_prep* N = next_pos >= 0 ? e->preps[engine_prep_slot(e, next_pos)] : nullptr;
+  if (N) {
+    rc = bp_mark_ids(N, e->mark, N->iteration, s);
+    if (rc) return rc;
+  }
+  BP_CUDA_TRY(cudaMemsetAsync(e->stats, 0, 2 * sizeof(int64_t), s));
+  stage_end(e, kStageApply, s);
+  bp_cache_view cv;
+  bp_cache_get_view(e->cache, &cv);
+  stage_begin(e, kStageTrainer, s);
+  rc = bp_stub_step(e->ctx, P, cv.d_values, e->slots_s, cv.d_dirty, dim, e->cfg.c_value, e->cfg.c_label, e->cfg.lr,
+                    BP_STUB_SGD, nullptr, N ? e->mark : nullptr, N ? N->iteration : 0, e->stats, s);
+  stage_end(e, kStageTrainer, s);
+  if (rc) return rc;
+  BP_CUDA_TRY(cudaEventRecord(ps.consumed, s));
+  ChunkSlot& c = e->chunks[chunk_slot];
+  BP_CUDA_TRY(cudaStreamWaitEvent(s, c.flushed, 0));  // its previous contents are durable
+  bp_evict_buffers eb{e->cfg.record_keys ? c.keys : nullptr, c.ids, c.rows, c.dirty, c.count};
+  stage_begin(e, kStageEvict, s);
+  rc = bp_cache_evict(e->cache, P->iteration, 0, &eb, e->chunk_cap, s);
+  stage_end(e, kStageEvict, s);
+  if (rc) return rc;
+  c.pending = true;
+  int64_t* h = e->h_result;
+  BP_CUDA_TRY(cudaMemcpyAsync(h + 0, P->d_num_unique, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  BP_CUDA_TRY(cudaMemcpyAsync(h + 1, ps.n_ins, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  BP_CUDA_TRY(cudaMemcpyAsync(h + 2, e->stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  BP_CUDA_TRY(cudaMemcpyAsync(h + 4, c.count, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  h[6] = h[7] = 0;
+  if (drain_slot >= 0) {
+    ChunkSlot& d = e->chunks[drain_slot];
+    BP_CUDA_TRY(cudaStreamWaitEvent(s, d.flushed, 0));
+    bp_evict_buffers db{e->cfg.record_keys ? d.keys : nullptr, d.ids, d.rows, d.dirty, d.count};
+    rc = bp_cache_evict(e->cache, P->iteration, 1, &db, e->cfg.capacity, s);
+    if (rc) return rc;
+    d.pending = true;
+    BP_CUDA_TRY(cudaMemcpyAsync(h + 6, d.count, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  }
+  bp_error_t err;
+  bp_ctx_check(e->ctx, s, &err);  // synchronises the compute stream
+  out->unique = h[0];
+  out->inserted = h[1];
+  out->critical = h[2];
+  out->dirty_keys = h[3];
+  out->evicted = h[4];
+  out->evicted_dirty = h[5];
+  out->drained = h[6];
+  out->drained_dirty = h[7];
+  out->err = err;
+  return BP_OK;
+}
+
+// Evicted keys of a chunk (device -> host), for event logs.
+extern "C" int bp_engine_chunk_keys(bp_engine* e, int32_t chunk_slot, uint64_t* h_out, int64_t n) {
+  if (n <= 0) return BP_OK;
+  if (!e->cfg.record_keys) return BP_ERR_INVALID;
+  BP_CUDA_TRY(cudaMemcpy(h_out, e->chunks[chunk_slot].keys, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return BP_OK;
+}
+
+extern "C" int bp_engine_chunk_view(bp_engine* e, int32_t chunk_slot, bp_evict_buffers* out) {
+  bp::ChunkSlot& c = e->chunks[chunk_slot];
+  *out = bp_evict_buffers{c.keys, c.ids, c.rows, c.dirty, c.count};
+  return BP_OK;
+}
+
+extern "C" int bp_engine_sync(bp_engine* e) {
+  BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
+  BP_CUDA_TRY(cudaStreamSynchronize(e->link));
+  return BP_OK;
+}

@@ -38,10 +38,9 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .cache import DynamicCache
-from .device import DevicePrep, Uploader
+from .device import DevicePrep, DeviceSchema, _wrap_device
 from .errors import CacheCapacityError, ConfigurationError, EngineError, IncomparableRunsError
-from .lookahead import CachePlan, DevicePlan, adapt_on_pressure, auto_lookahead, new_state
+from .lookahead import auto_lookahead, planner_dump
 from .report import IterationRecord, RunReport
 from .store import ShardedStore
 from .trainer import BP_STUB_SGD, StubModelConfig, f32
@@ -152,45 +151,32 @@ _METADATA = {
 }
 
 
-class _Chunk:
-    """Evictions of one iteration, still in HBM, awaiting a flush."""
+class _Plan:
+    """One emitted plan living in a native plan slot."""
 
-    __slots__ = ("ids", "rows", "dirty", "count", "n", "n_dirty", "keys")
+    __slots__ = ("iteration", "lookahead", "slot", "pos", "_counts")
 
-    def __init__(self, ids, rows, dirty, count, keys=None):
-        self.ids, self.rows, self.dirty, self.count, self.keys = ids, rows, dirty, count, keys
-        self.n = self.n_dirty = 0
-
-
-class _PendingPlan:
-    """An emitted plan whose device counters are read lazily (the next host
-    synchronisation makes them final), so emission never blocks the host."""
-
-    __slots__ = ("plan", "h_counts", "done")
-
-    def __init__(self, plan, stream):
-        self.plan = plan
-        self.h_counts = torch.empty(4, dtype=torch.int64, pin_memory=True)
-        self.h_counts.copy_(plan.device.counts, non_blocking=True)
-        self.done = torch.cuda.Event()
-        self.done.record(stream)
-
-    def counts(self):
-        if not self.done.query():
-            self.done.synchronize()
-        return self.h_counts
+    def __init__(self, iteration, lookahead, slot, pos):
+        self.iteration, self.lookahead, self.slot, self.pos = iteration, lookahead, slot, pos
+        self._counts = None
 
 
 class _Pipeline:
-    """One pipelined run (reference engine.py:239-649) driving the GPU.
+    """One pipelined run (reference engine.py:239-649) on the native engine.
 
-    ``begin`` / ``step(pos)`` / ``end`` split the reference's run loop so a
-    benchmark can time single iterations.  Each step enqueues its kernels
-    with device-side counts and synchronises exactly once, at the end, to
-    read the counters the simulated clock, the gate and the report need.
+    The host keeps the reference's scalar control flow -- window refill,
+    lazy pressure halving, dispatch gate, forced / boundary / final flushes,
+    round-robin flusher, simulated clock, records -- and drives the native
+    runtime (``csrc/engine.cu``) a few coarse calls per iteration:
+    add_batch / refill / pop (planner), fetch (link stream), train (one
+    synchronisation), flush (link stream).  ``begin`` / ``step(pos)`` /
+    ``end`` split the reference's loop so a benchmark can time iterations.
     """
 
-    def __init__(self, cfg: EngineConfig, schema: Schema, batches: list, fingerprint, fault, device_inputs=None):
+    STAGES = ("prep", "planner", "fetch", "apply", "trainer", "evict", "flush")
+
+    def __init__(self, cfg: EngineConfig, schema: Schema, batches: list, fingerprint, fault, device_inputs=None,
+                 timing: bool = False):
         if fault not in (None, FAULT_NO_GATE, FAULT_DROP_PREFETCH):
             raise ConfigurationError(f"unknown fault {fault!r}")
         self.cfg, self.schema, self.batches = cfg, schema, batches
@@ -198,30 +184,39 @@ class _Pipeline:
         self.base = batches[0].iteration
         self.n = len(batches)
         self.T = cfg.num_trainers
-        self.stream = torch.cuda.current_stream()
-        # Host-link traffic (prefetch gathers, write-back scatters) runs on its
-        # own stream so it overlaps the compute of the current iteration; the
-        # gate order of reference engine.py:302-377 is kept by issuing both in
-        # dispatch order on that one stream, fenced by events.
-        self.link = torch.cuda.Stream()
         self.device_inputs = device_inputs  # optional {pos: (d_keys, d_labels)} already in HBM
-        self._preps: dict = {}
-        self._uploader = None
+        self.probe = None
+        self.lib = L.lib()
         stub = cfg.stub()
-        self.c_value, self.c_label, self.lr = f32(stub.c_value), f32(stub.c_label), f32(stub.lr)
-        self.probe = None  # optional callable(name, phase) for kernel timing
 
-        self.L0 = cfg.lookahead or auto_lookahead(iter(batches), cfg.cache_capacity, schema=schema,
-                                                  prep_provider=self._prep_of_batch)
+        self.L0 = cfg.lookahead or auto_lookahead(iter(batches), cfg.cache_capacity, schema=schema)
         self.flush_interval = max(1, math.ceil(cfg.rpc_batch_proportion * self.L0))
-        self.store = ShardedStore(schema, cfg.num_shards, cfg.seed)
-        self.cache = DynamicCache(cfg.cache_capacity, schema.emb_dim, schema=schema)
+        max_occ = max(1, max(int(b.packed_occurrences()[0].size) for b in batches))
+        ec = L.EngineConfig(capacity=cfg.cache_capacity, max_occ=max_occ, seed=cfg.seed & 0xFFFFFFFFFFFFFFFF,
+                            dim=schema.emb_dim, num_ranks=self.T, c_value=f32(stub.c_value),
+                            c_label=f32(stub.c_label), lr=f32(stub.lr),
+                            record_keys=1 if (cfg.record_events or fault == FAULT_NO_GATE) else 0,
+                            plan_slots=self.L0 + 4, chunk_slots=self.flush_interval + 4,
+                            prep_slots=2 * self.L0 + 8, timing=1 if timing else 0)
+        h = C.c_void_p()
+        L.check(self.lib.bp_engine_create(L.Context.get().handle, DeviceSchema.get(schema).handle, C.byref(ec),
+                                          C.byref(h)), "bp_engine_create")
+        self.eng = h
+        parts = L.EngineParts()
+        self.lib.bp_engine_parts(h, C.byref(parts))
+        self.parts = parts
+        self.stream = torch.cuda.ExternalStream(parts.compute_stream)
+        self.link = torch.cuda.ExternalStream(parts.link_stream)
+        self.store = ShardedStore(schema, cfg.num_shards, cfg.seed, _handle=parts.store, _owner=self)
         self.occupancy = 0
-        self.state = new_state(self.L0, cfg.cache_capacity, schema=schema, num_ranks=self.T,
-                               prep_provider=self._prep_of_batch)
-        self.source = iter(batches)
+        self.lookahead = self.L0
+        self.queue: deque = deque()  # positions of the planner window
+        self.source_pos = 0
+        self.added: set = set()
         self.snapshots = {} if cfg.check_mirror else None
         self._adapt_pending = None
+        self.free_chunks = list(range(self.flush_interval + 4))
+        self.free_plans = set(range(self.L0 + 4))
 
         self.pending: deque = deque()
         self.exhausted = False
@@ -243,63 +238,82 @@ class _Pipeline:
         self.total_prefetched = 0
         self.peak_occupancy = 0
         self.drop_done = False
-        self.stats = torch.zeros(2, dtype=torch.int64, device="cuda")
-        # dense per-row stamp of the next batch's keys (critical-set test)
-        self.mark = torch.full((schema.total_rows,), -(1 << 62), dtype=torch.int64, device="cuda")
-        self.h_step = torch.zeros(8, dtype=torch.int64, pin_memory=True)
-        self.kernel_launches = 0
+        self.result = L.StepResult()
 
-    # -- batch preps (device) ------------------------------------------------------
-    def _prep_of_batch(self, batch: Batch) -> DevicePrep:
-        pos = batch.iteration - self.base
-        prep = self._preps.get(pos)
-        if prep is None:
-            dev = self.device_inputs.get(pos) if self.device_inputs else None
-            if dev is not None:
-                keys, labels = dev
-                n = keys.numel()
-                prep = DevicePrep(None, None, batch.rank_bounds(self.T), batch.iteration, self.schema,
-                                  stream=self.stream, d_keys=keys, d_labels=labels)
-            else:
-                if self._uploader is None:
-                    occ = batch.packed_occurrences()[0].size
-                    self._uploader = Uploader(max(1 << 20, 16 * occ), slots=8)
-                prep = DevicePrep.from_batch(batch, self.T, self.schema, stream=self.stream, uploader=self._uploader)
-            self._preps[pos] = prep
-        return prep
+    def stage_times(self) -> dict:
+        """{stage: (total ms, launches)} since the last call (timing=True)."""
+        ms = np.zeros(7, dtype=np.float64)
+        cnt = np.zeros(7, dtype=np.int64)
+        L.check(self.lib.bp_engine_stage_times(self.eng, ms.ctypes.data, cnt.ctypes.data), "bp_engine_stage_times")
+        return {name: (float(m), int(c)) for name, m, c in zip(self.STAGES, ms, cnt)}
 
-    def _prep(self, pos: int) -> DevicePrep:
-        return self._prep_of_batch(self.batches[pos])
+    def __del__(self):
+        try:
+            if getattr(self, "eng", None):
+                self.lib.bp_engine_destroy(self.eng)
+                self.eng = None
+        except Exception:
+            pass
+
+    # -- batches ---------------------------------------------------------------------
+    def _add(self, pos: int) -> None:
+        if pos in self.added:
+            return
+        b = self.batches[pos]
+        keys, labels, _ = b.packed_occurrences()
+        rb = np.ascontiguousarray(b.rank_bounds(self.T), dtype=np.int64)
+        dev = self.device_inputs.get(pos) if self.device_inputs else None
+        if dev is not None:
+            k, lab = dev
+            rc = self.lib.bp_engine_add_batch(self.eng, pos, b.iteration, L.ptr(k), L.ptr(lab), k.numel(),
+                                              rb.ctypes.data, self.T, 0)
+        else:
+            keys = np.ascontiguousarray(keys, dtype=np.uint64)
+            labels = np.ascontiguousarray(labels, dtype=np.uint8)
+            rc = self.lib.bp_engine_add_batch(self.eng, pos, b.iteration, keys.ctypes.data, labels.ctypes.data,
+                                              keys.size, rb.ctypes.data, self.T, 1)
+        L.check(rc, "bp_engine_add_batch")
+        self.added.add(pos)
+
+    def _release(self, pos: int) -> None:
+        if pos in self.added:
+            self.lib.bp_engine_release_batch(self.eng, pos)
+            self.added.discard(pos)
 
     # -- plan emission (reference engine.py:198-236, lookahead.py:64-123) --------
+    def _plan_counts(self, plan: _Plan):
+        if plan._counts is None:
+            out = np.zeros(4, dtype=np.int64)
+            L.check(self.lib.bp_engine_plan_counts(self.eng, plan.slot, out.ctypes.data), "bp_engine_plan_counts")
+            plan._counts = out
+        return plan._counts
+
     def _next_plan(self):
-        st = self.state
         if self._adapt_pending is not None:
-            # The reference adapts lazily, when the next plan is requested.
-            st.projected_occupancy = int(self._adapt_pending.counts()[2])
-            adapt_on_pressure(st)
+            # the reference adapts lazily, when the next plan is requested
+            projected = int(self._plan_counts(self._adapt_pending)[2])
+            if projected > self.cfg.cache_capacity and self.lookahead > 1:
+                self.lookahead = max(1, self.lookahead // 2)
             self._adapt_pending = None
-        lib = L.lib()
-        sp = L.stream_ptr(self.stream)
-        while len(st.batch_queue) < st.lookahead:
-            batch = next(self.source, None)
-            if batch is None:
-                break
-            prep = self._prep_of_batch(batch)
-            st.batch_queue.append(batch)
-            st._preps.append(prep)
-            L.check(lib.bp_planner_refill(st.handle, prep.handle, sp), "bp_planner_refill")
-        if not st.batch_queue:
+        while len(self.queue) < self.lookahead and self.source_pos < self.n:
+            pos = self.source_pos
+            self.source_pos += 1
+            self._add(pos)
+            L.check(self.lib.bp_engine_refill(self.eng, pos), "bp_engine_refill")
+            self.queue.append(pos)
+        if not self.queue:
             return None
-        batch = st.batch_queue.popleft()
-        prep = st._preps.popleft()
-        dev = DevicePlan(prep, exact=False)
-        L.check(lib.bp_planner_pop(st.handle, prep.handle, C.byref(dev.buffers()), sp), "bp_planner_pop")
-        plan = CachePlan(batch.iteration, None, None, st.lookahead, device=dev)
-        self._adapt_pending = _PendingPlan(plan, self.stream)
-        dev.h_pending = self._adapt_pending
+        pos = self.queue.popleft()
+        slot = C.c_int32()
+        L.check(self.lib.bp_engine_pop(self.eng, pos, C.byref(slot)), "bp_engine_pop")
+        if slot.value not in self.free_plans:
+            raise EngineError("plan ring overrun")
+        self.free_plans.discard(slot.value)
+        plan = _Plan(self.batches[pos].iteration, self.lookahead, slot.value, pos)
+        self._adapt_pending = plan
         if self.snapshots is not None:
-            self.snapshots[plan.iteration - self.base] = st.mirror_keys_u64()
+            keys, _, flags = planner_dump(self.parts.planner, self.stream)
+            self.snapshots[pos] = np.sort(keys[(flags & 2) != 0])
         return plan
 
     def _dispatch_pos(self, plan) -> int:
@@ -322,16 +336,8 @@ class _Pipeline:
             self._flush("forced", cur)
             self.forced_flushes += 1
         arrival = self._gate_time(theta) + self.cfg.fetch_latency
-        dev = plan.device
-        self.link.wait_event(dev.h_pending.done)  # the plan's pop has run
-        self._probe("store_fetch", 0, self.link)
-        rows = self.store.fetch_ids_async(dev.prefetch_ids, dev.cap, d_n=dev.counts[0:1], stream=self.link)
-        self._probe("store_fetch", 1, self.link)
-        for t in (rows, dev.prefetch_ids, dev.counts):
-            t.record_stream(self.link)
-        fetched = torch.cuda.Event()
-        fetched.record(self.link)
-        self.staged[plan.iteration - self.base] = (plan, rows, arrival, fetched)
+        L.check(self.lib.bp_engine_fetch(self.eng, plan.slot), "bp_engine_fetch")
+        self.staged[plan.iteration - self.base] = (plan, arrival)
 
     def _dispatch_until(self, cur: int) -> None:
         while True:
@@ -349,24 +355,15 @@ class _Pipeline:
             self.pending.popleft()
             self._dispatch(plan, cur)
 
-    def _probe(self, name: str, phase: int, stream=None) -> None:
-        if self.probe is not None:
-            self.probe(name, phase, stream or self.stream)
-
     # -- write-back (reference engine.py:350-377) ---------------------------------
     def _flush(self, kind: str, pos: int) -> None:
         flusher = self.flush_counter % self.T
         count = 0
         if self.chunks:
-            # Chunks were produced on the compute stream, which the host has
-            # synchronised since; the scatter runs on the link stream.
-            self._probe("store_write", 0, self.link)
-            for ch in self.chunks:  # in eviction order: the last write wins
-                self.store.write_ids_async(ch.ids, ch.rows, ch.n, d_mask=ch.dirty, stream=self.link)
-                for t in (ch.ids, ch.rows, ch.dirty):
-                    t.record_stream(self.link)
-            self._probe("store_write", 1, self.link)
+            slots = np.asarray([c[0] for c in self.chunks], dtype=np.int32)
+            L.check(self.lib.bp_engine_flush(self.eng, slots.ctypes.data, len(slots)), "bp_engine_flush")
             count = self._merged_count()
+            self.free_chunks.extend(int(s) for s in slots)
             self.store.write_calls += 1
             self.store.entries_written += count
         self.event_starts.append(self.flushed_through + 1)
@@ -382,43 +379,41 @@ class _Pipeline:
             # Under the gate a key cannot be evicted twice within one flush
             # window (its re-prefetch waits for the flush of the first
             # eviction), so chunk key sets are disjoint.
-            return sum(ch.n_dirty for ch in self.chunks)
-        ids = [L.to_host(ch.ids, ch.n)[L.to_host(ch.dirty, ch.n).astype(bool)] for ch in self.chunks]
-        return int(np.unique(np.concatenate(ids)).size)
+            return sum(c[2] for c in self.chunks)
+        keys = [k[d] for k, d in (self._chunk_keys(c[0], c[1], with_dirty=True) for c in self.chunks)]
+        return int(np.unique(np.concatenate(keys)).size)
 
-    # -- per iteration ---------------------------------------------------------------
-    def _evict(self, completed: int, drain: bool, out_cap: int) -> _Chunk:
-        cap = max(1, out_cap)
-        dim = self.schema.emb_dim
-        ch = _Chunk(torch.empty(cap, dtype=torch.uint32, device="cuda"),
-                    torch.empty((cap, dim), dtype=torch.float32, device="cuda"),
-                    torch.empty(cap, dtype=torch.uint8, device="cuda"),
-                    torch.zeros(2, dtype=torch.int64, device="cuda"),
-                    torch.empty(cap, dtype=torch.uint64, device="cuda") if self.events is not None else None)
-        buf = L.EvictBuffers(L.ptr(ch.keys), L.ptr(ch.ids), L.ptr(ch.rows), L.ptr(ch.dirty), L.ptr(ch.count))
-        L.check(L.lib().bp_cache_evict(self.cache.handle, completed, 1 if drain else 0, C.byref(buf), cap,
-                                       L.stream_ptr(self.stream)), "bp_cache_evict")
-        return ch
+    def _chunk_keys(self, slot: int, n: int, with_dirty: bool = False):
+        keys = np.zeros(n, dtype=np.uint64)
+        L.check(self.lib.bp_engine_chunk_keys(self.eng, slot, keys.ctypes.data, n), "bp_engine_chunk_keys")
+        if not with_dirty:
+            return keys
+        view = L.EvictBuffers()
+        self.lib.bp_engine_chunk_view(self.eng, slot, C.byref(view))
+        dirty = L.to_host(_wrap_device(view.d_dirty, torch.uint8, max(n, 1)), n).astype(bool)
+        return keys, dirty
 
-    def _buffer(self, ch: _Chunk, iteration: int) -> None:
-        self.clean_evictions += ch.n - ch.n_dirty
-        self.dirty_evictions += ch.n_dirty
-        if ch.n_dirty:
-            self.chunks.append(ch)
+    def _buffer(self, slot: int, n: int, n_dirty: int, iteration: int) -> None:
+        self.clean_evictions += n - n_dirty
+        self.dirty_evictions += n_dirty
+        if n_dirty:
+            self.chunks.append((slot, n, n_dirty))
             if self.min_unflushed_ttl is None or iteration < self.min_unflushed_ttl:
                 self.min_unflushed_ttl = iteration
+        else:
+            self.free_chunks.append(slot)
 
-    def _sorted_keys(self, ch: _Chunk) -> list:
-        if ch.keys is None or ch.n == 0:
-            return []
-        return unpack_keys(np.sort(L.to_host(ch.keys, ch.n)))
+    def _take_chunk(self) -> int:
+        if not self.free_chunks:
+            raise EngineError("eviction chunk ring overrun")
+        return self.free_chunks.pop(0)
 
+    # -- per iteration ---------------------------------------------------------------
     def begin(self) -> None:
         self._dispatch_until(-1)
 
     def step(self, pos: int) -> None:
-        cfg, lib, ctx = self.cfg, L.lib(), L.Context.get()
-        sp = L.stream_ptr(self.stream)
+        cfg, lib = self.cfg, self.lib
         bw = cfg.sync_bandwidth
         batch = self.batches[pos]
         if pos > 0:
@@ -427,56 +422,35 @@ class _Pipeline:
         staged = self.staged.pop(pos, None)
         if staged is None:
             raise EngineError(f"no staged prefetch for position {pos}")
-        plan, rows, arrival, fetched = staged
+        plan, arrival = staged
         if plan.iteration != iteration:
             raise EngineError(f"plan {plan.iteration} misaligned with batch {iteration}")
-        dev = plan.device
-        prep = self._prep(pos)
-        self.stream.wait_event(fetched)
-        off, skip_key, has_skip = 0, 0, 0
-        if self.fault == FAULT_DROP_PREFETCH and not self.drop_done and pos >= self.n // 2 and dev.n_prefetch:
+        skip_key, has_skip = 0, 0
+        if self.fault == FAULT_DROP_PREFETCH and not self.drop_done and pos >= self.n // 2 \
+                and self._plan_counts(plan)[0]:
             # Drop the first (smallest) prefetched key: it is neither inserted
             # nor TTL-updated, so the lookup must miss (reference engine.py:512-523).
-            skip_key = int(L.to_host(dev.prefetch_keys, 1)[0])
-            has_skip, off = 1, 1
+            skip_key = int(self._plan_keys(plan, 1)[0])
+            has_skip = 1
             self.drop_done = True
-        dim = self.schema.emb_dim
-        # apply_prefetch: device count (minus the dropped key), device-side capacity check
-        if off:
-            n_ins_dev = dev.counts[0:1] - off
-        else:
-            n_ins_dev = dev.counts[0:1]
-        self._probe("cache_insert", 0)
-        L.check(lib.bp_cache_insert(
-            self.cache.handle, L.ptr(dev.prefetch_keys) + 8 * off, L.ptr(dev.prefetch_ids) + 4 * off,
-            L.ptr(rows) + 4 * dim * off, L.ptr(dev.prefetch_ttls) + 8 * off, max(dev.cap - off, 0),
-            L.ptr(n_ins_dev), iteration, sp), "bp_cache_insert")
-        slots = torch.empty(max(prep.n_occ, 1), dtype=torch.int32, device="cuda")
-        L.check(lib.bp_cache_apply_resolve(self.cache.handle, prep.handle, L.ptr(dev.ttl_k), skip_key, has_skip,
-                                           L.ptr(slots), sp), "bp_cache_apply_resolve")
-        self._probe("cache_insert", 1)
-        nxt = self._prep(pos + 1) if pos + 1 < self.n else None
-        if nxt is not None:
-            L.check(lib.bp_mark_ids(nxt.handle, L.ptr(self.mark), nxt.iteration, sp), "bp_mark_ids")
-        self.stats.zero_()
-        self._probe("stub_step", 0)
-        L.check(lib.bp_stub_step(ctx.handle, prep.handle, L.ptr(self.cache.values), L.ptr(slots),
-                                 L.ptr(self.cache.dirty), dim, self.c_value, self.c_label, self.lr, BP_STUB_SGD, None,
-                                 L.ptr(self.mark) if nxt is not None else None,
-                                 nxt.iteration if nxt is not None else 0, L.ptr(self.stats), sp), "bp_stub_step")
-        self._probe("stub_step", 1)
-        self._probe("cache_evict", 0)
-        ch = self._evict(iteration, False, min(cfg.cache_capacity, max(prep.n_occ, 1)))
-        self._probe("cache_evict", 1)
-        # one host synchronisation: counters for the clock, gate and report
-        h = self.h_step
-        h[0:1].copy_(prep.tensor("d_num_unique", torch.int64, 1), non_blocking=True)
-        h[1:2].copy_(n_ins_dev, non_blocking=True)
-        h[2:4].copy_(self.stats, non_blocking=True)
-        h[4:6].copy_(ch.count, non_blocking=True)
-        ctx.raise_pending(self.stream)
-        u, n_ins, crit_count, _, n_ev, n_ev_dirty = (int(v) for v in h[:6].tolist())
-        ch.n, ch.n_dirty = n_ev, n_ev_dirty
+        last = pos == self.n - 1
+        nxt = pos + 1 if pos + 1 < self.n else -1
+        if nxt >= 0:
+            self._add(nxt)
+        chunk = self._take_chunk()
+        drain = self._take_chunk() if last else -1
+        res = self.result
+        if self.probe is not None:
+            self.probe("train", 0, self.stream)
+        L.check(lib.bp_engine_train(self.eng, pos, plan.slot, nxt, skip_key, has_skip, chunk, drain,
+                                    C.byref(res)), "bp_engine_train")
+        if self.probe is not None:
+            self.probe("train", 1, self.stream)
+        if res.err.code:
+            L.raise_error_record(res.err)
+        self.free_plans.add(plan.slot)
+        u, n_ins, crit_count = int(res.unique), int(res.inserted), int(res.critical)
+        n_ev, n_ev_dirty = int(res.evicted), int(res.evicted_dirty)
         self.occupancy += n_ins
         occupancy_peak = self.occupancy
         self.occupancy -= n_ev
@@ -490,7 +464,7 @@ class _Pipeline:
         blocked_eviction = stall - blocked_prefetch
         compute_end = self.crit_end + stall + cfg.compute_latency
         if cfg.split_sync:
-            critical_size = crit_count if nxt is not None else 0
+            critical_size = crit_count if nxt >= 0 else 0
             background_size = u - critical_size
         else:
             critical_size, background_size = u, 0
@@ -506,18 +480,38 @@ class _Pipeline:
             "background_size": background_size, "lookahead": plan.lookahead,
         }
         if self.events is not None:
-            ttl = plan.ttl_updates
+            ttl = self._plan_ttls(plan)
+            pf = unpack_keys(self._plan_keys(plan, int(self._plan_counts(plan)[0])))
             if has_skip:
                 lost = unpack_key(skip_key)
                 ttl = [(k, t) for k, t in ttl if k != lost]
-            partial["prefetch_keys"] = list(plan.prefetch[off:])
-            partial["ttl_updates"] = list(ttl)
-        self._maintenance(pos, ch, partial)
-        self._preps.pop(pos, None)
+                pf = pf[1:]
+            partial["prefetch_keys"] = pf
+            partial["ttl_updates"] = ttl
+        self._maintenance(pos, chunk, n_ev, n_ev_dirty, drain, int(res.drained), int(res.drained_dirty), partial)
+        self._release(pos)
+
+    def _plan_keys(self, plan, n: int) -> np.ndarray:
+        view = L.PlanBuffers()
+        self.lib.bp_engine_plan_view(self.eng, plan.slot, C.byref(view), None)
+        return L.to_host(_wrap_device(view.d_prefetch_keys, torch.uint64, max(n, 1)), n)
+
+    def _plan_ttls(self, plan) -> list:
+        prep = C.c_void_p()
+        L.check(self.lib.bp_engine_prep(self.eng, plan.pos, C.byref(prep)), "bp_engine_prep")
+        pv = L.PrepView()
+        self.lib.bp_prep_get_view(prep, C.byref(pv))
+        u = int(L.to_host(_wrap_device(pv.d_num_unique, torch.int64, 1))[0])
+        view = L.PlanBuffers()
+        self.lib.bp_engine_plan_view(self.eng, plan.slot, C.byref(view), None)
+        keys = unpack_keys(L.to_host(_wrap_device(pv.d_uniq_key_k, torch.uint64, max(u, 1)), u))
+        ttls = L.to_host(_wrap_device(view.d_ttl_k, torch.int64, max(u, 1)), u).tolist()
+        return list(zip(keys, ttls))
 
     def end(self) -> RunReport:
         if not self.exhausted and (self.pending or self._next_plan() is not None):
             raise EngineError("planner emitted more plans than batches")
+        L.check(self.lib.bp_engine_sync(self.eng), "bp_engine_sync")
         return self._report()
 
     def run(self) -> RunReport:
@@ -526,31 +520,31 @@ class _Pipeline:
             self.step(pos)
         return self.end()
 
-    def _maintenance(self, pos: int, ch: _Chunk, partial: dict) -> None:
+    def _maintenance(self, pos, chunk, n_ev, n_ev_dirty, drain, n_dr, n_dr_dirty, partial) -> None:
         iteration = self.base + pos
-        self._buffer(ch, iteration)
-        evicted_count = ch.n
-        evicted_keys = self._sorted_keys(ch) if self.events is not None else None
+        evicted_keys = None
+        if self.events is not None:
+            evicted_keys = unpack_keys(np.sort(self._chunk_keys(chunk, n_ev)))
+        self._buffer(chunk, n_ev, n_ev_dirty, iteration)
+        evicted_count = n_ev
         last = pos == self.n - 1
         if last:
-            drain = self._evict(iteration, True, max(1, self.occupancy))
-            self.h_step[4:6].copy_(drain.count, non_blocking=True)
-            L.Context.get().raise_pending(self.stream)
-            drain.n, drain.n_dirty = (int(v) for v in self.h_step[4:6].tolist())
-            self.occupancy -= drain.n
-            self._buffer(drain, iteration)
+            self.occupancy -= n_dr
+            if evicted_keys is not None:
+                evicted_keys = evicted_keys + unpack_keys(np.sort(self._chunk_keys(drain, n_dr)))
+            self._buffer(drain, n_dr, n_dr_dirty, iteration)
             if self.chunks:
                 self._flush("final", pos)
-            evicted_count += drain.n
-            if evicted_keys is not None:
-                evicted_keys = evicted_keys + self._sorted_keys(drain)
+            evicted_count += n_dr
         elif (pos + 1) % self.flush_interval == 0 and self.chunks:
             self._flush("boundary", pos)
         if self.snapshots is not None and not last:
             expect = self.snapshots.pop(pos, None)
             if expect is not None:
-                used = self.cache.used.cpu().numpy().astype(bool)
-                got = np.sort(self.cache.slot_key.cpu().numpy()[used])
+                view = L.CacheView()
+                self.lib.bp_cache_get_view(self.parts.cache, C.byref(view))
+                used = L.to_host(_wrap_device(view.d_used, torch.uint8, view.capacity)).astype(bool)
+                got = np.sort(L.to_host(_wrap_device(view.d_slot_key, torch.uint64, view.capacity))[used])
                 if not np.array_equal(expect, got):
                     raise EngineError(f"planner mirror diverged at position {pos}: "
                                       f"{len(expect)} mirrored vs {len(got)} resident")
@@ -585,7 +579,7 @@ class _Pipeline:
         })
         return RunReport(
             kind="pipelined", config=self.cfg.to_dict(), schema=_schema_dict(self.schema), iterations_run=self.n,
-            initial_lookahead=self.L0, final_lookahead=self.state.lookahead, flush_interval=self.flush_interval,
+            initial_lookahead=self.L0, final_lookahead=self.lookahead, flush_interval=self.flush_interval,
             totals=totals, metadata=dict(_METADATA), final_store_digest=digest, trace_fingerprint=self.fingerprint,
             flushes=self.flush_log, records=self.records, events=self.events, final_store=self.store,
         )

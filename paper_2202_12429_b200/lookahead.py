@@ -175,15 +175,7 @@ class LookaheadState:
         return st
 
     def _dump(self):
-        cap = max(1, int(self.stats().tracked) + int(self.stats().in_cache) + 1)
-        keys = torch.empty(cap, dtype=torch.uint64, device="cuda")
-        last = torch.empty(cap, dtype=torch.int64, device="cuda")
-        flags = torch.empty(cap, dtype=torch.uint8, device="cuda")
-        count = torch.zeros(1, dtype=torch.int64, device="cuda")
-        d = L.PlannerDump(L.ptr(keys), L.ptr(last), L.ptr(flags), L.ptr(count))
-        L.check(L.lib().bp_planner_dump(self.handle, C.byref(d), cap, L.stream_ptr()), "bp_planner_dump")
-        n = min(int(count.item()), cap)
-        return L.to_host(keys, n), L.to_host(last, n), L.to_host(flags, n)
+        return planner_dump(self.handle)
 
     @property
     def in_cache(self) -> set:
@@ -199,6 +191,22 @@ class LookaheadState:
         keys, last, flags = self._dump()
         sel = (flags & _TRACKED) != 0
         return dict(zip(unpack_keys(keys[sel]), last[sel].tolist()))
+
+
+def planner_dump(handle, stream=None):
+    """(keys, last iteration, flags) of every key with planner state."""
+    st = L.PlannerStats()
+    L.check(L.lib().bp_planner_get_stats(handle, L.stream_ptr(stream), C.byref(st)), "bp_planner_get_stats")
+    cap = max(1, int(st.tracked) + int(st.in_cache) + 1)
+    keys = torch.empty(cap, dtype=torch.uint64, device="cuda")
+    last = torch.empty(cap, dtype=torch.int64, device="cuda")
+    flags = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    count = torch.zeros(1, dtype=torch.int64, device="cuda")
+    d = L.PlannerDump(L.ptr(keys), L.ptr(last), L.ptr(flags), L.ptr(count))
+    L.check(L.lib().bp_planner_dump(handle, C.byref(d), cap, L.stream_ptr(stream)), "bp_planner_dump")
+    torch.cuda.synchronize()
+    n = min(int(count.item()), cap)
+    return L.to_host(keys, n), L.to_host(last, n), L.to_host(flags, n)
 
 
 def new_state(lookahead: int, cache_capacity: int, **kw) -> LookaheadState:

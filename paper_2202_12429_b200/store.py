@@ -48,7 +48,7 @@ def initial_values(schema: Schema, seed: int, tables, rows) -> np.ndarray:
 class ShardedStore:
     """All tables behind fetch / write-back; values in pinned host memory."""
 
-    def __init__(self, schema: Schema, num_shards: int, seed: int):
+    def __init__(self, schema: Schema, num_shards: int, seed: int, _handle=None, _owner=None):
         if num_shards < 1:
             raise ConfigurationError("num_shards must be >= 1")
         self.schema = schema
@@ -59,9 +59,14 @@ class ShardedStore:
         self.fetch_calls = 0
         self.write_calls = 0
         self.entries_written = 0
-        h = C.c_void_p()
-        L.check(L.lib().bp_store_create(L.Context.get().handle, self.dschema.handle, seed & 0xFFFFFFFFFFFFFFFF,
-                                        L.stream_ptr(), C.byref(h)), "bp_store_create")
+        self._owner = _owner  # native engine owning the store (None: we own it)
+        if _handle is None:
+            h = C.c_void_p()
+            L.check(L.lib().bp_store_create(L.Context.get().handle, self.dschema.handle,
+                                            seed & 0xFFFFFFFFFFFFFFFF, L.stream_ptr(), C.byref(h)),
+                    "bp_store_create")
+        else:
+            h = C.c_void_p(_handle)
         self.handle = h
         addr = L.lib().bp_store_host_table(h)
         count = schema.total_rows * schema.emb_dim
@@ -71,7 +76,7 @@ class ShardedStore:
 
     def __del__(self):
         try:
-            if getattr(self, "handle", None):
+            if getattr(self, "handle", None) and getattr(self, "_owner", None) is None:
                 torch.cuda.synchronize()
                 L.lib().bp_store_destroy(self.handle)
                 self.handle = None
