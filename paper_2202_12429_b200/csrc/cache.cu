@@ -93,7 +93,13 @@ __global__ void k_insert(const uint64_t* __restrict__ keys, const uint32_t* __re
     ttl[slot] = ttls[i];
     dirty[slot] = 0;
     used[slot] = 1;
-    for (int d = 0; d < dim; ++d) values[(long long)slot * dim + d] = rows[i * dim + d];
+    if ((dim & 3) == 0) {
+      const float4* src = reinterpret_cast<const float4*>(rows + i * dim);
+      float4* dst = reinterpret_cast<float4*>(values + (long long)slot * dim);
+      for (int d = 0; d < (dim >> 2); ++d) dst[d] = src[d];
+    } else {
+      for (int d = 0; d < dim; ++d) values[(long long)slot * dim + d] = rows[i * dim + d];
+    }
   }
 }
 
@@ -215,8 +221,15 @@ __global__ void k_evict_out(const uint32_t* __restrict__ flag, const uint32_t* _
     if (out_keys) out_keys[p] = slot_key[i];
     if (out_ids) out_ids[p] = slot_id[i];
     if (out_dirty) out_dirty[p] = dty;
-    if (out_rows)
-      for (int d = 0; d < dim; ++d) out_rows[p * dim + d] = values[i * dim + d];
+    if (out_rows) {
+      if ((dim & 3) == 0) {
+        const float4* src = reinterpret_cast<const float4*>(values + i * dim);
+        float4* dst = reinterpret_cast<float4*>(out_rows + p * dim);
+        for (int d = 0; d < (dim >> 2); ++d) dst[d] = src[d];
+      } else {
+        for (int d = 0; d < dim; ++d) out_rows[p * dim + d] = values[i * dim + d];
+      }
+    }
     slot_of[slot_id[i]] = -1;
     used[i] = 0;
     dirty[i] = 0;

@@ -110,8 +110,9 @@ struct bp_engine {
   bp_store* store;
   bp_cache* cache;
   bp_planner* planner;
-  cudaStream_t compute, link;
+  cudaStream_t compute, link, planq;
   std::vector<bp_prep*> preps;  // ring indexed by position
+  std::vector<cudaEvent_t> prep_ready;  // per prep slot, recorded on planq
   std::vector<bp::PlanSlot> plans;
   std::vector<bp::ChunkSlot> chunks;
   std::vector<bp::UploadSlot> uploads;
@@ -186,6 +187,10 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   // and must not delay the critical path's CTAs.
   BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->compute, cudaStreamNonBlocking, hi));
   BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->link, cudaStreamNonBlocking, lo));
+  // Batch prep and the planner window step of batches entering the window run
+  // on their own stream: they depend only on the trace, so they overlap the
+  // training of the iterations ahead of them.
+  BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->planq, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
   int rc = bp_store_create(ctx, sc, cfg->seed, e->compute, &e->store);
   if (rc) return rc;
   rc = bp_cache_create(ctx, sc, cfg->capacity, cfg->dim, &e->cache);
@@ -195,6 +200,8 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   const long long n = cfg->max_occ;
   const int dim = cfg->dim;
   e->preps.assign(cfg->prep_slots, nullptr);
+  e->prep_ready.resize(cfg->prep_slots);
+  for (auto& ev : e->prep_ready) BP_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   e->plans.resize(cfg->plan_slots);
   for (auto& p : e->plans) {
     BP_CUDA_TRY(cudaMalloc(&p.keys, n * sizeof(uint64_t)));
@@ -210,6 +217,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     BP_CUDA_TRY(cudaEventCreateWithFlags(&p.fetched, cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&p.consumed, cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventRecord(p.consumed, e->compute));
+    BP_CUDA_TRY(cudaEventRecord(p.popped, e->compute));
     p.prep_pos = -1;
   }
   e->chunk_cap = cfg->capacity < n ? cfg->capacity : n;
@@ -236,7 +244,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     BP_CUDA_TRY(cudaMalloc(&e->d_keys_staging[i], n * sizeof(uint64_t)));
     BP_CUDA_TRY(cudaMalloc(&e->d_labels_staging[i], n + 16));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->staging_free[i], cudaEventDisableTiming));
-    BP_CUDA_TRY(cudaEventRecord(e->staging_free[i], e->compute));
+    BP_CUDA_TRY(cudaEventRecord(e->staging_free[i], e->planq));
   }
   e->staging_i = 0;
   e->next_plan = 0;
@@ -247,6 +255,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   BP_CUDA_TRY(cudaMalloc(&e->stats, 2 * sizeof(int64_t)));
   BP_CUDA_TRY(cudaMallocHost(&e->h_result, 16 * sizeof(int64_t)));
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
+  BP_CUDA_TRY(cudaStreamSynchronize(e->planq));
   *out = e;
   return BP_OK;
 }
@@ -294,8 +303,10 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   bp_planner_destroy(e->planner);
   bp_cache_destroy(e->cache);
   bp_store_destroy(e->store);
+  for (auto& ev : e->prep_ready) cudaEventDestroy(ev);
   cudaStreamDestroy(e->compute);
   cudaStreamDestroy(e->link);
+  cudaStreamDestroy(e->planq);
   delete e;
   return BP_OK;
 }
@@ -317,42 +328,39 @@ extern "C" int bp_engine_add_batch(bp_engine* e, int64_t pos, int64_t iteration,
   using namespace bp;
   if (n_occ > e->cfg.max_occ) return BP_ERR_INVALID;
   const int slot = engine_prep_slot(e, pos);
+  cudaStream_t q = e->planq;
   if (e->preps[slot]) {
     bp_prep_destroy(e->preps[slot]);
     e->preps[slot] = nullptr;
   }
   const uint64_t* d_keys = keys;
   const uint8_t* d_labels = labels;
+  int si = -1;
   if (keys_on_host && n_occ > 0) {
     UploadSlot& u = e->uploads[e->next_upload];
     e->next_upload = (e->next_upload + 1) % (int)e->uploads.size();
     if (u.used) BP_CUDA_TRY(cudaEventSynchronize(u.done));
     std::memcpy(u.host, keys, n_occ * sizeof(uint64_t));
     std::memcpy(u.host + n_occ * sizeof(uint64_t), labels, n_occ);
-    const int si = e->staging_i;
+    si = e->staging_i;
     e->staging_i ^= 1;
-    BP_CUDA_TRY(cudaStreamWaitEvent(e->compute, e->staging_free[si], 0));
-    BP_CUDA_TRY(cudaMemcpyAsync(e->d_keys_staging[si], u.host, n_occ * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                                e->compute));
+    BP_CUDA_TRY(cudaStreamWaitEvent(q, e->staging_free[si], 0));
+    BP_CUDA_TRY(cudaMemcpyAsync(e->d_keys_staging[si], u.host, n_occ * sizeof(uint64_t), cudaMemcpyHostToDevice, q));
     BP_CUDA_TRY(cudaMemcpyAsync(e->d_labels_staging[si], u.host + n_occ * sizeof(uint64_t), n_occ,
-                                cudaMemcpyHostToDevice, e->compute));
-    BP_CUDA_TRY(cudaEventRecord(u.done, e->compute));
+                                cudaMemcpyHostToDevice, q));
+    BP_CUDA_TRY(cudaEventRecord(u.done, q));
     u.used = true;
     d_keys = e->d_keys_staging[si];
     d_labels = e->d_labels_staging[si];
-    stage_begin(e, kStagePrep, e->compute);
-    int rc = bp_prep_create(e->ctx, e->sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, 0, 0, 0,
-                            e->compute, &e->preps[slot]);
-    stage_end(e, kStagePrep, e->compute);
-    if (rc) return rc;
-    BP_CUDA_TRY(cudaEventRecord(e->staging_free[si], e->compute));  // prep consumed the staging copy
-    return BP_OK;
   }
-  stage_begin(e, kStagePrep, e->compute);
+  stage_begin(e, kStagePrep, q);
   const int rc = bp_prep_create(e->ctx, e->sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, 0, 0,
-                                0, e->compute, &e->preps[slot]);
-  stage_end(e, kStagePrep, e->compute);
-  return rc;
+                                0, q, &e->preps[slot]);
+  stage_end(e, kStagePrep, q);
+  if (rc) return rc;
+  if (si >= 0) BP_CUDA_TRY(cudaEventRecord(e->staging_free[si], q));  // prep consumed the staging copy
+  BP_CUDA_TRY(cudaEventRecord(e->prep_ready[slot], q));
+  return BP_OK;
 }
 
 extern "C" int bp_engine_prep(bp_engine* e, int64_t pos, bp_prep** out) {
@@ -362,8 +370,15 @@ extern "C" int bp_engine_prep(bp_engine* e, int64_t pos, bp_prep** out) {
 
 extern "C" int bp_engine_release_batch(bp_engine* e, int64_t pos) {
   const int slot = bp::engine_prep_slot(e, pos);
-  if (e->preps[slot] && e->preps[slot]->iteration >= 0) {
-    bp_prep_destroy(e->preps[slot]);  // stream-ordered free on the compute stream
+  if (e->preps[slot]) {
+    // The prep's memory is freed in stream order on the plan stream, after
+    // the compute stream's last use (its training).
+    cudaEvent_t done;
+    BP_CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    BP_CUDA_TRY(cudaEventRecord(done, e->compute));
+    BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, done, 0));
+    cudaEventDestroy(done);
+    bp_prep_destroy(e->preps[slot]);
     e->preps[slot] = nullptr;
   }
   return BP_OK;
@@ -372,9 +387,9 @@ extern "C" int bp_engine_release_batch(bp_engine* e, int64_t pos) {
 extern "C" int bp_engine_refill(bp_engine* e, int64_t pos) {
   bp_prep* P = e->preps[bp::engine_prep_slot(e, pos)];
   if (!P) return BP_ERR_ENGINE;
-  bp::stage_begin(e, bp::kStagePlanner, e->compute);
-  const int rc = bp_planner_refill(e->planner, P, e->compute);
-  bp::stage_end(e, bp::kStagePlanner, e->compute);
+  bp::stage_begin(e, bp::kStagePlanner, e->planq);
+  const int rc = bp_planner_refill(e->planner, P, e->planq);
+  bp::stage_end(e, bp::kStagePlanner, e->planq);
   return rc;
 }
 
@@ -387,14 +402,14 @@ extern "C" int bp_engine_pop(bp_engine* e, int64_t pos, int32_t* slot_out) {
   e->next_plan = (e->next_plan + 1) % (int)e->plans.size();
   PlanSlot& ps = e->plans[slot];
   // The slot's previous plan must have been consumed by training.
-  BP_CUDA_TRY(cudaStreamWaitEvent(e->compute, ps.consumed, 0));
+  BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, ps.consumed, 0));
   bp_plan_buffers b{ps.keys, ps.ids, ps.ttls, ps.ttl_k, ps.evict_keys, ps.counts};
-  stage_begin(e, kStagePlanner, e->compute);
-  int rc = bp_planner_pop(e->planner, P, &b, e->compute);
-  stage_end(e, kStagePlanner, e->compute);
+  stage_begin(e, kStagePlanner, e->planq);
+  int rc = bp_planner_pop(e->planner, P, &b, e->planq);
+  stage_end(e, kStagePlanner, e->planq);
   if (rc) return rc;
-  BP_CUDA_TRY(cudaMemcpyAsync(ps.h_counts, ps.counts, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, e->compute));
-  BP_CUDA_TRY(cudaEventRecord(ps.popped, e->compute));
+  BP_CUDA_TRY(cudaMemcpyAsync(ps.h_counts, ps.counts, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, e->planq));
+  BP_CUDA_TRY(cudaEventRecord(ps.popped, e->planq));
   ps.prep_pos = pos;
   *slot_out = slot;
   return BP_OK;
@@ -469,6 +484,7 @@ extern "C" int bp_engine_train(bp_engine* e, int64_t pos, int32_t plan_slot, int
   if (rc) return rc;
   bp_prep* N = next_pos >= 0 ? e->preps[engine_prep_slot(e, next_pos)] : nullptr;
   if (N) {
+    BP_CUDA_TRY(cudaStreamWaitEvent(s, e->prep_ready[engine_prep_slot(e, next_pos)], 0));
     rc = bp_mark_ids(N, e->mark, N->iteration, s);
     if (rc) return rc;
   }
@@ -535,6 +551,7 @@ extern "C" int bp_engine_chunk_view(bp_engine* e, int32_t chunk_slot, bp_evict_b
 
 extern "C" int bp_engine_sync(bp_engine* e) {
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
+  BP_CUDA_TRY(cudaStreamSynchronize(e->planq));
   BP_CUDA_TRY(cudaStreamSynchronize(e->link));
   return BP_OK;
 }

@@ -24,6 +24,8 @@ constexpr uint32_t kNoId = 0xFFFFFFFFu;
 // Segments at least this long (occurrences of one key in one batch) take the
 // shared-memory path of the trainer kernel (trainer.cu).
 constexpr uint32_t kLongSeg = 512;
+// ...and those this long are scheduled first (longest-processing-time order).
+constexpr uint32_t kVeryLongSeg = 4096;
 constexpr uint64_t kEmptyKey = ~0ull;
 
 // Memory from the device's stream-ordered pool (release threshold raised at
@@ -102,8 +104,10 @@ struct bp_prep {
   uint8_t* d_occ_label;
   uint32_t* d_occ_k;
   long long* d_rank_bounds;
-  uint32_t* d_long;        // key-sorted indices of segments with >= kLongSeg occurrences
-  long long* d_num_long;
+  uint32_t* d_long;        // segments with >= kLongSeg occurrences: very long ones from the
+                           // front, the others from the back (capacity long_cap)
+  long long* d_num_long;   // [2]: very long, long
+  long long long_cap;
   long long h_num_unique;  // -1 until read back
   cudaStream_t stream;
 };

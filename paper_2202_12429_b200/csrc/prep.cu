@@ -89,7 +89,7 @@ __global__ void k_prep_perm(const uint32_t* __restrict__ pos, const uint32_t* __
                             const uint64_t* __restrict__ uniq_key_s, uint32_t* __restrict__ perm_s2k,
                             uint32_t* __restrict__ perm_k2s, uint64_t* __restrict__ uniq_key_k,
                             const uint32_t* __restrict__ seg_start, uint32_t* __restrict__ long_list,
-                            unsigned long long* num_long) {
+                            unsigned long long* num_long, long long long_cap) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
     if (!head[j]) continue;
     const uint32_t s = segx[j];
@@ -97,7 +97,9 @@ __global__ void k_prep_perm(const uint32_t* __restrict__ pos, const uint32_t* __
     perm_s2k[s] = k;
     perm_k2s[k] = s;
     uniq_key_k[k] = uniq_key_s[s];
-    if (seg_start[s + 1] - seg_start[s] >= kLongSeg) long_list[atomicAdd(num_long, 1ull)] = s;
+    const uint32_t len = seg_start[s + 1] - seg_start[s];
+    if (len >= kVeryLongSeg) long_list[atomicAdd(&num_long[0], 1ull)] = s;
+    else if (len >= kLongSeg) long_list[long_cap - 1 - (long long)atomicAdd(&num_long[1], 1ull)] = s;
   }
 }
 
@@ -156,10 +158,10 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
                                        P->d_occ_label, P->d_num_unique, P->d_rank_bounds, P->num_ranks,
                                        P->ctx ? P->ctx->d_err : nullptr, P->iteration);
   BP_CUDA_TRY(exclusive_scan(first_flag, first_rank, n, nullptr, partials, nullptr, nullptr, s));
-  BP_CUDA_TRY(cudaMemsetAsync(P->d_num_long, 0, sizeof(long long), s));
+  BP_CUDA_TRY(cudaMemsetAsync(P->d_num_long, 0, 2 * sizeof(long long), s));
   k_prep_perm<<<g, 256, 0, s>>>(P->d_occ_pos, head, segx, first_rank, n, P->d_uniq_key_s, P->d_perm_s2k,
                                 P->d_perm_k2s, P->d_uniq_key_k, P->d_seg_start, P->d_long,
-                                (unsigned long long*)P->d_num_long);
+                                (unsigned long long*)P->d_num_long, P->long_cap);
   if (P->flags & BP_PREP_OCC_INDEX)
     k_prep_occ_k<<<g, 256, 0, s>>>(P->d_occ_pos, head, segx, n, P->d_perm_s2k, P->d_occ_k);
   BP_LAUNCH_CHECK();
@@ -207,14 +209,15 @@ extern "C" int bp_prep_create(bp_ctx* ctx, const bp_schema* sc, const uint64_t* 
   P->d_occ_k = nullptr;
   if (flags & BP_PREP_OCC_INDEX) BP_CUDA_TRY(pool_alloc(&P->d_occ_k, n, s));
   BP_CUDA_TRY(pool_alloc(&P->d_rank_bounds, num_ranks + 1, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_long, n / kLongSeg + 1, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_num_long, 1, s));
+  P->long_cap = n / kLongSeg + 1;
+  BP_CUDA_TRY(pool_alloc(&P->d_long, P->long_cap, s));
+  BP_CUDA_TRY(pool_alloc(&P->d_num_long, 2, s));
   BP_CUDA_TRY(cudaMemcpyAsync(P->d_rank_bounds, h_rank_bounds, sizeof(long long) * (num_ranks + 1),
                               cudaMemcpyHostToDevice, s));
   // The pageable H2D copy above is staged by the driver before returning, so
   // the caller's rank-bounds array may be released immediately.
   if (n_occ == 0) {
-    BP_CUDA_TRY(cudaMemsetAsync(P->d_num_long, 0, sizeof(long long), s));
+    BP_CUDA_TRY(cudaMemsetAsync(P->d_num_long, 0, 2 * sizeof(long long), s));
     BP_CUDA_TRY(cudaMemsetAsync(P->d_num_unique, 0, sizeof(long long), s));
     BP_CUDA_TRY(cudaMemsetAsync(P->d_seg_start, 0, sizeof(uint32_t), s));
     *out = P;

@@ -103,27 +103,40 @@ static __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(const uint
   }
   uint32_t block_total;
   const uint32_t thread_excl = block_inclusive_scan_256(run, sh_warp, &block_total) - run;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // Warp-parallel look-back: lane l inspects tile (j - l); the nearest
+    // tile holding an inclusive prefix ends the walk, and the aggregates of
+    // the tiles in front of it are summed in one warp reduction.
     volatile unsigned long long* st = state;
+    const unsigned lane = threadIdx.x;
+    const uint32_t ep = epoch & 0x3FFFFFFFu;
     uint32_t prefix = 0;
     if (tile == 0) {
-      st[0] = scan_pack(epoch, kFlagPrefix, block_total);
+      if (lane == 0) st[0] = scan_pack(epoch, kFlagPrefix, block_total);
     } else {
-      st[tile] = scan_pack(epoch, kFlagAgg, block_total);
-      for (long long j = tile - 1; j >= 0; --j) {
-        unsigned long long w;
-        do {
-          w = st[j];
-        } while ((uint32_t)(w >> 34) != (epoch & 0x3FFFFFFFu) || ((w >> 32) & 3ull) == 0);
-        prefix += (uint32_t)w;
-        if (((w >> 32) & 3ull) == kFlagPrefix) break;
+      if (lane == 0) st[tile] = scan_pack(epoch, kFlagAgg, block_total);
+      for (long long j = tile - 1;; j -= 32) {
+        const long long idx = j - (long long)lane;
+        unsigned long long w = 0;
+        if (idx >= 0) {
+          do {
+            w = st[idx];
+          } while ((uint32_t)(w >> 34) != ep || ((w >> 32) & 3ull) == 0);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, idx >= 0 && ((w >> 32) & 3ull) == kFlagPrefix);
+        const unsigned stop = pm ? (unsigned)(__ffs(pm) - 1) : 31u;
+        uint32_t v = (idx >= 0 && lane <= stop) ? (uint32_t)w : 0u;
+        prefix += warp_sum(v);
+        if (pm || j - 32 < 0) break;
       }
-      st[tile] = scan_pack(epoch, kFlagPrefix, prefix + block_total);
+      if (lane == 0) st[tile] = scan_pack(epoch, kFlagPrefix, prefix + block_total);
     }
-    sh_prefix = prefix;
-    if (base + kScanTile >= n) {
-      if (total) *total = prefix + block_total;
-      if (total64) *total64 = (long long)(prefix + block_total);
+    if (lane == 0) {
+      sh_prefix = prefix;
+      if (base + kScanTile >= n) {
+        if (total) *total = prefix + block_total;
+        if (total64) *total64 = (long long)(prefix + block_total);
+      }
     }
   }
   __syncthreads();

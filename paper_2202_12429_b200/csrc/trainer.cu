@@ -61,7 +61,7 @@ __device__ __forceinline__ void chain_chunk(const uint32_t (&word)[4], uint32_t 
   }
 }
 
-constexpr int kLongBlocks = 64;        // CTAs reserved for long segments
+constexpr int kLongBlocks = 128;       // CTAs reserved for long segments
 constexpr int kLongWindowChunks = 1024;  // 16 KB of occurrence bytes staged in smem
 
 // Fused trainer kernel.  CTAs [0, kLongBlocks) take the keys whose segment
@@ -77,7 +77,7 @@ template <int G, int DPL>
 __global__ void __launch_bounds__(256, 6) k_stub_step(
     const uint32_t* __restrict__ seg_start, const uint8_t* __restrict__ occ_label,
     const long long* __restrict__ d_U, const uint32_t* __restrict__ long_list,
-    const long long* __restrict__ d_num_long, float* __restrict__ rows, const int32_t* __restrict__ row_index,
+    const long long* __restrict__ d_num_long, long long long_cap, float* __restrict__ rows, const int32_t* __restrict__ row_index,
     uint8_t* __restrict__ dirty, int dim, float c_value, float c_label, float lr, int mode,
     float* __restrict__ grad_out, const uint32_t* __restrict__ my_ids, const int64_t* __restrict__ next_mark,
     long long next_tag, unsigned long long* __restrict__ stats) {
@@ -87,10 +87,11 @@ __global__ void __launch_bounds__(256, 6) k_stub_step(
 
   if (blockIdx.x < kLongBlocks) {
     __shared__ uint4 win[kLongWindowChunks];
-    const long long n_long = *d_num_long;
+    const long long n_vlong = d_num_long[0], n_long = n_vlong + d_num_long[1];
     const bool chain_lane = threadIdx.x < G;  // warp 0, lanes [0, G)
+    // very long segments first (front of the list), then the others (back)
     for (long long li = blockIdx.x; li < n_long; li += kLongBlocks) {
-      const uint32_t s = long_list[li];
+      const uint32_t s = li < n_vlong ? long_list[li] : long_list[long_cap - 1 - (li - n_vlong)];
       const uint32_t a = seg_start[s], b = seg_start[s + 1];
       const int32_t row = row_index ? row_index[s] : (int32_t)s;
       if (row < 0) continue;  // block-uniform: the miss is already recorded
@@ -335,7 +336,7 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   const int blocks = kLongBlocks + grid_for(groups * G, threads, kNumSMs * 6);
   BP_DISPATCH_GD(G, dpl,
                  (k_stub_step<g_, d_><<<blocks, threads, 0, s>>>(
-                     P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, d_rows,
+                     P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,
                      d_row_index, d_dirty, dim, c_value,
                      c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark, next_tag,
                      (unsigned long long*)d_stats)));
