@@ -243,6 +243,10 @@ int bp_cache_get_view(const bp_cache* cache, bp_cache_view* out);
  * digest order of reference store.py:179-185.  Initial values are computed on
  * the GPU (reference store.py:29-42) and streamed to the host table. */
 int bp_store_create(bp_ctx* ctx, const bp_schema* schema, uint64_t seed, bp_stream_t stream, bp_store** out);
+/* As bp_store_create; components >= init_dims of every row start at 0
+ * (optimizer state stored beside the weights). */
+int bp_store_create_ex(bp_ctx* ctx, const bp_schema* schema, uint64_t seed, int32_t init_dims, bp_stream_t stream,
+                       bp_store** out);
 int bp_store_destroy(bp_store* store);
 float* bp_store_host_table(bp_store* store);
 uint8_t* bp_store_written_bitmap(bp_store* store); /* device, 1 bit per row */
@@ -313,6 +317,8 @@ typedef struct bp_engine_config {
   int32_t record_keys; /* keep evicted keys for event logs */
   int32_t plan_slots, chunk_slots, prep_slots;
   int32_t timing;      /* record per-stage CUDA events (bp_engine_stage_times) */
+  int32_t init_dims;   /* store: components >= init_dims start at 0 (0 = all initialised) */
+  int32_t pad;
 } bp_engine_config;
 typedef struct bp_step_result {
   int64_t unique, inserted, critical, dirty_keys, evicted, evicted_dirty, drained, drained_dirty;
@@ -343,6 +349,16 @@ int bp_engine_fetch(bp_engine* engine, int32_t slot);
 int bp_engine_flush(bp_engine* engine, const int32_t* h_chunk_slots, int32_t n);
 int bp_engine_train(bp_engine* engine, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
                     int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out);
+/* DLRM mode iteration, split around the (PyTorch) dense model:
+ * forward = apply plan + lookup + next-batch stamp + EmbeddingBag forward of
+ * the batch's single-key bags into d_pooled[n_occ][model_dim] (async on the
+ * compute stream); backward = EmbeddingBag backward + optimizer in place +
+ * eviction (+ drain), counters, one synchronisation (like bp_engine_train). */
+int bp_engine_dlrm_forward(bp_engine* engine, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
+                           int32_t has_skip, int32_t model_dim, float* d_pooled);
+int bp_engine_dlrm_backward(bp_engine* engine, int64_t pos, int32_t plan_slot, const float* d_grad,
+                            int32_t model_dim, int32_t opt, float lr, float eps, int32_t chunk_slot,
+                            int32_t drain_slot, bp_step_result* out);
 int bp_engine_chunk_keys(bp_engine* engine, int32_t chunk_slot, uint64_t* h_out, int64_t n);
 int bp_engine_chunk_view(bp_engine* engine, int32_t chunk_slot, bp_evict_buffers* out);
 int bp_engine_sync(bp_engine* engine);
@@ -350,6 +366,27 @@ int bp_engine_sync(bp_engine* engine);
  * (link), apply (insert+TTL+lookup+mark), trainer, evict, flush (link).
  * Synchronises the device. */
 int bp_engine_stage_times(bp_engine* engine, double* h_ms7, int64_t* h_counts7);
+
+/* ------------------------------------------------------- EmbeddingBag (DLRM)
+ * North-star piece 4 (no reference counterpart: parity vs a PyTorch fp32 CPU
+ * model within tolerance).  Rows are read from a row arena (the cache) with
+ * row_stride >= dim; optimizer state (Adagrad) sits at [dim, 2*dim).
+ * forward: d_bag_offsets NULL => one occurrence per bag (bag = occurrence
+ * position, Criteo layout): each key's row is read once and scattered to its
+ * occurrences; otherwise bags [off[b], off[b+1]) of occurrences are summed
+ * (mode 1: mean) using d_occ_s from bp_prep_occ_sorted_index.
+ * backward: per unique key g = sum of its occurrences' bag gradients
+ * (x d_bag_scale[bag] if given), then SGD or Adagrad in place; dirty marks
+ * rows with g != 0; d_stats[1] += number of such keys. */
+#define BP_OPT_SGD 0
+#define BP_OPT_ADAGRAD 1
+int bp_embbag_forward(bp_prep* prep, const float* d_values, int32_t row_stride, const int32_t* d_slots_s,
+                      int32_t dim, const int64_t* d_bag_offsets, int64_t n_bags, int32_t mode,
+                      const uint32_t* d_occ_s, float* d_out, bp_stream_t stream);
+int bp_embbag_backward(bp_prep* prep, const float* d_grad, const int64_t* d_occ_bag, const float* d_bag_scale,
+                       float* d_values, int32_t row_stride, const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim,
+                       int32_t opt, float lr, float eps, int64_t* d_stats, bp_stream_t stream);
+int bp_prep_occ_sorted_index(bp_prep* prep, uint32_t* d_occ_s, bp_stream_t stream);
 
 /* ------------------------------------------------------------ utilities */
 /* Sort packed keys ascending with a u32 payload (stable); n host-known. */

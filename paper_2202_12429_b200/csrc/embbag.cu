@@ -1,0 +1,321 @@
+// EmbeddingBag forward / backward + sparse optimizer over the HBM cache
+// (north-star piece 4, DLRM mode).  The reference has no model (its trainer
+// is the stub of trainer.py), so parity for this mode is against a PyTorch
+// fp32 CPU model (nn.EmbeddingBag + the same MLPs) within a tolerance.
+//
+// Both kernels walk the batch prep's key-sorted CSR (prep.cu): every cached
+// row is read (forward) or read-modified-written (backward) exactly once per
+// batch, however many times the key occurs.
+//
+//   forward, single-key bags (Criteo layout: one key per table per example,
+//   bag = occurrence position): one G-lane group per unique key loads the
+//   row once and scatters it to all of the key's occurrence rows of
+//   pooled[n_occ][dim] -- N_occ x 64 B of writes, U x 64 B of reads.
+//   forward, multi-key bags: per bag, sum (or mean) of its keys' rows.
+//   backward: per unique key, g = sum over its occurrences of the bag
+//   gradient rows (x 1/|bag| for mean), then SGD (v -= lr g) or Adagrad
+//   (a += g^2; v -= lr g / (sqrt(a) + eps)) in place; optimizer state lives
+//   in the second half of the row (row stride 2*dim), so it travels with the
+//   row through eviction and write-back.  Keys with >= kLongSeg occurrences
+//   are reduced by whole CTAs (16 partial sums, fixed-order tree: run-to-run
+//   deterministic).
+#include "internal.cuh"
+
+namespace bp {
+
+constexpr int kBagLongBlocks = 128;
+
+template <int G, int DPL>
+__global__ void __launch_bounds__(256) k_embbag_fwd_scatter(const uint32_t* __restrict__ seg_start,
+                                                            const uint32_t* __restrict__ occ_pos,
+                                                            const long long* __restrict__ d_U,
+                                                            const float* __restrict__ values,
+                                                            const int32_t* __restrict__ slots_s, int dim,
+                                                            int row_stride, float* __restrict__ out) {
+  const long long U = *d_U;
+  const int lane_g = (int)(threadIdx.x & (G - 1));
+  const long long groups_total = (long long)gridDim.x * (blockDim.x / G);
+  for (long long s = (long long)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; s < U; s += groups_total) {
+    const uint32_t a = seg_start[s], b = seg_start[s + 1];
+    const int32_t slot = slots_s[s];
+    float v[DPL];
+#pragma unroll
+    for (int q = 0; q < DPL; ++q) {
+      const int d = lane_g + q * G;
+      v[q] = (slot >= 0 && d < dim) ? values[(long long)slot * row_stride + d] : 0.f;
+    }
+    for (uint32_t j = a; j < b; ++j) {
+      const long long p = occ_pos[j];
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) {
+        const int d = lane_g + q * G;
+        if (d < dim) out[p * dim + d] = v[q];
+      }
+    }
+  }
+}
+
+template <int G, int DPL>
+__global__ void __launch_bounds__(256) k_embbag_fwd_gather(const uint32_t* __restrict__ occ_s,
+                                                           const int32_t* __restrict__ slots_s,
+                                                           const float* __restrict__ values,
+                                                           const int64_t* __restrict__ bag_offsets, long long n_bags,
+                                                           int dim, int row_stride, int mean,
+                                                           float* __restrict__ out) {
+  const int lane_g = (int)(threadIdx.x & (G - 1));
+  const long long groups_total = (long long)gridDim.x * (blockDim.x / G);
+  for (long long bag = (long long)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; bag < n_bags;
+       bag += groups_total) {
+    const long long lo = bag_offsets[bag], hi = bag_offsets[bag + 1];
+    float acc[DPL];
+#pragma unroll
+    for (int q = 0; q < DPL; ++q) acc[q] = 0.f;
+    for (long long p = lo; p < hi; ++p) {
+      const int32_t slot = slots_s[occ_s[p]];
+      if (slot < 0) continue;
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) {
+        const int d = lane_g + q * G;
+        if (d < dim) acc[q] = __fadd_rn(acc[q], values[(long long)slot * row_stride + d]);
+      }
+    }
+    const float scale = (mean && hi > lo) ? __frcp_rn((float)(hi - lo)) : 1.f;
+#pragma unroll
+    for (int q = 0; q < DPL; ++q) {
+      const int d = lane_g + q * G;
+      if (d < dim) out[bag * dim + d] = mean ? __fmul_rn(acc[q], scale) : acc[q];
+    }
+  }
+}
+
+struct BagGrad {
+  const float* grad;        // [n_bags][dim]
+  const int64_t* occ_bag;   // bag of each occurrence position (NULL: identity)
+  const float* bag_scale;   // per bag multiplier (NULL: 1), e.g. 1/|bag| for mean
+};
+
+__device__ __forceinline__ float grad_at(const BagGrad& g, long long p, int d, int dim) {
+  const long long bag = g.occ_bag ? g.occ_bag[p] : p;
+  const float x = g.grad[bag * dim + d];
+  return g.bag_scale ? __fmul_rn(x, g.bag_scale[bag]) : x;
+}
+
+template <int DPL>
+__device__ __forceinline__ void apply_update(float* __restrict__ row, const float (&g)[DPL], int lane_g, int G, int dim,
+                                             int opt, float lr, float eps, bool& nonzero) {
+#pragma unroll
+  for (int q = 0; q < DPL; ++q) {
+    const int d = lane_g + q * G;
+    if (d >= dim) continue;
+    nonzero |= g[q] != 0.f;
+    const float v = row[d];
+    if (opt == BP_OPT_ADAGRAD) {
+      const float a = __fadd_rn(row[dim + d], __fmul_rn(g[q], g[q]));
+      row[dim + d] = a;
+      row[d] = __fsub_rn(v, __fdiv_rn(__fmul_rn(lr, g[q]), __fadd_rn(__fsqrt_rn(a), eps)));
+    } else {
+      row[d] = __fsub_rn(v, __fmul_rn(lr, g[q]));
+    }
+  }
+}
+
+template <int G, int DPL>
+__global__ void __launch_bounds__(256) k_embbag_bwd(const uint32_t* __restrict__ seg_start,
+                                                    const uint32_t* __restrict__ occ_pos,
+                                                    const long long* __restrict__ d_U,
+                                                    const uint32_t* __restrict__ long_list,
+                                                    const long long* __restrict__ d_num_long, long long long_cap,
+                                                    BagGrad bg, float* __restrict__ values,
+                                                    const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty,
+                                                    int dim, int row_stride, int opt, float lr, float eps,
+                                                    unsigned long long* __restrict__ stats) {
+  const unsigned lane = threadIdx.x & 31u;
+  if (blockIdx.x < kBagLongBlocks) {
+    // whole-CTA reduction of a long segment: 256/G partial sums, fixed tree
+    __shared__ float part[256 / 1 * 4];
+    const long long n_vlong = d_num_long[0], n_long = n_vlong + d_num_long[1];
+    const int groups = 256 / G;
+    const int grp = threadIdx.x / G, lane_g = threadIdx.x & (G - 1);
+    for (long long li = blockIdx.x; li < n_long; li += kBagLongBlocks) {
+      const uint32_t s = li < n_vlong ? long_list[li] : long_list[long_cap - 1 - (li - n_vlong)];
+      const uint32_t a = seg_start[s], b = seg_start[s + 1];
+      const int32_t slot = slots_s[s];
+      if (slot < 0) continue;
+      float acc[DPL];
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) acc[q] = 0.f;
+      for (uint32_t j = a + grp; j < b; j += groups) {
+        const long long p = occ_pos[j];
+#pragma unroll
+        for (int q = 0; q < DPL; ++q) {
+          const int d = lane_g + q * G;
+          if (d < dim) acc[q] = __fadd_rn(acc[q], grad_at(bg, p, d, dim));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) part[(grp * G + lane_g) * DPL + q] = acc[q];
+      __syncthreads();
+      for (int width = groups / 2; width > 0; width >>= 1) {
+        if (grp < width) {
+#pragma unroll
+          for (int q = 0; q < DPL; ++q)
+            part[(grp * G + lane_g) * DPL + q] =
+                __fadd_rn(part[(grp * G + lane_g) * DPL + q], part[((grp + width) * G + lane_g) * DPL + q]);
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x < 32) {
+        bool nonzero = false;
+        if (threadIdx.x < G) {
+          float g[DPL];
+#pragma unroll
+          for (int q = 0; q < DPL; ++q) g[q] = part[threadIdx.x * DPL + q];
+          apply_update<DPL>(values + (long long)slot * row_stride, g, threadIdx.x, G, dim, opt, lr, eps, nonzero);
+        }
+        const bool nz = __ballot_sync(0xffffffffu, nonzero) != 0;
+        if (threadIdx.x == 0) {
+          if (nz && dirty) dirty[slot] = 1;
+          if (nz && stats) atomicAdd(&stats[1], 1ull);
+        }
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const long long U = *d_U;
+  const int lane_g = (int)(lane & (G - 1));
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(unsigned)(G - 1)));
+  const long long groups_per_block = blockDim.x / G;
+  const long long groups_total = (long long)(gridDim.x - kBagLongBlocks) * groups_per_block;
+  const long long warp_first =
+      (long long)(blockIdx.x - kBagLongBlocks) * groups_per_block + (threadIdx.x >> 5) * (32 / G);
+  for (long long base = warp_first; base < U; base += groups_total) {
+    const long long s = base + (long long)(lane / G);
+    bool active = s < U;
+    uint32_t a = 0, b = 0;
+    int32_t slot = -1;
+    if (active) {
+      a = seg_start[s];
+      b = seg_start[s + 1];
+      slot = slots_s[s];
+      active = slot >= 0 && b - a < kLongSeg;
+    }
+    bool nonzero = false;
+    if (active) {
+      float g[DPL];
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) g[q] = 0.f;
+      for (uint32_t j = a; j < b; ++j) {
+        const long long p = occ_pos[j];
+#pragma unroll
+        for (int q = 0; q < DPL; ++q) {
+          const int d = lane_g + q * G;
+          if (d < dim) g[q] = __fadd_rn(g[q], grad_at(bg, p, d, dim));
+        }
+      }
+      apply_update<DPL>(values + (long long)slot * row_stride, g, lane_g, G, dim, opt, lr, eps, nonzero);
+    }
+    const unsigned nz = __ballot_sync(0xffffffffu, nonzero) & gmask;
+    if (active && lane_g == 0 && nz && dirty) dirty[slot] = 1;
+    if (stats) {
+      const unsigned dm = __ballot_sync(0xffffffffu, active && lane_g == 0 && nz != 0);
+      if (lane == 0 && dm) atomicAdd(&stats[1], (unsigned long long)__popc(dm));
+    }
+  }
+}
+
+// occ_s[p] = key-sorted unique index of occurrence p (segment of sorted slot j
+// found by binary search over the CSR offsets).
+__global__ void k_occ_sorted_index(const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ occ_pos,
+                                   const long long* __restrict__ d_U, long long n, uint32_t* __restrict__ occ_s) {
+  const long long U = *d_U;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    long long lo = 0, hi = U;  // largest s with seg_start[s] <= j
+    while (hi - lo > 1) {
+      const long long mid = (lo + hi) >> 1;
+      if (seg_start[mid] <= (uint32_t)j) lo = mid;
+      else hi = mid;
+    }
+    occ_s[occ_pos[j]] = (uint32_t)lo;
+  }
+}
+
+static inline void shape_of(int dim, int* G, int* dpl) {
+  int g = 1;
+  while (g < dim && g < 32) g <<= 1;
+  *G = g;
+  *dpl = (dim + g - 1) / g;
+}
+
+}  // namespace bp
+
+#define BP_BAG_DISPATCH(G, DPL, CALL)                                  \
+  switch (G * 16 + DPL) {                                               \
+    case 1 * 16 + 1: { constexpr int g_ = 1, d_ = 1; CALL; break; }   \
+    case 2 * 16 + 1: { constexpr int g_ = 2, d_ = 1; CALL; break; }   \
+    case 4 * 16 + 1: { constexpr int g_ = 4, d_ = 1; CALL; break; }   \
+    case 8 * 16 + 1: { constexpr int g_ = 8, d_ = 1; CALL; break; }   \
+    case 16 * 16 + 1: { constexpr int g_ = 16, d_ = 1; CALL; break; } \
+    case 32 * 16 + 1: { constexpr int g_ = 32, d_ = 1; CALL; break; } \
+    case 32 * 16 + 2: { constexpr int g_ = 32, d_ = 2; CALL; break; } \
+    case 32 * 16 + 3: { constexpr int g_ = 32, d_ = 3; CALL; break; } \
+    case 32 * 16 + 4: { constexpr int g_ = 32, d_ = 4; CALL; break; } \
+    default: return BP_ERR_INVALID;                                     \
+  }
+
+extern "C" int bp_embbag_forward(bp_prep* P, const float* d_values, int32_t row_stride, const int32_t* d_slots_s,
+                                 int32_t dim, const int64_t* d_bag_offsets, int64_t n_bags, int32_t mode,
+                                 const uint32_t* d_occ_s, float* d_out, bp_stream_t stream) {
+  using namespace bp;
+  if (dim < 1 || dim > 128) return BP_ERR_INVALID;
+  if (P->n_occ == 0) return BP_OK;
+  int G, dpl;
+  shape_of(dim, &G, &dpl);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!d_bag_offsets) {
+    const int blocks = grid_for(P->n_occ * G, 256, kNumSMs * 8);
+    BP_BAG_DISPATCH(G, dpl,
+                    (k_embbag_fwd_scatter<g_, d_><<<blocks, 256, 0, s>>>(P->d_seg_start, P->d_occ_pos,
+                                                                         P->d_num_unique, d_values, d_slots_s, dim,
+                                                                         row_stride, d_out)));
+  } else {
+    if (!d_occ_s) return BP_ERR_INVALID;
+    const int blocks = grid_for(n_bags * G, 256, kNumSMs * 8);
+    BP_BAG_DISPATCH(G, dpl,
+                    (k_embbag_fwd_gather<g_, d_><<<blocks, 256, 0, s>>>(d_occ_s, d_slots_s, d_values, d_bag_offsets,
+                                                                        n_bags, dim, row_stride, mode, d_out)));
+  }
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t* d_occ_bag,
+                                  const float* d_bag_scale, float* d_values, int32_t row_stride,
+                                  const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt, float lr,
+                                  float eps, int64_t* d_stats, bp_stream_t stream) {
+  using namespace bp;
+  if (dim < 1 || dim > 128) return BP_ERR_INVALID;
+  if (opt == BP_OPT_ADAGRAD && row_stride < 2 * dim) return BP_ERR_INVALID;
+  if (P->n_occ == 0) return BP_OK;
+  int G, dpl;
+  shape_of(dim, &G, &dpl);
+  cudaStream_t s = (cudaStream_t)stream;
+  const BagGrad bg{d_grad, d_occ_bag, d_bag_scale};
+  const int blocks = kBagLongBlocks + grid_for(P->n_occ * G, 256, kNumSMs * 6);
+  BP_BAG_DISPATCH(G, dpl,
+                  (k_embbag_bwd<g_, d_><<<blocks, 256, 0, s>>>(P->d_seg_start, P->d_occ_pos, P->d_num_unique,
+                                                               P->d_long, P->d_num_long, P->long_cap, bg, d_values,
+                                                               d_slots_s, d_dirty, dim, row_stride, opt, lr, eps,
+                                                               (unsigned long long*)d_stats)));
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_prep_occ_sorted_index(bp_prep* P, uint32_t* d_occ_s, bp_stream_t stream) {
+  using namespace bp;
+  if (P->n_occ == 0) return BP_OK;
+  k_occ_sorted_index<<<grid_for(P->n_occ, 256), 256, 0, (cudaStream_t)stream>>>(P->d_seg_start, P->d_occ_pos,
+                                                                                 P->d_num_unique, P->n_occ, d_occ_s);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}

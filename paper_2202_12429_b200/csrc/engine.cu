@@ -49,6 +49,11 @@ int bp_planner_pop(bp_planner*, bp_prep*, const bp_plan_buffers*, bp_stream_t);
 int bp_mark_ids(bp_prep*, int64_t*, int64_t, bp_stream_t);
 int bp_stub_step(bp_ctx*, bp_prep*, float*, const int32_t*, uint8_t*, int32_t, float, float, float, int32_t, float*,
                  const int64_t*, int64_t, int64_t*, bp_stream_t);
+int bp_store_create_ex(bp_ctx*, const bp_schema*, uint64_t, int32_t, bp_stream_t, bp_store**);
+int bp_embbag_forward(bp_prep*, const float*, int32_t, const int32_t*, int32_t, const int64_t*, int64_t, int32_t,
+                      const uint32_t*, float*, bp_stream_t);
+int bp_embbag_backward(bp_prep*, const float*, const int64_t*, const float*, float*, int32_t, const int32_t*,
+                       uint8_t*, int32_t, int32_t, float, float, int64_t*, bp_stream_t);
 }
 
 namespace bp {
@@ -191,7 +196,8 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   // on their own stream: they depend only on the trace, so they overlap the
   // training of the iterations ahead of them.
   BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->planq, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
-  int rc = bp_store_create(ctx, sc, cfg->seed, e->compute, &e->store);
+  int rc = bp_store_create_ex(ctx, sc, cfg->seed, cfg->init_dims > 0 ? cfg->init_dims : sc->emb_dim, e->compute,
+                              &e->store);
   if (rc) return rc;
   rc = bp_cache_create(ctx, sc, cfg->capacity, cfg->dim, &e->cache);
   if (rc) return rc;
@@ -459,18 +465,12 @@ extern "C" int bp_engine_flush(bp_engine* e, const int32_t* chunk_slots, int32_t
   return BP_OK;
 }
 
-// One training iteration on the compute stream (reference engine.py:525-606):
-// apply the staged prefetch (insert, minus an optional dropped first key),
-// TTL updates + lookup, next-batch stamp, fused trainer, eviction of
-// ttl <= iteration into ``chunk_slot`` (and a full drain into
-// ``drain_slot`` on the last iteration).  Synchronises the compute stream
-// once and fills ``out``; device contract violations come back in out->err.
-extern "C" int bp_engine_train(bp_engine* e, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
-                               int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out) {
-  using namespace bp;
-  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
-  if (!P) return BP_ERR_ENGINE;
-  PlanSlot& ps = e->plans[plan_slot];
+namespace bp {
+
+// Apply plan x (insert of its staged rows minus an optional dropped first
+// key), TTL updates + lookup into slots_s, and stamp the next batch's keys.
+static int engine_apply(bp_engine* e, bp_prep* P, PlanSlot& ps, int64_t next_pos, uint64_t skip_key,
+                        int32_t has_skip, bp_prep** next_out) {
   cudaStream_t s = e->compute;
   const int dim = e->cfg.dim;
   BP_CUDA_TRY(cudaStreamWaitEvent(s, ps.fetched, 0));
@@ -490,19 +490,31 @@ extern "C" int bp_engine_train(bp_engine* e, int64_t pos, int32_t plan_slot, int
   }
   BP_CUDA_TRY(cudaMemsetAsync(e->stats, 0, 2 * sizeof(int64_t), s));
   stage_end(e, kStageApply, s);
-  bp_cache_view cv;
-  bp_cache_get_view(e->cache, &cv);
-  stage_begin(e, kStageTrainer, s);
-  rc = bp_stub_step(e->ctx, P, cv.d_values, e->slots_s, cv.d_dirty, dim, e->cfg.c_value, e->cfg.c_label, e->cfg.lr,
-                    BP_STUB_SGD, nullptr, N ? e->mark : nullptr, N ? N->iteration : 0, e->stats, s);
-  stage_end(e, kStageTrainer, s);
-  if (rc) return rc;
+  *next_out = N;
+  return BP_OK;
+}
+
+__global__ void k_count_critical(const uint32_t* __restrict__ ids, const long long* __restrict__ d_U,
+                                 const int64_t* __restrict__ mark, long long tag, unsigned long long* stats) {
+  const long long U = *d_U;
+  unsigned long long c = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < U; i += (long long)gridDim.x * blockDim.x)
+    c += mark[ids[i]] == tag;
+  c = warp_sum(c);
+  if (lane_id() == 0 && c) atomicAdd(stats, c);
+}
+
+// Eviction of ttl <= iteration into chunk_slot (+ full drain into drain_slot
+// on the last iteration), counters to the host, one synchronisation.
+static int engine_finish(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_slot, int32_t drain_slot,
+                         bp_step_result* out) {
+  cudaStream_t s = e->compute;
   BP_CUDA_TRY(cudaEventRecord(ps.consumed, s));
   ChunkSlot& c = e->chunks[chunk_slot];
   BP_CUDA_TRY(cudaStreamWaitEvent(s, c.flushed, 0));  // its previous contents are durable
   bp_evict_buffers eb{e->cfg.record_keys ? c.keys : nullptr, c.ids, c.rows, c.dirty, c.count};
   stage_begin(e, kStageEvict, s);
-  rc = bp_cache_evict(e->cache, P->iteration, 0, &eb, e->chunk_cap, s);
+  int rc = bp_cache_evict(e->cache, P->iteration, 0, &eb, e->chunk_cap, s);
   stage_end(e, kStageEvict, s);
   if (rc) return rc;
   c.pending = true;
@@ -533,6 +545,78 @@ extern "C" int bp_engine_train(bp_engine* e, int64_t pos, int32_t plan_slot, int
   out->drained_dirty = h[7];
   out->err = err;
   return BP_OK;
+}
+
+}  // namespace bp
+
+// One stub-mode training iteration on the compute stream (reference
+// engine.py:525-606): apply plan + lookup + next-batch stamp, fused trainer,
+// eviction; synchronises once and fills ``out`` (device contract violations
+// come back in out->err).
+extern "C" int bp_engine_train(bp_engine* e, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
+                               int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out) {
+  using namespace bp;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  PlanSlot& ps = e->plans[plan_slot];
+  bp_prep* N = nullptr;
+  int rc = engine_apply(e, P, ps, next_pos, skip_key, has_skip, &N);
+  if (rc) return rc;
+  bp_cache_view cv;
+  bp_cache_get_view(e->cache, &cv);
+  stage_begin(e, kStageTrainer, e->compute);
+  rc = bp_stub_step(e->ctx, P, cv.d_values, e->slots_s, cv.d_dirty, e->cfg.dim, e->cfg.c_value, e->cfg.c_label,
+                    e->cfg.lr, BP_STUB_SGD, nullptr, N ? e->mark : nullptr, N ? N->iteration : 0, e->stats,
+                    e->compute);
+  stage_end(e, kStageTrainer, e->compute);
+  if (rc) return rc;
+  return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
+}
+
+// DLRM mode, part 1: apply plan x and gather the batch's pooled embeddings
+// (single-key bags) into d_pooled[n_occ][model_dim] on the compute stream.
+extern "C" int bp_engine_dlrm_forward(bp_engine* e, int64_t pos, int32_t plan_slot, int64_t next_pos,
+                                      uint64_t skip_key, int32_t has_skip, int32_t model_dim, float* d_pooled) {
+  using namespace bp;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  PlanSlot& ps = e->plans[plan_slot];
+  bp_prep* N = nullptr;
+  int rc = engine_apply(e, P, ps, next_pos, skip_key, has_skip, &N);
+  if (rc) return rc;
+  if (N) {
+    k_count_critical<<<grid_for(P->n_occ, 256), 256, 0, e->compute>>>(P->d_uniq_id_s, P->d_num_unique, e->mark,
+                                                                      N->iteration,
+                                                                      (unsigned long long*)e->stats);
+    BP_LAUNCH_CHECK();
+  }
+  bp_cache_view cv;
+  bp_cache_get_view(e->cache, &cv);
+  stage_begin(e, kStageTrainer, e->compute);
+  rc = bp_embbag_forward(P, cv.d_values, e->cfg.dim, e->slots_s, model_dim, nullptr, P->n_occ, 0, nullptr, d_pooled,
+                         e->compute);
+  stage_end(e, kStageTrainer, e->compute);
+  return rc;
+}
+
+// DLRM mode, part 2: EmbeddingBag backward + optimizer in place on the cached
+// rows (gradient of the pooled rows in d_grad, produced by the dense model on
+// the compute stream), then eviction and counters as bp_engine_train.
+extern "C" int bp_engine_dlrm_backward(bp_engine* e, int64_t pos, int32_t plan_slot, const float* d_grad,
+                                       int32_t model_dim, int32_t opt, float lr, float eps, int32_t chunk_slot,
+                                       int32_t drain_slot, bp_step_result* out) {
+  using namespace bp;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  PlanSlot& ps = e->plans[plan_slot];
+  bp_cache_view cv;
+  bp_cache_get_view(e->cache, &cv);
+  stage_begin(e, kStageTrainer, e->compute);
+  int rc = bp_embbag_backward(P, d_grad, nullptr, nullptr, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty,
+                              model_dim, opt, lr, eps, e->stats, e->compute);
+  stage_end(e, kStageTrainer, e->compute);
+  if (rc) return rc;
+  return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
 }
 
 // Evicted keys of a chunk (device -> host), for event logs.

@@ -15,8 +15,8 @@
 namespace bp {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanIpt = 16;
-constexpr int kScanTile = kScanThreads * kScanIpt;  // 4096
+constexpr int kScanIpt = 4;
+constexpr int kScanTile = kScanThreads * kScanIpt;  // 1024
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;

@@ -28,7 +28,7 @@ namespace bp {
 // One thread per (row, 4-component chunk); dims not divisible by 4 use a
 // scalar tail.  FNV over (t, r) is shared by all components of a row.
 __global__ void k_store_init(float* __restrict__ out, long long row0, long long nrows, uint32_t table,
-                             uint64_t seed, int dim) {
+                             uint64_t seed, int dim, int init_dims) {
   const int chunks = (dim + 3) >> 2;
   const long long total = nrows * chunks;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -39,7 +39,7 @@ __global__ void k_store_init(float* __restrict__ out, long long row0, long long 
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int j = c * 4 + q;
-      v[q] = j < dim ? init_component(seed, h_tr, (uint64_t)j) : 0.f;
+      v[q] = j < init_dims ? init_component(seed, h_tr, (uint64_t)j) : 0.f;
     }
     float* dst = out + (row0 + r) * dim + c * 4;
     if ((dim & 3) == 0) {
@@ -141,7 +141,17 @@ __global__ void k_store_write(float* __restrict__ table, uint32_t* __restrict__ 
 
 }  // namespace bp
 
+extern "C" int bp_store_create_ex(bp_ctx* ctx, const bp_schema* sc, uint64_t seed, int32_t init_dims,
+                                  bp_stream_t stream, bp_store** out);
+
 extern "C" int bp_store_create(bp_ctx* ctx, const bp_schema* sc, uint64_t seed, bp_stream_t stream, bp_store** out) {
+  return bp_store_create_ex(ctx, sc, seed, sc->emb_dim, stream, out);
+}
+
+// init_dims < emb_dim: components >= init_dims start at 0 (optimizer state
+// stored next to the weights, e.g. Adagrad accumulators).
+extern "C" int bp_store_create_ex(bp_ctx* ctx, const bp_schema* sc, uint64_t seed, int32_t init_dims,
+                                  bp_stream_t stream, bp_store** out) {
   using namespace bp;
   cudaStream_t s = (cudaStream_t)stream;
   bp_store* st = new bp_store();
@@ -159,7 +169,8 @@ extern "C" int bp_store_create(bp_ctx* ctx, const bp_schema* sc, uint64_t seed, 
   for (int t = 0; t < sc->num_tables; ++t) {
     const long long rows = sc->h_table_base[t + 1] - sc->h_table_base[t];
     k_store_init<<<grid_for(rows * chunks, 256, kNumSMs * 32), 256, 0, s>>>(st->d_table, sc->h_table_base[t], rows,
-                                                                            (uint32_t)t, seed, sc->emb_dim);
+                                                                            (uint32_t)t, seed, sc->emb_dim,
+                                                                            init_dims);
   }
   BP_LAUNCH_CHECK();
   BP_CUDA_TRY(cudaStreamSynchronize(s));

@@ -61,20 +61,22 @@ __device__ __forceinline__ void chain_chunk(const uint32_t (&word)[4], uint32_t 
   }
 }
 
-constexpr int kLongBlocks = 128;       // CTAs reserved for long segments
+constexpr int kLongBlocks = 148;       // CTAs of the long-segment launch (one per SM)
 constexpr int kLongWindowChunks = 1024;  // 16 KB of occurrence bytes staged in smem
 
-// Fused trainer kernel.  CTAs [0, kLongBlocks) take the keys whose segment
-// has >= kLongSeg occurrences (the Zipf-hot rows of tiny tables, up to ~9K
-// per batch at Criteo-Kaggle): the whole CTA stages the key's occurrence
-// bytes in shared memory with coalesced 16-byte loads, then one warp runs the
-// per-component chains from shared memory (broadcast reads, no global
-// latency inside the chain).  All other CTAs handle short segments with one
-// group of G lanes per key (lane = component, DPL components per lane when
-// dim > 32): every per-key load that does not depend on another is issued
-// up front, and the label chunks are prefetched two rounds ahead.
+// Fused trainer, two launches.  k_stub_step_long (first) takes the keys whose
+// segment has >= kLongSeg occurrences (the Zipf-hot rows of tiny tables, up
+// to ~9K per batch at Criteo-Kaggle), longest first: the CTA stages the key's
+// occurrence bytes in shared memory with coalesced 16-byte loads, then one
+// warp runs the per-component chains from shared memory (broadcast reads, no
+// global latency inside the chain).  Running alone keeps the chain warp's
+// issue slots free (3 instructions per occurrence on a 4-cycle add chain).
+// k_stub_step then handles the short segments with one group of G lanes per
+// key (lane = component, DPL components per lane when dim > 32): every
+// per-key load that does not depend on another is issued up front, and the
+// label chunks are prefetched two rounds ahead.
 template <int G, int DPL>
-__global__ void __launch_bounds__(256, 6) k_stub_step(
+__global__ void __launch_bounds__(128) k_stub_step_long(
     const uint32_t* __restrict__ seg_start, const uint8_t* __restrict__ occ_label,
     const long long* __restrict__ d_U, const uint32_t* __restrict__ long_list,
     const long long* __restrict__ d_num_long, long long long_cap, float* __restrict__ rows, const int32_t* __restrict__ row_index,
@@ -85,12 +87,12 @@ __global__ void __launch_bounds__(256, 6) k_stub_step(
   const uint4* __restrict__ chunks = reinterpret_cast<const uint4*>(occ_label);
   const float b0 = __fmul_rn(c_label, -0.5f), b1 = __fmul_rn(c_label, 0.5f);
 
-  if (blockIdx.x < kLongBlocks) {
+  {
     __shared__ uint4 win[kLongWindowChunks];
     const long long n_vlong = d_num_long[0], n_long = n_vlong + d_num_long[1];
     const bool chain_lane = threadIdx.x < G;  // warp 0, lanes [0, G)
     // very long segments first (front of the list), then the others (back)
-    for (long long li = blockIdx.x; li < n_long; li += kLongBlocks) {
+    for (long long li = blockIdx.x; li < n_long; li += gridDim.x) {
       const uint32_t s = li < n_vlong ? long_list[li] : long_list[long_cap - 1 - (li - n_vlong)];
       const uint32_t a = seg_start[s], b = seg_start[s + 1];
       const int32_t row = row_index ? row_index[s] : (int32_t)s;
@@ -150,14 +152,27 @@ __global__ void __launch_bounds__(256, 6) k_stub_step(
     return;
   }
 
+}
+
+template <int G, int DPL>
+__global__ void __launch_bounds__(256, 6) k_stub_step(
+    const uint32_t* __restrict__ seg_start, const uint8_t* __restrict__ occ_label,
+    const long long* __restrict__ d_U, const uint32_t* __restrict__ long_list,
+    const long long* __restrict__ d_num_long, long long long_cap, float* __restrict__ rows, const int32_t* __restrict__ row_index,
+    uint8_t* __restrict__ dirty, int dim, float c_value, float c_label, float lr, int mode,
+    float* __restrict__ grad_out, const uint32_t* __restrict__ my_ids, const int64_t* __restrict__ next_mark,
+    long long next_tag, unsigned long long* __restrict__ stats) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint4* __restrict__ chunks = reinterpret_cast<const uint4*>(occ_label);
+  const float b0 = __fmul_rn(c_label, -0.5f), b1 = __fmul_rn(c_label, 0.5f);
+
   const long long U = *d_U;
   const int lane_g = (int)(lane & (G - 1));
   const unsigned gbase = lane & ~(unsigned)(G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const long long groups_per_block = blockDim.x / G;
-  const long long groups_total = (long long)(gridDim.x - kLongBlocks) * groups_per_block;
-  const long long warp_first =
-      (long long)(blockIdx.x - kLongBlocks) * groups_per_block + (threadIdx.x >> 5) * (32 / G);
+  const long long groups_total = (long long)gridDim.x * groups_per_block;
+  const long long warp_first = (long long)blockIdx.x * groups_per_block + (threadIdx.x >> 5) * (32 / G);
 
   for (long long base = warp_first; base < U; base += groups_total) {
     const long long s = base + (long long)(lane / G);
@@ -333,7 +348,12 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   cudaStream_t s = (cudaStream_t)stream;
   const long long groups = P->n_occ;  // upper bound on U
   const int threads = 256;
-  const int blocks = kLongBlocks + grid_for(groups * G, threads, kNumSMs * 6);
+  const int blocks = grid_for(groups * G, threads, kNumSMs * 6);
+  BP_DISPATCH_GD(G, dpl,
+                 (k_stub_step_long<g_, d_><<<kLongBlocks, 128, 0, s>>>(
+                     P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,
+                     d_row_index, d_dirty, dim, c_value, c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark,
+                     next_tag, (unsigned long long*)d_stats)));
   BP_DISPATCH_GD(G, dpl,
                  (k_stub_step<g_, d_><<<blocks, threads, 0, s>>>(
                      P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,
