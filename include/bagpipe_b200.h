@@ -65,6 +65,11 @@ typedef struct bp_store bp_store;
 
 /* ---------------------------------------------------------------- context */
 const char* bp_version(void);
+/* sizeof of ABI structs (0 bp_error_t, 1 bp_prep_view, 2 bp_plan_buffers,
+ * 3 bp_planner_stats, 4 bp_cache_stats, 5 bp_evict_buffers, 6 bp_cache_view,
+ * 7 bp_engine_config, 8 bp_step_result, 9 bp_engine_parts_t,
+ * 10 bp_planner_dump_t); -1 for an unknown id. */
+int64_t bp_abi_sizeof(int32_t which);
 const char* bp_last_error_message(void);
 int bp_ctx_create(bp_ctx** out);
 int bp_ctx_destroy(bp_ctx* ctx);

@@ -77,7 +77,8 @@ class PlannerDump(C.Structure):
 class EngineConfig(C.Structure):
     _fields_ = [("capacity", c_i64), ("max_occ", c_i64), ("seed", c_u64), ("dim", c_i32), ("num_ranks", c_i32),
                 ("c_value", c_f32), ("c_label", c_f32), ("lr", c_f32), ("record_keys", c_i32),
-                ("plan_slots", c_i32), ("chunk_slots", c_i32), ("prep_slots", c_i32), ("timing", c_i32)]
+                ("plan_slots", c_i32), ("chunk_slots", c_i32), ("prep_slots", c_i32), ("timing", c_i32),
+                ("init_dims", c_i32), ("pad", c_i32)]
 
 
 class StepResult(C.Structure):
@@ -93,6 +94,7 @@ class EngineParts(C.Structure):
 P = C.POINTER
 _SIGS = {
     "bp_version": (C.c_char_p, []),
+    "bp_abi_sizeof": (c_i64, [c_i32]),
     "bp_last_error_message": (C.c_char_p, []),
     "bp_ctx_create": (c_i32, [P(c_vp)]),
     "bp_ctx_destroy": (c_i32, [c_vp]),
@@ -157,6 +159,14 @@ _SIGS = {
     "bp_engine_chunk_view": (c_i32, [c_vp, c_i32, P(EvictBuffers)]),
     "bp_engine_sync": (c_i32, [c_vp]),
     "bp_engine_stage_times": (c_i32, [c_vp, c_vp, c_vp]),
+    "bp_engine_dlrm_forward": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_u64, c_i32, c_i32, c_vp]),
+    "bp_engine_dlrm_backward": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_f32, c_f32, c_i32, c_i32,
+                                        P(StepResult)]),
+    "bp_embbag_forward": (c_i32, [c_vp, c_vp, c_i32, c_vp, c_i32, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "bp_embbag_backward": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32, c_f32,
+                                   c_vp, c_vp]),
+    "bp_prep_occ_sorted_index": (c_i32, [c_vp, c_vp, c_vp]),
+    "bp_store_create_ex": (c_i32, [c_vp, c_vp, c_u64, c_i32, c_vp, P(c_vp)]),
 }
 
 _lock = threading.Lock()
@@ -177,6 +187,12 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         fn = getattr(lib_, name)
         fn.restype = res
         fn.argtypes = args
+    structs = (ErrorT, PrepView, PlanBuffers, PlannerStats, CacheStats, EvictBuffers, CacheView, EngineConfig,
+               StepResult, EngineParts, PlannerDump)
+    for i, st in enumerate(structs):
+        if lib_.bp_abi_sizeof(i) != C.sizeof(st):
+            raise NativeUnavailable(f"ABI mismatch for {st.__name__}: library {lib_.bp_abi_sizeof(i)} bytes, "
+                                    f"binding {C.sizeof(st)} bytes (rebuild the library)")
     return lib_
 
 

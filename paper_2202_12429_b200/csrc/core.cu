@@ -12,6 +12,24 @@ void bp_set_last_error(const char* msg, const char* file, int line) {
 }
 
 extern "C" const char* bp_version(void) { return "bagpipe_b200 0.1.0 sm_100a"; }
+
+// Struct sizes of the ABI, so bindings can reject a stale header/library pair.
+extern "C" int64_t bp_abi_sizeof(int32_t which) {
+  switch (which) {
+    case 0: return (int64_t)sizeof(bp_error_t);
+    case 1: return (int64_t)sizeof(bp_prep_view);
+    case 2: return (int64_t)sizeof(bp_plan_buffers);
+    case 3: return (int64_t)sizeof(bp_planner_stats);
+    case 4: return (int64_t)sizeof(bp_cache_stats);
+    case 5: return (int64_t)sizeof(bp_evict_buffers);
+    case 6: return (int64_t)sizeof(bp_cache_view);
+    case 7: return (int64_t)sizeof(bp_engine_config);
+    case 8: return (int64_t)sizeof(bp_step_result);
+    case 9: return (int64_t)sizeof(bp_engine_parts_t);
+    case 10: return (int64_t)sizeof(bp_planner_dump_t);
+    default: return -1;
+  }
+}
 extern "C" const char* bp_last_error_message(void) { return g_last_error.c_str(); }
 
 static void raise_pool_threshold() {

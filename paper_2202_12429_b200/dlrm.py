@@ -1,0 +1,147 @@
+"""DLRM mode: the BagPipe embedding path feeding a real dense model.
+
+The reference replaces the model with a gradient stub (reference SPEC.md:8,
+trainer.py:1-8); the north star asks for the EmbeddingBag forward/backward
+with SGD/Adagrad on cached rows in front of DLRM's dense MLPs.  The dense
+part (bottom MLP, pairwise-dot interaction, top MLP) stays in PyTorch -- it
+is not the hot path -- and runs on the engine's compute stream between the
+two native halves of an iteration:
+
+    bp_engine_dlrm_forward   apply plan, lookup, EmbeddingBag gather -> pooled
+    (PyTorch)                dense model forward / backward, MLP SGD step
+    bp_engine_dlrm_backward  EmbeddingBag backward + SGD/Adagrad in place,
+                             dirty marking, eviction, counters
+
+Everything else (planner, prefetch, gate, write-back, report) is the
+pipelined engine of engine.py.  No reference counterpart exists, so parity is
+against a PyTorch fp32 CPU model (tests/test_gpu_dlrm.py, rel 1e-5).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+from torch import nn
+
+from . import _lib as L
+from .errors import ConfigurationError
+
+BP_OPT_SGD = 0
+BP_OPT_ADAGRAD = 1
+
+
+def mlp(sizes, last_act: bool) -> nn.Sequential:
+    layers = []
+    for i in range(len(sizes) - 1):
+        layers.append(nn.Linear(sizes[i], sizes[i + 1]))
+        if i < len(sizes) - 2 or last_act:
+            layers.append(nn.ReLU())
+    return nn.Sequential(*layers)
+
+
+class DLRMDense(nn.Module):
+    """Bottom MLP -> pairwise dot interaction with the T pooled embeddings -> top MLP."""
+
+    def __init__(self, num_dense: int, num_tables: int, dim: int, bottom=(512, 256, 64), top=(1024, 1024, 512, 256)):
+        super().__init__()
+        self.num_tables, self.dim = num_tables, dim
+        self.bottom = mlp((num_dense,) + tuple(bottom) + (dim,), last_act=True)
+        n = num_tables + 1
+        self.pairs = n * (n - 1) // 2
+        self.top = mlp((self.pairs + dim,) + tuple(top) + (1,), last_act=False)
+        li, lj = torch.tril_indices(n, n, offset=-1)
+        self.register_buffer("li", li, persistent=False)
+        self.register_buffer("lj", lj, persistent=False)
+
+    def forward(self, dense: torch.Tensor, pooled: torch.Tensor) -> torch.Tensor:
+        x = self.bottom(dense)                                # [B, D]
+        z = torch.cat([x.unsqueeze(1), pooled], dim=1)        # [B, T+1, D]
+        zz = torch.bmm(z, z.transpose(1, 2))                  # [B, T+1, T+1]
+        inter = zz[:, self.li, self.lj]                       # [B, pairs]
+        return self.top(torch.cat([x, inter], dim=1)).squeeze(1)
+
+
+@dataclass
+class DLRMConfig:
+    """Dense model + embedding optimizer for DLRM mode."""
+
+    emb_optimizer: str = "sgd"   # "sgd" | "adagrad"
+    emb_lr: float = 0.01
+    adagrad_eps: float = 1e-10
+    mlp_lr: float = 0.01
+    bottom: tuple = (512, 256, 64)
+    top: tuple = (1024, 1024, 512, 256)
+    mlp_dtype: str = "fp32"      # "fp32" | "bf16" (autocast for the dense MLPs only)
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.emb_optimizer not in ("sgd", "adagrad"):
+            raise ConfigurationError("emb_optimizer must be 'sgd' or 'adagrad'")
+        if self.mlp_dtype not in ("fp32", "bf16"):
+            raise ConfigurationError("mlp_dtype must be 'fp32' or 'bf16'")
+
+    @property
+    def opt_code(self) -> int:
+        return BP_OPT_ADAGRAD if self.emb_optimizer == "adagrad" else BP_OPT_SGD
+
+
+class DLRMTrainer:
+    """Runs the dense model between the two native halves of an iteration."""
+
+    def __init__(self, dcfg: DLRMConfig, num_dense: int, num_tables: int, dim: int, model: DLRMDense | None = None):
+        self.dcfg = dcfg
+        self.dim = dim
+        torch.manual_seed(dcfg.seed)
+        self.model = (model or DLRMDense(num_dense, num_tables, dim, dcfg.bottom, dcfg.top)).cuda()
+        self.opt = torch.optim.SGD(self.model.parameters(), lr=dcfg.mlp_lr)
+        self.losses: list = []
+        self._dense_dev: dict = {}
+
+    def row_width(self) -> int:
+        """Width of a stored row: weights (+ Adagrad accumulators)."""
+        return 2 * self.dim if self.dcfg.opt_code == BP_OPT_ADAGRAD else self.dim
+
+    def set_device_dense(self, pos: int, dense: torch.Tensor, labels: torch.Tensor) -> None:
+        self._dense_dev[pos] = (dense, labels)
+
+    def train(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res) -> None:
+        lib = pipe.lib
+        batch = pipe.batches[pos]
+        n_occ = int(batch.packed_occurrences()[0].size)
+        b = batch.num_examples
+        t = n_occ // max(b, 1)
+        stream = pipe.stream
+        with torch.cuda.stream(stream):
+            pooled = torch.empty((n_occ, self.dim), dtype=torch.float32, device="cuda")
+            L.check(lib.bp_engine_dlrm_forward(pipe.eng, pos, plan.slot, nxt, skip_key, has_skip, self.dim,
+                                               L.ptr(pooled)), "bp_engine_dlrm_forward")
+            dev = self._dense_dev.pop(pos, None)
+            if dev is None:
+                dense = torch.from_numpy(np.ascontiguousarray(batch.dense, dtype=np.float32)).to(
+                    "cuda", non_blocking=False)
+                labels = torch.from_numpy(np.ascontiguousarray(batch.labels, dtype=np.float32)).to("cuda")
+            else:
+                dense, labels = dev
+            emb = pooled.view(b, t, self.dim).requires_grad_(True)
+            if self.dcfg.mlp_dtype == "bf16":
+                with torch.autocast("cuda", dtype=torch.bfloat16):
+                    logits = self.model(dense, emb)
+                logits = logits.float()
+            else:
+                logits = self.model(dense, emb)
+            loss = nn.functional.binary_cross_entropy_with_logits(logits, labels)
+            self.opt.zero_grad(set_to_none=True)
+            loss.backward()
+            self.opt.step()
+            grad = emb.grad.contiguous()
+            self.losses.append(loss.detach())
+            L.check(lib.bp_engine_dlrm_backward(pipe.eng, pos, plan.slot, L.ptr(grad), self.dim, self.dcfg.opt_code,
+                                                float(np.float32(self.dcfg.emb_lr)),
+                                                float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
+                                                C.byref(res)), "bp_engine_dlrm_backward")
+
+    def loss_history(self) -> list:
+        return [float(x) for x in self.losses]

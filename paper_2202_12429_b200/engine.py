@@ -176,7 +176,7 @@ class _Pipeline:
     STAGES = ("prep", "planner", "fetch", "apply", "trainer", "evict", "flush")
 
     def __init__(self, cfg: EngineConfig, schema: Schema, batches: list, fingerprint, fault, device_inputs=None,
-                 timing: bool = False):
+                 timing: bool = False, trainer=None):
         if fault not in (None, FAULT_NO_GATE, FAULT_DROP_PREFETCH):
             raise ConfigurationError(f"unknown fault {fault!r}")
         self.cfg, self.schema, self.batches = cfg, schema, batches
@@ -187,27 +187,33 @@ class _Pipeline:
         self.device_inputs = device_inputs  # optional {pos: (d_keys, d_labels)} already in HBM
         self.probe = None
         self.lib = L.lib()
+        self.trainer = trainer  # None: the reference's stub trainer; else e.g. dlrm.DLRMTrainer
         stub = cfg.stub()
+        # Rows in the cache/store: the embedding (+ optimizer state in DLRM/Adagrad mode).
+        width = trainer.row_width() if trainer is not None else schema.emb_dim
+        self.row_schema = schema if width == schema.emb_dim else Schema(
+            schema.num_tables, schema.rows_per_table, schema.num_dense, width)
 
         self.L0 = cfg.lookahead or auto_lookahead(iter(batches), cfg.cache_capacity, schema=schema)
         self.flush_interval = max(1, math.ceil(cfg.rpc_batch_proportion * self.L0))
         max_occ = max(1, max(int(b.packed_occurrences()[0].size) for b in batches))
         ec = L.EngineConfig(capacity=cfg.cache_capacity, max_occ=max_occ, seed=cfg.seed & 0xFFFFFFFFFFFFFFFF,
-                            dim=schema.emb_dim, num_ranks=self.T, c_value=f32(stub.c_value),
+                            dim=width, num_ranks=self.T, c_value=f32(stub.c_value),
                             c_label=f32(stub.c_label), lr=f32(stub.lr),
                             record_keys=1 if (cfg.record_events or fault == FAULT_NO_GATE) else 0,
                             plan_slots=self.L0 + 4, chunk_slots=self.flush_interval + 4,
-                            prep_slots=2 * self.L0 + 8, timing=1 if timing else 0)
+                            prep_slots=2 * self.L0 + 8, timing=1 if timing else 0, init_dims=schema.emb_dim,
+                            pad=0)
         h = C.c_void_p()
-        L.check(self.lib.bp_engine_create(L.Context.get().handle, DeviceSchema.get(schema).handle, C.byref(ec),
-                                          C.byref(h)), "bp_engine_create")
+        L.check(self.lib.bp_engine_create(L.Context.get().handle, DeviceSchema.get(self.row_schema).handle,
+                                          C.byref(ec), C.byref(h)), "bp_engine_create")
         self.eng = h
         parts = L.EngineParts()
         self.lib.bp_engine_parts(h, C.byref(parts))
         self.parts = parts
         self.stream = torch.cuda.ExternalStream(parts.compute_stream)
         self.link = torch.cuda.ExternalStream(parts.link_stream)
-        self.store = ShardedStore(schema, cfg.num_shards, cfg.seed, _handle=parts.store, _owner=self)
+        self.store = ShardedStore(self.row_schema, cfg.num_shards, cfg.seed, _handle=parts.store, _owner=self)
         self.occupancy = 0
         self.lookahead = self.L0
         self.queue: deque = deque()  # positions of the planner window
@@ -440,12 +446,11 @@ class _Pipeline:
         chunk = self._take_chunk()
         drain = self._take_chunk() if last else -1
         res = self.result
-        if self.probe is not None:
-            self.probe("train", 0, self.stream)
-        L.check(lib.bp_engine_train(self.eng, pos, plan.slot, nxt, skip_key, has_skip, chunk, drain,
-                                    C.byref(res)), "bp_engine_train")
-        if self.probe is not None:
-            self.probe("train", 1, self.stream)
+        if self.trainer is None:
+            L.check(lib.bp_engine_train(self.eng, pos, plan.slot, nxt, skip_key, has_skip, chunk, drain,
+                                        C.byref(res)), "bp_engine_train")
+        else:
+            self.trainer.train(self, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
         if res.err.code:
             L.raise_error_record(res.err)
         self.free_plans.add(plan.slot)
@@ -593,6 +598,21 @@ def run_pipeline(cfg: EngineConfig, schema: Schema, trace: Iterable[Batch], *, t
 
 
 run_bagpipe = run_pipeline
+
+
+def run_dlrm(cfg: EngineConfig, schema: Schema, trace: Iterable[Batch], dlrm_cfg=None, *, trace_fingerprint=None,
+             model=None):
+    """Pipelined BagPipe training of a DLRM (dense MLPs in PyTorch, embedding
+    path native).  Returns (RunReport, DLRMTrainer); batches need dense
+    features (``Batch.dense``)."""
+    from .dlrm import DLRMConfig, DLRMTrainer
+
+    batches = _materialize(trace, cfg.iterations)
+    dcfg = dlrm_cfg or DLRMConfig(emb_lr=cfg.lr, mlp_lr=cfg.lr)
+    trainer = DLRMTrainer(dcfg, schema.num_dense, schema.num_tables, schema.emb_dim, model=model)
+    pipe = _Pipeline(cfg, schema, batches, trace_fingerprint, None, trainer=trainer)
+    report = pipe.run()
+    return report, trainer
 
 
 def run_synchronous_baseline(cfg: EngineConfig, schema: Schema, trace: Iterable[Batch], *,

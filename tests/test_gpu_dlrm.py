@@ -1,0 +1,106 @@
+"""DLRM mode vs a PyTorch fp32 CPU model (no reference counterpart: the
+reference trainer is a stub).  Same initial embeddings (functional init),
+same MLP weights, same SGD/Adagrad; the pipelined GPU engine (cache, plans,
+prefetch, eviction, write-back) must reproduce dense training within
+tolerance: losses rel 1e-4, final embedding tables and MLP weights
+rtol 1e-5 / atol 1e-6."""
+
+from __future__ import annotations
+
+import copy
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import bagpipe_oracle as O
+from paper_2202_12429_b200.traces import Schema, ZipfSpec, batchify_columns, generate_columns
+
+pytestmark = pytest.mark.gpu
+
+SCHEMA = Schema(4, (1000, 500, 50, 7), 13, 16)
+
+
+def _batches(n_batches=8, batch=256, seed=3):
+    rows, labels, dense = generate_columns(ZipfSpec(SCHEMA, 1.05, n_batches * batch, seed))
+    return batchify_columns(rows, labels, dense, batch)
+
+
+def cpu_reference(batches, model, opt_name, lr, eps, seed):
+    tables = [torch.nn.Parameter(torch.from_numpy(O.init_rows(seed, np.full(r, t), np.arange(r), SCHEMA.emb_dim)))
+              for t, r in enumerate(SCHEMA.rows_per_table)]
+    model = copy.deepcopy(model).cpu()
+    mopt = torch.optim.SGD(model.parameters(), lr=lr)
+    eopt = (torch.optim.Adagrad(tables, lr=lr, eps=eps) if opt_name == "adagrad" else torch.optim.SGD(tables, lr=lr))
+    losses = []
+    for b in batches:
+        rows = torch.from_numpy(b.rows)
+        emb = torch.stack([tables[t][rows[:, t]] for t in range(SCHEMA.num_tables)], dim=1)
+        logits = model(torch.from_numpy(b.dense), emb)
+        loss = torch.nn.functional.binary_cross_entropy_with_logits(logits, torch.from_numpy(b.labels.astype(np.float32)))
+        mopt.zero_grad()
+        eopt.zero_grad()
+        loss.backward()
+        mopt.step()
+        eopt.step()
+        losses.append(float(loss))
+    return losses, [t.detach().numpy() for t in tables], model
+
+
+@pytest.mark.parametrize("opt_name", ["sgd", "adagrad"])
+def test_dlrm_pipeline_matches_dense_cpu_training(opt_name):
+    from paper_2202_12429_b200.dlrm import DLRMConfig, DLRMDense
+    from paper_2202_12429_b200.engine import EngineConfig, run_dlrm
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    torch.manual_seed(0)
+    model = DLRMDense(SCHEMA.num_dense, SCHEMA.num_tables, SCHEMA.emb_dim, bottom=(64, 32), top=(64, 32))
+    batches = _batches()
+    lr, eps, seed = 0.05, 1e-10, 7
+    want_losses, want_tables, want_model = cpu_reference(batches, model, opt_name, lr, eps, seed)
+    cfg = EngineConfig(cache_capacity=1200, batch_size=256, lookahead=3, num_shards=1, seed=seed, lr=lr)
+    dcfg = DLRMConfig(emb_optimizer=opt_name, emb_lr=lr, mlp_lr=lr, adagrad_eps=eps, bottom=(64, 32), top=(64, 32))
+    report, trainer = run_dlrm(cfg, SCHEMA, batches, dcfg, model=copy.deepcopy(model))
+    np.testing.assert_allclose(trainer.loss_history(), want_losses, rtol=1e-4)
+    table = report.final_store.table_view()
+    base = SCHEMA.table_base()
+    for t in range(SCHEMA.num_tables):
+        got = table[base[t]:base[t + 1], :SCHEMA.emb_dim]
+        np.testing.assert_allclose(got, want_tables[t], rtol=1e-5, atol=1e-6)
+    for (name, p), (_, q) in zip(trainer.model.named_parameters(), want_model.named_parameters()):
+        np.testing.assert_allclose(p.detach().cpu().numpy(), q.detach().numpy(), rtol=1e-4, atol=1e-6, err_msg=name)
+    assert report.totals["dirty_evictions"] > 0
+
+
+def test_embedding_bag_forward_matches_torch():
+    """Multi-key bags with sum and mean pooling, against torch.nn.functional.embedding_bag."""
+    import ctypes as C
+
+    from paper_2202_12429_b200 import _lib as L
+    from paper_2202_12429_b200.device import DevicePrep
+    from paper_2202_12429_b200.traces import pack_keys
+
+    rng = np.random.default_rng(0)
+    n_rows, dim, n_bags = 300, 16, 500
+    weights = rng.standard_normal((n_rows, dim)).astype(np.float32)
+    lengths = rng.integers(0, 6, n_bags)
+    offsets = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    idx = rng.integers(0, n_rows, offsets[-1]).astype(np.int64)
+    keys = pack_keys(np.zeros_like(idx), idx)
+    prep = DevicePrep(keys, np.zeros(len(idx), np.uint8), np.asarray([0, len(idx)]), 0)
+    u = prep.num_unique
+    # row arena = the weights; slot of sorted unique s = its row id
+    slots = torch.empty(u, dtype=torch.int32, device="cuda")
+    L.check(L.lib().bp_prep_key_rows(prep.handle, L.ptr(slots), L.stream_ptr()), "key rows")
+    occ_s = torch.empty(len(idx), dtype=torch.uint32, device="cuda")
+    L.check(L.lib().bp_prep_occ_sorted_index(prep.handle, L.ptr(occ_s), L.stream_ptr()), "occ_s")
+    d_w = torch.from_numpy(weights).cuda()
+    d_off = torch.from_numpy(offsets).cuda()
+    for mode in (0, 1):
+        out = torch.empty((n_bags, dim), dtype=torch.float32, device="cuda")
+        L.check(L.lib().bp_embbag_forward(prep.handle, L.ptr(d_w), dim, L.ptr(slots), dim, L.ptr(d_off), n_bags,
+                                          mode, L.ptr(occ_s), L.ptr(out), L.stream_ptr()), "fwd")
+        want = torch.nn.functional.embedding_bag(torch.from_numpy(idx), torch.from_numpy(weights),
+                                                 torch.from_numpy(offsets[:-1]), mode="mean" if mode else "sum")
+        np.testing.assert_allclose(out.cpu().numpy(), want.numpy(), rtol=1e-5, atol=1e-6)
