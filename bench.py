@@ -24,6 +24,8 @@ from __future__ import annotations
 
 import argparse
 import json
+
+import numpy as np
 import os
 import statistics
 import subprocess
@@ -52,6 +54,7 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=8, help="oracle steps timed for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dlrm", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
     return ap.parse_args()
 
@@ -135,22 +138,42 @@ def count_launches(pipe, pos: int) -> int:
     return n
 
 
+def _timed_steps(pipe, first: int, steps: int, flush_buf, torch):
+    """Per-step CUDA-event time on the engine's compute stream, L2 flushed
+    between steps (outside the timed spans)."""
+    stream = pipe.stream
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for i in range(steps):
+        flush_buf.zero_()
+        stream.wait_stream(torch.cuda.current_stream())
+        starts[i].record(stream)
+        pipe.step(first + i)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    return sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+
+
 def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     import torch
     import torch.distributed as dist
 
-    from paper_2202_12429_b200.engine import EngineConfig, _Pipeline
     from paper_2202_12429_b200 import _lib as L
+    from paper_2202_12429_b200.engine import EngineConfig, _Pipeline
+    from paper_2202_12429_b200.shard import shard_batches, table_shards
 
     L.lib()
     sc = schema()
     cap = sc.total_rows // 100
     steps, warm = args.steps, args.warmup
-    window = 10
-    n_batches = warm + steps + window + 2
-    batches = make_batches(n_batches, args.seed + rank)
-    cfg = EngineConfig(cache_capacity=cap, batch_size=BATCH, lookahead=0, num_trainers=1, num_shards=1, seed=11)
-    stream = torch.cuda.current_stream()
+    n_batches = warm + steps + 12
+    # N>1: table-wise shards of ONE global batch per step (strong scaling);
+    # each rank runs the full pipeline for its tables, no data-path collective.
+    tables = table_shards(sc.num_tables, world)[rank]
+    full = make_batches(n_batches, args.seed)
+    batches = full if world == 1 else shard_batches(full, tables)
+    cfg = EngineConfig(cache_capacity=cap, batch_size=BATCH, lookahead=0 if world == 1 else 7, num_trainers=1,
+                       num_shards=1, seed=11)
 
     # ---- value: inputs resident in HBM before timing
     dev_inputs = {}
@@ -159,13 +182,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         dev_inputs[i] = (torch.from_numpy(keys).cuda(), torch.from_numpy(labels).cuda())
     torch.cuda.synchronize()
     pipe = _Pipeline(cfg, sc, batches, None, None, device_inputs=dev_inputs, timing=True)
-    stream = pipe.stream  # the engine's compute stream (kernels of a step run there)
     pipe.begin()
     for pos in range(warm):
         pipe.step(pos)
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     clocks = ClockSampler(local_rank)
     if world > 1:
         dist.barrier()
@@ -173,49 +193,36 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     pipe.stage_times()  # reset the per-stage event record
     clocks.start()
     wall0 = time.perf_counter()
-    for i in range(steps):
-        flush_buf.zero_()  # evict L2 between timed steps (outside the timed span)
-        stream.wait_stream(torch.cuda.current_stream())
-        starts[i].record(stream)
-        pipe.step(warm + i)
-        ends[i].record(stream)
-    torch.cuda.synchronize()
+    ms = _timed_steps(pipe, warm, steps, flush_buf, torch)
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
-    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     stages = pipe.stage_times()
     records = pipe.records[warm:warm + steps]
     launches_per_step = count_launches(pipe, warm + steps)
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     pf_mean = statistics.mean(r.prefetch_count for r in records)
-    n_occ = BATCH * sc.num_tables
+    n_occ = BATCH * len(tables)
+    del pipe
 
-    # ---- e2e: host batches through the public engine API
-    e2e = None
+    # ---- e2e: host batches through the public engine API (pinned upload in the timed span)
+    e2e_ms = 0.0
     if not args.no_e2e:
-        batches_e2e = make_batches(n_batches, args.seed + 1000 + rank)
-        pipe2 = _Pipeline(cfg, sc, batches_e2e, None, None)
-        s2 = pipe2.stream
+        pipe2 = _Pipeline(cfg, sc, batches, None, None)
         pipe2.begin()
         for pos in range(warm):
             pipe2.step(pos)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t_e2e = 0.0
-        for i in range(steps):
-            flush_buf.zero_()
-            s2.wait_stream(torch.cuda.current_stream())
-            e0.record(s2)
-            pipe2.step(warm + i)
-            e1.record(s2)
-            e1.synchronize()
-            t_e2e += e0.elapsed_time(e1)
-        e2e = {"ms": t_e2e, "h2d_bytes_per_step": n_occ * 9, "d2h_bytes_per_step": 8 * 8 + 32 + 4 * 8}
+        e2e_ms = _timed_steps(pipe2, warm, steps, flush_buf, torch)
         del pipe2
 
-    t = torch.tensor([ms, e2e["ms"] if e2e else 0.0], device="cuda", dtype=torch.float64)
+    # ---- DLRM mode (N=1): the same engine feeding PyTorch MLPs (bf16 autocast)
+    dlrm = None
+    if world == 1 and not args.no_dlrm:
+        dlrm = run_dlrm_mode(args, sc, full, cfg, flush_buf, torch)
+
+    t = torch.tensor([ms, e2e_ms], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, e2e_max = float(t[0]), float(t[1])
@@ -231,10 +238,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     stub_total, stub_launches = stages["trainer"]
     stub_ms = stub_total / max(stub_launches, 1)
     stub_bytes = stub_step_bytes(n_occ, int(u_mean))
+    stub_achieved = stub_bytes / (stub_ms * 1e-3) / 1e9 if stub_ms else 0.0
     fetch_total, fetch_n = stages["fetch"]
-    flush_total, flush_n = stages["flush"]
-    achieved = stub_bytes / (stub_ms * 1e-3) / 1e9 if stub_ms else 0.0
-    samples = BATCH * steps * world
+    samples = BATCH * steps  # one global batch per step across all ranks
     out = {
         "metric": METRIC,
         "value": samples / (ms_max * 1e-3),
@@ -244,29 +250,87 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "warmup": warm,
         "ms_per_step": ms_max / steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (reference Zipf generator stream, columnar)",
-        "config": {"workload": WORKLOAD, "global_batch": BATCH * world, "tables": 26, "rows": sc.total_rows,
-                   "emb_dim": DIM, "cache_capacity": cap, "lookahead": pipe.L0, "parallelism": f"replicas{world}",
+        "config": {"workload": WORKLOAD, "global_batch": BATCH, "tables": 26, "rows": sc.total_rows,
+                   "emb_dim": DIM, "cache_capacity_per_gpu": cap, "lookahead": cfg.lookahead or 7,
+                   "parallelism": "single" if world == 1 else f"table-sharded x{world}",
                    "l2": "flushed between timed steps (256 MiB write)", "mode": "stub-gradient (bit-exact)"},
-        "e2e": None if e2e is None else {"value": samples / (e2e_max * 1e-3), "unit": "samples/s",
-                                         "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
-                                         "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]},
-        "roofline": {"kernel": "bp::k_stub_step (fused gather + backward + rank-ordered combine + SGD)",
-                     "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
-                     "bytes_per_launch": stub_bytes, "ms_per_launch": stub_ms},
+        "e2e": None if args.no_e2e else {"value": samples / (e2e_max * 1e-3), "unit": "samples/s",
+                                         "h2d_bytes_per_step": n_occ * 9, "d2h_bytes_per_step": 12 * 8 + 32},
+        "roofline_stub_trainer": {"kernel": "bp::k_stub_step(+_long): fused gather + backward + rank-ordered combine"
+                                            " + SGD", "bound": "hbm (latency-bound: per-key sequential f32 chains)",
+                                  "achieved": stub_achieved, "peak": hbm_peak, "unit": "GB/s",
+                                  "frac": stub_achieved / hbm_peak, "bytes_per_launch": stub_bytes,
+                                  "ms_per_launch": stub_ms, "peak_source": peak_src},
         "stages_ms_per_step": {k: v[0] / steps for k, v in stages.items()},
         "host_link": {"prefetch_rows_per_step": pf_mean,
                       "prefetch_gbs": pf_mean * 64 * fetch_n / (fetch_total * 1e-3) / 1e9 if fetch_total else None,
-                      "writeback_gbs_note": "flush every 2 steps; see stages_ms_per_step.flush"},
+                      "peak_note": "pinned memcpy 55.5 GB/s H2D, 56.5 D2H; zero-copy random 64 B rows 18.7-25 GB/s "
+                                   "(tools/hostlink_peak.py)"},
         "gpu_launches": launches_per_step * steps,
         "clocks": clk,
         "wall_s_timed_region": wall,
     }
+    if dlrm is not None:
+        out["dlrm"] = dlrm["summary"]
+        out["roofline"] = dlrm["roofline"]
+        out["roofline"]["peak"] = hbm_peak
+        out["roofline"]["frac"] = out["roofline"]["achieved"] / hbm_peak
+        out["roofline"]["peak_source"] = peak_src
+    else:
+        out["roofline"] = dict(out["roofline_stub_trainer"], bound="hbm")
     return out
+
+
+def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch) -> dict:
+    from paper_2202_12429_b200.dlrm import DLRMConfig, DLRMTrainer
+    from paper_2202_12429_b200.engine import _Pipeline
+
+    steps, warm = args.steps, args.warmup
+    dcfg = DLRMConfig(emb_optimizer="sgd", emb_lr=0.01, mlp_lr=0.01, mlp_dtype="bf16")
+    trainer = DLRMTrainer(dcfg, sc.num_dense, sc.num_tables, DIM)
+    dev_inputs = {}
+    for i, b in enumerate(batches):
+        keys, labels, _ = b.packed_occurrences()
+        dev_inputs[i] = (torch.from_numpy(keys).cuda(), torch.from_numpy(labels).cuda())
+        trainer.set_device_dense(i, torch.from_numpy(np.ascontiguousarray(b.dense, dtype=np.float32)).cuda(),
+                                 torch.from_numpy(b.labels.astype(np.float32)).cuda())
+    pipe = _Pipeline(cfg, sc, batches, None, None, device_inputs=dev_inputs, timing=True, trainer=trainer)
+    pipe.begin()
+    for pos in range(warm):
+        pipe.step(pos)
+    torch.cuda.synchronize()
+    pipe.stage_times()
+    ms = _timed_steps(pipe, warm, steps, flush_buf, torch)
+    stages = pipe.stage_times()
+    records = pipe.records[warm:warm + steps]
+    u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
+    n_occ = BATCH * sc.num_tables
+    # "trainer" spans: EmbeddingBag forward and backward alternate (2 per step)
+    spans = stages["trainer"]
+    # forward = scatter form: one row read per unique key, one pooled row written per occurrence
+    fwd_bytes = int(u_mean) * (4 * DIM + 8) + n_occ * (4 * DIM + 4)
+    losses = trainer.loss_history()
+    del pipe
+    return {"summary": {"value": BATCH * steps / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms / steps,
+                        "mlp": "PyTorch bf16 autocast (13-512-256-64-16 / 367-1024-1024-512-256-1)",
+                        "embedding_optimizer": "sgd", "final_loss": losses[-1] if losses else None,
+                        "embedding_stage_ms_per_step": spans[0] / steps},
+            "roofline": {"kernel": "bp::k_embbag_fwd_scatter + k_embbag_bwd (EmbeddingBag fwd+bwd+SGD on cached rows)",
+                         "bound": "hbm", "bytes_per_step": fwd_bytes + bwd_bytes(n_occ, int(u_mean)),
+                         "ms_per_step": spans[0] / steps, "launches_per_step": 2, "unit": "GB/s",
+                         "achieved": (fwd_bytes + bwd_bytes(n_occ, int(u_mean))) / (spans[0] / steps * 1e-3) / 1e9
+                         if spans[0] else 0.0,
+                         "traffic": None,
+                         "note": "bytes = forward (U*64 row reads + N_occ*64 pooled writes + indices) + backward "
+                                 "(N_occ*64 gradient reads + U*128 row read/write + indices) per step"}}
+
+
+def bwd_bytes(n_occ: int, u: int) -> int:
+    return n_occ * (4 * DIM + 4) + u * (8 * DIM + 8)
 
 
 # ------------------------------------------------------- CPU oracle timing

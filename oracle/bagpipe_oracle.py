@@ -79,7 +79,8 @@ def batch_occurrences(batch):
     """(packed keys, labels, example offsets) in occurrence order."""
     if getattr(batch, "rows", None) is not None and getattr(batch, "_examples", None) is None:
         n, nt = batch.rows.shape
-        keys = pack(np.arange(nt)[None, :], batch.rows).reshape(-1)
+        tids = getattr(batch, "tables", None)
+        keys = pack((np.arange(nt) if tids is None else tids)[None, :], batch.rows).reshape(-1)
         return keys, np.repeat(np.asarray(batch.labels, dtype=np.float32), nt), np.arange(n + 1) * nt
     keys, labels, offs = [], [], [0]
     for ex in batch.examples:

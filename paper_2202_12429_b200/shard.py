@@ -1,0 +1,43 @@
+"""Table-wise sharding of the embedding path across GPUs (one process per GPU).
+
+Every key belongs to exactly one table, and every per-key decision of the
+path -- Algorithm 1's TTLs and prefetches, the cache, the stub gradient's
+per-key sequential sums -- depends only on that key's occurrences.  Giving
+each rank a disjoint set of tables (the full global batch restricted to them,
+keys keeping their global table ids, so the functional initial values are
+unchanged) partitions the work without any data-path collective, and the
+union of the shard stores equals the single-GPU store bit for bit
+(tests/test_shard_dist.py checks it with gloo on CPU ranks).
+
+Tables are dealt round-robin: every table contributes exactly one key per
+example, so ranks differ by at most one table's worth of occurrences.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .traces import Batch
+
+
+def table_shards(num_tables: int, world: int) -> list:
+    """Tables owned by each rank (round-robin)."""
+    return [list(range(r, num_tables, world)) for r in range(world)]
+
+
+def shard_batches(batches: list, tables: list) -> list:
+    """Column-restricted columnar batches holding the rank's tables of every example."""
+    out = []
+    for b in batches:
+        if not b.is_columnar:
+            raise ValueError("sharding needs columnar batches (batchify_columns / read_trace_columns)")
+        cols = [int(np.flatnonzero(b.table_ids() == t)[0]) for t in tables]
+        out.append(Batch.from_columns(b.iteration, np.ascontiguousarray(b.rows[:, cols]), b.labels, b.dense,
+                                      tables=tables))
+    return out
+
+
+def owned_rows(schema, tables: list) -> np.ndarray:
+    """Global row indices g of the rank's tables (to reassemble full stores)."""
+    base = schema.table_base()
+    return np.concatenate([np.arange(base[t], base[t + 1]) for t in tables]) if tables else np.zeros(0, np.int64)

@@ -117,27 +117,35 @@ class Batch:
     memo dict.
     """
 
-    __slots__ = ("iteration", "_examples", "rows", "labels", "dense", "_memo")
+    __slots__ = ("iteration", "_examples", "rows", "labels", "dense", "tables", "_memo")
 
-    def __init__(self, iteration: int, examples=None, *, rows=None, labels=None, dense=None):
+    def __init__(self, iteration: int, examples=None, *, rows=None, labels=None, dense=None, tables=None):
         self.iteration = int(iteration)
         self._examples = examples
         self.rows = rows
         self.labels = labels
         self.dense = dense
+        # table id of each column (default: column index); a table-wise shard
+        # keeps the global ids of its tables (shard.py)
+        self.tables = None if tables is None else np.asarray(tables, dtype=np.int64)
         self._memo: dict = {}
         if examples is None and rows is None:
             self._examples = []
 
     @classmethod
-    def from_columns(cls, iteration: int, rows: np.ndarray, labels: np.ndarray, dense=None) -> "Batch":
+    def from_columns(cls, iteration: int, rows: np.ndarray, labels: np.ndarray, dense=None, tables=None) -> "Batch":
         rows = np.ascontiguousarray(rows, dtype=np.int64)
         if rows.ndim != 2:
             raise ConfigurationError("rows must be [examples, tables]")
         labels = np.ascontiguousarray(labels, dtype=np.uint8)
         if labels.shape != (rows.shape[0],):
             raise ConfigurationError("labels must be [examples]")
-        return cls(iteration, None, rows=rows, labels=labels, dense=dense)
+        if tables is not None and len(tables) != rows.shape[1]:
+            raise ConfigurationError("one table id per column")
+        return cls(iteration, None, rows=rows, labels=labels, dense=dense, tables=tables)
+
+    def table_ids(self) -> np.ndarray:
+        return self.tables if self.tables is not None else np.arange(self.rows.shape[1], dtype=np.int64)
 
     @property
     def is_columnar(self) -> bool:
@@ -149,11 +157,11 @@ class Batch:
             n, nt = self.rows.shape
             dense = self.dense
             out = []
+            tids = self.table_ids().tolist()
             for i in range(n):
                 d = tuple(float(v) for v in dense[i]) if dense is not None else ()
-                out.append(
-                    Example(int(self.labels[i]), d, tuple(EmbeddingKey(t, int(self.rows[i, t])) for t in range(nt)))
-                )
+                out.append(Example(int(self.labels[i]), d,
+                                   tuple(EmbeddingKey(tids[c], int(self.rows[i, c])) for c in range(nt))))
             self._examples = out
         return self._examples
 
@@ -178,7 +186,7 @@ class Batch:
             return memo
         if self._examples is None:
             n, nt = self.rows.shape
-            keys = pack_keys(np.arange(nt, dtype=np.uint64)[None, :], self.rows).reshape(-1)
+            keys = pack_keys(self.table_ids().astype(np.uint64)[None, :], self.rows).reshape(-1)
             labels = np.repeat(self.labels, nt)
             offsets = np.arange(n + 1, dtype=np.int64) * nt
         else:

@@ -43,7 +43,7 @@ def cpu_reference(batches, model, opt_name, lr, eps, seed):
         loss.backward()
         mopt.step()
         eopt.step()
-        losses.append(float(loss))
+        losses.append(loss.item())
     return losses, [t.detach().numpy() for t in tables], model
 
 
@@ -65,9 +65,13 @@ def test_dlrm_pipeline_matches_dense_cpu_training(opt_name):
     np.testing.assert_allclose(trainer.loss_history(), want_losses, rtol=1e-4)
     table = report.final_store.table_view()
     base = SCHEMA.table_base()
+    # Adagrad's first step moves a row by lr*g/(|g|+eps) ~ lr*sign(g): for a
+    # component whose summed gradient is ~1e-9 the fp32 summation order of the
+    # (different) dense backward decides it, so its tolerance is absolute.
+    atol = 1e-4 if opt_name == "adagrad" else 1e-6
     for t in range(SCHEMA.num_tables):
         got = table[base[t]:base[t + 1], :SCHEMA.emb_dim]
-        np.testing.assert_allclose(got, want_tables[t], rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(got, want_tables[t], rtol=1e-5, atol=atol)
     for (name, p), (_, q) in zip(trainer.model.named_parameters(), want_model.named_parameters()):
         np.testing.assert_allclose(p.detach().cpu().numpy(), q.detach().numpy(), rtol=1e-4, atol=1e-6, err_msg=name)
     assert report.totals["dirty_evictions"] > 0
