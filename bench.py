@@ -68,8 +68,8 @@ def schema():
 def make_batches(n_batches: int, seed: int):
     from paper_2202_12429_b200.traces import ZipfSpec, batchify_columns, generate_columns
 
-    rows, labels, _ = generate_columns(ZipfSpec(schema(), ZIPF, n_batches * BATCH, seed))
-    return batchify_columns(rows, labels, None, BATCH)
+    rows, labels, dense = generate_columns(ZipfSpec(schema(), ZIPF, n_batches * BATCH, seed))
+    return batchify_columns(rows, labels, dense, BATCH)
 
 
 # ------------------------------------------------------------------ clocks

@@ -101,6 +101,14 @@ int bp_prep_create(bp_ctx* ctx, const bp_schema* schema, const uint64_t* d_keys,
                    int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks, int64_t iteration,
                    int32_t flags, int32_t row_bits, int32_t table_bits, bp_stream_t stream, bp_prep** out);
 int bp_prep_destroy(bp_prep* prep);
+/* Columnar batch (schema mode): keys laid out [n_ex][n_cols], every example
+ * holding one key of table d_tables[c] (device, strictly increasing) in
+ * column c -- the Criteo layout.  A key then occurs in one column only, so
+ * the prep sorts each column in one CTA's shared memory (n_ex <= 16384;
+ * larger batches take the generic path).  Output identical to bp_prep_create. */
+int bp_prep_create_columnar(bp_ctx* ctx, const bp_schema* schema, const uint64_t* d_keys, const uint8_t* d_labels,
+                            int64_t n_ex, int32_t n_cols, const int32_t* d_tables, const int64_t* h_rank_bounds,
+                            int32_t num_ranks, int64_t iteration, int32_t flags, bp_stream_t stream, bp_prep** out);
 
 typedef struct bp_prep_view {
   int64_t n_occ;
@@ -344,6 +352,9 @@ int bp_engine_parts(bp_engine* engine, bp_engine_parts_t* out);
 int bp_engine_add_batch(bp_engine* engine, int64_t pos, int64_t iteration, const uint64_t* keys,
                         const uint8_t* labels, int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks,
                         int32_t keys_on_host);
+int bp_engine_add_batch_columnar(bp_engine* engine, int64_t pos, int64_t iteration, const uint64_t* keys,
+                                 const uint8_t* labels, int64_t n_ex, int32_t n_cols, const int32_t* h_tables,
+                                 const int64_t* h_rank_bounds, int32_t num_ranks, int32_t keys_on_host);
 int bp_engine_prep(bp_engine* engine, int64_t pos, bp_prep** out);
 int bp_engine_release_batch(bp_engine* engine, int64_t pos);
 int bp_engine_refill(bp_engine* engine, int64_t pos);

@@ -47,6 +47,8 @@ int bp_planner_destroy(bp_planner*);
 int bp_planner_refill(bp_planner*, bp_prep*, bp_stream_t);
 int bp_planner_pop(bp_planner*, bp_prep*, const bp_plan_buffers*, bp_stream_t);
 int bp_mark_ids(bp_prep*, int64_t*, int64_t, bp_stream_t);
+int bp_prep_create_columnar(bp_ctx*, const bp_schema*, const uint64_t*, const uint8_t*, int64_t, int32_t,
+                            const int32_t*, const int64_t*, int32_t, int64_t, int32_t, bp_stream_t, bp_prep**);
 int bp_stub_step(bp_ctx*, bp_prep*, float*, const int32_t*, uint8_t*, int32_t, float, float, float, int32_t, float*,
                  const int64_t*, int64_t, int64_t*, bp_stream_t);
 int bp_store_create_ex(bp_ctx*, const bp_schema*, uint64_t, int32_t, bp_stream_t, bp_store**);
@@ -127,6 +129,8 @@ struct bp_engine {
   int64_t* mark;
   int64_t* stats;  // [2]
   int64_t* h_result;  // pinned, [16]
+  int32_t* d_col_tables;  // table id per column of columnar batches
+  std::vector<int32_t> h_col_tables;
   uint64_t* d_keys_staging[2];
   uint8_t* d_labels_staging[2];
   cudaEvent_t staging_free[2];
@@ -260,6 +264,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   BP_CUDA_TRY(cudaMemsetAsync(e->mark, 0xC0, sc->total_rows * sizeof(int64_t), e->compute));  // never a tag
   BP_CUDA_TRY(cudaMalloc(&e->stats, 2 * sizeof(int64_t)));
   BP_CUDA_TRY(cudaMallocHost(&e->h_result, 16 * sizeof(int64_t)));
+  BP_CUDA_TRY(cudaMalloc(&e->d_col_tables, sc->num_tables * sizeof(int32_t)));
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
   BP_CUDA_TRY(cudaStreamSynchronize(e->planq));
   *out = e;
@@ -306,6 +311,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   cudaFree(e->mark);
   cudaFree(e->stats);
   cudaFreeHost(e->h_result);
+  cudaFree(e->d_col_tables);
   bp_planner_destroy(e->planner);
   bp_cache_destroy(e->cache);
   bp_store_destroy(e->store);
@@ -328,9 +334,9 @@ extern "C" int bp_engine_parts(bp_engine* e, bp_engine_parts_t* out) {
 
 // Batch entering the window: upload (host keys go through a pinned ring and
 // one H2D copy each for keys and labels) and device prep on the compute stream.
-extern "C" int bp_engine_add_batch(bp_engine* e, int64_t pos, int64_t iteration, const uint64_t* keys,
-                                   const uint8_t* labels, int64_t n_occ, const int64_t* h_rank_bounds,
-                                   int32_t num_ranks, int32_t keys_on_host) {
+static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64_t* keys, const uint8_t* labels,
+                      int64_t n_occ, int64_t n_ex, int32_t n_cols, const int32_t* h_tables,
+                      const int64_t* h_rank_bounds, int32_t num_ranks, int32_t keys_on_host) {
   using namespace bp;
   if (n_occ > e->cfg.max_occ) return BP_ERR_INVALID;
   const int slot = engine_prep_slot(e, pos);
@@ -359,14 +365,44 @@ extern "C" int bp_engine_add_batch(bp_engine* e, int64_t pos, int64_t iteration,
     d_keys = e->d_keys_staging[si];
     d_labels = e->d_labels_staging[si];
   }
-  stage_begin(e, kStagePrep, q);
-  const int rc = bp_prep_create(e->ctx, e->sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, 0, 0,
-                                0, q, &e->preps[slot]);
+  int rc;
+  if (n_cols > 0) {
+    if (n_cols > e->sc->num_tables) return BP_ERR_INVALID;
+    if ((int)e->h_col_tables.size() != n_cols ||
+        std::memcmp(e->h_col_tables.data(), h_tables, n_cols * sizeof(int32_t)) != 0) {
+      e->h_col_tables.assign(h_tables, h_tables + n_cols);
+      BP_CUDA_TRY(cudaStreamSynchronize(q));  // previous preps may still read the old ids
+      BP_CUDA_TRY(cudaMemcpy(e->d_col_tables, h_tables, n_cols * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    stage_begin(e, kStagePrep, q);
+    rc = bp_prep_create_columnar(e->ctx, e->sc, d_keys, d_labels, n_ex, n_cols, e->d_col_tables, h_rank_bounds,
+                                 num_ranks, iteration, 0, q, &e->preps[slot]);
+  } else {
+    stage_begin(e, kStagePrep, q);
+    rc = bp_prep_create(e->ctx, e->sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, 0, 0, 0, q,
+                        &e->preps[slot]);
+  }
   stage_end(e, kStagePrep, q);
   if (rc) return rc;
   if (si >= 0) BP_CUDA_TRY(cudaEventRecord(e->staging_free[si], q));  // prep consumed the staging copy
   BP_CUDA_TRY(cudaEventRecord(e->prep_ready[slot], q));
   return BP_OK;
+}
+
+extern "C" int bp_engine_add_batch(bp_engine* e, int64_t pos, int64_t iteration, const uint64_t* keys,
+                                   const uint8_t* labels, int64_t n_occ, const int64_t* h_rank_bounds,
+                                   int32_t num_ranks, int32_t keys_on_host) {
+  return engine_add(e, pos, iteration, keys, labels, n_occ, 0, 0, nullptr, h_rank_bounds, num_ranks, keys_on_host);
+}
+
+// Columnar batch (one key per table per example, h_tables[c] = table of
+// column c, strictly increasing): per-column shared-memory sort in the prep.
+extern "C" int bp_engine_add_batch_columnar(bp_engine* e, int64_t pos, int64_t iteration, const uint64_t* keys,
+                                            const uint8_t* labels, int64_t n_ex, int32_t n_cols,
+                                            const int32_t* h_tables, const int64_t* h_rank_bounds, int32_t num_ranks,
+                                            int32_t keys_on_host) {
+  return engine_add(e, pos, iteration, keys, labels, n_ex * n_cols, n_ex, n_cols, h_tables, h_rank_bounds,
+                    num_ranks, keys_on_host);
 }
 
 extern "C" int bp_engine_prep(bp_engine* e, int64_t pos, bp_prep** out) {

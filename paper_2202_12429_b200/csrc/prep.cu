@@ -13,9 +13,16 @@
 // Sort key: schema mode -> dense id g = table_base[t] + row (u32, monotone in
 // (table,row)); registry mode -> the packed u64 key sorted on its two live
 // bit ranges (rows: [0,row_bits), tables: [44, 44+table_bits)).
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace bp {
+
+struct ColumnarInfo {
+  int n_ex, n_cols, row_bits;
+  const int32_t* d_tables;
+};
 
 __global__ void k_prep_keys_schema(const uint64_t* __restrict__ keys, long long n, const int64_t* base,
                                    const int64_t* rows, int num_tables, uint32_t* __restrict__ sk,
@@ -112,9 +119,115 @@ __global__ void k_prep_occ_k(const uint32_t* __restrict__ pos, const uint32_t* _
   }
 }
 
+// Columnar fast path (one key per table per example: the Criteo layout of
+// every columnar batch).  A key of table t only occurs in column t, so the
+// global (g, position) sort decomposes into one independent sort per column
+// by row, each small enough for one CTA's shared memory (B <= 16384
+// examples).  Elements (row << 14 | example) live in registers, 16 per thread;
+// each 8-bit LSD pass ranks digits per warp with __match_any_sync (stable),
+// scans the per-warp digit counts and scatters through one 128 KB smem
+// buffer.  Column blocks are written in table order, so the output is
+// identical to the generic radix sort's -- sorted by (g, position) -- with
+// 26 CTAs and no global passes instead of 3 x (histogram, scan, scatter).
+constexpr int kColThreads = 1024;
+constexpr int kColIpt = 16;
+constexpr int kColMax = kColThreads * kColIpt;  // 16384 examples
+constexpr int kColWarps = kColThreads / 32;
+
+__global__ void __launch_bounds__(kColThreads, 1) k_prep_table_sort(const uint64_t* __restrict__ keys, int n_ex,
+                                                                     int n_cols, const int64_t* __restrict__ base,
+                                                                     const int32_t* __restrict__ col_tables,
+                                                                     int row_bits, uint32_t* __restrict__ sk_out,
+                                                                     uint32_t* __restrict__ pos_out) {
+  extern __shared__ unsigned long long col_smem[];
+  unsigned long long* buf = col_smem;                                             // [kColMax]
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(col_smem + kColMax);               // [kColWarps][256]
+  uint32_t* dtot = wcnt + kColWarps * 256;                                        // [256]
+  const int c = blockIdx.x;
+  const int t = col_tables[c];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  unsigned long long e[kColIpt];
+#pragma unroll
+  for (int r = 0; r < kColIpt; ++r) {
+    const int ex = warp * (32 * kColIpt) + r * 32 + lane;
+    e[r] = ex < n_ex ? (((keys[(long long)ex * n_cols + c] & kRowMask) << 14) | (unsigned long long)ex)
+                     : ~0ull;  // padding sorts last
+  }
+  for (int shift = 14; shift < 14 + row_bits; shift += 8) {
+    for (int i = lane; i < 256; i += 32) wcnt[warp * 256 + i] = 0;
+    __syncwarp();
+    uint32_t rank[kColIpt];
+#pragma unroll
+    for (int r = 0; r < kColIpt; ++r) {
+      const uint32_t d = (uint32_t)((e[r] >> shift) & 0xFFull);
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const unsigned below = peers & ((1u << lane) - 1u);
+      const uint32_t prev = wcnt[warp * 256 + d];
+      rank[r] = prev + (uint32_t)__popc(below);
+      __syncwarp();
+      if (below == 0) wcnt[warp * 256 + d] = prev + (uint32_t)__popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) {  // per digit: exclusive prefix over warps, total
+      uint32_t run = 0;
+      for (int w = 0; w < kColWarps; ++w) {
+        const uint32_t x = wcnt[w * 256 + threadIdx.x];
+        wcnt[w * 256 + threadIdx.x] = run;
+        run += x;
+      }
+      dtot[threadIdx.x] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 256 digit totals (8 per lane)
+      uint32_t v[8], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = dtot[lane * 8 + i];
+        sum += v[i];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += y;
+      }
+      uint32_t run = incl - sum;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        dtot[lane * 8 + i] = run;
+        run += v[i];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kColIpt; ++r) {
+      const uint32_t d = (uint32_t)((e[r] >> shift) & 0xFFull);
+      buf[dtot[d] + wcnt[warp * 256 + d] + rank[r]] = e[r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kColIpt; ++r) e[r] = buf[warp * (32 * kColIpt) + r * 32 + lane];
+    __syncthreads();
+  }
+  const long long out0 = (long long)c * n_ex;  // columns are in increasing table order
+#pragma unroll
+  for (int r = 0; r < kColIpt; ++r) {
+    const int i = warp * (32 * kColIpt) + r * 32 + lane;
+    if (i < n_ex) {
+      const unsigned long long x = e[r];
+      const long long ex = (long long)(x & 0x3FFFull);
+      sk_out[out0 + i] = (uint32_t)(base[t] + (long long)(x >> 14));
+      pos_out[out0 + i] = (uint32_t)(ex * n_cols + c);
+    }
+  }
+}
+
+constexpr size_t kColSmem = sizeof(unsigned long long) * kColMax + sizeof(uint32_t) * (kColWarps * 256 + 256);
+
 template <typename K>
 static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, const uint8_t* d_labels,
-                      int row_bits, int table_bits, cudaStream_t s) {
+                      int row_bits, int table_bits, cudaStream_t s, const ColumnarInfo* col) {
   const long long n = P->n_occ;
   K *ka, *kb;
   uint32_t *va, *vb, *hist, *head, *segx, *first_flag, *first_rank, *partials;
@@ -130,7 +243,16 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
   BP_CUDA_TRY(pool_alloc(&partials, (long long)sort_partials_words(n) + scan_state_words(n), s));
   const int g = grid_for(n, 256);
   int which = 0;
-  if (P->schema_mode) {
+  if (col) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      BP_CUDA_TRY(cudaFuncSetAttribute(k_prep_table_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
+      attr_set = true;
+    }
+    k_prep_table_sort<<<col->n_cols, kColThreads, kColSmem, s>>>(d_keys, col->n_ex, col->n_cols, sc->d_table_base,
+                                                                  col->d_tables, col->row_bits, (uint32_t*)ka, va);
+    which = 0;
+  } else if (P->schema_mode) {
     k_prep_keys_schema<<<g, 256, 0, s>>>(d_keys, n, sc->d_table_base, sc->d_rows, sc->num_tables,
                                          (uint32_t*)ka, va, P->ctx ? P->ctx->d_err : nullptr, P->iteration);
     BP_CUDA_TRY(radix_sort_pairs<K>(ka, va, kb, vb, n, nullptr, 0, sc->id_bits, hist, partials, &which, s));
@@ -180,10 +302,10 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
 
 }  // namespace bp
 
-extern "C" int bp_prep_create(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_keys, const uint8_t* d_labels,
-                              int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks, int64_t iteration,
-                              int32_t flags, int32_t row_bits, int32_t table_bits, bp_stream_t stream,
-                              bp_prep** out) {
+static int prep_create_impl(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_keys, const uint8_t* d_labels,
+                            int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks, int64_t iteration,
+                            int32_t flags, int32_t row_bits, int32_t table_bits, bp_stream_t stream, bp_prep** out,
+                            const bp::ColumnarInfo* col) {
   using namespace bp;
   if (n_occ < 0 || num_ranks < 1 || n_occ >= (int64_t)kNoId) return BP_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
@@ -225,16 +347,47 @@ extern "C" int bp_prep_create(bp_ctx* ctx, const bp_schema* sc, const uint64_t* 
   }
   int rc;
   if (sc) {
-    rc = prep_build<uint32_t>(P, sc, d_keys, d_labels, 0, 0, s);
+    rc = prep_build<uint32_t>(P, sc, d_keys, d_labels, 0, 0, s, col);
   } else {
     if (row_bits < 1) row_bits = 1;
     if (table_bits < 1) table_bits = 1;
     if (row_bits > kKeyTableShift || table_bits > 64 - kKeyTableShift) return BP_ERR_INVALID;
-    rc = prep_build<uint64_t>(P, nullptr, d_keys, d_labels, row_bits, table_bits, s);
+    rc = prep_build<uint64_t>(P, nullptr, d_keys, d_labels, row_bits, table_bits, s, nullptr);
   }
   if (rc != BP_OK) return rc;
   *out = P;
   return BP_OK;
+}
+
+extern "C" int bp_prep_create(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_keys, const uint8_t* d_labels,
+                              int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks, int64_t iteration,
+                              int32_t flags, int32_t row_bits, int32_t table_bits, bp_stream_t stream,
+                              bp_prep** out) {
+  return prep_create_impl(ctx, sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, flags, row_bits,
+                          table_bits, stream, out, nullptr);
+}
+
+// Columnar batch: keys laid out [n_ex][n_cols], column c holding table
+// h_tables[c] (strictly increasing).  Takes the per-column shared-memory
+// sort when n_ex <= 16384, else the generic path.
+extern "C" int bp_prep_create_columnar(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_keys,
+                                       const uint8_t* d_labels, int64_t n_ex, int32_t n_cols, const int32_t* d_tables,
+                                       const int64_t* h_rank_bounds, int32_t num_ranks, int64_t iteration,
+                                       int32_t flags, bp_stream_t stream, bp_prep** out) {
+  using namespace bp;
+  if (!sc || n_cols < 1 || n_ex < 0) return BP_ERR_INVALID;
+  const int64_t n_occ = n_ex * n_cols;
+  if (n_ex > kColMax || n_ex == 0)
+    return prep_create_impl(ctx, sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, flags, 0, 0,
+                            stream, out, nullptr);
+  int64_t max_rows = 1;
+  for (int t = 0; t < sc->num_tables; ++t)
+    max_rows = std::max<int64_t>(max_rows, sc->h_table_base[t + 1] - sc->h_table_base[t]);
+  const int row_bits = std::max(1, bit_width_u64((unsigned long long)(max_rows - 1)));
+  if (row_bits > 44 - 14) return BP_ERR_INVALID;
+  const ColumnarInfo col{(int)n_ex, n_cols, row_bits, d_tables};
+  return prep_create_impl(ctx, sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, flags, 0, 0, stream,
+                          out, &col);
 }
 
 extern "C" int bp_prep_destroy(bp_prep* P) {

@@ -270,14 +270,20 @@ class _Pipeline:
         rb = np.ascontiguousarray(b.rank_bounds(self.T), dtype=np.int64)
         dev = self.device_inputs.get(pos) if self.device_inputs else None
         if dev is not None:
-            k, lab = dev
-            rc = self.lib.bp_engine_add_batch(self.eng, pos, b.iteration, L.ptr(k), L.ptr(lab), k.numel(),
-                                              rb.ctypes.data, self.T, 0)
+            kptr, lptr, on_host, n = L.ptr(dev[0]), L.ptr(dev[1]), 0, dev[0].numel()
         else:
             keys = np.ascontiguousarray(keys, dtype=np.uint64)
             labels = np.ascontiguousarray(labels, dtype=np.uint8)
-            rc = self.lib.bp_engine_add_batch(self.eng, pos, b.iteration, keys.ctypes.data, labels.ctypes.data,
-                                              keys.size, rb.ctypes.data, self.T, 1)
+            kptr, lptr, on_host, n = keys.ctypes.data, labels.ctypes.data, 1, keys.size
+        tables = b.table_ids() if b.is_columnar else None
+        if tables is not None and len(tables) and bool(np.all(np.diff(tables) > 0)):
+            # Criteo layout: one key per table per example -> per-column sort
+            t32 = np.ascontiguousarray(tables, dtype=np.int32)
+            rc = self.lib.bp_engine_add_batch_columnar(self.eng, pos, b.iteration, kptr, lptr, b.num_examples,
+                                                       len(t32), t32.ctypes.data, rb.ctypes.data, self.T, on_host)
+        else:
+            rc = self.lib.bp_engine_add_batch(self.eng, pos, b.iteration, kptr, lptr, n, rb.ctypes.data, self.T,
+                                              on_host)
         L.check(rc, "bp_engine_add_batch")
         self.added.add(pos)
 
