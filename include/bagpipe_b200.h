@@ -97,6 +97,7 @@ int64_t bp_schema_total_rows(const bp_schema* schema);
  * (registry mode only): bit widths of the largest row / table id, so the
  * sort runs only over live key bits. */
 #define BP_PREP_OCC_INDEX 1
+#define BP_PREP_OCC_SORTED 2 /* occurrence -> key-sorted unique index (EmbeddingBag gather) */
 int bp_prep_create(bp_ctx* ctx, const bp_schema* schema, const uint64_t* d_keys, const uint8_t* d_labels,
                    int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks, int64_t iteration,
                    int32_t flags, int32_t row_bits, int32_t table_bits, bp_stream_t stream, bp_prep** out);
@@ -149,7 +150,8 @@ typedef struct bp_plan_buffers {
   int64_t* d_prefetch_ttls;   /* ttl of each prefetched key */
   int64_t* d_ttl_k;           /* ttl per unique key, first-occurrence order */
   uint64_t* d_evict_keys;     /* planner's evict set {e : ttl == iteration}, sorted */
-  int64_t* d_counts;          /* [4]: n_prefetch, n_evict, projected, resident_before */
+  uint32_t* d_evict_ids;      /* dense ids of the above (may be NULL) */
+  int64_t* d_counts;          /* [5]: n_prefetch, n_evict, projected, resident_before, resident_after */
 } bp_plan_buffers;
 
 typedef struct bp_planner_stats {
@@ -235,6 +237,14 @@ int bp_cache_evict(bp_cache* cache, int64_t completed, int32_t drain, const bp_e
  * CACHE_MISS (index | 1<<40 marks the resolve phase). */
 int bp_cache_apply_resolve(bp_cache* cache, bp_prep* prep, const int64_t* d_ttl_k, uint64_t skip_key,
                            int32_t has_skip, int32_t* d_slots_s, bp_stream_t stream);
+/* Eviction of a planned, key-sorted evict set (engine fast path): releases
+ * exactly d_ids[0..*d_n) (ENGINE error if one is not resident) into *out in
+ * that order, then checks the cache occupancy against *d_expect (the
+ * planner mirror's size after the batch): any divergence from the
+ * ttl <= iteration scan semantics of bp_cache_evict is an ENGINE error. */
+int bp_cache_evict_planned(bp_cache* cache, const uint64_t* d_keys, const uint32_t* d_ids, const int64_t* d_n,
+                           int64_t n_max, const int64_t* d_expect, int64_t iteration, const bp_evict_buffers* out,
+                           bp_stream_t stream);
 /* content_checksum (reference cache.py:249-272) into a device u64. */
 int bp_cache_checksum(bp_cache* cache, uint64_t* d_out, bp_stream_t stream);
 /* Raw views for inspection (device pointers). */
@@ -331,7 +341,7 @@ typedef struct bp_engine_config {
   int32_t plan_slots, chunk_slots, prep_slots;
   int32_t timing;      /* record per-stage CUDA events (bp_engine_stage_times) */
   int32_t init_dims;   /* store: components >= init_dims start at 0 (0 = all initialised) */
-  int32_t pad;
+  int32_t prep_flags;  /* BP_PREP_* for every batch prep (BP_PREP_OCC_SORTED in DLRM mode) */
 } bp_engine_config;
 typedef struct bp_step_result {
   int64_t unique, inserted, critical, dirty_keys, evicted, evicted_dirty, drained, drained_dirty;
@@ -388,9 +398,10 @@ int bp_engine_stage_times(bp_engine* engine, double* h_ms7, int64_t* h_counts7);
  * model within tolerance).  Rows are read from a row arena (the cache) with
  * row_stride >= dim; optimizer state (Adagrad) sits at [dim, 2*dim).
  * forward: d_bag_offsets NULL => one occurrence per bag (bag = occurrence
- * position, Criteo layout): each key's row is read once and scattered to its
- * occurrences; otherwise bags [off[b], off[b+1]) of occurrences are summed
- * (mode 1: mean) using d_occ_s from bp_prep_occ_sorted_index.
+ * position, Criteo layout): pooled row p = cached row of occurrence p;
+ * otherwise bags [off[b], off[b+1]) of occurrences are summed (mode 1: mean).
+ * Both read the occurrence -> unique map d_occ_s (BP_PREP_OCC_SORTED prep,
+ * or bp_prep_occ_sorted_index).
  * backward: per unique key g = sum of its occurrences' bag gradients
  * (x d_bag_scale[bag] if given), then SGD or Adagrad in place; dirty marks
  * rows with g != 0; d_stats[1] += number of such keys. */

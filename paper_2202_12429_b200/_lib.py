@@ -46,7 +46,7 @@ class PrepView(C.Structure):
 class PlanBuffers(C.Structure):
     _fields_ = [
         ("d_prefetch_keys", c_vp), ("d_prefetch_ids", c_vp), ("d_prefetch_ttls", c_vp), ("d_ttl_k", c_vp),
-        ("d_evict_keys", c_vp), ("d_counts", c_vp),
+        ("d_evict_keys", c_vp), ("d_evict_ids", c_vp), ("d_counts", c_vp),
     ]
 
 
@@ -78,7 +78,7 @@ class EngineConfig(C.Structure):
     _fields_ = [("capacity", c_i64), ("max_occ", c_i64), ("seed", c_u64), ("dim", c_i32), ("num_ranks", c_i32),
                 ("c_value", c_f32), ("c_label", c_f32), ("lr", c_f32), ("record_keys", c_i32),
                 ("plan_slots", c_i32), ("chunk_slots", c_i32), ("prep_slots", c_i32), ("timing", c_i32),
-                ("init_dims", c_i32), ("pad", c_i32)]
+                ("init_dims", c_i32), ("prep_flags", c_i32)]
 
 
 class StepResult(C.Structure):
@@ -125,6 +125,7 @@ _SIGS = {
     "bp_cache_gather": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "bp_cache_update": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bp_cache_evict": (c_i32, [c_vp, c_i64, c_i32, P(EvictBuffers), c_i64, c_vp]),
+    "bp_cache_evict_planned": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, P(EvictBuffers), c_vp]),
     "bp_cache_checksum": (c_i32, [c_vp, c_vp, c_vp]),
     "bp_cache_get_view": (c_i32, [c_vp, P(CacheView)]),
     "bp_store_create": (c_i32, [c_vp, c_vp, c_u64, c_vp, P(c_vp)]),

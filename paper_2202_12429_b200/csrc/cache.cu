@@ -239,6 +239,56 @@ __global__ void k_evict_out(const uint32_t* __restrict__ flag, const uint32_t* _
   if (lane_id() == 0 && nd) atomicAdd(n_dirty, nd);
 }
 
+__global__ void k_evict_planned(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ids,
+                                const long long* __restrict__ d_n, long long n_max, int dim,
+                                const float* __restrict__ values, uint8_t* __restrict__ dirty,
+                                uint8_t* __restrict__ used, int32_t* __restrict__ slot_of,
+                                const CacheCounters* __restrict__ ctr, uint32_t* __restrict__ free_list,
+                                uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_ids,
+                                float* __restrict__ out_rows, uint8_t* __restrict__ out_dirty,
+                                long long* __restrict__ out_count, ErrorRecord* err, long long iteration) {
+  const long long n = load_count(n_max, d_n);
+  const long long top = ctr->free_top;
+  unsigned long long nd = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t id = ids[i];
+    const int32_t slot = slot_of[id];
+    if (slot < 0) {
+      raise_error(err, BP_ERR_ENGINE, iteration, (1ll << 41) | i, keys[i]);
+      continue;
+    }
+    const uint8_t dty = dirty[slot];
+    nd += dty;
+    if (out_keys) out_keys[i] = keys[i];
+    out_ids[i] = id;
+    out_dirty[i] = dty;
+    if ((dim & 3) == 0) {
+      const float4* src = reinterpret_cast<const float4*>(values + (long long)slot * dim);
+      float4* dst = reinterpret_cast<float4*>(out_rows + i * dim);
+      for (int d = 0; d < (dim >> 2); ++d) dst[d] = src[d];
+    } else {
+      for (int d = 0; d < dim; ++d) out_rows[i * dim + d] = values[(long long)slot * dim + d];
+    }
+    slot_of[id] = -1;
+    used[slot] = 0;
+    dirty[slot] = 0;
+    free_list[top + i] = (uint32_t)slot;
+  }
+  nd = warp_sum(nd);
+  if (lane_id() == 0 && nd) atomicAdd((unsigned long long*)&out_count[1], nd);
+}
+
+__global__ void k_evict_planned_end(CacheCounters* ctr, const long long* d_n, long long n_max,
+                                    const int64_t* d_expect, long long* out_count, ErrorRecord* err,
+                                    long long iteration) {
+  const long long n = load_count(n_max, d_n);
+  ctr->free_top += n;
+  ctr->occupancy -= n;
+  ctr->evictions += n;
+  out_count[0] = n;
+  if (d_expect && ctr->occupancy != *d_expect) raise_error(err, BP_ERR_ENGINE, iteration, 1ll << 41, 0);
+}
+
 __global__ void k_evict_end(CacheCounters* ctr, const long long* d_count, long long out_cap) {
   const long long cnt = *d_count;
   if (cnt > out_cap) return;
@@ -511,6 +561,22 @@ extern "C" int bp_cache_evict(bp_cache* c, int64_t completed, int32_t drain, con
                                                o->d_rows, o->d_dirty, (unsigned long long*)&o->d_count[1],
                                                c->ctx ? c->ctx->d_err : nullptr, completed);
   k_evict_end<<<1, 1, 0, s>>>(c->d_ctr, (const long long*)o->d_count, out_capacity);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_cache_evict_planned(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids, const int64_t* d_n,
+                                      int64_t n_max, const int64_t* d_expect, int64_t iteration,
+                                      const bp_evict_buffers* o, bp_stream_t stream) {
+  using namespace bp;
+  cudaStream_t s = (cudaStream_t)stream;
+  BP_CUDA_TRY(cudaMemsetAsync(o->d_count, 0, 2 * sizeof(int64_t), s));
+  ErrorRecord* err = c->ctx ? c->ctx->d_err : nullptr;
+  k_evict_planned<<<grid_for(n_max, 256, kNumSMs * 4), 256, 0, s>>>(
+      d_keys, d_ids, (const long long*)d_n, n_max, c->dim, c->d_values, c->d_dirty, c->d_used, c->d_slot_of, c->d_ctr,
+      c->d_free, o->d_keys, o->d_ids, o->d_rows, o->d_dirty, (long long*)o->d_count, err, iteration);
+  k_evict_planned_end<<<1, 1, 0, s>>>(c->d_ctr, (const long long*)d_n, n_max, d_expect, (long long*)o->d_count, err,
+                                      iteration);
   BP_LAUNCH_CHECK();
   return BP_OK;
 }

@@ -41,6 +41,8 @@ int bp_cache_insert(bp_cache*, const uint64_t*, const uint32_t*, const float*, c
                     const int64_t*, int64_t, bp_stream_t);
 int bp_cache_apply_resolve(bp_cache*, bp_prep*, const int64_t*, uint64_t, int32_t, int32_t*, bp_stream_t);
 int bp_cache_evict(bp_cache*, int64_t, int32_t, const bp_evict_buffers*, int64_t, bp_stream_t);
+int bp_cache_evict_planned(bp_cache*, const uint64_t*, const uint32_t*, const int64_t*, int64_t, const int64_t*,
+                           int64_t, const bp_evict_buffers*, bp_stream_t);
 int bp_cache_get_view(const bp_cache*, bp_cache_view*);
 int bp_planner_create(bp_ctx*, const bp_schema*, int64_t, bp_planner**);
 int bp_planner_destroy(bp_planner*);
@@ -71,8 +73,9 @@ struct PlanSlot {
   int64_t* ttls;
   int64_t* ttl_k;
   uint64_t* evict_keys;
-  int64_t* counts;   // [4] device
-  int64_t* h_counts;  // [4] pinned
+  uint32_t* evict_ids;
+  int64_t* counts;   // [5] device
+  int64_t* h_counts;  // [5] pinned
   float* staging;    // [max_occ, dim]
   int64_t* n_ins;    // device: counts[0] - dropped
   cudaEvent_t popped, fetched, consumed;
@@ -219,8 +222,9 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     BP_CUDA_TRY(cudaMalloc(&p.ttls, n * sizeof(int64_t)));
     BP_CUDA_TRY(cudaMalloc(&p.ttl_k, n * sizeof(int64_t)));
     BP_CUDA_TRY(cudaMalloc(&p.evict_keys, n * sizeof(uint64_t)));
-    BP_CUDA_TRY(cudaMalloc(&p.counts, 4 * sizeof(int64_t)));
-    BP_CUDA_TRY(cudaMallocHost(&p.h_counts, 4 * sizeof(int64_t)));
+    BP_CUDA_TRY(cudaMalloc(&p.evict_ids, n * sizeof(uint32_t)));
+    BP_CUDA_TRY(cudaMalloc(&p.counts, 5 * sizeof(int64_t)));
+    BP_CUDA_TRY(cudaMallocHost(&p.h_counts, 5 * sizeof(int64_t)));
     BP_CUDA_TRY(cudaMalloc(&p.staging, n * dim * sizeof(float)));
     BP_CUDA_TRY(cudaMalloc(&p.n_ins, sizeof(int64_t)));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&p.popped, cudaEventDisableTiming));
@@ -282,6 +286,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
     cudaFree(p.ttls);
     cudaFree(p.ttl_k);
     cudaFree(p.evict_keys);
+    cudaFree(p.evict_ids);
     cudaFree(p.counts);
     cudaFreeHost(p.h_counts);
     cudaFree(p.staging);
@@ -376,11 +381,11 @@ static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64
     }
     stage_begin(e, kStagePrep, q);
     rc = bp_prep_create_columnar(e->ctx, e->sc, d_keys, d_labels, n_ex, n_cols, e->d_col_tables, h_rank_bounds,
-                                 num_ranks, iteration, 0, q, &e->preps[slot]);
+                                 num_ranks, iteration, e->cfg.prep_flags, q, &e->preps[slot]);
   } else {
     stage_begin(e, kStagePrep, q);
-    rc = bp_prep_create(e->ctx, e->sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, 0, 0, 0, q,
-                        &e->preps[slot]);
+    rc = bp_prep_create(e->ctx, e->sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration,
+                        e->cfg.prep_flags, 0, 0, q, &e->preps[slot]);
   }
   stage_end(e, kStagePrep, q);
   if (rc) return rc;
@@ -445,12 +450,12 @@ extern "C" int bp_engine_pop(bp_engine* e, int64_t pos, int32_t* slot_out) {
   PlanSlot& ps = e->plans[slot];
   // The slot's previous plan must have been consumed by training.
   BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, ps.consumed, 0));
-  bp_plan_buffers b{ps.keys, ps.ids, ps.ttls, ps.ttl_k, ps.evict_keys, ps.counts};
+  bp_plan_buffers b{ps.keys, ps.ids, ps.ttls, ps.ttl_k, ps.evict_keys, ps.evict_ids, ps.counts};
   stage_begin(e, kStagePlanner, e->planq);
   int rc = bp_planner_pop(e->planner, P, &b, e->planq);
   stage_end(e, kStagePlanner, e->planq);
   if (rc) return rc;
-  BP_CUDA_TRY(cudaMemcpyAsync(ps.h_counts, ps.counts, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, e->planq));
+  BP_CUDA_TRY(cudaMemcpyAsync(ps.h_counts, ps.counts, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, e->planq));
   BP_CUDA_TRY(cudaEventRecord(ps.popped, e->planq));
   ps.prep_pos = pos;
   *slot_out = slot;
@@ -468,7 +473,7 @@ extern "C" int bp_engine_plan_counts(bp_engine* e, int32_t slot, int64_t* out4) 
 
 extern "C" int bp_engine_plan_view(bp_engine* e, int32_t slot, bp_plan_buffers* out, float** staging) {
   bp::PlanSlot& ps = e->plans[slot];
-  *out = bp_plan_buffers{ps.keys, ps.ids, ps.ttls, ps.ttl_k, ps.evict_keys, ps.counts};
+  *out = bp_plan_buffers{ps.keys, ps.ids, ps.ttls, ps.ttl_k, ps.evict_keys, ps.evict_ids, ps.counts};
   if (staging) *staging = ps.staging;
   return BP_OK;
 }
@@ -550,7 +555,11 @@ static int engine_finish(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_s
   BP_CUDA_TRY(cudaStreamWaitEvent(s, c.flushed, 0));  // its previous contents are durable
   bp_evict_buffers eb{e->cfg.record_keys ? c.keys : nullptr, c.ids, c.rows, c.dirty, c.count};
   stage_begin(e, kStageEvict, s);
-  int rc = bp_cache_evict(e->cache, P->iteration, 0, &eb, e->chunk_cap, s);
+  // The planner's key-sorted evict set is exactly {ttl <= iteration}
+  // (checked: the occupancy must then equal the mirror size after the pop);
+  // key order makes the later write-back walk the host table ascending.
+  int rc = bp_cache_evict_planned(e->cache, ps.evict_keys, ps.evict_ids, ps.counts + 1, e->chunk_cap, ps.counts + 4,
+                                  P->iteration, &eb, s);
   stage_end(e, kStageEvict, s);
   if (rc) return rc;
   c.pending = true;

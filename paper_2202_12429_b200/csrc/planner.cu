@@ -102,7 +102,7 @@ __global__ void k_pop_compact(const uint32_t* __restrict__ pf_flag, const uint32
                               const uint32_t* __restrict__ ids, const uint32_t* __restrict__ perm_s2k,
                               const int64_t* __restrict__ ttl_k, uint64_t* __restrict__ pf_keys,
                               uint32_t* __restrict__ pf_ids, int64_t* __restrict__ pf_ttls,
-                              uint64_t* __restrict__ ev_keys) {
+                              uint64_t* __restrict__ ev_keys, uint32_t* __restrict__ ev_ids) {
   const long long U = *d_U;
   for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < U; s += (long long)gridDim.x * blockDim.x) {
     if (pf_flag[s]) {
@@ -111,7 +111,10 @@ __global__ void k_pop_compact(const uint32_t* __restrict__ pf_flag, const uint32
       pf_ids[p] = ids[s];
       pf_ttls[p] = ttl_k[perm_s2k[s]];
     }
-    if (ev_flag[s] && ev_keys) ev_keys[ev_pos[s]] = keys_s[s];
+    if (ev_flag[s]) {
+      if (ev_keys) ev_keys[ev_pos[s]] = keys_s[s];
+      if (ev_ids) ev_ids[ev_pos[s]] = ids[s];
+    }
   }
 }
 
@@ -125,6 +128,7 @@ __global__ void k_pop_end(PlannerCounters* ctr, int64_t* counts) {
   ctr->in_cache += npf - nev;
   ctr->last_prefetch = npf;
   ctr->last_evict = nev;
+  counts[4] = ctr->in_cache;  // mirror size after this batch: the cache's occupancy after its evictions
 }
 
 static int planner_scratch(bp_planner* p, long long n, cudaStream_t s) {
@@ -273,7 +277,7 @@ extern "C" int bp_planner_pop(bp_planner* p, bp_prep* P, const bp_plan_buffers* 
                                (long long*)&b->d_counts[1], s));
     k_pop_compact<<<g, 256, 0, s>>>(p->d_pf_flag, p->d_ev_flag, p->d_pf_pos, p->d_ev_pos, P->d_num_unique,
                                     P->d_uniq_key_s, ids, P->d_perm_s2k, b->d_ttl_k, b->d_prefetch_keys,
-                                    b->d_prefetch_ids, b->d_prefetch_ttls, b->d_evict_keys);
+                                    b->d_prefetch_ids, b->d_prefetch_ttls, b->d_evict_keys, b->d_evict_ids);
   }
   k_pop_end<<<1, 1, 0, s>>>(p->d_ctr, b->d_counts);
   BP_LAUNCH_CHECK();

@@ -96,7 +96,8 @@ class DevicePrep:
 
     def __init__(self, keys: np.ndarray, labels: np.ndarray, rank_bounds: np.ndarray, iteration: int,
                  schema: Schema | None = None, occ_index: bool = False, stream=None,
-                 d_keys: torch.Tensor | None = None, d_labels: torch.Tensor | None = None, uploader=None):
+                 d_keys: torch.Tensor | None = None, d_labels: torch.Tensor | None = None, uploader=None,
+                 columns=None):
         lib = L.lib()
         self.stream = stream or torch.cuda.current_stream()
         self.n_occ = int(len(keys)) if d_keys is None else int(d_keys.numel())
@@ -114,10 +115,19 @@ class DevicePrep:
             table_bits = _bits(int((k >> np.uint64(44)).max()))
         sc = DeviceSchema.get(schema).handle if schema is not None else None
         h = C.c_void_p()
-        L.check(lib.bp_prep_create(L.Context.get().handle, sc, L.ptr(self.d_keys), L.ptr(self.d_labels),
-                                   self.n_occ, rb.ctypes.data, self.num_ranks, self.iteration,
-                                   1 if occ_index else 0, row_bits, table_bits, L.stream_ptr(self.stream),
-                                   C.byref(h)), "bp_prep_create")
+        if columns is not None and schema is not None:
+            # Criteo layout (one key per table per example): per-column sort
+            n_ex, tables = columns
+            self.d_tables = L.to_device(np.ascontiguousarray(tables, dtype=np.int32), self.stream)
+            L.check(lib.bp_prep_create_columnar(L.Context.get().handle, sc, L.ptr(self.d_keys), L.ptr(self.d_labels),
+                                                n_ex, len(tables), L.ptr(self.d_tables), rb.ctypes.data,
+                                                self.num_ranks, self.iteration, 1 if occ_index else 0,
+                                                L.stream_ptr(self.stream), C.byref(h)), "bp_prep_create_columnar")
+        else:
+            L.check(lib.bp_prep_create(L.Context.get().handle, sc, L.ptr(self.d_keys), L.ptr(self.d_labels),
+                                       self.n_occ, rb.ctypes.data, self.num_ranks, self.iteration,
+                                       1 if occ_index else 0, row_bits, table_bits, L.stream_ptr(self.stream),
+                                       C.byref(h)), "bp_prep_create")
         self.handle = h
         v = L.PrepView()
         L.check(lib.bp_prep_get_view(h, C.byref(v)), "bp_prep_get_view")
@@ -128,8 +138,13 @@ class DevicePrep:
     def from_batch(cls, batch: Batch, num_ranks: int = 1, schema: Schema | None = None, occ_index: bool = False,
                    stream=None, uploader=None) -> "DevicePrep":
         keys, labels, _ = batch.packed_occurrences()
+        columns = None
+        if schema is not None and batch.is_columnar and batch.num_examples:
+            tables = batch.table_ids()
+            if bool(np.all(np.diff(tables) > 0)):
+                columns = (batch.num_examples, tables)
         return cls(keys, labels, batch.rank_bounds(num_ranks), batch.iteration, schema, occ_index, stream,
-                   uploader=uploader)
+                   uploader=uploader, columns=columns)
 
     @property
     def num_unique(self) -> int:

@@ -203,7 +203,7 @@ class _Pipeline:
                             record_keys=1 if (cfg.record_events or fault == FAULT_NO_GATE) else 0,
                             plan_slots=self.L0 + 4, chunk_slots=self.flush_interval + 4,
                             prep_slots=2 * self.L0 + 8, timing=1 if timing else 0, init_dims=schema.emb_dim,
-                            pad=0)
+                            prep_flags=2 if trainer is not None else 0)
         h = C.c_void_p()
         L.check(self.lib.bp_engine_create(L.Context.get().handle, DeviceSchema.get(self.row_schema).handle,
                                           C.byref(ec), C.byref(h)), "bp_engine_create")

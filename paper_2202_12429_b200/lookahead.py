@@ -44,12 +44,12 @@ class DevicePlan:
         self.prefetch_ttls = torch.empty(max(u, 1), dtype=torch.int64, device=dev)
         self.ttl_k = torch.empty(max(u, 1), dtype=torch.int64, device=dev)
         self.evict_keys = torch.empty(max(u, 1), dtype=torch.uint64, device=dev)
-        self.counts = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.counts = torch.zeros(5, dtype=torch.int64, device=dev)
         self.h_counts = None
 
     def buffers(self) -> L.PlanBuffers:
         return L.PlanBuffers(L.ptr(self.prefetch_keys), L.ptr(self.prefetch_ids), L.ptr(self.prefetch_ttls),
-                             L.ptr(self.ttl_k), L.ptr(self.evict_keys), L.ptr(self.counts))
+                             L.ptr(self.ttl_k), L.ptr(self.evict_keys), None, L.ptr(self.counts))
 
     def read_counts(self) -> np.ndarray:
         if self.h_counts is None:

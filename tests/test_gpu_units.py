@@ -210,3 +210,32 @@ def test_label_only_term_and_local_gradients():
     np.testing.assert_array_equal(grads[k(1)], np.full(4, np.float32(0.0005)))
     with pytest.raises(CacheMissError):
         local_gradients([Example(1, (), (k(2),))], {}, cfg)
+
+
+# ---------------------------------------------------------------- prep
+def test_columnar_prep_equals_generic_prep():
+    """The per-column shared-memory sort and the generic global radix sort
+    produce identical preps (order of every array), incl. trainer ranks."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2202_12429_b200 import _lib as L
+    from paper_2202_12429_b200.device import DevicePrep
+    from paper_2202_12429_b200.traces import ZipfSpec, batchify_columns, generate_columns
+
+    schema = Schema(5, (3, 70_000, 1000, 5_000_000, 17), 0, 4)
+    rows, labels, _ = generate_columns(ZipfSpec(schema, 1.1, 2 * 16384, seed=9))
+    for b in batchify_columns(rows, labels, None, 16384):
+        keys, labs, _ = b.packed_occurrences()
+        rb = b.rank_bounds(3)
+        col = DevicePrep(keys, labs, rb, b.iteration, schema, columns=(b.num_examples, b.table_ids()))
+        gen = DevicePrep(keys, labs, rb, b.iteration, schema)
+        u = gen.num_unique
+        assert col.num_unique == u
+        n = gen.n_occ
+        for name, dt, cnt in (("d_uniq_key_s", torch.uint64, u), ("d_uniq_id_s", torch.uint32, u),
+                              ("d_uniq_key_k", torch.uint64, u), ("d_perm_s2k", torch.uint32, u),
+                              ("d_seg_start", torch.uint32, u + 1), ("d_occ_pos", torch.uint32, n),
+                              ("d_occ_label", torch.uint8, n)):
+            assert torch.equal(col.tensor(name, dt, cnt).cpu(), gen.tensor(name, dt, cnt).cpu()), name
