@@ -16,8 +16,11 @@ through the public API with host batches (H2D of the batch entering the
 window and D2H of the step counters inside the timed region).  L2 is
 flushed (256 MiB write) between timed steps.  ``--impl reference`` times the
 CPU oracle port of the reference (oracle/, reference unavailable on the box)
-on the host cores.  N>1: one independent engine replica per GPU ("replicas
-only"), timed as the max over ranks.
+on the host cores.  N>1: the 26 tables are sharded table-wise over the
+ranks (each rank runs the whole pipeline for its tables of the SAME global
+batch, no data-path collective; strong scaling), timed as the max over ranks.
+DLRM mode (N=1, reported under "dlrm" and in "roofline"): the same engine
+with EmbeddingBag fwd/bwd + SGD feeding PyTorch MLPs replayed as a CUDA graph.
 """
 
 from __future__ import annotations
@@ -311,26 +314,26 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch) -> dict:
     n_occ = BATCH * sc.num_tables
     # "trainer" spans: EmbeddingBag forward and backward alternate (2 per step)
     spans = stages["trainer"]
-    # forward = scatter form: one row read per unique key, one pooled row written per occurrence
-    fwd_bytes = int(u_mean) * (4 * DIM + 8) + n_occ * (4 * DIM + 4)
+    # forward N_occ*(64 row read + 64 pooled write + 4 index)
+    fwd_bytes = n_occ * (8 * DIM + 4)
     losses = trainer.loss_history()
     del pipe
     return {"summary": {"value": BATCH * steps / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms / steps,
-                        "mlp": "PyTorch bf16 autocast (13-512-256-64-16 / 367-1024-1024-512-256-1)",
+                        "mlp": "PyTorch bf16 autocast, one CUDA graph per step (13-512-256-64-16 / 367-1024-1024-512-256-1)",
                         "embedding_optimizer": "sgd", "final_loss": losses[-1] if losses else None,
                         "embedding_stage_ms_per_step": spans[0] / steps},
-            "roofline": {"kernel": "bp::k_embbag_fwd_scatter + k_embbag_bwd (EmbeddingBag fwd+bwd+SGD on cached rows)",
+            "roofline": {"kernel": "bp::k_embbag_fwd_rows_v4 + k_embbag_bwd (EmbeddingBag fwd+bwd+SGD on cached rows)",
                          "bound": "hbm", "bytes_per_step": fwd_bytes + bwd_bytes(n_occ, int(u_mean)),
                          "ms_per_step": spans[0] / steps, "launches_per_step": 2, "unit": "GB/s",
                          "achieved": (fwd_bytes + bwd_bytes(n_occ, int(u_mean))) / (spans[0] / steps * 1e-3) / 1e9
                          if spans[0] else 0.0,
                          "traffic": None,
-                         "note": "bytes = forward (U*64 row reads + N_occ*64 pooled writes + indices) + backward "
-                                 "(N_occ*64 gradient reads + U*128 row read/write + indices) per step"}}
+                         "note": "SURVEY 8(d) algorithmic bytes: forward N_occ*(64 row read + 64 pooled write + 4 "
+                                 "index) + backward N_occ*(64 gradient read + 4 index) + U*(64 read + 64 write)"}}
 
 
 def bwd_bytes(n_occ: int, u: int) -> int:
-    return n_occ * (4 * DIM + 4) + u * (8 * DIM + 8)
+    return n_occ * (4 * DIM + 4) + u * (8 * DIM)
 
 
 # ------------------------------------------------------- CPU oracle timing

@@ -76,6 +76,7 @@ class DLRMConfig:
     top: tuple = (1024, 1024, 512, 256)
     mlp_dtype: str = "fp32"      # "fp32" | "bf16" (autocast for the dense MLPs only)
     seed: int = 0
+    cuda_graph: bool = True      # replay the dense step (fwd + bwd + SGD) as one captured CUDA graph
 
     def __post_init__(self):
         if self.emb_optimizer not in ("sgd", "adagrad"):
@@ -99,6 +100,7 @@ class DLRMTrainer:
         self.opt = torch.optim.SGD(self.model.parameters(), lr=dcfg.mlp_lr)
         self.losses: list = []
         self._dense_dev: dict = {}
+        self._graphs: dict = {}
 
     def row_width(self) -> int:
         """Width of a stored row: weights (+ Adagrad accumulators)."""
@@ -115,9 +117,6 @@ class DLRMTrainer:
         t = n_occ // max(b, 1)
         stream = pipe.stream
         with torch.cuda.stream(stream):
-            pooled = torch.empty((n_occ, self.dim), dtype=torch.float32, device="cuda")
-            L.check(lib.bp_engine_dlrm_forward(pipe.eng, pos, plan.slot, nxt, skip_key, has_skip, self.dim,
-                                               L.ptr(pooled)), "bp_engine_dlrm_forward")
             dev = self._dense_dev.pop(pos, None)
             if dev is None:
                 dense = torch.from_numpy(np.ascontiguousarray(batch.dense, dtype=np.float32)).to(
@@ -125,23 +124,73 @@ class DLRMTrainer:
                 labels = torch.from_numpy(np.ascontiguousarray(batch.labels, dtype=np.float32)).to("cuda")
             else:
                 dense, labels = dev
-            emb = pooled.view(b, t, self.dim).requires_grad_(True)
-            if self.dcfg.mlp_dtype == "bf16":
-                with torch.autocast("cuda", dtype=torch.bfloat16):
-                    logits = self.model(dense, emb)
-                logits = logits.float()
+            g = self._graph(b, t, dense.shape[1]) if self.dcfg.cuda_graph else None
+            # the native forward writes the pooled rows straight into the
+            # graph's static input (or a fresh leaf in eager mode)
+            pooled = g["emb"] if g is not None else torch.empty((b, t, self.dim), dtype=torch.float32, device="cuda")
+            L.check(lib.bp_engine_dlrm_forward(pipe.eng, pos, plan.slot, nxt, skip_key, has_skip, self.dim,
+                                               L.ptr(pooled)), "bp_engine_dlrm_forward")
+            if g is not None:
+                g["dense"].copy_(dense)
+                g["labels"].copy_(labels)
+                g["graph"].replay()
+                grad = g["grad"]
+                self.losses.append(g["loss"].detach().clone())
             else:
-                logits = self.model(dense, emb)
-            loss = nn.functional.binary_cross_entropy_with_logits(logits, labels)
-            self.opt.zero_grad(set_to_none=True)
-            loss.backward()
-            self.opt.step()
-            grad = emb.grad.contiguous()
-            self.losses.append(loss.detach())
+                emb = pooled.requires_grad_(True)
+                loss = self._loss(dense, emb, labels)
+                self.opt.zero_grad(set_to_none=True)
+                loss.backward()
+                self.opt.step()
+                grad = emb.grad.contiguous()
+                self.losses.append(loss.detach())
             L.check(lib.bp_engine_dlrm_backward(pipe.eng, pos, plan.slot, L.ptr(grad), self.dim, self.dcfg.opt_code,
                                                 float(np.float32(self.dcfg.emb_lr)),
                                                 float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
                                                 C.byref(res)), "bp_engine_dlrm_backward")
+
+    def _loss(self, dense, emb, labels):
+        if self.dcfg.mlp_dtype == "bf16":
+            with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+                logits = self.model(dense, emb)
+            logits = logits.float()
+        else:
+            logits = self.model(dense, emb)
+        return nn.functional.binary_cross_entropy_with_logits(logits, labels)
+
+    def _graph(self, b: int, t: int, n_dense: int) -> dict:
+        """The dense step for a (B, T) batch shape, captured once as a CUDA
+        graph over static input buffers (the pooled embeddings, dense
+        features, labels).  Replaying it costs one launch instead of ~100
+        eager kernel launches from Python.  Warm-up passes before capture run
+        forward+backward only, so the model's parameters are untouched."""
+        key = (b, t, n_dense)
+        g = self._graphs.get(key)
+        if g is not None:
+            return g
+        dev = "cuda"
+        emb = torch.zeros((b, t, self.dim), dtype=torch.float32, device=dev, requires_grad=True)
+        dense = torch.zeros((b, n_dense), dtype=torch.float32, device=dev)
+        labels = torch.zeros((b,), dtype=torch.float32, device=dev)
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                self._loss(dense, emb, labels).backward()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.opt.zero_grad(set_to_none=True)
+        emb.grad = None
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+            loss = self._loss(dense, emb, labels)
+            loss.backward()
+            self.opt.step()
+            grad = emb.grad.contiguous()
+        g = {"graph": graph, "emb": emb, "dense": dense, "labels": labels, "loss": loss, "grad": grad}
+        self._graphs[key] = g
+        return g
 
     def loss_history(self) -> list:
         return [float(x) for x in self.losses]

@@ -47,8 +47,9 @@ def cpu_reference(batches, model, opt_name, lr, eps, seed):
     return losses, [t.detach().numpy() for t in tables], model
 
 
-@pytest.mark.parametrize("opt_name", ["sgd", "adagrad"])
-def test_dlrm_pipeline_matches_dense_cpu_training(opt_name):
+@pytest.mark.parametrize("opt_name,cuda_graph", [("sgd", False), ("adagrad", False), ("sgd", True),
+                                                 ("adagrad", True)])
+def test_dlrm_pipeline_matches_dense_cpu_training(opt_name, cuda_graph):
     from paper_2202_12429_b200.dlrm import DLRMConfig, DLRMDense
     from paper_2202_12429_b200.engine import EngineConfig, run_dlrm
 
@@ -60,7 +61,8 @@ def test_dlrm_pipeline_matches_dense_cpu_training(opt_name):
     lr, eps, seed = 0.05, 1e-10, 7
     want_losses, want_tables, want_model = cpu_reference(batches, model, opt_name, lr, eps, seed)
     cfg = EngineConfig(cache_capacity=1200, batch_size=256, lookahead=3, num_shards=1, seed=seed, lr=lr)
-    dcfg = DLRMConfig(emb_optimizer=opt_name, emb_lr=lr, mlp_lr=lr, adagrad_eps=eps, bottom=(64, 32), top=(64, 32))
+    dcfg = DLRMConfig(emb_optimizer=opt_name, emb_lr=lr, mlp_lr=lr, adagrad_eps=eps, bottom=(64, 32), top=(64, 32),
+                      cuda_graph=cuda_graph)
     report, trainer = run_dlrm(cfg, SCHEMA, batches, dcfg, model=copy.deepcopy(model))
     np.testing.assert_allclose(trainer.loss_history(), want_losses, rtol=1e-4)
     table = report.final_store.table_view()
