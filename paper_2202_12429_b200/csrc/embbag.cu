@@ -211,6 +211,148 @@ __global__ void __launch_bounds__(256) k_embbag_bwd(const uint32_t* __restrict__
   }
 }
 
+// Backward as a tiled reduce-by-key over the key-sorted occurrence order
+// (dim % 4 == 0; needs the prep's seg_of, BP_PREP_OCC_SORTED).  Tile b holds
+// sorted positions [b*T, b*T+T) (T*dim/4 = 2048 float4 = 32 KB): the CTA
+// gathers the T gradient rows into shared memory (16-byte loads, all issued
+// before any add), runs a segmented Hillis-Steele scan, and at the last row
+// of every key in the tile holds that key's partial sum.  A key wholly inside
+// the tile is updated right there; a key spanning tiles (the Zipf-hot rows:
+// ~9K occurrences = 18 tiles at Criteo-Kaggle) leaves one partial per tile,
+// and the last tile to arrive (per-key counter) sums them in tile order and
+// applies the update.  Every summation order is fixed by the data, not by
+// scheduling, so the result is run-to-run deterministic; all occurrence work
+// is parallel (no per-key dependent chains as in the stub trainer, whose
+// order is pinned by the reference).
+constexpr int kBwdTileF4 = 2048;
+constexpr int kBwdPer = kBwdTileF4 / 256;
+
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+
+__device__ __forceinline__ float upd1(float v, float& a, float g, int opt, float lr, float eps) {
+  if (opt == BP_OPT_ADAGRAD) {
+    a = __fadd_rn(a, __fmul_rn(g, g));
+    return __fsub_rn(v, __fdiv_rn(__fmul_rn(lr, g), __fadd_rn(__fsqrt_rn(a), eps)));
+  }
+  return __fsub_rn(v, __fmul_rn(lr, g));
+}
+
+__device__ __forceinline__ bool apply_row4(float* __restrict__ row, int dim, int c, float4 g, int opt, float lr,
+                                           float eps) {
+  float4* v4 = reinterpret_cast<float4*>(row) + c;
+  float4 v = *v4;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4* a4 = reinterpret_cast<float4*>(row + dim) + c;
+  if (opt == BP_OPT_ADAGRAD) a = *a4;
+  v.x = upd1(v.x, a.x, g.x, opt, lr, eps);
+  v.y = upd1(v.y, a.y, g.y, opt, lr, eps);
+  v.z = upd1(v.z, a.z, g.z, opt, lr, eps);
+  v.w = upd1(v.w, a.w, g.w, opt, lr, eps);
+  *v4 = v;
+  if (opt == BP_OPT_ADAGRAD) *a4 = a;
+  return g.x != 0.f || g.y != 0.f || g.z != 0.f || g.w != 0.f;
+}
+
+__global__ void __launch_bounds__(256) k_embbag_bwd_tiles(
+    const uint32_t* __restrict__ occ_pos, const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start,
+    long long n, int q, int T, const float4* __restrict__ grad, const int64_t* __restrict__ occ_bag,
+    const float* __restrict__ bag_scale, float* __restrict__ values, int row_stride,
+    const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
+    float4* __restrict__ parts, uint32_t* __restrict__ cnt, unsigned long long* __restrict__ stats) {
+  extern __shared__ float4 tile[];  // [T*q] gradient rows, then [T] segment ids
+  uint32_t* seg = reinterpret_cast<uint32_t*>(tile + kBwdTileF4);
+  __shared__ unsigned int n_dirty;
+  const long long t0 = (long long)blockIdx.x * T;
+  const int rows = (int)min((long long)T, n - t0);
+  const int dim = 4 * q;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  long long pk[kBwdPer];
+#pragma unroll
+  for (int k = 0; k < kBwdPer; ++k) {
+    const int i = threadIdx.x + k * 256, r = i / q;
+    pk[k] = r < rows ? (long long)occ_pos[t0 + r] : -1;
+  }
+  if (occ_bag) {
+#pragma unroll
+    for (int k = 0; k < kBwdPer; ++k)
+      if (pk[k] >= 0) pk[k] = occ_bag[pk[k]];
+  }
+  float4 v[kBwdPer];
+#pragma unroll
+  for (int k = 0; k < kBwdPer; ++k) {
+    const int i = threadIdx.x + k * 256, c = i - (i / q) * q;
+    v[k] = pk[k] >= 0 ? grad[pk[k] * q + c] : zero;
+  }
+  if (bag_scale) {
+#pragma unroll
+    for (int k = 0; k < kBwdPer; ++k)
+      if (pk[k] >= 0) {
+        const float sc = bag_scale[pk[k]];
+        v[k] = make_float4(__fmul_rn(v[k].x, sc), __fmul_rn(v[k].y, sc), __fmul_rn(v[k].z, sc), __fmul_rn(v[k].w, sc));
+      }
+  }
+#pragma unroll
+  for (int k = 0; k < kBwdPer; ++k) tile[threadIdx.x + k * 256] = v[k];
+  for (int r = threadIdx.x; r < T; r += 256) seg[r] = r < rows ? seg_of[t0 + r] : 0xffffffffu;
+  if (threadIdx.x == 0) n_dirty = 0;
+  __syncthreads();
+  for (int off = 1; off < rows; off <<= 1) {
+    bool take[kBwdPer];
+#pragma unroll
+    for (int k = 0; k < kBwdPer; ++k) {
+      const int i = threadIdx.x + k * 256, r = i / q;
+      take[k] = r >= off && r < rows && seg[r - off] == seg[r];
+      if (take[k]) v[k] = tile[i - off * q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBwdPer; ++k) {
+      const int i = threadIdx.x + k * 256;
+      if (take[k]) tile[i] = f4_add(tile[i], v[k]);
+    }
+    __syncthreads();
+  }
+  unsigned my_dirty = 0;
+  for (int r = threadIdx.x; r < rows; r += 256) {
+    const uint32_t s = seg[r];
+    if (r + 1 < rows && seg[r + 1] == s) continue;  // not this key's last row in the tile
+    const int32_t slot = slots_s[s];
+    if (slot < 0) continue;
+    const long long a = seg_start[s], b = seg_start[s + 1];
+    float* row = values + (long long)slot * row_stride;
+    bool nz = false;
+    if (a >= t0 && b <= t0 + rows) {
+      for (int c = 0; c < q; ++c) nz |= apply_row4(row, dim, c, tile[r * q + c], opt, lr, eps);
+    } else {
+      float4* dst = parts + ((long long)blockIdx.x * 2 + (s == seg[0] ? 0 : 1)) * q;
+      for (int c = 0; c < q; ++c) dst[c] = tile[r * q + c];
+      __threadfence();
+      const long long ft = a / T, lt = (b - 1) / T;
+      if (atomicAdd(&cnt[s], 1u) != (uint32_t)(lt - ft)) continue;
+      __threadfence();
+      cnt[s] = 0;  // self-resetting for the next call
+      for (int c = 0; c < q; ++c) {
+        float4 g = zero;
+        for (long long t = ft; t <= lt; ++t) {
+          const int half = (t == ft && a != ft * T) ? 1 : 0;
+          const float4 x = __ldcg(parts + (t * 2 + half) * q + c);
+          g = t == ft ? x : f4_add(g, x);
+        }
+        nz |= apply_row4(row, dim, c, g, opt, lr, eps);
+      }
+    }
+    if (nz) {
+      if (dirty) dirty[slot] = 1;
+      ++my_dirty;
+    }
+  }
+  if (stats && my_dirty) atomicAdd(&n_dirty, my_dirty);
+  __syncthreads();
+  if (stats && threadIdx.x == 0 && n_dirty) atomicAdd(&stats[1], (unsigned long long)n_dirty);
+}
+
 // occ_s[p] = key-sorted unique index of occurrence p (segment of sorted slot j
 // found by binary search over the CSR offsets).
 __global__ void k_occ_sorted_index(const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ occ_pos,
@@ -288,6 +430,29 @@ extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t
   int G, dpl;
   shape_of(dim, &G, &dpl);
   cudaStream_t s = (cudaStream_t)stream;
+  if (P->d_seg_of && (dim & 3) == 0 && (row_stride & 3) == 0 && dim <= 128) {
+    const int q = dim / 4, T = kBwdTileF4 / q;
+    const long long tiles = (P->n_occ + T - 1) / T;
+    float4* parts = nullptr;
+    uint32_t* cnt = nullptr;
+    BP_CUDA_TRY(pool_alloc(&parts, (size_t)tiles * 2 * q, s));
+    BP_CUDA_TRY(pool_alloc(&cnt, (size_t)P->n_occ, s));
+    BP_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * P->n_occ, s));
+    const size_t smem = sizeof(float4) * kBwdTileF4 + sizeof(uint32_t) * T;
+    static bool attr = false;
+    if (!attr) {
+      BP_CUDA_TRY(cudaFuncSetAttribute(k_embbag_bwd_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+      attr = true;
+    }
+    k_embbag_bwd_tiles<<<(unsigned)tiles, 256, smem, s>>>(
+        P->d_occ_pos, P->d_seg_of, P->d_seg_start, P->n_occ, q, T, reinterpret_cast<const float4*>(d_grad), d_occ_bag,
+        d_bag_scale, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts, cnt,
+        (unsigned long long*)d_stats);
+    BP_LAUNCH_CHECK();
+    cudaFreeAsync(parts, s);
+    cudaFreeAsync(cnt, s);
+    return BP_OK;
+  }
   const BagGrad bg{d_grad, d_occ_bag, d_bag_scale};
   const int blocks = kBagLongBlocks + grid_for(P->n_occ * G, 256, kNumSMs * 6);
   BP_BAG_DISPATCH(G, dpl,

@@ -104,6 +104,7 @@ struct bp_prep {
   uint8_t* d_occ_label;
   uint32_t* d_occ_k;
   uint32_t* d_occ_s;       // occurrence -> key-sorted unique index (BP_PREP_OCC_SORTED)
+  uint32_t* d_seg_of;      // sorted position -> key-sorted unique index (BP_PREP_OCC_SORTED)
   long long* d_rank_bounds;
   uint32_t* d_long;        // segments with >= kLongSeg occurrences: very long ones from the
                            // front, the others from the back (capacity long_cap)

@@ -112,11 +112,13 @@ __global__ void k_prep_perm(const uint32_t* __restrict__ pos, const uint32_t* __
 
 __global__ void k_prep_occ_k(const uint32_t* __restrict__ pos, const uint32_t* __restrict__ head,
                              const uint32_t* __restrict__ segx, long long n, const uint32_t* __restrict__ perm_s2k,
-                             uint32_t* __restrict__ occ_k, uint32_t* __restrict__ occ_s) {
+                             uint32_t* __restrict__ occ_k, uint32_t* __restrict__ occ_s,
+                             uint32_t* __restrict__ seg_of) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
     const uint32_t s = segx[j] + head[j] - 1u;  // inclusive segment index
     if (occ_k) occ_k[pos[j]] = perm_s2k[s];
     if (occ_s) occ_s[pos[j]] = s;
+    if (seg_of) seg_of[j] = s;
   }
 }
 
@@ -286,7 +288,8 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
                                 P->d_perm_k2s, P->d_uniq_key_k, P->d_seg_start, P->d_long,
                                 (unsigned long long*)P->d_num_long, P->long_cap);
   if (P->flags & (BP_PREP_OCC_INDEX | BP_PREP_OCC_SORTED))
-    k_prep_occ_k<<<g, 256, 0, s>>>(P->d_occ_pos, head, segx, n, P->d_perm_s2k, P->d_occ_k, P->d_occ_s);
+    k_prep_occ_k<<<g, 256, 0, s>>>(P->d_occ_pos, head, segx, n, P->d_perm_s2k, P->d_occ_k, P->d_occ_s,
+                                   P->d_seg_of);
   BP_LAUNCH_CHECK();
   cudaFreeAsync(ka, s);
   cudaFreeAsync(kb, s);
@@ -331,8 +334,12 @@ static int prep_create_impl(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_
   BP_CUDA_TRY(pool_alloc(&P->d_occ_label, n + 16, s));  // read as 16-byte chunks
   P->d_occ_k = nullptr;
   P->d_occ_s = nullptr;
+  P->d_seg_of = nullptr;
   if (flags & BP_PREP_OCC_INDEX) BP_CUDA_TRY(pool_alloc(&P->d_occ_k, n, s));
-  if (flags & BP_PREP_OCC_SORTED) BP_CUDA_TRY(pool_alloc(&P->d_occ_s, n, s));
+  if (flags & BP_PREP_OCC_SORTED) {
+    BP_CUDA_TRY(pool_alloc(&P->d_occ_s, n, s));
+    BP_CUDA_TRY(pool_alloc(&P->d_seg_of, n, s));
+  }
   BP_CUDA_TRY(pool_alloc(&P->d_rank_bounds, num_ranks + 1, s));
   P->long_cap = n / kLongSeg + 1;
   BP_CUDA_TRY(pool_alloc(&P->d_long, P->long_cap, s));
@@ -407,6 +414,7 @@ extern "C" int bp_prep_destroy(bp_prep* P) {
   cudaFreeAsync(P->d_occ_label, s);
   if (P->d_occ_k) cudaFreeAsync(P->d_occ_k, s);
   if (P->d_occ_s) cudaFreeAsync(P->d_occ_s, s);
+  if (P->d_seg_of) cudaFreeAsync(P->d_seg_of, s);
   cudaFreeAsync(P->d_rank_bounds, s);
   cudaFreeAsync(P->d_long, s);
   cudaFreeAsync(P->d_num_long, s);

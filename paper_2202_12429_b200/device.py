@@ -95,7 +95,7 @@ class DevicePrep:
     occurrence lists, labels, trainer-rank bounds."""
 
     def __init__(self, keys: np.ndarray, labels: np.ndarray, rank_bounds: np.ndarray, iteration: int,
-                 schema: Schema | None = None, occ_index: bool = False, stream=None,
+                 schema: Schema | None = None, occ_index: int = 0, stream=None,
                  d_keys: torch.Tensor | None = None, d_labels: torch.Tensor | None = None, uploader=None,
                  columns=None):
         lib = L.lib()
@@ -121,12 +121,12 @@ class DevicePrep:
             self.d_tables = L.to_device(np.ascontiguousarray(tables, dtype=np.int32), self.stream)
             L.check(lib.bp_prep_create_columnar(L.Context.get().handle, sc, L.ptr(self.d_keys), L.ptr(self.d_labels),
                                                 n_ex, len(tables), L.ptr(self.d_tables), rb.ctypes.data,
-                                                self.num_ranks, self.iteration, 1 if occ_index else 0,
+                                                self.num_ranks, self.iteration, int(occ_index),
                                                 L.stream_ptr(self.stream), C.byref(h)), "bp_prep_create_columnar")
         else:
             L.check(lib.bp_prep_create(L.Context.get().handle, sc, L.ptr(self.d_keys), L.ptr(self.d_labels),
                                        self.n_occ, rb.ctypes.data, self.num_ranks, self.iteration,
-                                       1 if occ_index else 0, row_bits, table_bits, L.stream_ptr(self.stream),
+                                       int(occ_index), row_bits, table_bits, L.stream_ptr(self.stream),
                                        C.byref(h)), "bp_prep_create")
         self.handle = h
         v = L.PrepView()

@@ -33,13 +33,30 @@ BP_OPT_SGD = 0
 BP_OPT_ADAGRAD = 1
 
 
-def mlp(sizes, last_act: bool) -> nn.Sequential:
+def mlp(sizes, last_act: bool, in_pad: int = 0) -> nn.Sequential:
+    """Linear+ReLU stack.  ``in_pad`` extra input features (always fed zeros)
+    widen the first layer to a multiple of 8 so bf16 GEMMs hit aligned
+    tensor-core kernels; their weight columns start at zero and, with zero
+    inputs, get zero gradient, so the model equals the unpadded one (the
+    live columns keep the unpadded layer's init)."""
     layers = []
     for i in range(len(sizes) - 1):
-        layers.append(nn.Linear(sizes[i], sizes[i + 1]))
+        fan_in = sizes[i] + (in_pad if i == 0 else 0)
+        lin = nn.Linear(fan_in, sizes[i + 1])
+        if fan_in != sizes[i]:
+            ref = nn.Linear(sizes[i], sizes[i + 1])
+            with torch.no_grad():
+                lin.weight.zero_()
+                lin.weight[:, :sizes[i]].copy_(ref.weight)
+                lin.bias.copy_(ref.bias)
+        layers.append(lin)
         if i < len(sizes) - 2 or last_act:
             layers.append(nn.ReLU())
     return nn.Sequential(*layers)
+
+
+def _pad8(n: int) -> int:
+    return (-n) % 8
 
 
 class DLRMDense(nn.Module):
@@ -47,21 +64,30 @@ class DLRMDense(nn.Module):
 
     def __init__(self, num_dense: int, num_tables: int, dim: int, bottom=(512, 256, 64), top=(1024, 1024, 512, 256)):
         super().__init__()
-        self.num_tables, self.dim = num_tables, dim
-        self.bottom = mlp((num_dense,) + tuple(bottom) + (dim,), last_act=True)
+        self.num_tables, self.dim, self.num_dense = num_tables, dim, num_dense
+        self.dense_pad = _pad8(num_dense)
+        self.bottom = mlp((num_dense,) + tuple(bottom) + (dim,), last_act=True, in_pad=self.dense_pad)
         n = num_tables + 1
         self.pairs = n * (n - 1) // 2
-        self.top = mlp((self.pairs + dim,) + tuple(top) + (1,), last_act=False)
+        self.top_pad = _pad8(self.pairs + dim)
+        self.top = mlp((self.pairs + dim,) + tuple(top) + (1,), last_act=False, in_pad=self.top_pad)
         li, lj = torch.tril_indices(n, n, offset=-1)
-        self.register_buffer("li", li, persistent=False)
-        self.register_buffer("lj", lj, persistent=False)
+        # strictly-lower-triangle entries of the flattened [n, n] Gram matrix;
+        # index_select's backward is a plain index_add (no sort), unlike the
+        # advanced-indexing form zz[:, li, lj]
+        self.register_buffer("tril_flat", li * n + lj, persistent=False)
 
     def forward(self, dense: torch.Tensor, pooled: torch.Tensor) -> torch.Tensor:
+        if dense.shape[1] == self.num_dense and self.dense_pad:
+            dense = nn.functional.pad(dense, (0, self.dense_pad))
         x = self.bottom(dense)                                # [B, D]
-        z = torch.cat([x.unsqueeze(1), pooled], dim=1)        # [B, T+1, D]
+        z = torch.cat([x.unsqueeze(1).to(pooled.dtype), pooled], dim=1)  # [B, T+1, D]
         zz = torch.bmm(z, z.transpose(1, 2))                  # [B, T+1, T+1]
-        inter = zz[:, self.li, self.lj]                       # [B, pairs]
-        return self.top(torch.cat([x, inter], dim=1)).squeeze(1)
+        inter = zz.flatten(1).index_select(1, self.tril_flat)  # [B, pairs]
+        feats = [x.to(inter.dtype), inter]
+        if self.top_pad:
+            feats.append(inter.new_zeros((inter.shape[0], self.top_pad)))
+        return self.top(torch.cat(feats, dim=1)).squeeze(1)
 
 
 @dataclass
@@ -131,7 +157,7 @@ class DLRMTrainer:
             L.check(lib.bp_engine_dlrm_forward(pipe.eng, pos, plan.slot, nxt, skip_key, has_skip, self.dim,
                                                L.ptr(pooled)), "bp_engine_dlrm_forward")
             if g is not None:
-                g["dense"].copy_(dense)
+                g["dense"][:, :dense.shape[1]].copy_(dense)
                 g["labels"].copy_(labels)
                 g["graph"].replay()
                 grad = g["grad"]
@@ -170,7 +196,7 @@ class DLRMTrainer:
             return g
         dev = "cuda"
         emb = torch.zeros((b, t, self.dim), dtype=torch.float32, device=dev, requires_grad=True)
-        dense = torch.zeros((b, n_dense), dtype=torch.float32, device=dev)
+        dense = torch.zeros((b, n_dense + self.model.dense_pad), dtype=torch.float32, device=dev)
         labels = torch.zeros((b,), dtype=torch.float32, device=dev)
         torch.cuda.synchronize()
         side = torch.cuda.Stream()

@@ -110,3 +110,67 @@ def test_embedding_bag_forward_matches_torch():
         want = torch.nn.functional.embedding_bag(torch.from_numpy(idx), torch.from_numpy(weights),
                                                  torch.from_numpy(offsets[:-1]), mode="mean" if mode else "sum")
         np.testing.assert_allclose(out.cpu().numpy(), want.numpy(), rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("flags", [0, 2])
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("opt_name", ["sgd", "adagrad"])
+def test_embedding_bag_backward_matches_torch(flags, mode, opt_name):
+    """Multi-key bags (sum/mean), hot keys spanning many reduction tiles
+    (flags=2: the tiled reduce-by-key kernel; 0: the per-key kernel), SGD and
+    Adagrad in place, against torch autograd of embedding_bag."""
+    from paper_2202_12429_b200 import _lib as L
+    from paper_2202_12429_b200.device import DevicePrep
+    from paper_2202_12429_b200.traces import pack_keys
+
+    rng = np.random.default_rng(1 + flags + 2 * mode)
+    n_rows, dim, n_bags = 200, 16, 6000
+    lengths = rng.integers(0, 8, n_bags)
+    offsets = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    n = int(offsets[-1])
+    idx = np.minimum(rng.zipf(1.3, n) - 1, n_rows - 1).astype(np.int64)  # row 0 ~ 40% of occurrences
+    weights = rng.standard_normal((n_rows, dim)).astype(np.float32)
+    grad_out = rng.standard_normal((n_bags, dim)).astype(np.float32)
+    lr, eps = 0.05, 1e-10
+    # torch reference
+    w = torch.from_numpy(weights.copy()).requires_grad_(True)
+    out = torch.nn.functional.embedding_bag(torch.from_numpy(idx), w, torch.from_numpy(offsets[:-1]),
+                                            mode="mean" if mode else "sum")
+    out.backward(torch.from_numpy(grad_out))
+    g = w.grad.numpy()
+    if opt_name == "adagrad":
+        acc = g * g
+        want = weights - lr * g / (np.sqrt(acc) + eps)
+    else:
+        want = weights - lr * g
+    # ours: row arena [n_rows][2*dim] (weights | adagrad state), slot of sorted unique = row id
+    keys = pack_keys(np.zeros_like(idx), idx)
+    prep = DevicePrep(keys, np.zeros(n, np.uint8), np.asarray([0, n]), 0, occ_index=flags)
+    u = prep.num_unique
+    slots = torch.empty(u, dtype=torch.int32, device="cuda")
+    L.check(L.lib().bp_prep_key_rows(prep.handle, L.ptr(slots), L.stream_ptr()), "key rows")
+    arena = np.zeros((n_rows, 2 * dim), np.float32)
+    arena[:, :dim] = weights
+    d_arena = torch.from_numpy(arena).cuda()
+    bag_of = np.repeat(np.arange(n_bags), lengths).astype(np.int64)
+    d_bag = torch.from_numpy(bag_of).cuda()
+    scale = None
+    if mode:
+        scale = torch.from_numpy((1.0 / np.maximum(lengths, 1)).astype(np.float32)).cuda()
+    d_grad = torch.from_numpy(grad_out).cuda()
+    dirty = torch.zeros(n_rows, dtype=torch.uint8, device="cuda")
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    opt = 1 if opt_name == "adagrad" else 0
+    L.check(L.lib().bp_embbag_backward(prep.handle, L.ptr(d_grad), L.ptr(d_bag), L.ptr(scale) if mode else None,
+                                       L.ptr(d_arena), 2 * dim, L.ptr(slots), L.ptr(dirty), dim, opt,
+                                       float(np.float32(lr)), float(np.float32(eps)), L.ptr(stats), L.stream_ptr()),
+            "bwd")
+    got = d_arena.cpu().numpy()
+    np.testing.assert_allclose(got[:, :dim], want, rtol=1e-5, atol=2e-5)
+    touched = np.zeros(n_rows, bool)
+    touched[idx] = True
+    nonzero = touched & np.any(g != 0, axis=1)
+    assert np.array_equal(dirty.cpu().numpy().astype(bool), nonzero)
+    assert int(stats[1]) == int(nonzero.sum())
+    if opt_name == "adagrad":
+        np.testing.assert_allclose(got[:, dim:], g * g, rtol=1e-4, atol=1e-5)

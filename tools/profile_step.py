@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--torch-prof", action="store_true")
     ap.add_argument("--host-inputs", action="store_true")
     ap.add_argument("--cprofile", action="store_true")
+    ap.add_argument("--dlrm", action="store_true", help="DLRM mode (EmbeddingBag + MLP graph) instead of the stub")
     args = ap.parse_args()
     sc = bench.schema()
     n = args.warmup + args.steps + 12
@@ -42,7 +43,15 @@ def main():
         for i, b in enumerate(batches):
             k, lab, _ = b.packed_occurrences()
             dev[i] = (torch.from_numpy(k).cuda(), torch.from_numpy(lab).cuda())
-    pipe = _Pipeline(cfg, sc, batches, None, None, device_inputs=dev)
+    trainer = None
+    if args.dlrm:
+        from paper_2202_12429_b200.dlrm import DLRMConfig, DLRMTrainer
+
+        trainer = DLRMTrainer(DLRMConfig(mlp_dtype="bf16"), sc.num_dense, sc.num_tables, sc.emb_dim)
+        for i, b in enumerate(batches):
+            trainer.set_device_dense(i, torch.from_numpy(b.dense.astype("float32")).cuda(),
+                                     torch.from_numpy(b.labels.astype("float32")).cuda())
+    pipe = _Pipeline(cfg, sc, batches, None, None, device_inputs=dev, trainer=trainer)
     pipe.begin()
     for pos in range(args.warmup):
         pipe.step(pos)
