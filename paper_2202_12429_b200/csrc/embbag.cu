@@ -218,9 +218,8 @@ __global__ void __launch_bounds__(256) k_embbag_bwd(const uint32_t* __restrict__
 // before any add), runs a segmented Hillis-Steele scan, and at the last row
 // of every key in the tile holds that key's partial sum.  A key wholly inside
 // the tile is updated right there; a key spanning tiles (the Zipf-hot rows:
-// ~9K occurrences = 18 tiles at Criteo-Kaggle) leaves one partial per tile,
-// and the last tile to arrive (per-key counter) sums them in tile order and
-// applies the update.  Every summation order is fixed by the data, not by
+// ~9K occurrences = 18 tiles at Criteo-Kaggle) leaves one partial per tile
+// that k_embbag_bwd_span combines in a fixed order and applies.  Every summation order is fixed by the data, not by
 // scheduling, so the result is run-to-run deterministic; all occurrence work
 // is parallel (no per-key dependent chains as in the stub trainer, whose
 // order is pinned by the reference).
@@ -260,7 +259,7 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_tiles(
     long long n, int q, int T, const float4* __restrict__ grad, const int64_t* __restrict__ occ_bag,
     const float* __restrict__ bag_scale, float* __restrict__ values, int row_stride,
     const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
-    float4* __restrict__ parts, uint32_t* __restrict__ cnt, unsigned long long* __restrict__ stats) {
+    float4* __restrict__ parts, unsigned long long* __restrict__ stats) {
   extern __shared__ float4 tile[];  // [T*q] gradient rows, then [T] segment ids
   uint32_t* seg = reinterpret_cast<uint32_t*>(tile + kBwdTileF4);
   __shared__ unsigned int n_dirty;
@@ -325,23 +324,9 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_tiles(
     bool nz = false;
     if (a >= t0 && b <= t0 + rows) {
       for (int c = 0; c < q; ++c) nz |= apply_row4(row, dim, c, tile[r * q + c], opt, lr, eps);
-    } else {
+    } else {  // spans tiles: leave this tile's partial for k_embbag_bwd_span
       float4* dst = parts + ((long long)blockIdx.x * 2 + (s == seg[0] ? 0 : 1)) * q;
       for (int c = 0; c < q; ++c) dst[c] = tile[r * q + c];
-      __threadfence();
-      const long long ft = a / T, lt = (b - 1) / T;
-      if (atomicAdd(&cnt[s], 1u) != (uint32_t)(lt - ft)) continue;
-      __threadfence();
-      cnt[s] = 0;  // self-resetting for the next call
-      for (int c = 0; c < q; ++c) {
-        float4 g = zero;
-        for (long long t = ft; t <= lt; ++t) {
-          const int half = (t == ft && a != ft * T) ? 1 : 0;
-          const float4 x = __ldcg(parts + (t * 2 + half) * q + c);
-          g = t == ft ? x : f4_add(g, x);
-        }
-        nz |= apply_row4(row, dim, c, g, opt, lr, eps);
-      }
     }
     if (nz) {
       if (dirty) dirty[slot] = 1;
@@ -351,6 +336,60 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_tiles(
   if (stats && my_dirty) atomicAdd(&n_dirty, my_dirty);
   __syncthreads();
   if (stats && threadIdx.x == 0 && n_dirty) atomicAdd(&stats[1], (unsigned long long)n_dirty);
+}
+
+// Keys spanning several tiles: one warp per tile t; the warp of the key's
+// first tile (the key is t's last segment and starts inside t) sums the
+// per-tile partials -- lanes split (tile, float4) so all loads are in flight
+// at once, each lane accumulates its tiles in ascending order and a fixed
+// xor tree combines the lanes -- and applies the update.
+__global__ void __launch_bounds__(256) k_embbag_bwd_span(
+    const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start, long long n, int q, int T,
+    long long tiles, const float4* __restrict__ parts, float* __restrict__ values, int row_stride,
+    const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
+    unsigned long long* __restrict__ stats) {
+  const unsigned lane = threadIdx.x & 31u;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int per = 32 / q;  // tiles per pass
+  const int c = (int)lane % q, tl = (int)lane / q;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < tiles; t += warps) {
+    const long long last = min((t + 1) * (long long)T, n) - 1;
+    const uint32_t s = seg_of[last];
+    const long long a = seg_start[s], b = seg_start[s + 1];
+    if (a < t * T || b <= (t + 1) * (long long)T) continue;  // not a spanning key's first tile
+    const int32_t slot = slots_s[s];
+    if (slot < 0) continue;
+    const long long lt = (b - 1) / T, nt = lt - t + 1;
+    float4 acc = zero;
+    bool any = false;
+    if (tl < per) {
+      for (long long k = tl; k < nt; k += per) {
+        const long long tt = t + k;
+        const int half = (k == 0 && a != t * T) ? 1 : 0;
+        const float4 x = __ldcg(parts + (tt * 2 + half) * q + c);
+        acc = any ? f4_add(acc, x) : x;
+        any = true;
+      }
+    }
+    for (int off = per / 2; off > 0; off >>= 1) {  // fixed tree over the tile lanes
+      float4 o;
+      o.x = __shfl_down_sync(0xffffffffu, acc.x, off * q);
+      o.y = __shfl_down_sync(0xffffffffu, acc.y, off * q);
+      o.z = __shfl_down_sync(0xffffffffu, acc.z, off * q);
+      o.w = __shfl_down_sync(0xffffffffu, acc.w, off * q);
+      const bool oany = __shfl_down_sync(0xffffffffu, any ? 1 : 0, off * q) != 0;
+      if (tl < off && oany) acc = any ? f4_add(acc, o) : o;
+      any = any || (tl < off && oany);
+    }
+    bool nz = false;
+    if (tl == 0) nz = apply_row4(values + (long long)slot * row_stride, 4 * q, c, acc, opt, lr, eps);
+    const bool dirty_key = __ballot_sync(0xffffffffu, nz) != 0;
+    if (lane == 0 && dirty_key) {
+      if (dirty) dirty[slot] = 1;
+      if (stats) atomicAdd(&stats[1], 1ull);
+    }
+  }
 }
 
 // occ_s[p] = key-sorted unique index of occurrence p (segment of sorted slot j
@@ -434,10 +473,7 @@ extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t
     const int q = dim / 4, T = kBwdTileF4 / q;
     const long long tiles = (P->n_occ + T - 1) / T;
     float4* parts = nullptr;
-    uint32_t* cnt = nullptr;
     BP_CUDA_TRY(pool_alloc(&parts, (size_t)tiles * 2 * q, s));
-    BP_CUDA_TRY(pool_alloc(&cnt, (size_t)P->n_occ, s));
-    BP_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * P->n_occ, s));
     const size_t smem = sizeof(float4) * kBwdTileF4 + sizeof(uint32_t) * T;
     static bool attr = false;
     if (!attr) {
@@ -446,11 +482,12 @@ extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t
     }
     k_embbag_bwd_tiles<<<(unsigned)tiles, 256, smem, s>>>(
         P->d_occ_pos, P->d_seg_of, P->d_seg_start, P->n_occ, q, T, reinterpret_cast<const float4*>(d_grad), d_occ_bag,
-        d_bag_scale, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts, cnt,
-        (unsigned long long*)d_stats);
+        d_bag_scale, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts, (unsigned long long*)d_stats);
+    k_embbag_bwd_span<<<grid_for(tiles * 32, 256, kNumSMs * 8), 256, 0, s>>>(
+        P->d_seg_of, P->d_seg_start, P->n_occ, q, T, tiles, parts, d_values, row_stride, d_slots_s, d_dirty, opt, lr,
+        eps, (unsigned long long*)d_stats);
     BP_LAUNCH_CHECK();
     cudaFreeAsync(parts, s);
-    cudaFreeAsync(cnt, s);
     return BP_OK;
   }
   const BagGrad bg{d_grad, d_occ_bag, d_bag_scale};

@@ -173,4 +173,5 @@ def test_embedding_bag_backward_matches_torch(flags, mode, opt_name):
     assert np.array_equal(dirty.cpu().numpy().astype(bool), nonzero)
     assert int(stats[1]) == int(nonzero.sum())
     if opt_name == "adagrad":
-        np.testing.assert_allclose(got[:, dim:], g * g, rtol=1e-4, atol=1e-5)
+        # g sums ~10K terms with cancellation on the hot rows: order-sensitive
+        np.testing.assert_allclose(got[:, dim:], g * g, rtol=1e-3, atol=1e-4)
