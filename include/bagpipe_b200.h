@@ -388,6 +388,9 @@ int bp_engine_dlrm_backward(bp_engine* engine, int64_t pos, int32_t plan_slot, c
 int bp_engine_chunk_keys(bp_engine* engine, int32_t chunk_slot, uint64_t* h_out, int64_t n);
 int bp_engine_chunk_view(bp_engine* engine, int32_t chunk_slot, bp_evict_buffers* out);
 int bp_engine_sync(bp_engine* engine);
+/* Make `stream` wait for all work issued so far on the engine's streams
+ * (compute, plan, host-link) without blocking the host. */
+int bp_engine_join(bp_engine* engine, bp_stream_t stream);
 /* Per-stage device time since the last call, 7 stages: prep, planner, fetch
  * (link), apply (insert+TTL+lookup+mark), trainer, evict, flush (link).
  * Synchronises the device. */

@@ -137,6 +137,7 @@ struct bp_engine {
   uint64_t* d_keys_staging[2];
   uint8_t* d_labels_staging[2];
   cudaEvent_t staging_free[2];
+  cudaEvent_t join_ev[2];  // bp_engine_join: planq, link
   int staging_i;
   long long chunk_cap;
 };
@@ -258,6 +259,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     BP_CUDA_TRY(cudaMalloc(&e->d_keys_staging[i], n * sizeof(uint64_t)));
     BP_CUDA_TRY(cudaMalloc(&e->d_labels_staging[i], n + 16));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->staging_free[i], cudaEventDisableTiming));
+    BP_CUDA_TRY(cudaEventCreateWithFlags(&e->join_ev[i], cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventRecord(e->staging_free[i], e->planq));
   }
   e->staging_i = 0;
@@ -311,6 +313,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
     cudaFree(e->d_keys_staging[i]);
     cudaFree(e->d_labels_staging[i]);
     cudaEventDestroy(e->staging_free[i]);
+    cudaEventDestroy(e->join_ev[i]);
   }
   cudaFree(e->slots_s);
   cudaFree(e->mark);
@@ -675,6 +678,20 @@ extern "C" int bp_engine_chunk_keys(bp_engine* e, int32_t chunk_slot, uint64_t* 
 extern "C" int bp_engine_chunk_view(bp_engine* e, int32_t chunk_slot, bp_evict_buffers* out) {
   bp::ChunkSlot& c = e->chunks[chunk_slot];
   *out = bp_evict_buffers{c.keys, c.ids, c.rows, c.dirty, c.count};
+  return BP_OK;
+}
+
+extern "C" int bp_engine_join(bp_engine* e, bp_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  BP_CUDA_TRY(cudaEventRecord(e->join_ev[0], e->planq));
+  BP_CUDA_TRY(cudaEventRecord(e->join_ev[1], e->link));
+  BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[0], 0));
+  BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[1], 0));
+  if (s != e->compute) {
+    cudaEvent_t c = e->join_ev[0];
+    BP_CUDA_TRY(cudaEventRecord(c, e->compute));
+    BP_CUDA_TRY(cudaStreamWaitEvent(s, c, 0));
+  }
   return BP_OK;
 }
 
