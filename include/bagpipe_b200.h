@@ -418,6 +418,19 @@ int bp_embbag_backward(bp_prep* prep, const float* d_grad, const int64_t* d_occ_
                        int32_t opt, float lr, float eps, int64_t* d_stats, bp_stream_t stream);
 int bp_prep_occ_sorted_index(bp_prep* prep, uint32_t* d_occ_s, bp_stream_t stream);
 
+/* DLRM feature interaction (dense-model side of DLRM mode; the reference has
+ * no model).  z = [x; emb_0..emb_{T-1}] per sample (T+1 vectors of D);
+ * out row = [x | z_i . z_j, i > j, torch.tril_indices(T+1, T+1, -1) order |
+ * zeros up to out_stride].  x / out / gout / gx are bf16 when the flag is
+ * set, else f32; emb and gemb are f32; fp32 arithmetic.  backward:
+ * gx = gout[:, :D] + (G z)_0, gemb_t = (G z)_{t+1}, G the symmetric pair
+ * gradient.  T <= 127, D <= 256. */
+int bp_dlrm_interact_forward(const void* d_x, int32_t x_bf16, const float* d_emb, int64_t B, int32_t T, int32_t D,
+                             void* d_out, int32_t out_bf16, int32_t out_stride, bp_stream_t stream);
+int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const float* d_emb, const void* d_gout, int32_t g_bf16,
+                              int64_t B, int32_t T, int32_t D, int32_t out_stride, void* d_gx, float* d_gemb,
+                              bp_stream_t stream);
+
 /* ------------------------------------------------------------ utilities */
 /* Sort packed keys ascending with a u32 payload (stable); n host-known. */
 int bp_sort_keys_u64(uint64_t* d_keys, uint32_t* d_vals, int64_t n, int32_t key_bits, bp_stream_t stream);

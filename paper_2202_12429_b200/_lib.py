@@ -168,6 +168,9 @@ _SIGS = {
     "bp_engine_dlrm_forward": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_u64, c_i32, c_i32, c_vp]),
     "bp_engine_dlrm_backward": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_f32, c_f32, c_i32, c_i32,
                                         P(StepResult)]),
+    "bp_dlrm_interact_forward": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp]),
+    "bp_dlrm_interact_backward": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp,
+                                          c_vp]),
     "bp_embbag_forward": (c_i32, [c_vp, c_vp, c_i32, c_vp, c_i32, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "bp_embbag_backward": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32, c_f32,
                                    c_vp, c_vp]),

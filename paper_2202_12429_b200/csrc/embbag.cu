@@ -338,6 +338,139 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_tiles(
   if (stats && threadIdx.x == 0 && n_dirty) atomicAdd(&stats[1], (unsigned long long)n_dirty);
 }
 
+// Warp tiles (dim 4..32, the DLRM shapes): one warp reduces T = 32 * R
+// sorted positions (R = 8 / Q rows per lane, Q float4 per row), entirely in
+// registers: per-lane segmented sum over its R rows, then a segmented
+// Hillis-Steele scan of the lanes' last-segment partials with shuffles
+// (element (has_head, value), earlier + later), then the carry-in of each
+// lane's first segment.  No shared memory, no barriers; every order is fixed.
+template <int Q>
+__global__ void __launch_bounds__(256) k_embbag_bwd_warp(
+    const uint32_t* __restrict__ occ_pos, const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start,
+    long long n, const float4* __restrict__ grad, const int64_t* __restrict__ occ_bag,
+    const float* __restrict__ bag_scale, float* __restrict__ values, int row_stride,
+    const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
+    float4* __restrict__ parts, unsigned long long* __restrict__ stats) {
+  constexpr int R = 8 / Q, T = 32 * R;
+  const unsigned lane = threadIdx.x & 31u;
+  const long long tile = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long t0 = tile * T;
+  if (t0 >= n) return;
+  const long long r0 = t0 + (long long)lane * R;
+  uint32_t sg[R];
+  long long pk[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const bool ok = r0 + j < n;
+    sg[j] = ok ? seg_of[r0 + j] : 0xffffffffu;
+    pk[j] = ok ? (long long)occ_pos[r0 + j] : -1;
+  }
+  if (occ_bag) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (pk[j] >= 0) pk[j] = occ_bag[pk[j]];
+  }
+  float4 v[R][Q];
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int c = 0; c < Q; ++c) v[j][c] = pk[j] >= 0 ? grad[pk[j] * Q + c] : zero;
+  if (bag_scale) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (pk[j] >= 0) {
+        const float sc = bag_scale[pk[j]];
+#pragma unroll
+        for (int c = 0; c < Q; ++c)
+          v[j][c] = make_float4(__fmul_rn(v[j][c].x, sc), __fmul_rn(v[j][c].y, sc), __fmul_rn(v[j][c].z, sc),
+                                __fmul_rn(v[j][c].w, sc));
+      }
+  }
+  // per-lane inclusive segmented sums
+  bool inner_head = false;
+#pragma unroll
+  for (int j = 1; j < R; ++j) {
+    if (sg[j] == sg[j - 1]) {
+#pragma unroll
+      for (int c = 0; c < Q; ++c) v[j][c] = f4_add(v[j - 1][c], v[j][c]);
+    } else {
+      inner_head = true;
+    }
+  }
+  const uint32_t prev_last = __shfl_up_sync(0xffffffffu, sg[R - 1], 1);
+  const bool first_head = lane == 0 || sg[0] != prev_last;
+  // segmented inclusive scan over lanes of (flag, last-segment partial)
+  bool flag = first_head || inner_head;
+  float4 agg[Q];
+#pragma unroll
+  for (int c = 0; c < Q; ++c) agg[c] = v[R - 1][c];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const bool fo = __shfl_up_sync(0xffffffffu, flag ? 1 : 0, off) != 0;
+#pragma unroll
+    for (int c = 0; c < Q; ++c) {
+      float4 o;
+      o.x = __shfl_up_sync(0xffffffffu, agg[c].x, off);
+      o.y = __shfl_up_sync(0xffffffffu, agg[c].y, off);
+      o.z = __shfl_up_sync(0xffffffffu, agg[c].z, off);
+      o.w = __shfl_up_sync(0xffffffffu, agg[c].w, off);
+      if (lane >= (unsigned)off && !flag) agg[c] = f4_add(o, agg[c]);
+    }
+    if (lane >= (unsigned)off) flag = flag || fo;
+  }
+  // carry-in for the first segment of this lane = previous lane's inclusive aggregate
+  float4 carry[Q];
+#pragma unroll
+  for (int c = 0; c < Q; ++c) {
+    carry[c].x = __shfl_up_sync(0xffffffffu, agg[c].x, 1);
+    carry[c].y = __shfl_up_sync(0xffffffffu, agg[c].y, 1);
+    carry[c].z = __shfl_up_sync(0xffffffffu, agg[c].z, 1);
+    carry[c].w = __shfl_up_sync(0xffffffffu, agg[c].w, 1);
+  }
+  if (!first_head) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (sg[j] == sg[0]) {
+#pragma unroll
+        for (int c = 0; c < Q; ++c) v[j][c] = f4_add(carry[c], v[j][c]);
+      }
+  }
+  const uint32_t next_first = __shfl_down_sync(0xffffffffu, sg[0], 1);
+  const uint32_t tile_first = __shfl_sync(0xffffffffu, sg[0], 0);
+  const long long rows = min((long long)T, n - t0);
+  const int dim = 4 * Q;
+  unsigned n_nz = 0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (r0 + j >= n) break;
+    const bool end = (j < R - 1) ? sg[j + 1] != sg[j] : (lane == 31 || r0 + j + 1 >= n || next_first != sg[j]);
+    if (!end) continue;
+    const uint32_t s = sg[j];
+    const int32_t slot = slots_s[s];
+    if (slot < 0) continue;
+    const long long a = seg_start[s], b = seg_start[s + 1];
+    if (a >= t0 && b <= t0 + rows) {
+      float* row = values + (long long)slot * row_stride;
+      bool nz = false;
+#pragma unroll
+      for (int c = 0; c < Q; ++c) nz |= apply_row4(row, dim, c, v[j][c], opt, lr, eps);
+      if (nz) {
+        if (dirty) dirty[slot] = 1;
+        ++n_nz;
+      }
+    } else {  // spans tiles: this tile's partial for k_embbag_bwd_span
+      float4* dst = parts + (tile * 2 + (s == tile_first ? 0 : 1)) * Q;
+#pragma unroll
+      for (int c = 0; c < Q; ++c) dst[c] = v[j][c];
+    }
+  }
+  if (stats) {
+    for (int off = 16; off > 0; off >>= 1) n_nz += __shfl_down_sync(0xffffffffu, n_nz, off);
+    if (lane == 0 && n_nz) atomicAdd(&stats[1], (unsigned long long)n_nz);
+  }
+}
+
 // Keys spanning several tiles: one warp per tile t; the warp of the key's
 // first tile (the key is t's last segment and starts inside t) sums the
 // per-tile partials -- lanes split (tile, float4) so all loads are in flight
@@ -361,17 +494,30 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_span(
     const int32_t slot = slots_s[s];
     if (slot < 0) continue;
     const long long lt = (b - 1) / T, nt = lt - t + 1;
-    float4 acc = zero;
-    bool any = false;
-    if (tl < per) {
-      for (long long k = tl; k < nt; k += per) {
-        const long long tt = t + k;
-        const int half = (k == 0 && a != t * T) ? 1 : 0;
-        const float4 x = __ldcg(parts + (tt * 2 + half) * q + c);
-        acc = any ? f4_add(acc, x) : x;
-        any = true;
+    // four independent accumulators per lane (fixed assignment k % 4), so
+    // four partial loads are in flight; combined in a fixed order below
+    float4 acc4[4] = {zero, zero, zero, zero};
+    bool any4[4] = {false, false, false, false};
+    for (long long k0 = tl; k0 < nt; k0 += 4 * per) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long k = k0 + (long long)u * per;
+        if (k < nt) {
+          const int half = (k == 0 && a != t * T) ? 1 : 0;
+          const float4 x = __ldcg(parts + ((t + k) * 2 + half) * q + c);
+          acc4[u] = any4[u] ? f4_add(acc4[u], x) : x;
+          any4[u] = true;
+        }
       }
     }
+    float4 acc = acc4[0];
+    bool any = any4[0];
+#pragma unroll
+    for (int u = 1; u < 4; ++u)
+      if (any4[u]) {
+        acc = any ? f4_add(acc, acc4[u]) : acc4[u];
+        any = true;
+      }
     for (int off = per / 2; off > 0; off >>= 1) {  // fixed tree over the tile lanes
       float4 o;
       o.x = __shfl_down_sync(0xffffffffu, acc.x, off * q);
@@ -469,6 +615,31 @@ extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t
   int G, dpl;
   shape_of(dim, &G, &dpl);
   cudaStream_t s = (cudaStream_t)stream;
+  if (P->d_seg_of && (dim & 3) == 0 && (row_stride & 3) == 0 && dim <= 32 && (32 % dim) == 0) {
+    const int q = dim / 4, T = 32 * (8 / q);
+    const long long tiles = (P->n_occ + T - 1) / T;
+    float4* parts = nullptr;
+    BP_CUDA_TRY(pool_alloc(&parts, (size_t)tiles * 2 * q, s));
+    const unsigned blocks = (unsigned)((tiles + 7) / 8);
+#define BP_BWD_WARP(QQ)                                                                                        \
+  k_embbag_bwd_warp<QQ><<<blocks, 256, 0, s>>>(P->d_occ_pos, P->d_seg_of, P->d_seg_start, P->n_occ,              \
+                                               reinterpret_cast<const float4*>(d_grad), d_occ_bag, d_bag_scale,  \
+                                               d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts,    \
+                                               (unsigned long long*)d_stats)
+    switch (q) {
+      case 1: BP_BWD_WARP(1); break;
+      case 2: BP_BWD_WARP(2); break;
+      case 4: BP_BWD_WARP(4); break;
+      default: BP_BWD_WARP(8); break;
+    }
+#undef BP_BWD_WARP
+    k_embbag_bwd_span<<<grid_for(tiles * 32, 256, kNumSMs * 8), 256, 0, s>>>(
+        P->d_seg_of, P->d_seg_start, P->n_occ, q, T, tiles, parts, d_values, row_stride, d_slots_s, d_dirty, opt, lr,
+        eps, (unsigned long long*)d_stats);
+    BP_LAUNCH_CHECK();
+    cudaFreeAsync(parts, s);
+    return BP_OK;
+  }
   if (P->d_seg_of && (dim & 3) == 0 && (row_stride & 3) == 0 && dim <= 128) {
     const int q = dim / 4, T = kBwdTileF4 / q;
     const long long tiles = (P->n_occ + T - 1) / T;

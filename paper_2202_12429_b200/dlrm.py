@@ -55,6 +55,36 @@ def mlp(sizes, last_act: bool, in_pad: int = 0) -> nn.Sequential:
     return nn.Sequential(*layers)
 
 
+class _Interact(torch.autograd.Function):
+    """Fused DLRM interaction (csrc/interact.cu): [x | tril(z z^T) | 0-pad]."""
+
+    @staticmethod
+    def forward(ctx, x, emb, out_stride: int):
+        x = x.contiguous()
+        emb = emb.contiguous().float()
+        b, t, d = emb.shape
+        bf = x.dtype == torch.bfloat16
+        out = torch.empty((b, out_stride), dtype=x.dtype, device=x.device)
+        L.check(L.lib().bp_dlrm_interact_forward(L.ptr(x), int(bf), L.ptr(emb), b, t, d, L.ptr(out), int(bf),
+                                                 out_stride, L.stream_ptr()), "bp_dlrm_interact_forward")
+        ctx.save_for_backward(x, emb)
+        ctx.out_stride = out_stride
+        return out
+
+    @staticmethod
+    def backward(ctx, gout):
+        x, emb = ctx.saved_tensors
+        b, t, d = emb.shape
+        gout = gout.contiguous()
+        gx = torch.empty_like(x)
+        gemb = torch.empty_like(emb)
+        L.check(L.lib().bp_dlrm_interact_backward(L.ptr(x), int(x.dtype == torch.bfloat16), L.ptr(emb), L.ptr(gout),
+                                                  int(gout.dtype == torch.bfloat16), b, t, d, ctx.out_stride,
+                                                  L.ptr(gx), L.ptr(gemb), L.stream_ptr()),
+                "bp_dlrm_interact_backward")
+        return gx, gemb, None
+
+
 def _pad8(n: int) -> int:
     return (-n) % 8
 
@@ -81,6 +111,9 @@ class DLRMDense(nn.Module):
         if dense.shape[1] == self.num_dense and self.dense_pad:
             dense = nn.functional.pad(dense, (0, self.dense_pad))
         x = self.bottom(dense)                                # [B, D]
+        if pooled.is_cuda:
+            # fused CUDA interaction (no eager fallback on the GPU path)
+            return self.top(_Interact.apply(x, pooled, self.pairs + self.dim + self.top_pad)).squeeze(1)
         z = torch.cat([x.unsqueeze(1).to(pooled.dtype), pooled], dim=1)  # [B, T+1, D]
         zz = torch.bmm(z, z.transpose(1, 2))                  # [B, T+1, T+1]
         inter = zz.flatten(1).index_select(1, self.tril_flat)  # [B, pairs]

@@ -112,19 +112,20 @@ def test_embedding_bag_forward_matches_torch():
         np.testing.assert_allclose(out.cpu().numpy(), want.numpy(), rtol=1e-5, atol=1e-6)
 
 
-@pytest.mark.parametrize("flags", [0, 2])
+@pytest.mark.parametrize("flags,dim", [(0, 16), (2, 16), (2, 8), (2, 64), (2, 12)])
 @pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("opt_name", ["sgd", "adagrad"])
-def test_embedding_bag_backward_matches_torch(flags, mode, opt_name):
-    """Multi-key bags (sum/mean), hot keys spanning many reduction tiles
-    (flags=2: the tiled reduce-by-key kernel; 0: the per-key kernel), SGD and
-    Adagrad in place, against torch autograd of embedding_bag."""
+def test_embedding_bag_backward_matches_torch(flags, dim, mode, opt_name):
+    """Multi-key bags (sum/mean), hot keys spanning many reduction tiles, SGD
+    and Adagrad in place, against torch autograd of embedding_bag.  flags=2
+    selects the reduce-by-key kernels (warp tiles for dim 8/16, block tiles
+    for 64 and 12); flags=0 the per-key kernel."""
     from paper_2202_12429_b200 import _lib as L
     from paper_2202_12429_b200.device import DevicePrep
     from paper_2202_12429_b200.traces import pack_keys
 
     rng = np.random.default_rng(1 + flags + 2 * mode)
-    n_rows, dim, n_bags = 200, 16, 6000
+    n_rows, n_bags = 200, 6000
     lengths = rng.integers(0, 8, n_bags)
     offsets = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
     n = int(offsets[-1])
@@ -175,3 +176,31 @@ def test_embedding_bag_backward_matches_torch(flags, mode, opt_name):
     if opt_name == "adagrad":
         # g sums ~10K terms with cancellation on the hot rows: order-sensitive
         np.testing.assert_allclose(got[:, dim:], g * g, rtol=1e-3, atol=1e-4)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_fused_interaction_matches_torch(dtype):
+    """csrc/interact.cu forward/backward vs cat + bmm + tril gather in fp32."""
+    from paper_2202_12429_b200.dlrm import _Interact
+
+    torch.manual_seed(0)
+    b, t, d = 300, 26, 16
+    n = t + 1
+    pairs = n * (n - 1) // 2
+    stride = d + pairs + 1
+    x = torch.randn(b, d, device="cuda").to(dtype).requires_grad_(True)
+    emb = torch.randn(b, t, d, device="cuda", requires_grad=True)
+    out = _Interact.apply(x, emb, stride)
+    g = torch.randn(b, stride, device="cuda").to(dtype)
+    out.backward(g)
+    x32 = x.detach().float().requires_grad_(True)
+    e32 = emb.detach().clone().requires_grad_(True)
+    z = torch.cat([x32.unsqueeze(1), e32], 1)
+    li, lj = torch.tril_indices(n, n, offset=-1, device="cuda")
+    want = torch.cat([x32, torch.bmm(z, z.transpose(1, 2))[:, li, lj], torch.zeros(b, 1, device="cuda")], 1)
+    want.backward(g.float())
+    tol = dict(rtol=1e-5, atol=1e-5) if dtype == torch.float32 else dict(rtol=2e-2, atol=5e-2)
+    torch.testing.assert_close(out.float(), want.detach(), **tol)
+    torch.testing.assert_close(x.grad.float(), x32.grad, **tol)
+    torch.testing.assert_close(emb.grad, e32.grad, rtol=1e-5 if dtype == torch.float32 else 2e-2,
+                               atol=1e-4 if dtype == torch.float32 else 5e-2)

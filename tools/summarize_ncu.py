@@ -2,6 +2,7 @@
 
   python tools/summarize_ncu.py launches <launches.csv> [steps]   -> markdown table of per-kernel device time
   python tools/summarize_ncu.py full <report.ncu-rep>            -> key metrics per captured kernel
+  python tools/summarize_ncu.py lines <report.ncu-rep> <kernel regex> [n]  -> top CUDA lines by stall samples
 """
 
 from __future__ import annotations
@@ -59,6 +60,40 @@ def full(path: str) -> str:
     return "\n".join(out)
 
 
+def lines(path: str, kernel: str, n: int = 15) -> str:
+    raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass,cuda",
+                          "--kernel-name", f"regex:{kernel}", "--launch-count", "1"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    agg = collections.defaultdict(lambda: [0, ""])
+    hdr, last = None, ""
+    for r in rows:
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or len(r) < len(hdr):
+            continue
+        try:
+            samples = int(r[4] or 0)
+        except ValueError:
+            continue
+        key = r[0] or last  # SASS rows after the first of a CUDA line carry no line number
+        last = key
+        agg[key][0] += samples
+        if not agg[key][1]:
+            agg[key][1] = r[1].strip()
+    tot = sum(v[0] for v in agg.values()) or 1
+    out = [f"{kernel}: {tot} stall samples", "", "| line | samples | share | source |", "|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda x: -x[1][0])[:n]:
+        out.append(f"| {k} | {v[0]} | {100 * v[0] / tot:.1f}% | `{v[1][:90]}` |")
+    return "\n".join(out)
+
+
 if __name__ == "__main__":
     kind, path = sys.argv[1], sys.argv[2]
-    print(launches(path, int(sys.argv[3]) if len(sys.argv) > 3 else 1) if kind == "launches" else full(path))
+    if kind == "launches":
+        print(launches(path, int(sys.argv[3]) if len(sys.argv) > 3 else 1))
+    elif kind == "lines":
+        print(lines(path, sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else 15))
+    else:
+        print(full(path))
