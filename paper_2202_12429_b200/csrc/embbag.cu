@@ -483,7 +483,8 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_span(
     unsigned long long* __restrict__ stats) {
   const unsigned lane = threadIdx.x & 31u;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  const int per = 32 / q;  // tiles per pass
+  int per = 1;  // tiles per pass: a power of two (the xor tree below), per * q <= 32
+  while (per * 2 * q <= 32) per *= 2;
   const int c = (int)lane % q, tl = (int)lane / q;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < tiles; t += warps) {
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_span(
     // four partial loads are in flight; combined in a fixed order below
     float4 acc4[4] = {zero, zero, zero, zero};
     bool any4[4] = {false, false, false, false};
-    for (long long k0 = tl; k0 < nt; k0 += 4 * per) {
+    for (long long k0 = tl; tl < per && k0 < nt; k0 += 4 * per) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const long long k = k0 + (long long)u * per;

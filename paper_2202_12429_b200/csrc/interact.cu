@@ -99,6 +99,126 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd(const void* __re
   }
 }
 
+// Fast path (n = T+1 <= 32, D in {4, 8, 16, 32}): lane i owns z_i in
+// registers and walks j < i (forward) or all j (backward) over shared-memory
+// rows read as float4 broadcasts (every lane reads the same z_j: no bank
+// conflicts); the output row is staged in shared memory and written
+// coalesced.  G rows use an odd stride (conflict-free column walks).
+template <int D>
+__global__ void __launch_bounds__(kIxWarps * 32) k_interact_fwd_reg(const void* __restrict__ x, int x_bf16,
+                                                                    const float* __restrict__ emb, long long B,
+                                                                    int T, void* __restrict__ out, int out_bf16,
+                                                                    int out_stride) {
+  extern __shared__ float ix_smem[];
+  const int n = T + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* z = ix_smem + warp * (32 * D + ((out_stride + 3) & ~3));  // [n][D] then the staged output row
+  float* o = z + 32 * D;
+  for (long long b = (long long)blockIdx.x * kIxWarps + warp; b < B; b += (long long)gridDim.x * kIxWarps) {
+    for (int e = lane; e < n * D; e += 32)
+      z[e] = e < D ? ld_any(x, b * D + e, x_bf16) : emb[b * T * D + (e - D)];
+    __syncwarp();
+    if (lane < n) {
+      float zi[D];
+#pragma unroll
+      for (int d = 0; d < D; d += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(z + lane * D + d);
+        zi[d] = v.x; zi[d + 1] = v.y; zi[d + 2] = v.z; zi[d + 3] = v.w;
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) o[d] = zi[d];
+      }
+      float* orow = o + D + lane * (lane - 1) / 2;
+      for (int j = 0; j < lane; ++j) {
+        float acc = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; d += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(z + j * D + d);
+          acc = fmaf(zi[d], v.x, acc);
+          acc = fmaf(zi[d + 1], v.y, acc);
+          acc = fmaf(zi[d + 2], v.z, acc);
+          acc = fmaf(zi[d + 3], v.w, acc);
+        }
+        orow[j] = acc;
+      }
+    }
+    const int P = n * (n - 1) / 2;
+    for (int c = D + P + lane; c < out_stride; c += 32) o[c] = 0.f;
+    __syncwarp();
+    const long long ob = b * out_stride;
+    if (out_bf16 && (out_stride & 1) == 0) {
+      __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(out) + ob;
+      for (int c = 2 * lane; c < out_stride; c += 64) {
+        if (c + 1 < out_stride) {
+          *reinterpret_cast<__nv_bfloat162*>(op + c) = __floats2bfloat162_rn(o[c], o[c + 1]);
+        } else {
+          op[c] = __float2bfloat16_rn(o[c]);
+        }
+      }
+    } else {
+      for (int c = lane; c < out_stride; c += 32) st_any(out, ob + c, o[c], out_bf16);
+    }
+    __syncwarp();
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* __restrict__ x, int x_bf16,
+                                                                    const float* __restrict__ emb,
+                                                                    const void* __restrict__ gout, int g_bf16,
+                                                                    long long B, int T, int out_stride,
+                                                                    void* __restrict__ gx, float* __restrict__ gemb) {
+  extern __shared__ float ix_smem[];
+  constexpr int LG = 33;  // G row stride (odd)
+  const int n = T + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* z = ix_smem + warp * (32 * D + 32 * LG);
+  float* G = z + 32 * D;
+  for (long long b = (long long)blockIdx.x * kIxWarps + warp; b < B; b += (long long)gridDim.x * kIxWarps) {
+    for (int e = lane; e < n * D; e += 32)
+      z[e] = e < D ? ld_any(x, b * D + e, x_bf16) : emb[b * T * D + (e - D)];
+    const long long ob = b * out_stride;
+    const int P = n * (n - 1) / 2;
+    if (lane < n) G[lane * LG + lane] = 0.f;
+    for (int k = lane; k < P; k += 32) {
+      int i = (int)((1.f + sqrtf(1.f + 8.f * (float)k)) * 0.5f);
+      while (i * (i - 1) / 2 > k) --i;
+      while ((i + 1) * i / 2 <= k) ++i;
+      const int j = k - i * (i - 1) / 2;
+      const float g = ld_any(gout, ob + D + k, g_bf16);
+      G[i * LG + j] = g;
+      G[j * LG + i] = g;
+    }
+    __syncwarp();
+    if (lane < n) {
+      float acc[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) acc[d] = 0.f;
+      for (int j = 0; j < n; ++j) {
+        const float g = G[lane * LG + j];
+#pragma unroll
+        for (int d = 0; d < D; d += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(z + j * D + d);
+          acc[d] = fmaf(g, v.x, acc[d]);
+          acc[d + 1] = fmaf(g, v.y, acc[d + 1]);
+          acc[d + 2] = fmaf(g, v.z, acc[d + 2]);
+          acc[d + 3] = fmaf(g, v.w, acc[d + 3]);
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) st_any(gx, b * D + d, acc[d] + ld_any(gout, ob + d, g_bf16), x_bf16);
+      } else {
+        float4* dst = reinterpret_cast<float4*>(gemb + (b * T + (lane - 1)) * D);
+#pragma unroll
+        for (int d = 0; d < D; d += 4) dst[d / 4] = make_float4(acc[d], acc[d + 1], acc[d + 2], acc[d + 3]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 static size_t fwd_smem(int T, int D) {
   const int n = T + 1;
   return sizeof(float) * kIxWarps * n * (D + 1) + 2 * (size_t)(n * (n - 1) / 2) + 16;
@@ -126,6 +246,25 @@ extern "C" int bp_dlrm_interact_forward(const void* d_x, int32_t x_bf16, const f
   const int rc = check_shape(B, T, D, out_stride);
   if (rc != BP_OK) return rc;
   if (B == 0) return BP_OK;
+  const long long nblk = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * 16);
+  if (T + 1 <= 32 && (D == 4 || D == 8 || D == 16 || D == 32)) {
+    const size_t sm = sizeof(float) * kIxWarps * (32 * D + ((out_stride + 3) & ~3));
+#define BP_IX_FWD(DD)                                                                                              \
+  {                                                                                                                \
+    BP_CUDA_TRY(cudaFuncSetAttribute(k_interact_fwd_reg<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_interact_fwd_reg<DD><<<(unsigned)nblk, kIxWarps * 32, sm, (cudaStream_t)stream>>>(d_x, x_bf16, d_emb, B, T,    \
+                                                                                        d_out, out_bf16, out_stride); \
+  }
+    switch (D) {
+      case 4: BP_IX_FWD(4); break;
+      case 8: BP_IX_FWD(8); break;
+      case 16: BP_IX_FWD(16); break;
+      default: BP_IX_FWD(32); break;
+    }
+#undef BP_IX_FWD
+    BP_LAUNCH_CHECK();
+    return BP_OK;
+  }
   const size_t smem = fwd_smem(T, D);
   BP_CUDA_TRY(cudaFuncSetAttribute(k_interact_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const long long blocks = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * 16);
@@ -142,6 +281,25 @@ extern "C" int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const 
   const int rc = check_shape(B, T, D, out_stride);
   if (rc != BP_OK) return rc;
   if (B == 0) return BP_OK;
+  const long long nblk = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * 16);
+  if (T + 1 <= 32 && (D == 4 || D == 8 || D == 16 || D == 32)) {
+    const size_t sm = sizeof(float) * kIxWarps * (32 * D + 32 * 33);
+#define BP_IX_BWD(DD)                                                                                              \
+  {                                                                                                                \
+    BP_CUDA_TRY(cudaFuncSetAttribute(k_interact_bwd_reg<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_interact_bwd_reg<DD><<<(unsigned)nblk, kIxWarps * 32, sm, (cudaStream_t)stream>>>(                          \
+        d_x, x_bf16, d_emb, d_gout, g_bf16, B, T, out_stride, d_gx, d_gemb);                                         \
+  }
+    switch (D) {
+      case 4: BP_IX_BWD(4); break;
+      case 8: BP_IX_BWD(8); break;
+      case 16: BP_IX_BWD(16); break;
+      default: BP_IX_BWD(32); break;
+    }
+#undef BP_IX_BWD
+    BP_LAUNCH_CHECK();
+    return BP_OK;
+  }
   const size_t smem = bwd_smem(T, D);
   BP_CUDA_TRY(cudaFuncSetAttribute(k_interact_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const long long blocks = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * 16);

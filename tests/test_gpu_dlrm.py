@@ -178,16 +178,19 @@ def test_embedding_bag_backward_matches_torch(flags, dim, mode, opt_name):
         np.testing.assert_allclose(got[:, dim:], g * g, rtol=1e-3, atol=1e-4)
 
 
+@pytest.mark.parametrize("t,d,pad", [(26, 16, 1), (26, 16, 0), (5, 8, 3), (40, 16, 2), (26, 12, 1)])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_fused_interaction_matches_torch(dtype):
-    """csrc/interact.cu forward/backward vs cat + bmm + tril gather in fp32."""
+def test_fused_interaction_matches_torch(dtype, t, d, pad):
+    """csrc/interact.cu forward/backward (register fast path for T+1 <= 32
+    and D in {4,8,16,32}, generic kernels otherwise) vs cat + bmm + tril
+    gather in fp32."""
     from paper_2202_12429_b200.dlrm import _Interact
 
     torch.manual_seed(0)
-    b, t, d = 300, 26, 16
+    b = 300
     n = t + 1
     pairs = n * (n - 1) // 2
-    stride = d + pairs + 1
+    stride = d + pairs + pad
     x = torch.randn(b, d, device="cuda").to(dtype).requires_grad_(True)
     emb = torch.randn(b, t, d, device="cuda", requires_grad=True)
     out = _Interact.apply(x, emb, stride)
@@ -197,7 +200,7 @@ def test_fused_interaction_matches_torch(dtype):
     e32 = emb.detach().clone().requires_grad_(True)
     z = torch.cat([x32.unsqueeze(1), e32], 1)
     li, lj = torch.tril_indices(n, n, offset=-1, device="cuda")
-    want = torch.cat([x32, torch.bmm(z, z.transpose(1, 2))[:, li, lj], torch.zeros(b, 1, device="cuda")], 1)
+    want = torch.cat([x32, torch.bmm(z, z.transpose(1, 2))[:, li, lj], torch.zeros(b, pad, device="cuda")], 1)
     want.backward(g.float())
     tol = dict(rtol=1e-5, atol=1e-5) if dtype == torch.float32 else dict(rtol=2e-2, atol=5e-2)
     torch.testing.assert_close(out.float(), want.detach(), **tol)

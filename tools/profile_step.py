@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--torch-prof", action="store_true")
     ap.add_argument("--host-inputs", action="store_true")
     ap.add_argument("--cprofile", action="store_true")
+    ap.add_argument("--trace", default=None, help="write a chrome trace (kernel timeline per stream) here")
+    ap.add_argument("--flush", action="store_true", help="256 MiB L2 flush before each step, like bench.py")
     ap.add_argument("--dlrm", action="store_true", help="DLRM mode (EmbeddingBag + MLP graph) instead of the stub")
     args = ap.parse_args()
     sc = bench.schema()
@@ -56,13 +58,24 @@ def main():
     for pos in range(args.warmup):
         pipe.step(pos)
     torch.cuda.synchronize()
-    if args.torch_prof:
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
+
+    def one(i):
+        if flush_buf is not None:
+            with torch.cuda.stream(pipe.stream):
+                flush_buf.zero_()
+        pipe.step(args.warmup + i)
+
+    if args.torch_prof or args.trace:
         from torch.profiler import ProfilerActivity, profile
 
         with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
             for i in range(args.steps):
-                pipe.step(args.warmup + i)
+                one(i)
             torch.cuda.synchronize()
+        if args.trace:
+            prof.export_chrome_trace(args.trace)
+            return
         print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=40))
         print(prof.key_averages().table(sort_by="cpu_time_total", row_limit=25))
         return
@@ -82,7 +95,7 @@ def main():
     for i in range(args.steps):
         if args.nvtx:
             torch.cuda.nvtx.range_push("timed_step")
-        pipe.step(args.warmup + i)
+        one(i)
         if args.nvtx:
             torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
