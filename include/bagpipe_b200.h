@@ -370,6 +370,7 @@ int bp_engine_release_batch(bp_engine* engine, int64_t pos);
 int bp_engine_refill(bp_engine* engine, int64_t pos);
 int bp_engine_pop(bp_engine* engine, int64_t pos, int32_t* slot_out);
 int bp_engine_plan_counts(bp_engine* engine, int32_t slot, int64_t* h_out4); /* waits for that pop */
+int bp_engine_plan_ready(bp_engine* engine, int32_t slot, int32_t* out);      /* non-blocking query */
 int bp_engine_plan_view(bp_engine* engine, int32_t slot, bp_plan_buffers* out, float** d_staging);
 int bp_engine_fetch(bp_engine* engine, int32_t slot);
 int bp_engine_flush(bp_engine* engine, const int32_t* h_chunk_slots, int32_t n);

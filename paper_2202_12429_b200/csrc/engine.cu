@@ -474,6 +474,19 @@ extern "C" int bp_engine_plan_counts(bp_engine* e, int32_t slot, int64_t* out4) 
   return BP_OK;
 }
 
+// 1 if the pop of plan slot `slot` has completed on the device, else 0
+// (non-blocking: lets the host emit plans ahead without stalling).
+extern "C" int bp_engine_plan_ready(bp_engine* e, int32_t slot, int32_t* out) {
+  const cudaError_t q = cudaEventQuery(e->plans[slot].popped);
+  if (q == cudaErrorNotReady) {
+    *out = 0;
+    return BP_OK;
+  }
+  BP_CUDA_TRY(q);
+  *out = 1;
+  return BP_OK;
+}
+
 extern "C" int bp_engine_plan_view(bp_engine* e, int32_t slot, bp_plan_buffers* out, float** staging) {
   bp::PlanSlot& ps = e->plans[slot];
   *out = bp_plan_buffers{ps.keys, ps.ids, ps.ttls, ps.ttl_k, ps.evict_keys, ps.evict_ids, ps.counts};

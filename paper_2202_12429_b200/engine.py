@@ -162,6 +162,7 @@ class _Plan:
 
 
 class _Pipeline:
+    EMIT_AHEAD = 3  # plans emitted ahead of dispatch (see _emit_ahead)
     """One pipelined run (reference engine.py:239-649) on the native engine.
 
     The host keeps the reference's scalar control flow -- window refill,
@@ -201,8 +202,9 @@ class _Pipeline:
                             dim=width, num_ranks=self.T, c_value=f32(stub.c_value),
                             c_label=f32(stub.c_label), lr=f32(stub.lr),
                             record_keys=1 if (cfg.record_events or fault == FAULT_NO_GATE) else 0,
-                            plan_slots=self.L0 + 4, chunk_slots=self.flush_interval + 4,
-                            prep_slots=2 * self.L0 + 8, timing=1 if timing else 0, init_dims=schema.emb_dim,
+                            plan_slots=self.L0 + 4 + self.EMIT_AHEAD, chunk_slots=self.flush_interval + 4,
+                            prep_slots=2 * self.L0 + 8 + self.EMIT_AHEAD, timing=1 if timing else 0,
+                            init_dims=schema.emb_dim,
                             prep_flags=2 if trainer is not None else 0)
         h = C.c_void_p()
         L.check(self.lib.bp_engine_create(L.Context.get().handle, DeviceSchema.get(self.row_schema).handle,
@@ -222,7 +224,7 @@ class _Pipeline:
         self.snapshots = {} if cfg.check_mirror else None
         self._adapt_pending = None
         self.free_chunks = list(range(self.flush_interval + 4))
-        self.free_plans = set(range(self.L0 + 4))
+        self.free_plans = set(range(self.L0 + 4 + self.EMIT_AHEAD))
 
         self.pending: deque = deque()
         self.exhausted = False
@@ -501,6 +503,27 @@ class _Pipeline:
             partial["ttl_updates"] = ttl
         self._maintenance(pos, chunk, n_ev, n_ev_dirty, drain, int(res.drained), int(res.drained_dirty), partial)
         self._release(pos)
+        self._emit_ahead()
+
+    def _emit_ahead(self) -> None:
+        """Emit plans ahead of their dispatch while the previous pop already
+        finished on the device (non-blocking query), so the reference's lazy
+        adapt (which needs the previous plan's projected occupancy) never
+        stalls the host on a pop it has just queued.  The plan sequence is a
+        function of the trace and capacity only, so emitting earlier does
+        not change any plan."""
+        while len(self.pending) < self.EMIT_AHEAD and not self.exhausted:
+            prev = self._adapt_pending
+            if prev is not None:
+                ready = C.c_int32()
+                L.check(self.lib.bp_engine_plan_ready(self.eng, prev.slot, C.byref(ready)), "bp_engine_plan_ready")
+                if not ready.value:
+                    return
+            plan = self._next_plan()
+            if plan is None:
+                self.exhausted = True
+                return
+            self.pending.append(plan)
 
     def _plan_keys(self, plan, n: int) -> np.ndarray:
         view = L.PlanBuffers()
