@@ -163,6 +163,7 @@ _SIGS = {
     "bp_engine_chunk_keys": (c_i32, [c_vp, c_i32, c_vp, c_i64]),
     "bp_engine_chunk_view": (c_i32, [c_vp, c_i32, P(EvictBuffers)]),
     "bp_engine_sync": (c_i32, [c_vp]),
+    "bp_set_link_blocks": (c_i32, [c_i32]),
     "bp_engine_plan_ready": (c_i32, [c_vp, c_i32, c_vp]),
     "bp_engine_join": (c_i32, [c_vp, c_vp]),
     "bp_engine_stage_times": (c_i32, [c_vp, c_vp, c_vp]),

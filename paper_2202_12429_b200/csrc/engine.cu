@@ -131,7 +131,8 @@ struct bp_engine {
   int32_t* slots_s;
   int64_t* mark;
   int64_t* stats;  // [2]
-  int64_t* h_result;  // pinned, [16]
+  int64_t* h_result;  // pinned + mapped, [16]: counters [0..8), error record [8..)
+  int64_t* d_result;  // device alias of h_result
   int32_t* d_col_tables;  // table id per column of columnar batches
   std::vector<int32_t> h_col_tables;
   uint64_t* d_keys_staging[2];
@@ -269,7 +270,8 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   BP_CUDA_TRY(cudaMalloc(&e->mark, sc->total_rows * sizeof(int64_t)));
   BP_CUDA_TRY(cudaMemsetAsync(e->mark, 0xC0, sc->total_rows * sizeof(int64_t), e->compute));  // never a tag
   BP_CUDA_TRY(cudaMalloc(&e->stats, 2 * sizeof(int64_t)));
-  BP_CUDA_TRY(cudaMallocHost(&e->h_result, 16 * sizeof(int64_t)));
+  BP_CUDA_TRY(cudaHostAlloc(&e->h_result, 16 * sizeof(int64_t), cudaHostAllocMapped));
+  BP_CUDA_TRY(cudaHostGetDevicePointer((void**)&e->d_result, e->h_result, 0));
   BP_CUDA_TRY(cudaMalloc(&e->d_col_tables, sc->num_tables * sizeof(int32_t)));
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
   BP_CUDA_TRY(cudaStreamSynchronize(e->planq));
@@ -551,6 +553,25 @@ static int engine_apply(bp_engine* e, bp_prep* P, PlanSlot& ps, int64_t next_pos
   return BP_OK;
 }
 
+__global__ void k_step_counters(const uint64_t* num_unique, const uint64_t* n_ins, const uint64_t* stats,
+                                const uint64_t* chunk_count, const uint64_t* drain_count, const uint64_t* err,
+                                uint64_t* out) {
+  if (threadIdx.x == 0) {
+    out[0] = *num_unique;
+    out[1] = *n_ins;
+    out[2] = stats[0];
+    out[3] = stats[1];
+    out[4] = chunk_count[0];
+    out[5] = chunk_count[1];
+    out[6] = drain_count ? drain_count[0] : 0;
+    out[7] = drain_count ? drain_count[1] : 0;
+  }
+  constexpr int kErrWords = sizeof(bp_error_t) / sizeof(uint64_t);
+  static_assert(sizeof(bp_error_t) % sizeof(uint64_t) == 0 && kErrWords <= 8, "error record layout");
+  if (threadIdx.x < kErrWords) out[8 + threadIdx.x] = err[threadIdx.x];
+  __threadfence_system();
+}
+
 __global__ void k_count_critical(const uint32_t* __restrict__ ids, const long long* __restrict__ d_U,
                                  const int64_t* __restrict__ mark, long long tag, unsigned long long* stats) {
   const long long U = *d_U;
@@ -579,12 +600,7 @@ static int engine_finish(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_s
   stage_end(e, kStageEvict, s);
   if (rc) return rc;
   c.pending = true;
-  int64_t* h = e->h_result;
-  BP_CUDA_TRY(cudaMemcpyAsync(h + 0, P->d_num_unique, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  BP_CUDA_TRY(cudaMemcpyAsync(h + 1, ps.n_ins, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  BP_CUDA_TRY(cudaMemcpyAsync(h + 2, e->stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  BP_CUDA_TRY(cudaMemcpyAsync(h + 4, c.count, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  h[6] = h[7] = 0;
+  const uint64_t* d_drain_count = nullptr;
   if (drain_slot >= 0) {
     ChunkSlot& d = e->chunks[drain_slot];
     BP_CUDA_TRY(cudaStreamWaitEvent(s, d.flushed, 0));
@@ -592,10 +608,22 @@ static int engine_finish(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_s
     rc = bp_cache_evict(e->cache, P->iteration, 1, &db, e->cfg.capacity, s);
     if (rc) return rc;
     d.pending = true;
-    BP_CUDA_TRY(cudaMemcpyAsync(h + 6, d.count, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    d_drain_count = (const uint64_t*)d.count;
   }
+  // all step counters + the error record in ONE kernel writing mapped pinned
+  // memory, then one synchronisation (instead of 5 small D2H copies)
+  volatile int64_t* h = e->h_result;
+  k_step_counters<<<1, 32, 0, s>>>((const uint64_t*)P->d_num_unique, (const uint64_t*)ps.n_ins,
+                                   (const uint64_t*)e->stats, (const uint64_t*)c.count, d_drain_count,
+                                   (const uint64_t*)e->ctx->d_err, (uint64_t*)e->d_result);
+  BP_LAUNCH_CHECK();
+  BP_CUDA_TRY(cudaStreamSynchronize(s));
   bp_error_t err;
-  bp_ctx_check(e->ctx, s, &err);  // synchronises the compute stream
+  std::memcpy(&err, (const void*)(h + 8), sizeof(bp_error_t));
+  if (err.code != 0) {
+    BP_CUDA_TRY(cudaMemsetAsync(e->ctx->d_err, 0, sizeof(bp_error_t), s));
+    BP_CUDA_TRY(cudaStreamSynchronize(s));
+  }
   out->unique = h[0];
   out->inserted = h[1];
   out->critical = h[2];

@@ -228,6 +228,15 @@ __global__ void __launch_bounds__(kColThreads, 1) k_prep_table_sort(const uint64
 
 constexpr size_t kColSmem = sizeof(unsigned long long) * kColMax + sizeof(uint32_t) * (kColWarps * 256 + 256);
 
+struct RankBounds {
+  static constexpr int kMax = 64;
+  long long v[kMax];
+};
+
+__global__ void k_set_rank_bounds(RankBounds rb, int n, long long* out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = rb.v[i];
+}
+
 template <typename K>
 static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, const uint8_t* d_labels,
                       int row_bits, int table_bits, cudaStream_t s, const ColumnarInfo* col) {
@@ -344,10 +353,18 @@ static int prep_create_impl(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_
   P->long_cap = n / kLongSeg + 1;
   BP_CUDA_TRY(pool_alloc(&P->d_long, P->long_cap, s));
   BP_CUDA_TRY(pool_alloc(&P->d_num_long, 2, s));
-  BP_CUDA_TRY(cudaMemcpyAsync(P->d_rank_bounds, h_rank_bounds, sizeof(long long) * (num_ranks + 1),
-                              cudaMemcpyHostToDevice, s));
-  // The pageable H2D copy above is staged by the driver before returning, so
-  // the caller's rank-bounds array may be released immediately.
+  if (num_ranks + 1 <= RankBounds::kMax) {
+    // by value as a kernel parameter: a pageable H2D copy would first wait
+    // for the whole stream (host-blocking)
+    RankBounds rb;
+    for (int i = 0; i <= num_ranks; ++i) rb.v[i] = h_rank_bounds[i];
+    k_set_rank_bounds<<<1, 32, 0, s>>>(rb, num_ranks + 1, P->d_rank_bounds);
+  } else {
+    // The pageable H2D copy is staged by the driver before returning, so the
+    // caller's rank-bounds array may be released immediately.
+    BP_CUDA_TRY(cudaMemcpyAsync(P->d_rank_bounds, h_rank_bounds, sizeof(long long) * (num_ranks + 1),
+                                cudaMemcpyHostToDevice, s));
+  }
   if (n_occ == 0) {
     BP_CUDA_TRY(cudaMemsetAsync(P->d_num_long, 0, 2 * sizeof(long long), s));
     BP_CUDA_TRY(cudaMemsetAsync(P->d_num_unique, 0, sizeof(long long), s));

@@ -68,6 +68,12 @@ __global__ void k_init_values(uint64_t seed, int dim, const uint64_t* __restrict
 // flight (random 64 B rows are latency-bound on PCIe).
 constexpr int kIlp = 4;
 
+// Blocks of the host-link kernels.  Each block keeps 256 x kIlp 16-byte host
+// reads in flight; a few dozen blocks saturate PCIe, and fewer blocks leave
+// more SMs whose L1/LSU queues are not clogged by microsecond-latency host
+// accesses (co-resident compute kernels stall behind them).
+static int g_link_blocks = 32;
+
 __global__ void k_store_fetch_v4(const float4* __restrict__ table, const uint32_t* __restrict__ ids, long long n,
                                  const long long* d_n, int q, float4* __restrict__ out) {
   n = load_count(n, d_n);
@@ -197,7 +203,7 @@ extern "C" int bp_store_fetch(bp_store* st, const uint32_t* d_ids, int64_t n, co
   const int dim = st->dim;
   if ((dim & 3) == 0) {
     const int q = dim >> 2;
-    k_store_fetch_v4<<<grid_for(n * q, 256 * kIlp, kNumSMs), 256, 0, s>>>(
+    k_store_fetch_v4<<<grid_for(n * q, 256 * kIlp, g_link_blocks), 256, 0, s>>>(
         reinterpret_cast<const float4*>(st->d_table), d_ids, n, (const long long*)d_n, q,
         reinterpret_cast<float4*>(d_out));
   } else {
@@ -213,7 +219,7 @@ extern "C" int bp_store_write(bp_store* st, const uint32_t* d_ids, const float* 
   using namespace bp;
   if (n <= 0) return BP_OK;
   const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
-  k_store_write<<<grid_for(n * q, 256 * kIlp, kNumSMs), 256, 0, (cudaStream_t)stream>>>(
+  k_store_write<<<grid_for(n * q, 256 * kIlp, g_link_blocks), 256, 0, (cudaStream_t)stream>>>(
       st->d_table, st->d_written, d_ids, d_rows, nullptr, n, (const long long*)d_n, st->dim);
   BP_LAUNCH_CHECK();
   return BP_OK;
@@ -224,7 +230,7 @@ extern "C" int bp_store_write_masked(bp_store* st, const uint32_t* d_ids, const 
   using namespace bp;
   if (n <= 0) return BP_OK;
   const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
-  k_store_write<<<grid_for(n * q, 256 * kIlp, kNumSMs), 256, 0, (cudaStream_t)stream>>>(
+  k_store_write<<<grid_for(n * q, 256 * kIlp, g_link_blocks), 256, 0, (cudaStream_t)stream>>>(
       st->d_table, st->d_written, d_ids, d_rows, d_mask, n, (const long long*)d_n, st->dim);
   BP_LAUNCH_CHECK();
   return BP_OK;
@@ -236,5 +242,11 @@ extern "C" int bp_init_values(uint64_t seed, int32_t dim, const uint64_t* d_keys
   if (n <= 0) return BP_OK;
   k_init_values<<<grid_for(n * dim, 256), 256, 0, (cudaStream_t)stream>>>(seed, dim, d_keys, n, d_out);
   BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_set_link_blocks(int32_t blocks) {
+  if (blocks < 1 || blocks > 4096) return BP_ERR_INVALID;
+  bp::g_link_blocks = blocks;
   return BP_OK;
 }

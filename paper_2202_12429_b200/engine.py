@@ -326,6 +326,7 @@ class _Pipeline:
         plan = _Plan(self.batches[pos].iteration, self.lookahead, slot.value, pos)
         self._adapt_pending = plan
         if self.snapshots is not None:
+            self._plan_counts(plan)  # the pop ran on the plan stream: wait for it before dumping
             keys, _, flags = planner_dump(self.parts.planner, self.stream)
             self.snapshots[pos] = np.sort(keys[(flags & 2) != 0])
         return plan

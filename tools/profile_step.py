@@ -32,8 +32,13 @@ def main():
     ap.add_argument("--cprofile", action="store_true")
     ap.add_argument("--trace", default=None, help="write a chrome trace (kernel timeline per stream) here")
     ap.add_argument("--flush", action="store_true", help="256 MiB L2 flush before each step, like bench.py")
+    ap.add_argument("--link-blocks", type=int, default=0, help="grid of the host-link kernels (0: default)")
     ap.add_argument("--dlrm", action="store_true", help="DLRM mode (EmbeddingBag + MLP graph) instead of the stub")
     args = ap.parse_args()
+    if args.link_blocks:
+        from paper_2202_12429_b200 import _lib as L
+
+        L.check(L.lib().bp_set_link_blocks(args.link_blocks), "bp_set_link_blocks")
     sc = bench.schema()
     n = args.warmup + args.steps + 12
     batches = bench.make_batches(n, 1)
