@@ -376,6 +376,11 @@ int bp_engine_fetch(bp_engine* engine, int32_t slot);
 int bp_engine_flush(bp_engine* engine, const int32_t* h_chunk_slots, int32_t n);
 int bp_engine_train(bp_engine* engine, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
                     int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out);
+/* The same iteration split in two: _begin enqueues it (no host wait), _end
+ * waits for it and fills ``out``; the host can emit plans in between. */
+int bp_engine_train_begin(bp_engine* engine, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
+                          int32_t has_skip, int32_t chunk_slot, int32_t drain_slot);
+int bp_engine_train_end(bp_engine* engine, bp_step_result* out);
 /* DLRM mode iteration, split around the (PyTorch) dense model:
  * forward = apply plan + lookup + next-batch stamp + EmbeddingBag forward of
  * the batch's single-key bags into d_pooled[n_occ][model_dim] (async on the

@@ -139,6 +139,8 @@ struct bp_engine {
   uint8_t* d_labels_staging[2];
   cudaEvent_t staging_free[2];
   cudaEvent_t join_ev[2];  // bp_engine_join: planq, link
+  cudaEvent_t step_done;   // end of the last enqueued step (engine_finish_begin)
+  bool step_open = false;
   int staging_i;
   long long chunk_cap;
 };
@@ -261,6 +263,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     BP_CUDA_TRY(cudaMalloc(&e->d_labels_staging[i], n + 16));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->staging_free[i], cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->join_ev[i], cudaEventDisableTiming));
+    if (i == 0) BP_CUDA_TRY(cudaEventCreateWithFlags(&e->step_done, cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventRecord(e->staging_free[i], e->planq));
   }
   e->staging_i = 0;
@@ -316,6 +319,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
     cudaFree(e->d_labels_staging[i]);
     cudaEventDestroy(e->staging_free[i]);
     cudaEventDestroy(e->join_ev[i]);
+    if (i == 0) cudaEventDestroy(e->step_done);
   }
   cudaFree(e->slots_s);
   cudaFree(e->mark);
@@ -584,8 +588,7 @@ __global__ void k_count_critical(const uint32_t* __restrict__ ids, const long lo
 
 // Eviction of ttl <= iteration into chunk_slot (+ full drain into drain_slot
 // on the last iteration), counters to the host, one synchronisation.
-static int engine_finish(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_slot, int32_t drain_slot,
-                         bp_step_result* out) {
+static int engine_finish_begin(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_slot, int32_t drain_slot) {
   cudaStream_t s = e->compute;
   BP_CUDA_TRY(cudaEventRecord(ps.consumed, s));
   ChunkSlot& c = e->chunks[chunk_slot];
@@ -612,17 +615,26 @@ static int engine_finish(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_s
   }
   // all step counters + the error record in ONE kernel writing mapped pinned
   // memory, then one synchronisation (instead of 5 small D2H copies)
-  volatile int64_t* h = e->h_result;
   k_step_counters<<<1, 32, 0, s>>>((const uint64_t*)P->d_num_unique, (const uint64_t*)ps.n_ins,
                                    (const uint64_t*)e->stats, (const uint64_t*)c.count, d_drain_count,
                                    (const uint64_t*)e->ctx->d_err, (uint64_t*)e->d_result);
   BP_LAUNCH_CHECK();
-  BP_CUDA_TRY(cudaStreamSynchronize(s));
+  BP_CUDA_TRY(cudaEventRecord(e->step_done, s));
+  e->step_open = true;
+  return BP_OK;
+}
+
+// Waits for the step enqueued by engine_finish_begin and reads its counters.
+static int engine_finish_end(bp_engine* e, bp_step_result* out) {
+  if (!e->step_open) return BP_ERR_ENGINE;
+  e->step_open = false;
+  BP_CUDA_TRY(cudaEventSynchronize(e->step_done));
+  volatile int64_t* h = e->h_result;
   bp_error_t err;
   std::memcpy(&err, (const void*)(h + 8), sizeof(bp_error_t));
   if (err.code != 0) {
-    BP_CUDA_TRY(cudaMemsetAsync(e->ctx->d_err, 0, sizeof(bp_error_t), s));
-    BP_CUDA_TRY(cudaStreamSynchronize(s));
+    BP_CUDA_TRY(cudaMemsetAsync(e->ctx->d_err, 0, sizeof(bp_error_t), e->compute));
+    BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
   }
   out->unique = h[0];
   out->inserted = h[1];
@@ -636,15 +648,22 @@ static int engine_finish(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_s
   return BP_OK;
 }
 
+static int engine_finish(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_slot, int32_t drain_slot,
+                         bp_step_result* out) {
+  const int rc = engine_finish_begin(e, P, ps, chunk_slot, drain_slot);
+  return rc ? rc : engine_finish_end(e, out);
+}
+
 }  // namespace bp
 
 // One stub-mode training iteration on the compute stream (reference
 // engine.py:525-606): apply plan + lookup + next-batch stamp, fused trainer,
 // eviction; synchronises once and fills ``out`` (device contract violations
 // come back in out->err).
-extern "C" int bp_engine_train(bp_engine* e, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
-                               int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out) {
+extern "C" int bp_engine_train_begin(bp_engine* e, int64_t pos, int32_t plan_slot, int64_t next_pos,
+                                     uint64_t skip_key, int32_t has_skip, int32_t chunk_slot, int32_t drain_slot) {
   using namespace bp;
+  if (e->step_open) return BP_ERR_ENGINE;
   bp_prep* P = e->preps[engine_prep_slot(e, pos)];
   if (!P) return BP_ERR_ENGINE;
   PlanSlot& ps = e->plans[plan_slot];
@@ -659,7 +678,15 @@ extern "C" int bp_engine_train(bp_engine* e, int64_t pos, int32_t plan_slot, int
                     e->compute);
   stage_end(e, kStageTrainer, e->compute);
   if (rc) return rc;
-  return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
+  return engine_finish_begin(e, P, ps, chunk_slot, drain_slot);
+}
+
+extern "C" int bp_engine_train_end(bp_engine* e, bp_step_result* out) { return bp::engine_finish_end(e, out); }
+
+extern "C" int bp_engine_train(bp_engine* e, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
+                               int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out) {
+  const int rc = bp_engine_train_begin(e, pos, plan_slot, next_pos, skip_key, has_skip, chunk_slot, drain_slot);
+  return rc ? rc : bp_engine_train_end(e, out);
 }
 
 // DLRM mode, part 1: apply plan x and gather the batch's pooled embeddings

@@ -456,8 +456,11 @@ class _Pipeline:
         drain = self._take_chunk() if last else -1
         res = self.result
         if self.trainer is None:
-            L.check(lib.bp_engine_train(self.eng, pos, plan.slot, nxt, skip_key, has_skip, chunk, drain,
-                                        C.byref(res)), "bp_engine_train")
+            L.check(lib.bp_engine_train_begin(self.eng, pos, plan.slot, nxt, skip_key, has_skip, chunk, drain),
+                    "bp_engine_train_begin")
+            # plan emission (planner stream) overlaps this iteration's GPU work
+            self._emit_ahead()
+            L.check(lib.bp_engine_train_end(self.eng, C.byref(res)), "bp_engine_train_end")
         else:
             self.trainer.train(self, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
         if res.err.code:
