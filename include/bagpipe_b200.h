@@ -373,6 +373,9 @@ int bp_engine_plan_counts(bp_engine* engine, int32_t slot, int64_t* h_out4); /* 
 int bp_engine_plan_ready(bp_engine* engine, int32_t slot, int32_t* out);      /* non-blocking query */
 int bp_engine_plan_view(bp_engine* engine, int32_t slot, bp_plan_buffers* out, float** d_staging);
 int bp_engine_fetch(bp_engine* engine, int32_t slot);
+/* Host-link mode: 0 = zero-copy row kernels, 1 = copy engines + `threads`
+ * host threads gathering/scattering rows in pinned staging (0: auto). */
+int bp_engine_set_link_mode(bp_engine* engine, int32_t mode, int32_t threads);
 int bp_engine_flush(bp_engine* engine, const int32_t* h_chunk_slots, int32_t n);
 int bp_engine_train(bp_engine* engine, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
                     int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out);

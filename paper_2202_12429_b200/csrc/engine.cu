@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "hostpool.h"
 
 struct bp_store;
 struct bp_cache;
@@ -88,9 +89,56 @@ struct ChunkSlot {
   float* rows;
   uint8_t* dirty;
   int64_t* count;  // [2] device
+  long long h_count = -1;  // rows, known on the host after the step that filled it
   cudaEvent_t flushed;
   bool pending;
 };
+
+// DMA host-link mode (see hostpool.h): one pinned staging set per direction,
+// reused in link-stream order; host callbacks gather / scatter rows.
+struct LinkJob {
+  HostPool* pool;
+  const float* table_src;  // gather: host table
+  float* table_dst;        // scatter: host table
+  const uint32_t* ids;
+  const uint8_t* dirty;    // scatter only: rows with dirty == 0 are skipped
+  const float* rows_src;
+  float* rows_dst;
+  long long n;
+  size_t row_bytes;
+};
+
+static void CUDART_CB link_gather_cb(void* p) {
+  const LinkJob* j = static_cast<const LinkJob*>(p);
+  const size_t rb = j->row_bytes;
+  const char* table = reinterpret_cast<const char*>(j->table_src);
+  char* out = reinterpret_cast<char*>(j->rows_dst);
+  j->pool->parallel_for(j->n, [&](long long a, long long b) {
+    for (long long i = a; i < b; ++i) {
+      if (i + 8 < b) __builtin_prefetch(table + (size_t)j->ids[i + 8] * rb);
+      std::memcpy(out + (size_t)i * rb, table + (size_t)j->ids[i] * rb, rb);
+    }
+  });
+}
+
+static void CUDART_CB link_scatter_cb(void* p) {
+  const LinkJob* j = static_cast<const LinkJob*>(p);
+  const size_t rb = j->row_bytes;
+  char* table = reinterpret_cast<char*>(j->table_dst);
+  const char* in = reinterpret_cast<const char*>(j->rows_src);
+  j->pool->parallel_for(j->n, [&](long long a, long long b) {
+    for (long long i = a; i < b; ++i) {
+      if (i + 8 < b) __builtin_prefetch(table + (size_t)j->ids[i + 8] * rb, 1);
+      if (j->dirty[i]) std::memcpy(table + (size_t)j->ids[i] * rb, in + (size_t)i * rb, rb);
+    }
+  });
+}
+
+__global__ void k_mark_written(const uint32_t* __restrict__ ids, const uint8_t* __restrict__ dirty, long long n,
+                               uint32_t* __restrict__ written) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (dirty[i]) atomicOr(&written[ids[i] >> 5], 1u << (ids[i] & 31));
+}
 
 struct UploadSlot {
   uint8_t* host;  // pinned
@@ -141,6 +189,17 @@ struct bp_engine {
   cudaEvent_t join_ev[2];  // bp_engine_join: planq, link
   cudaEvent_t step_done;   // end of the last enqueued step (engine_finish_begin)
   bool step_open = false;
+  int open_chunk = -1, open_drain = -1;
+  // DMA host-link mode
+  int link_mode = 0;  // 0: zero-copy kernels, 1: copy engines + host pool
+  bp::HostPool* pool = nullptr;
+  uint32_t* h_fetch_ids = nullptr;
+  float* h_fetch_rows = nullptr;
+  uint32_t* h_flush_ids = nullptr;
+  uint8_t* h_flush_dirty = nullptr;
+  float* h_flush_rows = nullptr;
+  std::vector<bp::LinkJob> jobs;  // ring: callbacks read their job when they run
+  int next_job = 0;
   int staging_i;
   long long chunk_cap;
 };
@@ -285,6 +344,12 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
 extern "C" int bp_engine_destroy(bp_engine* e) {
   if (!e) return BP_OK;
   cudaDeviceSynchronize();
+  delete e->pool;
+  cudaFreeHost(e->h_fetch_ids);
+  cudaFreeHost(e->h_fetch_rows);
+  cudaFreeHost(e->h_flush_ids);
+  cudaFreeHost(e->h_flush_dirty);
+  cudaFreeHost(e->h_flush_rows);
   for (auto* p : e->preps)
     if (p) bp_prep_destroy(p);
   for (auto& p : e->plans) {
@@ -503,13 +568,62 @@ extern "C" int bp_engine_plan_view(bp_engine* e, int32_t slot, bp_plan_buffers* 
 // Prefetch of a plan on the link stream: zero-copy gather of its rows from
 // the pinned store, after the plan's pop and after every earlier write-back
 // issued on the same stream (the gate).
+// Host-link mode of the engine: 0 = zero-copy row kernels (SM-driven PCIe
+// gathers/scatters), 1 = copy engines + a pool of `threads` host threads
+// gathering/scattering rows in pinned staging (no SM time on the link).
+extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threads) {
+  if (mode != 0 && mode != 1) return BP_ERR_INVALID;
+  BP_CUDA_TRY(cudaStreamSynchronize(e->link));
+  e->link_mode = mode;
+  if (mode == 0) return BP_OK;
+  if (threads < 1) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    threads = (int)std::max(2u, std::min(16u, hw / 4));
+  }
+  if (!e->pool || e->pool->size() != threads) {
+    delete e->pool;
+    e->pool = new bp::HostPool(threads);
+  }
+  const size_t rb = (size_t)e->cfg.dim * sizeof(float);
+  if (!e->h_fetch_ids) {
+    BP_CUDA_TRY(cudaMallocHost(&e->h_fetch_ids, (size_t)e->cfg.max_occ * sizeof(uint32_t)));
+    BP_CUDA_TRY(cudaMallocHost(&e->h_fetch_rows, (size_t)e->cfg.max_occ * rb));
+    BP_CUDA_TRY(cudaMallocHost(&e->h_flush_ids, (size_t)e->chunk_cap * sizeof(uint32_t)));
+    BP_CUDA_TRY(cudaMallocHost(&e->h_flush_dirty, (size_t)e->chunk_cap));
+    BP_CUDA_TRY(cudaMallocHost(&e->h_flush_rows, (size_t)e->chunk_cap * rb));
+    e->jobs.resize(256);
+  }
+  return BP_OK;
+}
+
+static bp::LinkJob* next_job(bp_engine* e) {
+  bp::LinkJob* j = &e->jobs[e->next_job];
+  e->next_job = (e->next_job + 1) % (int)e->jobs.size();
+  return j;
+}
+
 extern "C" int bp_engine_fetch(bp_engine* e, int32_t slot) {
   bp::PlanSlot& ps = e->plans[slot];
   BP_CUDA_TRY(cudaStreamWaitEvent(e->link, ps.popped, 0));
   bp::stage_begin(e, bp::kStageFetch, e->link);
-  int rc = bp_store_fetch(e->store, ps.ids, e->cfg.max_occ, ps.counts, ps.staging, e->link);
+  if (e->link_mode == 1) {
+    // prefetch count on the host (the pop finished long before dispatch)
+    BP_CUDA_TRY(cudaEventSynchronize(ps.popped));
+    const long long n = ps.h_counts[0];
+    if (n > 0) {
+      const size_t rb = (size_t)e->cfg.dim * sizeof(float);
+      BP_CUDA_TRY(cudaMemcpyAsync(e->h_fetch_ids, ps.ids, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, e->link));
+      bp::LinkJob* j = next_job(e);
+      *j = bp::LinkJob{e->pool, bp_store_host_table(e->store), nullptr, e->h_fetch_ids, nullptr, nullptr,
+                       e->h_fetch_rows, n, rb};
+      BP_CUDA_TRY(cudaLaunchHostFunc(e->link, bp::link_gather_cb, j));
+      BP_CUDA_TRY(cudaMemcpyAsync(ps.staging, e->h_fetch_rows, n * rb, cudaMemcpyHostToDevice, e->link));
+    }
+  } else {
+    int rc = bp_store_fetch(e->store, ps.ids, e->cfg.max_occ, ps.counts, ps.staging, e->link);
+    if (rc) return rc;
+  }
   bp::stage_end(e, bp::kStageFetch, e->link);
-  if (rc) return rc;
   BP_CUDA_TRY(cudaEventRecord(ps.fetched, e->link));
   return BP_OK;
 }
@@ -519,8 +633,25 @@ extern "C" int bp_engine_flush(bp_engine* e, const int32_t* chunk_slots, int32_t
   bp::stage_begin(e, bp::kStageFlush, e->link);
   for (int i = 0; i < n; ++i) {
     bp::ChunkSlot& c = e->chunks[chunk_slots[i]];
-    int rc = bp_store_write_masked(e->store, c.ids, c.rows, c.dirty, e->cfg.capacity, c.count, e->link);
-    if (rc) return rc;
+    if (e->link_mode == 1 && c.h_count >= 0) {
+      const long long m = c.h_count;
+      if (m > 0) {
+        const size_t rb = (size_t)e->cfg.dim * sizeof(float);
+        BP_CUDA_TRY(cudaMemcpyAsync(e->h_flush_ids, c.ids, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, e->link));
+        BP_CUDA_TRY(cudaMemcpyAsync(e->h_flush_dirty, c.dirty, m, cudaMemcpyDeviceToHost, e->link));
+        BP_CUDA_TRY(cudaMemcpyAsync(e->h_flush_rows, c.rows, m * rb, cudaMemcpyDeviceToHost, e->link));
+        bp::k_mark_written<<<bp::grid_for(m, 256), 256, 0, e->link>>>(
+            c.ids, c.dirty, m, reinterpret_cast<uint32_t*>(bp_store_written_bitmap(e->store)));
+        BP_LAUNCH_CHECK();
+        bp::LinkJob* j = next_job(e);
+        *j = bp::LinkJob{e->pool, nullptr, bp_store_host_table(e->store), e->h_flush_ids, e->h_flush_dirty,
+                         e->h_flush_rows, nullptr, m, rb};
+        BP_CUDA_TRY(cudaLaunchHostFunc(e->link, bp::link_scatter_cb, j));
+      }
+    } else {
+      int rc = bp_store_write_masked(e->store, c.ids, c.rows, c.dirty, e->cfg.capacity, c.count, e->link);
+      if (rc) return rc;
+    }
     BP_CUDA_TRY(cudaEventRecord(c.flushed, e->link));
     c.pending = false;
   }
@@ -589,6 +720,8 @@ __global__ void k_count_critical(const uint32_t* __restrict__ ids, const long lo
 // Eviction of ttl <= iteration into chunk_slot (+ full drain into drain_slot
 // on the last iteration), counters to the host, one synchronisation.
 static int engine_finish_begin(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_slot, int32_t drain_slot) {
+  e->open_chunk = chunk_slot;
+  e->open_drain = drain_slot;
   cudaStream_t s = e->compute;
   BP_CUDA_TRY(cudaEventRecord(ps.consumed, s));
   ChunkSlot& c = e->chunks[chunk_slot];
@@ -645,6 +778,8 @@ static int engine_finish_end(bp_engine* e, bp_step_result* out) {
   out->drained = h[6];
   out->drained_dirty = h[7];
   out->err = err;
+  if (e->open_chunk >= 0) e->chunks[e->open_chunk].h_count = h[4];
+  if (e->open_drain >= 0) e->chunks[e->open_drain].h_count = h[6];
   return BP_OK;
 }
 

@@ -29,6 +29,7 @@ import ctypes as C
 import hashlib
 import json
 import math
+import os
 from bisect import bisect_right
 from collections import deque
 from dataclasses import asdict, dataclass, field
@@ -177,7 +178,7 @@ class _Pipeline:
     STAGES = ("prep", "planner", "fetch", "apply", "trainer", "evict", "flush")
 
     def __init__(self, cfg: EngineConfig, schema: Schema, batches: list, fingerprint, fault, device_inputs=None,
-                 timing: bool = False, trainer=None):
+                 timing: bool = False, trainer=None, link_mode: int | None = None):
         if fault not in (None, FAULT_NO_GATE, FAULT_DROP_PREFETCH):
             raise ConfigurationError(f"unknown fault {fault!r}")
         self.cfg, self.schema, self.batches = cfg, schema, batches
@@ -213,6 +214,12 @@ class _Pipeline:
         parts = L.EngineParts()
         self.lib.bp_engine_parts(h, C.byref(parts))
         self.parts = parts
+        # host link: 1 = copy engines + host worker pool (default), 0 = zero-copy kernels
+        if link_mode is None:
+            link_mode = int(os.environ.get("BAGPIPE_B200_LINK_MODE", "1"))
+        L.check(self.lib.bp_engine_set_link_mode(h, link_mode, int(os.environ.get("BAGPIPE_B200_LINK_THREADS", "0"))),
+                "bp_engine_set_link_mode")
+        self.link_mode = link_mode
         self.stream = torch.cuda.ExternalStream(parts.compute_stream)
         self.link = torch.cuda.ExternalStream(parts.link_stream)
         self.store = ShardedStore(self.row_schema, cfg.num_shards, cfg.seed, _handle=parts.store, _owner=self)

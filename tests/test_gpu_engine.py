@@ -33,8 +33,11 @@ def _assert_report(report, blob):
     assert report.to_csv_bytes().decode() == blob["csv"]
 
 
+@pytest.mark.parametrize("link_mode", [1, 0])
 @pytest.mark.parametrize("case", SMALL_CASES)
-def test_pipeline_report_byte_identical(small_schema, small_batches, case):
+def test_pipeline_report_byte_identical(small_schema, small_batches, case, link_mode, monkeypatch):
+    """Both host-link modes: copy engines + host pool (1), zero-copy kernels (0)."""
+    monkeypatch.setenv("BAGPIPE_B200_LINK_MODE", str(link_mode))
     blob = golden("reports_small.json")[case]
     report = _engine().run_pipeline(_cfg(blob["config"]), small_schema, small_batches)
     _assert_report(report, blob)
@@ -77,9 +80,11 @@ def test_dropped_prefetch_is_a_miss_at_the_reference_key(small_schema, small_bat
     assert err.value.key == unpack(want["key"])
 
 
-def test_ungated_run_reproduces_reference_staleness(small_schema, small_batches):
+@pytest.mark.parametrize("link_mode", [1, 0])
+def test_ungated_run_reproduces_reference_staleness(small_schema, small_batches, link_mode, monkeypatch):
     """fault=no_gate: the stale digest equals the reference's stale digest bit
     for bit, and differs from the baseline with a non-empty diff."""
+    monkeypatch.setenv("BAGPIPE_B200_LINK_MODE", str(link_mode))
     eng = _engine()
     blob = golden("reports_small.json")["fault_no_gate"]
     cfg = _cfg(blob["config"])
