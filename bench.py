@@ -159,7 +159,8 @@ def _timed_steps(pipe, first: int, steps: int, flush_buf, torch):
     for i in range(steps):
         with torch.cuda.stream(stream):
             flush_buf.zero_()
-        pipe.step(first + i)
+        # the last timed step must not enqueue step K+1 ahead of time
+        pipe.step(first + i, early=i < steps - 1)
     L.check(pipe.lib.bp_engine_join(pipe.eng, L.stream_ptr(stream)), "bp_engine_join")
     end.record(stream)
     torch.cuda.synchronize()

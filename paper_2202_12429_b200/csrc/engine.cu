@@ -179,7 +179,7 @@ struct bp_engine {
   int32_t* slots_s;
   int64_t* mark;
   int64_t* stats;  // [2]
-  int64_t* h_result;  // pinned + mapped, [16]: counters [0..8), error record [8..)
+  int64_t* h_result;  // pinned + mapped, [kStepRing][16]: counters [0..8), error record [8..)
   int64_t* d_result;  // device alias of h_result
   int32_t* d_col_tables;  // table id per column of columnar batches
   std::vector<int32_t> h_col_tables;
@@ -187,9 +187,12 @@ struct bp_engine {
   uint8_t* d_labels_staging[2];
   cudaEvent_t staging_free[2];
   cudaEvent_t join_ev[2];  // bp_engine_join: planq, link
-  cudaEvent_t step_done;   // end of the last enqueued step (engine_finish_begin)
-  bool step_open = false;
-  int open_chunk = -1, open_drain = -1;
+  // steps enqueued by engine_finish_begin and not yet ended: a FIFO ring, so
+  // the host can enqueue iteration x+1 before reading iteration x's counters
+  static constexpr int kStepRing = 2;
+  cudaEvent_t step_done[kStepRing];
+  int step_chunk[kStepRing], step_drain[kStepRing];
+  int step_head = 0, step_count = 0;
   // DMA host-link mode
   int link_mode = 0;  // 0: zero-copy kernels, 1: copy engines + host pool
   bp::HostPool* pool = nullptr;
@@ -322,7 +325,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     BP_CUDA_TRY(cudaMalloc(&e->d_labels_staging[i], n + 16));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->staging_free[i], cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->join_ev[i], cudaEventDisableTiming));
-    if (i == 0) BP_CUDA_TRY(cudaEventCreateWithFlags(&e->step_done, cudaEventDisableTiming));
+    BP_CUDA_TRY(cudaEventCreateWithFlags(&e->step_done[i], cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventRecord(e->staging_free[i], e->planq));
   }
   e->staging_i = 0;
@@ -332,7 +335,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   BP_CUDA_TRY(cudaMalloc(&e->mark, sc->total_rows * sizeof(int64_t)));
   BP_CUDA_TRY(cudaMemsetAsync(e->mark, 0xC0, sc->total_rows * sizeof(int64_t), e->compute));  // never a tag
   BP_CUDA_TRY(cudaMalloc(&e->stats, 2 * sizeof(int64_t)));
-  BP_CUDA_TRY(cudaHostAlloc(&e->h_result, 16 * sizeof(int64_t), cudaHostAllocMapped));
+  BP_CUDA_TRY(cudaHostAlloc(&e->h_result, bp_engine::kStepRing * 16 * sizeof(int64_t), cudaHostAllocMapped));
   BP_CUDA_TRY(cudaHostGetDevicePointer((void**)&e->d_result, e->h_result, 0));
   BP_CUDA_TRY(cudaMalloc(&e->d_col_tables, sc->num_tables * sizeof(int32_t)));
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
@@ -384,7 +387,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
     cudaFree(e->d_labels_staging[i]);
     cudaEventDestroy(e->staging_free[i]);
     cudaEventDestroy(e->join_ev[i]);
-    if (i == 0) cudaEventDestroy(e->step_done);
+    cudaEventDestroy(e->step_done[i]);
   }
   cudaFree(e->slots_s);
   cudaFree(e->mark);
@@ -720,8 +723,10 @@ __global__ void k_count_critical(const uint32_t* __restrict__ ids, const long lo
 // Eviction of ttl <= iteration into chunk_slot (+ full drain into drain_slot
 // on the last iteration), counters to the host, one synchronisation.
 static int engine_finish_begin(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_slot, int32_t drain_slot) {
-  e->open_chunk = chunk_slot;
-  e->open_drain = drain_slot;
+  if (e->step_count == bp_engine::kStepRing) return BP_ERR_ENGINE;
+  const int rs = (e->step_head + e->step_count) % bp_engine::kStepRing;
+  e->step_chunk[rs] = chunk_slot;
+  e->step_drain[rs] = drain_slot;
   cudaStream_t s = e->compute;
   BP_CUDA_TRY(cudaEventRecord(ps.consumed, s));
   ChunkSlot& c = e->chunks[chunk_slot];
@@ -750,19 +755,21 @@ static int engine_finish_begin(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t c
   // memory, then one synchronisation (instead of 5 small D2H copies)
   k_step_counters<<<1, 32, 0, s>>>((const uint64_t*)P->d_num_unique, (const uint64_t*)ps.n_ins,
                                    (const uint64_t*)e->stats, (const uint64_t*)c.count, d_drain_count,
-                                   (const uint64_t*)e->ctx->d_err, (uint64_t*)e->d_result);
+                                   (const uint64_t*)e->ctx->d_err, (uint64_t*)(e->d_result + 16 * rs));
   BP_LAUNCH_CHECK();
-  BP_CUDA_TRY(cudaEventRecord(e->step_done, s));
-  e->step_open = true;
+  BP_CUDA_TRY(cudaEventRecord(e->step_done[rs], s));
+  ++e->step_count;
   return BP_OK;
 }
 
 // Waits for the step enqueued by engine_finish_begin and reads its counters.
 static int engine_finish_end(bp_engine* e, bp_step_result* out) {
-  if (!e->step_open) return BP_ERR_ENGINE;
-  e->step_open = false;
-  BP_CUDA_TRY(cudaEventSynchronize(e->step_done));
-  volatile int64_t* h = e->h_result;
+  if (e->step_count == 0) return BP_ERR_ENGINE;
+  const int rs = e->step_head;
+  e->step_head = (e->step_head + 1) % bp_engine::kStepRing;
+  --e->step_count;
+  BP_CUDA_TRY(cudaEventSynchronize(e->step_done[rs]));
+  volatile int64_t* h = e->h_result + 16 * rs;
   bp_error_t err;
   std::memcpy(&err, (const void*)(h + 8), sizeof(bp_error_t));
   if (err.code != 0) {
@@ -778,8 +785,8 @@ static int engine_finish_end(bp_engine* e, bp_step_result* out) {
   out->drained = h[6];
   out->drained_dirty = h[7];
   out->err = err;
-  if (e->open_chunk >= 0) e->chunks[e->open_chunk].h_count = h[4];
-  if (e->open_drain >= 0) e->chunks[e->open_drain].h_count = h[6];
+  if (e->step_chunk[rs] >= 0) e->chunks[e->step_chunk[rs]].h_count = h[4];
+  if (e->step_drain[rs] >= 0) e->chunks[e->step_drain[rs]].h_count = h[6];
   return BP_OK;
 }
 
@@ -798,7 +805,7 @@ static int engine_finish(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t chunk_s
 extern "C" int bp_engine_train_begin(bp_engine* e, int64_t pos, int32_t plan_slot, int64_t next_pos,
                                      uint64_t skip_key, int32_t has_skip, int32_t chunk_slot, int32_t drain_slot) {
   using namespace bp;
-  if (e->step_open) return BP_ERR_ENGINE;
+  if (e->step_count == bp_engine::kStepRing) return BP_ERR_ENGINE;
   bp_prep* P = e->preps[engine_prep_slot(e, pos)];
   if (!P) return BP_ERR_ENGINE;
   PlanSlot& ps = e->plans[plan_slot];

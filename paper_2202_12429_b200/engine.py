@@ -214,9 +214,9 @@ class _Pipeline:
         parts = L.EngineParts()
         self.lib.bp_engine_parts(h, C.byref(parts))
         self.parts = parts
-        # host link: 1 = copy engines + host worker pool (default), 0 = zero-copy kernels
+        # host link: 0 = zero-copy kernels (default), 1 = copy engines + host worker pool
         if link_mode is None:
-            link_mode = int(os.environ.get("BAGPIPE_B200_LINK_MODE", "1"))
+            link_mode = int(os.environ.get("BAGPIPE_B200_LINK_MODE", "0"))
         L.check(self.lib.bp_engine_set_link_mode(h, link_mode, int(os.environ.get("BAGPIPE_B200_LINK_THREADS", "0"))),
                 "bp_engine_set_link_mode")
         self.link_mode = link_mode
@@ -254,6 +254,7 @@ class _Pipeline:
         self.peak_occupancy = 0
         self.drop_done = False
         self.result = L.StepResult()
+        self._inflight: dict = {}
 
     def stage_times(self) -> dict:
         """{stage: (total ms, launches)} since the last call (timing=True)."""
@@ -434,12 +435,28 @@ class _Pipeline:
     def begin(self) -> None:
         self._dispatch_until(-1)
 
-    def step(self, pos: int) -> None:
-        cfg, lib = self.cfg, self.lib
-        bw = cfg.sync_bandwidth
-        batch = self.batches[pos]
+    def step(self, pos: int, early: bool = True) -> None:
+        """One reference iteration.  In stub mode the next iteration is
+        enqueued on the GPU before this one's counters are read (when its plan
+        is already staged), so host bookkeeping overlaps device work; the
+        reference order of every host decision is unchanged."""
         if pos > 0:
             self._dispatch_until(pos - 1)
+        if pos not in self._inflight:
+            self._begin(pos)
+        nxt = pos + 1
+        if (early and self.trainer is None and self.fault is None and self.events is None and self.snapshots is None
+                and nxt < self.n and nxt in self.staged and nxt not in self._inflight
+                and len(self.free_chunks) >= (2 if nxt == self.n - 1 else 1)):
+            self._begin(nxt)
+        if self.trainer is None:
+            # plan emission (planner stream) overlaps the queued GPU work
+            self._emit_ahead()
+        self._end(pos)
+
+    def _begin(self, pos: int) -> None:
+        lib = self.lib
+        batch = self.batches[pos]
         iteration = batch.iteration
         staged = self.staged.pop(pos, None)
         if staged is None:
@@ -461,12 +478,18 @@ class _Pipeline:
             self._add(nxt)
         chunk = self._take_chunk()
         drain = self._take_chunk() if last else -1
-        res = self.result
+        self._inflight[pos] = (plan, arrival, skip_key, has_skip, nxt, chunk, drain)
         if self.trainer is None:
             L.check(lib.bp_engine_train_begin(self.eng, pos, plan.slot, nxt, skip_key, has_skip, chunk, drain),
                     "bp_engine_train_begin")
-            # plan emission (planner stream) overlaps this iteration's GPU work
-            self._emit_ahead()
+
+    def _end(self, pos: int) -> None:
+        cfg, lib = self.cfg, self.lib
+        bw = cfg.sync_bandwidth
+        iteration = self.batches[pos].iteration
+        plan, arrival, skip_key, has_skip, nxt, chunk, drain = self._inflight.pop(pos)
+        res = self.result
+        if self.trainer is None:
             L.check(lib.bp_engine_train_end(self.eng, C.byref(res)), "bp_engine_train_end")
         else:
             self.trainer.train(self, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
