@@ -441,8 +441,12 @@ int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const float* d_em
                               bp_stream_t stream);
 
 /* ------------------------------------------------------------ utilities */
-/* Grid size of the host-link (zero-copy fetch / write-back) kernels; default 32. */
+/* Launch shape of the host-link (zero-copy fetch / write-back) kernels:
+ * blocks (default 16), threads per block (1024) and unused dynamic shared
+ * memory per block (200 KB: one link block owns its SM, so compute kernels
+ * never share an SM with PCIe traffic). */
 int bp_set_link_blocks(int32_t blocks);
+int bp_set_link_config(int32_t blocks, int32_t threads, int32_t smem_bytes);
 /* Sort packed keys ascending with a u32 payload (stable); n host-known. */
 int bp_sort_keys_u64(uint64_t* d_keys, uint32_t* d_vals, int64_t n, int32_t key_bits, bp_stream_t stream);
 /* Order-independent digest helpers for parity tests. */

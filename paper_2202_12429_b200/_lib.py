@@ -167,6 +167,7 @@ _SIGS = {
     "bp_engine_train_begin": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_u64, c_i32, c_i32, c_i32]),
     "bp_engine_train_end": (c_i32, [c_vp, P(StepResult)]),
     "bp_set_link_blocks": (c_i32, [c_i32]),
+    "bp_set_link_config": (c_i32, [c_i32, c_i32, c_i32]),
     "bp_engine_plan_ready": (c_i32, [c_vp, c_i32, c_vp]),
     "bp_engine_join": (c_i32, [c_vp, c_vp]),
     "bp_engine_stage_times": (c_i32, [c_vp, c_vp, c_vp]),

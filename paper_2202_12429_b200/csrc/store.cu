@@ -72,7 +72,13 @@ constexpr int kIlp = 4;
 // reads in flight; a few dozen blocks saturate PCIe, and fewer blocks leave
 // more SMs whose L1/LSU queues are not clogged by microsecond-latency host
 // accesses (co-resident compute kernels stall behind them).
-static int g_link_blocks = 32;
+static int g_link_blocks = 16;
+// Threads per link block and dynamic shared memory requested (unused) so a
+// link block occupies its SM alone: compute kernels' CTAs then never share an
+// SM with the PCIe traffic (they run on the other SMs at full speed).
+static int g_link_threads = 1024;
+static int g_link_smem = 200 << 10;
+
 
 __global__ void k_store_fetch_v4(const float4* __restrict__ table, const uint32_t* __restrict__ ids, long long n,
                                  const long long* d_n, int q, float4* __restrict__ out) {
@@ -145,6 +151,16 @@ __global__ void k_store_write(float* __restrict__ table, uint32_t* __restrict__ 
   }
 }
 
+static cudaError_t link_attrs() {
+  static int done_smem = -1;
+  if (done_smem == g_link_smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_store_fetch_v4, cudaFuncAttributeMaxDynamicSharedMemorySize, g_link_smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_store_write, cudaFuncAttributeMaxDynamicSharedMemorySize, g_link_smem);
+  if (e == cudaSuccess) done_smem = g_link_smem;
+  return e;
+}
+
 }  // namespace bp
 
 extern "C" int bp_store_create_ex(bp_ctx* ctx, const bp_schema* sc, uint64_t seed, int32_t init_dims,
@@ -203,7 +219,8 @@ extern "C" int bp_store_fetch(bp_store* st, const uint32_t* d_ids, int64_t n, co
   const int dim = st->dim;
   if ((dim & 3) == 0) {
     const int q = dim >> 2;
-    k_store_fetch_v4<<<grid_for(n * q, 256 * kIlp, g_link_blocks), 256, 0, s>>>(
+    BP_CUDA_TRY(link_attrs());
+    k_store_fetch_v4<<<grid_for(n * q, g_link_threads * kIlp, g_link_blocks), g_link_threads, g_link_smem, s>>>(
         reinterpret_cast<const float4*>(st->d_table), d_ids, n, (const long long*)d_n, q,
         reinterpret_cast<float4*>(d_out));
   } else {
@@ -219,7 +236,9 @@ extern "C" int bp_store_write(bp_store* st, const uint32_t* d_ids, const float* 
   using namespace bp;
   if (n <= 0) return BP_OK;
   const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
-  k_store_write<<<grid_for(n * q, 256 * kIlp, g_link_blocks), 256, 0, (cudaStream_t)stream>>>(
+  BP_CUDA_TRY(link_attrs());
+  k_store_write<<<grid_for(n * q, g_link_threads * kIlp, g_link_blocks), g_link_threads, g_link_smem,
+                  (cudaStream_t)stream>>>(
       st->d_table, st->d_written, d_ids, d_rows, nullptr, n, (const long long*)d_n, st->dim);
   BP_LAUNCH_CHECK();
   return BP_OK;
@@ -230,7 +249,9 @@ extern "C" int bp_store_write_masked(bp_store* st, const uint32_t* d_ids, const 
   using namespace bp;
   if (n <= 0) return BP_OK;
   const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
-  k_store_write<<<grid_for(n * q, 256 * kIlp, g_link_blocks), 256, 0, (cudaStream_t)stream>>>(
+  BP_CUDA_TRY(link_attrs());
+  k_store_write<<<grid_for(n * q, g_link_threads * kIlp, g_link_blocks), g_link_threads, g_link_smem,
+                  (cudaStream_t)stream>>>(
       st->d_table, st->d_written, d_ids, d_rows, d_mask, n, (const long long*)d_n, st->dim);
   BP_LAUNCH_CHECK();
   return BP_OK;
@@ -248,5 +269,15 @@ extern "C" int bp_init_values(uint64_t seed, int32_t dim, const uint64_t* d_keys
 extern "C" int bp_set_link_blocks(int32_t blocks) {
   if (blocks < 1 || blocks > 4096) return BP_ERR_INVALID;
   bp::g_link_blocks = blocks;
+  return BP_OK;
+}
+
+extern "C" int bp_set_link_config(int32_t blocks, int32_t threads, int32_t smem_bytes) {
+  if (blocks < 1 || blocks > 4096 || threads < 32 || threads > 1024 || (threads & 31) || smem_bytes < 0 ||
+      smem_bytes > (227 << 10))
+    return BP_ERR_INVALID;
+  bp::g_link_blocks = blocks;
+  bp::g_link_threads = threads;
+  bp::g_link_smem = smem_bytes;
   return BP_OK;
 }

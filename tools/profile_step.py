@@ -33,8 +33,13 @@ def main():
     ap.add_argument("--trace", default=None, help="write a chrome trace (kernel timeline per stream) here")
     ap.add_argument("--flush", action="store_true", help="256 MiB L2 flush before each step, like bench.py")
     ap.add_argument("--link-blocks", type=int, default=0, help="grid of the host-link kernels (0: default)")
+    ap.add_argument("--link-config", default="", help="blocks,threads,smem of the host-link kernels")
     ap.add_argument("--dlrm", action="store_true", help="DLRM mode (EmbeddingBag + MLP graph) instead of the stub")
     args = ap.parse_args()
+    if args.link_config:
+        from paper_2202_12429_b200 import _lib as L
+
+        L.check(L.lib().bp_set_link_config(*[int(x) for x in args.link_config.split(",")]), "bp_set_link_config")
     if args.link_blocks:
         from paper_2202_12429_b200 import _lib as L
 
