@@ -442,9 +442,8 @@ int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const float* d_em
 
 /* ------------------------------------------------------------ utilities */
 /* Launch shape of the host-link (zero-copy fetch / write-back) kernels:
- * blocks (default 16), threads per block (1024) and unused dynamic shared
- * memory per block (200 KB: one link block owns its SM, so compute kernels
- * never share an SM with PCIe traffic). */
+ * blocks (default 32), threads per block (256) and unused dynamic shared
+ * memory per block (default 0; ~200 KB makes a link block own its SM). */
 int bp_set_link_blocks(int32_t blocks);
 int bp_set_link_config(int32_t blocks, int32_t threads, int32_t smem_bytes);
 /* Sort packed keys ascending with a u32 payload (stable); n host-known. */

@@ -112,4 +112,9 @@ struct bp_prep {
   long long long_cap;
   long long h_num_unique;  // -1 until read back
   cudaStream_t stream;
+  // one stream-ordered allocation holds every buffer above and the build
+  // temporaries below (one cudaMallocAsync / cudaFreeAsync per batch)
+  void* d_arena;
+  void *t_ka, *t_kb;
+  uint32_t *t_va, *t_vb, *t_hist, *t_head, *t_segx, *t_first_flag, *t_first_rank, *t_partials;
 };

@@ -241,18 +241,10 @@ template <typename K>
 static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, const uint8_t* d_labels,
                       int row_bits, int table_bits, cudaStream_t s, const ColumnarInfo* col) {
   const long long n = P->n_occ;
-  K *ka, *kb;
-  uint32_t *va, *vb, *hist, *head, *segx, *first_flag, *first_rank, *partials;
-  BP_CUDA_TRY(pool_alloc(&ka, n, s));
-  BP_CUDA_TRY(pool_alloc(&kb, n, s));
-  BP_CUDA_TRY(pool_alloc(&va, n, s));
-  BP_CUDA_TRY(pool_alloc(&vb, n, s));
-  BP_CUDA_TRY(pool_alloc(&hist, sort_hist_words(n), s));
-  BP_CUDA_TRY(pool_alloc(&head, n, s));
-  BP_CUDA_TRY(pool_alloc(&segx, n, s));
-  BP_CUDA_TRY(pool_alloc(&first_flag, n, s));
-  BP_CUDA_TRY(pool_alloc(&first_rank, n, s));
-  BP_CUDA_TRY(pool_alloc(&partials, (long long)sort_partials_words(n) + scan_state_words(n), s));
+  K* ka = static_cast<K*>(P->t_ka);
+  K* kb = static_cast<K*>(P->t_kb);
+  uint32_t *va = P->t_va, *vb = P->t_vb, *hist = P->t_hist, *head = P->t_head, *segx = P->t_segx;
+  uint32_t *first_flag = P->t_first_flag, *first_rank = P->t_first_rank, *partials = P->t_partials;
   const int g = grid_for(n, 256);
   int which = 0;
   if (col) {
@@ -300,17 +292,51 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
     k_prep_occ_k<<<g, 256, 0, s>>>(P->d_occ_pos, head, segx, n, P->d_perm_s2k, P->d_occ_k, P->d_occ_s,
                                    P->d_seg_of);
   BP_LAUNCH_CHECK();
-  cudaFreeAsync(ka, s);
-  cudaFreeAsync(kb, s);
-  cudaFreeAsync(va, s);
-  cudaFreeAsync(vb, s);
-  cudaFreeAsync(hist, s);
-  cudaFreeAsync(head, s);
-  cudaFreeAsync(segx, s);
-  cudaFreeAsync(first_flag, s);
-  cudaFreeAsync(first_rank, s);
-  cudaFreeAsync(partials, s);
   return BP_OK;
+}
+
+// Byte layout of a prep's arena (base == nullptr: size only).
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+static size_t prep_layout(bp_prep* P, char* base, long long n, int num_ranks, int flags) {
+  Carve c{base};
+  P->d_num_unique = c.take<long long>(1);
+  P->d_uniq_key_s = c.take<uint64_t>(n);
+  P->d_uniq_id_s = c.take<uint32_t>(n);
+  P->d_uniq_key_k = c.take<uint64_t>(n);
+  P->d_perm_s2k = c.take<uint32_t>(n);
+  P->d_perm_k2s = c.take<uint32_t>(n);
+  P->d_seg_start = c.take<uint32_t>(n + 1);
+  P->d_occ_pos = c.take<uint32_t>(n);
+  P->d_occ_label = c.take<uint8_t>(n + 16);  // read as 16-byte chunks
+  P->d_occ_k = (flags & BP_PREP_OCC_INDEX) ? c.take<uint32_t>(n) : nullptr;
+  P->d_occ_s = (flags & BP_PREP_OCC_SORTED) ? c.take<uint32_t>(n) : nullptr;
+  P->d_seg_of = (flags & BP_PREP_OCC_SORTED) ? c.take<uint32_t>(n) : nullptr;
+  P->d_rank_bounds = c.take<long long>(num_ranks + 1);
+  P->long_cap = n / kLongSeg + 1;
+  P->d_long = c.take<uint32_t>(P->long_cap);
+  P->d_num_long = c.take<long long>(2);
+  P->t_ka = c.take<uint64_t>(n);
+  P->t_kb = c.take<uint64_t>(n);
+  P->t_va = c.take<uint32_t>(n);
+  P->t_vb = c.take<uint32_t>(n);
+  P->t_hist = c.take<uint32_t>(sort_hist_words(n));
+  P->t_head = c.take<uint32_t>(n);
+  P->t_segx = c.take<uint32_t>(n);
+  P->t_first_flag = c.take<uint32_t>(n);
+  P->t_first_rank = c.take<uint32_t>(n);
+  P->t_partials = c.take<uint32_t>((long long)sort_partials_words(n) + scan_state_words(n));
+  return c.off;
 }
 
 }  // namespace bp
@@ -332,27 +358,11 @@ static int prep_create_impl(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_
   P->stream = s;
   P->h_num_unique = n_occ == 0 ? 0 : -1;
   const long long n = n_occ > 0 ? n_occ : 1;
-  BP_CUDA_TRY(pool_alloc(&P->d_num_unique, 1, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_uniq_key_s, n, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_uniq_id_s, n, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_uniq_key_k, n, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_perm_s2k, n, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_perm_k2s, n, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_seg_start, n + 1, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_occ_pos, n, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_occ_label, n + 16, s));  // read as 16-byte chunks
-  P->d_occ_k = nullptr;
-  P->d_occ_s = nullptr;
-  P->d_seg_of = nullptr;
-  if (flags & BP_PREP_OCC_INDEX) BP_CUDA_TRY(pool_alloc(&P->d_occ_k, n, s));
-  if (flags & BP_PREP_OCC_SORTED) {
-    BP_CUDA_TRY(pool_alloc(&P->d_occ_s, n, s));
-    BP_CUDA_TRY(pool_alloc(&P->d_seg_of, n, s));
-  }
-  BP_CUDA_TRY(pool_alloc(&P->d_rank_bounds, num_ranks + 1, s));
-  P->long_cap = n / kLongSeg + 1;
-  BP_CUDA_TRY(pool_alloc(&P->d_long, P->long_cap, s));
-  BP_CUDA_TRY(pool_alloc(&P->d_num_long, 2, s));
+  const size_t bytes = prep_layout(P, nullptr, n, num_ranks, flags);
+  void* arena = nullptr;
+  BP_CUDA_TRY(cudaMallocAsync(&arena, bytes, s));
+  P->d_arena = arena;
+  prep_layout(P, static_cast<char*>(arena), n, num_ranks, flags);
   if (num_ranks + 1 <= RankBounds::kMax) {
     // by value as a kernel parameter: a pageable H2D copy would first wait
     // for the whole stream (host-blocking)
@@ -419,22 +429,7 @@ extern "C" int bp_prep_create_columnar(bp_ctx* ctx, const bp_schema* sc, const u
 
 extern "C" int bp_prep_destroy(bp_prep* P) {
   if (!P) return BP_OK;
-  cudaStream_t s = P->stream;
-  cudaFreeAsync(P->d_num_unique, s);
-  cudaFreeAsync(P->d_uniq_key_s, s);
-  cudaFreeAsync(P->d_uniq_id_s, s);
-  cudaFreeAsync(P->d_uniq_key_k, s);
-  cudaFreeAsync(P->d_perm_s2k, s);
-  cudaFreeAsync(P->d_perm_k2s, s);
-  cudaFreeAsync(P->d_seg_start, s);
-  cudaFreeAsync(P->d_occ_pos, s);
-  cudaFreeAsync(P->d_occ_label, s);
-  if (P->d_occ_k) cudaFreeAsync(P->d_occ_k, s);
-  if (P->d_occ_s) cudaFreeAsync(P->d_occ_s, s);
-  if (P->d_seg_of) cudaFreeAsync(P->d_seg_of, s);
-  cudaFreeAsync(P->d_rank_bounds, s);
-  cudaFreeAsync(P->d_long, s);
-  cudaFreeAsync(P->d_num_long, s);
+  cudaFreeAsync(P->d_arena, P->stream);
   delete P;
   return BP_OK;
 }

@@ -72,12 +72,12 @@ constexpr int kIlp = 4;
 // reads in flight; a few dozen blocks saturate PCIe, and fewer blocks leave
 // more SMs whose L1/LSU queues are not clogged by microsecond-latency host
 // accesses (co-resident compute kernels stall behind them).
-static int g_link_blocks = 16;
-// Threads per link block and dynamic shared memory requested (unused) so a
-// link block occupies its SM alone: compute kernels' CTAs then never share an
-// SM with the PCIe traffic (they run on the other SMs at full speed).
-static int g_link_threads = 1024;
-static int g_link_smem = 200 << 10;
+static int g_link_blocks = 32;
+// Threads per link block and dynamic shared memory requested (unused; > 0
+// makes a link block own its SM so no compute CTA shares it with the PCIe
+// traffic -- measured no better on the bench step, so off by default).
+static int g_link_threads = 256;
+static int g_link_smem = 0;
 
 
 __global__ void k_store_fetch_v4(const float4* __restrict__ table, const uint32_t* __restrict__ ids, long long n,

@@ -44,7 +44,7 @@ def main():
     from paper_2202_12429_b200 import _lib as L
 
     for blocks in (8, 16, 32, 64, 148):
-        L.check(L.lib().bp_set_link_config(blocks, 1024, 200 << 10), "bp_set_link_config")
+        L.check(L.lib().bp_set_link_config(blocks, 256, 0), "bp_set_link_config")
         ids = np.sort(rng.integers(0, sc.total_rows, 35_000)).astype(np.uint32)
         d_ids = torch.from_numpy(ids).cuda()
         rows = torch.empty((35_000, sc.emb_dim), dtype=torch.float32, device="cuda")
@@ -52,7 +52,7 @@ def main():
             lambda: store.fetch_ids_async(d_ids, 35_000)) / 1e9
         out[f"scatter_random_35000_blocks{blocks}_gbs"] = 35_000 * 64 / timed(
             lambda: store.write_ids_async(d_ids, rows, 35_000)) / 1e9
-    L.check(L.lib().bp_set_link_config(16, 1024, 200 << 10), "bp_set_link_config")
+    L.check(L.lib().bp_set_link_config(32, 256, 0), "bp_set_link_config")
     for n in (35_000, 1_000_000):
         for kind in ("random", "sequential"):
             ids = rng.integers(0, sc.total_rows, n) if kind == "random" else np.arange(n)

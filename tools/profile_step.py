@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--cprofile", action="store_true")
     ap.add_argument("--trace", default=None, help="write a chrome trace (kernel timeline per stream) here")
     ap.add_argument("--flush", action="store_true", help="256 MiB L2 flush before each step, like bench.py")
+    ap.add_argument("--sync-flush", action="store_true", help="drain all engine streams before each flush")
     ap.add_argument("--link-blocks", type=int, default=0, help="grid of the host-link kernels (0: default)")
     ap.add_argument("--link-config", default="", help="blocks,threads,smem of the host-link kernels")
     ap.add_argument("--dlrm", action="store_true", help="DLRM mode (EmbeddingBag + MLP graph) instead of the stub")
@@ -71,6 +72,8 @@ def main():
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
 
     def one(i):
+        if flush_buf is not None and args.sync_flush:
+            pipe.lib.bp_engine_sync(pipe.eng)
         if flush_buf is not None:
             with torch.cuda.stream(pipe.stream):
                 flush_buf.zero_()
