@@ -376,6 +376,9 @@ int bp_engine_fetch(bp_engine* engine, int32_t slot);
 /* Host-link mode: 0 = zero-copy row kernels, 1 = copy engines + `threads`
  * host threads gathering/scattering rows in pinned staging (0: auto). */
 int bp_engine_set_link_mode(bp_engine* engine, int32_t mode, int32_t threads);
+/* Host worker-pool row gather (op 0) / scatter (op 1) rate probe (tools). */
+int bp_host_rows_bench(float* table, int32_t dim, const uint32_t* ids, int64_t n, int32_t threads, int32_t op,
+                       double* seconds);
 int bp_engine_flush(bp_engine* engine, const int32_t* h_chunk_slots, int32_t n);
 int bp_engine_train(bp_engine* engine, int64_t pos, int32_t plan_slot, int64_t next_pos, uint64_t skip_key,
                     int32_t has_skip, int32_t chunk_slot, int32_t drain_slot, bp_step_result* out);

@@ -163,6 +163,7 @@ _SIGS = {
     "bp_engine_chunk_keys": (c_i32, [c_vp, c_i32, c_vp, c_i64]),
     "bp_engine_chunk_view": (c_i32, [c_vp, c_i32, P(EvictBuffers)]),
     "bp_engine_sync": (c_i32, [c_vp]),
+    "bp_host_rows_bench": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp]),
     "bp_engine_set_link_mode": (c_i32, [c_vp, c_i32, c_i32]),
     "bp_engine_train_begin": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_u64, c_i32, c_i32, c_i32]),
     "bp_engine_train_end": (c_i32, [c_vp, P(StepResult)]),

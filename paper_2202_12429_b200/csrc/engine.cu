@@ -26,6 +26,8 @@
 #include "internal.cuh"
 #include "hostpool.h"
 
+#include <chrono>
+
 struct bp_store;
 struct bp_cache;
 struct bp_planner;
@@ -909,5 +911,25 @@ extern "C" int bp_engine_sync(bp_engine* e) {
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
   BP_CUDA_TRY(cudaStreamSynchronize(e->planq));
   BP_CUDA_TRY(cudaStreamSynchronize(e->link));
+  return BP_OK;
+}
+
+// Host-side row gather (op 0) / scatter (op 1) rate of the DMA link mode's
+// worker pool, for tools/hostlink_peak.py: n random rows of `dim` floats
+// between `table` and a scratch buffer; wall seconds in *seconds.
+extern "C" int bp_host_rows_bench(float* table, int32_t dim, const uint32_t* ids, int64_t n, int32_t threads, int32_t op,
+                                  double* seconds) {
+  if (n <= 0 || dim <= 0 || threads < 1) return BP_ERR_INVALID;
+  std::vector<float> scratch((size_t)n * dim);
+  std::vector<uint8_t> dirty((size_t)n, 1);
+  bp::HostPool pool(threads);
+  bp::LinkJob j{&pool, table, table, ids, dirty.data(), scratch.data(), scratch.data(), n, (size_t)dim * sizeof(float)};
+  if (op == 1) {  // scatter the rows' current values back (content unchanged)
+    bp::link_gather_cb(&j);
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  if (op == 0) bp::link_gather_cb(&j);
+  else bp::link_scatter_cb(&j);
+  *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return BP_OK;
 }

@@ -53,6 +53,18 @@ def main():
         out[f"scatter_random_35000_blocks{blocks}_gbs"] = 35_000 * 64 / timed(
             lambda: store.write_ids_async(d_ids, rows, 35_000)) / 1e9
     L.check(L.lib().bp_set_link_config(32, 256, 0), "bp_set_link_config")
+    # host worker pool gather/scatter of random rows of the pinned table (DMA link mode)
+    import ctypes as C
+
+    table = L.lib().bp_store_host_table(store.handle)
+    if table:
+        ids = np.sort(rng.integers(0, sc.total_rows, 35_000)).astype(np.uint32)
+        for threads in (1, 2, 4, 8, 12):
+            for op, name in ((0, "gather"), (1, "scatter")):
+                sec = C.c_double()
+                L.check(L.lib().bp_host_rows_bench(table, sc.emb_dim, ids.ctypes.data, 35_000, threads, op,
+                                                   C.byref(sec)), "bp_host_rows_bench")
+                out[f"host_{name}_35000_threads{threads}_us"] = sec.value * 1e6
     for n in (35_000, 1_000_000):
         for kind in ("random", "sequential"):
             ids = rng.integers(0, sc.total_rows, n) if kind == "random" else np.arange(n)
