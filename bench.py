@@ -245,8 +245,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
 
     # ---- DLRM mode (N=1): the same engine feeding PyTorch MLPs (bf16 autocast)
     dlrm = None
-    if world == 1 and not args.no_dlrm:
-        dlrm = run_dlrm_mode(args, sc, full, cfg, flush_buf, torch)
+    if not args.no_dlrm:
+        dlrm = run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank, world, len(tables))
 
     t = torch.tensor([ms, e2e_ms], device="cuda", dtype=torch.float64)
     if world > 1:
@@ -314,13 +314,20 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     return out
 
 
-def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch) -> dict:
+def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, local_tables=26) -> dict:
+    """DLRM mode; N > 1 = hybrid parallel (hybrid.py): this rank's table shard
+    through the engine over the global batch, all-to-all of pooled rows and
+    their gradients, data-parallel MLPs with a mean all-reduce."""
+    import torch.distributed as dist
+
     from paper_2202_12429_b200.dlrm import DLRMConfig, DLRMTrainer
     from paper_2202_12429_b200.engine import _Pipeline
+    from paper_2202_12429_b200.hybrid import EmbeddingExchange
 
     steps, warm = args.steps, args.warmup
     dcfg = DLRMConfig(emb_optimizer="sgd", emb_lr=0.01, mlp_lr=0.01, mlp_dtype="bf16")
-    trainer = DLRMTrainer(dcfg, sc.num_dense, sc.num_tables, DIM)
+    ex = EmbeddingExchange(sc.num_tables, DIM, rank, world) if world > 1 else None
+    trainer = DLRMTrainer(dcfg, sc.num_dense, sc.num_tables, DIM, exchange=ex)
     dev_inputs = {}
     for i, b in enumerate(batches):
         keys, labels, _ = b.packed_occurrences()
@@ -332,12 +339,18 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch) -> dict:
     for pos in range(warm):
         pipe.step(pos)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     pipe.stage_times()
     ms, _ = _timed_steps(pipe, warm, steps, flush_buf, torch)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
     stages = pipe.stage_times()
     records = pipe.records[warm:warm + steps]
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
-    n_occ = BATCH * sc.num_tables
+    n_occ = BATCH * local_tables
     # "trainer" spans: EmbeddingBag forward and backward alternate (2 per step)
     spans = stages["trainer"]
     # forward N_occ*(64 row read + 64 pooled write + 4 index)
@@ -345,6 +358,8 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch) -> dict:
     losses = trainer.loss_history()
     del pipe
     return {"summary": {"value": BATCH * steps / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms / steps,
+                        "parallelism": "single" if world == 1 else
+                        f"hybrid: table-sharded embeddings + data-parallel MLP x{world}",
                         "mlp": "PyTorch bf16 autocast, one CUDA graph per step (13-512-256-64-16 / 367-1024-1024-512-256-1)",
                         "embedding_optimizer": "sgd", "final_loss": losses[-1] if losses else None,
                         "embedding_stage_ms_per_step": spans[0] / steps},

@@ -151,9 +151,13 @@ class DLRMConfig:
 class DLRMTrainer:
     """Runs the dense model between the two native halves of an iteration."""
 
-    def __init__(self, dcfg: DLRMConfig, num_dense: int, num_tables: int, dim: int, model: DLRMDense | None = None):
+    def __init__(self, dcfg: DLRMConfig, num_dense: int, num_tables: int, dim: int, model: DLRMDense | None = None,
+                 exchange=None):
+        """exchange: a hybrid.EmbeddingExchange for N > 1 (model-parallel tables,
+        data-parallel MLPs); None on one GPU."""
         self.dcfg = dcfg
         self.dim = dim
+        self.exchange = exchange
         torch.manual_seed(dcfg.seed)
         self.model = (model or DLRMDense(num_dense, num_tables, dim, dcfg.bottom, dcfg.top)).cuda()
         self.opt = torch.optim.SGD(self.model.parameters(), lr=dcfg.mlp_lr)
@@ -169,6 +173,8 @@ class DLRMTrainer:
         self._dense_dev[pos] = (dense, labels)
 
     def train(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res) -> None:
+        if self.exchange is not None and self.exchange.world > 1:
+            return self._train_hybrid(pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
         lib = pipe.lib
         batch = pipe.batches[pos]
         n_occ = int(batch.packed_occurrences()[0].size)
@@ -176,13 +182,7 @@ class DLRMTrainer:
         t = n_occ // max(b, 1)
         stream = pipe.stream
         with torch.cuda.stream(stream):
-            dev = self._dense_dev.pop(pos, None)
-            if dev is None:
-                dense = torch.from_numpy(np.ascontiguousarray(batch.dense, dtype=np.float32)).to(
-                    "cuda", non_blocking=False)
-                labels = torch.from_numpy(np.ascontiguousarray(batch.labels, dtype=np.float32)).to("cuda")
-            else:
-                dense, labels = dev
+            dense, labels = self._inputs(pos, batch, slice(None))
             g = self._graph(b, t, dense.shape[1]) if self.dcfg.cuda_graph else None
             # the native forward writes the pooled rows straight into the
             # graph's static input (or a fresh leaf in eager mode)
@@ -193,6 +193,8 @@ class DLRMTrainer:
                 g["dense"][:, :dense.shape[1]].copy_(dense)
                 g["labels"].copy_(labels)
                 g["graph"].replay()
+                if g["step"] is not None:
+                    g["step"].replay()
                 grad = g["grad"]
                 self.losses.append(g["loss"].detach().clone())
             else:
@@ -203,10 +205,63 @@ class DLRMTrainer:
                 self.opt.step()
                 grad = emb.grad.contiguous()
                 self.losses.append(loss.detach())
-            L.check(lib.bp_engine_dlrm_backward(pipe.eng, pos, plan.slot, L.ptr(grad), self.dim, self.dcfg.opt_code,
-                                                float(np.float32(self.dcfg.emb_lr)),
-                                                float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
-                                                C.byref(res)), "bp_engine_dlrm_backward")
+            self._backward(pipe, pos, plan, grad, chunk, drain, res)
+
+    def _inputs(self, pos, batch, sl):
+        dev = self._dense_dev.pop(pos, None)
+        if dev is None:
+            dense = torch.from_numpy(np.ascontiguousarray(batch.dense[sl], dtype=np.float32)).to("cuda")
+            labels = torch.from_numpy(np.ascontiguousarray(batch.labels[sl], dtype=np.float32)).to("cuda")
+            return dense, labels
+        dense, labels = dev
+        return dense[sl], labels[sl]
+
+    def _backward(self, pipe, pos, plan, grad, chunk, drain, res) -> None:
+        L.check(pipe.lib.bp_engine_dlrm_backward(pipe.eng, pos, plan.slot, L.ptr(grad), self.dim, self.dcfg.opt_code,
+                                                 float(np.float32(self.dcfg.emb_lr)),
+                                                 float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
+                                                 C.byref(res)), "bp_engine_dlrm_backward")
+
+    def _train_hybrid(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res) -> None:
+        """N > 1 (hybrid.py): this rank's tables over the global batch ->
+        all-to-all -> the dense step on this rank's B/N examples -> reverse
+        all-to-all (x 1/N) -> mean all-reduce of MLP gradients -> SGD."""
+        from .hybrid import allreduce_mean_
+
+        ex = self.exchange
+        lib = pipe.lib
+        batch = pipe.batches[pos]
+        b = batch.num_examples
+        t_local = int(batch.packed_occurrences()[0].size) // max(b, 1)
+        bl = b // ex.world
+        sl = slice(ex.rank * bl, (ex.rank + 1) * bl)
+        with torch.cuda.stream(pipe.stream):
+            dense, labels = self._inputs(pos, batch, sl)
+            pooled = torch.empty((b, t_local, self.dim), dtype=torch.float32, device="cuda")
+            L.check(lib.bp_engine_dlrm_forward(pipe.eng, pos, plan.slot, nxt, skip_key, has_skip, self.dim,
+                                               L.ptr(pooled)), "bp_engine_dlrm_forward")
+            emb_in = ex.forward(pooled)
+            g = self._graph(bl, ex.num_tables, dense.shape[1], with_step=False) if self.dcfg.cuda_graph else None
+            if g is not None:
+                g["emb"].detach().copy_(emb_in)
+                g["dense"][:, :dense.shape[1]].copy_(dense)
+                g["labels"].copy_(labels)
+                g["graph"].replay()
+                grad, loss = g["grad"], g["loss"]
+            else:
+                emb = emb_in.requires_grad_(True)
+                loss = self._loss(dense, emb, labels)
+                self.opt.zero_grad(set_to_none=True)
+                loss.backward()
+                grad = emb.grad.contiguous()
+            self.losses.append(loss.detach().clone())
+            allreduce_mean_([p.grad for p in self.model.parameters()], ex.world)
+            if g is not None and g["step"] is not None:
+                g["step"].replay()
+            else:
+                self.opt.step()
+            grad_local = ex.backward(grad, scale=1.0 / ex.world)
+            self._backward(pipe, pos, plan, grad_local, chunk, drain, res)
 
     def _loss(self, dense, emb, labels):
         if self.dcfg.mlp_dtype == "bf16":
@@ -217,13 +272,13 @@ class DLRMTrainer:
             logits = self.model(dense, emb)
         return nn.functional.binary_cross_entropy_with_logits(logits, labels)
 
-    def _graph(self, b: int, t: int, n_dense: int) -> dict:
+    def _graph(self, b: int, t: int, n_dense: int, with_step: bool = True) -> dict:
         """The dense step for a (B, T) batch shape, captured once as a CUDA
         graph over static input buffers (the pooled embeddings, dense
         features, labels).  Replaying it costs one launch instead of ~100
         eager kernel launches from Python.  Warm-up passes before capture run
         forward+backward only, so the model's parameters are untouched."""
-        key = (b, t, n_dense)
+        key = (b, t, n_dense, with_step)
         g = self._graphs.get(key)
         if g is not None:
             return g
@@ -245,9 +300,17 @@ class DLRMTrainer:
         with torch.cuda.graph(graph, capture_error_mode="thread_local"):
             loss = self._loss(dense, emb, labels)
             loss.backward()
-            self.opt.step()
+            if with_step:
+                self.opt.step()
             grad = emb.grad.contiguous()
-        g = {"graph": graph, "emb": emb, "dense": dense, "labels": labels, "loss": loss, "grad": grad}
+        step = None
+        if not with_step:
+            # the SGD step as its own graph, replayed after the gradient all-reduce
+            step = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(step, pool=graph.pool(), capture_error_mode="thread_local"):
+                self.opt.step()
+        g = {"graph": graph, "step": step if not with_step else None, "emb": emb, "dense": dense, "labels": labels,
+             "loss": loss, "grad": grad}
         self._graphs[key] = g
         return g
 

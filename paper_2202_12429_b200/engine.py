@@ -664,15 +664,16 @@ run_bagpipe = run_pipeline
 
 
 def run_dlrm(cfg: EngineConfig, schema: Schema, trace: Iterable[Batch], dlrm_cfg=None, *, trace_fingerprint=None,
-             model=None):
+             model=None, exchange=None):
     """Pipelined BagPipe training of a DLRM (dense MLPs in PyTorch, embedding
     path native).  Returns (RunReport, DLRMTrainer); batches need dense
-    features (``Batch.dense``)."""
+    features (``Batch.dense``).  N > 1: pass this rank's table-sharded batches
+    (shard.shard_batches) and a hybrid.EmbeddingExchange."""
     from .dlrm import DLRMConfig, DLRMTrainer
 
     batches = _materialize(trace, cfg.iterations)
     dcfg = dlrm_cfg or DLRMConfig(emb_lr=cfg.lr, mlp_lr=cfg.lr)
-    trainer = DLRMTrainer(dcfg, schema.num_dense, schema.num_tables, schema.emb_dim, model=model)
+    trainer = DLRMTrainer(dcfg, schema.num_dense, schema.num_tables, schema.emb_dim, model=model, exchange=exchange)
     pipe = _Pipeline(cfg, schema, batches, trace_fingerprint, None, trainer=trainer)
     report = pipe.run()
     return report, trainer

@@ -207,3 +207,24 @@ def test_fused_interaction_matches_torch(dtype, t, d, pad):
     torch.testing.assert_close(x.grad.float(), x32.grad, **tol)
     torch.testing.assert_close(emb.grad, e32.grad, rtol=1e-5 if dtype == torch.float32 else 2e-2,
                                atol=1e-4 if dtype == torch.float32 else 5e-2)
+
+
+@pytest.mark.parametrize("opt_name", ["sgd", "adagrad"])
+def test_hybrid_dlrm_two_gpus_matches_cpu(opt_name):
+    """Hybrid parallel DLRM (table-sharded engines + NCCL all-to-all +
+    data-parallel MLPs) on 2 GPUs == one-process CPU training."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(root, "tools", "hybrid_check.py"), opt_name]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
