@@ -30,13 +30,25 @@ __device__ __forceinline__ void chain_chunk(const uint32_t (&word)[4], uint32_t 
   const uint32_t flags_lo = word[0] & 0x80808080u;
   if (lo == 0 && hi == 16 && !big && !flags_hi && (flags_lo == 0 || (first_q == 0 && flags_lo == 0x80u))) {
     // 16 occurrences, labels 0/1, no rank change: one select + one add each.
+    if constexpr (DPL == 1) {
+      // all 16 selects first (independent of the chain), then the 16
+      // dependent adds back to back: the chain runs at the add latency
+      float v[16];
 #pragma unroll
-    for (int wi = 0; wi < 4; ++wi) {
+      for (int i = 0; i < 16; ++i) v[i] = ((word[i >> 2] >> ((i & 3) * 8)) & 1u) ? t1[0] : t0[0];
+      float a = acc[0];
 #pragma unroll
-      for (int bi = 0; bi < 4; ++bi) {
-        const bool one = (word[wi] >> (bi * 8)) & 1u;
+      for (int i = 0; i < 16; ++i) a = __fadd_rn(a, v[i]);
+      acc[0] = a;
+    } else {
 #pragma unroll
-        for (int q = 0; q < DPL; ++q) acc[q] = __fadd_rn(acc[q], one ? t1[q] : t0[q]);
+      for (int wi = 0; wi < 4; ++wi) {
+#pragma unroll
+        for (int bi = 0; bi < 4; ++bi) {
+          const bool one = (word[wi] >> (bi * 8)) & 1u;
+#pragma unroll
+          for (int q = 0; q < DPL; ++q) acc[q] = __fadd_rn(acc[q], one ? t1[q] : t0[q]);
+        }
       }
     }
     return;
@@ -114,9 +126,11 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
         for (uint32_t k = threadIdx.x; k < nchunk; k += blockDim.x) win[k] = chunks[wc + k];
         __syncthreads();
         if (chain_lane) {
+          uint4 nxt4 = win[0];
 #pragma unroll 2
           for (uint32_t k = 0; k < nchunk; ++k) {
-            const uint4 w4 = win[k];
+            const uint4 w4 = nxt4;
+            if (k + 1 < nchunk) nxt4 = win[k + 1];  // next chunk's bytes in flight during this chain
             const uint32_t word[4] = {w4.x, w4.y, w4.z, w4.w};
             const uint32_t cbase = (wc + k) << 4;
             const uint32_t lo = a > cbase ? a - cbase : 0u;
