@@ -326,7 +326,16 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
 
     steps, warm = args.steps, args.warmup
     dcfg = DLRMConfig(emb_optimizer="sgd", emb_lr=0.01, mlp_lr=0.01, mlp_dtype="bf16")
-    ex = EmbeddingExchange(sc.num_tables, DIM, rank, world) if world > 1 else None
+    ex = None
+    if world > 1:
+        from paper_2202_12429_b200.hybrid import PeerExchange
+
+        # NVLink peer-memory exchange fused into the EmbeddingBag kernels
+        # (default) or the NCCL all-to-all version
+        if os.environ.get("BAGPIPE_B200_EXCHANGE", "peer") == "peer":
+            ex = PeerExchange(sc.num_tables, DIM, rank, world, BATCH // world)
+        else:
+            ex = EmbeddingExchange(sc.num_tables, DIM, rank, world)
     trainer = DLRMTrainer(dcfg, sc.num_dense, sc.num_tables, DIM, exchange=ex)
     dev_inputs = {}
     for i, b in enumerate(batches):
@@ -359,7 +368,8 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
     del pipe
     return {"summary": {"value": BATCH * steps / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms / steps,
                         "parallelism": "single" if world == 1 else
-                        f"hybrid: table-sharded embeddings + data-parallel MLP x{world}",
+                        f"hybrid: table-sharded embeddings + data-parallel MLP x{world}, "
+                        f"{'NVLink peer-memory' if hasattr(ex, 'rows_x') else 'NCCL all-to-all'} exchange",
                         "mlp": "PyTorch bf16 autocast, one CUDA graph per step (13-512-256-64-16 / 367-1024-1024-512-256-1)",
                         "embedding_optimizer": "sgd", "final_loss": losses[-1] if losses else None,
                         "embedding_stage_ms_per_step": spans[0] / steps},

@@ -430,6 +430,54 @@ int bp_embbag_backward(bp_prep* prep, const float* d_grad, const int64_t* d_occ_
                        int32_t opt, float lr, float eps, int64_t* d_stats, bp_stream_t stream);
 int bp_prep_occ_sorted_index(bp_prep* prep, uint32_t* d_occ_s, bp_stream_t stream);
 
+/* ---------------------------------------------------------- peer exchange */
+/* DLRM hybrid parallelism over NVLink peer memory (csrc/peer.cu).  Rank
+ * `rank` of `world` owns the embedding columns d_col_tables[0..n_cols)
+ * (global table ids) of a global batch of world * bl examples, occurrences
+ * example-major ([B][n_cols]).  Example owner q holds, for its bl examples,
+ * a [bl][t_global][dim] f32 row buffer that every rank addresses through
+ * d_peer_rows[q] (CUDA IPC); d_peer_flags[q] is q's flag array ([world]
+ * u32), d_flags this rank's own.  The forward stores pooled rows into the
+ * example owners' buffers, the backward loads gradient rows from them. */
+#define BP_IPC_HANDLE_BYTES 64
+typedef struct bp_peer_xchg {
+  int32_t world;
+  int32_t rank;
+  int64_t bl;
+  int32_t t_global;
+  int32_t n_cols;
+  const int32_t* d_col_tables;
+  float* const* d_peer_rows;
+  uint32_t* const* d_peer_flags;
+  uint32_t* d_flags;
+} bp_peer_xchg;
+int bp_ipc_alloc(int64_t bytes, void** d_ptr, uint8_t* handle); /* zeroed cudaMalloc + IPC handle */
+int bp_ipc_open(const uint8_t* handle, void** d_ptr);
+int bp_ipc_close(void* d_ptr);
+int bp_ipc_free(void* d_ptr);
+/* All ranks: store `epoch` into every peer's flags (after a system fence),
+ * wait until every rank's flag here reached it (bounded: ENGINE error in the
+ * context instead of a hang). */
+int bp_peer_barrier(bp_ctx* ctx, const bp_peer_xchg* x, uint32_t epoch, bp_stream_t stream);
+/* EmbeddingBag forward of single-key bags straight into the example owners'
+ * row buffers (d_peer_rows of `rows`). */
+int bp_embbag_forward_peer(bp_prep* prep, const float* d_values, int32_t row_stride, const int32_t* d_slots_s,
+                           int32_t dim, const bp_peer_xchg* rows, bp_stream_t stream);
+/* EmbeddingBag backward + optimizer reading each occurrence's gradient row
+ * from the example owner's buffer (d_peer_rows of `grads`) times `scale`. */
+int bp_embbag_backward_peer(bp_prep* prep, const bp_peer_xchg* grads, float scale, float* d_values,
+                            int32_t row_stride, const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt,
+                            float lr, float eps, int64_t* d_stats, bp_stream_t stream);
+/* Engine DLRM iteration with the peer exchange: forward = apply + lookup +
+ * bp_embbag_forward_peer into `rows`; backward = bp_embbag_backward_peer from
+ * `grads` (x scale) + eviction + counters (synchronises like
+ * bp_engine_dlrm_backward).  The caller runs the barriers. */
+int bp_engine_dlrm_forward_peer(bp_engine* engine, int64_t pos, int32_t plan_slot, int64_t next_pos,
+                                uint64_t skip_key, int32_t has_skip, int32_t model_dim, const bp_peer_xchg* rows);
+int bp_engine_dlrm_backward_peer(bp_engine* engine, int64_t pos, int32_t plan_slot, const bp_peer_xchg* grads,
+                                 float scale, int32_t model_dim, int32_t opt, float lr, float eps,
+                                 int32_t chunk_slot, int32_t drain_slot, bp_step_result* out);
+
 /* DLRM feature interaction (dense-model side of DLRM mode; the reference has
  * no model).  z = [x; emb_0..emb_{T-1}] per sample (T+1 vectors of D);
  * out row = [x | z_i . z_j, i > j, torch.tril_indices(T+1, T+1, -1) order |

@@ -86,6 +86,11 @@ class StepResult(C.Structure):
                                      "drained", "drained_dirty")] + [("err", ErrorT)]
 
 
+class PeerXchg(C.Structure):  # bp_peer_xchg
+    _fields_ = [("world", c_i32), ("rank", c_i32), ("bl", c_i64), ("t_global", c_i32), ("n_cols", c_i32),
+                ("d_col_tables", c_vp), ("d_peer_rows", c_vp), ("d_peer_flags", c_vp), ("d_flags", c_vp)]
+
+
 class EngineParts(C.Structure):
     _fields_ = [("store", c_vp), ("cache", c_vp), ("planner", c_vp), ("compute_stream", c_vp),
                 ("link_stream", c_vp)]
@@ -163,6 +168,17 @@ _SIGS = {
     "bp_engine_chunk_keys": (c_i32, [c_vp, c_i32, c_vp, c_i64]),
     "bp_engine_chunk_view": (c_i32, [c_vp, c_i32, P(EvictBuffers)]),
     "bp_engine_sync": (c_i32, [c_vp]),
+    "bp_ipc_alloc": (c_i32, [c_i64, P(c_vp), c_vp]),
+    "bp_ipc_open": (c_i32, [c_vp, P(c_vp)]),
+    "bp_ipc_close": (c_i32, [c_vp]),
+    "bp_ipc_free": (c_i32, [c_vp]),
+    "bp_peer_barrier": (c_i32, [c_vp, P(PeerXchg), C.c_uint32, c_vp]),
+    "bp_embbag_forward_peer": (c_i32, [c_vp, c_vp, c_i32, c_vp, c_i32, P(PeerXchg), c_vp]),
+    "bp_embbag_backward_peer": (c_i32, [c_vp, P(PeerXchg), c_f32, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32,
+                                        c_f32, c_vp, c_vp]),
+    "bp_engine_dlrm_forward_peer": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_u64, c_i32, c_i32, P(PeerXchg)]),
+    "bp_engine_dlrm_backward_peer": (c_i32, [c_vp, c_i64, c_i32, P(PeerXchg), c_f32, c_i32, c_i32, c_f32, c_f32,
+                                             c_i32, c_i32, P(StepResult)]),
     "bp_host_rows_bench": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp]),
     "bp_engine_set_link_mode": (c_i32, [c_vp, c_i32, c_i32]),
     "bp_engine_train_begin": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_u64, c_i32, c_i32, c_i32]),
@@ -204,7 +220,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         fn.restype = res
         fn.argtypes = args
     structs = (ErrorT, PrepView, PlanBuffers, PlannerStats, CacheStats, EvictBuffers, CacheView, EngineConfig,
-               StepResult, EngineParts, PlannerDump)
+               StepResult, EngineParts, PlannerDump, PeerXchg)
     for i, st in enumerate(structs):
         if lib_.bp_abi_sizeof(i) != C.sizeof(st):
             raise NativeUnavailable(f"ABI mismatch for {st.__name__}: library {lib_.bp_abi_sizeof(i)} bytes, "

@@ -42,6 +42,40 @@ __global__ void __launch_bounds__(256) k_embbag_fwd_rows_v4(const uint32_t* __re
   }
 }
 
+// Gradient / row source in a peer example owner's [bl][t_global][Q] buffer
+// (csrc/peer.cu); rows == nullptr: local gradient rows.
+struct PeerSrc {
+  float4* const* rows;
+  const int32_t* col_tables;
+  long long bl;
+  int t_global;
+  int n_cols;
+  float scale;
+};
+
+__device__ __forceinline__ float4* peer_row(const PeerSrc& ps, long long p, int q) {
+  const long long b = p / ps.n_cols;
+  const int j = (int)(p - b * ps.n_cols);
+  const long long r = b / ps.bl;
+  return ps.rows[r] + ((b - r * ps.bl) * ps.t_global + ps.col_tables[j]) * q;
+}
+
+// Forward fused with the all-to-all: pooled row of occurrence p (example b,
+// local column j) stored straight into example owner b / bl's buffer at its
+// global-table column, over NVLink.
+__global__ void __launch_bounds__(256) k_embbag_fwd_peer_v4(const uint32_t* __restrict__ occ_s,
+                                                           const int32_t* __restrict__ slots_s,
+                                                           const float4* __restrict__ values, int q, int row_q,
+                                                           long long n, PeerSrc dst) {
+  const long long total = n * q;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long p = i / q;
+    const int c = (int)(i - p * q);
+    const int32_t slot = slots_s[occ_s[p]];
+    peer_row(dst, p, q)[c] = slot >= 0 ? values[(long long)slot * row_q + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 template <int G, int DPL>
 __global__ void __launch_bounds__(256) k_embbag_fwd_gather(const uint32_t* __restrict__ occ_s,
                                                            const int32_t* __restrict__ slots_s,
@@ -350,7 +384,7 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
     long long n, const float4* __restrict__ grad, const int64_t* __restrict__ occ_bag,
     const float* __restrict__ bag_scale, float* __restrict__ values, int row_stride,
     const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
-    float4* __restrict__ parts, unsigned long long* __restrict__ stats) {
+    float4* __restrict__ parts, unsigned long long* __restrict__ stats, PeerSrc src) {
   constexpr int R = 8 / Q, T = 32 * R;
   const unsigned lane = threadIdx.x & 31u;
   const long long tile = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -372,10 +406,27 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
   }
   float4 v[R][Q];
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (src.rows) {  // gradient rows in the example owners' buffers (NVLink loads)
 #pragma unroll
-  for (int j = 0; j < R; ++j)
+    for (int j = 0; j < R; ++j) {
+      const float4* row = pk[j] >= 0 ? peer_row(src, pk[j], Q) : nullptr;
 #pragma unroll
-    for (int c = 0; c < Q; ++c) v[j][c] = pk[j] >= 0 ? grad[pk[j] * Q + c] : zero;
+      for (int c = 0; c < Q; ++c) v[j][c] = row ? row[c] : zero;
+    }
+    if (src.scale != 1.f) {
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int c = 0; c < Q; ++c)
+          v[j][c] = make_float4(__fmul_rn(v[j][c].x, src.scale), __fmul_rn(v[j][c].y, src.scale),
+                                __fmul_rn(v[j][c].z, src.scale), __fmul_rn(v[j][c].w, src.scale));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+      for (int c = 0; c < Q; ++c) v[j][c] = pk[j] >= 0 ? grad[pk[j] * Q + c] : zero;
+  }
   if (bag_scale) {
 #pragma unroll
     for (int j = 0; j < R; ++j)
@@ -605,10 +656,10 @@ extern "C" int bp_embbag_forward(bp_prep* P, const float* d_values, int32_t row_
   return BP_OK;
 }
 
-extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t* d_occ_bag,
-                                  const float* d_bag_scale, float* d_values, int32_t row_stride,
-                                  const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt, float lr,
-                                  float eps, int64_t* d_stats, bp_stream_t stream) {
+static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* d_occ_bag, const float* d_bag_scale,
+                                float* d_values, int32_t row_stride, const int32_t* d_slots_s, uint8_t* d_dirty,
+                                int32_t dim, int32_t opt, float lr, float eps, int64_t* d_stats, bp_stream_t stream,
+                                const bp::PeerSrc* peer_src) {
   using namespace bp;
   if (dim < 1 || dim > 128) return BP_ERR_INVALID;
   if (opt == BP_OPT_ADAGRAD && row_stride < 2 * dim) return BP_ERR_INVALID;
@@ -619,6 +670,7 @@ extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t
   if (P->d_seg_of && (dim & 3) == 0 && (row_stride & 3) == 0 && dim <= 32 && (32 % dim) == 0) {
     const int q = dim / 4, T = 32 * (8 / q);
     const long long tiles = (P->n_occ + T - 1) / T;
+    const PeerSrc psrc = peer_src ? *peer_src : PeerSrc{nullptr, nullptr, 1, 1, 1, 1.f};
     float4* parts = nullptr;
     BP_CUDA_TRY(pool_alloc(&parts, (size_t)tiles * 2 * q, s));
     const unsigned blocks = (unsigned)((tiles + 7) / 8);
@@ -626,7 +678,7 @@ extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t
   k_embbag_bwd_warp<QQ><<<blocks, 256, 0, s>>>(P->d_occ_pos, P->d_seg_of, P->d_seg_start, P->n_occ,              \
                                                reinterpret_cast<const float4*>(d_grad), d_occ_bag, d_bag_scale,  \
                                                d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts,    \
-                                               (unsigned long long*)d_stats)
+                                               (unsigned long long*)d_stats, psrc)
     switch (q) {
       case 1: BP_BWD_WARP(1); break;
       case 2: BP_BWD_WARP(2); break;
@@ -641,6 +693,7 @@ extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t
     cudaFreeAsync(parts, s);
     return BP_OK;
   }
+  if (peer_src) return BP_ERR_INVALID;  // the peer source needs the warp-tile path
   if (P->d_seg_of && (dim & 3) == 0 && (row_stride & 3) == 0 && dim <= 128) {
     const int q = dim / 4, T = kBwdTileF4 / q;
     const long long tiles = (P->n_occ + T - 1) / T;
@@ -678,6 +731,43 @@ extern "C" int bp_prep_occ_sorted_index(bp_prep* P, uint32_t* d_occ_s, bp_stream
   if (P->n_occ == 0) return BP_OK;
   k_occ_sorted_index<<<grid_for(P->n_occ, 256), 256, 0, (cudaStream_t)stream>>>(P->d_seg_start, P->d_occ_pos,
                                                                                  P->d_num_unique, P->n_occ, d_occ_s);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_embbag_backward(bp_prep* P, const float* d_grad, const int64_t* d_occ_bag,
+                                  const float* d_bag_scale, float* d_values, int32_t row_stride,
+                                  const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt, float lr,
+                                  float eps, int64_t* d_stats, bp_stream_t stream) {
+  return embbag_backward_impl(P, d_grad, d_occ_bag, d_bag_scale, d_values, row_stride, d_slots_s, d_dirty, dim, opt,
+                              lr, eps, d_stats, stream, nullptr);
+}
+
+extern "C" int bp_embbag_backward_peer(bp_prep* P, const bp_peer_xchg* x, float scale, float* d_values,
+                                       int32_t row_stride, const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim,
+                                       int32_t opt, float lr, float eps, int64_t* d_stats, bp_stream_t stream) {
+  using namespace bp;
+  if (!x || !P->d_seg_of || (dim & 3) != 0 || dim > 32 || (32 % dim) != 0 || x->n_cols < 1 || x->bl < 1)
+    return BP_ERR_INVALID;
+  if (P->n_occ != x->bl * x->world * x->n_cols) return BP_ERR_INVALID;
+  const PeerSrc ps{reinterpret_cast<float4* const*>(x->d_peer_rows), x->d_col_tables, x->bl, x->t_global, x->n_cols,
+                   scale};
+  return embbag_backward_impl(P, nullptr, nullptr, nullptr, d_values, row_stride, d_slots_s, d_dirty, dim, opt, lr,
+                              eps, d_stats, stream, &ps);
+}
+
+extern "C" int bp_embbag_forward_peer(bp_prep* P, const float* d_values, int32_t row_stride, const int32_t* d_slots_s,
+                                      int32_t dim, const bp_peer_xchg* x, bp_stream_t stream) {
+  using namespace bp;
+  if (!x || !P->d_occ_s || (dim & 3) != 0 || (row_stride & 3) != 0 || x->n_cols < 1 || x->bl < 1)
+    return BP_ERR_INVALID;
+  if (P->n_occ != x->bl * x->world * x->n_cols) return BP_ERR_INVALID;
+  if (P->n_occ == 0) return BP_OK;
+  const int q = dim / 4;
+  const PeerSrc dst{reinterpret_cast<float4* const*>(x->d_peer_rows), x->d_col_tables, x->bl, x->t_global, x->n_cols,
+                    1.f};
+  k_embbag_fwd_peer_v4<<<grid_for(P->n_occ * q, 256, kNumSMs * 16), 256, 0, (cudaStream_t)stream>>>(
+      P->d_occ_s, d_slots_s, reinterpret_cast<const float4*>(d_values), q, row_stride / 4, P->n_occ, dst);
   BP_LAUNCH_CHECK();
   return BP_OK;
 }

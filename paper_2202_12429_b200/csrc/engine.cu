@@ -57,6 +57,9 @@ int bp_prep_create_columnar(bp_ctx*, const bp_schema*, const uint64_t*, const ui
 int bp_stub_step(bp_ctx*, bp_prep*, float*, const int32_t*, uint8_t*, int32_t, float, float, float, int32_t, float*,
                  const int64_t*, int64_t, int64_t*, bp_stream_t);
 int bp_store_create_ex(bp_ctx*, const bp_schema*, uint64_t, int32_t, bp_stream_t, bp_store**);
+int bp_embbag_forward_peer(bp_prep*, const float*, int32_t, const int32_t*, int32_t, const bp_peer_xchg*, bp_stream_t);
+int bp_embbag_backward_peer(bp_prep*, const bp_peer_xchg*, float, float*, int32_t, const int32_t*, uint8_t*, int32_t,
+                            int32_t, float, float, int64_t*, bp_stream_t);
 int bp_embbag_forward(bp_prep*, const float*, int32_t, const int32_t*, int32_t, const int64_t*, int64_t, int32_t,
                       const uint32_t*, float*, bp_stream_t);
 int bp_embbag_backward(bp_prep*, const float*, const int64_t*, const float*, float*, int32_t, const int32_t*,
@@ -874,6 +877,50 @@ extern "C" int bp_engine_dlrm_backward(bp_engine* e, int64_t pos, int32_t plan_s
   stage_begin(e, kStageTrainer, e->compute);
   int rc = bp_embbag_backward(P, d_grad, nullptr, nullptr, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty,
                               model_dim, opt, lr, eps, e->stats, e->compute);
+  stage_end(e, kStageTrainer, e->compute);
+  if (rc) return rc;
+  return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
+}
+
+// DLRM hybrid parallel over NVLink peer memory (csrc/peer.cu): the same two
+// halves, the forward storing pooled rows into the example owners' buffers,
+// the backward loading gradient rows from them.
+extern "C" int bp_engine_dlrm_forward_peer(bp_engine* e, int64_t pos, int32_t plan_slot, int64_t next_pos,
+                                           uint64_t skip_key, int32_t has_skip, int32_t model_dim,
+                                           const bp_peer_xchg* rows) {
+  using namespace bp;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  PlanSlot& ps = e->plans[plan_slot];
+  bp_prep* N = nullptr;
+  int rc = engine_apply(e, P, ps, next_pos, skip_key, has_skip, &N);
+  if (rc) return rc;
+  if (N) {
+    k_count_critical<<<grid_for(P->n_occ, 256), 256, 0, e->compute>>>(P->d_uniq_id_s, P->d_num_unique, e->mark,
+                                                                      N->iteration,
+                                                                      (unsigned long long*)e->stats);
+    BP_LAUNCH_CHECK();
+  }
+  bp_cache_view cv;
+  bp_cache_get_view(e->cache, &cv);
+  stage_begin(e, kStageTrainer, e->compute);
+  rc = bp_embbag_forward_peer(P, cv.d_values, e->cfg.dim, e->slots_s, model_dim, rows, e->compute);
+  stage_end(e, kStageTrainer, e->compute);
+  return rc;
+}
+
+extern "C" int bp_engine_dlrm_backward_peer(bp_engine* e, int64_t pos, int32_t plan_slot, const bp_peer_xchg* grads,
+                                            float scale, int32_t model_dim, int32_t opt, float lr, float eps,
+                                            int32_t chunk_slot, int32_t drain_slot, bp_step_result* out) {
+  using namespace bp;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  PlanSlot& ps = e->plans[plan_slot];
+  bp_cache_view cv;
+  bp_cache_get_view(e->cache, &cv);
+  stage_begin(e, kStageTrainer, e->compute);
+  int rc = bp_embbag_backward_peer(P, grads, scale, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim, opt,
+                                   lr, eps, e->stats, e->compute);
   stage_end(e, kStageTrainer, e->compute);
   if (rc) return rc;
   return engine_finish(e, P, ps, chunk_slot, drain_slot, out);

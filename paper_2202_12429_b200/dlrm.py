@@ -174,6 +174,8 @@ class DLRMTrainer:
 
     def train(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res) -> None:
         if self.exchange is not None and self.exchange.world > 1:
+            if hasattr(self.exchange, "rows_x"):
+                return self._train_peer(pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
             return self._train_hybrid(pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
         lib = pipe.lib
         batch = pipe.batches[pos]
@@ -263,6 +265,55 @@ class DLRMTrainer:
             grad_local = ex.backward(grad, scale=1.0 / ex.world)
             self._backward(pipe, pos, plan, grad_local, chunk, drain, res)
 
+    def _train_peer(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res) -> None:
+        """N > 1 over NVLink peer memory (hybrid.PeerExchange): the forward
+        stores pooled rows into the example owners' buffers, a device
+        barrier, the dense step reading its buffer in place, gradients into
+        the local gradient buffer, a barrier, the mean all-reduce of MLP
+        gradients + SGD, and the table owners' backward loading the
+        gradients over NVLink (x 1/N)."""
+        import ctypes as C
+
+        from .hybrid import allreduce_mean_
+
+        ex = self.exchange
+        lib = pipe.lib
+        batch = pipe.batches[pos]
+        bl = batch.num_examples // ex.world
+        sl = slice(ex.rank * bl, (ex.rank + 1) * bl)
+        stream = pipe.stream
+        with torch.cuda.stream(stream):
+            dense, labels = self._inputs(pos, batch, sl)
+            L.check(lib.bp_engine_dlrm_forward_peer(pipe.eng, pos, plan.slot, nxt, skip_key, has_skip, self.dim,
+                                                    C.byref(ex.rows_x)), "bp_engine_dlrm_forward_peer")
+            ex.barrier(stream)
+            g = self._graph(bl, ex.num_tables, dense.shape[1], with_step=False, emb=ex.rows) \
+                if self.dcfg.cuda_graph else None
+            if g is not None:
+                g["dense"][:, :dense.shape[1]].copy_(dense)
+                g["labels"].copy_(labels)
+                g["graph"].replay()
+                grad, loss = g["grad"], g["loss"]
+            else:
+                emb = ex.rows.detach().requires_grad_(True)
+                loss = self._loss(dense, emb, labels)
+                self.opt.zero_grad(set_to_none=True)
+                loss.backward()
+                grad = emb.grad
+            ex.grads.copy_(grad)
+            ex.barrier(stream)
+            self.losses.append(loss.detach().clone())
+            allreduce_mean_([p.grad for p in self.model.parameters()], ex.world)
+            if g is not None and g["step"] is not None:
+                g["step"].replay()
+            else:
+                self.opt.step()
+            L.check(lib.bp_engine_dlrm_backward_peer(pipe.eng, pos, plan.slot, C.byref(ex.grads_x),
+                                                     1.0 / ex.world, self.dim, self.dcfg.opt_code,
+                                                     float(np.float32(self.dcfg.emb_lr)),
+                                                     float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
+                                                     C.byref(res)), "bp_engine_dlrm_backward_peer")
+
     def _loss(self, dense, emb, labels):
         if self.dcfg.mlp_dtype == "bf16":
             with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
@@ -272,18 +323,21 @@ class DLRMTrainer:
             logits = self.model(dense, emb)
         return nn.functional.binary_cross_entropy_with_logits(logits, labels)
 
-    def _graph(self, b: int, t: int, n_dense: int, with_step: bool = True) -> dict:
+    def _graph(self, b: int, t: int, n_dense: int, with_step: bool = True, emb=None) -> dict:
         """The dense step for a (B, T) batch shape, captured once as a CUDA
         graph over static input buffers (the pooled embeddings, dense
         features, labels).  Replaying it costs one launch instead of ~100
         eager kernel launches from Python.  Warm-up passes before capture run
         forward+backward only, so the model's parameters are untouched."""
-        key = (b, t, n_dense, with_step)
+        key = (b, t, n_dense, with_step, None if emb is None else emb.data_ptr())
         g = self._graphs.get(key)
         if g is not None:
             return g
         dev = "cuda"
-        emb = torch.zeros((b, t, self.dim), dtype=torch.float32, device=dev, requires_grad=True)
+        # static input: a fresh buffer, or caller memory read in place (the
+        # peer exchange's row buffer)
+        emb = torch.zeros((b, t, self.dim), dtype=torch.float32, device=dev, requires_grad=True) if emb is None \
+            else emb.detach().requires_grad_(True)
         dense = torch.zeros((b, n_dense + self.model.dense_pad), dtype=torch.float32, device=dev)
         labels = torch.zeros((b,), dtype=torch.float32, device=dev)
         torch.cuda.synchronize()

@@ -92,3 +92,87 @@ def allreduce_mean_(tensors, world: int, group=None) -> None:
         k = t.numel()
         t.copy_(flat[off:off + k].view_as(t))
         off += k
+
+
+class PeerExchange:
+    """The exchange over NVLink peer memory (csrc/peer.cu): no NCCL on the
+    embedding data path.  Every rank owns two [bl, T, D] f32 buffers, shared
+    with CUDA IPC handles exchanged over torch.distributed:
+
+    * ``rows``  -- the table owners' EmbeddingBag forward stores pooled rows
+      straight into the example owner's buffer, at the row's global table
+      column (the dense step reads it in place);
+    * ``grads`` -- the example owner writes its pooled-row gradients here and
+      the table owners' reduce-by-key backward loads them over NVLink.
+
+    Two flag barriers per iteration (rows ready, gradients ready) order the
+    phases and protect buffer reuse.  Same interface fields as
+    EmbeddingExchange (shards, local_tables, world, rank, num_tables)."""
+
+    def __init__(self, num_tables: int, dim: int, rank: int, world: int, bl: int, group=None):
+        import ctypes as C
+
+        from . import _lib as L
+        from .device import _wrap_device
+
+        self.num_tables, self.dim, self.rank, self.world, self.bl, self.group = num_tables, dim, rank, world, bl, group
+        self.shards = table_shards(num_tables, world)
+        self.local_tables = self.shards[rank]
+        lib = L.lib()
+        self._lib, self._L = lib, L
+        nbytes = bl * num_tables * dim * 4
+        own, handles = {}, {}
+        for name, size in (("rows", nbytes), ("grads", nbytes), ("flags", 4 * world)):
+            ptr, h = C.c_void_p(), (C.c_uint8 * 64)()
+            L.check(lib.bp_ipc_alloc(size, C.byref(ptr), h), "bp_ipc_alloc")
+            own[name], handles[name] = ptr.value, bytes(h)
+        self._own = own
+        gathered = [None] * world
+        dist.all_gather_object(gathered, handles, group=group)
+        self._opened = []
+        peers = {name: [] for name in own}
+        for q in range(world):
+            for name in own:
+                if q == rank:
+                    peers[name].append(own[name])
+                    continue
+                ptr = C.c_void_p()
+                buf = (C.c_uint8 * 64).from_buffer_copy(gathered[q][name])
+                L.check(lib.bp_ipc_open(buf, C.byref(ptr)), "bp_ipc_open")
+                self._opened.append(ptr.value)
+                peers[name].append(ptr.value)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self._d_rows = torch.tensor(peers["rows"], dtype=torch.int64, device=dev)
+        self._d_grads = torch.tensor(peers["grads"], dtype=torch.int64, device=dev)
+        self._d_flags = torch.tensor(peers["flags"], dtype=torch.int64, device=dev)
+        self._d_cols = torch.tensor(self.local_tables, dtype=torch.int32, device=dev)
+        t_r = len(self.local_tables)
+        self.rows_x = L.PeerXchg(world, rank, bl, num_tables, t_r, L.ptr(self._d_cols), L.ptr(self._d_rows),
+                                 L.ptr(self._d_flags), own["flags"])
+        self.grads_x = L.PeerXchg(world, rank, bl, num_tables, t_r, L.ptr(self._d_cols), L.ptr(self._d_grads),
+                                  L.ptr(self._d_flags), own["flags"])
+        self.rows = _wrap_device(own["rows"], torch.float32, bl * num_tables * dim).view(bl, num_tables, dim)
+        self.grads = _wrap_device(own["grads"], torch.float32, bl * num_tables * dim).view(bl, num_tables, dim)
+        self.epoch = 0
+        dist.barrier(group=group)  # every rank opened every handle
+
+    def barrier(self, stream) -> None:
+        """Device-side barrier of all ranks on `stream` (bounded spin)."""
+        import ctypes as C
+
+        self.epoch += 1
+        L = self._L
+        L.check(self._lib.bp_peer_barrier(L.Context.get().handle, C.byref(self.rows_x), self.epoch,
+                                          L.stream_ptr(stream)), "bp_peer_barrier")
+
+    def close(self) -> None:
+        if getattr(self, "_own", None) is None:
+            return
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        for p in self._opened:
+            self._lib.bp_ipc_close(p)
+        dist.barrier(group=self.group)
+        for p in self._own.values():
+            self._lib.bp_ipc_free(p)
+        self._own = None

@@ -209,9 +209,11 @@ def test_fused_interaction_matches_torch(dtype, t, d, pad):
                                atol=1e-4 if dtype == torch.float32 else 5e-2)
 
 
+@pytest.mark.parametrize("kind", ["peer", "nccl"])
 @pytest.mark.parametrize("opt_name", ["sgd", "adagrad"])
-def test_hybrid_dlrm_two_gpus_matches_cpu(opt_name):
-    """Hybrid parallel DLRM (table-sharded engines + NCCL all-to-all +
+def test_hybrid_dlrm_two_gpus_matches_cpu(opt_name, kind):
+    """Hybrid parallel DLRM (table-sharded engines + the NVLink peer-memory
+    exchange fused into the EmbeddingBag kernels, or NCCL all-to-all +
     data-parallel MLPs) on 2 GPUs == one-process CPU training."""
     import os
     import socket
@@ -225,6 +227,6 @@ def test_hybrid_dlrm_two_gpus_matches_cpu(opt_name):
         port = s.getsockname()[1]
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", str(port), os.path.join(root, "tools", "hybrid_check.py"), opt_name]
+           "127.0.0.1", "--master-port", str(port), os.path.join(root, "tools", "hybrid_check.py"), opt_name, kind]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

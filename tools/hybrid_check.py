@@ -1,6 +1,7 @@
 """DLRM hybrid parallelism on N GPUs vs one-process PyTorch CPU training.
 
-  python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/hybrid_check.py [sgd|adagrad]
+  python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/hybrid_check.py \
+      [sgd|adagrad] [peer|nccl]
 
 Each rank runs the pipelined engine for its table shard (hybrid.py) with the
 NCCL all-to-all exchange; rank 0 gathers the final tables and MLP weights
@@ -24,6 +25,7 @@ import torch.distributed as dist  # noqa: E402
 
 def main() -> int:
     opt_name = sys.argv[1] if len(sys.argv) > 1 else "sgd"
+    kind = sys.argv[2] if len(sys.argv) > 2 else "peer"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
@@ -31,7 +33,7 @@ def main() -> int:
 
     from paper_2202_12429_b200.dlrm import DLRMConfig, DLRMDense
     from paper_2202_12429_b200.engine import EngineConfig, run_dlrm
-    from paper_2202_12429_b200.hybrid import EmbeddingExchange
+    from paper_2202_12429_b200.hybrid import EmbeddingExchange, PeerExchange
     from paper_2202_12429_b200.shard import shard_batches
 
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -40,7 +42,10 @@ def main() -> int:
     model = DLRMDense(SCHEMA.num_dense, SCHEMA.num_tables, SCHEMA.emb_dim, bottom=(64, 32), top=(64, 32))
     batches = _batches()
     lr, eps, seed = 0.05, 1e-10, 7
-    ex = EmbeddingExchange(SCHEMA.num_tables, SCHEMA.emb_dim, rank, world)
+    if kind == "peer":
+        ex = PeerExchange(SCHEMA.num_tables, SCHEMA.emb_dim, rank, world, 256 // world)
+    else:
+        ex = EmbeddingExchange(SCHEMA.num_tables, SCHEMA.emb_dim, rank, world)
     cfg = EngineConfig(cache_capacity=1200, batch_size=256, lookahead=3, num_shards=1, seed=seed, lr=lr)
     dcfg = DLRMConfig(emb_optimizer=opt_name, emb_lr=lr, mlp_lr=lr, adagrad_eps=eps, bottom=(64, 32), top=(64, 32))
     report, trainer = run_dlrm(cfg, SCHEMA, shard_batches(batches, ex.local_tables), dcfg, model=copy.deepcopy(model),
@@ -67,8 +72,10 @@ def main() -> int:
         for (name, p), (_, q) in zip(trainer.model.named_parameters(), want_model.named_parameters()):
             np.testing.assert_allclose(p.detach().cpu().numpy(), q.detach().numpy(), rtol=1e-4, atol=1e-6,
                                        err_msg=name)
-        print(f"hybrid DLRM x{world} ({opt_name}) == single-process CPU training", flush=True)
+        print(f"hybrid DLRM x{world} ({opt_name}, {kind} exchange) == single-process CPU training", flush=True)
     dist.barrier()
+    if kind == "peer":
+        ex.close()
     dist.destroy_process_group()
     return 0 if ok else 1
 
