@@ -33,12 +33,33 @@ __global__ void __launch_bounds__(256) k_embbag_fwd_rows_v4(const uint32_t* __re
                                                            const int32_t* __restrict__ slots_s,
                                                            const float4* __restrict__ values, int q,
                                                            int row_q, long long n, float4* __restrict__ out) {
+  // 4 elements per thread, their three dependent loads (unique index, slot,
+  // row) issued as batches so the latency chain is paid once per 4 rows
+  constexpr int U = 4;
   const long long total = n * q;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long p = i / q;
-    const int c = (int)(i - p * q);
-    const int32_t slot = slots_s[occ_s[p]];
-    out[i] = slot >= 0 ? values[(long long)slot * row_q + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += stride * U) {
+    uint32_t u[U];
+    int32_t sl[U];
+    float4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      u[k] = i < total ? occ_s[i / q] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) sl[k] = i0 + k * stride < total ? slots_s[u[k]] : -1;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      const int c = (int)(i - (i / q) * q);
+      v[k] = sl[k] >= 0 ? values[(long long)sl[k] * row_q + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      if (i < total) out[i] = v[k];
+    }
   }
 }
 
@@ -293,7 +314,8 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_tiles(
     long long n, int q, int T, const float4* __restrict__ grad, const int64_t* __restrict__ occ_bag,
     const float* __restrict__ bag_scale, float* __restrict__ values, int row_stride,
     const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
-    float4* __restrict__ parts, unsigned long long* __restrict__ stats) {
+    float4* __restrict__ parts, unsigned long long* __restrict__ stats, uint32_t* __restrict__ span_list,
+    unsigned int* __restrict__ span_count) {
   extern __shared__ float4 tile[];  // [T*q] gradient rows, then [T] segment ids
   uint32_t* seg = reinterpret_cast<uint32_t*>(tile + kBwdTileF4);
   __shared__ unsigned int n_dirty;
@@ -361,6 +383,7 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_tiles(
     } else {  // spans tiles: leave this tile's partial for k_embbag_bwd_span
       float4* dst = parts + ((long long)blockIdx.x * 2 + (s == seg[0] ? 0 : 1)) * q;
       for (int c = 0; c < q; ++c) dst[c] = tile[r * q + c];
+      if (a >= t0) span_list[atomicAdd(span_count, 1u)] = blockIdx.x;  // the key's first tile
     }
     if (nz) {
       if (dirty) dirty[slot] = 1;
@@ -384,7 +407,8 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
     long long n, const float4* __restrict__ grad, const int64_t* __restrict__ occ_bag,
     const float* __restrict__ bag_scale, float* __restrict__ values, int row_stride,
     const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
-    float4* __restrict__ parts, unsigned long long* __restrict__ stats, PeerSrc src) {
+    float4* __restrict__ parts, unsigned long long* __restrict__ stats, PeerSrc src,
+    uint32_t* __restrict__ span_list, unsigned int* __restrict__ span_count) {
   constexpr int R = 8 / Q, T = 32 * R;
   const unsigned lane = threadIdx.x & 31u;
   const long long tile = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -514,6 +538,7 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
       float4* dst = parts + (tile * 2 + (s == tile_first ? 0 : 1)) * Q;
 #pragma unroll
       for (int c = 0; c < Q; ++c) dst[c] = v[j][c];
+      if (a >= t0) span_list[atomicAdd(span_count, 1u)] = (uint32_t)tile;  // the key's first tile
     }
   }
   if (stats) {
@@ -529,7 +554,8 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
 // xor tree combines the lanes -- and applies the update.
 __global__ void __launch_bounds__(256) k_embbag_bwd_span(
     const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start, long long n, int q, int T,
-    long long tiles, const float4* __restrict__ parts, float* __restrict__ values, int row_stride,
+    const uint32_t* __restrict__ span_list, const unsigned int* __restrict__ span_count,
+    const float4* __restrict__ parts, float* __restrict__ values, int row_stride,
     const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
     unsigned long long* __restrict__ stats) {
   const unsigned lane = threadIdx.x & 31u;
@@ -538,11 +564,12 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_span(
   while (per * 2 * q <= 32) per *= 2;
   const int c = (int)lane % q, tl = (int)lane / q;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < tiles; t += warps) {
+  const long long n_span = *span_count;
+  for (long long li = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); li < n_span; li += warps) {
+    const long long t = span_list[li];
     const long long last = min((t + 1) * (long long)T, n) - 1;
     const uint32_t s = seg_of[last];
     const long long a = seg_start[s], b = seg_start[s + 1];
-    if (a < t * T || b <= (t + 1) * (long long)T) continue;  // not a spanning key's first tile
     const int32_t slot = slots_s[s];
     if (slot < 0) continue;
     const long long lt = (b - 1) / T, nt = lt - t + 1;
@@ -642,7 +669,7 @@ extern "C" int bp_embbag_forward(bp_prep* P, const float* d_values, int32_t row_
   if (!d_occ_s) return BP_ERR_INVALID;
   if (!d_bag_offsets && (dim & 3) == 0 && (row_stride & 3) == 0) {
     const int q = dim / 4;
-    k_embbag_fwd_rows_v4<<<grid_for(P->n_occ * q, 256, kNumSMs * 16), 256, 0, s>>>(
+    k_embbag_fwd_rows_v4<<<grid_for(P->n_occ * q, 256 * 4, kNumSMs * 8), 256, 0, s>>>(
         d_occ_s, d_slots_s, reinterpret_cast<const float4*>(d_values), q, row_stride / 4, P->n_occ,
         reinterpret_cast<float4*>(d_out));
   } else {
@@ -671,14 +698,21 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
     const int q = dim / 4, T = 32 * (8 / q);
     const long long tiles = (P->n_occ + T - 1) / T;
     const PeerSrc psrc = peer_src ? *peer_src : PeerSrc{nullptr, nullptr, 1, 1, 1, 1.f};
-    float4* parts = nullptr;
-    BP_CUDA_TRY(pool_alloc(&parts, (size_t)tiles * 2 * q, s));
+    // one allocation: tile partials, the spanning-key list and its count
+    const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
+    const size_t list_bytes = ((size_t)tiles * sizeof(uint32_t) + 255) & ~size_t(255);
+    char* scratch = nullptr;
+    BP_CUDA_TRY(pool_alloc(&scratch, parts_bytes + list_bytes + 256, s));
+    float4* parts = reinterpret_cast<float4*>(scratch);
+    uint32_t* span_list = reinterpret_cast<uint32_t*>(scratch + parts_bytes);
+    unsigned int* span_count = reinterpret_cast<unsigned int*>(scratch + parts_bytes + list_bytes);
+    BP_CUDA_TRY(cudaMemsetAsync(span_count, 0, sizeof(unsigned int), s));
     const unsigned blocks = (unsigned)((tiles + 7) / 8);
 #define BP_BWD_WARP(QQ)                                                                                        \
   k_embbag_bwd_warp<QQ><<<blocks, 256, 0, s>>>(P->d_occ_pos, P->d_seg_of, P->d_seg_start, P->n_occ,              \
                                                reinterpret_cast<const float4*>(d_grad), d_occ_bag, d_bag_scale,  \
                                                d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts,    \
-                                               (unsigned long long*)d_stats, psrc)
+                                               (unsigned long long*)d_stats, psrc, span_list, span_count)
     switch (q) {
       case 1: BP_BWD_WARP(1); break;
       case 2: BP_BWD_WARP(2); break;
@@ -686,19 +720,25 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
       default: BP_BWD_WARP(8); break;
     }
 #undef BP_BWD_WARP
-    k_embbag_bwd_span<<<grid_for(tiles * 32, 256, kNumSMs * 8), 256, 0, s>>>(
-        P->d_seg_of, P->d_seg_start, P->n_occ, q, T, tiles, parts, d_values, row_stride, d_slots_s, d_dirty, opt, lr,
-        eps, (unsigned long long*)d_stats);
+    k_embbag_bwd_span<<<kNumSMs * 2, 256, 0, s>>>(P->d_seg_of, P->d_seg_start, P->n_occ, q, T, span_list, span_count,
+                                                  parts, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps,
+                                                  (unsigned long long*)d_stats);
     BP_LAUNCH_CHECK();
-    cudaFreeAsync(parts, s);
+    cudaFreeAsync(scratch, s);
     return BP_OK;
   }
   if (peer_src) return BP_ERR_INVALID;  // the peer source needs the warp-tile path
   if (P->d_seg_of && (dim & 3) == 0 && (row_stride & 3) == 0 && dim <= 128) {
     const int q = dim / 4, T = kBwdTileF4 / q;
     const long long tiles = (P->n_occ + T - 1) / T;
-    float4* parts = nullptr;
-    BP_CUDA_TRY(pool_alloc(&parts, (size_t)tiles * 2 * q, s));
+    const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
+    const size_t list_bytes = ((size_t)tiles * sizeof(uint32_t) + 255) & ~size_t(255);
+    char* scratch = nullptr;
+    BP_CUDA_TRY(pool_alloc(&scratch, parts_bytes + list_bytes + 256, s));
+    float4* parts = reinterpret_cast<float4*>(scratch);
+    uint32_t* span_list = reinterpret_cast<uint32_t*>(scratch + parts_bytes);
+    unsigned int* span_count = reinterpret_cast<unsigned int*>(scratch + parts_bytes + list_bytes);
+    BP_CUDA_TRY(cudaMemsetAsync(span_count, 0, sizeof(unsigned int), s));
     const size_t smem = sizeof(float4) * kBwdTileF4 + sizeof(uint32_t) * T;
     static bool attr = false;
     if (!attr) {
@@ -707,12 +747,13 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
     }
     k_embbag_bwd_tiles<<<(unsigned)tiles, 256, smem, s>>>(
         P->d_occ_pos, P->d_seg_of, P->d_seg_start, P->n_occ, q, T, reinterpret_cast<const float4*>(d_grad), d_occ_bag,
-        d_bag_scale, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts, (unsigned long long*)d_stats);
-    k_embbag_bwd_span<<<grid_for(tiles * 32, 256, kNumSMs * 8), 256, 0, s>>>(
-        P->d_seg_of, P->d_seg_start, P->n_occ, q, T, tiles, parts, d_values, row_stride, d_slots_s, d_dirty, opt, lr,
-        eps, (unsigned long long*)d_stats);
+        d_bag_scale, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts, (unsigned long long*)d_stats,
+        span_list, span_count);
+    k_embbag_bwd_span<<<kNumSMs * 2, 256, 0, s>>>(P->d_seg_of, P->d_seg_start, P->n_occ, q, T, span_list, span_count,
+                                                  parts, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps,
+                                                  (unsigned long long*)d_stats);
     BP_LAUNCH_CHECK();
-    cudaFreeAsync(parts, s);
+    cudaFreeAsync(scratch, s);
     return BP_OK;
   }
   const BagGrad bg{d_grad, d_occ_bag, d_bag_scale};
