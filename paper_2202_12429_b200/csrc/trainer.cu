@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
 
   {
     __shared__ uint4 win[kLongWindowChunks];
+    __shared__ uint32_t winfo[kLongWindowChunks];
     const long long n_vlong = d_num_long[0], n_long = n_vlong + d_num_long[1];
     const bool chain_lane = threadIdx.x < G;  // warp 0, lanes [0, G)
     // very long segments first (front of the list), then the others (back)
@@ -123,14 +124,41 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
       const uint32_t c0 = a >> 4, c_end = ((b - 1) >> 4) + 1;
       for (uint32_t wc = c0; wc < c_end; wc += kLongWindowChunks) {
         const uint32_t nchunk = min((uint32_t)kLongWindowChunks, c_end - wc);
-        for (uint32_t k = threadIdx.x; k < nchunk; k += blockDim.x) win[k] = chunks[wc + k];
+        // all warps stage the bytes and classify each chunk: info = 16-bit
+        // label mask | (1 << 16) when the chunk is a plain run (16 of this
+        // key's occurrences, labels 0/1, no rank change) -- so the chain warp
+        // does only select + add on those
+        for (uint32_t k = threadIdx.x; k < nchunk; k += blockDim.x) {
+          const uint4 w4 = chunks[wc + k];
+          win[k] = w4;
+          const uint32_t cbase = (wc + k) << 4;
+          const uint32_t word[4] = {w4.x, w4.y, w4.z, w4.w};
+          const uint32_t big = (w4.x | w4.y | w4.z | w4.w) & 0x7E7E7E7Eu;
+          const uint32_t flags_hi = (w4.y | w4.z | w4.w) & 0x80808080u;
+          const uint32_t flags_lo = w4.x & 0x80808080u;
+          const bool full = a <= cbase && b >= cbase + 16;
+          const bool plain = full && !big && !flags_hi && (flags_lo == 0 || (a == cbase && flags_lo == 0x80u));
+          uint32_t m = 0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) m |= ((word[i >> 2] >> ((i & 3) * 8)) & 1u) << i;
+          winfo[k] = m | (plain ? 0x10000u : 0u);
+        }
         __syncthreads();
         if (chain_lane) {
-          uint4 nxt4 = win[0];
-#pragma unroll 2
+          uint32_t nxt = winfo[0];
           for (uint32_t k = 0; k < nchunk; ++k) {
-            const uint4 w4 = nxt4;
-            if (k + 1 < nchunk) nxt4 = win[k + 1];  // next chunk's bytes in flight during this chain
+            const uint32_t info = nxt;
+            if (k + 1 < nchunk) nxt = winfo[k + 1];
+            if constexpr (DPL == 1) {
+              if (info & 0x10000u) {
+                float a0 = acc[0];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) a0 = __fadd_rn(a0, ((info >> i) & 1u) ? t1[0] : t0[0]);
+                acc[0] = a0;
+                continue;
+              }
+            }
+            const uint4 w4 = win[k];
             const uint32_t word[4] = {w4.x, w4.y, w4.z, w4.w};
             const uint32_t cbase = (wc + k) << 4;
             const uint32_t lo = a > cbase ? a - cbase : 0u;
