@@ -1,0 +1,108 @@
+"""Isolated timings of the hot kernels on one Criteo-Kaggle batch (no engine,
+no host-link traffic competing): CUDA events around R repetitions, L2
+flushed before each.
+
+  python tools/kernel_bench.py [--reps 20]
+
+prints one JSON line: per kernel family the mean microseconds per call.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2202_12429_b200 import _lib as L  # noqa: E402
+from paper_2202_12429_b200.device import DevicePrep  # noqa: E402
+
+
+def timed(fn, reps, flush):
+    times = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        times.append(a.elapsed_time(b) * 1e3)
+    return float(np.median(times))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    lib = L.lib()
+    sc = bench.schema()
+    batch = bench.make_batches(1, 1)[0]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    out = {}
+    dim = bench.DIM
+
+    # batch prep (columnar per-table sort + segments) from device-resident keys
+    keys, labels, _ = batch.packed_occurrences()
+    d_keys, d_labels = torch.from_numpy(keys).cuda(), torch.from_numpy(labels).cuda()
+    cols = (batch.num_examples, batch.table_ids())
+    rb = batch.rank_bounds(1)
+
+    def make_prep(flags=0):
+        return DevicePrep(keys, labels, rb, batch.iteration, sc, flags, d_keys=d_keys, d_labels=d_labels,
+                          columns=cols)
+
+    prep = make_prep()
+    keep = []
+    out["prep_columnar_us"] = timed(lambda: keep.append(make_prep()), args.reps, flush)
+    keep.clear()
+
+    u = prep.num_unique
+    rows = torch.randn((u, dim), dtype=torch.float32, device="cuda") * 0.05
+    row_index = torch.arange(u, dtype=torch.int32, device="cuda")
+    dirty = torch.zeros(u, dtype=torch.uint8, device="cuda")
+    ctx = L.Context.get().handle
+
+    def stub():
+        L.check(lib.bp_stub_step(ctx, prep.handle, L.ptr(rows), L.ptr(row_index), L.ptr(dirty), dim,
+                                 np.float32(0.01), np.float32(0.001), np.float32(0.01), 0, None, None, 0, None,
+                                 L.stream_ptr()), "bp_stub_step")
+
+    out["stub_step_us"] = timed(stub, args.reps, flush)
+
+    # EmbeddingBag forward / backward (DLRM prep: occurrence->unique maps)
+    prep2 = make_prep(2)
+    u2 = prep2.num_unique
+    values = torch.randn((u2, dim), dtype=torch.float32, device="cuda")
+    slots = torch.arange(u2, dtype=torch.int32, device="cuda")
+    n = prep2.n_occ
+    pooled = torch.empty((n, dim), dtype=torch.float32, device="cuda")
+    grad = torch.randn((n, dim), dtype=torch.float32, device="cuda") * 1e-3
+
+    def fwd():
+        L.check(lib.bp_embbag_forward(prep2.handle, L.ptr(values), dim, L.ptr(slots), dim, None, n, 0, None,
+                                      L.ptr(pooled), L.stream_ptr()), "fwd")
+
+    def bwd():
+        L.check(lib.bp_embbag_backward(prep2.handle, L.ptr(grad), None, None, L.ptr(values), dim, L.ptr(slots), None,
+                                       dim, 0, np.float32(0.01), np.float32(0.0), None, L.stream_ptr()), "bwd")
+
+    out["embbag_fwd_us"] = timed(fwd, args.reps, flush)
+    out["embbag_bwd_us"] = timed(bwd, args.reps, flush)
+    fwd_bytes = n * (8 * dim + 4)
+    bwd_bytes = n * (4 * dim + 4) + u2 * (8 * dim)
+    out["embbag_fwd_gbs"] = fwd_bytes / (out["embbag_fwd_us"] * 1e-6) / 1e9
+    out["embbag_bwd_gbs"] = bwd_bytes / (out["embbag_bwd_us"] * 1e-6) / 1e9
+    out["embbag_fwd_bwd_gbs"] = (fwd_bytes + bwd_bytes) / ((out["embbag_fwd_us"] + out["embbag_bwd_us"]) * 1e-6) / 1e9
+    out["n_occ"], out["unique"] = n, u
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
