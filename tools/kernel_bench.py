@@ -70,9 +70,9 @@ def main():
     ctx = L.Context.get().handle
 
     def stub():
-        L.check(lib.bp_stub_step(ctx, prep.handle, L.ptr(rows), L.ptr(row_index), L.ptr(dirty), dim,
-                                 np.float32(0.01), np.float32(0.001), np.float32(0.01), 0, None, None, 0, None,
-                                 L.stream_ptr()), "bp_stub_step")
+        f = float(np.float32(0.01))
+        L.check(lib.bp_stub_step(ctx, prep.handle, L.ptr(rows), L.ptr(row_index), L.ptr(dirty), dim, f,
+                                 float(np.float32(0.001)), f, 0, None, None, 0, None, L.stream_ptr()), "bp_stub_step")
 
     out["stub_step_us"] = timed(stub, args.reps, flush)
 
@@ -91,7 +91,7 @@ def main():
 
     def bwd():
         L.check(lib.bp_embbag_backward(prep2.handle, L.ptr(grad), None, None, L.ptr(values), dim, L.ptr(slots), None,
-                                       dim, 0, np.float32(0.01), np.float32(0.0), None, L.stream_ptr()), "bwd")
+                                       dim, 0, float(np.float32(0.01)), 0.0, None, L.stream_ptr()), "bwd")
 
     out["embbag_fwd_us"] = timed(fwd, args.reps, flush)
     out["embbag_bwd_us"] = timed(bwd, args.reps, flush)
