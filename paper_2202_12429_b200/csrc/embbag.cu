@@ -428,6 +428,22 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
     for (int j = 0; j < R; ++j)
       if (pk[j] >= 0) pk[j] = occ_bag[pk[j]];
   }
+  // which of this lane's rows end a key's run in the tile, and that key's
+  // slot / CSR bounds: loaded now, in flight with the gradient loads, and the
+  // cached row pulled into L2 -- the update after the scan then waits on L2
+  // instead of a chain of DRAM round trips
+  const uint32_t next_first = __shfl_down_sync(0xffffffffu, sg[0], 1);
+  bool endj[R];
+  int32_t slotj[R];
+  long long aj[R], bj[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    endj[j] = r0 + j < n &&
+              ((j < R - 1) ? sg[j + 1] != sg[j] : (lane == 31 || r0 + j + 1 >= n || next_first != sg[j]));
+    slotj[j] = endj[j] ? slots_s[sg[j]] : -1;
+    aj[j] = endj[j] ? (long long)seg_start[sg[j]] : 0;
+    bj[j] = endj[j] ? (long long)seg_start[sg[j] + 1] : 0;
+  }
   float4 v[R][Q];
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   if (src.rows) {  // gradient rows in the example owners' buffers (NVLink loads)
@@ -462,6 +478,10 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
                                 __fmul_rn(v[j][c].w, sc));
       }
   }
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (slotj[j] >= 0)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(values + (long long)slotj[j] * row_stride));
   // per-lane inclusive segmented sums
   bool inner_head = false;
 #pragma unroll
@@ -511,20 +531,17 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
         for (int c = 0; c < Q; ++c) v[j][c] = f4_add(carry[c], v[j][c]);
       }
   }
-  const uint32_t next_first = __shfl_down_sync(0xffffffffu, sg[0], 1);
   const uint32_t tile_first = __shfl_sync(0xffffffffu, sg[0], 0);
   const long long rows = min((long long)T, n - t0);
   const int dim = 4 * Q;
   unsigned n_nz = 0;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    if (r0 + j >= n) break;
-    const bool end = (j < R - 1) ? sg[j + 1] != sg[j] : (lane == 31 || r0 + j + 1 >= n || next_first != sg[j]);
-    if (!end) continue;
+    if (!endj[j]) continue;
     const uint32_t s = sg[j];
-    const int32_t slot = slots_s[s];
+    const int32_t slot = slotj[j];
     if (slot < 0) continue;
-    const long long a = seg_start[s], b = seg_start[s + 1];
+    const long long a = aj[j], b = bj[j];
     if (a >= t0 && b <= t0 + rows) {
       float* row = values + (long long)slot * row_stride;
       bool nz = false;
@@ -547,37 +564,34 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
   }
 }
 
-// Keys spanning several tiles: one warp per tile t; the warp of the key's
-// first tile (the key is t's last segment and starts inside t) sums the
-// per-tile partials -- lanes split (tile, float4) so all loads are in flight
-// at once, each lane accumulates its tiles in ascending order and a fixed
-// xor tree combines the lanes -- and applies the update.
+// Keys spanning several tiles (listed by the tile kernels at the key's first
+// tile): one CTA per key.  Threads split (tile, float4): each sums its tiles
+// in ascending order (four independent accumulators, combined in a fixed
+// order), then a fixed shared-memory tree over the tile lanes -- every order
+// is data-independent -- and the first tile lane applies the update.
 __global__ void __launch_bounds__(256) k_embbag_bwd_span(
     const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start, long long n, int q, int T,
     const uint32_t* __restrict__ span_list, const unsigned int* __restrict__ span_count,
     const float4* __restrict__ parts, float* __restrict__ values, int row_stride,
     const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
     unsigned long long* __restrict__ stats) {
-  const unsigned lane = threadIdx.x & 31u;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  int per = 1;  // tiles per pass: a power of two (the xor tree below), per * q <= 32
-  while (per * 2 * q <= 32) per *= 2;
-  const int c = (int)lane % q, tl = (int)lane / q;
+  __shared__ float4 red[256];
+  __shared__ int any_nz;
+  const int per = 256 / q;  // tile lanes (power of two: q in {1, 2, 4, 8, 16, 32})
+  const int c = threadIdx.x % q, tl = threadIdx.x / q;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   const long long n_span = *span_count;
-  for (long long li = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); li < n_span; li += warps) {
+  for (long long li = blockIdx.x; li < n_span; li += gridDim.x) {
     const long long t = span_list[li];
     const long long last = min((t + 1) * (long long)T, n) - 1;
     const uint32_t s = seg_of[last];
     const long long a = seg_start[s], b = seg_start[s + 1];
     const int32_t slot = slots_s[s];
-    if (slot < 0) continue;
-    const long long lt = (b - 1) / T, nt = lt - t + 1;
-    // four independent accumulators per lane (fixed assignment k % 4), so
-    // four partial loads are in flight; combined in a fixed order below
+    if (slot < 0) continue;  // block-uniform
+    const long long nt = (b - 1) / T - t + 1;
     float4 acc4[4] = {zero, zero, zero, zero};
     bool any4[4] = {false, false, false, false};
-    for (long long k0 = tl; tl < per && k0 < nt; k0 += 4 * per) {
+    for (long long k0 = tl; k0 < nt; k0 += 4 * per) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const long long k = k0 + (long long)u * per;
@@ -590,30 +604,23 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_span(
       }
     }
     float4 acc = acc4[0];
-    bool any = any4[0];
 #pragma unroll
     for (int u = 1; u < 4; ++u)
-      if (any4[u]) {
-        acc = any ? f4_add(acc, acc4[u]) : acc4[u];
-        any = true;
-      }
-    for (int off = per / 2; off > 0; off >>= 1) {  // fixed tree over the tile lanes
-      float4 o;
-      o.x = __shfl_down_sync(0xffffffffu, acc.x, off * q);
-      o.y = __shfl_down_sync(0xffffffffu, acc.y, off * q);
-      o.z = __shfl_down_sync(0xffffffffu, acc.z, off * q);
-      o.w = __shfl_down_sync(0xffffffffu, acc.w, off * q);
-      const bool oany = __shfl_down_sync(0xffffffffu, any ? 1 : 0, off * q) != 0;
-      if (tl < off && oany) acc = any ? f4_add(acc, o) : o;
-      any = any || (tl < off && oany);
+      if (any4[u]) acc = f4_add(acc, acc4[u]);  // any4[u] implies any4[0]
+    red[threadIdx.x] = any4[0] ? acc : zero;
+    if (threadIdx.x == 0) any_nz = 0;
+    __syncthreads();
+    for (int off = per / 2; off > 0; off >>= 1) {
+      if (tl < off) red[threadIdx.x] = f4_add(red[threadIdx.x], red[threadIdx.x + off * q]);
+      __syncthreads();
     }
-    bool nz = false;
-    if (tl == 0) nz = apply_row4(values + (long long)slot * row_stride, 4 * q, c, acc, opt, lr, eps);
-    const bool dirty_key = __ballot_sync(0xffffffffu, nz) != 0;
-    if (lane == 0 && dirty_key) {
+    if (tl == 0 && apply_row4(values + (long long)slot * row_stride, 4 * q, c, red[c], opt, lr, eps)) any_nz = 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && any_nz) {
       if (dirty) dirty[slot] = 1;
       if (stats) atomicAdd(&stats[1], 1ull);
     }
+    __syncthreads();
   }
 }
 
