@@ -101,6 +101,21 @@ def main():
     out["embbag_bwd_gbs"] = bwd_bytes / (out["embbag_bwd_us"] * 1e-6) / 1e9
     out["embbag_fwd_bwd_gbs"] = (fwd_bytes + bwd_bytes) / ((out["embbag_fwd_us"] + out["embbag_bwd_us"]) * 1e-6) / 1e9
     out["n_occ"], out["unique"] = n, u
+    # per-kernel device times (CUPTI) of one call each, L2 flushed first
+    from torch.profiler import ProfilerActivity, profile
+
+    kernels = {}
+    for fn in (stub, fwd, bwd):
+        flush.zero_()
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        for ev in prof.events():
+            if ev.device_type == torch.autograd.DeviceType.CUDA and "bp::" in (ev.name or ""):
+                name = ev.name.split("(")[0].replace("void ", "")
+                kernels[name] = round(kernels.get(name, 0.0) + ev.device_time, 2)
+    out["kernels_us"] = kernels
     print(json.dumps(out), flush=True)
 
 
