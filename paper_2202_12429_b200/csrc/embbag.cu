@@ -577,7 +577,8 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_span(
     unsigned long long* __restrict__ stats) {
   __shared__ float4 red[256];
   __shared__ int any_nz;
-  const int per = 256 / q;  // tile lanes (power of two: q in {1, 2, 4, 8, 16, 32})
+  int per = 1;  // tile lanes: the largest power of two with per * q <= 256 (others idle)
+  while (per * 2 * q <= 256) per *= 2;
   const int c = threadIdx.x % q, tl = threadIdx.x / q;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   const long long n_span = *span_count;
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_span(
     const long long nt = (b - 1) / T - t + 1;
     float4 acc4[4] = {zero, zero, zero, zero};
     bool any4[4] = {false, false, false, false};
-    for (long long k0 = tl; k0 < nt; k0 += 4 * per) {
+    for (long long k0 = tl; tl < per && k0 < nt; k0 += 4 * per) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const long long k = k0 + (long long)u * per;
