@@ -24,6 +24,8 @@
 namespace bp {
 
 constexpr int kBagLongBlocks = 128;
+constexpr int kSpanWarpTiles = 32;         // spanning keys up to this many tiles: a warp each
+constexpr int kSpanSmallBlocks = 148 * 2;  // CTAs of k_embbag_bwd_span on those (the rest: a CTA per key)
 
 // Single-key bags: pooled[p] = cached row of occurrence p's key, one 16-byte
 // lane per (occurrence, 4 components): coalesced pooled writes in occurrence
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_tiles(
     const float* __restrict__ bag_scale, float* __restrict__ values, int row_stride,
     const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
     float4* __restrict__ parts, unsigned long long* __restrict__ stats, uint32_t* __restrict__ span_list,
-    unsigned int* __restrict__ span_count) {
+    unsigned int* __restrict__ span_count, long long span_cap) {
   extern __shared__ float4 tile[];  // [T*q] gradient rows, then [T] segment ids
   uint32_t* seg = reinterpret_cast<uint32_t*>(tile + kBwdTileF4);
   __shared__ unsigned int n_dirty;
@@ -383,7 +385,10 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_tiles(
     } else {  // spans tiles: leave this tile's partial for k_embbag_bwd_span
       float4* dst = parts + ((long long)blockIdx.x * 2 + (s == seg[0] ? 0 : 1)) * q;
       for (int c = 0; c < q; ++c) dst[c] = tile[r * q + c];
-      if (a >= t0) span_list[atomicAdd(span_count, 1u)] = blockIdx.x;  // the key's first tile
+      if (a >= t0) {  // the key's first tile: list it for k_embbag_bwd_span
+        const bool big = (b - 1) / T - (long long)blockIdx.x + 1 > kSpanWarpTiles;
+        span_list[(big ? span_cap : 0) + atomicAdd(span_count + (big ? 1 : 0), 1u)] = blockIdx.x;
+      }
     }
     if (nz) {
       if (dirty) dirty[slot] = 1;
@@ -408,7 +413,7 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
     const float* __restrict__ bag_scale, float* __restrict__ values, int row_stride,
     const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
     float4* __restrict__ parts, unsigned long long* __restrict__ stats, PeerSrc src,
-    uint32_t* __restrict__ span_list, unsigned int* __restrict__ span_count) {
+    uint32_t* __restrict__ span_list, unsigned int* __restrict__ span_count, long long span_cap) {
   constexpr int R = 8 / Q, T = 32 * R;
   const unsigned lane = threadIdx.x & 31u;
   const long long tile = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -555,7 +560,10 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
       float4* dst = parts + (tile * 2 + (s == tile_first ? 0 : 1)) * Q;
 #pragma unroll
       for (int c = 0; c < Q; ++c) dst[c] = v[j][c];
-      if (a >= t0) span_list[atomicAdd(span_count, 1u)] = (uint32_t)tile;  // the key's first tile
+      if (a >= t0) {  // the key's first tile: list it for k_embbag_bwd_span
+        const bool big = (b - 1) / T - tile + 1 > kSpanWarpTiles;
+        span_list[(big ? span_cap : 0) + atomicAdd(span_count + (big ? 1 : 0), 1u)] = (uint32_t)tile;
+      }
     }
   }
   if (stats) {
@@ -564,51 +572,99 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
   }
 }
 
-// Keys spanning several tiles (listed by the tile kernels at the key's first
-// tile): one CTA per key.  Threads split (tile, float4): each sums its tiles
-// in ascending order (four independent accumulators, combined in a fixed
-// order), then a fixed shared-memory tree over the tile lanes -- every order
-// is data-independent -- and the first tile lane applies the update.
+// Keys spanning several tiles, listed by the tile kernels at the key's first
+// tile: up to kSpanWarpTiles tiles (the many keys that merely cross a tile
+// boundary) one warp per key, longer ones (the Zipf-hot rows) one CTA per
+// key.  Lanes / threads split (tile, float4): each sums its tiles in
+// ascending order (four independent accumulators, combined in a fixed
+// order), then a fixed xor-shuffle or shared-memory tree over the tile lanes
+// -- every order is data-independent -- and the first tile lane applies the
+// update.
+
+__device__ __forceinline__ void span_sum(const float4* __restrict__ parts, long long t, long long nt, long long a,
+                                         int T, int q, int c, int tl, int per, float4& acc, bool& any) {
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc4[4] = {zero, zero, zero, zero};
+  bool any4[4] = {false, false, false, false};
+  for (long long k0 = tl; tl < per && k0 < nt; k0 += 4 * per) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long k = k0 + (long long)u * per;
+      if (k < nt) {
+        const int half = (k == 0 && a != t * T) ? 1 : 0;
+        const float4 x = __ldcg(parts + ((t + k) * 2 + half) * q + c);
+        acc4[u] = any4[u] ? f4_add(acc4[u], x) : x;
+        any4[u] = true;
+      }
+    }
+  }
+  acc = acc4[0];
+#pragma unroll
+  for (int u = 1; u < 4; ++u)
+    if (any4[u]) acc = f4_add(acc, acc4[u]);  // any4[u] implies any4[0]
+  any = any4[0];
+}
+
 __global__ void __launch_bounds__(256) k_embbag_bwd_span(
     const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start, long long n, int q, int T,
-    const uint32_t* __restrict__ span_list, const unsigned int* __restrict__ span_count,
+    const uint32_t* __restrict__ small_list, const unsigned int* __restrict__ small_count,
+    const uint32_t* __restrict__ big_list, const unsigned int* __restrict__ big_count,
     const float4* __restrict__ parts, float* __restrict__ values, int row_stride,
     const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty, int opt, float lr, float eps,
     unsigned long long* __restrict__ stats) {
   __shared__ float4 red[256];
   __shared__ int any_nz;
-  int per = 1;  // tile lanes: the largest power of two with per * q <= 256 (others idle)
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (blockIdx.x < kSpanSmallBlocks) {  // warp per key
+    const unsigned lane = threadIdx.x & 31u;
+    int per = 1;
+    while (per * 2 * q <= 32) per *= 2;
+    const int c = (int)lane % q, tl = (int)lane / q;
+    const long long warps = (long long)kSpanSmallBlocks * (blockDim.x >> 5);
+    const long long n_span = *small_count;
+    for (long long li = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); li < n_span; li += warps) {
+      const long long t = small_list[li];
+      const long long last = min((t + 1) * (long long)T, n) - 1;
+      const uint32_t s = seg_of[last];
+      const long long a = seg_start[s], b = seg_start[s + 1];
+      const int32_t slot = slots_s[s];
+      if (slot < 0) continue;  // warp-uniform
+      float4 acc;
+      bool any;
+      span_sum(parts, t, (b - 1) / T - t + 1, a, T, q, c, tl, per, acc, any);
+      if (!any) acc = zero;
+      for (int off = per / 2; off > 0; off >>= 1) {
+        float4 o;
+        o.x = __shfl_down_sync(0xffffffffu, acc.x, off * q);
+        o.y = __shfl_down_sync(0xffffffffu, acc.y, off * q);
+        o.z = __shfl_down_sync(0xffffffffu, acc.z, off * q);
+        o.w = __shfl_down_sync(0xffffffffu, acc.w, off * q);
+        if (tl < off) acc = f4_add(acc, o);
+      }
+      bool nz = false;
+      if (tl == 0) nz = apply_row4(values + (long long)slot * row_stride, 4 * q, c, acc, opt, lr, eps);
+      if (__ballot_sync(0xffffffffu, nz) != 0 && lane == 0) {
+        if (dirty) dirty[slot] = 1;
+        if (stats) atomicAdd(&stats[1], 1ull);
+      }
+    }
+    return;
+  }
+  int per = 1;  // CTA per key: the largest power of two with per * q <= 256 (others idle)
   while (per * 2 * q <= 256) per *= 2;
   const int c = threadIdx.x % q, tl = threadIdx.x / q;
-  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-  const long long n_span = *span_count;
-  for (long long li = blockIdx.x; li < n_span; li += gridDim.x) {
-    const long long t = span_list[li];
+  const long long n_span = *big_count;
+  for (long long li = blockIdx.x - kSpanSmallBlocks; li < n_span; li += gridDim.x - kSpanSmallBlocks) {
+    const long long t = big_list[li];
     const long long last = min((t + 1) * (long long)T, n) - 1;
     const uint32_t s = seg_of[last];
     const long long a = seg_start[s], b = seg_start[s + 1];
     const int32_t slot = slots_s[s];
     if (slot < 0) continue;  // block-uniform
-    const long long nt = (b - 1) / T - t + 1;
-    float4 acc4[4] = {zero, zero, zero, zero};
-    bool any4[4] = {false, false, false, false};
-    for (long long k0 = tl; tl < per && k0 < nt; k0 += 4 * per) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long long k = k0 + (long long)u * per;
-        if (k < nt) {
-          const int half = (k == 0 && a != t * T) ? 1 : 0;
-          const float4 x = __ldcg(parts + ((t + k) * 2 + half) * q + c);
-          acc4[u] = any4[u] ? f4_add(acc4[u], x) : x;
-          any4[u] = true;
-        }
-      }
-    }
-    float4 acc = acc4[0];
-#pragma unroll
-    for (int u = 1; u < 4; ++u)
-      if (any4[u]) acc = f4_add(acc, acc4[u]);  // any4[u] implies any4[0]
-    red[threadIdx.x] = any4[0] ? acc : zero;
+    float4 acc;
+    bool any;
+    span_sum(parts, t, (b - 1) / T - t + 1, a, T, q, c, tl, per, acc, any);
+    red[threadIdx.x] = any ? acc : zero;
     if (threadIdx.x == 0) any_nz = 0;
     __syncthreads();
     for (int off = per / 2; off > 0; off >>= 1) {
@@ -708,19 +764,19 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
     const PeerSrc psrc = peer_src ? *peer_src : PeerSrc{nullptr, nullptr, 1, 1, 1, 1.f};
     // one allocation: tile partials, the spanning-key list and its count
     const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
-    const size_t list_bytes = ((size_t)tiles * sizeof(uint32_t) + 255) & ~size_t(255);
+    const size_t list_bytes = ((size_t)2 * tiles * sizeof(uint32_t) + 255) & ~size_t(255);
     char* scratch = nullptr;
     BP_CUDA_TRY(pool_alloc(&scratch, parts_bytes + list_bytes + 256, s));
     float4* parts = reinterpret_cast<float4*>(scratch);
     uint32_t* span_list = reinterpret_cast<uint32_t*>(scratch + parts_bytes);
     unsigned int* span_count = reinterpret_cast<unsigned int*>(scratch + parts_bytes + list_bytes);
-    BP_CUDA_TRY(cudaMemsetAsync(span_count, 0, sizeof(unsigned int), s));
+    BP_CUDA_TRY(cudaMemsetAsync(span_count, 0, 2 * sizeof(unsigned int), s));
     const unsigned blocks = (unsigned)((tiles + 7) / 8);
 #define BP_BWD_WARP(QQ)                                                                                        \
   k_embbag_bwd_warp<QQ><<<blocks, 256, 0, s>>>(P->d_occ_pos, P->d_seg_of, P->d_seg_start, P->n_occ,              \
                                                reinterpret_cast<const float4*>(d_grad), d_occ_bag, d_bag_scale,  \
                                                d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts,    \
-                                               (unsigned long long*)d_stats, psrc, span_list, span_count)
+                                               (unsigned long long*)d_stats, psrc, span_list, span_count, tiles)
     switch (q) {
       case 1: BP_BWD_WARP(1); break;
       case 2: BP_BWD_WARP(2); break;
@@ -728,9 +784,9 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
       default: BP_BWD_WARP(8); break;
     }
 #undef BP_BWD_WARP
-    k_embbag_bwd_span<<<kNumSMs * 2, 256, 0, s>>>(P->d_seg_of, P->d_seg_start, P->n_occ, q, T, span_list, span_count,
-                                                  parts, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps,
-                                                  (unsigned long long*)d_stats);
+    k_embbag_bwd_span<<<kSpanSmallBlocks + kNumSMs, 256, 0, s>>>(
+        P->d_seg_of, P->d_seg_start, P->n_occ, q, T, span_list, span_count, span_list + tiles, span_count + 1, parts,
+        d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, (unsigned long long*)d_stats);
     BP_LAUNCH_CHECK();
     cudaFreeAsync(scratch, s);
     return BP_OK;
@@ -740,13 +796,13 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
     const int q = dim / 4, T = kBwdTileF4 / q;
     const long long tiles = (P->n_occ + T - 1) / T;
     const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
-    const size_t list_bytes = ((size_t)tiles * sizeof(uint32_t) + 255) & ~size_t(255);
+    const size_t list_bytes = ((size_t)2 * tiles * sizeof(uint32_t) + 255) & ~size_t(255);
     char* scratch = nullptr;
     BP_CUDA_TRY(pool_alloc(&scratch, parts_bytes + list_bytes + 256, s));
     float4* parts = reinterpret_cast<float4*>(scratch);
     uint32_t* span_list = reinterpret_cast<uint32_t*>(scratch + parts_bytes);
     unsigned int* span_count = reinterpret_cast<unsigned int*>(scratch + parts_bytes + list_bytes);
-    BP_CUDA_TRY(cudaMemsetAsync(span_count, 0, sizeof(unsigned int), s));
+    BP_CUDA_TRY(cudaMemsetAsync(span_count, 0, 2 * sizeof(unsigned int), s));
     const size_t smem = sizeof(float4) * kBwdTileF4 + sizeof(uint32_t) * T;
     static bool attr = false;
     if (!attr) {
@@ -756,10 +812,10 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
     k_embbag_bwd_tiles<<<(unsigned)tiles, 256, smem, s>>>(
         P->d_occ_pos, P->d_seg_of, P->d_seg_start, P->n_occ, q, T, reinterpret_cast<const float4*>(d_grad), d_occ_bag,
         d_bag_scale, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts, (unsigned long long*)d_stats,
-        span_list, span_count);
-    k_embbag_bwd_span<<<kNumSMs * 2, 256, 0, s>>>(P->d_seg_of, P->d_seg_start, P->n_occ, q, T, span_list, span_count,
-                                                  parts, d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps,
-                                                  (unsigned long long*)d_stats);
+        span_list, span_count, tiles);
+    k_embbag_bwd_span<<<kSpanSmallBlocks + kNumSMs, 256, 0, s>>>(
+        P->d_seg_of, P->d_seg_start, P->n_occ, q, T, span_list, span_count, span_list + tiles, span_count + 1, parts,
+        d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, (unsigned long long*)d_stats);
     BP_LAUNCH_CHECK();
     cudaFreeAsync(scratch, s);
     return BP_OK;

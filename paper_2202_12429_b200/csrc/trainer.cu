@@ -74,6 +74,10 @@ __device__ __forceinline__ void chain_chunk(const uint32_t (&word)[4], uint32_t 
 }
 
 constexpr int kLongBlocks = 148;       // CTAs of the long-segment launch (one per SM)
+// Unused dynamic shared memory that keeps the long-segment CTAs one per SM:
+// the block scheduler would otherwise pack several 128-thread CTAs onto one
+// SM and their chain warps would share issue slots.
+constexpr int kLongSmemPad = 120 << 10;
 constexpr int kLongWindowChunks = 1024;  // 16 KB of occurrence bytes staged in smem
 
 // Fused trainer, two launches.  k_stub_step_long (first) takes the keys whose
@@ -378,6 +382,15 @@ extern "C" int bp_mark_ids(bp_prep* P, int64_t* d_mark, int64_t tag, bp_stream_t
   return BP_OK;
 }
 
+template <int G, int DPL>
+static void long_attr() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(bp::k_stub_step_long<G, DPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bp::kLongSmemPad);
+    done = true;
+  }
+}
+
 extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_t* d_row_index, uint8_t* d_dirty,
                             int32_t dim, float c_value, float c_label, float lr, int32_t mode, float* d_grad_out,
                             const int64_t* d_next_mark, int64_t next_tag, int64_t* d_stats, bp_stream_t stream) {
@@ -392,7 +405,7 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   const int threads = 256;
   const int blocks = grid_for(groups * G, threads, kNumSMs * 6);
   BP_DISPATCH_GD(G, dpl,
-                 (k_stub_step_long<g_, d_><<<kLongBlocks, 128, 0, s>>>(
+                 (long_attr<g_, d_>(), k_stub_step_long<g_, d_><<<kLongBlocks, 128, kLongSmemPad, s>>>(
                      P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,
                      d_row_index, d_dirty, dim, c_value, c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark,
                      next_tag, (unsigned long long*)d_stats)));
