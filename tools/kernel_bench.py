@@ -75,6 +75,21 @@ def main():
                                  float(np.float32(0.001)), f, 0, None, None, 0, None, L.stream_ptr()), "bp_stub_step")
 
     out["stub_step_us"] = timed(stub, args.reps, flush)
+    # phase clocks of the long-segment kernel's CTAs (the hottest chain)
+    trace = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+    L.check(lib.bp_debug_long_trace(L.ptr(trace)), "bp_debug_long_trace")
+    flush.zero_()
+    stub()
+    torch.cuda.synchronize()
+    L.check(lib.bp_debug_long_trace(None), "bp_debug_long_trace")
+    tr = trace.view(148, 8).cpu().numpy()
+    hot = int(np.argmax(tr[:, 5]))
+    t = tr[hot]
+    out["long_hot_cta"] = {"occurrences": int(t[5]), "setup_cyc": int(t[1] - t[0]), "window_cyc": int(t[2] - t[1]),
+                           "chain_cyc": int(t[3] - t[2]), "tail_cyc": int(t[4] - t[3]),
+                           "cta_total_cyc": int(t[4] - t[0])}
+    starts = tr[:, 0]
+    out["long_cta_start_spread_cyc"] = int(starts.max() - starts.min())
 
     # EmbeddingBag forward / backward (DLRM prep: occurrence->unique maps)
     prep2 = make_prep(2)
