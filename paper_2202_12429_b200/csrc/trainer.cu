@@ -74,14 +74,14 @@ __device__ __forceinline__ void chain_chunk(const uint32_t (&word)[4], uint32_t 
 }
 
 constexpr int kLongBlocks = 148;       // CTAs of the long-segment launch (one per SM)
-// Optional per-CTA phase timestamps of k_stub_step_long (tools/kernel_bench.py
-// --trace; nullptr in production): [cta][8] = start, setup, window staged,
-// chain done, end, segment length.
+// Optional per-CTA phase timestamps of k_stub_step_long (tools/kernel_bench.py;
+// nullptr in production): [cta][8] = start, setup, window staged, chain
+// done, end, segment length.
 __device__ unsigned long long* g_long_trace = nullptr;
-// Dynamic shared memory of the long kernel (its per-occurrence value
-// buffers); its size also keeps the long-segment CTAs one per SM.
-constexpr int kLongPhase = 32;  // chunks per producer/consumer phase of the long kernel
-constexpr int kLongSmemPad = 2 * kLongPhase * 16 * 32 * 4;  // the value buffers (128 KB)
+// Unused dynamic shared memory that keeps the long-segment CTAs one per SM:
+// the block scheduler would otherwise pack several 128-thread CTAs onto one
+// SM and their chain warps would share issue slots.
+constexpr int kLongSmemPad = 120 << 10;
 constexpr int kLongWindowChunks = 1024;  // 16 KB of occurrence bytes staged in smem
 
 // Fused trainer, two launches.  k_stub_step_long (first) takes the keys whose
@@ -110,8 +110,6 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
   {
     __shared__ uint4 win[kLongWindowChunks];
     __shared__ uint32_t winfo[kLongWindowChunks];
-    __shared__ float st0[32], st1[32];
-    extern __shared__ float long_dyn[];  // [2][kLongPhase][16][G] (DPL == 1)
     const long long n_vlong = d_num_long[0], n_long = n_vlong + d_num_long[1];
     const bool chain_lane = threadIdx.x < G;  // warp 0, lanes [0, G)
     // very long segments first (front of the list), then the others (back)
@@ -159,71 +157,31 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
         }
         __syncthreads();
         if (tr && threadIdx.x == 0) tr[2] = clock64();
-        if constexpr (DPL == 1) {
-          // Producer/consumer over phases of kLongPhase chunks: warps 1..3
-          // expand the label masks of phase p into the per-occurrence values
-          // vals[p & 1][chunk][occ][lane] (t0 or t1 of each component) while
-          // the chain lanes run phase p - 1 as shared-memory loads + adds, so
-          // the dependent add chain carries no select work (7.7 -> ~4.5
-          // cycles per occurrence, tools/mb/chain.cu).
-          float* vals = long_dyn;
-          if (chain_lane) {
-            st0[threadIdx.x] = t0[0];
-            st1[threadIdx.x] = t1[0];
-          }
-          __syncthreads();
-          const uint32_t nph = (nchunk + kLongPhase - 1) / kLongPhase;
-          for (uint32_t p = 0; p <= nph; ++p) {
-            if (threadIdx.x >= 32 && p < nph) {
-              float* dst = vals + (p & 1) * (kLongPhase * 16 * G);
-              const uint32_t k0 = p * kLongPhase, kn = min((uint32_t)kLongPhase, nchunk - k0);
-              for (uint32_t e = threadIdx.x - 32; e < kn * 16 * G; e += blockDim.x - 32) {
-                const uint32_t kk = e / (16 * G), rem = e - kk * (16 * G), i = rem / G, d = rem - i * G;
-                dst[e] = ((winfo[k0 + kk] >> i) & 1u) ? st1[d] : st0[d];
+        if (chain_lane) {
+          uint32_t nxt = winfo[0];
+          for (uint32_t k = 0; k < nchunk; ++k) {
+            const uint32_t info = nxt;
+            if (k + 1 < nchunk) nxt = winfo[k + 1];
+            if constexpr (DPL == 1) {
+              if (info & 0x10000u) {
+                float a0 = acc[0];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) a0 = __fadd_rn(a0, ((info >> i) & 1u) ? t1[0] : t0[0]);
+                acc[0] = a0;
+                continue;
               }
             }
-            if (p > 0 && chain_lane) {
-              const float* srcv = vals + ((p - 1) & 1) * (kLongPhase * 16 * G) + threadIdx.x;
-              const uint32_t k0 = (p - 1) * kLongPhase, kn = min((uint32_t)kLongPhase, nchunk - k0);
-              for (uint32_t kk = 0; kk < kn; ++kk) {
-                const uint32_t k = k0 + kk;
-                if (winfo[k] & 0x10000u) {
-                  const float* vp = srcv + kk * (16 * G);
-                  float x[16];
-#pragma unroll
-                  for (int i = 0; i < 16; ++i) x[i] = vp[i * G];
-                  float a0 = acc[0];
-#pragma unroll
-                  for (int i = 0; i < 16; ++i) a0 = __fadd_rn(a0, x[i]);
-                  acc[0] = a0;
-                  continue;
-                }
-                const uint4 w4 = win[k];
-                const uint32_t word[4] = {w4.x, w4.y, w4.z, w4.w};
-                const uint32_t cbase = (wc + k) << 4;
-                const uint32_t lo = a > cbase ? a - cbase : 0u;
-                const uint32_t hi = b - cbase < 16u ? b - cbase : 16u;
-                const uint32_t first_q = (a >= cbase && a < cbase + 16) ? a - cbase : 16u;
-                chain_chunk<DPL>(word, lo, hi, first_q, acc, comb, t0, t1, sc, c_label);
-              }
-            }
-            __syncthreads();
+            const uint4 w4 = win[k];
+            const uint32_t word[4] = {w4.x, w4.y, w4.z, w4.w};
+            const uint32_t cbase = (wc + k) << 4;
+            const uint32_t lo = a > cbase ? a - cbase : 0u;
+            const uint32_t hi = b - cbase < 16u ? b - cbase : 16u;
+            const uint32_t first_q = (a >= cbase && a < cbase + 16) ? a - cbase : 16u;
+            chain_chunk<DPL>(word, lo, hi, first_q, acc, comb, t0, t1, sc, c_label);
           }
           if (tr && threadIdx.x == 0) tr[3] = clock64() + 0 * (unsigned long long)__float_as_uint(acc[0]);
-        } else {
-          if (chain_lane) {
-            for (uint32_t k = 0; k < nchunk; ++k) {
-              const uint4 w4 = win[k];
-              const uint32_t word[4] = {w4.x, w4.y, w4.z, w4.w};
-              const uint32_t cbase = (wc + k) << 4;
-              const uint32_t lo = a > cbase ? a - cbase : 0u;
-              const uint32_t hi = b - cbase < 16u ? b - cbase : 16u;
-              const uint32_t first_q = (a >= cbase && a < cbase + 16) ? a - cbase : 16u;
-              chain_chunk<DPL>(word, lo, hi, first_q, acc, comb, t0, t1, sc, c_label);
-            }
-          }
-          __syncthreads();
         }
+        __syncthreads();
       }
       if (threadIdx.x < 32) {
         bool nonzero = false;
