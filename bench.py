@@ -378,9 +378,19 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
                          "ms_per_step": spans[0] / steps, "launches_per_step": 2, "unit": "GB/s",
                          "achieved": (fwd_bytes + bwd_bytes(n_occ, int(u_mean))) / (spans[0] / steps * 1e-3) / 1e9
                          if spans[0] else 0.0,
-                         "traffic": None,
+                         "traffic": _traffic(),
                          "note": "SURVEY 8(d) algorithmic bytes: forward N_occ*(64 row read + 64 pooled write + 4 "
                                  "index) + backward N_occ*(64 gradient read + 4 index) + U*(64 read + 64 write)"}}
+
+
+def _traffic():
+    """DRAM bytes (read + write) per step of the EmbeddingBag kernels from the
+    committed ncu --set full capture (profiles/round1/traffic.json)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "round1", "traffic.json")))[
+            "embbag_fwd_bwd_dram_bytes_per_step"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def bwd_bytes(n_occ: int, u: int) -> int:
