@@ -73,6 +73,9 @@ constexpr int kIlp = 4;
 // more SMs whose L1/LSU queues are not clogged by microsecond-latency host
 // accesses (co-resident compute kernels stall behind them).
 static int g_link_blocks = 32;
+// Debug only (tools/profile_step.py --skip-link): store fetch/write kernels
+// become no-ops, to measure what the host-link traffic costs the step.
+static int g_skip_link = 0;
 // Threads per link block and dynamic shared memory requested (unused; > 0
 // makes a link block own its SM so no compute CTA shares it with the PCIe
 // traffic -- measured no better on the bench step, so off by default).
@@ -214,7 +217,7 @@ extern "C" uint8_t* bp_store_written_bitmap(bp_store* st) { return (uint8_t*)st-
 extern "C" int bp_store_fetch(bp_store* st, const uint32_t* d_ids, int64_t n, const int64_t* d_n, float* d_out,
                               bp_stream_t stream) {
   using namespace bp;
-  if (n <= 0) return BP_OK;
+  if (n <= 0 || g_skip_link) return BP_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int dim = st->dim;
   if ((dim & 3) == 0) {
@@ -247,7 +250,7 @@ extern "C" int bp_store_write(bp_store* st, const uint32_t* d_ids, const float* 
 extern "C" int bp_store_write_masked(bp_store* st, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_mask,
                                      int64_t n, const int64_t* d_n, bp_stream_t stream) {
   using namespace bp;
-  if (n <= 0) return BP_OK;
+  if (n <= 0 || g_skip_link) return BP_OK;
   const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
   BP_CUDA_TRY(link_attrs());
   k_store_write<<<grid_for(n * q, g_link_threads * kIlp, g_link_blocks), g_link_threads, g_link_smem,
@@ -279,5 +282,10 @@ extern "C" int bp_set_link_config(int32_t blocks, int32_t threads, int32_t smem_
   bp::g_link_blocks = blocks;
   bp::g_link_threads = threads;
   bp::g_link_smem = smem_bytes;
+  return BP_OK;
+}
+
+extern "C" int bp_debug_skip_link(int32_t skip) {
+  bp::g_skip_link = skip;
   return BP_OK;
 }
