@@ -495,8 +495,8 @@ int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const float* d_em
 /* Debug: per-CTA phase clock64() stamps of the long-segment trainer kernel
  * into d_buf[148][8] (NULL disables; tools/kernel_bench.py --trace). */
 int bp_debug_long_trace(void* d_buf);
-/* Debug: 1 turns the store's fetch/write kernels into no-ops (results become
- * wrong; only for measuring the host link's share of a step). */
+/* Debug: bit 0 turns the store's fetch kernels, bit 1 its write kernels into
+ * no-ops (results become wrong; only for measuring the host link's share). */
 int bp_debug_skip_link(int32_t skip);
 /* Launch shape of the host-link (zero-copy fetch / write-back) kernels:
  * blocks (default 32), threads per block (256) and unused dynamic shared

@@ -217,7 +217,7 @@ extern "C" uint8_t* bp_store_written_bitmap(bp_store* st) { return (uint8_t*)st-
 extern "C" int bp_store_fetch(bp_store* st, const uint32_t* d_ids, int64_t n, const int64_t* d_n, float* d_out,
                               bp_stream_t stream) {
   using namespace bp;
-  if (n <= 0 || g_skip_link) return BP_OK;
+  if (n <= 0 || (g_skip_link & 1)) return BP_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int dim = st->dim;
   if ((dim & 3) == 0) {
@@ -250,7 +250,7 @@ extern "C" int bp_store_write(bp_store* st, const uint32_t* d_ids, const float* 
 extern "C" int bp_store_write_masked(bp_store* st, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_mask,
                                      int64_t n, const int64_t* d_n, bp_stream_t stream) {
   using namespace bp;
-  if (n <= 0 || g_skip_link) return BP_OK;
+  if (n <= 0 || (g_skip_link & 2)) return BP_OK;
   const int q = (st->dim & 3) == 0 ? st->dim / 4 : st->dim;
   BP_CUDA_TRY(link_attrs());
   k_store_write<<<grid_for(n * q, g_link_threads * kIlp, g_link_blocks), g_link_threads, g_link_smem,

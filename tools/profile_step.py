@@ -35,13 +35,14 @@ def main():
     ap.add_argument("--sync-flush", action="store_true", help="drain all engine streams before each flush")
     ap.add_argument("--link-blocks", type=int, default=0, help="grid of the host-link kernels (0: default)")
     ap.add_argument("--link-config", default="", help="blocks,threads,smem of the host-link kernels")
-    ap.add_argument("--skip-link", action="store_true", help="debug: no host-link kernels (wrong results)")
+    ap.add_argument("--skip-link", type=int, default=0,
+                    help="debug: 1 = no fetch kernels, 2 = no write-back kernels, 3 = neither (wrong results)")
     ap.add_argument("--dlrm", action="store_true", help="DLRM mode (EmbeddingBag + MLP graph) instead of the stub")
     args = ap.parse_args()
     if args.skip_link:
         from paper_2202_12429_b200 import _lib as L
 
-        L.check(L.lib().bp_debug_skip_link(1), "bp_debug_skip_link")
+        L.check(L.lib().bp_debug_skip_link(args.skip_link), "bp_debug_skip_link")
     if args.link_config:
         from paper_2202_12429_b200 import _lib as L
 
