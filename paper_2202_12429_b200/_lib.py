@@ -170,6 +170,7 @@ _SIGS = {
     "bp_engine_sync": (c_i32, [c_vp]),
     "bp_debug_long_trace": (c_i32, [c_vp]),
     "bp_debug_skip_link": (c_i32, [c_i32]),
+    "bp_debug_link_cb_stats": (c_i32, [c_vp]),
     "bp_ipc_alloc": (c_i32, [c_i64, P(c_vp), c_vp]),
     "bp_ipc_open": (c_i32, [c_vp, P(c_vp)]),
     "bp_ipc_close": (c_i32, [c_vp]),

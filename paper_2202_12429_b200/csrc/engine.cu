@@ -26,6 +26,7 @@
 #include "internal.cuh"
 #include "hostpool.h"
 
+#include <atomic>
 #include <chrono>
 
 struct bp_store;
@@ -113,8 +114,23 @@ struct LinkJob {
   size_t row_bytes;
 };
 
+// Debug counters of the host-link callbacks (bp_debug_link_cb_stats).
+static std::atomic<long long> g_cb_ns[2], g_cb_calls[2], g_cb_rows[2];
+
+struct CbTimer {
+  int k;
+  long long n;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  ~CbTimer() {
+    g_cb_ns[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    g_cb_calls[k] += 1;
+    g_cb_rows[k] += n;
+  }
+};
+
 static void CUDART_CB link_gather_cb(void* p) {
   const LinkJob* j = static_cast<const LinkJob*>(p);
+  CbTimer timer{0, j->n};
   const size_t rb = j->row_bytes;
   const char* table = reinterpret_cast<const char*>(j->table_src);
   char* out = reinterpret_cast<char*>(j->rows_dst);
@@ -128,6 +144,7 @@ static void CUDART_CB link_gather_cb(void* p) {
 
 static void CUDART_CB link_scatter_cb(void* p) {
   const LinkJob* j = static_cast<const LinkJob*>(p);
+  CbTimer timer{1, j->n};
   const size_t rb = j->row_bytes;
   char* table = reinterpret_cast<char*>(j->table_dst);
   const char* in = reinterpret_cast<const char*>(j->rows_src);
@@ -978,5 +995,16 @@ extern "C" int bp_host_rows_bench(float* table, int32_t dim, const uint32_t* ids
   if (op == 0) bp::link_gather_cb(&j);
   else bp::link_scatter_cb(&j);
   *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return BP_OK;
+}
+
+// Debug: {gather ns, calls, rows, scatter ns, calls, rows} of the DMA link
+// mode's host callbacks since the last call (reset).
+extern "C" int bp_debug_link_cb_stats(int64_t* out6) {
+  for (int k = 0; k < 2; ++k) {
+    out6[3 * k] = bp::g_cb_ns[k].exchange(0);
+    out6[3 * k + 1] = bp::g_cb_calls[k].exchange(0);
+    out6[3 * k + 2] = bp::g_cb_rows[k].exchange(0);
+  }
   return BP_OK;
 }
