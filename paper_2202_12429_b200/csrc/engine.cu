@@ -26,6 +26,9 @@
 #include "internal.cuh"
 #include "hostpool.h"
 
+#include <cuda.h>
+#include <thread>
+
 #include <atomic>
 #include <chrono>
 
@@ -156,6 +159,88 @@ static void CUDART_CB link_scatter_cb(void* p) {
   });
 }
 
+// Host worker for the DMA link mode, driven by stream memory operations
+// instead of cudaLaunchHostFunc (whose callbacks serialise with the
+// launching thread's CUDA calls): the link stream writes the job's sequence
+// number into pinned memory (cuStreamWriteValue32) and then waits
+// (cuStreamWaitValue32 >=) until this thread, which polls that word, has run
+// the job's gather/scatter on the pool and published the same number.
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct LinkWorker {
+  static constexpr int kRing = 256;
+  HostPool pool;
+  std::vector<LinkJob> jobs = std::vector<LinkJob>(kRing);
+  volatile uint32_t* flags = nullptr;  // pinned, mapped: [0] ready (GPU writes), [32] done (CPU writes)
+  CUdeviceptr d_ready = 0, d_done = 0;
+  uint32_t issued = 0;  // host-enqueued jobs
+  std::atomic<bool> stop{false};
+  std::thread thr;
+  WriteValueFn write_value = nullptr;
+  WaitValueFn wait_value = nullptr;
+
+  explicit LinkWorker(int threads) : pool(threads) {}
+
+  cudaError_t init() {
+    cudaError_t e = cudaHostAlloc((void**)&flags, 256, cudaHostAllocMapped);
+    if (e != cudaSuccess) return e;
+    flags[0] = 0;
+    flags[32] = 0;
+    void* d = nullptr;
+    e = cudaHostGetDevicePointer(&d, (void*)flags, 0);
+    if (e != cudaSuccess) return e;
+    d_ready = (CUdeviceptr)d;
+    d_done = (CUdeviceptr)((char*)d + 128);
+    cudaDriverEntryPointQueryResult q;
+    e = cudaGetDriverEntryPoint("cuStreamWriteValue32", (void**)&write_value, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !write_value) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    e = cudaGetDriverEntryPoint("cuStreamWaitValue32", (void**)&wait_value, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !wait_value) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    thr = std::thread([this] { loop(); });
+    return cudaSuccess;
+  }
+
+  ~LinkWorker() {
+    stop = true;
+    if (thr.joinable()) thr.join();
+    if (flags) cudaFreeHost((void*)flags);
+  }
+
+  void loop() {
+    uint32_t processed = 0;
+    unsigned idle = 0;
+    while (!stop.load(std::memory_order_relaxed)) {
+      const uint32_t ready = flags[0];
+      if ((int32_t)(ready - processed) <= 0) {
+        if (++idle > 4096) std::this_thread::yield();
+        continue;
+      }
+      idle = 0;
+      ++processed;
+      LinkJob& j = jobs[processed % kRing];
+      if (j.table_src) link_gather_cb(&j);
+      else link_scatter_cb(&j);
+      std::atomic_thread_fence(std::memory_order_seq_cst);  // table writes before the flag
+      flags[32] = processed;
+    }
+  }
+
+  // Host: the job the link stream will hand over next (call before enqueue()).
+  LinkJob* next() {
+    while ((int32_t)(issued + 1 - flags[32]) >= kRing) std::this_thread::yield();  // ring full
+    return &jobs[(issued + 1) % kRing];
+  }
+
+  // Stream side: publish the job and wait until the worker finished it.
+  int enqueue(cudaStream_t s) {
+    ++issued;
+    if (write_value((CUstream)s, d_ready, issued, 0) != CUDA_SUCCESS) return BP_ERR_CUDA;
+    if (wait_value((CUstream)s, d_done, issued, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) return BP_ERR_CUDA;
+    return BP_OK;
+  }
+};
+
 __global__ void k_mark_written(const uint32_t* __restrict__ ids, const uint8_t* __restrict__ dirty, long long n,
                                uint32_t* __restrict__ written) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -217,14 +302,13 @@ struct bp_engine {
   int step_head = 0, step_count = 0;
   // DMA host-link mode
   int link_mode = 0;  // 0: zero-copy kernels, 1: copy engines + host pool
-  bp::HostPool* pool = nullptr;
+  bp::LinkWorker* worker = nullptr;
   uint32_t* h_fetch_ids = nullptr;
   float* h_fetch_rows = nullptr;
   uint32_t* h_flush_ids = nullptr;
   uint8_t* h_flush_dirty = nullptr;
   float* h_flush_rows = nullptr;
-  std::vector<bp::LinkJob> jobs;  // ring: callbacks read their job when they run
-  int next_job = 0;
+
   int staging_i;
   long long chunk_cap;
 };
@@ -369,7 +453,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
 extern "C" int bp_engine_destroy(bp_engine* e) {
   if (!e) return BP_OK;
   cudaDeviceSynchronize();
-  delete e->pool;
+  delete e->worker;
   cudaFreeHost(e->h_fetch_ids);
   cudaFreeHost(e->h_fetch_rows);
   cudaFreeHost(e->h_flush_ids);
@@ -605,9 +689,16 @@ extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threa
     const unsigned hw = std::thread::hardware_concurrency();
     threads = (int)std::max(2u, std::min(16u, hw / 4));
   }
-  if (!e->pool || e->pool->size() != threads) {
-    delete e->pool;
-    e->pool = new bp::HostPool(threads);
+  if (!e->worker || e->worker->pool.size() != threads) {
+    delete e->worker;
+    e->worker = new bp::LinkWorker(threads);
+    const cudaError_t err = e->worker->init();
+    if (err != cudaSuccess) {
+      delete e->worker;
+      e->worker = nullptr;
+      e->link_mode = 0;
+      BP_CUDA_TRY(err);
+    }
   }
   const size_t rb = (size_t)e->cfg.dim * sizeof(float);
   if (!e->h_fetch_ids) {
@@ -616,15 +707,8 @@ extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threa
     BP_CUDA_TRY(cudaMallocHost(&e->h_flush_ids, (size_t)e->chunk_cap * sizeof(uint32_t)));
     BP_CUDA_TRY(cudaMallocHost(&e->h_flush_dirty, (size_t)e->chunk_cap));
     BP_CUDA_TRY(cudaMallocHost(&e->h_flush_rows, (size_t)e->chunk_cap * rb));
-    e->jobs.resize(256);
   }
   return BP_OK;
-}
-
-static bp::LinkJob* next_job(bp_engine* e) {
-  bp::LinkJob* j = &e->jobs[e->next_job];
-  e->next_job = (e->next_job + 1) % (int)e->jobs.size();
-  return j;
 }
 
 extern "C" int bp_engine_fetch(bp_engine* e, int32_t slot) {
@@ -638,10 +722,11 @@ extern "C" int bp_engine_fetch(bp_engine* e, int32_t slot) {
     if (n > 0) {
       const size_t rb = (size_t)e->cfg.dim * sizeof(float);
       BP_CUDA_TRY(cudaMemcpyAsync(e->h_fetch_ids, ps.ids, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, e->link));
-      bp::LinkJob* j = next_job(e);
-      *j = bp::LinkJob{e->pool, bp_store_host_table(e->store), nullptr, e->h_fetch_ids, nullptr, nullptr,
+      bp::LinkJob* j = e->worker->next();
+      *j = bp::LinkJob{&e->worker->pool, bp_store_host_table(e->store), nullptr, e->h_fetch_ids, nullptr, nullptr,
                        e->h_fetch_rows, n, rb};
-      BP_CUDA_TRY(cudaLaunchHostFunc(e->link, bp::link_gather_cb, j));
+      const int rc = e->worker->enqueue(e->link);
+      if (rc) return rc;
       BP_CUDA_TRY(cudaMemcpyAsync(ps.staging, e->h_fetch_rows, n * rb, cudaMemcpyHostToDevice, e->link));
     }
   } else {
@@ -668,10 +753,11 @@ extern "C" int bp_engine_flush(bp_engine* e, const int32_t* chunk_slots, int32_t
         bp::k_mark_written<<<bp::grid_for(m, 256), 256, 0, e->link>>>(
             c.ids, c.dirty, m, reinterpret_cast<uint32_t*>(bp_store_written_bitmap(e->store)));
         BP_LAUNCH_CHECK();
-        bp::LinkJob* j = next_job(e);
-        *j = bp::LinkJob{e->pool, nullptr, bp_store_host_table(e->store), e->h_flush_ids, e->h_flush_dirty,
+        bp::LinkJob* j = e->worker->next();
+        *j = bp::LinkJob{&e->worker->pool, nullptr, bp_store_host_table(e->store), e->h_flush_ids, e->h_flush_dirty,
                          e->h_flush_rows, nullptr, m, rb};
-        BP_CUDA_TRY(cudaLaunchHostFunc(e->link, bp::link_scatter_cb, j));
+        const int wrc = e->worker->enqueue(e->link);
+        if (wrc) return wrc;
       }
     } else {
       int rc = bp_store_write_masked(e->store, c.ids, c.rows, c.dirty, e->cfg.capacity, c.count, e->link);
