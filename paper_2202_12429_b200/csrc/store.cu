@@ -95,7 +95,9 @@ __global__ void k_store_fetch_v4(const float4* __restrict__ table, const uint32_
       const long long i = i0 + r * stride;
       if (i < total) {
         const long long row = i / q;
-        v[r] = table[(long long)ids[row] * q + (i - row * q)];
+        // evict-first: host rows are used once, keep them from displacing
+        // the L2-resident cache arena
+        v[r] = __ldcs(table + (long long)ids[row] * q + (i - row * q));
       }
     }
 #pragma unroll
@@ -148,8 +150,8 @@ __global__ void k_store_write(float* __restrict__ table, uint32_t* __restrict__ 
 #pragma unroll
     for (int r = 0; r < kIlp; ++r) {
       if (dst[r] < 0) continue;
-      if (v4) reinterpret_cast<float4*>(table)[dst[r]] = v[r];
-      else table[dst[r]] = v[r].x;
+      if (v4) __stcs(reinterpret_cast<float4*>(table) + dst[r], v[r]);
+      else __stcs(table + dst[r], v[r].x);
     }
   }
 }
