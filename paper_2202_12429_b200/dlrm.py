@@ -19,6 +19,7 @@ against a PyTorch fp32 CPU model (tests/test_gpu_dlrm.py, rel 1e-5).
 
 from __future__ import annotations
 
+import copy
 import ctypes as C
 from dataclasses import dataclass
 
@@ -89,6 +90,47 @@ def _pad8(n: int) -> int:
     return (-n) % 8
 
 
+class _LinearAct(torch.autograd.Function):
+    """y = relu?(x W^T + b) on the GPU: bias (and ReLU) in the cuBLASLt GEMM
+    epilogue (torch._addmm_activation), and in backward the bias gradient as
+    a GEMV against a ones vector instead of a column reduction over the
+    batch (measured 23 us per layer at B = 16,384 as a reduction)."""
+
+    _ones: dict = {}
+
+    @staticmethod
+    def forward(ctx, x, w, b, relu: bool):
+        y = torch._addmm_activation(b, x, w.t(), use_gelu=False) if relu else torch.addmm(b, x, w.t())
+        ctx.save_for_backward(x, w, y if relu else None)
+        ctx.relu = relu
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w, y = ctx.saved_tensors
+        if ctx.relu:
+            g = torch.ops.aten.threshold_backward(g, y, 0)
+        key = (g.shape[0], g.dtype, g.device)
+        ones = _LinearAct._ones.get(key)
+        if ones is None:
+            ones = _LinearAct._ones[key] = torch.ones(g.shape[0], dtype=g.dtype, device=g.device)
+        return g @ w, g.t() @ x, torch.mv(g.t(), ones), None
+
+
+def _run_mlp(seq: nn.Sequential, x: torch.Tensor) -> torch.Tensor:
+    """nn.Sequential of Linear (+ ReLU) through _LinearAct on CUDA tensors."""
+    if not x.is_cuda:
+        return seq(x)
+    mods = list(seq)
+    i = 0
+    while i < len(mods):
+        lin = mods[i]
+        relu = i + 1 < len(mods) and isinstance(mods[i + 1], nn.ReLU)
+        x = _LinearAct.apply(x.to(lin.weight.dtype), lin.weight, lin.bias, relu)
+        i += 2 if relu else 1
+    return x
+
+
 class DLRMDense(nn.Module):
     """Bottom MLP -> pairwise dot interaction with the T pooled embeddings -> top MLP."""
 
@@ -110,10 +152,10 @@ class DLRMDense(nn.Module):
     def forward(self, dense: torch.Tensor, pooled: torch.Tensor) -> torch.Tensor:
         if dense.shape[1] == self.num_dense and self.dense_pad:
             dense = nn.functional.pad(dense, (0, self.dense_pad))
-        x = self.bottom(dense)                                # [B, D]
+        x = _run_mlp(self.bottom, dense)                      # [B, D]
         if pooled.is_cuda:
             # fused CUDA interaction (no eager fallback on the GPU path)
-            return self.top(_Interact.apply(x, pooled, self.pairs + self.dim + self.top_pad)).squeeze(1)
+            return _run_mlp(self.top, _Interact.apply(x, pooled, self.pairs + self.dim + self.top_pad)).squeeze(1)
         z = torch.cat([x.unsqueeze(1).to(pooled.dtype), pooled], dim=1)  # [B, T+1, D]
         zz = torch.bmm(z, z.transpose(1, 2))                  # [B, T+1, T+1]
         inter = zz.flatten(1).index_select(1, self.tril_flat)  # [B, pairs]
@@ -148,6 +190,25 @@ class DLRMConfig:
         return BP_OPT_ADAGRAD if self.emb_optimizer == "adagrad" else BP_OPT_SGD
 
 
+class _MasterSGD:
+    """SGD on fp32 master weights from the gradients of a bf16 compute copy,
+    then the copy refreshed from the masters (mixed precision without
+    autocast's per-layer casts)."""
+
+    def __init__(self, master: list, lowp: list, lr: float):
+        self.master, self.lowp, self.lr = master, lowp, lr
+
+    def zero_grad(self, set_to_none: bool = True):
+        for p in self.lowp:
+            p.grad = None
+
+    @torch.no_grad()
+    def step(self):
+        for m, p in zip(self.master, self.lowp):
+            m.add_(p.grad, alpha=-self.lr)
+        torch._foreach_copy_(self.lowp, self.master)
+
+
 class DLRMTrainer:
     """Runs the dense model between the two native halves of an iteration."""
 
@@ -160,7 +221,13 @@ class DLRMTrainer:
         self.exchange = exchange
         torch.manual_seed(dcfg.seed)
         self.model = (model or DLRMDense(num_dense, num_tables, dim, dcfg.bottom, dcfg.top)).cuda()
-        self.opt = torch.optim.SGD(self.model.parameters(), lr=dcfg.mlp_lr)
+        if dcfg.mlp_dtype == "bf16":
+            # bf16 compute copy of the fp32 master model: no per-step casts
+            self.compute_model = copy.deepcopy(self.model).to(torch.bfloat16)
+            self.opt = _MasterSGD(list(self.model.parameters()), list(self.compute_model.parameters()), dcfg.mlp_lr)
+        else:
+            self.compute_model = self.model
+            self.opt = torch.optim.SGD(self.model.parameters(), lr=dcfg.mlp_lr)
         self.losses: list = []
         self._dense_dev: dict = {}
         self._graphs: dict = {}
@@ -257,7 +324,7 @@ class DLRMTrainer:
                 loss.backward()
                 grad = emb.grad.contiguous()
             self.losses.append(loss.detach().clone())
-            allreduce_mean_([p.grad for p in self.model.parameters()], ex.world)
+            allreduce_mean_([p.grad for p in self.compute_model.parameters()], ex.world)
             if g is not None and g["step"] is not None:
                 g["step"].replay()
             else:
@@ -303,7 +370,7 @@ class DLRMTrainer:
             ex.grads.copy_(grad)
             ex.barrier(stream)
             self.losses.append(loss.detach().clone())
-            allreduce_mean_([p.grad for p in self.model.parameters()], ex.world)
+            allreduce_mean_([p.grad for p in self.compute_model.parameters()], ex.world)
             if g is not None and g["step"] is not None:
                 g["step"].replay()
             else:
@@ -315,12 +382,7 @@ class DLRMTrainer:
                                                      C.byref(res)), "bp_engine_dlrm_backward_peer")
 
     def _loss(self, dense, emb, labels):
-        if self.dcfg.mlp_dtype == "bf16":
-            with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
-                logits = self.model(dense, emb)
-            logits = logits.float()
-        else:
-            logits = self.model(dense, emb)
+        logits = self.compute_model(dense, emb).float()
         return nn.functional.binary_cross_entropy_with_logits(logits, labels)
 
     def _graph(self, b: int, t: int, n_dense: int, with_step: bool = True, emb=None) -> dict:

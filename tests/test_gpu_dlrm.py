@@ -230,3 +230,22 @@ def test_hybrid_dlrm_two_gpus_matches_cpu(opt_name, kind):
            "127.0.0.1", "--master-port", str(port), os.path.join(root, "tools", "hybrid_check.py"), opt_name, kind]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_bf16_mixed_precision_tracks_fp32():
+    """mlp_dtype=bf16 (bf16 compute copy + fp32 master SGD, CUDA graph) stays
+    close to the fp32 run: losses within 2e-2, embedding tables within 2e-3."""
+    from paper_2202_12429_b200.dlrm import DLRMConfig, DLRMDense
+    from paper_2202_12429_b200.engine import EngineConfig, run_dlrm
+
+    torch.manual_seed(0)
+    model = DLRMDense(SCHEMA.num_dense, SCHEMA.num_tables, SCHEMA.emb_dim, bottom=(64, 32), top=(64, 32))
+    batches = _batches()
+    cfg = EngineConfig(cache_capacity=1200, batch_size=256, lookahead=3, num_shards=1, seed=7, lr=0.05)
+    out = {}
+    for dt in ("fp32", "bf16"):
+        dcfg = DLRMConfig(emb_lr=0.05, mlp_lr=0.05, bottom=(64, 32), top=(64, 32), mlp_dtype=dt)
+        report, trainer = run_dlrm(cfg, SCHEMA, batches, dcfg, model=copy.deepcopy(model))
+        out[dt] = (np.asarray(trainer.loss_history()), report.final_store.table_view().copy())
+    np.testing.assert_allclose(out["bf16"][0], out["fp32"][0], rtol=2e-2)
+    np.testing.assert_allclose(out["bf16"][1], out["fp32"][1], rtol=0, atol=2e-3)
