@@ -403,6 +403,10 @@ int bp_engine_sync(bp_engine* engine);
 /* Make `stream` wait for all work issued so far on the engine's streams
  * (compute, plan, host-link) without blocking the host. */
 int bp_engine_join(bp_engine* engine, bp_stream_t stream);
+/* Benchmarks: every iteration first writes `bytes` (> L2) of d_buf on the
+ * compute stream; exclusive != 0 fences the plan and host-link streams
+ * around the write.  d_buf = NULL disables. */
+int bp_engine_set_l2_flush(bp_engine* engine, void* d_buf, int64_t bytes, int32_t exclusive);
 /* Per-stage device time since the last call, 7 stages: prep, planner, fetch
  * (link), apply (insert+TTL+lookup+mark), trainer, evict, flush (link).
  * Synchronises the device. */

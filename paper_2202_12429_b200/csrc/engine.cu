@@ -300,6 +300,10 @@ struct bp_engine {
   cudaEvent_t step_done[kStepRing];
   int step_chunk[kStepRing], step_drain[kStepRing];
   int step_head = 0, step_count = 0;
+  void* l2_flush_buf = nullptr;  // bp_engine_set_l2_flush (benchmarks)
+  size_t l2_flush_bytes = 0;
+  int l2_flush_exclusive = 0;
+  cudaEvent_t flush_ev = nullptr;
   // DMA host-link mode
   int link_mode = 0;  // 0: zero-copy kernels, 1: copy engines + host pool
   bp::LinkWorker* worker = nullptr;
@@ -454,6 +458,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   if (!e) return BP_OK;
   cudaDeviceSynchronize();
   delete e->worker;
+  if (e->flush_ev) cudaEventDestroy(e->flush_ev);
   cudaFreeHost(e->h_fetch_ids);
   cudaFreeHost(e->h_fetch_rows);
   cudaFreeHost(e->h_flush_ids);
@@ -691,10 +696,12 @@ extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threa
   }
   if (!e->worker || e->worker->pool.size() != threads) {
     delete e->worker;
+  if (e->flush_ev) cudaEventDestroy(e->flush_ev);
     e->worker = new bp::LinkWorker(threads);
     const cudaError_t err = e->worker->init();
     if (err != cudaSuccess) {
       delete e->worker;
+  if (e->flush_ev) cudaEventDestroy(e->flush_ev);
       e->worker = nullptr;
       e->link_mode = 0;
       BP_CUDA_TRY(err);
@@ -778,6 +785,22 @@ static int engine_apply(bp_engine* e, bp_prep* P, PlanSlot& ps, int64_t next_pos
                         int32_t has_skip, bp_prep** next_out) {
   cudaStream_t s = e->compute;
   const int dim = e->cfg.dim;
+  if (e->l2_flush_buf) {
+    // benchmark hygiene (bp_engine_set_l2_flush): every iteration starts on a
+    // cold L2; exclusive = no other engine work overlaps the flush write
+    if (e->l2_flush_exclusive) {
+      BP_CUDA_TRY(cudaEventRecord(e->join_ev[0], e->planq));
+      BP_CUDA_TRY(cudaEventRecord(e->join_ev[1], e->link));
+      BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[0], 0));
+      BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[1], 0));
+    }
+    BP_CUDA_TRY(cudaMemsetAsync(e->l2_flush_buf, 0, e->l2_flush_bytes, s));
+    if (e->l2_flush_exclusive) {
+      BP_CUDA_TRY(cudaEventRecord(e->flush_ev, s));
+      BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, e->flush_ev, 0));
+      BP_CUDA_TRY(cudaStreamWaitEvent(e->link, e->flush_ev, 0));
+    }
+  }
   BP_CUDA_TRY(cudaStreamWaitEvent(s, ps.fetched, 0));
   stage_begin(e, kStageApply, s);
   const int off = has_skip ? 1 : 0;
@@ -1040,6 +1063,18 @@ extern "C" int bp_engine_chunk_keys(bp_engine* e, int32_t chunk_slot, uint64_t* 
 extern "C" int bp_engine_chunk_view(bp_engine* e, int32_t chunk_slot, bp_evict_buffers* out) {
   bp::ChunkSlot& c = e->chunks[chunk_slot];
   *out = bp_evict_buffers{c.keys, c.ids, c.rows, c.dirty, c.count};
+  return BP_OK;
+}
+
+// Benchmark hygiene: every iteration first writes `bytes` of `d_buf` (larger
+// than L2) on the compute stream; exclusive != 0 also fences the plan and
+// host-link streams around that write so nothing overlaps it.  NULL disables.
+extern "C" int bp_engine_set_l2_flush(bp_engine* e, void* d_buf, int64_t bytes, int32_t exclusive) {
+  if (d_buf && bytes <= 0) return BP_ERR_INVALID;
+  if (!e->flush_ev) BP_CUDA_TRY(cudaEventCreateWithFlags(&e->flush_ev, cudaEventDisableTiming));
+  e->l2_flush_buf = d_buf;
+  e->l2_flush_bytes = (size_t)bytes;
+  e->l2_flush_exclusive = exclusive;
   return BP_OK;
 }
 

@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--trace", default=None, help="write a chrome trace (kernel timeline per stream) here")
     ap.add_argument("--flush", action="store_true", help="256 MiB L2 flush before each step, like bench.py")
     ap.add_argument("--sync-flush", action="store_true", help="drain all engine streams before each flush")
+    ap.add_argument("--engine-flush", type=int, default=-1,
+                    help="flush inside the engine at each iteration start (0: overlapped, 1: exclusive)")
     ap.add_argument("--link-blocks", type=int, default=0, help="grid of the host-link kernels (0: default)")
     ap.add_argument("--link-config", default="", help="blocks,threads,smem of the host-link kernels")
     ap.add_argument("--skip-link", type=int, default=0,
@@ -76,6 +78,14 @@ def main():
         pipe.step(pos)
     torch.cuda.synchronize()
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
+
+    if args.engine_flush >= 0:
+        from paper_2202_12429_b200 import _lib as L
+
+        flush_buf = None
+        eng_flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        L.check(pipe.lib.bp_engine_set_l2_flush(pipe.eng, L.ptr(eng_flush), eng_flush.numel(), args.engine_flush),
+                "bp_engine_set_l2_flush")
 
     def one(i):
         if flush_buf is not None and args.sync_flush:
