@@ -171,7 +171,10 @@ def _timed_steps(pipe, first: int, steps: int, flush_buf, torch):
 
 
 def _flush_ms(flush_buf, steps: int, torch) -> float:
-    """Device time of the per-step L2 flush alone (reported, not subtracted)."""
+    """Device time of the per-iteration L2 flush alone (reported, not
+    subtracted): the same memset, warmed up, timed over K repetitions."""
+    for _ in range(3):
+        flush_buf.zero_()
     s = torch.cuda.Event(enable_timing=True)
     e = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -222,8 +225,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     pipe.stage_times()  # reset the per-stage event record
     clocks.start()
     ms, wall_ms = _timed_steps(pipe, warm, steps, flush_buf, torch)
-    clk = clocks.stop()
     flush_ms = _flush_ms(flush_buf, steps, torch)
+    clk = clocks.stop()
     stages = pipe.stage_times()
     records = pipe.records[warm:warm + steps]
     launches_per_step = count_launches(pipe, warm + steps)
