@@ -276,6 +276,7 @@ struct bp_engine {
   bp_cache* cache;
   bp_planner* planner;
   cudaStream_t compute, link, planq;
+  cudaStream_t prepq;  // batch uploads + preps, ahead of and apart from the planner
   std::vector<bp_prep*> preps;  // ring indexed by position
   std::vector<cudaEvent_t> prep_ready;  // per prep slot, recorded on planq
   std::vector<bp::PlanSlot> plans;
@@ -293,7 +294,7 @@ struct bp_engine {
   uint64_t* d_keys_staging[2];
   uint8_t* d_labels_staging[2];
   cudaEvent_t staging_free[2];
-  cudaEvent_t join_ev[2];  // bp_engine_join: planq, link
+  cudaEvent_t join_ev[3];  // bp_engine_join: planq, link, prepq
   // steps enqueued by engine_finish_begin and not yet ended: a FIFO ring, so
   // the host can enqueue iteration x+1 before reading iteration x's counters
   static constexpr int kStepRing = 2;
@@ -379,6 +380,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   // on their own stream: they depend only on the trace, so they overlap the
   // training of the iterations ahead of them.
   BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->planq, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
+  BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->prepq, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
   int rc = bp_store_create_ex(ctx, sc, cfg->seed, cfg->init_dims > 0 ? cfg->init_dims : sc->emb_dim, e->compute,
                               &e->store);
   if (rc) return rc;
@@ -435,8 +437,9 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     BP_CUDA_TRY(cudaMalloc(&e->d_labels_staging[i], n + 16));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->staging_free[i], cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->join_ev[i], cudaEventDisableTiming));
+    if (i == 0) BP_CUDA_TRY(cudaEventCreateWithFlags(&e->join_ev[2], cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->step_done[i], cudaEventDisableTiming));
-    BP_CUDA_TRY(cudaEventRecord(e->staging_free[i], e->planq));
+    BP_CUDA_TRY(cudaEventRecord(e->staging_free[i], e->prepq));
   }
   e->staging_i = 0;
   e->next_plan = 0;
@@ -450,6 +453,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   BP_CUDA_TRY(cudaMalloc(&e->d_col_tables, sc->num_tables * sizeof(int32_t)));
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
   BP_CUDA_TRY(cudaStreamSynchronize(e->planq));
+  BP_CUDA_TRY(cudaStreamSynchronize(e->prepq));
   *out = e;
   return BP_OK;
 }
@@ -498,6 +502,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
     cudaFree(e->d_labels_staging[i]);
     cudaEventDestroy(e->staging_free[i]);
     cudaEventDestroy(e->join_ev[i]);
+    if (i == 0) cudaEventDestroy(e->join_ev[2]);
     cudaEventDestroy(e->step_done[i]);
   }
   cudaFree(e->slots_s);
@@ -512,6 +517,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   cudaStreamDestroy(e->compute);
   cudaStreamDestroy(e->link);
   cudaStreamDestroy(e->planq);
+  cudaStreamDestroy(e->prepq);
   delete e;
   return BP_OK;
 }
@@ -533,7 +539,7 @@ static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64
   using namespace bp;
   if (n_occ > e->cfg.max_occ) return BP_ERR_INVALID;
   const int slot = engine_prep_slot(e, pos);
-  cudaStream_t q = e->planq;
+  cudaStream_t q = e->prepq;
   if (e->preps[slot]) {
     bp_prep_destroy(e->preps[slot]);
     e->preps[slot] = nullptr;
@@ -606,12 +612,13 @@ extern "C" int bp_engine_prep(bp_engine* e, int64_t pos, bp_prep** out) {
 extern "C" int bp_engine_release_batch(bp_engine* e, int64_t pos) {
   const int slot = bp::engine_prep_slot(e, pos);
   if (e->preps[slot]) {
-    // The prep's memory is freed in stream order on the plan stream, after
-    // the compute stream's last use (its training).
+    // The prep's memory is freed in stream order on the prep stream, after
+    // the compute stream's last use (its training; the planner's uses
+    // precede it through the fetch/popped events).
     cudaEvent_t done;
     BP_CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventRecord(done, e->compute));
-    BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, done, 0));
+    BP_CUDA_TRY(cudaStreamWaitEvent(e->prepq, done, 0));
     cudaEventDestroy(done);
     bp_prep_destroy(e->preps[slot]);
     e->preps[slot] = nullptr;
@@ -620,8 +627,10 @@ extern "C" int bp_engine_release_batch(bp_engine* e, int64_t pos) {
 }
 
 extern "C" int bp_engine_refill(bp_engine* e, int64_t pos) {
-  bp_prep* P = e->preps[bp::engine_prep_slot(e, pos)];
+  const int pslot = bp::engine_prep_slot(e, pos);
+  bp_prep* P = e->preps[pslot];
   if (!P) return BP_ERR_ENGINE;
+  BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, e->prep_ready[pslot], 0));
   bp::stage_begin(e, bp::kStagePlanner, e->planq);
   const int rc = bp_planner_refill(e->planner, P, e->planq);
   bp::stage_end(e, bp::kStagePlanner, e->planq);
@@ -638,6 +647,7 @@ extern "C" int bp_engine_pop(bp_engine* e, int64_t pos, int32_t* slot_out) {
   PlanSlot& ps = e->plans[slot];
   // The slot's previous plan must have been consumed by training.
   BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, ps.consumed, 0));
+  BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, e->prep_ready[engine_prep_slot(e, pos)], 0));
   bp_plan_buffers b{ps.keys, ps.ids, ps.ttls, ps.ttl_k, ps.evict_keys, ps.evict_ids, ps.counts};
   stage_begin(e, kStagePlanner, e->planq);
   int rc = bp_planner_pop(e->planner, P, &b, e->planq);
@@ -791,14 +801,17 @@ static int engine_apply(bp_engine* e, bp_prep* P, PlanSlot& ps, int64_t next_pos
     if (e->l2_flush_exclusive) {
       BP_CUDA_TRY(cudaEventRecord(e->join_ev[0], e->planq));
       BP_CUDA_TRY(cudaEventRecord(e->join_ev[1], e->link));
+      BP_CUDA_TRY(cudaEventRecord(e->join_ev[2], e->prepq));
       BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[0], 0));
       BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[1], 0));
+      BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[2], 0));
     }
     BP_CUDA_TRY(cudaMemsetAsync(e->l2_flush_buf, 0, e->l2_flush_bytes, s));
     if (e->l2_flush_exclusive) {
       BP_CUDA_TRY(cudaEventRecord(e->flush_ev, s));
       BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, e->flush_ev, 0));
       BP_CUDA_TRY(cudaStreamWaitEvent(e->link, e->flush_ev, 0));
+      BP_CUDA_TRY(cudaStreamWaitEvent(e->prepq, e->flush_ev, 0));
     }
   }
   BP_CUDA_TRY(cudaStreamWaitEvent(s, ps.fetched, 0));
@@ -1082,8 +1095,10 @@ extern "C" int bp_engine_join(bp_engine* e, bp_stream_t stream) {
   cudaStream_t s = (cudaStream_t)stream;
   BP_CUDA_TRY(cudaEventRecord(e->join_ev[0], e->planq));
   BP_CUDA_TRY(cudaEventRecord(e->join_ev[1], e->link));
+  BP_CUDA_TRY(cudaEventRecord(e->join_ev[2], e->prepq));
   BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[0], 0));
   BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[1], 0));
+  BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[2], 0));
   if (s != e->compute) {
     cudaEvent_t c = e->join_ev[0];
     BP_CUDA_TRY(cudaEventRecord(c, e->compute));
@@ -1095,6 +1110,7 @@ extern "C" int bp_engine_join(bp_engine* e, bp_stream_t stream) {
 extern "C" int bp_engine_sync(bp_engine* e) {
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
   BP_CUDA_TRY(cudaStreamSynchronize(e->planq));
+  BP_CUDA_TRY(cudaStreamSynchronize(e->prepq));
   BP_CUDA_TRY(cudaStreamSynchronize(e->link));
   return BP_OK;
 }

@@ -164,6 +164,7 @@ class _Plan:
 
 class _Pipeline:
     EMIT_AHEAD = 3  # plans emitted ahead of dispatch (see _emit_ahead)
+    PREP_AHEAD = 4  # batches prepped (own stream) ahead of entering the planner window
     """One pipelined run (reference engine.py:239-649) on the native engine.
 
     The host keeps the reference's scalar control flow -- window refill,
@@ -204,7 +205,8 @@ class _Pipeline:
                             c_label=f32(stub.c_label), lr=f32(stub.lr),
                             record_keys=1 if (cfg.record_events or fault == FAULT_NO_GATE) else 0,
                             plan_slots=self.L0 + 4 + self.EMIT_AHEAD, chunk_slots=self.flush_interval + 4,
-                            prep_slots=2 * self.L0 + 8 + self.EMIT_AHEAD, timing=1 if timing else 0,
+                            prep_slots=2 * self.L0 + 8 + self.EMIT_AHEAD + self.PREP_AHEAD,
+                            timing=1 if timing else 0,
                             init_dims=schema.emb_dim,
                             prep_flags=2 if trainer is not None else 0)
         h = C.c_void_p()
@@ -545,7 +547,11 @@ class _Pipeline:
         adapt (which needs the previous plan's projected occupancy) never
         stalls the host on a pop it has just queued.  The plan sequence is a
         function of the trace and capacity only, so emitting earlier does
-        not change any plan."""
+        not change any plan.  Batch preps run PREP_AHEAD batches ahead of
+        the window on their own stream, so an emission only waits for the
+        planner's refill + pop."""
+        for p in range(self.source_pos, min(self.n, self.source_pos + self.PREP_AHEAD)):
+            self._add(p)
         while len(self.pending) < self.EMIT_AHEAD and not self.exhausted:
             prev = self._adapt_pending
             if prev is not None:
