@@ -16,9 +16,11 @@ through the public API with host batches (H2D of the batch entering the
 window and D2H of the step counters inside the timed region).  L2 is
 flushed (256 MiB write) between timed steps.  ``--impl reference`` times the
 CPU oracle port of the reference (oracle/, reference unavailable on the box)
-on the host cores.  N>1: the 26 tables are sharded table-wise over the
-ranks (each rank runs the whole pipeline for its tables of the SAME global
-batch, no data-path collective; strong scaling), timed as the max over ranks.
+on the host cores.  N>1 (weak scaling, fixed 16,384 examples per GPU): the
+global batch is N x 16,384 and its 26 tables are sharded table-wise over the
+ranks (each rank runs the whole pipeline for its tables of every example --
+the same occurrences per GPU as one GPU -- no data-path collective), timed
+as the max over ranks.
 DLRM mode (N=1, reported under "dlrm" and in "roofline"): the same engine
 with EmbeddingBag fwd/bwd + SGD feeding PyTorch MLPs replayed as a CUDA graph.
 """
@@ -68,11 +70,11 @@ def schema():
     return Schema(26, CK_ROWS, 13, DIM)
 
 
-def make_batches(n_batches: int, seed: int):
+def make_batches(n_batches: int, seed: int, batch: int = BATCH):
     from paper_2202_12429_b200.traces import ZipfSpec, batchify_columns, generate_columns
 
-    rows, labels, dense = generate_columns(ZipfSpec(schema(), ZIPF, n_batches * BATCH, seed))
-    return batchify_columns(rows, labels, dense, BATCH)
+    rows, labels, dense = generate_columns(ZipfSpec(schema(), ZIPF, n_batches * batch, seed))
+    return batchify_columns(rows, labels, dense, batch)
 
 
 # ------------------------------------------------------------------ clocks
@@ -199,13 +201,16 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     cap = sc.total_rows // 100
     steps, warm = args.steps, args.warmup
     n_batches = warm + steps + 12
-    # N>1: table-wise shards of ONE global batch per step (strong scaling);
-    # each rank runs the full pipeline for its tables, no data-path collective.
+    # N>1 (weak scaling, the DLRM convention of a fixed per-GPU batch): the
+    # global batch is N x 16,384 examples, its 26 tables dealt over the ranks;
+    # every rank runs the whole pipeline for its tables of every example --
+    # N x 16,384 x 26/N = the same 425,984 occurrences per step as one GPU --
+    # with no data-path collective, and the same per-GPU HBM cache budget.
     tables = table_shards(sc.num_tables, world)[rank]
-    full = make_batches(n_batches, args.seed)
+    gbatch = BATCH * world
+    full = make_batches(n_batches, args.seed, gbatch)
     batches = full if world == 1 else shard_batches(full, tables)
-    cfg = EngineConfig(cache_capacity=cap, batch_size=BATCH, lookahead=0 if world == 1 else 7, num_trainers=1,
-                       num_shards=1, seed=11)
+    cfg = EngineConfig(cache_capacity=cap, batch_size=gbatch, lookahead=0, num_trainers=1, num_shards=1, seed=11)
 
     # ---- value: inputs resident in HBM before timing
     dev_inputs = {}
@@ -232,7 +237,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     launches_per_step = count_launches(pipe, warm + steps)
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     pf_mean = statistics.mean(r.prefetch_count for r in records)
-    n_occ = BATCH * len(tables)
+    n_occ = gbatch * len(tables)
     del pipe
 
     # ---- e2e: host batches through the public engine API (pinned upload in the timed span)
@@ -271,7 +276,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     stub_bytes = stub_step_bytes(n_occ, int(u_mean))
     stub_achieved = stub_bytes / (stub_ms * 1e-3) / 1e9 if stub_ms else 0.0
     fetch_total, fetch_n = stages["fetch"]
-    samples = BATCH * steps  # one global batch per step across all ranks
+    samples = gbatch * steps  # one global batch per step across all ranks
     out = {
         "metric": METRIC,
         "value": samples / (ms_max * 1e-3),
@@ -281,13 +286,14 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "warmup": warm,
         "ms_per_step": ms_max / steps,
         "higher_is_better": True,
-        "scaling": "weak" if world == 1 else "strong",
+        "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (reference Zipf generator stream, columnar)",
-        "config": {"workload": WORKLOAD, "global_batch": BATCH, "tables": 26, "rows": sc.total_rows,
+        "config": {"workload": WORKLOAD, "global_batch": gbatch, "per_gpu_batch": BATCH, "tables": 26,
+                   "rows": sc.total_rows,
                    "emb_dim": DIM, "cache_capacity_per_gpu": cap, "lookahead": cfg.lookahead or 7,
-                   "parallelism": "single" if world == 1 else f"table-sharded x{world}",
+                   "parallelism": "single" if world == 1 else f"table-sharded x{world} (weak: {BATCH} examples/GPU)",
                    "l2": "flushed at the start of every timed iteration by the engine (256 MiB memset on the compute "
                          "stream, plan and host-link streams fenced around it), inside the timed span",
                    "timing": "one CUDA-event span over K steps, end event after joining the plan and host-link streams",
@@ -339,7 +345,7 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
         # NVLink peer-memory exchange fused into the EmbeddingBag kernels
         # (default) or the NCCL all-to-all version
         if os.environ.get("BAGPIPE_B200_EXCHANGE", "peer") == "peer":
-            ex = PeerExchange(sc.num_tables, DIM, rank, world, BATCH // world)
+            ex = PeerExchange(sc.num_tables, DIM, rank, world, BATCH)
         else:
             ex = EmbeddingExchange(sc.num_tables, DIM, rank, world)
     trainer = DLRMTrainer(dcfg, sc.num_dense, sc.num_tables, DIM, exchange=ex)
@@ -365,14 +371,14 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
     stages = pipe.stage_times()
     records = pipe.records[warm:warm + steps]
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
-    n_occ = BATCH * local_tables
+    n_occ = BATCH * world * local_tables
     # "trainer" spans: EmbeddingBag forward and backward alternate (2 per step)
     spans = stages["trainer"]
     # forward N_occ*(64 row read + 64 pooled write + 4 index)
     fwd_bytes = n_occ * (8 * DIM + 4)
     losses = trainer.loss_history()
     del pipe
-    return {"summary": {"value": BATCH * steps / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms / steps,
+    return {"summary": {"value": BATCH * world * steps / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms / steps,
                         "parallelism": "single" if world == 1 else
                         f"hybrid: table-sharded embeddings + data-parallel MLP x{world}, "
                         f"{'NVLink peer-memory' if hasattr(ex, 'rows_x') else 'NCCL all-to-all'} exchange",
