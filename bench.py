@@ -219,6 +219,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         dev_inputs[i] = (torch.from_numpy(keys).cuda(), torch.from_numpy(labels).cuda())
     torch.cuda.synchronize()
     pipe = _Pipeline(cfg, sc, batches, None, None, device_inputs=dev_inputs, timing=True)
+    lookahead0 = pipe.L0  # auto lookahead of this rank's trace
     pipe.begin()
     for pos in range(warm):
         pipe.step(pos)
@@ -292,7 +293,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "data": "synthetic (reference Zipf generator stream, columnar)",
         "config": {"workload": WORKLOAD, "global_batch": gbatch, "per_gpu_batch": BATCH, "tables": 26,
                    "rows": sc.total_rows,
-                   "emb_dim": DIM, "cache_capacity_per_gpu": cap, "lookahead": cfg.lookahead or 7,
+                   "emb_dim": DIM, "cache_capacity_per_gpu": cap, "lookahead": lookahead0,
                    "parallelism": "single" if world == 1 else f"table-sharded x{world} (weak: {BATCH} examples/GPU)",
                    "l2": "flushed at the start of every timed iteration by the engine (256 MiB memset on the compute "
                          "stream, plan and host-link streams fenced around it), inside the timed span",
