@@ -158,15 +158,19 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
         __syncthreads();
         if (tr && threadIdx.x == 0) tr[2] = clock64();
         if (chain_lane) {
-          uint32_t nxt = winfo[0];
-          for (uint32_t k = 0; k < nchunk; ++k) {
-            const uint32_t info = nxt;
-            if (k + 1 < nchunk) nxt = winfo[k + 1];
+          uint32_t k = 0;
+          while (k < nchunk) {
+            uint32_t info = winfo[k];
             if constexpr (DPL == 1) {
               if (info & 0x10000u) {
+                // a run of plain chunks: a tight loop of R2P + select + add
                 float a0 = acc[0];
+                do {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) a0 = __fadd_rn(a0, ((info >> i) & 1u) ? t1[0] : t0[0]);
+                  for (int i = 0; i < 16; ++i) a0 = __fadd_rn(a0, ((info >> i) & 1u) ? t1[0] : t0[0]);
+                  ++k;
+                  info = k < nchunk ? winfo[k] : 0u;
+                } while (info & 0x10000u);
                 acc[0] = a0;
                 continue;
               }
@@ -178,6 +182,7 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
             const uint32_t hi = b - cbase < 16u ? b - cbase : 16u;
             const uint32_t first_q = (a >= cbase && a < cbase + 16) ? a - cbase : 16u;
             chain_chunk<DPL>(word, lo, hi, first_q, acc, comb, t0, t1, sc, c_label);
+            ++k;
           }
           if (tr && threadIdx.x == 0) tr[3] = clock64() + 0 * (unsigned long long)__float_as_uint(acc[0]);
         }
