@@ -357,8 +357,10 @@ typedef struct bp_engine_parts_t {
 int bp_engine_create(bp_ctx* ctx, const bp_schema* schema, const bp_engine_config* cfg, bp_engine** out);
 int bp_engine_destroy(bp_engine* engine);
 int bp_engine_parts(bp_engine* engine, bp_engine_parts_t* out);
-/* keys/labels: host pointers (keys_on_host=1, copied through a pinned ring)
- * or device pointers that stay valid until the prep kernels ran. */
+/* keys/labels: host pointers (keys_on_host=1: copied into a pinned ring by
+ * the engine's upload worker thread, asynchronously -- they must stay valid
+ * until bp_engine_release_batch of that position) or device pointers that
+ * stay valid until the prep kernels ran. */
 int bp_engine_add_batch(bp_engine* engine, int64_t pos, int64_t iteration, const uint64_t* keys,
                         const uint8_t* labels, int64_t n_occ, const int64_t* h_rank_bounds, int32_t num_ranks,
                         int32_t keys_on_host);

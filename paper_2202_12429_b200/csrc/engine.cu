@@ -115,7 +115,25 @@ struct LinkJob {
   float* rows_dst;
   long long n;
   size_t row_bytes;
+  // copy jobs (batch uploads into pinned memory): up to two (src, dst, bytes)
+  int copies = 0;
+  const void* csrc[2];
+  void* cdst[2];
+  size_t cbytes[2];
 };
+
+static void host_copy(const LinkJob* j) {
+  for (int c = 0; c < j->copies; ++c) {
+    const char* src = static_cast<const char*>(j->csrc[c]);
+    char* dst = static_cast<char*>(j->cdst[c]);
+    const size_t bytes = j->cbytes[c];
+    constexpr size_t kPiece = 256 << 10;
+    j->pool->parallel_for((long long)((bytes + kPiece - 1) / kPiece), [&](long long a, long long b) {
+      const size_t lo = (size_t)a * kPiece, hi = std::min(bytes, (size_t)b * kPiece);
+      if (hi > lo) std::memcpy(dst + lo, src + lo, hi - lo);
+    });
+  }
+}
 
 // Debug counters of the host-link callbacks (bp_debug_link_cb_stats).
 static std::atomic<long long> g_cb_ns[2], g_cb_calls[2], g_cb_rows[2];
@@ -219,7 +237,8 @@ struct LinkWorker {
       idle = 0;
       ++processed;
       LinkJob& j = jobs[processed % kRing];
-      if (j.table_src) link_gather_cb(&j);
+      if (j.copies) host_copy(&j);
+      else if (j.table_src) link_gather_cb(&j);
       else link_scatter_cb(&j);
       std::atomic_thread_fence(std::memory_order_seq_cst);  // table writes before the flag
       flags[32] = processed;
@@ -308,6 +327,7 @@ struct bp_engine {
   // DMA host-link mode
   int link_mode = 0;  // 0: zero-copy kernels, 1: copy engines + host pool
   bp::LinkWorker* worker = nullptr;
+  bp::LinkWorker* upload_worker = nullptr;  // host-batch uploads: copies into the pinned ring off the caller's thread
   uint32_t* h_fetch_ids = nullptr;
   float* h_fetch_rows = nullptr;
   uint32_t* h_flush_ids = nullptr;
@@ -462,6 +482,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   if (!e) return BP_OK;
   cudaDeviceSynchronize();
   delete e->worker;
+  delete e->upload_worker;
   if (e->flush_ev) cudaEventDestroy(e->flush_ev);
   cudaFreeHost(e->h_fetch_ids);
   cudaFreeHost(e->h_fetch_rows);
@@ -551,11 +572,34 @@ static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64
     UploadSlot& u = e->uploads[e->next_upload];
     e->next_upload = (e->next_upload + 1) % (int)e->uploads.size();
     if (u.used) BP_CUDA_TRY(cudaEventSynchronize(u.done));
-    std::memcpy(u.host, keys, n_occ * sizeof(uint64_t));
-    std::memcpy(u.host + n_occ * sizeof(uint64_t), labels, n_occ);
+    if (!e->upload_worker) {
+      e->upload_worker = new bp::LinkWorker(4);
+      const cudaError_t err = e->upload_worker->init();
+      if (err != cudaSuccess) {
+        delete e->upload_worker;
+        e->upload_worker = nullptr;
+        BP_CUDA_TRY(err);
+      }
+    }
     si = e->staging_i;
     e->staging_i ^= 1;
     BP_CUDA_TRY(cudaStreamWaitEvent(q, e->staging_free[si], 0));
+    // the copy into the pinned slot runs on the upload worker (4 threads);
+    // the stream waits for it, the caller does not (its arrays must stay
+    // alive until bp_engine_release_batch)
+    bp::LinkJob* j = e->upload_worker->next();
+    *j = bp::LinkJob{&e->upload_worker->pool, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0};
+    j->copies = 2;
+    j->csrc[0] = keys;
+    j->cdst[0] = u.host;
+    j->cbytes[0] = n_occ * sizeof(uint64_t);
+    j->csrc[1] = labels;
+    j->cdst[1] = u.host + n_occ * sizeof(uint64_t);
+    j->cbytes[1] = n_occ;
+    {
+      const int wrc = e->upload_worker->enqueue(q);
+      if (wrc) return wrc;
+    }
     BP_CUDA_TRY(cudaMemcpyAsync(e->d_keys_staging[si], u.host, n_occ * sizeof(uint64_t), cudaMemcpyHostToDevice, q));
     BP_CUDA_TRY(cudaMemcpyAsync(e->d_labels_staging[si], u.host + n_occ * sizeof(uint64_t), n_occ,
                                 cudaMemcpyHostToDevice, q));
@@ -706,11 +750,13 @@ extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threa
   }
   if (!e->worker || e->worker->pool.size() != threads) {
     delete e->worker;
+  delete e->upload_worker;
   if (e->flush_ev) cudaEventDestroy(e->flush_ev);
     e->worker = new bp::LinkWorker(threads);
     const cudaError_t err = e->worker->init();
     if (err != cudaSuccess) {
       delete e->worker;
+  delete e->upload_worker;
   if (e->flush_ev) cudaEventDestroy(e->flush_ev);
       e->worker = nullptr;
       e->link_mode = 0;

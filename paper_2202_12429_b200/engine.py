@@ -257,6 +257,7 @@ class _Pipeline:
         self.drop_done = False
         self.result = L.StepResult()
         self._inflight: dict = {}
+        self._host_refs: dict = {}
 
     def stage_times(self) -> dict:
         """{stage: (total ms, launches)} since the last call (timing=True)."""
@@ -287,6 +288,8 @@ class _Pipeline:
             keys = np.ascontiguousarray(keys, dtype=np.uint64)
             labels = np.ascontiguousarray(labels, dtype=np.uint8)
             kptr, lptr, on_host, n = keys.ctypes.data, labels.ctypes.data, 1, keys.size
+            # the engine copies them asynchronously: keep them alive until release
+            self._host_refs[pos] = (keys, labels)
         tables = b.table_ids() if b.is_columnar else None
         if tables is not None and len(tables) and bool(np.all(np.diff(tables) > 0)):
             # Criteo layout: one key per table per example -> per-column sort
@@ -303,6 +306,7 @@ class _Pipeline:
         if pos in self.added:
             self.lib.bp_engine_release_batch(self.eng, pos)
             self.added.discard(pos)
+        self._host_refs.pop(pos, None)
 
     # -- plan emission (reference engine.py:198-236, lookahead.py:64-123) --------
     def _plan_counts(self, plan: _Plan):
