@@ -68,11 +68,12 @@ def test_terabyte_like_shape_dim64():
     _run_and_compare(schema, batches, cfg)
 
 
-@pytest.mark.parametrize("window,cache_pct,zipf", [(50, 5.0, 0.8), (200, 1.0, 1.05), (1000, 0.5, 1.2),
-                                                   (50, 0.1, 1.05)])
+@pytest.mark.parametrize("window,cache_pct,zipf", [(50, 40.0, 0.8), (200, 30.0, 1.05), (1000, 20.0, 1.2),
+                                                   (50, 8.0, 1.2), (50, 5.0, 0.8), (50, 0.1, 1.05)])
 def test_sweep_cells(window, cache_pct, zipf):
-    """Config 5 cells (reduced): both sides run, or both fail at the same
-    iteration with the capacity exceeded."""
+    """Config 5 cells (reduced): both sides run (one with pressure halving),
+    or both fail at the same iteration with the capacity exceeded (iteration
+    1 and 0 in the last two cells)."""
     from paper_2202_12429_b200.errors import CacheCapacityError
 
     schema = Schema(4, (20_000, 5_000, 300, 7), 0, 8)
