@@ -239,6 +239,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     pf_mean = statistics.mean(r.prefetch_count for r in records)
     n_occ = gbatch * len(tables)
+    pipe.close()
     del pipe
 
     # ---- e2e: host batches through the public engine API (pinned upload in the timed span)
@@ -252,6 +253,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
             dist.barrier()
         torch.cuda.synchronize()
         e2e_ms, _ = _timed_steps(pipe2, warm, steps, flush_buf, torch)
+        pipe2.close()
         del pipe2
 
     # ---- DLRM mode (N=1): the same engine feeding PyTorch MLPs (bf16 autocast)
@@ -378,6 +380,7 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
     # forward N_occ*(64 row read + 64 pooled write + 4 index)
     fwd_bytes = n_occ * (8 * DIM + 4)
     losses = trainer.loss_history()
+    pipe.close()
     del pipe
     return {"summary": {"value": BATCH * world * steps / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms / steps,
                         "parallelism": "single" if world == 1 else

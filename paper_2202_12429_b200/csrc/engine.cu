@@ -30,6 +30,7 @@
 #include <thread>
 
 #include <atomic>
+#include <mutex>
 #include <chrono>
 
 struct bp_store;
@@ -281,6 +282,7 @@ namespace bp {
 enum Stage { kStagePrep = 0, kStagePlanner, kStageFetch, kStageApply, kStageTrainer, kStageEvict, kStageFlush,
              kNumStages };
 struct StageTimer {
+  std::mutex mu;  // the planner thread (prep/planner stages) and the training thread record concurrently
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans[kNumStages];
   cudaEvent_t open[kNumStages] = {};
 };
@@ -344,6 +346,7 @@ static int engine_prep_slot(bp_engine* e, long long pos) { return (int)(pos % (l
 
 static void stage_begin(bp_engine* e, int stage, cudaStream_t s) {
   if (!e->cfg.timing) return;
+  std::lock_guard<std::mutex> lk(e->timer.mu);
   cudaEvent_t ev;
   cudaEventCreate(&ev);
   cudaEventRecord(ev, s);
@@ -351,7 +354,9 @@ static void stage_begin(bp_engine* e, int stage, cudaStream_t s) {
 }
 
 static void stage_end(bp_engine* e, int stage, cudaStream_t s) {
-  if (!e->cfg.timing || !e->timer.open[stage]) return;
+  if (!e->cfg.timing) return;
+  std::lock_guard<std::mutex> lk(e->timer.mu);
+  if (!e->timer.open[stage]) return;
   cudaEvent_t ev;
   cudaEventCreate(&ev);
   cudaEventRecord(ev, s);
@@ -365,6 +370,7 @@ static void stage_end(bp_engine* e, int stage, cudaStream_t s) {
 // synchronises the device, then clears the record.
 extern "C" int bp_engine_stage_times(bp_engine* e, double* h_ms, int64_t* h_counts) {
   BP_CUDA_TRY(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lk(e->timer.mu);
   for (int st = 0; st < bp::kNumStages; ++st) {
     double total = 0;
     for (auto& pr : e->timer.spans[st]) {

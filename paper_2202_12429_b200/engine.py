@@ -30,6 +30,7 @@ import hashlib
 import json
 import math
 import os
+import threading
 from bisect import bisect_right
 from collections import deque
 from dataclasses import asdict, dataclass, field
@@ -179,7 +180,7 @@ class _Pipeline:
     STAGES = ("prep", "planner", "fetch", "apply", "trainer", "evict", "flush")
 
     def __init__(self, cfg: EngineConfig, schema: Schema, batches: list, fingerprint, fault, device_inputs=None,
-                 timing: bool = False, trainer=None, link_mode: int | None = None):
+                 timing: bool = False, trainer=None, link_mode: int | None = None, threaded: bool | None = None):
         if fault not in (None, FAULT_NO_GATE, FAULT_DROP_PREFETCH):
             raise ConfigurationError(f"unknown fault {fault!r}")
         self.cfg, self.schema, self.batches = cfg, schema, batches
@@ -258,6 +259,17 @@ class _Pipeline:
         self.result = L.StepResult()
         self._inflight: dict = {}
         self._host_refs: dict = {}
+        # planner thread (see _planner_loop): the plain fast path only; fault
+        # injection, event logs and mirror checks keep the single-thread order
+        self._threaded = (threaded if threaded is not None else
+                          os.environ.get("BAGPIPE_B200_PLANNER_THREAD", "1") == "1") and \
+            fault is None and self.events is None and self.snapshots is None
+        self._thread = None
+        self._stop = False
+        self._planner_error = None
+        self._cond = threading.Condition()
+        self._add_lock = threading.Lock()
+        self._plan_lock = threading.Lock()
 
     def stage_times(self) -> dict:
         """{stage: (total ms, launches)} since the last call (timing=True)."""
@@ -265,6 +277,15 @@ class _Pipeline:
         cnt = np.zeros(7, dtype=np.int64)
         L.check(self.lib.bp_engine_stage_times(self.eng, ms.ctypes.data, cnt.ctypes.data), "bp_engine_stage_times")
         return {name: (float(m), int(c)) for name, m, c in zip(self.STAGES, ms, cnt)}
+
+    def close(self) -> None:
+        """Stop the planner thread and free the native engine (callers that
+        step a pipeline without end())."""
+        self._stop_planner()
+        if getattr(self, "eng", None):
+            L.check(self.lib.bp_engine_sync(self.eng), "bp_engine_sync")
+            self.lib.bp_engine_destroy(self.eng)
+            self.eng = None
 
     def __del__(self):
         try:
@@ -276,6 +297,10 @@ class _Pipeline:
 
     # -- batches ---------------------------------------------------------------------
     def _add(self, pos: int) -> None:
+        with self._add_lock:  # the planner thread and the training loop may both add
+            self._add_locked(pos)
+
+    def _add_locked(self, pos: int) -> None:
         if pos in self.added:
             return
         b = self.batches[pos]
@@ -334,9 +359,10 @@ class _Pipeline:
         pos = self.queue.popleft()
         slot = C.c_int32()
         L.check(self.lib.bp_engine_pop(self.eng, pos, C.byref(slot)), "bp_engine_pop")
-        if slot.value not in self.free_plans:
-            raise EngineError("plan ring overrun")
-        self.free_plans.discard(slot.value)
+        with self._plan_lock:
+            if slot.value not in self.free_plans:
+                raise EngineError("plan ring overrun")
+            self.free_plans.discard(slot.value)
         plan = _Plan(self.batches[pos].iteration, self.lookahead, slot.value, pos)
         self._adapt_pending = plan
         if self.snapshots is not None:
@@ -369,6 +395,8 @@ class _Pipeline:
         self.staged[plan.iteration - self.base] = (plan, arrival)
 
     def _dispatch_until(self, cur: int) -> None:
+        if self._thread is not None:
+            return self._dispatch_until_threaded(cur)
         while True:
             if not self.pending:
                 if self.exhausted:
@@ -438,7 +466,64 @@ class _Pipeline:
         return self.free_chunks.pop(0)
 
     # -- per iteration ---------------------------------------------------------------
+    def _dispatch_until_threaded(self, cur: int) -> None:
+        while True:
+            with self._cond:
+                while not self.pending and not self.exhausted:
+                    self._cond.wait()
+                if self._planner_error is not None:
+                    raise self._planner_error
+                if not self.pending:
+                    return
+                plan = self.pending[0]
+                if self._dispatch_pos(plan) > cur:
+                    return
+                self.pending.popleft()
+                self._cond.notify_all()
+            self._dispatch(plan, cur)
+
+    def _planner_loop(self) -> None:
+        """Planner thread: batch preps and plan emission (the reference's
+        emit_next_plan + lazy adapt, in order) run here, ahead of the
+        training loop, whose thread keeps only dispatch, training and
+        write-back.  ctypes drops the GIL inside every native call, so the
+        two threads' CUDA API calls overlap."""
+        try:
+            torch.cuda.set_device(self._device)  # the CUDA current device is per thread
+            while True:
+                with self._cond:
+                    while not self._stop and (self.exhausted or len(self.pending) >= self.EMIT_AHEAD):
+                        self._cond.wait()
+                    if self._stop:
+                        return
+                for p in range(self.source_pos, min(self.n, self.source_pos + self.PREP_AHEAD)):
+                    self._add(p)
+                plan = self._next_plan()
+                with self._cond:
+                    if plan is None:
+                        self.exhausted = True
+                    else:
+                        self.pending.append(plan)
+                    self._cond.notify_all()
+        except BaseException as err:  # surfaced on the training thread
+            with self._cond:
+                self._planner_error = err
+                self.exhausted = True
+                self._cond.notify_all()
+
+    def _stop_planner(self) -> None:
+        if self._thread is not None:
+            with self._cond:
+                self._stop = True
+                self._cond.notify_all()
+            self._thread.join()
+            self._thread = None
+
     def begin(self) -> None:
+        if self._threaded:
+            self._device = torch.cuda.current_device()
+            self._thread = threading.Thread(target=self._planner_loop, name="bagpipe-planner", daemon=True)
+            self._thread.start()
         self._dispatch_until(-1)
 
     def step(self, pos: int, early: bool = True) -> None:
@@ -455,7 +540,7 @@ class _Pipeline:
                 and nxt < self.n and nxt in self.staged and nxt not in self._inflight
                 and len(self.free_chunks) >= (2 if nxt == self.n - 1 else 1)):
             self._begin(nxt)
-        if self.trainer is None:
+        if self.trainer is None and self._thread is None:
             # plan emission (planner stream) overlaps the queued GPU work
             self._emit_ahead()
         self._end(pos)
@@ -501,7 +586,8 @@ class _Pipeline:
             self.trainer.train(self, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
         if res.err.code:
             L.raise_error_record(res.err)
-        self.free_plans.add(plan.slot)
+        with self._plan_lock:
+            self.free_plans.add(plan.slot)
         u, n_ins, crit_count = int(res.unique), int(res.inserted), int(res.critical)
         n_ev, n_ev_dirty = int(res.evicted), int(res.evicted_dirty)
         self.occupancy += n_ins
@@ -543,7 +629,8 @@ class _Pipeline:
             partial["ttl_updates"] = ttl
         self._maintenance(pos, chunk, n_ev, n_ev_dirty, drain, int(res.drained), int(res.drained_dirty), partial)
         self._release(pos)
-        self._emit_ahead()
+        if self._thread is None:
+            self._emit_ahead()
 
     def _emit_ahead(self) -> None:
         """Emit plans ahead of their dispatch while the previous pop already
@@ -587,6 +674,9 @@ class _Pipeline:
         return list(zip(keys, ttls))
 
     def end(self) -> RunReport:
+        self._stop_planner()
+        if self._planner_error is not None:
+            raise self._planner_error
         if not self.exhausted and (self.pending or self._next_plan() is not None):
             raise EngineError("planner emitted more plans than batches")
         L.check(self.lib.bp_engine_sync(self.eng), "bp_engine_sync")
