@@ -172,6 +172,19 @@ def _timed_steps(pipe, first: int, steps: int, flush_buf, torch):
     return start.elapsed_time(end), wall
 
 
+def _stage_breakdown(pipe, first: int, k: int):
+    """Per-stage device time over k extra (untimed) steps with the engine's
+    stage events on; the timed region runs with them off (they cost host
+    calls).  Returns ({stage: (ms per step, launches per step)}, k)."""
+    pipe.lib.bp_engine_set_timing(pipe.eng, 1)
+    pipe.stage_times()
+    for i in range(k):
+        pipe.step(first + i, early=i < k - 1)
+    st = pipe.stage_times()
+    pipe.lib.bp_engine_set_timing(pipe.eng, 0)
+    return {name: (ms / k, n / k) for name, (ms, n) in st.items()}
+
+
 def _flush_ms(flush_buf, steps: int, torch) -> float:
     """Device time of the per-iteration L2 flush alone (reported, not
     subtracted): the same memset, warmed up, timed over K repetitions."""
@@ -228,14 +241,14 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    pipe.stage_times()  # reset the per-stage event record
+    pipe.lib.bp_engine_set_timing(pipe.eng, 0)
     clocks.start()
     ms, wall_ms = _timed_steps(pipe, warm, steps, flush_buf, torch)
     flush_ms = _flush_ms(flush_buf, steps, torch)
     clk = clocks.stop()
-    stages = pipe.stage_times()
     records = pipe.records[warm:warm + steps]
     launches_per_step = count_launches(pipe, warm + steps)
+    stages = _stage_breakdown(pipe, warm + steps + 1, 8)
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     pf_mean = statistics.mean(r.prefetch_count for r in records)
     n_occ = gbatch * len(tables)
@@ -275,10 +288,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     stub_total, stub_launches = stages["trainer"]
-    stub_ms = stub_total / max(stub_launches, 1)
+    stub_ms = stub_total / max(stub_launches, 1e-9)
     stub_bytes = stub_step_bytes(n_occ, int(u_mean))
     stub_achieved = stub_bytes / (stub_ms * 1e-3) / 1e9 if stub_ms else 0.0
-    fetch_total, fetch_n = stages["fetch"]
+    fetch_total, fetch_n = stages["fetch"]  # per step
     samples = gbatch * steps  # one global batch per step across all ranks
     out = {
         "metric": METRIC,
@@ -308,9 +321,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                                   "achieved": stub_achieved, "peak": hbm_peak, "unit": "GB/s",
                                   "frac": stub_achieved / hbm_peak, "bytes_per_launch": stub_bytes,
                                   "ms_per_launch": stub_ms, "peak_source": peak_src},
-        "stages_ms_per_step": {k: v[0] / steps for k, v in stages.items()},
+        "stages_ms_per_step": {k: v[0] for k, v in stages.items()},
         "host_link": {"prefetch_rows_per_step": pf_mean,
-                      "prefetch_gbs": pf_mean * 64 * fetch_n / (fetch_total * 1e-3) / 1e9 if fetch_total else None,
+                      "prefetch_gbs": pf_mean * 64 / (fetch_total * 1e-3) / 1e9 if fetch_total else None,
                       "peak_note": "pinned memcpy 55.5 GB/s H2D, 56.5 D2H; zero-copy random 64 B rows 18.7-25 GB/s "
                                    "(tools/hostlink_peak.py)"},
         "gpu_launches": launches_per_step * steps,
@@ -365,17 +378,17 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    pipe.stage_times()
+    pipe.lib.bp_engine_set_timing(pipe.eng, 0)
     ms, _ = _timed_steps(pipe, warm, steps, flush_buf, torch)
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
-    stages = pipe.stage_times()
     records = pipe.records[warm:warm + steps]
+    stages = _stage_breakdown(pipe, warm + steps, 8)
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     n_occ = BATCH * world * local_tables
-    # "trainer" spans: EmbeddingBag forward and backward alternate (2 per step)
+    # "trainer" spans: EmbeddingBag forward and backward (2 per step), per step
     spans = stages["trainer"]
     # forward N_occ*(64 row read + 64 pooled write + 4 index)
     fwd_bytes = n_occ * (8 * DIM + 4)
@@ -386,13 +399,13 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
                         "parallelism": "single" if world == 1 else
                         f"hybrid: table-sharded embeddings + data-parallel MLP x{world}, "
                         f"{'NVLink peer-memory' if hasattr(ex, 'rows_x') else 'NCCL all-to-all'} exchange",
-                        "mlp": "PyTorch bf16 autocast, one CUDA graph per step (13-512-256-64-16 / 367-1024-1024-512-256-1)",
+                        "mlp": "PyTorch, bf16 compute copy + fp32 master SGD, one CUDA graph per step (13-512-256-64-16 / 367-1024-1024-512-256-1)",
                         "embedding_optimizer": "sgd", "final_loss": losses[-1] if losses else None,
-                        "embedding_stage_ms_per_step": spans[0] / steps},
+                        "embedding_stage_ms_per_step": spans[0]},
             "roofline": {"kernel": "bp::k_embbag_fwd_rows_v4 + k_embbag_bwd (EmbeddingBag fwd+bwd+SGD on cached rows)",
                          "bound": "hbm", "bytes_per_step": fwd_bytes + bwd_bytes(n_occ, int(u_mean)),
-                         "ms_per_step": spans[0] / steps, "launches_per_step": 2, "unit": "GB/s",
-                         "achieved": (fwd_bytes + bwd_bytes(n_occ, int(u_mean))) / (spans[0] / steps * 1e-3) / 1e9
+                         "ms_per_step": spans[0], "launches_per_step": 2, "unit": "GB/s",
+                         "achieved": (fwd_bytes + bwd_bytes(n_occ, int(u_mean))) / (spans[0] * 1e-3) / 1e9
                          if spans[0] else 0.0,
                          "traffic": _traffic(),
                          "note": "SURVEY 8(d) algorithmic bytes: forward N_occ*(64 row read + 64 pooled write + 4 "

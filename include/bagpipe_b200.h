@@ -405,6 +405,8 @@ int bp_engine_sync(bp_engine* engine);
 /* Make `stream` wait for all work issued so far on the engine's streams
  * (compute, plan, host-link) without blocking the host. */
 int bp_engine_join(bp_engine* engine, bp_stream_t stream);
+/* Per-stage event timing on/off (bp_engine_stage_times). */
+int bp_engine_set_timing(bp_engine* engine, int32_t on);
 /* Benchmarks: every iteration first writes `bytes` (> L2) of d_buf on the
  * compute stream; exclusive != 0 fences the plan and host-link streams
  * around the write.  d_buf = NULL disables. */

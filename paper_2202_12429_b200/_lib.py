@@ -190,6 +190,7 @@ _SIGS = {
     "bp_set_link_config": (c_i32, [c_i32, c_i32, c_i32]),
     "bp_engine_plan_ready": (c_i32, [c_vp, c_i32, c_vp]),
     "bp_engine_join": (c_i32, [c_vp, c_vp]),
+    "bp_engine_set_timing": (c_i32, [c_vp, c_i32]),
     "bp_engine_set_l2_flush": (c_i32, [c_vp, c_vp, c_i64, c_i32]),
     "bp_engine_stage_times": (c_i32, [c_vp, c_vp, c_vp]),
     "bp_engine_dlrm_forward": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_u64, c_i32, c_i32, c_vp]),

@@ -1131,6 +1131,15 @@ extern "C" int bp_engine_chunk_view(bp_engine* e, int32_t chunk_slot, bp_evict_b
   return BP_OK;
 }
 
+// Per-stage event timing on/off (cfg.timing at creation); spans recorded so
+// far are kept until bp_engine_stage_times.
+extern "C" int bp_engine_set_timing(bp_engine* e, int32_t on) {
+  std::lock_guard<std::mutex> lk(e->timer.mu);
+  e->cfg.timing = on ? 1 : 0;
+  for (auto& ev : e->timer.open) ev = nullptr;
+  return BP_OK;
+}
+
 // Benchmark hygiene: every iteration first writes `bytes` of `d_buf` (larger
 // than L2) on the compute stream; exclusive != 0 also fences the plan and
 // host-link streams around that write so nothing overlaps it.  NULL disables.
