@@ -297,6 +297,8 @@ class _Pipeline:
 
     # -- batches ---------------------------------------------------------------------
     def _add(self, pos: int) -> None:
+        if pos in self.added:  # lock-free fast path (set membership is atomic)
+            return
         with self._add_lock:  # the planner thread and the training loop may both add
             self._add_locked(pos)
 
