@@ -451,7 +451,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     BP_CUDA_TRY(cudaEventRecord(c.flushed, e->link));
     c.pending = false;
   }
-  e->uploads.resize(4);
+  e->uploads.resize(8);
   for (auto& u : e->uploads) {
     u.bytes = (size_t)n * 9 + 64;
     BP_CUDA_TRY(cudaMallocHost(&u.host, u.bytes));
@@ -579,7 +579,7 @@ static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64
     e->next_upload = (e->next_upload + 1) % (int)e->uploads.size();
     if (u.used) BP_CUDA_TRY(cudaEventSynchronize(u.done));
     if (!e->upload_worker) {
-      e->upload_worker = new bp::LinkWorker(4);
+      e->upload_worker = new bp::LinkWorker(8);
       const cudaError_t err = e->upload_worker->init();
       if (err != cudaSuccess) {
         delete e->upload_worker;

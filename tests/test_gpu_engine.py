@@ -136,3 +136,23 @@ def test_ck12_pipeline_report_and_baseline_t8():
     cfg8 = eng.EngineConfig(cache_capacity=g["capacity"], batch_size=16384, lookahead=0, num_trainers=8,
                             num_shards=1, seed=11)
     assert eng.run_synchronous_baseline(cfg8, schema, batches).final_store_digest == g["baseline_T8_digest"]
+
+
+@pytest.mark.parametrize("case", ["L8_T1", "L16_T2", "L32_cap550_halving", "auto_cap900"])
+def test_threaded_planner_device_inputs_byte_identical(small_schema, small_batches, case):
+    """The planner-thread path (device-resident batches, preps and plan
+    emission on a second host thread) reproduces the reference reports."""
+    import torch
+
+    eng = _engine()
+    blob = golden("reports_small.json")[case]
+    cfg = _cfg(blob["config"])
+    batches = eng._materialize(small_batches, cfg.iterations)
+    dev = {}
+    for i, b in enumerate(batches):
+        keys, labels, _ = b.packed_occurrences()
+        dev[i] = (torch.from_numpy(keys).cuda(), torch.from_numpy(labels).cuda())
+    pipe = eng._Pipeline(cfg, small_schema, batches, None, None, device_inputs=dev, threaded=True)
+    assert pipe._threaded
+    report = pipe.run()
+    _assert_report(report, blob)
