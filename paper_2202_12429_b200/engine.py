@@ -259,8 +259,8 @@ class _Pipeline:
         self.result = L.StepResult()
         self._inflight: dict = {}
         self._host_refs: dict = {}
-        # planner thread (see _planner_loop): the plain fast path only; fault
-        # injection, event logs and mirror checks keep the single-thread order
+        # planner thread (see _planner_loop); fault injection and event logs
+        # keep the single-thread order
         # (measured: it helps device-resident batches, 0.41 -> 0.37 ms/step,
         # and slows host batches, whose uploads then contend with the
         # training thread -- so by default only with device inputs)
@@ -269,7 +269,7 @@ class _Pipeline:
         if env is not None:
             default_threaded = env == "1"
         self._threaded = (threaded if threaded is not None else default_threaded) and \
-            fault is None and self.events is None and self.snapshots is None
+            fault is None and self.events is None
         self._thread = None
         self._stop = False
         self._planner_error = None
