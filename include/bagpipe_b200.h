@@ -506,9 +506,9 @@ int bp_debug_long_trace(void* d_buf);
 /* Debug: bit 0 turns the store's fetch kernels, bit 1 its write kernels into
  * no-ops (results become wrong; only for measuring the host link's share). */
 int bp_debug_skip_link(int32_t skip);
-/* Debug: {gather ns, calls, rows, scatter ns, calls, rows} of the DMA link
- * mode's host callbacks since the previous call. */
-int bp_debug_link_cb_stats(int64_t* out6);
+/* Debug: {gather ns, calls, rows, scatter ns, calls, rows, upload-copy ns,
+ * calls, bytes} of the host worker jobs since the previous call. */
+int bp_debug_link_cb_stats(int64_t* out9);
 /* Launch shape of the host-link (zero-copy fetch / write-back) kernels:
  * blocks (default 32), threads per block (256) and unused dynamic shared
  * memory per block (default 0; ~200 KB makes a link block own its SM). */

@@ -137,7 +137,7 @@ static void host_copy(const LinkJob* j) {
 }
 
 // Debug counters of the host-link callbacks (bp_debug_link_cb_stats).
-static std::atomic<long long> g_cb_ns[2], g_cb_calls[2], g_cb_rows[2];
+static std::atomic<long long> g_cb_ns[3], g_cb_calls[3], g_cb_rows[3];
 
 struct CbTimer {
   int k;
@@ -238,9 +238,14 @@ struct LinkWorker {
       idle = 0;
       ++processed;
       LinkJob& j = jobs[processed % kRing];
-      if (j.copies) host_copy(&j);
-      else if (j.table_src) link_gather_cb(&j);
-      else link_scatter_cb(&j);
+      if (j.copies) {
+        CbTimer timer{2, (long long)(j.cbytes[0] + j.cbytes[1])};
+        host_copy(&j);
+      }
+      else if (j.table_src)
+        link_gather_cb(&j);
+      else
+        link_scatter_cb(&j);
       std::atomic_thread_fence(std::memory_order_seq_cst);  // table writes before the flag
       flags[32] = processed;
     }
@@ -579,7 +584,7 @@ static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64
     e->next_upload = (e->next_upload + 1) % (int)e->uploads.size();
     if (u.used) BP_CUDA_TRY(cudaEventSynchronize(u.done));
     if (!e->upload_worker) {
-      e->upload_worker = new bp::LinkWorker(8);
+      e->upload_worker = new bp::LinkWorker(1);  // measured: one thread copies fastest on the 16-vCPU box
       const cudaError_t err = e->upload_worker->init();
       if (err != cudaSuccess) {
         delete e->upload_worker;
@@ -590,7 +595,7 @@ static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64
     si = e->staging_i;
     e->staging_i ^= 1;
     BP_CUDA_TRY(cudaStreamWaitEvent(q, e->staging_free[si], 0));
-    // the copy into the pinned slot runs on the upload worker (4 threads);
+    // the copy into the pinned slot runs on the upload worker thread;
     // the stream waits for it, the caller does not (its arrays must stay
     // alive until bp_engine_release_batch)
     bp::LinkJob* j = e->upload_worker->next();
@@ -1199,8 +1204,8 @@ extern "C" int bp_host_rows_bench(float* table, int32_t dim, const uint32_t* ids
 // Debug: {gather ns, calls, rows, scatter ns, calls, rows} of the DMA link
 // mode's host callbacks since the last call (reset).
 extern "C" int bp_debug_link_cb_stats(int64_t* out6) {
-  for (int k = 0; k < 2; ++k) {
-    out6[3 * k] = bp::g_cb_ns[k].exchange(0);
+  for (int k = 0; k < 3; ++k) {
+    out6[3 * k] = bp::g_cb_ns[k].exchange(0);  // out6 holds 9 values
     out6[3 * k + 1] = bp::g_cb_calls[k].exchange(0);
     out6[3 * k + 2] = bp::g_cb_rows[k].exchange(0);
   }

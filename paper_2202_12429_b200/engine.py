@@ -165,7 +165,7 @@ class _Plan:
 
 class _Pipeline:
     EMIT_AHEAD = 3  # plans emitted ahead of dispatch (see _emit_ahead)
-    PREP_AHEAD = 4  # batches prepped (own stream) ahead of entering the planner window
+    PREP_AHEAD = int(os.environ.get("BAGPIPE_B200_PREP_AHEAD", "4"))  # batches prepped ahead of the window
     """One pipelined run (reference engine.py:239-649) on the native engine.
 
     The host keeps the reference's scalar control flow -- window refill,

@@ -129,15 +129,15 @@ def main():
             torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     print(f"{args.steps} steps in {(time.perf_counter() - t0) * 1e3:.2f} ms")
-    if getattr(pipe, "link_mode", 0) == 1:
-        import numpy as np
+    import numpy as np
 
-        from paper_2202_12429_b200 import _lib as L
+    from paper_2202_12429_b200 import _lib as L
 
-        st = np.zeros(6, dtype=np.int64)
-        L.lib().bp_debug_link_cb_stats(st.ctypes.data)
-        print(f"host-link callbacks: gather {st[1]} calls {st[2]} rows {st[0] / 1e3:.0f} us; "
-              f"scatter {st[4]} calls {st[5]} rows {st[3] / 1e3:.0f} us")
+    st = np.zeros(9, dtype=np.int64)
+    L.lib().bp_debug_link_cb_stats(st.ctypes.data)
+    print(f"host workers: gather {st[1]} calls {st[2]} rows {st[0] / 1e3:.0f} us; "
+          f"scatter {st[4]} calls {st[5]} rows {st[3] / 1e3:.0f} us; upload copies {st[7]} calls "
+          f"{st[8] / 1e6:.1f} MB {st[6] / 1e3:.0f} us")
 
 
 if __name__ == "__main__":
