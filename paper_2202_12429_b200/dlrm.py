@@ -204,7 +204,9 @@ class _MasterSGD:
 
     @torch.no_grad()
     def step(self):
-        torch._foreach_add_(self.master, [p.grad for p in self.lowp], alpha=-self.lr)
+        # per tensor: the mixed-dtype foreach path is not CUDA-graph capturable
+        for m, p in zip(self.master, self.lowp):
+            m.add_(p.grad, alpha=-self.lr)
         torch._foreach_copy_(self.lowp, self.master)
 
 
