@@ -156,3 +156,22 @@ def test_threaded_planner_device_inputs_byte_identical(small_schema, small_batch
     assert pipe._threaded
     report = pipe.run()
     _assert_report(report, blob)
+
+
+@pytest.mark.parametrize("split", [True, False])
+@pytest.mark.parametrize("rpc", [0.25, 1.0])
+@pytest.mark.parametrize("capacity", [16_000, 50_000])
+@pytest.mark.parametrize("lookahead", [1, 8, 64, 200])
+@pytest.mark.parametrize("trainers", [1, 2, 4])
+def test_acceptance_criterion2_matrix(acceptance_batches, trainers, lookahead, capacity, rpc, split):
+    """Reference acceptance criteria 2 and 6 (tests/test_acceptance.py:142-153,
+    258-267): the 48-cell matrix T x L x rpc x capacity, with and without the
+    critical/background split, 500 iterations each, every pipelined digest
+    bit-exact with the synchronous baseline (whose T=1 digest is the frozen
+    f2c6d9f7...)."""
+    schema, batches = acceptance_batches
+    eng = _engine()
+    cfg = eng.EngineConfig(cache_capacity=capacity, batch_size=512, lookahead=lookahead, num_trainers=trainers,
+                           num_shards=4, seed=11, rpc_batch_proportion=rpc, split_sync=split)
+    rep = eng.run_pipeline(cfg, schema, batches, trace_fingerprint="zipf1337/512x500")
+    assert rep.final_store_digest == golden("acceptance.json")["baseline"][str(trainers)]
