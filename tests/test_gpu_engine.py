@@ -175,3 +175,20 @@ def test_acceptance_criterion2_matrix(acceptance_batches, trainers, lookahead, c
                            num_shards=4, seed=11, rpc_batch_proportion=rpc, split_sync=split)
     rep = eng.run_pipeline(cfg, schema, batches, trace_fingerprint="zipf1337/512x500")
     assert rep.final_store_digest == golden("acceptance.json")["baseline"][str(trainers)]
+
+
+def test_threaded_mode_equals_serial(small_schema, small_batches):
+    """mode="threaded" (reference engine.py:214-223) produces the serial
+    run's records and digest (the reference asserts byte identity,
+    tests/test_engine.py:275-299)."""
+    import dataclasses
+    import json as _json
+
+    eng = _engine()
+    cfg = _cfg(golden("reports_small.json")["L16_T2"]["config"])
+    serial = eng.run_pipeline(cfg, small_schema, small_batches)
+    threaded = eng.run_pipeline(dataclasses.replace(cfg, mode="threaded"), small_schema, small_batches)
+    a, b = _json.loads(serial.to_json_bytes()), _json.loads(threaded.to_json_bytes())
+    a["config"].pop("mode"), b["config"].pop("mode")
+    assert a == b
+    assert threaded.final_store_digest == serial.final_store_digest
