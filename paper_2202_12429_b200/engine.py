@@ -691,10 +691,13 @@ class _Pipeline:
         return self._report()
 
     def run(self) -> RunReport:
-        self.begin()
-        for pos in range(self.n):
-            self.step(pos)
-        return self.end()
+        try:
+            self.begin()
+            for pos in range(self.n):
+                self.step(pos)
+            return self.end()
+        finally:
+            self._stop_planner()  # also on errors: the thread holds the pipeline alive
 
     def _maintenance(self, pos, chunk, n_ev, n_ev_dirty, drain, n_dr, n_dr_dirty, partial) -> None:
         iteration = self.base + pos
