@@ -353,7 +353,8 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
     from paper_2202_12429_b200.hybrid import EmbeddingExchange
 
     steps, warm = args.steps, args.warmup
-    dcfg = DLRMConfig(emb_optimizer="sgd", emb_lr=0.01, mlp_lr=0.01, mlp_dtype="bf16")
+    dcfg = DLRMConfig(emb_optimizer="sgd", emb_lr=0.01, mlp_lr=0.01, mlp_dtype="bf16",
+                      sorted_grad=os.environ.get("BAGPIPE_B200_SORTED_GRAD", "1") != "0")
     ex = None
     if world > 1:
         from paper_2202_12429_b200.hybrid import PeerExchange
@@ -402,7 +403,8 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
                         "mlp": "PyTorch, bf16 compute copy + fp32 master SGD, one CUDA graph per step (13-512-256-64-16 / 367-1024-1024-512-256-1)",
                         "embedding_optimizer": "sgd", "final_loss": losses[-1] if losses else None,
                         "embedding_stage_ms_per_step": spans[0]},
-            "roofline": {"kernel": "bp::k_embbag_fwd_rows_v4 + k_embbag_bwd (EmbeddingBag fwd+bwd+SGD on cached rows)",
+            "roofline": {"kernel": "bp::k_embbag_fwd_rows_v4 + k_embbag_bwd_staged (EmbeddingBag fwd + sorted-gradient "
+                                   "bwd+SGD on cached rows)",
                          "bound": "hbm", "bytes_per_step": fwd_bytes + bwd_bytes(n_occ, int(u_mean)),
                          "ms_per_step": spans[0], "launches_per_step": 2, "unit": "GB/s",
                          "achieved": (fwd_bytes + bwd_bytes(n_occ, int(u_mean))) / (spans[0] * 1e-3) / 1e9

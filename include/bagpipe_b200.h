@@ -399,6 +399,14 @@ int bp_engine_dlrm_forward(bp_engine* engine, int64_t pos, int32_t plan_slot, in
 int bp_engine_dlrm_backward(bp_engine* engine, int64_t pos, int32_t plan_slot, const float* d_grad,
                             int32_t model_dim, int32_t opt, float lr, float eps, int32_t chunk_slot,
                             int32_t drain_slot, bp_step_result* out);
+/* Sorted-gradient backward (no reference counterpart; DLRM mode): the dense
+ * model stores the pooled-row gradient of occurrence p at row d_rows[p] (from
+ * bp_engine_dlrm_grad_rows: the key-sorted position, bp_prep_occ_rank), and
+ * the EmbeddingBag backward streams it (bp_embbag_backward_sorted). */
+int bp_engine_dlrm_grad_rows(bp_engine* engine, int64_t pos, uint32_t* d_rows);
+int bp_engine_dlrm_backward_sorted(bp_engine* engine, int64_t pos, int32_t plan_slot, const float* d_grad_sorted,
+                                   int32_t model_dim, int32_t opt, float lr, float eps, int32_t chunk_slot,
+                                   int32_t drain_slot, bp_step_result* out);
 int bp_engine_chunk_keys(bp_engine* engine, int32_t chunk_slot, uint64_t* h_out, int64_t n);
 int bp_engine_chunk_view(bp_engine* engine, int32_t chunk_slot, bp_evict_buffers* out);
 int bp_engine_sync(bp_engine* engine);
@@ -437,6 +445,14 @@ int bp_embbag_backward(bp_prep* prep, const float* d_grad, const int64_t* d_occ_
                        float* d_values, int32_t row_stride, const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim,
                        int32_t opt, float lr, float eps, int64_t* d_stats, bp_stream_t stream);
 int bp_prep_occ_sorted_index(bp_prep* prep, uint32_t* d_occ_s, bp_stream_t stream);
+/* d_out[p] = key-sorted position of occurrence p (BP_PREP_OCC_SORTED prep). */
+int bp_prep_occ_rank(bp_prep* prep, uint32_t* d_out, bp_stream_t stream);
+/* backward over gradient rows already in key-sorted order (row j = gradient
+ * of sorted occurrence j): dim in {4, 8, 16, 32}; same update as
+ * bp_embbag_backward, summation order fixed by the data. */
+int bp_embbag_backward_sorted(bp_prep* prep, const float* d_grad_sorted, float* d_values, int32_t row_stride,
+                              const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt, float lr,
+                              float eps, int64_t* d_stats, bp_stream_t stream);
 
 /* ---------------------------------------------------------- peer exchange */
 /* DLRM hybrid parallelism over NVLink peer memory (csrc/peer.cu).  Rank
@@ -498,11 +514,18 @@ int bp_dlrm_interact_forward(const void* d_x, int32_t x_bf16, const float* d_emb
 int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const float* d_emb, const void* d_gout, int32_t g_bf16,
                               int64_t B, int32_t T, int32_t D, int32_t out_stride, void* d_gx, float* d_gemb,
                               bp_stream_t stream);
+/* As bp_dlrm_interact_backward, with gemb row of (b, t) = d_gemb_rows[b*T + t]
+ * (NULL: b*T + t), e.g. the EmbeddingBag's key-sorted order. */
+int bp_dlrm_interact_backward_rows(const void* d_x, int32_t x_bf16, const float* d_emb, const void* d_gout,
+                                   int32_t g_bf16, int64_t B, int32_t T, int32_t D, int32_t out_stride, void* d_gx,
+                                   float* d_gemb, const uint32_t* d_gemb_rows, bp_stream_t stream);
 
 /* ------------------------------------------------------------ utilities */
 /* Debug: per-CTA phase clock64() stamps of the long-segment trainer kernel
  * into d_buf[148][8] (NULL disables; tools/kernel_bench.py --trace). */
 int bp_debug_long_trace(void* d_buf);
+/* Debug: launch shape of bp_embbag_backward_sorted (0 default; tools/kernel_bench.py). */
+int bp_debug_bwd_variant(int32_t variant);
 /* Debug: bit 0 turns the store's fetch kernels, bit 1 its write kernels into
  * no-ops (results become wrong; only for measuring the host link's share). */
 int bp_debug_skip_link(int32_t skip);

@@ -203,6 +203,15 @@ _SIGS = {
     "bp_embbag_backward": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32, c_f32,
                                    c_vp, c_vp]),
     "bp_prep_occ_sorted_index": (c_i32, [c_vp, c_vp, c_vp]),
+    "bp_prep_occ_rank": (c_i32, [c_vp, c_vp, c_vp]),
+    "bp_debug_bwd_variant": (c_i32, [c_i32]),
+    "bp_embbag_backward_sorted": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32, c_f32, c_vp,
+                                          c_vp]),
+    "bp_dlrm_interact_backward_rows": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp,
+                                               c_vp, c_vp, c_vp]),
+    "bp_engine_dlrm_grad_rows": (c_i32, [c_vp, c_i64, c_vp]),
+    "bp_engine_dlrm_backward_sorted": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_f32, c_f32, c_i32, c_i32,
+                                               P(StepResult)]),
     "bp_store_create_ex": (c_i32, [c_vp, c_vp, c_u64, c_i32, c_vp, P(c_vp)]),
 }
 
@@ -244,7 +253,15 @@ def lib() -> C.CDLL:
                 if not torch.cuda.is_available():
                     raise NativeUnavailable("no CUDA device visible: the embedding path runs only on the GPU")
                 torch.cuda.init()
-                _lib = load_library()
+                lb = load_library()
+                # tuning knob: launch shape of the host-link kernels, "blocks,threads,smem_bytes"
+                lc = os.environ.get("BAGPIPE_B200_LINK_CONFIG")
+                if lc:
+                    check(lb.bp_set_link_config(*[int(x) for x in lc.split(",")]), "bp_set_link_config")
+                bv = os.environ.get("BAGPIPE_B200_BWD_VARIANT")  # tuning knob: sorted backward launch shape
+                if bv:
+                    check(lb.bp_debug_bwd_variant(int(bv)), "bp_debug_bwd_variant")
+                _lib = lb
     return _lib
 
 

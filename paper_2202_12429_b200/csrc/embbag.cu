@@ -572,6 +572,473 @@ __global__ void __launch_bounds__(256) k_embbag_bwd_warp(
   }
 }
 
+// Backward over gradient rows already in key-sorted order: the producer (the
+// fused interaction backward, csrc/interact.cu) stored occurrence p's row at
+// its sorted position occ_rank[p], so the random 64-byte gradient gather of
+// k_embbag_bwd_warp becomes a contiguous stream and the kernel is a pure
+// segmented reduce.  Warp tile = T = G * R sorted rows; lane = (row group g,
+// float4 column c): Q lanes per row, G = 32 / Q groups of R consecutive rows,
+// so every load instruction covers G whole rows with fully used sectors.
+// Per lane a sequential segmented sum over its R rows, a segmented scan
+// across the groups (shuffles by Q), the carry-in of each group's first run;
+// each key ending in the tile is then updated by its Q lanes (one 16-byte
+// column each).  Only the tile's first and last runs can span tiles; their
+// bounds come from two broadcast loads.  A spanning key leaves one partial
+// per tile and counts its tiles on an arrival counter at its first tile: the
+// warp that completes the count sums all partials in ascending tile order
+// (groups stride the tiles, fixed shuffle tree) and applies the update -- no
+// second launch, and the order is fixed by the data: run-to-run
+// deterministic.
+constexpr int kSortedRows = 8;  // rows per lane group in k_embbag_bwd_sorted
+
+template <int Q>
+__device__ __forceinline__ bool span_combine(const float4* __restrict__ parts, uint32_t ft, uint32_t nt, bool mid,
+                                             int g, int c, float* __restrict__ row, int opt, float lr, float eps) {
+  constexpr int G = 32 / Q;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc = zero;
+  bool any = false;
+  for (uint32_t k = g; k < nt; k += G) {
+    const uint32_t half = (k == 0 && mid) ? 1u : 0u;
+    const float4 x = __ldcg(parts + (size_t)((ft + k) * 2 + half) * Q + c);
+    acc = any ? f4_add(acc, x) : x;
+    any = true;
+  }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) {
+    float4 o;
+    o.x = __shfl_down_sync(0xffffffffu, acc.x, off * Q);
+    o.y = __shfl_down_sync(0xffffffffu, acc.y, off * Q);
+    o.z = __shfl_down_sync(0xffffffffu, acc.z, off * Q);
+    o.w = __shfl_down_sync(0xffffffffu, acc.w, off * Q);
+    const bool ao = __shfl_down_sync(0xffffffffu, any ? 1 : 0, off * Q) != 0;
+    if (g < off && ao) {
+      acc = any ? f4_add(acc, o) : o;
+      any = true;
+    }
+  }
+  return g == 0 && apply_row4(row, 4 * Q, c, acc, opt, lr, eps);
+}
+
+template <int Q, int R, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_embbag_bwd_sorted(
+    const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start, uint32_t n,
+    const float4* __restrict__ grad, float* __restrict__ values, int row_stride, const int32_t* __restrict__ slots_s,
+    uint8_t* __restrict__ dirty, int opt, float lr, float eps, float4* __restrict__ parts,
+    unsigned int* __restrict__ arrivals, unsigned long long* __restrict__ stats) {
+  constexpr int G = 32 / Q, T = G * R;
+  const unsigned lane = threadIdx.x & 31u;
+  const int c = (int)lane % Q, g = (int)lane / Q;
+  const uint32_t tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint32_t t0 = tile * T;
+  if (t0 >= n) return;
+  const uint32_t rows = min((uint32_t)T, n - t0);
+  const uint32_t r0 = t0 + g * R;  // first row of this lane's group
+  uint32_t sg[R];
+  if (r0 + R <= n) {
+    if constexpr (R % 4 == 0) {
+#pragma unroll
+      for (int k = 0; k < R / 4; ++k) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(seg_of + r0) + k);
+        sg[4 * k] = x.x, sg[4 * k + 1] = x.y, sg[4 * k + 2] = x.z, sg[4 * k + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < R; ++j) sg[j] = seg_of[r0 + j];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) sg[j] = r0 + j < n ? seg_of[r0 + j] : 0xffffffffu;
+  }
+  const uint32_t tile_first = seg_of[t0], tile_last = seg_of[t0 + rows - 1];
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 v[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) v[j] = r0 + j < n ? __ldcs(grad + (size_t)(r0 + j) * Q + c) : zero;
+  // bounds of the two runs that may span tiles (broadcast loads)
+  const uint32_t fa = seg_start[tile_first], fb = seg_start[tile_first + 1];
+  const uint32_t la = seg_start[tile_last], lb = seg_start[tile_last + 1];
+  // rows ending a key's run in the tile: slot loaded now, the cached row
+  // pulled into L2 while the scan runs
+  const uint32_t next_first = __shfl_down_sync(0xffffffffu, sg[0], Q);
+  int32_t slotj[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const bool e = r0 + j < n && ((j < R - 1) ? sg[j + 1] != sg[j] : (g == G - 1 || next_first != sg[j]));
+    slotj[j] = e ? slots_s[sg[j]] : -1;
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (c == 0 && slotj[j] >= 0)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(values + (size_t)slotj[j] * row_stride));
+  bool inner_head = false;
+#pragma unroll
+  for (int j = 1; j < R; ++j) {
+    if (sg[j] == sg[j - 1]) v[j] = f4_add(v[j - 1], v[j]);
+    else inner_head = true;
+  }
+  const uint32_t prev_last = __shfl_up_sync(0xffffffffu, sg[R - 1], Q);
+  const bool first_head = g == 0 || sg[0] != prev_last;
+  bool flag = first_head || inner_head;
+  float4 agg = v[R - 1];
+#pragma unroll
+  for (int off = 1; off < G; off <<= 1) {
+    const bool fo = __shfl_up_sync(0xffffffffu, flag ? 1 : 0, off * Q) != 0;
+    float4 o;
+    o.x = __shfl_up_sync(0xffffffffu, agg.x, off * Q);
+    o.y = __shfl_up_sync(0xffffffffu, agg.y, off * Q);
+    o.z = __shfl_up_sync(0xffffffffu, agg.z, off * Q);
+    o.w = __shfl_up_sync(0xffffffffu, agg.w, off * Q);
+    if (g >= off && !flag) agg = f4_add(o, agg);
+    if (g >= off) flag = flag || fo;
+  }
+  float4 carry;
+  carry.x = __shfl_up_sync(0xffffffffu, agg.x, Q);
+  carry.y = __shfl_up_sync(0xffffffffu, agg.y, Q);
+  carry.z = __shfl_up_sync(0xffffffffu, agg.z, Q);
+  carry.w = __shfl_up_sync(0xffffffffu, agg.w, Q);
+  if (!first_head) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (sg[j] == sg[0]) v[j] = f4_add(carry, v[j]);
+  }
+  const unsigned gm = (Q == 32 ? 0xffffffffu : ((1u << Q) - 1u)) << (g * Q);
+  // spanning keys: the tile's first run if its key extends past either tile
+  // edge, the last run (a different key) if it continues in a later tile
+  const bool span1 = fa < t0 || fb > t0 + rows;
+  const bool span2 = tile_last != tile_first && lb > t0 + rows;
+  // spanning partials first, then their arrivals: the release fence waits
+  // only for these stores, not for the row updates below
+  bool wrote = false;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (slotj[j] >= 0 && (sg[j] == tile_first ? span1 : (sg[j] == tile_last && span2))) {
+      parts[(size_t)(tile * 2 + (sg[j] == tile_first ? 0 : 1)) * Q + c] = v[j];
+      slotj[j] = -1;  // not an in-tile update
+      wrote = true;
+    }
+  }
+  unsigned last = 0;  // bit k: this warp completed spanning key k's arrivals
+  if (span1 || span2) {
+    if (wrote) __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (!(k == 0 ? span1 : span2)) continue;
+        // a key not in the cache (slot < 0) is skipped on every tile: no partials, no arrivals
+        if (slots_s[k == 0 ? tile_first : tile_last] < 0) continue;
+        const uint32_t a = k == 0 ? fa : la, b = k == 0 ? fb : lb;
+        const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
+        if (atomicAdd(arrivals + ft, 1u) == nt - 1) last |= 1u << k;
+      }
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+  }
+  // in-tile keys: the row loads of a batch of end rows issued before any of
+  // its stores (the compiler cannot move loads across possibly aliasing stores)
+  unsigned n_nz = 0;
+  constexpr int B = R < 4 ? R : 4;
+#pragma unroll
+  for (int j0 = 0; j0 < R; j0 += B) {
+    float4 w[B], acc[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int32_t sl = slotj[j0 + u];
+      const float4* row = reinterpret_cast<const float4*>(values + (size_t)(sl >= 0 ? sl : 0) * row_stride);
+      w[u] = sl >= 0 ? row[c] : zero;
+      acc[u] = (sl >= 0 && opt == BP_OPT_ADAGRAD) ? row[Q + c] : zero;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int32_t sl = slotj[j0 + u];
+      bool nz = false;
+      if (sl >= 0) {
+        const float4 gg = v[j0 + u];
+        float4 x = w[u], a = acc[u];
+        x.x = upd1(x.x, a.x, gg.x, opt, lr, eps);
+        x.y = upd1(x.y, a.y, gg.y, opt, lr, eps);
+        x.z = upd1(x.z, a.z, gg.z, opt, lr, eps);
+        x.w = upd1(x.w, a.w, gg.w, opt, lr, eps);
+        float4* row = reinterpret_cast<float4*>(values + (size_t)sl * row_stride);
+        row[c] = x;
+        if (opt == BP_OPT_ADAGRAD) row[Q + c] = a;
+        nz = gg.x != 0.f || gg.y != 0.f || gg.z != 0.f || gg.w != 0.f;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, nz);
+      if (sl >= 0 && c == 0 && (bal & gm)) {
+        if (dirty) dirty[sl] = 1;
+        ++n_nz;
+      }
+    }
+  }
+  // the warp that completed a spanning key's arrivals combines its partials
+  // (ascending tiles, fixed tree) and applies the update
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (!((last >> k) & 1u)) continue;  // warp-uniform
+    __threadfence();
+    const uint32_t key = k == 0 ? tile_first : tile_last;
+    const uint32_t a = k == 0 ? fa : la, b = k == 0 ? fb : lb;
+    const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
+    const int32_t slot = slots_s[key];
+    const bool nz = span_combine<Q>(parts, ft, nt, a != ft * T, g, c, values + (size_t)slot * row_stride, opt, lr,
+                                    eps);
+    if (__ballot_sync(0xffffffffu, nz) != 0 && lane == 0) {
+      if (dirty) dirty[slot] = 1;
+      ++n_nz;
+    }
+  }
+  if (stats) {
+    for (int off = 16; off > 0; off >>= 1) n_nz += __shfl_down_sync(0xffffffffu, n_nz, off);
+    if (lane == 0 && n_nz) atomicAdd(&stats[1], (unsigned long long)n_nz);
+  }
+}
+
+// Staged backward over sorted gradients (the default of
+// bp_embbag_backward_sorted): a CTA owns a 32 KB tile of T = 2048/Q sorted
+// rows, pulled into shared memory by one bulk async copy (TMA engine,
+// mbarrier completion) together with its segment ids -- no per-thread load
+// queues.  While the copy is in flight the CTA stages the cache slots of the
+// tile's keys (a contiguous range of unique ids) in shared memory and pulls
+// their rows into L2.  In shared memory: 256/Q lane groups of T/(256/Q)
+// consecutive rows turn their rows into running segmented sums in place; a
+// two-level segmented scan of the group totals (warp shuffles, then the 8
+// warp totals in a fixed sequential order) gives each group its carry-in;
+// then every (row, column) item of a key's last row in the tile applies the
+// update (cache-row loads batched ahead of their stores).  Spanning keys:
+// partials + arrival counters as in k_embbag_bwd_sorted.  Fixed orders
+// throughout: run-to-run deterministic.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+constexpr int kStagedF4 = 2048;  // float4 per k_embbag_bwd_staged tile (32 KB)
+
+template <int Q>
+__global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
+    const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start, uint32_t n,
+    const float4* __restrict__ grad, float* __restrict__ values, int row_stride, const int32_t* __restrict__ slots_s,
+    uint8_t* __restrict__ dirty, int opt, float lr, float eps, float4* __restrict__ parts,
+    unsigned int* __restrict__ arrivals, unsigned long long* __restrict__ stats) {
+  constexpr int T = kStagedF4 / Q, NG = 256 / Q, RPG = T / NG, GW = 32 / Q;
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  float4* tile = reinterpret_cast<float4*>(st_smem);          // [T][Q]
+  uint32_t* sgs = reinterpret_cast<uint32_t*>(tile + T * Q);  // [T]
+  int32_t* tslot = reinterpret_cast<int32_t*>(sgs + T);          // [T] cache slots of the tile's keys
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ float4 gcarry[NG][Q];
+  __shared__ float4 wagg[8][Q];
+  __shared__ int wflag[8][Q];
+  __shared__ uint8_t ghead[NG];
+  __shared__ unsigned last_sh, nnz_sh;
+  const uint32_t t0 = blockIdx.x * T;
+  const uint32_t rows = min((uint32_t)T, n - t0);
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    last_sh = 0;
+    nnz_sh = 0;
+  }
+  __syncthreads();
+  const uint32_t seg_bytes = (rows / 4) * 16;  // whole 16-byte chunks of segment ids
+  if (tid == 0) {
+    const uint32_t gbytes = rows * Q * 16;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
+                 "r"(gbytes + seg_bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(tile)),
+                 "l"(grad + (size_t)t0 * Q), "r"(gbytes), "r"(smem_u32(&bar))
+                 : "memory");
+    if (seg_bytes)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(sgs)),
+                   "l"(seg_of + t0), "r"(seg_bytes), "r"(smem_u32(&bar))
+                   : "memory");
+  }
+  // meanwhile: the bounds of the tile's first and last runs, and the cache
+  // slots of its keys -- a contiguous range of unique ids -- staged in shared
+  // memory, their rows pulled into L2 for the updates
+  const uint32_t tile_first = seg_of[t0], tile_last = seg_of[t0 + rows - 1];
+  const uint32_t fa = seg_start[tile_first], fb = seg_start[tile_first + 1];
+  const uint32_t la = seg_start[tile_last], lb = seg_start[tile_last + 1];
+  const uint32_t nu = tile_last - tile_first + 1;
+  for (uint32_t i = tid; i < nu; i += 256) {
+    const int32_t sl = slots_s[tile_first + i];
+    tslot[i] = sl;
+    if (sl >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(values + (size_t)sl * row_stride));
+  }
+  if (tid < rows - seg_bytes / 4) sgs[seg_bytes / 4 + tid] = seg_of[t0 + seg_bytes / 4 + tid];  // < 4 tail ids
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT%=;\n}\n" ::"r"(
+          smem_u32(&bar))
+      : "memory");
+  __syncthreads();  // the tail segment ids
+  const int c = (int)(tid % Q), gi = (int)(tid / Q), w = (int)(tid >> 5), gw = (int)((tid & 31) / Q);
+  const uint32_t r0 = gi * RPG;
+  // pass 1: running segmented sums of the group's rows, in place
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc = zero;
+  bool flag = false;
+  if (r0 < rows) {
+    uint32_t ps = sgs[r0];
+    acc = tile[r0 * Q + c];
+    flag = r0 == 0 || sgs[r0 - 1] != ps;
+    if (c == 0) ghead[gi] = flag ? 1 : 0;
+    const uint32_t re = min(r0 + RPG, rows);
+    for (uint32_t r = r0 + 1; r < re; ++r) {
+      const uint32_t sr = sgs[r];
+      const float4 x = tile[r * Q + c];
+      if (sr == ps) {
+        acc = f4_add(acc, x);
+      } else {
+        acc = x;
+        flag = true;
+      }
+      tile[r * Q + c] = acc;
+      ps = sr;
+    }
+  } else if (c == 0) {
+    ghead[gi] = 1;
+  }
+  // pass 2: segmented scan of the group totals; warp level first
+  float4 inc = acc;
+  bool finc = flag;
+#pragma unroll
+  for (int off = 1; off < GW; off <<= 1) {
+    const bool fo = __shfl_up_sync(0xffffffffu, finc ? 1 : 0, off * Q) != 0;
+    float4 o;
+    o.x = __shfl_up_sync(0xffffffffu, inc.x, off * Q);
+    o.y = __shfl_up_sync(0xffffffffu, inc.y, off * Q);
+    o.z = __shfl_up_sync(0xffffffffu, inc.z, off * Q);
+    o.w = __shfl_up_sync(0xffffffffu, inc.w, off * Q);
+    if (gw >= off && !finc) inc = f4_add(o, inc);
+    if (gw >= off) finc = finc || fo;
+  }
+  if (gw == GW - 1) {
+    wagg[w][c] = inc;
+    wflag[w][c] = finc ? 1 : 0;
+  }
+  // exclusive (within the warp) value for this group
+  float4 ex;
+  ex.x = __shfl_up_sync(0xffffffffu, inc.x, Q);
+  ex.y = __shfl_up_sync(0xffffffffu, inc.y, Q);
+  ex.z = __shfl_up_sync(0xffffffffu, inc.z, Q);
+  ex.w = __shfl_up_sync(0xffffffffu, inc.w, Q);
+  const bool fex = __shfl_up_sync(0xffffffffu, finc ? 1 : 0, Q) != 0;
+  __syncthreads();
+  // carry into this warp: the warp totals before it, in order
+  float4 cw = zero;
+  for (int k = 0; k < w; ++k) cw = wflag[k][c] ? wagg[k][c] : f4_add(cw, wagg[k][c]);
+  const float4 carry = gw == 0 ? cw : (fex ? ex : f4_add(cw, ex));
+  gcarry[gi][c] = carry;
+  __syncthreads();
+  // spanning keys of the tile
+  const bool span1 = fa < t0 || fb > t0 + rows;
+  const bool span2 = tile_last != tile_first && lb > t0 + rows;
+  // pass 3: (row, column) items; a key's last row in the tile holds its sum
+  unsigned my_nz = 0;
+  bool wrote = false;
+  constexpr int ITEMS = T * Q / 256, B = 4;
+#pragma unroll 1
+  for (int k0 = 0; k0 < ITEMS; k0 += B) {
+    int32_t sl[B];
+    float4 val[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const uint32_t r = (uint32_t)(tid / Q) + (uint32_t)(k0 + u) * NG;
+      sl[u] = -1;
+      if (r >= rows) continue;
+      const uint32_t s = sgs[r];
+      if (r + 1 < rows && sgs[r + 1] == s) continue;  // not the last row of its run
+      const int32_t slot = tslot[s - tile_first];
+      if (slot < 0) continue;
+      const uint32_t g = r / RPG;
+      float4 x = tile[r * Q + c];
+      if (!ghead[g] && s == sgs[g * RPG]) x = f4_add(gcarry[g][c], x);
+      if (s == tile_first ? span1 : (s == tile_last && span2)) {
+        parts[(size_t)(blockIdx.x * 2 + (s == tile_first ? 0 : 1)) * Q + c] = x;
+        wrote = true;
+        continue;
+      }
+      sl[u] = slot;
+      val[u] = x;
+    }
+    float4 wv[B], av[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const float4* row = reinterpret_cast<const float4*>(values + (size_t)(sl[u] >= 0 ? sl[u] : 0) * row_stride);
+      wv[u] = sl[u] >= 0 ? row[c] : zero;
+      av[u] = (sl[u] >= 0 && opt == BP_OPT_ADAGRAD) ? row[Q + c] : zero;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      bool nz = false;
+      if (sl[u] >= 0) {
+        const float4 gg = val[u];
+        float4 x = wv[u], a = av[u];
+        x.x = upd1(x.x, a.x, gg.x, opt, lr, eps);
+        x.y = upd1(x.y, a.y, gg.y, opt, lr, eps);
+        x.z = upd1(x.z, a.z, gg.z, opt, lr, eps);
+        x.w = upd1(x.w, a.w, gg.w, opt, lr, eps);
+        float4* row = reinterpret_cast<float4*>(values + (size_t)sl[u] * row_stride);
+        row[c] = x;
+        if (opt == BP_OPT_ADAGRAD) row[Q + c] = a;
+        nz = gg.x != 0.f || gg.y != 0.f || gg.z != 0.f || gg.w != 0.f;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, nz);
+      const unsigned gm = (Q == 32 ? 0xffffffffu : ((1u << Q) - 1u)) << ((tid & 31) / Q * Q);
+      if (sl[u] >= 0 && c == 0 && (bal & gm)) {
+        if (dirty) dirty[sl[u]] = 1;
+        ++my_nz;
+      }
+    }
+  }
+  if (span1 || span2) {
+    if (wrote) __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      unsigned lst = 0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (!(k == 0 ? span1 : span2)) continue;
+        if (tslot[k == 0 ? 0 : nu - 1] < 0) continue;
+        const uint32_t a = k == 0 ? fa : la, b = k == 0 ? fb : lb;
+        const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
+        if (atomicAdd(arrivals + ft, 1u) == nt - 1) lst |= 1u << k;
+      }
+      last_sh = lst;
+    }
+    __syncthreads();
+    const unsigned lst = last_sh;
+    if (lst && w == 0) {
+      __threadfence();
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (!((lst >> k) & 1u)) continue;
+        const uint32_t key = k == 0 ? tile_first : tile_last;
+        const uint32_t a = k == 0 ? fa : la, b = k == 0 ? fb : lb;
+        const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
+        const int32_t slot = slots_s[key];
+        const bool nz = span_combine<Q>(parts, ft, nt, a != ft * T, (int)(tid / Q), c,
+                                        values + (size_t)slot * row_stride, opt, lr, eps);
+        if (__ballot_sync(0xffffffffu, nz) != 0 && tid == 0) {
+          if (dirty) dirty[slot] = 1;
+          ++my_nz;
+        }
+      }
+    }
+  }
+  if (stats) {
+    for (int off = 16; off > 0; off >>= 1) my_nz += __shfl_down_sync(0xffffffffu, my_nz, off);
+    if ((tid & 31) == 0 && my_nz) atomicAdd(&nnz_sh, my_nz);
+    __syncthreads();
+    if (tid == 0 && nnz_sh) atomicAdd(&stats[1], (unsigned long long)nnz_sh);
+  }
+}
+
 // Keys spanning several tiles, listed by the tile kernels at the key's first
 // tile: up to kSpanWarpTiles tiles (the many keys that merely cross a tile
 // boundary) one warp per key, longer ones (the Zipf-hot rows) one CTA per
@@ -828,6 +1295,108 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
                                                                d_slots_s, d_dirty, dim, row_stride, opt, lr, eps,
                                                                (unsigned long long*)d_stats)));
   BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+// debug: the kernel behind bp_embbag_backward_sorted (0: k_embbag_bwd_staged,
+// the default -- measured fastest inside the DLRM step; warp tiles: 1: R=8 x 3
+// CTAs/SM, 2: R=4 x 4, 3: R=8 x 2)
+static int g_bwd_variant = 0;
+
+extern "C" int bp_debug_bwd_variant(int32_t v) {
+  g_bwd_variant = v;
+  return BP_OK;
+}
+
+template <int R, int MINB>
+static int launch_bwd_sorted(bp_prep* P, const float* d_grad_sorted, float* d_values, int32_t row_stride,
+                             const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt, float lr,
+                             float eps, int64_t* d_stats, cudaStream_t s) {
+  using namespace bp;
+  const int q = dim / 4, T = (32 / q) * R;
+  const long long tiles = (P->n_occ + T - 1) / T;
+  // one allocation: tile partials (2 per tile) and the arrival counters
+  const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
+  char* scratch = nullptr;
+  BP_CUDA_TRY(pool_alloc(&scratch, parts_bytes + tiles * sizeof(unsigned int) + 256, s));
+  float4* parts = reinterpret_cast<float4*>(scratch);
+  unsigned int* arrivals = reinterpret_cast<unsigned int*>(scratch + parts_bytes);
+  BP_CUDA_TRY(cudaMemsetAsync(arrivals, 0, tiles * sizeof(unsigned int), s));
+  const unsigned blocks = (unsigned)((tiles + 7) / 8);
+#define BP_BWD_SORTED(QQ)                                                                                         \
+  k_embbag_bwd_sorted<QQ, R, MINB><<<blocks, 256, 0, s>>>(P->d_seg_of, P->d_seg_start, (uint32_t)P->n_occ,        \
+                                                          reinterpret_cast<const float4*>(d_grad_sorted), d_values, \
+                                                          row_stride, d_slots_s, d_dirty, opt, lr, eps, parts,  \
+                                                          arrivals, (unsigned long long*)d_stats)
+  switch (q) {
+    case 1: BP_BWD_SORTED(1); break;
+    case 2: BP_BWD_SORTED(2); break;
+    case 4: BP_BWD_SORTED(4); break;
+    default: BP_BWD_SORTED(8); break;
+  }
+#undef BP_BWD_SORTED
+  BP_LAUNCH_CHECK();
+  cudaFreeAsync(scratch, s);
+  return BP_OK;
+}
+
+extern "C" int bp_embbag_backward_sorted(bp_prep* P, const float* d_grad_sorted, float* d_values, int32_t row_stride,
+                                         const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt,
+                                         float lr, float eps, int64_t* d_stats, bp_stream_t stream) {
+  using namespace bp;
+  if (!P->d_seg_of || (dim & 3) != 0 || (row_stride & 3) != 0 || dim > 32 || (32 % dim) != 0) return BP_ERR_INVALID;
+  if (opt == BP_OPT_ADAGRAD && row_stride < 2 * dim) return BP_ERR_INVALID;
+  if (P->n_occ == 0) return BP_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (g_bwd_variant) {
+    case 0: {
+      const int q = dim / 4, T = kStagedF4 / q;
+      const unsigned tiles = (unsigned)((P->n_occ + T - 1) / T);
+      const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
+      char* scratch = nullptr;
+      BP_CUDA_TRY(pool_alloc(&scratch, parts_bytes + tiles * sizeof(unsigned int) + 256, s));
+      float4* parts = reinterpret_cast<float4*>(scratch);
+      unsigned int* arrivals = reinterpret_cast<unsigned int*>(scratch + parts_bytes);
+      BP_CUDA_TRY(cudaMemsetAsync(arrivals, 0, tiles * sizeof(unsigned int), s));
+      const size_t smem = (size_t)T * q * sizeof(float4) + 2 * (size_t)T * sizeof(uint32_t);
+#define BP_BWD_STAGED(QQ)                                                                                      \
+  {                                                                                                            \
+    static bool attr = false;                                                                                  \
+    if (!attr) {                                                                                               \
+      BP_CUDA_TRY(cudaFuncSetAttribute(k_embbag_bwd_staged<QQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                       (int)smem));                                                            \
+      attr = true;                                                                                             \
+    }                                                                                                          \
+    k_embbag_bwd_staged<QQ><<<tiles, 256, smem, s>>>(P->d_seg_of, P->d_seg_start, (uint32_t)P->n_occ,           \
+                                                     reinterpret_cast<const float4*>(d_grad_sorted), d_values,  \
+                                                     row_stride, d_slots_s, d_dirty, opt, lr, eps, parts,       \
+                                                     arrivals, (unsigned long long*)d_stats);                   \
+  }
+      switch (q) {
+        case 1: BP_BWD_STAGED(1); break;
+        case 2: BP_BWD_STAGED(2); break;
+        case 4: BP_BWD_STAGED(4); break;
+        default: BP_BWD_STAGED(8); break;
+      }
+#undef BP_BWD_STAGED
+      BP_LAUNCH_CHECK();
+      cudaFreeAsync(scratch, s);
+      return BP_OK;
+    }
+    case 1: return launch_bwd_sorted<8, 3>(P, d_grad_sorted, d_values, row_stride, d_slots_s, d_dirty, dim, opt, lr,
+                                           eps, d_stats, s);
+    case 2: return launch_bwd_sorted<4, 4>(P, d_grad_sorted, d_values, row_stride, d_slots_s, d_dirty, dim, opt, lr,
+                                           eps, d_stats, s);
+    default: return launch_bwd_sorted<8, 2>(P, d_grad_sorted, d_values, row_stride, d_slots_s, d_dirty, dim, opt, lr,
+                                            eps, d_stats, s);  // 3
+  }
+}
+
+extern "C" int bp_prep_occ_rank(bp_prep* P, uint32_t* d_out, bp_stream_t stream) {
+  if (!P->d_occ_rank) return BP_ERR_INVALID;
+  if (P->n_occ == 0) return BP_OK;
+  BP_CUDA_TRY(cudaMemcpyAsync(d_out, P->d_occ_rank, P->n_occ * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                              (cudaStream_t)stream));
   return BP_OK;
 }
 

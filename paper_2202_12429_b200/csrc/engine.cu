@@ -1078,6 +1078,35 @@ extern "C" int bp_engine_dlrm_backward(bp_engine* e, int64_t pos, int32_t plan_s
   return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
 }
 
+// Sorted-gradient variant: d_out[p] = key-sorted position of occurrence p of
+// batch `pos` (compute stream), for the dense model's interaction backward
+// to store the pooled-row gradients in that order; bp_engine_dlrm_backward_
+// sorted then reduces them as a contiguous stream.
+extern "C" int bp_engine_dlrm_grad_rows(bp_engine* e, int64_t pos, uint32_t* d_out) {
+  using namespace bp;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  return bp_prep_occ_rank(P, d_out, e->compute);
+}
+
+extern "C" int bp_engine_dlrm_backward_sorted(bp_engine* e, int64_t pos, int32_t plan_slot,
+                                              const float* d_grad_sorted, int32_t model_dim, int32_t opt, float lr,
+                                              float eps, int32_t chunk_slot, int32_t drain_slot,
+                                              bp_step_result* out) {
+  using namespace bp;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  PlanSlot& ps = e->plans[plan_slot];
+  bp_cache_view cv;
+  bp_cache_get_view(e->cache, &cv);
+  stage_begin(e, kStageTrainer, e->compute);
+  int rc = bp_embbag_backward_sorted(P, d_grad_sorted, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim,
+                                     opt, lr, eps, e->stats, e->compute);
+  stage_end(e, kStageTrainer, e->compute);
+  if (rc) return rc;
+  return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
+}
+
 // DLRM hybrid parallel over NVLink peer memory (csrc/peer.cu): the same two
 // halves, the forward storing pooled rows into the example owners' buffers,
 // the backward loading gradient rows from them.

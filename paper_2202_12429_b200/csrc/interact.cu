@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd(const void* __re
                                                                 const float* __restrict__ emb,
                                                                 const void* __restrict__ gout, int g_bf16,
                                                                 long long B, int T, int D, int out_stride,
-                                                                void* __restrict__ gx, float* __restrict__ gemb) {
+                                                                void* __restrict__ gx, float* __restrict__ gemb,
+                                                                const uint32_t* __restrict__ gemb_rows) {
   extern __shared__ float ix_smem[];
   const int n = T + 1, ld = D + 1, lg = n + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd(const void* __re
       float acc = 0.f;
       for (int j = 0; j < n; ++j) acc = fmaf(G[i * lg + j], z[j * ld + d], acc);
       if (i == 0) st_any(gx, b * D + d, acc + ld_any(gout, o + d, g_bf16), x_bf16);
-      else gemb[(b * T + (i - 1)) * D + d] = acc;
+      else gemb[(gemb_rows ? (long long)gemb_rows[b * T + (i - 1)] : b * T + (i - 1)) * D + d] = acc;
     }
     __syncwarp();
   }
@@ -168,7 +169,8 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
                                                                     const float* __restrict__ emb,
                                                                     const void* __restrict__ gout, int g_bf16,
                                                                     long long B, int T, int out_stride,
-                                                                    void* __restrict__ gx, float* __restrict__ gemb) {
+                                                                    void* __restrict__ gx, float* __restrict__ gemb,
+                                                                    const uint32_t* __restrict__ gemb_rows) {
   extern __shared__ float ix_smem[];
   constexpr int LG = 33;  // G row stride (odd)
   const int n = T + 1;
@@ -176,6 +178,8 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
   float* z = ix_smem + warp * (32 * D + 32 * LG);
   float* G = z + 32 * D;
   for (long long b = (long long)blockIdx.x * kIxWarps + warp; b < B; b += (long long)gridDim.x * kIxWarps) {
+    const long long p = b * T + (lane - 1);  // this lane's embedding-gradient row (lanes 1..T)
+    const long long drow = (gemb_rows && lane >= 1 && lane < n) ? (long long)gemb_rows[p] : p;
     for (int e = lane; e < n * D; e += 32)
       z[e] = e < D ? ld_any(x, b * D + e, x_bf16) : emb[b * T * D + (e - D)];
     const long long ob = b * out_stride;
@@ -210,7 +214,7 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
 #pragma unroll
         for (int d = 0; d < D; ++d) st_any(gx, b * D + d, acc[d] + ld_any(gout, ob + d, g_bf16), x_bf16);
       } else {
-        float4* dst = reinterpret_cast<float4*>(gemb + (b * T + (lane - 1)) * D);
+        float4* dst = reinterpret_cast<float4*>(gemb + drow * D);
 #pragma unroll
         for (int d = 0; d < D; d += 4) dst[d / 4] = make_float4(acc[d], acc[d + 1], acc[d + 2], acc[d + 3]);
       }
@@ -274,9 +278,25 @@ extern "C" int bp_dlrm_interact_forward(const void* d_x, int32_t x_bf16, const f
   return BP_OK;
 }
 
+extern "C" int bp_dlrm_interact_backward_rows(const void* d_x, int32_t x_bf16, const float* d_emb,
+                                              const void* d_gout, int32_t g_bf16, int64_t B, int32_t T, int32_t D,
+                                              int32_t out_stride, void* d_gx, float* d_gemb,
+                                              const uint32_t* d_gemb_rows, bp_stream_t stream);
+
 extern "C" int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const float* d_emb, const void* d_gout,
                                          int32_t g_bf16, int64_t B, int32_t T, int32_t D, int32_t out_stride,
                                          void* d_gx, float* d_gemb, bp_stream_t stream) {
+  return bp_dlrm_interact_backward_rows(d_x, x_bf16, d_emb, d_gout, g_bf16, B, T, D, out_stride, d_gx, d_gemb,
+                                        nullptr, stream);
+}
+
+// d_gemb_rows (optional): embedding-gradient row of (b, t) = d_gemb_rows[b*T + t]
+// instead of b*T + t -- the EmbeddingBag's key-sorted order (bp_prep_occ_rank),
+// so bp_embbag_backward_sorted streams it.
+extern "C" int bp_dlrm_interact_backward_rows(const void* d_x, int32_t x_bf16, const float* d_emb,
+                                              const void* d_gout, int32_t g_bf16, int64_t B, int32_t T, int32_t D,
+                                              int32_t out_stride, void* d_gx, float* d_gemb,
+                                              const uint32_t* d_gemb_rows, bp_stream_t stream) {
   using namespace bp;
   const int rc = check_shape(B, T, D, out_stride);
   if (rc != BP_OK) return rc;
@@ -288,7 +308,7 @@ extern "C" int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const 
   {                                                                                                                \
     BP_CUDA_TRY(cudaFuncSetAttribute(k_interact_bwd_reg<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     k_interact_bwd_reg<DD><<<(unsigned)nblk, kIxWarps * 32, sm, (cudaStream_t)stream>>>(                          \
-        d_x, x_bf16, d_emb, d_gout, g_bf16, B, T, out_stride, d_gx, d_gemb);                                         \
+        d_x, x_bf16, d_emb, d_gout, g_bf16, B, T, out_stride, d_gx, d_gemb, d_gemb_rows);                                         \
   }
     switch (D) {
       case 4: BP_IX_BWD(4); break;
@@ -304,7 +324,7 @@ extern "C" int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const 
   BP_CUDA_TRY(cudaFuncSetAttribute(k_interact_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const long long blocks = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * 16);
   k_interact_bwd<<<(unsigned)blocks, kIxWarps * 32, smem, (cudaStream_t)stream>>>(
-      d_x, x_bf16, d_emb, d_gout, g_bf16, B, T, D, out_stride, d_gx, d_gemb);
+      d_x, x_bf16, d_emb, d_gout, g_bf16, B, T, D, out_stride, d_gx, d_gemb, d_gemb_rows);
   BP_LAUNCH_CHECK();
   return BP_OK;
 }

@@ -105,6 +105,7 @@ struct bp_prep {
   uint32_t* d_occ_k;
   uint32_t* d_occ_s;       // occurrence -> key-sorted unique index (BP_PREP_OCC_SORTED)
   uint32_t* d_seg_of;      // sorted position -> key-sorted unique index (BP_PREP_OCC_SORTED)
+  uint32_t* d_occ_rank;    // occurrence -> sorted position (BP_PREP_OCC_SORTED)
   long long* d_rank_bounds;
   uint32_t* d_long;        // segments with >= kLongSeg occurrences: very long ones from the
                            // front, the others from the back (capacity long_cap)

@@ -113,12 +113,14 @@ __global__ void k_prep_perm(const uint32_t* __restrict__ pos, const uint32_t* __
 __global__ void k_prep_occ_k(const uint32_t* __restrict__ pos, const uint32_t* __restrict__ head,
                              const uint32_t* __restrict__ segx, long long n, const uint32_t* __restrict__ perm_s2k,
                              uint32_t* __restrict__ occ_k, uint32_t* __restrict__ occ_s,
-                             uint32_t* __restrict__ seg_of) {
+                             uint32_t* __restrict__ seg_of, uint32_t* __restrict__ occ_rank) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
     const uint32_t s = segx[j] + head[j] - 1u;  // inclusive segment index
-    if (occ_k) occ_k[pos[j]] = perm_s2k[s];
-    if (occ_s) occ_s[pos[j]] = s;
+    const uint32_t p = pos[j];
+    if (occ_k) occ_k[p] = perm_s2k[s];
+    if (occ_s) occ_s[p] = s;
     if (seg_of) seg_of[j] = s;
+    if (occ_rank) occ_rank[p] = (uint32_t)j;
   }
 }
 
@@ -290,7 +292,7 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
                                 (unsigned long long*)P->d_num_long, P->long_cap);
   if (P->flags & (BP_PREP_OCC_INDEX | BP_PREP_OCC_SORTED))
     k_prep_occ_k<<<g, 256, 0, s>>>(P->d_occ_pos, head, segx, n, P->d_perm_s2k, P->d_occ_k, P->d_occ_s,
-                                   P->d_seg_of);
+                                   P->d_seg_of, P->d_occ_rank);
   BP_LAUNCH_CHECK();
   return BP_OK;
 }
@@ -322,6 +324,7 @@ static size_t prep_layout(bp_prep* P, char* base, long long n, int num_ranks, in
   P->d_occ_k = (flags & BP_PREP_OCC_INDEX) ? c.take<uint32_t>(n) : nullptr;
   P->d_occ_s = (flags & BP_PREP_OCC_SORTED) ? c.take<uint32_t>(n) : nullptr;
   P->d_seg_of = (flags & BP_PREP_OCC_SORTED) ? c.take<uint32_t>(n) : nullptr;
+  P->d_occ_rank = (flags & BP_PREP_OCC_SORTED) ? c.take<uint32_t>(n) : nullptr;
   P->d_rank_bounds = c.take<long long>(num_ranks + 1);
   P->long_cap = n / kLongSeg + 1;
   P->d_long = c.take<uint32_t>(P->long_cap);

@@ -60,7 +60,7 @@ class _Interact(torch.autograd.Function):
     """Fused DLRM interaction (csrc/interact.cu): [x | tril(z z^T) | 0-pad]."""
 
     @staticmethod
-    def forward(ctx, x, emb, out_stride: int):
+    def forward(ctx, x, emb, out_stride: int, grad_rows=None):
         x = x.contiguous()
         emb = emb.contiguous().float()
         b, t, d = emb.shape
@@ -70,6 +70,7 @@ class _Interact(torch.autograd.Function):
                                                  out_stride, L.stream_ptr()), "bp_dlrm_interact_forward")
         ctx.save_for_backward(x, emb)
         ctx.out_stride = out_stride
+        ctx.grad_rows = grad_rows
         return out
 
     @staticmethod
@@ -79,11 +80,15 @@ class _Interact(torch.autograd.Function):
         gout = gout.contiguous()
         gx = torch.empty_like(x)
         gemb = torch.empty_like(emb)
-        L.check(L.lib().bp_dlrm_interact_backward(L.ptr(x), int(x.dtype == torch.bfloat16), L.ptr(emb), L.ptr(gout),
-                                                  int(gout.dtype == torch.bfloat16), b, t, d, ctx.out_stride,
-                                                  L.ptr(gx), L.ptr(gemb), L.stream_ptr()),
-                "bp_dlrm_interact_backward")
-        return gx, gemb, None
+        # grad_rows (optional): row of (b, t) in gemb -- the EmbeddingBag's
+        # key-sorted order, so the embedding backward streams it
+        rows = ctx.grad_rows
+        L.check(L.lib().bp_dlrm_interact_backward_rows(L.ptr(x), int(x.dtype == torch.bfloat16), L.ptr(emb),
+                                                       L.ptr(gout), int(gout.dtype == torch.bfloat16), b, t, d,
+                                                       ctx.out_stride, L.ptr(gx), L.ptr(gemb),
+                                                       L.ptr(rows) if rows is not None else None, L.stream_ptr()),
+                "bp_dlrm_interact_backward_rows")
+        return gx, gemb, None, None
 
 
 def _pad8(n: int) -> int:
@@ -149,13 +154,16 @@ class DLRMDense(nn.Module):
         # advanced-indexing form zz[:, li, lj]
         self.register_buffer("tril_flat", li * n + lj, persistent=False)
 
-    def forward(self, dense: torch.Tensor, pooled: torch.Tensor) -> torch.Tensor:
+    def forward(self, dense: torch.Tensor, pooled: torch.Tensor, grad_rows: torch.Tensor | None = None) -> torch.Tensor:
+        """grad_rows (CUDA only, int32 [B*T]): store the gradient of pooled row
+        (b, t) at row grad_rows[b*T + t] of pooled.grad (a permutation)."""
         if dense.shape[1] == self.num_dense and self.dense_pad:
             dense = nn.functional.pad(dense, (0, self.dense_pad))
         x = _run_mlp(self.bottom, dense)                      # [B, D]
         if pooled.is_cuda:
             # fused CUDA interaction (no eager fallback on the GPU path)
-            return _run_mlp(self.top, _Interact.apply(x, pooled, self.pairs + self.dim + self.top_pad)).squeeze(1)
+            return _run_mlp(self.top, _Interact.apply(x, pooled, self.pairs + self.dim + self.top_pad,
+                                                      grad_rows)).squeeze(1)
         z = torch.cat([x.unsqueeze(1).to(pooled.dtype), pooled], dim=1)  # [B, T+1, D]
         zz = torch.bmm(z, z.transpose(1, 2))                  # [B, T+1, T+1]
         inter = zz.flatten(1).index_select(1, self.tril_flat)  # [B, pairs]
@@ -178,6 +186,7 @@ class DLRMConfig:
     mlp_dtype: str = "fp32"      # "fp32" | "bf16" (autocast for the dense MLPs only)
     seed: int = 0
     cuda_graph: bool = True      # replay the dense step (fwd + bwd + SGD) as one captured CUDA graph
+    sorted_grad: bool = True     # interaction backward stores pooled-row gradients in key-sorted order (1 GPU)
 
     def __post_init__(self):
         if self.emb_optimizer not in ("sgd", "adagrad"):
@@ -230,6 +239,8 @@ class DLRMTrainer:
             self.compute_model = self.model
             self.opt = torch.optim.SGD(self.model.parameters(), lr=dcfg.mlp_lr)
         self.losses: list = []
+        # single GPU, dims the sorted backward supports: gradients in key-sorted order
+        self._sorted = dcfg.sorted_grad and (exchange is None or exchange.world <= 1) and dim in (4, 8, 16, 32)
         self._dense_dev: dict = {}
         self._graphs: dict = {}
 
@@ -259,6 +270,10 @@ class DLRMTrainer:
             pooled = g["emb"] if g is not None else torch.empty((b, t, self.dim), dtype=torch.float32, device="cuda")
             L.check(lib.bp_engine_dlrm_forward(pipe.eng, pos, plan.slot, nxt, skip_key, has_skip, self.dim,
                                                L.ptr(pooled)), "bp_engine_dlrm_forward")
+            rows = None
+            if self._sorted:
+                rows = g["rows"] if g is not None else torch.empty(b * t, dtype=torch.int32, device="cuda")
+                L.check(lib.bp_engine_dlrm_grad_rows(pipe.eng, pos, L.ptr(rows)), "bp_engine_dlrm_grad_rows")
             if g is not None:
                 g["dense"][:, :dense.shape[1]].copy_(dense)
                 g["labels"].copy_(labels)
@@ -269,7 +284,7 @@ class DLRMTrainer:
                 self.losses.append(g["loss"].detach().clone())
             else:
                 emb = pooled.requires_grad_(True)
-                loss = self._loss(dense, emb, labels)
+                loss = self._loss(dense, emb, labels, rows)
                 self.opt.zero_grad(set_to_none=True)
                 loss.backward()
                 self.opt.step()
@@ -287,7 +302,8 @@ class DLRMTrainer:
         return dense[sl], labels[sl]
 
     def _backward(self, pipe, pos, plan, grad, chunk, drain, res) -> None:
-        L.check(pipe.lib.bp_engine_dlrm_backward(pipe.eng, pos, plan.slot, L.ptr(grad), self.dim, self.dcfg.opt_code,
+        fn = pipe.lib.bp_engine_dlrm_backward_sorted if self._sorted else pipe.lib.bp_engine_dlrm_backward
+        L.check(fn(pipe.eng, pos, plan.slot, L.ptr(grad), self.dim, self.dcfg.opt_code,
                                                  float(np.float32(self.dcfg.emb_lr)),
                                                  float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
                                                  C.byref(res)), "bp_engine_dlrm_backward")
@@ -382,8 +398,8 @@ class DLRMTrainer:
                                                      float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
                                                      C.byref(res)), "bp_engine_dlrm_backward_peer")
 
-    def _loss(self, dense, emb, labels):
-        logits = self.compute_model(dense, emb).float()
+    def _loss(self, dense, emb, labels, grad_rows=None):
+        logits = self.compute_model(dense, emb, grad_rows).float()
         return nn.functional.binary_cross_entropy_with_logits(logits, labels)
 
     def _graph(self, b: int, t: int, n_dense: int, with_step: bool = True, emb=None) -> dict:
@@ -397,25 +413,30 @@ class DLRMTrainer:
         if g is not None:
             return g
         dev = "cuda"
+        own_emb = emb is None
         # static input: a fresh buffer, or caller memory read in place (the
         # peer exchange's row buffer)
         emb = torch.zeros((b, t, self.dim), dtype=torch.float32, device=dev, requires_grad=True) if emb is None \
             else emb.detach().requires_grad_(True)
         dense = torch.zeros((b, n_dense + self.model.dense_pad), dtype=torch.float32, device=dev)
         labels = torch.zeros((b,), dtype=torch.float32, device=dev)
+        # sorted-gradient row map (filled per batch by bp_engine_dlrm_grad_rows
+        # before each replay; identity for the warm-up passes)
+        rows = torch.arange(b * t, dtype=torch.int32, device=dev) if (self._sorted and with_step and own_emb) \
+            else None
         torch.cuda.synchronize()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             for _ in range(2):
-                self._loss(dense, emb, labels).backward()
+                self._loss(dense, emb, labels, rows).backward()
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.opt.zero_grad(set_to_none=True)
         emb.grad = None
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, capture_error_mode="thread_local"):
-            loss = self._loss(dense, emb, labels)
+            loss = self._loss(dense, emb, labels, rows)
             loss.backward()
             if with_step:
                 self.opt.step()
@@ -427,7 +448,7 @@ class DLRMTrainer:
             with torch.cuda.graph(step, pool=graph.pool(), capture_error_mode="thread_local"):
                 self.opt.step()
         g = {"graph": graph, "step": step if not with_step else None, "emb": emb, "dense": dense, "labels": labels,
-             "loss": loss, "grad": grad}
+             "loss": loss, "grad": grad, "rows": rows}
         self._graphs[key] = g
         return g
 

@@ -47,9 +47,10 @@ def cpu_reference(batches, model, opt_name, lr, eps, seed):
     return losses, [t.detach().numpy() for t in tables], model
 
 
-@pytest.mark.parametrize("opt_name,cuda_graph", [("sgd", False), ("adagrad", False), ("sgd", True),
-                                                 ("adagrad", True)])
-def test_dlrm_pipeline_matches_dense_cpu_training(opt_name, cuda_graph):
+@pytest.mark.parametrize("opt_name,cuda_graph,sorted_grad", [("sgd", False, True), ("adagrad", False, True),
+                                                             ("sgd", True, True), ("adagrad", True, True),
+                                                             ("sgd", True, False), ("adagrad", False, False)])
+def test_dlrm_pipeline_matches_dense_cpu_training(opt_name, cuda_graph, sorted_grad):
     from paper_2202_12429_b200.dlrm import DLRMConfig, DLRMDense
     from paper_2202_12429_b200.engine import EngineConfig, run_dlrm
 
@@ -62,7 +63,7 @@ def test_dlrm_pipeline_matches_dense_cpu_training(opt_name, cuda_graph):
     want_losses, want_tables, want_model = cpu_reference(batches, model, opt_name, lr, eps, seed)
     cfg = EngineConfig(cache_capacity=1200, batch_size=256, lookahead=3, num_shards=1, seed=seed, lr=lr)
     dcfg = DLRMConfig(emb_optimizer=opt_name, emb_lr=lr, mlp_lr=lr, adagrad_eps=eps, bottom=(64, 32), top=(64, 32),
-                      cuda_graph=cuda_graph)
+                      cuda_graph=cuda_graph, sorted_grad=sorted_grad)
     report, trainer = run_dlrm(cfg, SCHEMA, batches, dcfg, model=copy.deepcopy(model))
     np.testing.assert_allclose(trainer.loss_history(), want_losses, rtol=1e-4)
     table = report.final_store.table_view()
@@ -249,3 +250,93 @@ def test_bf16_mixed_precision_tracks_fp32():
         out[dt] = (np.asarray(trainer.loss_history()), report.final_store.table_view().copy())
     np.testing.assert_allclose(out["bf16"][0], out["fp32"][0], rtol=2e-2)
     np.testing.assert_allclose(out["bf16"][1], out["fp32"][1], rtol=0, atol=2e-3)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("dim", [4, 8, 16, 32])
+@pytest.mark.parametrize("opt_name", ["sgd", "adagrad"])
+def test_sorted_gradient_backward(dim, opt_name, variant):
+    """bp_prep_occ_rank is the stable key-sorted position of every occurrence;
+    bp_embbag_backward_sorted over gradients stored in that order (as the
+    interaction backward stores them) equals torch's embedding backward +
+    SGD/Adagrad within fp32 tolerance, incl. Zipf-hot keys spanning many
+    tiles, ragged last tile and keys crossing tile boundaries."""
+    from paper_2202_12429_b200 import _lib as L
+    from paper_2202_12429_b200.device import DevicePrep
+    from paper_2202_12429_b200.traces import pack_keys
+
+    rng = np.random.default_rng(dim + (100 if opt_name == "adagrad" else 0))
+    n_rows, n = 400, 20011
+    L.check(L.lib().bp_debug_bwd_variant(variant), "variant")
+    idx = np.minimum(rng.zipf(1.2, n) - 1, n_rows - 1).astype(np.int64)
+    w = rng.standard_normal((n_rows, dim)).astype(np.float32)
+    g = rng.standard_normal((n, dim)).astype(np.float32)
+    lr, eps = 0.05, 1e-10
+    lib = L.lib()
+    prep = DevicePrep(pack_keys(np.zeros_like(idx), idx), np.zeros(n, np.uint8), np.asarray([0, n]), 0, occ_index=2)
+    rank = torch.empty(n, dtype=torch.int32, device="cuda")
+    L.check(lib.bp_prep_occ_rank(prep.handle, L.ptr(rank), L.stream_ptr()), "occ rank")
+    want_rank = np.empty(n, np.int64)
+    want_rank[np.argsort(idx, kind="stable")] = np.arange(n)
+    assert np.array_equal(rank.cpu().numpy(), want_rank)
+    slots = torch.empty(prep.num_unique, dtype=torch.int32, device="cuda")
+    L.check(lib.bp_prep_key_rows(prep.handle, L.ptr(slots), L.stream_ptr()), "key rows")
+    arena = np.zeros((n_rows, 2 * dim), np.float32)
+    arena[:, :dim] = w
+    d_arena = torch.from_numpy(arena).cuda()
+    g_sorted = np.empty_like(g)
+    g_sorted[want_rank] = g
+    d_g = torch.from_numpy(g_sorted).cuda()
+    dirty = torch.zeros(n_rows, dtype=torch.uint8, device="cuda")
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    opt = 1 if opt_name == "adagrad" else 0
+    L.check(lib.bp_embbag_backward_sorted(prep.handle, L.ptr(d_g), L.ptr(d_arena), 2 * dim, L.ptr(slots),
+                                          L.ptr(dirty), dim, opt, float(np.float32(lr)), float(np.float32(eps)),
+                                          L.ptr(stats), L.stream_ptr()), "bwd sorted")
+    gs = np.zeros((n_rows, dim), np.float64)
+    np.add.at(gs, idx, g.astype(np.float64))
+    got = d_arena.cpu().numpy()
+    if opt_name == "adagrad":
+        want = w - lr * gs / (np.sqrt(gs * gs) + eps)
+        np.testing.assert_allclose(got[:, dim:], gs * gs, rtol=1e-3, atol=1e-4)
+        # lr*g/|g| ~ lr*sign(g): components whose sum is ~0 depend on fp32 order
+        ok = np.abs(gs) > 1e-3
+        np.testing.assert_allclose(got[:, :dim][ok], want[ok], rtol=1e-5, atol=1e-4)
+    else:
+        np.testing.assert_allclose(got[:, :dim], w - lr * gs, rtol=1e-5, atol=2e-5)
+    touched = np.zeros(n_rows, bool)
+    touched[idx] = True
+    assert np.array_equal(dirty.cpu().numpy().astype(bool), touched)
+    assert int(stats[1]) == int(touched.sum())
+    # deterministic: a second run from the same state gives identical bits
+    d_arena2 = torch.from_numpy(arena).cuda()
+    L.check(lib.bp_embbag_backward_sorted(prep.handle, L.ptr(d_g), L.ptr(d_arena2), 2 * dim, L.ptr(slots), None,
+                                          dim, opt, float(np.float32(lr)), float(np.float32(eps)), None,
+                                          L.stream_ptr()), "bwd sorted 2")
+    L.check(lib.bp_debug_bwd_variant(0), "variant")
+    assert torch.equal(d_arena, d_arena2)
+
+
+def test_interaction_backward_rows_is_a_permuted_store():
+    """bp_dlrm_interact_backward_rows writes row (b, t) of the embedding
+    gradient at d_gemb_rows[b*T + t]: equal to the plain backward permuted."""
+    from paper_2202_12429_b200 import _lib as L
+
+    b, t, d = 300, 26, 16
+    n = t + 1
+    stride = d + n * (n - 1) // 2 + 1
+    torch.manual_seed(0)
+    x = torch.randn(b, d, device="cuda")
+    emb = torch.randn(b, t, d, device="cuda")
+    gout = torch.randn(b, stride, device="cuda")
+    rows = torch.randperm(b * t, device="cuda").to(torch.int32)
+    outs = []
+    for r in (None, rows):
+        gx = torch.empty_like(x)
+        gemb = torch.empty_like(emb)
+        L.check(L.lib().bp_dlrm_interact_backward_rows(L.ptr(x), 0, L.ptr(emb), L.ptr(gout), 0, b, t, d, stride,
+                                                       L.ptr(gx), L.ptr(gemb), L.ptr(r) if r is not None else None,
+                                                       L.stream_ptr()), "ix bwd")
+        outs.append((gx, gemb.reshape(b * t, d)))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[1][1][rows.long()], outs[0][1])

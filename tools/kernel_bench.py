@@ -108,19 +108,61 @@ def main():
         L.check(lib.bp_embbag_backward(prep2.handle, L.ptr(grad), None, None, L.ptr(values), dim, L.ptr(slots), None,
                                        dim, 0, float(np.float32(0.01)), 0.0, None, L.stream_ptr()), "bwd")
 
+    def bwd_sorted():  # gradients in key-sorted order (as the interaction backward stores them)
+        L.check(lib.bp_embbag_backward_sorted(prep2.handle, L.ptr(grad), L.ptr(values), dim, L.ptr(slots), None,
+                                              dim, 0, float(np.float32(0.01)), 0.0, None, L.stream_ptr()),
+                "bwd sorted")
+
+    # warm: the gradient rows just written (L2-resident, as after the
+    # interaction backward in a DLRM step), no flush
+    grad_src = grad.clone()
+
+    def timed_warm(fn, reps):
+        times = []
+        for _ in range(reps):
+            grad.copy_(grad_src)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            times.append(a.elapsed_time(b) * 1e3)
+        return float(np.median(times))
+
+    out["embbag_bwd_warm_us"] = timed_warm(bwd, args.reps)
+    for var in (0, 1, 2, 3):
+        lib.bp_debug_bwd_variant(var)
+        out[f"embbag_bwd_sorted_v{var}_warm_us"] = timed_warm(bwd_sorted, args.reps)
+    lib.bp_debug_bwd_variant(0)
     out["embbag_fwd_us"] = timed(fwd, args.reps, flush)
     out["embbag_bwd_us"] = timed(bwd, args.reps, flush)
+    out["embbag_bwd_sorted_us"] = timed(bwd_sorted, args.reps, flush)
+    for var in (1, 2, 3):  # other launch shapes of the sorted kernel
+        lib.bp_debug_bwd_variant(var)
+        out[f"embbag_bwd_sorted_v{var}_us"] = timed(bwd_sorted, args.reps, flush)
+    lib.bp_debug_bwd_variant(0)
     fwd_bytes = n * (8 * dim + 4)
     bwd_bytes = n * (4 * dim + 4) + u2 * (8 * dim)
     out["embbag_fwd_gbs"] = fwd_bytes / (out["embbag_fwd_us"] * 1e-6) / 1e9
     out["embbag_bwd_gbs"] = bwd_bytes / (out["embbag_bwd_us"] * 1e-6) / 1e9
     out["embbag_fwd_bwd_gbs"] = (fwd_bytes + bwd_bytes) / ((out["embbag_fwd_us"] + out["embbag_bwd_us"]) * 1e-6) / 1e9
+    out["embbag_bwd_sorted_gbs"] = bwd_bytes / (out["embbag_bwd_sorted_us"] * 1e-6) / 1e9
+    out["embbag_fwd_bwd_sorted_gbs"] = (fwd_bytes + bwd_bytes) / (
+        (out["embbag_fwd_us"] + out["embbag_bwd_sorted_us"]) * 1e-6) / 1e9
     out["n_occ"], out["unique"] = n, u
     # per-kernel device times (CUPTI) of one call each, L2 flushed first
     from torch.profiler import ProfilerActivity, profile
 
     kernels = {}
-    for fn in (stub, fwd, bwd):
+
+    def variant(v):
+        def run():
+            lib.bp_debug_bwd_variant(v)
+            bwd_sorted()
+            lib.bp_debug_bwd_variant(0)
+        return run
+
+    for fn in (stub, fwd, bwd, bwd_sorted, variant(1), variant(2), variant(3)):
         flush.zero_()
         torch.cuda.synchronize()
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
