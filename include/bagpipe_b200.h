@@ -376,7 +376,8 @@ int bp_engine_plan_ready(bp_engine* engine, int32_t slot, int32_t* out);      /*
 int bp_engine_plan_view(bp_engine* engine, int32_t slot, bp_plan_buffers* out, float** d_staging);
 int bp_engine_fetch(bp_engine* engine, int32_t slot);
 /* Host-link mode: 0 = zero-copy row kernels, 1 = copy engines + `threads`
- * host threads gathering/scattering rows in pinned staging (0: auto). */
+ * host threads gathering/scattering rows in pinned staging (0: auto),
+ * 2 = zero-copy prefetch, copy-engine write-back + host scatter. */
 int bp_engine_set_link_mode(bp_engine* engine, int32_t mode, int32_t threads);
 /* Host worker-pool row gather (op 0) / scatter (op 1) rate probe (tools). */
 int bp_host_rows_bench(float* table, int32_t dim, const uint32_t* ids, int64_t n, int32_t threads, int32_t op,

@@ -749,9 +749,11 @@ extern "C" int bp_engine_plan_view(bp_engine* e, int32_t slot, bp_plan_buffers* 
 // issued on the same stream (the gate).
 // Host-link mode of the engine: 0 = zero-copy row kernels (SM-driven PCIe
 // gathers/scatters), 1 = copy engines + a pool of `threads` host threads
-// gathering/scattering rows in pinned staging (no SM time on the link).
+// gathering/scattering rows in pinned staging (no SM time on the link),
+// 2 = zero-copy prefetch gathers, write-back by copy engine + host scatter
+// (zero-copy scatters are the worst interferers: tools/mb/interfere.cu).
 extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threads) {
-  if (mode != 0 && mode != 1) return BP_ERR_INVALID;
+  if (mode < 0 || mode > 2) return BP_ERR_INVALID;
   BP_CUDA_TRY(cudaStreamSynchronize(e->link));
   e->link_mode = mode;
   if (mode == 0) return BP_OK;
@@ -817,7 +819,7 @@ extern "C" int bp_engine_flush(bp_engine* e, const int32_t* chunk_slots, int32_t
   bp::stage_begin(e, bp::kStageFlush, e->link);
   for (int i = 0; i < n; ++i) {
     bp::ChunkSlot& c = e->chunks[chunk_slots[i]];
-    if (e->link_mode == 1 && c.h_count >= 0) {
+    if (e->link_mode >= 1 && c.h_count >= 0) {
       const long long m = c.h_count;
       if (m > 0) {
         const size_t rb = (size_t)e->cfg.dim * sizeof(float);

@@ -217,7 +217,8 @@ class _Pipeline:
         parts = L.EngineParts()
         self.lib.bp_engine_parts(h, C.byref(parts))
         self.parts = parts
-        # host link: 0 = zero-copy kernels (default), 1 = copy engines + host worker pool
+        # host link: 0 = zero-copy kernels (default), 1 = copy engines + host worker pool,
+        # 2 = zero-copy prefetch + copy-engine write-back with host scatter
         if link_mode is None:
             link_mode = int(os.environ.get("BAGPIPE_B200_LINK_MODE", "0"))
         L.check(self.lib.bp_engine_set_link_mode(h, link_mode, int(os.environ.get("BAGPIPE_B200_LINK_THREADS", "0"))),

@@ -33,7 +33,7 @@ def _assert_report(report, blob):
     assert report.to_csv_bytes().decode() == blob["csv"]
 
 
-@pytest.mark.parametrize("link_mode", [1, 0])
+@pytest.mark.parametrize("link_mode", [1, 2, 0])
 @pytest.mark.parametrize("case", SMALL_CASES)
 def test_pipeline_report_byte_identical(small_schema, small_batches, case, link_mode, monkeypatch):
     """Both host-link modes: copy engines + host pool (1), zero-copy kernels (0)."""
@@ -80,7 +80,7 @@ def test_dropped_prefetch_is_a_miss_at_the_reference_key(small_schema, small_bat
     assert err.value.key == unpack(want["key"])
 
 
-@pytest.mark.parametrize("link_mode", [1, 0])
+@pytest.mark.parametrize("link_mode", [1, 2, 0])
 def test_ungated_run_reproduces_reference_staleness(small_schema, small_batches, link_mode, monkeypatch):
     """fault=no_gate: the stale digest equals the reference's stale digest bit
     for bit, and differs from the baseline with a non-empty diff."""
