@@ -277,6 +277,25 @@ uint8_t* bp_store_written_bitmap(bp_store* store); /* device, 1 bit per row */
  * pinned table over the host link into d_out[n, dim]. */
 int bp_store_fetch(bp_store* store, const uint32_t* d_ids, int64_t n, const int64_t* d_n, float* d_out,
                    bp_stream_t stream);
+/* fetch as store.py:106-129 states it: written rows (device bitmap) gathered
+ * over the host link, never-written rows computed on the GPU from their
+ * packed keys d_keys[i] (functional init, store.py:29-42) -- no PCIe read. */
+int bp_store_fetch_lazy(bp_store* store, const uint32_t* d_ids, const uint64_t* d_keys, int64_t n,
+                        const int64_t* d_n, float* d_out, bp_stream_t stream);
+/* Write-back log (log-structured host store): bp_store_log_append copies a
+ * chunk of rows into a pinned log by one copy-engine DMA and commits its
+ * dirty rows (d_dirty NULL: all) as the newest copies of their ids; fetches
+ * read a row from the log or the table, whichever is newest.  Compaction
+ * (when the log is full, or explicitly before host-side reads of the table)
+ * folds the newest log entries into the table.  Stream-ordered. */
+int bp_store_enable_log(bp_store* store, int64_t log_rows, bp_stream_t stream);
+int bp_store_log_append(bp_store* store, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_dirty,
+                        int64_t m, bp_stream_t stream);
+int bp_store_compact(bp_store* store, bp_stream_t stream);
+int64_t bp_store_log_rows(bp_store* store); /* capacity, 0 = no log */
+/* lazy-fetch counters since creation: [0] rows read over the host link,
+ * [1] rows computed on the GPU.  Synchronises the device. */
+int bp_store_link_counters(bp_store* store, int64_t* h_out2);
 /* write_back (reference store.py:131-155): zero-copy scatter into the
  * pinned table; ids must be unique within one call. */
 int bp_store_write(bp_store* store, const uint32_t* d_ids, const float* d_rows, int64_t n,
@@ -379,6 +398,8 @@ int bp_engine_fetch(bp_engine* engine, int32_t slot);
  * host threads gathering/scattering rows in pinned staging (0: auto),
  * 2 = zero-copy prefetch, copy-engine write-back + host scatter. */
 int bp_engine_set_link_mode(bp_engine* engine, int32_t mode, int32_t threads);
+/* Enable the store's write-back log (mode 0 flushes append to it by DMA). */
+int bp_engine_set_write_log(bp_engine* engine, int64_t log_rows);
 /* Host worker-pool row gather (op 0) / scatter (op 1) rate probe (tools). */
 int bp_host_rows_bench(float* table, int32_t dim, const uint32_t* ids, int64_t n, int32_t threads, int32_t op,
                        double* seconds);
@@ -538,6 +559,8 @@ int bp_debug_link_cb_stats(int64_t* out9);
  * memory per block (default 0; ~200 KB makes a link block own its SM). */
 int bp_set_link_blocks(int32_t blocks);
 int bp_set_link_config(int32_t blocks, int32_t threads, int32_t smem_bytes);
+/* Blocks of the write-back scatter kernel (0: the link kernels' block count). */
+int bp_set_write_blocks(int32_t blocks);
 /* Sort packed keys ascending with a u32 payload (stable); n host-known. */
 int bp_sort_keys_u64(uint64_t* d_keys, uint32_t* d_vals, int64_t n, int32_t key_bits, bp_stream_t stream);
 /* Order-independent digest helpers for parity tests. */

@@ -138,6 +138,13 @@ _SIGS = {
     "bp_store_host_table": (c_vp, [c_vp]),
     "bp_store_written_bitmap": (c_vp, [c_vp]),
     "bp_store_fetch": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "bp_store_fetch_lazy": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "bp_store_link_counters": (c_i32, [c_vp, c_vp]),
+    "bp_store_enable_log": (c_i32, [c_vp, c_i64, c_vp]),
+    "bp_store_log_append": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "bp_store_compact": (c_i32, [c_vp, c_vp]),
+    "bp_store_log_rows": (c_i64, [c_vp]),
+    "bp_engine_set_write_log": (c_i32, [c_vp, c_i64]),
     "bp_store_write": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bp_store_write_masked": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bp_init_values": (c_i32, [c_u64, c_i32, c_vp, c_i64, c_vp, c_vp]),
@@ -188,6 +195,7 @@ _SIGS = {
     "bp_engine_train_end": (c_i32, [c_vp, P(StepResult)]),
     "bp_set_link_blocks": (c_i32, [c_i32]),
     "bp_set_link_config": (c_i32, [c_i32, c_i32, c_i32]),
+    "bp_set_write_blocks": (c_i32, [c_i32]),
     "bp_engine_plan_ready": (c_i32, [c_vp, c_i32, c_vp]),
     "bp_engine_join": (c_i32, [c_vp, c_vp]),
     "bp_engine_set_timing": (c_i32, [c_vp, c_i32]),
@@ -258,6 +266,12 @@ def lib() -> C.CDLL:
                 lc = os.environ.get("BAGPIPE_B200_LINK_CONFIG")
                 if lc:
                     check(lb.bp_set_link_config(*[int(x) for x in lc.split(",")]), "bp_set_link_config")
+                wb = os.environ.get("BAGPIPE_B200_WRITE_BLOCKS")  # tuning knob: write-back scatter grid
+                if wb:
+                    check(lb.bp_set_write_blocks(int(wb)), "bp_set_write_blocks")
+                sk = os.environ.get("BAGPIPE_B200_DEBUG_SKIP_LINK")  # debug only: results become wrong
+                if sk:
+                    check(lb.bp_debug_skip_link(int(sk)), "bp_debug_skip_link")
                 bv = os.environ.get("BAGPIPE_B200_BWD_VARIANT")  # tuning knob: sorted backward launch shape
                 if bv:
                     check(lb.bp_debug_bwd_variant(int(bv)), "bp_debug_bwd_variant")

@@ -755,6 +755,11 @@ extern "C" int bp_engine_plan_view(bp_engine* e, int32_t slot, bp_plan_buffers* 
 extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threads) {
   if (mode < 0 || mode > 2) return BP_ERR_INVALID;
   BP_CUDA_TRY(cudaStreamSynchronize(e->link));
+  if (mode != 0) {  // the host worker paths read / write the table itself
+    const int rc = bp_store_compact(e->store, e->link);
+    if (rc) return rc;
+    BP_CUDA_TRY(cudaStreamSynchronize(e->link));
+  }
   e->link_mode = mode;
   if (mode == 0) return BP_OK;
   if (threads < 1) {
@@ -787,6 +792,13 @@ extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threa
   return BP_OK;
 }
 
+// Write-back log of the engine's store (mode 0): log_rows pinned rows that
+// flushes append to by DMA (0: zero-copy scatter into the table).
+extern "C" int bp_engine_set_write_log(bp_engine* e, int64_t log_rows) {
+  if (log_rows <= 0) return BP_OK;
+  return bp_store_enable_log(e->store, log_rows, e->link);
+}
+
 extern "C" int bp_engine_fetch(bp_engine* e, int32_t slot) {
   bp::PlanSlot& ps = e->plans[slot];
   BP_CUDA_TRY(cudaStreamWaitEvent(e->link, ps.popped, 0));
@@ -806,7 +818,7 @@ extern "C" int bp_engine_fetch(bp_engine* e, int32_t slot) {
       BP_CUDA_TRY(cudaMemcpyAsync(ps.staging, e->h_fetch_rows, n * rb, cudaMemcpyHostToDevice, e->link));
     }
   } else {
-    int rc = bp_store_fetch(e->store, ps.ids, e->cfg.max_occ, ps.counts, ps.staging, e->link);
+    int rc = bp_store_fetch_lazy(e->store, ps.ids, ps.keys, e->cfg.max_occ, ps.counts, ps.staging, e->link);
     if (rc) return rc;
   }
   bp::stage_end(e, bp::kStageFetch, e->link);
@@ -835,6 +847,11 @@ extern "C" int bp_engine_flush(bp_engine* e, const int32_t* chunk_slots, int32_t
         const int wrc = e->worker->enqueue(e->link);
         if (wrc) return wrc;
       }
+    } else if (e->link_mode == 0 && c.h_count >= 0 && c.h_count <= bp_store_log_rows(e->store)) {
+      // write-back log: one copy-engine append of the chunk + a commit kernel
+      // (no zero-copy scatter stalling the compute stream)
+      int rc = bp_store_log_append(e->store, c.ids, c.rows, c.dirty, c.h_count, e->link);
+      if (rc) return rc;
     } else {
       int rc = bp_store_write_masked(e->store, c.ids, c.rows, c.dirty, e->cfg.capacity, c.count, e->link);
       if (rc) return rc;

@@ -8,7 +8,8 @@ step for step, so reports are byte-identical.  Every per-key operation runs
 on the device:
 
   plan emission   bp_planner_refill / bp_planner_pop        (csrc/planner.cu)
-  prefetch        bp_store_fetch: zero-copy gather from the pinned table
+  prefetch        bp_store_fetch_lazy: zero-copy gather of written rows from
+                  the pinned table, functional init of the others on the GPU
   apply + lookup  bp_cache_insert + bp_cache_apply_resolve  (csrc/cache.cu)
   train           bp_stub_step: gradient, rank-ordered combine, SGD, dirty,
                   critical-set count, fused                 (csrc/trainer.cu)
@@ -224,6 +225,9 @@ class _Pipeline:
         L.check(self.lib.bp_engine_set_link_mode(h, link_mode, int(os.environ.get("BAGPIPE_B200_LINK_THREADS", "0"))),
                 "bp_engine_set_link_mode")
         self.link_mode = link_mode
+        # write-back log rows (log-structured host store; 0 = zero-copy scatter into the table)
+        log_rows = int(os.environ.get("BAGPIPE_B200_LOG_ROWS", str(min(self.row_schema.total_rows, 1 << 24))))
+        L.check(self.lib.bp_engine_set_write_log(h, log_rows), "bp_engine_set_write_log")
         self.stream = torch.cuda.ExternalStream(parts.compute_stream)
         self.link = torch.cuda.ExternalStream(parts.link_stream)
         self.store = ShardedStore(self.row_schema, cfg.num_shards, cfg.seed, _handle=parts.store, _owner=self)
@@ -812,7 +816,7 @@ def run_synchronous_baseline(cfg: EngineConfig, schema: Schema, trace: Iterable[
         u = prep.num_unique
         if u:
             ids = prep.tensor("d_uniq_id_s", torch.uint32, u)
-            rows = store.fetch_ids_async(ids, u, stream=stream)
+            rows = store.fetch_ids_async(ids, u, stream=stream, d_keys=prep.tensor("d_uniq_key_s", torch.uint64, u))
             store.fetch_calls += 1
             L.check(lib.bp_stub_step(ctx.handle, prep.handle, L.ptr(rows), None, None, schema.emb_dim, c_value,
                                      c_label, lr, BP_STUB_SGD, None, None, 0, None, sp), "bp_stub_step")

@@ -26,7 +26,7 @@ from . import _lib as L
 from .device import DeviceSchema
 from .errors import ConfigurationError, StoreError, StoreKeyError, TraceFormatError
 from .hashing import fnv1a64_u64_arrays
-from .traces import EmbeddingKey, Schema
+from .traces import EmbeddingKey, Schema, pack_keys
 
 DUMP_MAGIC = b"EMSTD1"
 
@@ -100,12 +100,18 @@ class ShardedStore:
         return (self._base[tables] + rows).astype(np.uint32)
 
     # -- device-path entry points used by the engine -------------------------
-    def fetch_ids_async(self, d_ids: torch.Tensor, n: int, d_n=None, stream=None) -> torch.Tensor:
-        """Gather rows for dense ids already on the device (no host round trip)."""
+    def fetch_ids_async(self, d_ids: torch.Tensor, n: int, d_n=None, stream=None, d_keys=None) -> torch.Tensor:
+        """Gather rows for dense ids already on the device (no host round trip).
+        With the packed keys (d_keys), never-written rows are computed on the
+        GPU (functional init) instead of read over the host link."""
         out = torch.empty((max(n, 0), self.schema.emb_dim), dtype=torch.float32, device="cuda")
         if n > 0:
-            L.check(L.lib().bp_store_fetch(self.handle, L.ptr(d_ids), n, L.ptr(d_n), L.ptr(out),
-                                           L.stream_ptr(stream)), "bp_store_fetch")
+            if d_keys is not None:
+                L.check(L.lib().bp_store_fetch_lazy(self.handle, L.ptr(d_ids), L.ptr(d_keys), n, L.ptr(d_n),
+                                                    L.ptr(out), L.stream_ptr(stream)), "bp_store_fetch_lazy")
+            else:
+                L.check(L.lib().bp_store_fetch(self.handle, L.ptr(d_ids), n, L.ptr(d_n), L.ptr(out),
+                                               L.stream_ptr(stream)), "bp_store_fetch")
         return out
 
     def write_ids_async(self, d_ids, d_rows, n: int, d_n=None, d_mask=None, stream=None) -> None:
@@ -127,8 +133,10 @@ class ShardedStore:
         with self._lock:
             self.fetch_calls += 1
             ids = self._ids(keys)
+            arr = np.asarray(keys, dtype=np.int64).reshape(len(keys), 2)
             d_ids = L.to_device(ids)
-            out = self.fetch_ids_async(d_ids, len(ids))
+            d_keys = L.to_device(pack_keys(arr[:, 0], arr[:, 1]))
+            out = self.fetch_ids_async(d_ids, len(ids), d_keys=d_keys)
             return out.cpu().numpy()
 
     def write_back(self, keys, values) -> None:
@@ -146,7 +154,10 @@ class ShardedStore:
             self.entries_written += len(keys)
 
     def table_view(self) -> np.ndarray:
-        """The whole store as a (total_rows, emb_dim) view of pinned memory."""
+        """The whole store as a (total_rows, emb_dim) view of pinned memory
+        (write-back log folded in first)."""
+        torch.cuda.synchronize()
+        L.check(L.lib().bp_store_compact(self.handle, L.stream_ptr()), "bp_store_compact")
         torch.cuda.synchronize()
         return self._table
 

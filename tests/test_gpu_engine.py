@@ -48,6 +48,19 @@ def test_pipeline_report_byte_identical(small_schema, small_batches, case, link_
         assert got == blob["events"]
 
 
+@pytest.mark.parametrize("log_rows", ["0", "40", "700"])
+@pytest.mark.parametrize("case", ["L8_T1", "L4_T3_rpc1", "L32_cap550_halving"])
+def test_write_back_log_sizes(small_schema, small_batches, case, log_rows, monkeypatch):
+    """Write-back log (DMA appends + commit, compaction when full): disabled
+    (0: zero-copy scatter), smaller than most flush chunks (those fall back to
+    the scatter, mixing both paths), and compacting every few flushes -- the
+    report and digest stay byte-identical to the reference."""
+    monkeypatch.setenv("BAGPIPE_B200_LOG_ROWS", log_rows)
+    blob = golden("reports_small.json")[case]
+    report = _engine().run_pipeline(_cfg(blob["config"]), small_schema, small_batches)
+    _assert_report(report, blob)
+
+
 @pytest.mark.parametrize("trainers", [1, 2, 3])
 def test_baseline_report_byte_identical(small_schema, small_batches, trainers):
     blob = golden("reports_small.json")[f"baseline_T{trainers}"]

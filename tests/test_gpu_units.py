@@ -159,6 +159,27 @@ def test_store_fetch_write_digest():
     assert s.snapshot_digest() != before
 
 
+def test_store_lazy_fetch_equals_host_gather():
+    """bp_store_fetch_lazy (init computed on the GPU for never-written rows)
+    returns exactly what the full host-table gather returns."""
+    import torch
+
+    from paper_2202_12429_b200 import _lib as L
+    from paper_2202_12429_b200.traces import pack_keys
+
+    s = store(seed=5)
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(100, 60, replace=False))
+    s.write_back([k(int(r)) for r in rows[::3]], rng.standard_normal((len(rows[::3]), 4)).astype(np.float32))
+    ids = torch.from_numpy(rows.astype(np.uint32)).cuda()
+    keys = torch.from_numpy(pack_keys(np.zeros_like(rows), rows)).cuda()
+    lazy = s.fetch_ids_async(ids, len(rows), d_keys=keys)
+    full = s.fetch_ids_async(ids, len(rows))
+    torch.cuda.synchronize()
+    assert torch.equal(lazy, full)
+    assert L.lib() is not None
+
+
 def test_store_dump_round_trip(tmp_path):
     from paper_2202_12429_b200.store import read_store_dump, write_store_dump
 
