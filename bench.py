@@ -50,6 +50,12 @@ WORKLOAD = ("criteo-kaggle-shape 26 tables 33.76M rows D=16 fp32, batch 16384, z
             "lookahead auto(7), pinned-host table; stub-gradient engine iteration (reference run_pipeline)")
 
 
+# L2 flush at every iteration start: 0 = the memset runs on the compute
+# stream while the plan / host-link streams keep working (the pipeline stays
+# overlapped across iterations), 1 = every engine stream drained around it
+FLUSH_EXCLUSIVE = int(os.environ.get("BAGPIPE_B200_BENCH_FLUSH_EXCLUSIVE", "0"))
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -143,18 +149,20 @@ def count_launches(pipe, pos: int) -> int:
     return n
 
 
-def _timed_steps(pipe, first: int, steps: int, flush_buf, torch):
+def _timed_steps(pipe, first: int, steps: int, flush_buf, torch, exclusive: int | None = None):
     """K steps as ONE span on the engine's compute stream, bracketed by
     device syncs: CUDA events, the end event recorded after the compute
     stream joined the engine's plan and host-link streams, so every kernel
     and copy the K steps issued is inside.  L2 is flushed at the start of
     every iteration by the engine itself (bp_engine_set_l2_flush: a 256 MiB
-    memset on the compute stream, the plan and host-link streams fenced
-    around it), inside the span.  Returns (span ms, wall ms)."""
+    memset on the compute stream; exclusive=1 also fences the plan and
+    host-link streams around it), inside the span.  Returns (span ms, wall ms)."""
     from paper_2202_12429_b200 import _lib as L
 
     stream = pipe.stream
-    L.check(pipe.lib.bp_engine_set_l2_flush(pipe.eng, L.ptr(flush_buf), flush_buf.numel(), 1),
+    if exclusive is None:
+        exclusive = FLUSH_EXCLUSIVE
+    L.check(pipe.lib.bp_engine_set_l2_flush(pipe.eng, L.ptr(flush_buf), flush_buf.numel(), exclusive),
             "bp_engine_set_l2_flush")
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
@@ -213,7 +221,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     sc = schema()
     cap = sc.total_rows // 100
     steps, warm = args.steps, args.warmup
-    n_batches = warm + steps + 12
+    n_batches = warm + 2 * steps + 12
     # N>1 (weak scaling, the DLRM convention of a fixed per-GPU batch): the
     # global batch is N x 16,384 examples, its 26 tables dealt over the ranks;
     # every rank runs the whole pipeline for its tables of every example --
@@ -249,6 +257,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     records = pipe.records[warm:warm + steps]
     launches_per_step = count_launches(pipe, warm + steps)
     stages = _stage_breakdown(pipe, warm + steps + 1, 8)
+    # the same K steps with every engine stream drained around each flush
+    # (no overlap across iterations): reported beside the value
+    ms_excl, _ = _timed_steps(pipe, warm + steps + 9, steps, flush_buf, torch, exclusive=1)
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     pf_mean = statistics.mean(r.prefetch_count for r in records)
     n_occ = gbatch * len(tables)
@@ -314,7 +325,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                    "emb_dim": DIM, "cache_capacity_per_gpu": cap, "lookahead": lookahead0,
                    "parallelism": "single" if world == 1 else f"table-sharded x{world} (weak: {BATCH} examples/GPU)",
                    "l2": "flushed at the start of every timed iteration by the engine (256 MiB memset on the compute "
-                         "stream, plan and host-link streams fenced around it), inside the timed span",
+                         "stream, inside the timed span; " + ("plan and host-link streams fenced around it"
+                                                              if FLUSH_EXCLUSIVE else
+                                                              "plan and host-link streams keep running: the pipeline "
+                                                              "stays overlapped across iterations") + ")",
                    "timing": "one CUDA-event span over K steps, end event after joining the plan and host-link streams",
                    "mode": "stub-gradient (bit-exact)"},
         "e2e": None if args.no_e2e else {"value": samples / (e2e_max * 1e-3), "unit": "samples/s",
@@ -337,6 +351,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "clocks": clk,
         "wall_ms_timed_region": wall_ms,
         "l2_flush_ms_per_step": flush_ms / steps,
+        "ms_per_step_exclusive_flush": ms_excl / steps,
     }
     if dlrm is not None:
         out["dlrm"] = dlrm["summary"]

@@ -330,6 +330,10 @@ int bp_schema_ids(bp_ctx* ctx, const bp_schema* schema, const uint64_t* d_keys, 
 int bp_stub_step(bp_ctx* ctx, bp_prep* prep, float* d_rows, const int32_t* d_row_index, uint8_t* d_dirty,
                  int32_t dim, float c_value, float c_label, float lr, int32_t mode, float* d_grad_out,
                  const int64_t* d_next_mark, int64_t next_tag, int64_t* d_stats, bp_stream_t stream);
+/* bp_stub_step runs its long-segment kernel on a side stream of the calling
+ * thread, concurrently with the short-segment kernel (1, default) or both on
+ * `stream` in sequence (0). */
+int bp_set_stub_fork(int32_t on);
 /* mark[id] = tag for every unique key of a schema-mode prep. */
 int bp_mark_ids(bp_prep* prep, int64_t* d_mark, int64_t tag, bp_stream_t stream);
 /* np.add.at(out, idx, vals) row-wise in input order, over a registry-mode

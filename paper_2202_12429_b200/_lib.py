@@ -196,6 +196,7 @@ _SIGS = {
     "bp_set_link_blocks": (c_i32, [c_i32]),
     "bp_set_link_config": (c_i32, [c_i32, c_i32, c_i32]),
     "bp_set_write_blocks": (c_i32, [c_i32]),
+    "bp_set_stub_fork": (c_i32, [c_i32]),
     "bp_engine_plan_ready": (c_i32, [c_vp, c_i32, c_vp]),
     "bp_engine_join": (c_i32, [c_vp, c_vp]),
     "bp_engine_set_timing": (c_i32, [c_vp, c_i32]),
@@ -272,6 +273,9 @@ def lib() -> C.CDLL:
                 sk = os.environ.get("BAGPIPE_B200_DEBUG_SKIP_LINK")  # debug only: results become wrong
                 if sk:
                     check(lb.bp_debug_skip_link(int(sk)), "bp_debug_skip_link")
+                sf = os.environ.get("BAGPIPE_B200_STUB_FORK")  # tuning knob: long trainer kernel beside the short
+                if sf:
+                    check(lb.bp_set_stub_fork(int(sf)), "bp_set_stub_fork")
                 bv = os.environ.get("BAGPIPE_B200_BWD_VARIANT")  # tuning knob: sorted backward launch shape
                 if bv:
                     check(lb.bp_debug_bwd_variant(int(bv)), "bp_debug_bwd_variant")

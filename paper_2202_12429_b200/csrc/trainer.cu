@@ -398,6 +398,28 @@ extern "C" int bp_mark_ids(bp_prep* P, int64_t* d_mark, int64_t tag, bp_stream_t
   return BP_OK;
 }
 
+// Side stream of the calling thread for the long-segment kernel (created on
+// first use, high priority: its chains are the trainer's critical path).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  SideStream() {
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess)
+      s = nullptr;
+  }
+};
+
+static SideStream& side_stream() {
+  thread_local SideStream side;
+  return side;
+}
+
+static bool g_fork_long = true;
+
 template <int G, int DPL>
 static void long_attr() {
   static bool done = false;
@@ -420,8 +442,18 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   const long long groups = P->n_occ;  // upper bound on U
   const int threads = 256;
   const int blocks = grid_for(groups * G, threads, kNumSMs * 6);
+  // the long-segment kernel (a few sequential hot-key chains) runs on a side
+  // stream beside the short-segment kernel: the two touch disjoint keys
+  cudaStream_t ls = s;
+  if (g_fork_long) {
+    SideStream& side = side_stream();
+    if (!side.s) return BP_ERR_CUDA;
+    BP_CUDA_TRY(cudaEventRecord(side.fork, s));
+    BP_CUDA_TRY(cudaStreamWaitEvent(side.s, side.fork, 0));
+    ls = side.s;
+  }
   BP_DISPATCH_GD(G, dpl,
-                 (long_attr<g_, d_>(), k_stub_step_long<g_, d_><<<kLongBlocks, 128, kLongSmemPad, s>>>(
+                 (long_attr<g_, d_>(), k_stub_step_long<g_, d_><<<kLongBlocks, 128, kLongSmemPad, ls>>>(
                      P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,
                      d_row_index, d_dirty, dim, c_value, c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark,
                      next_tag, (unsigned long long*)d_stats)));
@@ -432,6 +464,16 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
                      c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark, next_tag,
                      (unsigned long long*)d_stats)));
   BP_LAUNCH_CHECK();
+  if (ls != s) {
+    SideStream& side = side_stream();
+    BP_CUDA_TRY(cudaEventRecord(side.join, ls));
+    BP_CUDA_TRY(cudaStreamWaitEvent(s, side.join, 0));
+  }
+  return BP_OK;
+}
+
+extern "C" int bp_set_stub_fork(int32_t on) {
+  g_fork_long = on != 0;
   return BP_OK;
 }
 
