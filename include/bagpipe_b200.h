@@ -433,6 +433,11 @@ int bp_engine_dlrm_grad_rows(bp_engine* engine, int64_t pos, uint32_t* d_rows);
 int bp_engine_dlrm_backward_sorted(bp_engine* engine, int64_t pos, int32_t plan_slot, const float* d_grad_sorted,
                                    int32_t model_dim, int32_t opt, float lr, float eps, int32_t chunk_slot,
                                    int32_t drain_slot, bp_step_result* out);
+/* Asynchronous form of the DLRM backward (either gradient order): enqueues
+ * only; bp_engine_train_end waits for the iteration and reads its counters. */
+int bp_engine_dlrm_backward_begin(bp_engine* engine, int64_t pos, int32_t plan_slot, const float* d_grad,
+                                  int32_t grad_sorted, int32_t model_dim, int32_t opt, float lr, float eps,
+                                  int32_t chunk_slot, int32_t drain_slot);
 int bp_engine_chunk_keys(bp_engine* engine, int32_t chunk_slot, uint64_t* h_out, int64_t n);
 int bp_engine_chunk_view(bp_engine* engine, int32_t chunk_slot, bp_evict_buffers* out);
 int bp_engine_sync(bp_engine* engine);
@@ -545,6 +550,19 @@ int bp_dlrm_interact_backward(const void* d_x, int32_t x_bf16, const float* d_em
 int bp_dlrm_interact_backward_rows(const void* d_x, int32_t x_bf16, const float* d_emb, const void* d_gout,
                                    int32_t g_bf16, int64_t B, int32_t T, int32_t D, int32_t out_stride, void* d_gx,
                                    float* d_gemb, const uint32_t* d_gemb_rows, bp_stream_t stream);
+/* Mixed-precision SGD of the dense model in one launch: for each tensor k,
+ * master[k] -= lr * grad[k] (bf16 gradient, fp32 master), then lowp[k] =
+ * bf16(master[k]).  The table is read at launch (CUDA-graph capturable). */
+#define BP_SGD_MAX_TENSORS 32
+typedef struct bp_sgd_tensors {
+  int32_t n;
+  int32_t pad;
+  float* master[BP_SGD_MAX_TENSORS];
+  void* lowp[BP_SGD_MAX_TENSORS];       /* bf16 */
+  const void* grad[BP_SGD_MAX_TENSORS]; /* bf16 */
+  int64_t numel[BP_SGD_MAX_TENSORS];
+} bp_sgd_tensors;
+int bp_dlrm_master_sgd(const bp_sgd_tensors* tensors, float lr, bp_stream_t stream);
 
 /* ------------------------------------------------------------ utilities */
 /* Debug: per-CTA phase clock64() stamps of the long-segment trainer kernel

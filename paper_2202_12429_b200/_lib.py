@@ -91,6 +91,14 @@ class PeerXchg(C.Structure):  # bp_peer_xchg
                 ("d_col_tables", c_vp), ("d_peer_rows", c_vp), ("d_peer_flags", c_vp), ("d_flags", c_vp)]
 
 
+SGD_MAX_TENSORS = 32
+
+
+class SgdTensors(C.Structure):  # bp_sgd_tensors
+    _fields_ = [("n", c_i32), ("pad", c_i32), ("master", c_vp * SGD_MAX_TENSORS), ("lowp", c_vp * SGD_MAX_TENSORS),
+                ("grad", c_vp * SGD_MAX_TENSORS), ("numel", c_i64 * SGD_MAX_TENSORS)]
+
+
 class EngineParts(C.Structure):
     _fields_ = [("store", c_vp), ("cache", c_vp), ("planner", c_vp), ("compute_stream", c_vp),
                 ("link_stream", c_vp)]
@@ -197,6 +205,9 @@ _SIGS = {
     "bp_set_link_config": (c_i32, [c_i32, c_i32, c_i32]),
     "bp_set_write_blocks": (c_i32, [c_i32]),
     "bp_set_stub_fork": (c_i32, [c_i32]),
+    "bp_dlrm_master_sgd": (c_i32, [P(SgdTensors), c_f32, c_vp]),
+    "bp_engine_dlrm_backward_begin": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_i32, c_f32, c_f32, c_i32,
+                                              c_i32]),
     "bp_engine_plan_ready": (c_i32, [c_vp, c_i32, c_vp]),
     "bp_engine_join": (c_i32, [c_vp, c_vp]),
     "bp_engine_set_timing": (c_i32, [c_vp, c_i32]),
@@ -243,7 +254,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         fn.restype = res
         fn.argtypes = args
     structs = (ErrorT, PrepView, PlanBuffers, PlannerStats, CacheStats, EvictBuffers, CacheView, EngineConfig,
-               StepResult, EngineParts, PlannerDump, PeerXchg)
+               StepResult, EngineParts, PlannerDump, PeerXchg, SgdTensors)
     for i, st in enumerate(structs):
         if lib_.bp_abi_sizeof(i) != C.sizeof(st):
             raise NativeUnavailable(f"ABI mismatch for {st.__name__}: library {lib_.bp_abi_sizeof(i)} bytes, "

@@ -28,6 +28,7 @@ extern "C" int64_t bp_abi_sizeof(int32_t which) {
     case 9: return (int64_t)sizeof(bp_engine_parts_t);
     case 10: return (int64_t)sizeof(bp_planner_dump_t);
     case 11: return (int64_t)sizeof(bp_peer_xchg);
+    case 12: return (int64_t)sizeof(bp_sgd_tensors);
     default: return -1;
   }
 }

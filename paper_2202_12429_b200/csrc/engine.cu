@@ -1126,6 +1126,30 @@ extern "C" int bp_engine_dlrm_backward_sorted(bp_engine* e, int64_t pos, int32_t
   return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
 }
 
+// Asynchronous DLRM part 2: the backward + eviction + counters enqueued only
+// (grad_sorted: rows in key-sorted order, else occurrence order);
+// bp_engine_train_end waits and reads the counters, so the host can enqueue
+// the next iteration's forward and dense step first.
+extern "C" int bp_engine_dlrm_backward_begin(bp_engine* e, int64_t pos, int32_t plan_slot, const float* d_grad,
+                                             int32_t grad_sorted, int32_t model_dim, int32_t opt, float lr, float eps,
+                                             int32_t chunk_slot, int32_t drain_slot) {
+  using namespace bp;
+  if (e->step_count == bp_engine::kStepRing) return BP_ERR_ENGINE;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  PlanSlot& ps = e->plans[plan_slot];
+  bp_cache_view cv;
+  bp_cache_get_view(e->cache, &cv);
+  stage_begin(e, kStageTrainer, e->compute);
+  int rc = grad_sorted ? bp_embbag_backward_sorted(P, d_grad, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty,
+                                                   model_dim, opt, lr, eps, e->stats, e->compute)
+                       : bp_embbag_backward(P, d_grad, nullptr, nullptr, cv.d_values, e->cfg.dim, e->slots_s,
+                                            cv.d_dirty, model_dim, opt, lr, eps, e->stats, e->compute);
+  stage_end(e, kStageTrainer, e->compute);
+  if (rc) return rc;
+  return engine_finish_begin(e, P, ps, chunk_slot, drain_slot);
+}
+
 // DLRM hybrid parallel over NVLink peer memory (csrc/peer.cu): the same two
 // halves, the forward storing pooled rows into the example owners' buffers,
 // the backward loading gradient rows from them.

@@ -328,3 +328,54 @@ extern "C" int bp_dlrm_interact_backward_rows(const void* d_x, int32_t x_bf16, c
   BP_LAUNCH_CHECK();
   return BP_OK;
 }
+
+// Mixed-precision SGD of the dense MLPs in one launch (DLRM mode, bf16
+// compute copy): for every tensor k, master_k -= lr * float(grad_k) (fp32),
+// then lowp_k = bf16(master_k) -- replaces ~2 x (#tensors) eager kernels per
+// step.  The tensor table travels by value in the kernel parameters, so the
+// launch is CUDA-graph capturable.
+namespace bp {
+
+struct SgdTable {
+  int n;
+  float lr;
+  float* master[BP_SGD_MAX_TENSORS];
+  __nv_bfloat16* lowp[BP_SGD_MAX_TENSORS];
+  const __nv_bfloat16* grad[BP_SGD_MAX_TENSORS];
+  long long end[BP_SGD_MAX_TENSORS];  // inclusive prefix sums of the sizes
+};
+
+__global__ void __launch_bounds__(256) k_master_sgd(const SgdTable t) {
+  const long long total = t.end[t.n - 1];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    int k = 0;
+    while (i >= t.end[k]) ++k;
+    const long long j = i - (k ? t.end[k - 1] : 0);
+    const float m = __fsub_rn(t.master[k][j], __fmul_rn(t.lr, __bfloat162float(t.grad[k][j])));
+    t.master[k][j] = m;
+    t.lowp[k][j] = __float2bfloat16_rn(m);
+  }
+}
+
+}  // namespace bp
+
+extern "C" int bp_dlrm_master_sgd(const bp_sgd_tensors* tensors, float lr, bp_stream_t stream) {
+  using namespace bp;
+  if (!tensors || tensors->n < 1 || tensors->n > BP_SGD_MAX_TENSORS) return BP_ERR_INVALID;
+  SgdTable t;
+  t.n = tensors->n;
+  t.lr = lr;
+  long long acc = 0;
+  for (int k = 0; k < t.n; ++k) {
+    if (tensors->numel[k] < 0) return BP_ERR_INVALID;
+    t.master[k] = tensors->master[k];
+    t.lowp[k] = reinterpret_cast<__nv_bfloat16*>(tensors->lowp[k]);
+    t.grad[k] = reinterpret_cast<const __nv_bfloat16*>(tensors->grad[k]);
+    acc += tensors->numel[k];
+    t.end[k] = acc;
+  }
+  if (acc == 0) return BP_OK;
+  k_master_sgd<<<grid_for(acc, 256, kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(t);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}

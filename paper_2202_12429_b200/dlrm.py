@@ -213,7 +213,17 @@ class _MasterSGD:
 
     @torch.no_grad()
     def step(self):
-        # per tensor: the mixed-dtype foreach path is not CUDA-graph capturable
+        # one fused launch over every tensor (bp_dlrm_master_sgd): fp32 master
+        # update from the bf16 gradient, then the bf16 copy refreshed
+        if self.master[0].is_cuda and len(self.master) <= L.SGD_MAX_TENSORS:
+            t = L.SgdTensors()
+            t.n = len(self.master)
+            for k, (m, p) in enumerate(zip(self.master, self.lowp)):
+                t.master[k], t.lowp[k], t.grad[k] = m.data_ptr(), p.data_ptr(), p.grad.data_ptr()
+                t.numel[k] = m.numel()
+            L.check(L.lib().bp_dlrm_master_sgd(C.byref(t), float(np.float32(self.lr)), L.stream_ptr()),
+                    "bp_dlrm_master_sgd")
+            return
         for m, p in zip(self.master, self.lowp):
             m.add_(p.grad, alpha=-self.lr)
         torch._foreach_copy_(self.lowp, self.master)
@@ -248,14 +258,33 @@ class DLRMTrainer:
         """Width of a stored row: weights (+ Adagrad accumulators)."""
         return 2 * self.dim if self.dcfg.opt_code == BP_OPT_ADAGRAD else self.dim
 
+    def _pad_dense(self, dense: torch.Tensor) -> torch.Tensor:
+        """Dense features padded to the bottom MLP's aligned input width once,
+        so the per-step copy into the graph's static input is contiguous (a
+        strided [B, 13] -> [B, 16] copy runs as a slow 2D memcpy)."""
+        pad = self.model.dense_pad
+        if pad and dense.shape[1] == self.model.num_dense:
+            dense = nn.functional.pad(dense, (0, pad))
+        return dense.contiguous()
+
     def set_device_dense(self, pos: int, dense: torch.Tensor, labels: torch.Tensor) -> None:
-        self._dense_dev[pos] = (dense, labels)
+        self._dense_dev[pos] = (self._pad_dense(dense), labels)
+
+    def can_split(self) -> bool:
+        """Single GPU: the iteration is enqueued by train_begin and its counters
+        read later by the engine (bp_engine_train_end), so the host prepares
+        the next iteration while this one runs."""
+        return self.exchange is None or self.exchange.world <= 1
 
     def train(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res) -> None:
         if self.exchange is not None and self.exchange.world > 1:
             if hasattr(self.exchange, "rows_x"):
                 return self._train_peer(pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
             return self._train_hybrid(pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
+        self.train_begin(pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain)
+        L.check(pipe.lib.bp_engine_train_end(pipe.eng, C.byref(res)), "bp_engine_train_end")
+
+    def train_begin(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain) -> None:
         lib = pipe.lib
         batch = pipe.batches[pos]
         n_occ = int(batch.packed_occurrences()[0].size)
@@ -290,23 +319,20 @@ class DLRMTrainer:
                 self.opt.step()
                 grad = emb.grad.contiguous()
                 self.losses.append(loss.detach())
-            self._backward(pipe, pos, plan, grad, chunk, drain, res)
+            L.check(lib.bp_engine_dlrm_backward_begin(pipe.eng, pos, plan.slot, L.ptr(grad), int(self._sorted),
+                                                      self.dim, self.dcfg.opt_code,
+                                                      float(np.float32(self.dcfg.emb_lr)),
+                                                      float(np.float32(self.dcfg.adagrad_eps)), chunk, drain),
+                    "bp_engine_dlrm_backward_begin")
 
     def _inputs(self, pos, batch, sl):
         dev = self._dense_dev.pop(pos, None)
         if dev is None:
             dense = torch.from_numpy(np.ascontiguousarray(batch.dense[sl], dtype=np.float32)).to("cuda")
             labels = torch.from_numpy(np.ascontiguousarray(batch.labels[sl], dtype=np.float32)).to("cuda")
-            return dense, labels
+            return self._pad_dense(dense), labels
         dense, labels = dev
         return dense[sl], labels[sl]
-
-    def _backward(self, pipe, pos, plan, grad, chunk, drain, res) -> None:
-        fn = pipe.lib.bp_engine_dlrm_backward_sorted if self._sorted else pipe.lib.bp_engine_dlrm_backward
-        L.check(fn(pipe.eng, pos, plan.slot, L.ptr(grad), self.dim, self.dcfg.opt_code,
-                                                 float(np.float32(self.dcfg.emb_lr)),
-                                                 float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
-                                                 C.byref(res)), "bp_engine_dlrm_backward")
 
     def _train_hybrid(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res) -> None:
         """N > 1 (hybrid.py): this rank's tables over the global batch ->
@@ -418,7 +444,7 @@ class DLRMTrainer:
         # peer exchange's row buffer)
         emb = torch.zeros((b, t, self.dim), dtype=torch.float32, device=dev, requires_grad=True) if emb is None \
             else emb.detach().requires_grad_(True)
-        dense = torch.zeros((b, n_dense + self.model.dense_pad), dtype=torch.float32, device=dev)
+        dense = torch.zeros((b, self.model.num_dense + self.model.dense_pad), dtype=torch.float32, device=dev)
         labels = torch.zeros((b,), dtype=torch.float32, device=dev)
         # sorted-gradient row map (filled per batch by bp_engine_dlrm_grad_rows
         # before each replay; identity for the warm-up passes)

@@ -193,6 +193,9 @@ class _Pipeline:
         self.probe = None
         self.lib = L.lib()
         self.trainer = trainer  # None: the reference's stub trainer; else e.g. dlrm.DLRMTrainer
+        # iteration enqueued in _begin, counters read in _end (stub mode and
+        # single-GPU DLRM): the next iteration can be enqueued in between
+        self._split = trainer is None or bool(getattr(trainer, "can_split", lambda: False)())
         stub = cfg.stub()
         # Rows in the cache/store: the embedding (+ optimizer state in DLRM/Adagrad mode).
         width = trainer.row_width() if trainer is not None else schema.emb_dim
@@ -549,11 +552,11 @@ class _Pipeline:
         if pos not in self._inflight:
             self._begin(pos)
         nxt = pos + 1
-        if (early and self.trainer is None and self.fault is None and self.events is None and self.snapshots is None
+        if (early and self._split and self.fault is None and self.events is None and self.snapshots is None
                 and nxt < self.n and nxt in self.staged and nxt not in self._inflight
                 and len(self.free_chunks) >= (2 if nxt == self.n - 1 else 1)):
             self._begin(nxt)
-        if self.trainer is None and self._thread is None:
+        if self._split and self._thread is None:
             # plan emission (planner stream) overlaps the queued GPU work
             self._emit_ahead()
         self._end(pos)
@@ -586,6 +589,8 @@ class _Pipeline:
         if self.trainer is None:
             L.check(lib.bp_engine_train_begin(self.eng, pos, plan.slot, nxt, skip_key, has_skip, chunk, drain),
                     "bp_engine_train_begin")
+        elif self._split:
+            self.trainer.train_begin(self, pos, plan, nxt, skip_key, has_skip, chunk, drain)
 
     def _end(self, pos: int) -> None:
         cfg, lib = self.cfg, self.lib
@@ -593,7 +598,7 @@ class _Pipeline:
         iteration = self.batches[pos].iteration
         plan, arrival, skip_key, has_skip, nxt, chunk, drain = self._inflight.pop(pos)
         res = self.result
-        if self.trainer is None:
+        if self._split:
             L.check(lib.bp_engine_train_end(self.eng, C.byref(res)), "bp_engine_train_end")
         else:
             self.trainer.train(self, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
