@@ -231,7 +231,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     gbatch = BATCH * world
     full = make_batches(n_batches, args.seed, gbatch)
     batches = full if world == 1 else shard_batches(full, tables)
-    cfg = EngineConfig(cache_capacity=cap, batch_size=gbatch, lookahead=0, num_trainers=1, num_shards=1, seed=11)
+    # N GPUs = the reference's N data-parallel trainers (rank r = examples
+    # [r*B/N, (r+1)*B/N) of the global batch; gradients combined in rank order)
+    trainers = int(os.environ.get("BAGPIPE_B200_BENCH_TRAINERS", str(world)))
+    cfg = EngineConfig(cache_capacity=cap, batch_size=gbatch, lookahead=0, num_trainers=trainers, num_shards=1,
+                       seed=11)
 
     # ---- value: inputs resident in HBM before timing
     dev_inputs = {}
@@ -257,6 +261,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     records = pipe.records[warm:warm + steps]
     launches_per_step = count_launches(pipe, warm + steps)
     stages = _stage_breakdown(pipe, warm + steps + 1, 8)
+    dump = os.environ.get("BAGPIPE_B200_BENCH_DUMP")  # debug: per-rank stage times
+    if dump:
+        with open(f"{dump}.rank{rank}.json", "w") as fh:
+            json.dump({"rank": rank, "tables": list(tables), "ms_per_step": ms / steps,
+                       "stages": {k: v[0] for k, v in stages.items()}}, fh)
     # the same K steps with every engine stream drained around each flush
     # (no overlap across iterations): reported beside the value
     ms_excl, _ = _timed_steps(pipe, warm + steps + 9, steps, flush_buf, torch, exclusive=1)
@@ -289,7 +298,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         dlrm = run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank, world, len(tables))
 
     t = torch.tensor([ms, e2e_ms], device="cuda", dtype=torch.float64)
+    by_rank = [ms / steps]
     if world > 1:
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        by_rank = [float(x[0]) / steps for x in allt]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, e2e_max = float(t[0]), float(t[1])
     if rank != 0:
@@ -324,6 +337,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                    "rows": sc.total_rows,
                    "emb_dim": DIM, "cache_capacity_per_gpu": cap, "lookahead": lookahead0,
                    "parallelism": "single" if world == 1 else f"table-sharded x{world} (weak: {BATCH} examples/GPU)",
+                   "num_trainers": trainers,
                    "l2": "flushed at the start of every timed iteration by the engine (256 MiB memset on the compute "
                          "stream, inside the timed span; " + ("plan and host-link streams fenced around it"
                                                               if FLUSH_EXCLUSIVE else
@@ -352,6 +366,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "wall_ms_timed_region": wall_ms,
         "l2_flush_ms_per_step": flush_ms / steps,
         "ms_per_step_exclusive_flush": ms_excl / steps,
+        "ms_per_step_by_rank": by_rank,
     }
     if dlrm is not None:
         out["dlrm"] = dlrm["summary"]

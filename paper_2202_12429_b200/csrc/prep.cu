@@ -138,7 +138,12 @@ constexpr int kColThreads = 1024;
 constexpr int kColIpt = 16;
 constexpr int kColMax = kColThreads * kColIpt;  // 16384 examples
 constexpr int kColWarps = kColThreads / 32;
+constexpr int kColMaxChunks = 64;  // columnar path up to 64 x 16,384 examples
 
+// Batches of more than kColMax examples (N-GPU weak scaling: N x 16,384):
+// CTA (column c, chunk k) sorts examples [k*kColMax, (k+1)*kColMax) of the
+// column, then k_prep_col_merge places every element at its rank in the
+// column's merged order.
 __global__ void __launch_bounds__(kColThreads, 1) k_prep_table_sort(const uint64_t* __restrict__ keys, int n_ex,
                                                                      int n_cols, const int64_t* __restrict__ base,
                                                                      const int32_t* __restrict__ col_tables,
@@ -150,13 +155,15 @@ __global__ void __launch_bounds__(kColThreads, 1) k_prep_table_sort(const uint64
   uint32_t* dtot = wcnt + kColWarps * 256;                                        // [256]
   const int c = blockIdx.x;
   const int t = col_tables[c];
+  const int ex0 = blockIdx.y * kColMax;  // this CTA's chunk of examples
+  const int n_chunk = min(kColMax, n_ex - ex0);
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   unsigned long long e[kColIpt];
 #pragma unroll
   for (int r = 0; r < kColIpt; ++r) {
     const int ex = warp * (32 * kColIpt) + r * 32 + lane;
-    e[r] = ex < n_ex ? (((keys[(long long)ex * n_cols + c] & kRowMask) << 14) | (unsigned long long)ex)
-                     : ~0ull;  // padding sorts last
+    e[r] = ex < n_chunk ? (((keys[(long long)(ex0 + ex) * n_cols + c] & kRowMask) << 14) | (unsigned long long)ex)
+                        : ~0ull;  // padding sorts last
   }
   for (int shift = 14; shift < 14 + row_bits; shift += 8) {
     for (int i = lane; i < 256; i += 32) wcnt[warp * 256 + i] = 0;
@@ -215,16 +222,55 @@ __global__ void __launch_bounds__(kColThreads, 1) k_prep_table_sort(const uint64
     for (int r = 0; r < kColIpt; ++r) e[r] = buf[warp * (32 * kColIpt) + r * 32 + lane];
     __syncthreads();
   }
-  const long long out0 = (long long)c * n_ex;  // columns are in increasing table order
+  const long long out0 = (long long)c * n_ex + ex0;  // columns are in increasing table order
 #pragma unroll
   for (int r = 0; r < kColIpt; ++r) {
     const int i = warp * (32 * kColIpt) + r * 32 + lane;
-    if (i < n_ex) {
+    if (i < n_chunk) {
       const unsigned long long x = e[r];
-      const long long ex = (long long)(x & 0x3FFFull);
+      const long long ex = ex0 + (long long)(x & 0x3FFFull);
       sk_out[out0 + i] = (uint32_t)(base[t] + (long long)(x >> 14));
       pos_out[out0 + i] = (uint32_t)(ex * n_cols + c);
     }
+  }
+}
+
+// Stable merge of a column's sorted chunks: element i of chunk k goes to
+// (its index in chunk k) + (# keys <= it in earlier chunks) + (# keys < it in
+// later chunks) -- earlier chunks hold smaller positions, so equal keys keep
+// position order, exactly the single-sort output.
+__global__ void k_prep_col_merge(const uint32_t* __restrict__ sk_in, const uint32_t* __restrict__ pos_in, int n_ex,
+                                 int n_cols, int n_chunks, uint32_t* __restrict__ sk_out,
+                                 uint32_t* __restrict__ pos_out) {
+  const long long total = (long long)n_ex * n_cols;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long c = i / n_ex;
+    const int j = (int)(i - c * n_ex);
+    const int k = j / kColMax;
+    const uint32_t key = sk_in[i];
+    const uint32_t* col = sk_in + c * n_ex;
+    long long dst = j - (long long)k * kColMax;
+    for (int k2 = 0; k2 < n_chunks; ++k2) {
+      if (k2 == k) continue;
+      const int lo0 = k2 * kColMax, hi0 = min(n_ex, lo0 + kColMax);
+      int lo = lo0, hi = hi0;
+      if (k2 < k) {  // upper bound: keys <= key
+        while (lo < hi) {
+          const int m = (lo + hi) >> 1;
+          if (col[m] <= key) lo = m + 1;
+          else hi = m;
+        }
+      } else {  // lower bound: keys < key
+        while (lo < hi) {
+          const int m = (lo + hi) >> 1;
+          if (col[m] < key) lo = m + 1;
+          else hi = m;
+        }
+      }
+      dst += lo - lo0;
+    }
+    sk_out[c * n_ex + dst] = key;
+    pos_out[c * n_ex + dst] = pos_in[i];
   }
 }
 
@@ -255,8 +301,17 @@ static int prep_build(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, c
       BP_CUDA_TRY(cudaFuncSetAttribute(k_prep_table_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
       attr_set = true;
     }
-    k_prep_table_sort<<<col->n_cols, kColThreads, kColSmem, s>>>(d_keys, col->n_ex, col->n_cols, sc->d_table_base,
-                                                                  col->d_tables, col->row_bits, (uint32_t*)ka, va);
+    const int n_chunks = (col->n_ex + kColMax - 1) / kColMax;
+    if (n_chunks == 1) {
+      k_prep_table_sort<<<col->n_cols, kColThreads, kColSmem, s>>>(d_keys, col->n_ex, col->n_cols,
+                                                                    sc->d_table_base, col->d_tables, col->row_bits,
+                                                                    (uint32_t*)ka, va);
+    } else {
+      k_prep_table_sort<<<dim3(col->n_cols, n_chunks), kColThreads, kColSmem, s>>>(
+          d_keys, col->n_ex, col->n_cols, sc->d_table_base, col->d_tables, col->row_bits, (uint32_t*)kb, vb);
+      k_prep_col_merge<<<grid_for(n, 256), 256, 0, s>>>((const uint32_t*)kb, vb, col->n_ex, col->n_cols, n_chunks,
+                                                        (uint32_t*)ka, va);
+    }
     which = 0;
   } else if (P->schema_mode) {
     k_prep_keys_schema<<<g, 256, 0, s>>>(d_keys, n, sc->d_table_base, sc->d_rows, sc->num_tables,
@@ -409,7 +464,8 @@ extern "C" int bp_prep_create(bp_ctx* ctx, const bp_schema* sc, const uint64_t* 
 
 // Columnar batch: keys laid out [n_ex][n_cols], column c holding table
 // h_tables[c] (strictly increasing).  Takes the per-column shared-memory
-// sort when n_ex <= 16384, else the generic path.
+// sort (chunks of 16,384 examples merged by rank above that), else the
+// generic path.
 extern "C" int bp_prep_create_columnar(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_keys,
                                        const uint8_t* d_labels, int64_t n_ex, int32_t n_cols, const int32_t* d_tables,
                                        const int64_t* h_rank_bounds, int32_t num_ranks, int64_t iteration,
@@ -417,7 +473,7 @@ extern "C" int bp_prep_create_columnar(bp_ctx* ctx, const bp_schema* sc, const u
   using namespace bp;
   if (!sc || n_cols < 1 || n_ex < 0) return BP_ERR_INVALID;
   const int64_t n_occ = n_ex * n_cols;
-  if (n_ex > kColMax || n_ex == 0)
+  if (n_ex > kColMax * kColMaxChunks || n_ex == 0)
     return prep_create_impl(ctx, sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, flags, 0, 0,
                             stream, out, nullptr);
   int64_t max_rows = 1;

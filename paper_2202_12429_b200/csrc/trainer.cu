@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
     const long long* __restrict__ d_num_long, long long long_cap, float* __restrict__ rows, const int32_t* __restrict__ row_index,
     uint8_t* __restrict__ dirty, int dim, float c_value, float c_label, float lr, int mode,
     float* __restrict__ grad_out, const uint32_t* __restrict__ my_ids, const int64_t* __restrict__ next_mark,
-    long long next_tag, unsigned long long* __restrict__ stats) {
+    long long next_tag, unsigned long long* __restrict__ stats, const uint32_t* __restrict__ occ_pos,
+    const long long* __restrict__ rank_bounds, int num_ranks, float* __restrict__ rank_parts) {
   const unsigned lane = threadIdx.x & 31u;
   const uint4* __restrict__ chunks = reinterpret_cast<const uint4*>(occ_label);
   const float b0 = __fmul_rn(c_label, -0.5f), b1 = __fmul_rn(c_label, 0.5f);
@@ -115,11 +116,49 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
     // very long segments first (front of the list), then the others (back)
     unsigned long long* tr = g_long_trace ? g_long_trace + blockIdx.x * 8 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = clock64();
-    for (long long li = blockIdx.x; li < n_long; li += gridDim.x) {
+    // rank split (rank_parts != nullptr, num_ranks > 1): one work item per
+    // (key, rank) -- the rank's run of the key's occurrences is an
+    // independent sequential chain; k_stub_long_combine adds the rank
+    // partials in ascending rank order, which is exactly the reference's
+    // combine (a rank without occurrences contributes +0.0, an exact no-op)
+    const int T = rank_parts ? num_ranks : 1;
+    for (long long it = blockIdx.x; it < n_long * T; it += gridDim.x) {
+      const long long li = it / T;
+      const int rk = (int)(it - li * T);
       const uint32_t s = li < n_vlong ? long_list[li] : long_list[long_cap - 1 - (li - n_vlong)];
-      const uint32_t a = seg_start[s], b = seg_start[s + 1];
+      uint32_t a = seg_start[s], b = seg_start[s + 1];
       const int32_t row = row_index ? row_index[s] : (int32_t)s;
       if (row < 0) continue;  // block-uniform: the miss is already recorded
+      if (T > 1) {
+        // the rank's occurrences: positions ascend within the key's run
+        uint32_t lo = a, hi = b;
+        if (rk > 0) {
+          const long long bound = rank_bounds[rk];
+          uint32_t l = a, h = b;
+          while (l < h) {
+            const uint32_t m = (l + h) >> 1;
+            if ((long long)occ_pos[m] < bound) l = m + 1;
+            else h = m;
+          }
+          lo = l;
+        }
+        if (rk + 1 < T) {
+          const long long bound = rank_bounds[rk + 1];
+          uint32_t l = lo, h = b;
+          while (l < h) {
+            const uint32_t m = (l + h) >> 1;
+            if ((long long)occ_pos[m] < bound) l = m + 1;
+            else h = m;
+          }
+          hi = l;
+        }
+        if (lo >= hi) {  // block-uniform: no occurrence in this rank
+          for (int d = threadIdx.x; d < dim; d += blockDim.x) rank_parts[(it)*dim + d] = 0.f;
+          continue;
+        }
+        a = lo;
+        b = hi;
+      }
       if (tr && threadIdx.x == 0) tr[5] = b - a;
       float v[DPL], t0[DPL], t1[DPL], sc[DPL], acc[DPL], comb[DPL];
 #pragma unroll
@@ -187,6 +226,16 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
           if (tr && threadIdx.x == 0) tr[3] = clock64() + 0 * (unsigned long long)__float_as_uint(acc[0]);
         }
         __syncthreads();
+      }
+      if (T > 1) {  // the rank partial, for k_stub_long_combine
+        if (chain_lane) {
+#pragma unroll
+          for (int q = 0; q < DPL; ++q) {
+            const int d = (int)threadIdx.x + q * G;
+            if (d < dim) rank_parts[it * dim + d] = __fadd_rn(comb[q], acc[q]);
+          }
+        }
+        continue;
       }
       if (threadIdx.x < 32) {
         bool nonzero = false;
@@ -308,6 +357,50 @@ __global__ void __launch_bounds__(256, 6) k_stub_step(
       if (lane == 0) {
         if (cm) atomicAdd(&stats[0], (unsigned long long)__popc(cm));
         if (dm) atomicAdd(&stats[1], (unsigned long long)__popc(dm));
+      }
+    }
+  }
+}
+
+// Rank partials of the long keys -> per key ((0 + G_0) + G_1) + ... in rank
+// order, then the SGD update / gradient output, dirty and counters (the tail
+// of k_stub_step_long for the rank-split case).  A warp per long key.
+template <int G, int DPL>
+__global__ void __launch_bounds__(256) k_stub_long_combine(
+    const long long* __restrict__ d_num_long, const uint32_t* __restrict__ long_list, long long long_cap, int T,
+    const float* __restrict__ rank_parts, float* __restrict__ rows, const int32_t* __restrict__ row_index,
+    uint8_t* __restrict__ dirty, int dim, float lr, int mode, float* __restrict__ grad_out,
+    const uint32_t* __restrict__ my_ids, const int64_t* __restrict__ next_mark, long long next_tag,
+    unsigned long long* __restrict__ stats) {
+  const long long n_vlong = d_num_long[0], n_long = n_vlong + d_num_long[1];
+  const unsigned lane = threadIdx.x & 31u;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long li = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); li < n_long; li += warps) {
+    const uint32_t s = li < n_vlong ? long_list[li] : long_list[long_cap - 1 - (li - n_vlong)];
+    const int32_t row = row_index ? row_index[s] : (int32_t)s;
+    if (row < 0) continue;  // warp-uniform
+    bool nonzero = false;
+#pragma unroll
+    for (int q = 0; q < DPL; ++q) {
+      const int d = (int)lane + q * G;
+      if (lane < (unsigned)G && d < dim) {
+        float comb = 0.f;
+        for (int r = 0; r < T; ++r) comb = __fadd_rn(comb, rank_parts[(li * T + r) * dim + d]);
+        nonzero |= comb != 0.f;
+        if (mode == BP_STUB_SGD) {
+          const float v = rows[(long long)row * dim + d];
+          rows[(long long)row * dim + d] = __fsub_rn(v, __fmul_rn(lr, comb));
+        } else {
+          grad_out[(long long)s * dim + d] = comb;
+        }
+      }
+    }
+    const bool nz = __ballot_sync(0xffffffffu, nonzero) != 0;
+    if (lane == 0) {
+      if (nz && dirty && mode == BP_STUB_SGD) dirty[row] = 1;
+      if (stats) {
+        if (next_mark && next_mark[my_ids[s]] == next_tag) atomicAdd(&stats[0], 1ull);
+        if (nz) atomicAdd(&stats[1], 1ull);
       }
     }
   }
@@ -452,11 +545,23 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
     BP_CUDA_TRY(cudaStreamWaitEvent(side.s, side.fork, 0));
     ls = side.s;
   }
+  // T > 1: the long keys' rank runs are separate chains (rank partials in a
+  // stream-ordered scratch), combined in rank order by k_stub_long_combine
+  const int T = P->num_ranks;
+  float* parts = nullptr;
+  if (T > 1) BP_CUDA_TRY(pool_alloc(&parts, (size_t)P->long_cap * T * dim, ls));
   BP_DISPATCH_GD(G, dpl,
                  (long_attr<g_, d_>(), k_stub_step_long<g_, d_><<<kLongBlocks, 128, kLongSmemPad, ls>>>(
                      P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,
                      d_row_index, d_dirty, dim, c_value, c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark,
-                     next_tag, (unsigned long long*)d_stats)));
+                     next_tag, (unsigned long long*)d_stats, P->d_occ_pos, P->d_rank_bounds, T, parts)));
+  if (T > 1) {
+    BP_DISPATCH_GD(G, dpl,
+                   (k_stub_long_combine<g_, d_><<<kNumSMs, 256, 0, ls>>>(
+                       P->d_num_long, P->d_long, P->long_cap, T, parts, d_rows, d_row_index, d_dirty, dim, lr, mode,
+                       d_grad_out, P->d_uniq_id_s, d_next_mark, next_tag, (unsigned long long*)d_stats)));
+    cudaFreeAsync(parts, ls);
+  }
   BP_DISPATCH_GD(G, dpl,
                  (k_stub_step<g_, d_><<<blocks, threads, 0, s>>>(
                      P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,

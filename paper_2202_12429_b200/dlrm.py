@@ -334,6 +334,13 @@ class DLRMTrainer:
         dense, labels = dev
         return dense[sl], labels[sl]
 
+    def _backward(self, pipe, pos, plan, grad, chunk, drain, res) -> None:
+        """Synchronous EmbeddingBag backward (hybrid NCCL path; occurrence-order gradients)."""
+        L.check(pipe.lib.bp_engine_dlrm_backward(pipe.eng, pos, plan.slot, L.ptr(grad), self.dim, self.dcfg.opt_code,
+                                                 float(np.float32(self.dcfg.emb_lr)),
+                                                 float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
+                                                 C.byref(res)), "bp_engine_dlrm_backward")
+
     def _train_hybrid(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res) -> None:
         """N > 1 (hybrid.py): this rank's tables over the global batch ->
         all-to-all -> the dense step on this rank's B/N examples -> reverse

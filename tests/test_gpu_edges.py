@@ -57,8 +57,8 @@ def test_single_row_tables_every_occurrence_one_key():
 
 
 def test_batch_larger_than_columnar_sort():
-    """20,000 examples per batch > the 16,384 of the per-table smem sort:
-    the generic radix-sort prep path."""
+    """20,000 examples per batch > the 16,384 of one per-table smem sort:
+    two chunk sorts per column merged by rank."""
     schema = Schema(2, (50_000, 300), 0, 4)
     rows, labels, dense = generate_columns(ZipfSpec(schema, 1.05, 3 * 20_000, seed=8))
     batches = batchify_columns(rows, labels, dense, 20_000)

@@ -234,9 +234,11 @@ def test_label_only_term_and_local_gradients():
 
 
 # ---------------------------------------------------------------- prep
-def test_columnar_prep_equals_generic_prep():
-    """The per-column shared-memory sort and the generic global radix sort
-    produce identical preps (order of every array), incl. trainer ranks."""
+@pytest.mark.parametrize("batch", [16384, 40000])
+def test_columnar_prep_equals_generic_prep(batch):
+    """The per-column shared-memory sort (for > 16,384 examples: chunk sorts
+    merged by rank) and the generic global radix sort produce identical
+    preps (order of every array), incl. trainer ranks."""
     import ctypes as C
 
     import torch
@@ -246,8 +248,8 @@ def test_columnar_prep_equals_generic_prep():
     from paper_2202_12429_b200.traces import ZipfSpec, batchify_columns, generate_columns
 
     schema = Schema(5, (3, 70_000, 1000, 5_000_000, 17), 0, 4)
-    rows, labels, _ = generate_columns(ZipfSpec(schema, 1.1, 2 * 16384, seed=9))
-    for b in batchify_columns(rows, labels, None, 16384):
+    rows, labels, _ = generate_columns(ZipfSpec(schema, 1.1, 2 * batch, seed=9))
+    for b in batchify_columns(rows, labels, None, batch):
         keys, labs, _ = b.packed_occurrences()
         rb = b.rank_bounds(3)
         col = DevicePrep(keys, labs, rb, b.iteration, schema, columns=(b.num_examples, b.table_ids()))
