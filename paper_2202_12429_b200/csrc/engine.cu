@@ -563,8 +563,18 @@ extern "C" int bp_engine_parts(bp_engine* e, bp_engine_parts_t* out) {
   return BP_OK;
 }
 
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 // Batch entering the window: upload (host keys go through a pinned ring and
-// one H2D copy each for keys and labels) and device prep on the compute stream.
+// one H2D copy each for keys and labels -- or straight from the caller's
+// arrays when they are pinned) and device prep on the prep stream.
 static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64_t* keys, const uint8_t* labels,
                       int64_t n_occ, int64_t n_ex, int32_t n_cols, const int32_t* h_tables,
                       const int64_t* h_rank_bounds, int32_t num_ranks, int32_t keys_on_host) {
@@ -579,7 +589,17 @@ static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64
   const uint64_t* d_keys = keys;
   const uint8_t* d_labels = labels;
   int si = -1;
-  if (keys_on_host && n_occ > 0) {
+  if (keys_on_host && n_occ > 0 && host_pinned(keys) && host_pinned(labels)) {
+    // the caller's arrays are pinned already: DMA them straight from there
+    // (no copy into the upload ring; they stay alive until release)
+    si = e->staging_i;
+    e->staging_i ^= 1;
+    BP_CUDA_TRY(cudaStreamWaitEvent(q, e->staging_free[si], 0));
+    BP_CUDA_TRY(cudaMemcpyAsync(e->d_keys_staging[si], keys, n_occ * sizeof(uint64_t), cudaMemcpyHostToDevice, q));
+    BP_CUDA_TRY(cudaMemcpyAsync(e->d_labels_staging[si], labels, n_occ, cudaMemcpyHostToDevice, q));
+    d_keys = e->d_keys_staging[si];
+    d_labels = e->d_labels_staging[si];
+  } else if (keys_on_host && n_occ > 0) {
     UploadSlot& u = e->uploads[e->next_upload];
     e->next_upload = (e->next_upload + 1) % (int)e->uploads.size();
     if (u.used) BP_CUDA_TRY(cudaEventSynchronize(u.done));

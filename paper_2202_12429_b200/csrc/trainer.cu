@@ -202,13 +202,19 @@ __global__ void __launch_bounds__(128) k_stub_step_long(
             uint32_t info = winfo[k];
             if constexpr (DPL == 1) {
               if (info & 0x10000u) {
-                // a run of plain chunks: a tight loop of R2P + select + add
+                // a run of plain chunks: a tight loop of R2P + select + add;
+                // the chunk info two ahead is loaded each round and consumed
+                // two rounds later, so its shared-memory latency never sits
+                // in front of the 16-add chain
                 float a0 = acc[0];
+                uint32_t nxt = k + 1 < nchunk ? winfo[k + 1] : 0u;
                 do {
+                  const uint32_t cur = info;
+                  info = nxt;
+                  nxt = k + 2 < nchunk ? winfo[k + 2] : 0u;
 #pragma unroll
-                  for (int i = 0; i < 16; ++i) a0 = __fadd_rn(a0, ((info >> i) & 1u) ? t1[0] : t0[0]);
+                  for (int i = 0; i < 16; ++i) a0 = __fadd_rn(a0, ((cur >> i) & 1u) ? t1[0] : t0[0]);
                   ++k;
-                  info = k < nchunk ? winfo[k] : 0u;
                 } while (info & 0x10000u);
                 acc[0] = a0;
                 continue;

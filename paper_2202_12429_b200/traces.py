@@ -175,6 +175,20 @@ class Batch:
     def __repr__(self) -> str:
         return f"Batch(iteration={self.iteration}, examples={self.num_examples})"
 
+    def pin_memory(self) -> "Batch":
+        """Keep the packed occurrences (keys, labels) in pinned host memory, so
+        the engine DMAs them straight to the GPU (no staging copy)."""
+        import torch
+
+        keys, labels, offsets = self.packed_occurrences()
+        pk = torch.empty(keys.size, dtype=torch.uint64, pin_memory=True)
+        pl = torch.empty(labels.size, dtype=torch.uint8, pin_memory=True)
+        pk.numpy()[:] = keys
+        pl.numpy()[:] = labels
+        self._memo["pinned"] = (pk, pl)  # owners of the pinned memory
+        self._memo["occ"] = (pk.numpy(), pl.numpy(), offsets)
+        return self
+
     def packed_occurrences(self) -> tuple:
         """(keys u64[n_occ], labels u8[n_occ], example_offsets i64[n+1]).
 
