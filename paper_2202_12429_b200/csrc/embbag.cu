@@ -831,15 +831,12 @@ __global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
   __shared__ float4 wagg[8][Q];
   __shared__ int wflag[8][Q];
   __shared__ uint8_t ghead[NG];
-  __shared__ unsigned last_sh, nnz_sh;
   const uint32_t t0 = blockIdx.x * T;
   const uint32_t rows = min((uint32_t)T, n - t0);
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    last_sh = 0;
-    nnz_sh = 0;
   }
   __syncthreads();
   const uint32_t seg_bytes = (rows / 4) * 16;  // whole 16-byte chunks of segment ids
@@ -996,11 +993,19 @@ __global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
       }
     }
   }
+  // stats: one atomic per warp (no CTA-wide reduction barrier)
+  if (stats) {
+    for (int off = 16; off > 0; off >>= 1) my_nz += __shfl_down_sync(0xffffffffu, my_nz, off);
+    if ((tid & 31) == 0 && my_nz) atomicAdd(&stats[1], (unsigned long long)my_nz);
+  }
   if (span1 || span2) {
+    // partials visible device-wide, then warp 0 alone counts the arrivals and
+    // (if it completed a key) combines; the other warps are done
     if (wrote) __threadfence();
     __syncthreads();
+    if (w != 0) return;
+    unsigned lst = 0;
     if (tid == 0) {
-      unsigned lst = 0;
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         if (!(k == 0 ? span1 : span2)) continue;
@@ -1009,33 +1014,26 @@ __global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
         const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
         if (atomicAdd(arrivals + ft, 1u) == nt - 1) lst |= 1u << k;
       }
-      last_sh = lst;
     }
-    __syncthreads();
-    const unsigned lst = last_sh;
-    if (lst && w == 0) {
-      __threadfence();
+    lst = __shfl_sync(0xffffffffu, lst, 0);
+    if (!lst) return;
+    __threadfence();
+    unsigned n_comb = 0;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        if (!((lst >> k) & 1u)) continue;
-        const uint32_t key = k == 0 ? tile_first : tile_last;
-        const uint32_t a = k == 0 ? fa : la, b = k == 0 ? fb : lb;
-        const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
-        const int32_t slot = slots_s[key];
-        const bool nz = span_combine<Q>(parts, ft, nt, a != ft * T, (int)(tid / Q), c,
-                                        values + (size_t)slot * row_stride, opt, lr, eps);
-        if (__ballot_sync(0xffffffffu, nz) != 0 && tid == 0) {
-          if (dirty) dirty[slot] = 1;
-          ++my_nz;
-        }
+    for (int k = 0; k < 2; ++k) {
+      if (!((lst >> k) & 1u)) continue;
+      const uint32_t key = k == 0 ? tile_first : tile_last;
+      const uint32_t a = k == 0 ? fa : la, b = k == 0 ? fb : lb;
+      const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
+      const int32_t slot = tslot[key - tile_first];
+      const bool nz = span_combine<Q>(parts, ft, nt, a != ft * T, (int)(tid / Q), c,
+                                      values + (size_t)slot * row_stride, opt, lr, eps);
+      if (__ballot_sync(0xffffffffu, nz) != 0 && tid == 0) {
+        if (dirty) dirty[slot] = 1;
+        ++n_comb;
       }
     }
-  }
-  if (stats) {
-    for (int off = 16; off > 0; off >>= 1) my_nz += __shfl_down_sync(0xffffffffu, my_nz, off);
-    if ((tid & 31) == 0 && my_nz) atomicAdd(&nnz_sh, my_nz);
-    __syncthreads();
-    if (tid == 0 && nnz_sh) atomicAdd(&stats[1], (unsigned long long)nnz_sh);
+    if (stats && tid == 0 && n_comb) atomicAdd(&stats[1], (unsigned long long)n_comb);
   }
 }
 
