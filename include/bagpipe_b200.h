@@ -402,6 +402,11 @@ int bp_engine_fetch(bp_engine* engine, int32_t slot);
  * host threads gathering/scattering rows in pinned staging (0: auto),
  * 2 = zero-copy prefetch, copy-engine write-back + host scatter. */
 int bp_engine_set_link_mode(bp_engine* engine, int32_t mode, int32_t threads);
+/* Link gate (DLRM mode): each prefetch waits for the latest EmbeddingBag
+ * forward enqueued before it, so its host-link reads overlap the dense step
+ * rather than the embedding kernels (deadlock-free: everything waiting on a
+ * fetch is enqueued after it). */
+int bp_engine_set_link_gate(bp_engine* engine, int32_t on);
 /* Enable the store's write-back log (mode 0 flushes append to it by DMA). */
 int bp_engine_set_write_log(bp_engine* engine, int64_t log_rows);
 /* Host worker-pool row gather (op 0) / scatter (op 1) rate probe (tools). */

@@ -153,6 +153,7 @@ _SIGS = {
     "bp_store_compact": (c_i32, [c_vp, c_vp]),
     "bp_store_log_rows": (c_i64, [c_vp]),
     "bp_engine_set_write_log": (c_i32, [c_vp, c_i64]),
+    "bp_engine_set_link_gate": (c_i32, [c_vp, c_i32]),
     "bp_store_write": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bp_store_write_masked": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bp_init_values": (c_i32, [c_u64, c_i32, c_vp, c_i64, c_vp, c_vp]),

@@ -331,6 +331,11 @@ struct bp_engine {
   size_t l2_flush_bytes = 0;
   int l2_flush_exclusive = 0;
   cudaEvent_t flush_ev = nullptr;
+  // link gate (DLRM mode): prefetches wait for the latest EmbeddingBag
+  // forward, so their zero-copy reads run under the dense step instead of
+  // beside the embedding kernels
+  bool link_gate = false;
+  cudaEvent_t gate_ev = nullptr;
   // DMA host-link mode
   int link_mode = 0;  // 0: zero-copy kernels, 1: copy engines + host pool
   bp::LinkWorker* worker = nullptr;
@@ -495,6 +500,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   delete e->worker;
   delete e->upload_worker;
   if (e->flush_ev) cudaEventDestroy(e->flush_ev);
+  if (e->gate_ev) cudaEventDestroy(e->gate_ev);
   cudaFreeHost(e->h_fetch_ids);
   cudaFreeHost(e->h_fetch_rows);
   cudaFreeHost(e->h_flush_ids);
@@ -788,14 +794,10 @@ extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threa
   }
   if (!e->worker || e->worker->pool.size() != threads) {
     delete e->worker;
-  delete e->upload_worker;
-  if (e->flush_ev) cudaEventDestroy(e->flush_ev);
     e->worker = new bp::LinkWorker(threads);
     const cudaError_t err = e->worker->init();
     if (err != cudaSuccess) {
       delete e->worker;
-  delete e->upload_worker;
-  if (e->flush_ev) cudaEventDestroy(e->flush_ev);
       e->worker = nullptr;
       e->link_mode = 0;
       BP_CUDA_TRY(err);
@@ -819,9 +821,18 @@ extern "C" int bp_engine_set_write_log(bp_engine* e, int64_t log_rows) {
   return bp_store_enable_log(e->store, log_rows, e->link);
 }
 
+extern "C" int bp_engine_set_link_gate(bp_engine* e, int32_t on) {
+  if (on && !e->gate_ev) BP_CUDA_TRY(cudaEventCreateWithFlags(&e->gate_ev, cudaEventDisableTiming));
+  e->link_gate = on != 0;
+  return BP_OK;
+}
+
 extern "C" int bp_engine_fetch(bp_engine* e, int32_t slot) {
   bp::PlanSlot& ps = e->plans[slot];
   BP_CUDA_TRY(cudaStreamWaitEvent(e->link, ps.popped, 0));
+  // the waited-for forward was enqueued before this fetch and everything
+  // that waits on the fetch (the plan's apply) is enqueued after it: no cycle
+  if (e->link_gate) BP_CUDA_TRY(cudaStreamWaitEvent(e->link, e->gate_ev, 0));
   bp::stage_begin(e, bp::kStageFetch, e->link);
   if (e->link_mode == 1) {
     // prefetch count on the host (the pop finished long before dispatch)
@@ -1094,6 +1105,7 @@ extern "C" int bp_engine_dlrm_forward(bp_engine* e, int64_t pos, int32_t plan_sl
   rc = bp_embbag_forward(P, cv.d_values, e->cfg.dim, e->slots_s, model_dim, nullptr, P->n_occ, 0, nullptr, d_pooled,
                          e->compute);
   stage_end(e, kStageTrainer, e->compute);
+  if (!rc && e->link_gate) BP_CUDA_TRY(cudaEventRecord(e->gate_ev, e->compute));
   return rc;
 }
 

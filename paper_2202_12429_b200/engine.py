@@ -231,6 +231,10 @@ class _Pipeline:
         # write-back log rows (log-structured host store; 0 = zero-copy scatter into the table)
         log_rows = int(os.environ.get("BAGPIPE_B200_LOG_ROWS", str(min(self.row_schema.total_rows, 1 << 24))))
         L.check(self.lib.bp_engine_set_write_log(h, log_rows), "bp_engine_set_write_log")
+        # DLRM option: prefetches run under the dense step, not beside the EmbeddingBag
+        # kernels (measured no faster on the bench step, so off by default)
+        gate = trainer is not None and self._split and os.environ.get("BAGPIPE_B200_LINK_GATE", "0") == "1"
+        L.check(self.lib.bp_engine_set_link_gate(h, int(gate)), "bp_engine_set_link_gate")
         self.stream = torch.cuda.ExternalStream(parts.compute_stream)
         self.link = torch.cuda.ExternalStream(parts.link_stream)
         self.store = ShardedStore(self.row_schema, cfg.num_shards, cfg.seed, _handle=parts.store, _owner=self)
