@@ -18,6 +18,7 @@ namespace bp {
 
 struct CacheCounters {
   long long occupancy, free_top, insertions, evictions, peak_occupancy, abort;
+  unsigned int ticket;  // k_insert: blocks finished (the last one commits the counters)
 };
 
 }  // namespace bp
@@ -59,57 +60,60 @@ __global__ void k_free_init(uint32_t* free_list, long long cap) {
     free_list[i] = (uint32_t)(cap - 1 - i);  // pops (from the top) yield 0, 1, 2, ...
 }
 
-__global__ void k_insert_check(CacheCounters* ctr, long long n, const long long* d_n, long long capacity,
-                               ErrorRecord* err, long long iteration) {
-  n = load_count(n, d_n);
-  if (ctr->occupancy + n > capacity) {
-    raise_error(err, BP_ERR_CACHE_CAPACITY, iteration, 0, 0);
-    ctr->abort = 1;
-  } else {
-    ctr->abort = 0;
-  }
-}
-
+// One launch: every block checks the capacity against the counters as they
+// were at launch (nothing changes them until the last block), inserts its
+// share, and the last block to finish commits free_top / occupancy /
+// insertions / peak -- all blocks have read the counters by then.
 __global__ void k_insert(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ids,
                          const float* __restrict__ rows, const int64_t* __restrict__ ttls, long long n,
-                         const long long* d_n, int dim, const CacheCounters* __restrict__ ctr,
+                         const long long* d_n, int dim, CacheCounters* __restrict__ ctr, long long capacity,
                          int32_t* __restrict__ slot_of, uint64_t* __restrict__ slot_key,
                          uint32_t* __restrict__ slot_id, long long* __restrict__ ttl, uint8_t* __restrict__ dirty,
                          uint8_t* __restrict__ used, float* __restrict__ values, const uint32_t* __restrict__ free_list,
                          ErrorRecord* err, long long iteration) {
   n = load_count(n, d_n);
-  if (ctr->abort) return;
-  const long long top = ctr->free_top;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const uint32_t id = ids[i];
-    if (id == kNoId || slot_of[id] >= 0) {
-      raise_error(err, BP_ERR_CACHE_ORDERING, iteration, i, keys[i]);
-      continue;
-    }
-    const uint32_t slot = free_list[top - 1 - i];
-    slot_of[id] = (int32_t)slot;
-    slot_key[slot] = keys[i];
-    slot_id[slot] = id;
-    ttl[slot] = ttls[i];
-    dirty[slot] = 0;
-    used[slot] = 1;
-    if ((dim & 3) == 0) {
-      const float4* src = reinterpret_cast<const float4*>(rows + i * dim);
-      float4* dst = reinterpret_cast<float4*>(values + (long long)slot * dim);
-      for (int d = 0; d < (dim >> 2); ++d) dst[d] = src[d];
-    } else {
-      for (int d = 0; d < dim; ++d) values[(long long)slot * dim + d] = rows[i * dim + d];
+  const long long occ = ctr->occupancy, top = ctr->free_top;
+  const bool abort = occ + n > capacity;
+  if (abort) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(err, BP_ERR_CACHE_CAPACITY, iteration, 0, 0);
+  } else {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+      const uint32_t id = ids[i];
+      if (id == kNoId || slot_of[id] >= 0) {
+        raise_error(err, BP_ERR_CACHE_ORDERING, iteration, i, keys[i]);
+        continue;
+      }
+      const uint32_t slot = free_list[top - 1 - i];
+      slot_of[id] = (int32_t)slot;
+      slot_key[slot] = keys[i];
+      slot_id[slot] = id;
+      ttl[slot] = ttls[i];
+      dirty[slot] = 0;
+      used[slot] = 1;
+      if ((dim & 3) == 0) {
+        const float4* src = reinterpret_cast<const float4*>(rows + i * dim);
+        float4* dst = reinterpret_cast<float4*>(values + (long long)slot * dim);
+        for (int d = 0; d < (dim >> 2); ++d) dst[d] = src[d];
+      } else {
+        for (int d = 0; d < dim; ++d) values[(long long)slot * dim + d] = rows[i * dim + d];
+      }
     }
   }
-}
-
-__global__ void k_insert_end(CacheCounters* ctr, long long n, const long long* d_n) {
-  if (ctr->abort) return;
-  n = load_count(n, d_n);
-  ctr->free_top -= n;
-  ctr->occupancy += n;
-  ctr->insertions += n;
-  if (ctr->occupancy > ctr->peak_occupancy) ctr->peak_occupancy = ctr->occupancy;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ctr->ticket, 1u) == gridDim.x - 1) {
+      ctr->abort = abort ? 1 : 0;
+      if (!abort) {
+        ctr->free_top = top - n;
+        ctr->occupancy = occ + n;
+        ctr->insertions += n;
+        if (occ + n > ctr->peak_occupancy) ctr->peak_occupancy = occ + n;
+      }
+      ctr->ticket = 0;
+    }
+  }
 }
 
 __global__ void k_set_ttl(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ids,
@@ -478,11 +482,9 @@ extern "C" int bp_cache_insert(bp_cache* c, const uint64_t* d_keys, const uint32
   int rc = cache_ids(c, d_keys, d_ids, n, (const long long*)d_n, 1, &ids, s);
   if (rc) return rc;
   ErrorRecord* err = c->ctx ? c->ctx->d_err : nullptr;
-  k_insert_check<<<1, 1, 0, s>>>(c->d_ctr, n, (const long long*)d_n, c->capacity, err, iteration);
   k_insert<<<grid_for(n, 256), 256, 0, s>>>(d_keys, ids, d_rows, d_ttls, n, (const long long*)d_n, c->dim, c->d_ctr,
-                                            c->d_slot_of, c->d_slot_key, c->d_slot_id, c->d_ttl, c->d_dirty,
-                                            c->d_used, c->d_values, c->d_free, err, iteration);
-  k_insert_end<<<1, 1, 0, s>>>(c->d_ctr, n, (const long long*)d_n);
+                                            c->capacity, c->d_slot_of, c->d_slot_key, c->d_slot_id, c->d_ttl,
+                                            c->d_dirty, c->d_used, c->d_values, c->d_free, err, iteration);
   BP_LAUNCH_CHECK();
   return BP_OK;
 }

@@ -335,6 +335,7 @@ struct bp_engine {
   // forward, so their zero-copy reads run under the dense step instead of
   // beside the embedding kernels
   bool link_gate = false;
+  bool side_gate = false;  // the same for batch preps and planner passes
   cudaEvent_t gate_ev = nullptr;
   // DMA host-link mode
   int link_mode = 0;  // 0: zero-copy kernels, 1: copy engines + host pool
@@ -645,6 +646,7 @@ static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64
     d_keys = e->d_keys_staging[si];
     d_labels = e->d_labels_staging[si];
   }
+  if (e->side_gate) BP_CUDA_TRY(cudaStreamWaitEvent(q, e->gate_ev, 0));
   int rc;
   if (n_cols > 0) {
     if (n_cols > e->sc->num_tables) return BP_ERR_INVALID;
@@ -712,6 +714,7 @@ extern "C" int bp_engine_refill(bp_engine* e, int64_t pos) {
   bp_prep* P = e->preps[pslot];
   if (!P) return BP_ERR_ENGINE;
   BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, e->prep_ready[pslot], 0));
+  if (e->side_gate) BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, e->gate_ev, 0));
   bp::stage_begin(e, bp::kStagePlanner, e->planq);
   const int rc = bp_planner_refill(e->planner, P, e->planq);
   bp::stage_end(e, bp::kStagePlanner, e->planq);
@@ -821,9 +824,13 @@ extern "C" int bp_engine_set_write_log(bp_engine* e, int64_t log_rows) {
   return bp_store_enable_log(e->store, log_rows, e->link);
 }
 
+// bit 0: prefetches, bit 1: batch preps and planner passes wait for the
+// latest EmbeddingBag forward (deadlock-free: the awaited forward is always
+// enqueued before, everything waiting on the gated work after it)
 extern "C" int bp_engine_set_link_gate(bp_engine* e, int32_t on) {
   if (on && !e->gate_ev) BP_CUDA_TRY(cudaEventCreateWithFlags(&e->gate_ev, cudaEventDisableTiming));
-  e->link_gate = on != 0;
+  e->link_gate = (on & 1) != 0;
+  e->side_gate = (on & 2) != 0;
   return BP_OK;
 }
 
@@ -1105,7 +1112,7 @@ extern "C" int bp_engine_dlrm_forward(bp_engine* e, int64_t pos, int32_t plan_sl
   rc = bp_embbag_forward(P, cv.d_values, e->cfg.dim, e->slots_s, model_dim, nullptr, P->n_occ, 0, nullptr, d_pooled,
                          e->compute);
   stage_end(e, kStageTrainer, e->compute);
-  if (!rc && e->link_gate) BP_CUDA_TRY(cudaEventRecord(e->gate_ev, e->compute));
+  if (!rc && (e->link_gate || e->side_gate)) BP_CUDA_TRY(cudaEventRecord(e->gate_ev, e->compute));
   return rc;
 }
 

@@ -233,8 +233,8 @@ class _Pipeline:
         L.check(self.lib.bp_engine_set_write_log(h, log_rows), "bp_engine_set_write_log")
         # DLRM option: prefetches run under the dense step, not beside the EmbeddingBag
         # kernels (measured no faster on the bench step, so off by default)
-        gate = trainer is not None and self._split and os.environ.get("BAGPIPE_B200_LINK_GATE", "0") == "1"
-        L.check(self.lib.bp_engine_set_link_gate(h, int(gate)), "bp_engine_set_link_gate")
+        gate = int(os.environ.get("BAGPIPE_B200_LINK_GATE", "0")) if trainer is not None and self._split else 0
+        L.check(self.lib.bp_engine_set_link_gate(h, gate), "bp_engine_set_link_gate")
         self.stream = torch.cuda.ExternalStream(parts.compute_stream)
         self.link = torch.cuda.ExternalStream(parts.link_stream)
         self.store = ShardedStore(self.row_schema, cfg.num_shards, cfg.seed, _handle=parts.store, _owner=self)
@@ -276,7 +276,10 @@ class _Pipeline:
         # (measured: it helps device-resident batches, 0.41 -> 0.37 ms/step,
         # and slows host batches, whose uploads then contend with the
         # training thread -- so by default only with device inputs)
-        default_threaded = bool(self.device_inputs)
+        # batches in pinned memory are DMA'd straight from there (no upload
+        # copy on a host thread), so they take the planner thread as well
+        default_threaded = bool(self.device_inputs) or (
+            bool(batches) and all("pinned" in getattr(b, "_memo", {}) for b in batches))
         env = os.environ.get("BAGPIPE_B200_PLANNER_THREAD")
         if env is not None:
             default_threaded = env == "1"
