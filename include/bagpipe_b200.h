@@ -489,6 +489,13 @@ int bp_prep_occ_rank(bp_prep* prep, uint32_t* d_out, bp_stream_t stream);
 int bp_embbag_backward_sorted(bp_prep* prep, const float* d_grad_sorted, float* d_values, int32_t row_stride,
                               const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt, float lr,
                               float eps, int64_t* d_stats, bp_stream_t stream);
+/* The same with a caller-owned scratch of bp_embbag_bwd_scratch_bytes(n_occ,
+ * dim) bytes, zeroed once (kept zero between calls): no per-call allocation. */
+int64_t bp_embbag_bwd_scratch_bytes(int64_t n_occ, int32_t dim);
+int bp_embbag_backward_sorted_scratch(bp_prep* prep, const float* d_grad_sorted, float* d_values, int32_t row_stride,
+                                      const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt, float lr,
+                                      float eps, int64_t* d_stats, void* d_scratch, int64_t scratch_bytes,
+                                      bp_stream_t stream);
 
 /* ---------------------------------------------------------- peer exchange */
 /* DLRM hybrid parallelism over NVLink peer memory (csrc/peer.cu).  Rank

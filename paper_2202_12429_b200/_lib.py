@@ -225,6 +225,9 @@ _SIGS = {
                                    c_vp, c_vp]),
     "bp_prep_occ_sorted_index": (c_i32, [c_vp, c_vp, c_vp]),
     "bp_prep_occ_rank": (c_i32, [c_vp, c_vp, c_vp]),
+    "bp_embbag_bwd_scratch_bytes": (c_i64, [c_i64, c_i32]),
+    "bp_embbag_backward_sorted_scratch": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32, c_f32,
+                                                  c_vp, c_vp, c_i64, c_vp]),
     "bp_debug_bwd_variant": (c_i32, [c_i32]),
     "bp_embbag_backward_sorted": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32, c_f32, c_vp,
                                           c_vp]),

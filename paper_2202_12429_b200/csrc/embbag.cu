@@ -1012,7 +1012,10 @@ __global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
         if (tslot[k == 0 ? 0 : nu - 1] < 0) continue;
         const uint32_t a = k == 0 ? fa : la, b = k == 0 ? fb : lb;
         const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
-        if (atomicAdd(arrivals + ft, 1u) == nt - 1) lst |= 1u << k;
+        if (atomicAdd(arrivals + ft, 1u) == nt - 1) {
+          lst |= 1u << k;
+          arrivals[ft] = 0;  // every arrival is in: the counter is free again (persistent scratch)
+        }
       }
     }
     lst = __shfl_sync(0xffffffffu, lst, 0);
@@ -1338,9 +1341,42 @@ static int launch_bwd_sorted(bp_prep* P, const float* d_grad_sorted, float* d_va
   return BP_OK;
 }
 
+// Scratch of the staged backward for n_occ occurrences: tile partials, then
+// the arrival counters (zero between calls: the last arriver resets them).
+extern "C" int64_t bp_embbag_bwd_scratch_bytes(int64_t n_occ, int32_t dim) {
+  if (dim < 4 || (dim & 3) != 0) return 0;
+  const int q = dim / 4, T = bp::kStagedF4 / q;
+  const long long tiles = (n_occ + T - 1) / T;
+  return (((long long)tiles * 2 * q * 16 + 255) & ~255ll) + tiles * 4 + 256;
+}
+
+static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, float* d_values, int32_t row_stride,
+                                       const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt,
+                                       float lr, float eps, int64_t* d_stats, bp_stream_t stream, char* own_scratch,
+                                       size_t own_bytes);
+
 extern "C" int bp_embbag_backward_sorted(bp_prep* P, const float* d_grad_sorted, float* d_values, int32_t row_stride,
                                          const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt,
                                          float lr, float eps, int64_t* d_stats, bp_stream_t stream) {
+  return embbag_backward_sorted_impl(P, d_grad_sorted, d_values, row_stride, d_slots_s, d_dirty, dim, opt, lr, eps,
+                                     d_stats, stream, nullptr, 0);
+}
+
+// With a caller-owned scratch (bp_embbag_bwd_scratch_bytes, zeroed once):
+// no per-call stream-ordered allocation (whose reuse of memory freed on
+// another stream can make this stream wait for that one) and no memset.
+extern "C" int bp_embbag_backward_sorted_scratch(bp_prep* P, const float* d_grad_sorted, float* d_values,
+                                                 int32_t row_stride, const int32_t* d_slots_s, uint8_t* d_dirty,
+                                                 int32_t dim, int32_t opt, float lr, float eps, int64_t* d_stats,
+                                                 void* d_scratch, int64_t scratch_bytes, bp_stream_t stream) {
+  return embbag_backward_sorted_impl(P, d_grad_sorted, d_values, row_stride, d_slots_s, d_dirty, dim, opt, lr, eps,
+                                     d_stats, stream, static_cast<char*>(d_scratch), (size_t)scratch_bytes);
+}
+
+static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, float* d_values, int32_t row_stride,
+                                       const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim, int32_t opt,
+                                       float lr, float eps, int64_t* d_stats, bp_stream_t stream, char* own_scratch,
+                                       size_t own_bytes) {
   using namespace bp;
   if (!P->d_seg_of || (dim & 3) != 0 || (row_stride & 3) != 0 || dim > 32 || (32 % dim) != 0) return BP_ERR_INVALID;
   if (opt == BP_OPT_ADAGRAD && row_stride < 2 * dim) return BP_ERR_INVALID;
@@ -1351,11 +1387,12 @@ extern "C" int bp_embbag_backward_sorted(bp_prep* P, const float* d_grad_sorted,
       const int q = dim / 4, T = kStagedF4 / q;
       const unsigned tiles = (unsigned)((P->n_occ + T - 1) / T);
       const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
-      char* scratch = nullptr;
-      BP_CUDA_TRY(pool_alloc(&scratch, parts_bytes + tiles * sizeof(unsigned int) + 256, s));
+      const bool own = own_scratch && own_bytes >= (size_t)bp_embbag_bwd_scratch_bytes(P->n_occ, dim);
+      char* scratch = own ? own_scratch : nullptr;
+      if (!own) BP_CUDA_TRY(pool_alloc(&scratch, parts_bytes + tiles * sizeof(unsigned int) + 256, s));
       float4* parts = reinterpret_cast<float4*>(scratch);
       unsigned int* arrivals = reinterpret_cast<unsigned int*>(scratch + parts_bytes);
-      BP_CUDA_TRY(cudaMemsetAsync(arrivals, 0, tiles * sizeof(unsigned int), s));
+      if (!own) BP_CUDA_TRY(cudaMemsetAsync(arrivals, 0, tiles * sizeof(unsigned int), s));
       const size_t smem = (size_t)T * q * sizeof(float4) + 2 * (size_t)T * sizeof(uint32_t);
 #define BP_BWD_STAGED(QQ)                                                                                      \
   {                                                                                                            \
@@ -1378,7 +1415,7 @@ extern "C" int bp_embbag_backward_sorted(bp_prep* P, const float* d_grad_sorted,
       }
 #undef BP_BWD_STAGED
       BP_LAUNCH_CHECK();
-      cudaFreeAsync(scratch, s);
+      if (!own) cudaFreeAsync(scratch, s);
       return BP_OK;
     }
     case 1: return launch_bwd_sorted<8, 3>(P, d_grad_sorted, d_values, row_stride, d_slots_s, d_dirty, dim, opt, lr,

@@ -334,6 +334,9 @@ struct bp_engine {
   // link gate (DLRM mode): prefetches wait for the latest EmbeddingBag
   // forward, so their zero-copy reads run under the dense step instead of
   // beside the embedding kernels
+  // persistent scratch of the sorted EmbeddingBag backward (zeroed once)
+  void* bwd_scratch = nullptr;
+  size_t bwd_scratch_bytes = 0;
   bool link_gate = false;
   bool side_gate = false;  // the same for batch preps and planner passes
   cudaEvent_t gate_ev = nullptr;
@@ -502,6 +505,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   delete e->upload_worker;
   if (e->flush_ev) cudaEventDestroy(e->flush_ev);
   if (e->gate_ev) cudaEventDestroy(e->gate_ev);
+  if (e->bwd_scratch) cudaFree(e->bwd_scratch);
   cudaFreeHost(e->h_fetch_ids);
   cudaFreeHost(e->h_fetch_rows);
   cudaFreeHost(e->h_flush_ids);
@@ -1180,8 +1184,21 @@ extern "C" int bp_engine_dlrm_backward_begin(bp_engine* e, int64_t pos, int32_t 
   bp_cache_view cv;
   bp_cache_get_view(e->cache, &cv);
   stage_begin(e, kStageTrainer, e->compute);
-  int rc = grad_sorted ? bp_embbag_backward_sorted(P, d_grad, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty,
-                                                   model_dim, opt, lr, eps, e->stats, e->compute)
+  if (grad_sorted) {
+    const size_t need = (size_t)bp_embbag_bwd_scratch_bytes(P->n_occ, model_dim);
+    if (need > e->bwd_scratch_bytes) {
+      BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
+      if (e->bwd_scratch) BP_CUDA_TRY(cudaFree(e->bwd_scratch));
+      e->bwd_scratch = nullptr;
+      e->bwd_scratch_bytes = 0;
+      BP_CUDA_TRY(cudaMalloc(&e->bwd_scratch, need));
+      BP_CUDA_TRY(cudaMemset(e->bwd_scratch, 0, need));
+      e->bwd_scratch_bytes = need;
+    }
+  }
+  int rc = grad_sorted ? bp_embbag_backward_sorted_scratch(P, d_grad, cv.d_values, e->cfg.dim, e->slots_s,
+                                                           cv.d_dirty, model_dim, opt, lr, eps, e->stats,
+                                                           e->bwd_scratch, (int64_t)e->bwd_scratch_bytes, e->compute)
                        : bp_embbag_backward(P, d_grad, nullptr, nullptr, cv.d_values, e->cfg.dim, e->slots_s,
                                             cv.d_dirty, model_dim, opt, lr, eps, e->stats, e->compute);
   stage_end(e, kStageTrainer, e->compute);

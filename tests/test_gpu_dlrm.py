@@ -315,6 +315,18 @@ def test_sorted_gradient_backward(dim, opt_name, variant):
                                           L.stream_ptr()), "bwd sorted 2")
     L.check(lib.bp_debug_bwd_variant(0), "variant")
     assert torch.equal(d_arena, d_arena2)
+    if variant == 0:
+        # persistent caller scratch: counters left at zero by each call, so
+        # repeated calls on the same scratch give the same bits
+        nb = lib.bp_embbag_bwd_scratch_bytes(n, dim)
+        scratch = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        for _ in range(2):
+            d_arena3 = torch.from_numpy(arena).cuda()
+            L.check(lib.bp_embbag_backward_sorted_scratch(prep.handle, L.ptr(d_g), L.ptr(d_arena3), 2 * dim,
+                                                          L.ptr(slots), None, dim, opt, float(np.float32(lr)),
+                                                          float(np.float32(eps)), None, L.ptr(scratch), nb,
+                                                          L.stream_ptr()), "bwd sorted scratch")
+            assert torch.equal(d_arena, d_arena3)
 
 
 def test_interaction_backward_rows_is_a_permuted_store():
