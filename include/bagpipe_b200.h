@@ -582,6 +582,8 @@ int bp_dlrm_master_sgd(const bp_sgd_tensors* tensors, float lr, bp_stream_t stre
 int bp_debug_long_trace(void* d_buf);
 /* Debug: launch shape of bp_embbag_backward_sorted (0 default; tools/kernel_bench.py). */
 int bp_debug_bwd_variant(int32_t variant);
+/* Debug: EmbeddingBag single-key forward shape (0 occurrence-order gather, 1 key-sorted scatter). */
+int bp_debug_fwd_variant(int32_t variant);
 /* Debug: bit 0 turns the store's fetch kernels, bit 1 its write kernels into
  * no-ops (results become wrong; only for measuring the host link's share). */
 int bp_debug_skip_link(int32_t skip);

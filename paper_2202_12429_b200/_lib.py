@@ -229,6 +229,7 @@ _SIGS = {
     "bp_embbag_backward_sorted_scratch": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32, c_f32,
                                                   c_vp, c_vp, c_i64, c_vp]),
     "bp_debug_bwd_variant": (c_i32, [c_i32]),
+    "bp_debug_fwd_variant": (c_i32, [c_i32]),
     "bp_embbag_backward_sorted": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32, c_f32, c_vp,
                                           c_vp]),
     "bp_dlrm_interact_backward_rows": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp,
@@ -291,6 +292,9 @@ def lib() -> C.CDLL:
                 sf = os.environ.get("BAGPIPE_B200_STUB_FORK")  # tuning knob: long trainer kernel beside the short
                 if sf:
                     check(lb.bp_set_stub_fork(int(sf)), "bp_set_stub_fork")
+                fv = os.environ.get("BAGPIPE_B200_FWD_VARIANT")  # tuning knob: EmbeddingBag forward shape
+                if fv:
+                    check(lb.bp_debug_fwd_variant(int(fv)), "bp_debug_fwd_variant")
                 bv = os.environ.get("BAGPIPE_B200_BWD_VARIANT")  # tuning knob: sorted backward launch shape
                 if bv:
                     check(lb.bp_debug_bwd_variant(int(bv)), "bp_debug_bwd_variant")

@@ -65,6 +65,54 @@ __global__ void __launch_bounds__(256) k_embbag_fwd_rows_v4(const uint32_t* __re
   }
 }
 
+// Same output from the key-sorted side: one float4 lane per (sorted position
+// j, 4 components); segment id and slot loads are coalesced (consecutive j
+// share a key, so its row is read once into L1 and broadcast), and the row
+// is stored to its occurrence position occ_pos[j] -- 64-byte scattered
+// stores, which never stall the thread, instead of a random 4-byte slot
+// gather per occurrence.
+__global__ void __launch_bounds__(256) k_embbag_fwd_sorted_v4(const uint32_t* __restrict__ seg_of,
+                                                             const uint32_t* __restrict__ occ_pos,
+                                                             const int32_t* __restrict__ slots_s,
+                                                             const float4* __restrict__ values, int q, int row_q,
+                                                             long long n, float4* __restrict__ out) {
+  constexpr int U = 4;
+  const long long total = n * q;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += stride * U) {
+    uint32_t sg[U], pos[U];
+    int32_t sl[U];
+    float4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      const long long j = i / q;
+      sg[k] = i < total ? seg_of[j] : 0u;
+      pos[k] = i < total ? occ_pos[j] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) sl[k] = i0 + k * stride < total ? slots_s[sg[k]] : -1;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      const int c = (int)(i - (i / q) * q);
+      v[k] = sl[k] >= 0 ? values[(long long)sl[k] * row_q + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      if (i < total) out[(long long)pos[k] * q + (i - (i / q) * q)] = v[k];
+    }
+  }
+}
+
+static int g_fwd_variant = 0;  // debug: 0 = occurrence-order gather, 1 = key-sorted scatter
+
+extern "C" int bp_debug_fwd_variant(int32_t v) {
+  g_fwd_variant = v;
+  return BP_OK;
+}
+
 // Gradient / row source in a peer example owner's [bl][t_global][Q] buffer
 // (csrc/peer.cu); rows == nullptr: local gradient rows.
 struct PeerSrc {
@@ -1199,7 +1247,13 @@ extern "C" int bp_embbag_forward(bp_prep* P, const float* d_values, int32_t row_
   cudaStream_t s = (cudaStream_t)stream;
   if (!d_occ_s) d_occ_s = P->d_occ_s;
   if (!d_occ_s) return BP_ERR_INVALID;
-  if (!d_bag_offsets && (dim & 3) == 0 && (row_stride & 3) == 0) {
+  if (!d_bag_offsets && (dim & 3) == 0 && (row_stride & 3) == 0 && g_fwd_variant == 1 && P->d_seg_of &&
+      d_occ_s == P->d_occ_s) {
+    const int q = dim / 4;
+    k_embbag_fwd_sorted_v4<<<grid_for(P->n_occ * q, 256 * 4, kNumSMs * 8), 256, 0, s>>>(
+        P->d_seg_of, P->d_occ_pos, d_slots_s, reinterpret_cast<const float4*>(d_values), q, row_stride / 4,
+        P->n_occ, reinterpret_cast<float4*>(d_out));
+  } else if (!d_bag_offsets && (dim & 3) == 0 && (row_stride & 3) == 0) {
     const int q = dim / 4;
     k_embbag_fwd_rows_v4<<<grid_for(P->n_occ * q, 256 * 4, kNumSMs * 8), 256, 0, s>>>(
         d_occ_s, d_slots_s, reinterpret_cast<const float4*>(d_values), q, row_stride / 4, P->n_occ,

@@ -135,6 +135,12 @@ def main():
         out[f"embbag_bwd_sorted_v{var}_warm_us"] = timed_warm(bwd_sorted, args.reps)
     lib.bp_debug_bwd_variant(0)
     out["embbag_fwd_us"] = timed(fwd, args.reps, flush)
+    lib.bp_debug_fwd_variant(1)
+    out["embbag_fwd_sorted_us"] = timed(fwd, args.reps, flush)
+    ref = pooled.clone()
+    lib.bp_debug_fwd_variant(0)
+    fwd()
+    out["embbag_fwd_variants_equal"] = bool(torch.equal(ref, pooled))
     out["embbag_bwd_us"] = timed(bwd, args.reps, flush)
     out["embbag_bwd_sorted_us"] = timed(bwd_sorted, args.reps, flush)
     for var in (1, 2, 3):  # other launch shapes of the sorted kernel
@@ -162,7 +168,12 @@ def main():
             lib.bp_debug_bwd_variant(0)
         return run
 
-    for fn in (stub, fwd, bwd, bwd_sorted, variant(1), variant(2), variant(3)):
+    def fwd_sorted():
+        lib.bp_debug_fwd_variant(1)
+        fwd()
+        lib.bp_debug_fwd_variant(0)
+
+    for fn in (stub, fwd, fwd_sorted, bwd, bwd_sorted, variant(1), variant(2), variant(3)):
         flush.zero_()
         torch.cuda.synchronize()
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
