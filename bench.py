@@ -6,21 +6,23 @@ the public Kaggle cardinalities (33,762,577 rows), emb dim 16 fp32, batch
 16,384, Zipf 1.05 synthetic IDs (reference generator stream), HBM cache = 1%
 of rows (337,625 entries), lookahead auto (-> 7), host-pinned embedding
 table.  One step = one engine iteration over one batch: plan emission
-(GPU dedupe + Algorithm 1), zero-copy prefetch from the pinned store, cache
-insert + TTL + lookup, fused stub backward + rank-ordered combine + SGD,
-eviction, batched dirty write-back -- the reference's run_pipeline
+(GPU dedupe + Algorithm 1), prefetch from the pinned store (written rows over
+the host link, never-written rows computed on the GPU), cache insert + TTL +
+lookup, fused stub backward + rank-ordered combine + SGD, eviction, batched
+dirty write-back (copy-engine log appends) -- the reference's run_pipeline
 iteration (engine.py:495-606), bit-exact with it.
 
 value: samples/s with every batch's keys already in HBM; e2e: the same steps
-through the public API with host batches (H2D of the batch entering the
-window and D2H of the step counters inside the timed region).  L2 is
-flushed (256 MiB write) between timed steps.  ``--impl reference`` times the
-CPU oracle port of the reference (oracle/, reference unavailable on the box)
-on the host cores.  N>1 (weak scaling, fixed 16,384 examples per GPU): the
-global batch is N x 16,384 and its 26 tables are sharded table-wise over the
-ranks (each rank runs the whole pipeline for its tables of every example --
-the same occurrences per GPU as one GPU -- no data-path collective), timed
-as the max over ranks.
+through the public API with host batches in pinned memory (H2D DMA of the
+batch entering the window and D2H of the step counters inside the timed
+region).  L2 is flushed (256 MiB write on the compute stream) at the start of
+every timed iteration.  ``--impl reference`` times the CPU oracle port of the
+reference (oracle/, the reference itself is unavailable on the box) on the
+host cores.  N>1 (weak scaling, fixed 16,384 examples per GPU): the global
+batch is N x 16,384, the N GPUs are the reference's N trainers, and the 26
+tables are sharded table-wise over the ranks (each rank runs the whole
+pipeline for its tables of every example -- the same occurrences per GPU as
+one GPU -- no data-path collective), timed as the max over ranks.
 DLRM mode (N=1, reported under "dlrm" and in "roofline"): the same engine
 with EmbeddingBag fwd/bwd + SGD feeding PyTorch MLPs replayed as a CUDA graph.
 """
@@ -33,7 +35,6 @@ import json
 import numpy as np
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time

@@ -177,21 +177,29 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* z = ix_smem + warp * (32 * D + 32 * LG);
   float* G = z + 32 * D;
+  // (i, j) of every lower-triangle pair k, once per block (not a sqrt and
+  // two search loops per pair and sample)
+  const int P = n * (n - 1) / 2;
+  uint16_t* pij = reinterpret_cast<uint16_t*>(ix_smem + kIxWarps * (32 * D + 32 * LG));
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    int i = 1;
+    while ((i + 1) * i / 2 <= k) ++i;
+    const int j = k - i * (i - 1) / 2;  // i <= 31, j <= 30: i*LG + j < 2^11, j < 2^5
+    pij[k] = (uint16_t)((i * LG + j) | (j << 11));
+  }
+  __syncthreads();
   for (long long b = (long long)blockIdx.x * kIxWarps + warp; b < B; b += (long long)gridDim.x * kIxWarps) {
     const long long p = b * T + (lane - 1);  // this lane's embedding-gradient row (lanes 1..T)
     const long long drow = (gemb_rows && lane >= 1 && lane < n) ? (long long)gemb_rows[p] : p;
     for (int e = lane; e < n * D; e += 32)
       z[e] = e < D ? ld_any(x, b * D + e, x_bf16) : emb[b * T * D + (e - D)];
     const long long ob = b * out_stride;
-    const int P = n * (n - 1) / 2;
     if (lane < n) G[lane * LG + lane] = 0.f;
     for (int k = lane; k < P; k += 32) {
-      int i = (int)((1.f + sqrtf(1.f + 8.f * (float)k)) * 0.5f);
-      while (i * (i - 1) / 2 > k) --i;
-      while ((i + 1) * i / 2 <= k) ++i;
-      const int j = k - i * (i - 1) / 2;
+      const uint32_t e = pij[k];
+      const int ij = (int)(e & 0x7FFu), j = (int)(e >> 11), i = (ij - j) / LG;
       const float g = ld_any(gout, ob + D + k, g_bf16);
-      G[i * LG + j] = g;
+      G[ij] = g;
       G[j * LG + i] = g;
     }
     __syncwarp();
@@ -303,7 +311,7 @@ extern "C" int bp_dlrm_interact_backward_rows(const void* d_x, int32_t x_bf16, c
   if (B == 0) return BP_OK;
   const long long nblk = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * 16);
   if (T + 1 <= 32 && (D == 4 || D == 8 || D == 16 || D == 32)) {
-    const size_t sm = sizeof(float) * kIxWarps * (32 * D + 32 * 33);
+    const size_t sm = sizeof(float) * kIxWarps * (32 * D + 32 * 33) + sizeof(uint16_t) * 512;
 #define BP_IX_BWD(DD)                                                                                              \
   {                                                                                                                \
     BP_CUDA_TRY(cudaFuncSetAttribute(k_interact_bwd_reg<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
