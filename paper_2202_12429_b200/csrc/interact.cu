@@ -100,11 +100,28 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd(const void* __re
   }
 }
 
-// Fast path (n = T+1 <= 32, D in {4, 8, 16, 32}): lane i owns z_i in
-// registers and walks j < i (forward) or all j (backward) over shared-memory
-// rows read as float4 broadcasts (every lane reads the same z_j: no bank
-// conflicts); the output row is staged in shared memory and written
-// coalesced.  G rows use an odd stride (conflict-free column walks).
+// Fast path (n = T+1 <= 32, D in {4, 8, 16, 32}), a warp per sample.
+//   forward: lane i owns z_i in registers and walks j < i over shared-memory
+//   rows read as float4 broadcasts (every lane reads the same z_j: no bank
+//   conflicts); the output row is staged in shared memory and written
+//   coalesced.  (A balanced variant -- lanes taking pairs round-robin,
+//   both rows from shared memory -- measured slower, 37 vs 30 us: twice the
+//   shared-memory traffic and no broadcasts.)
+//   backward: the next sample's inputs are loaded into registers while the
+//   current one is computed (each warp walks ~4 samples); G (symmetric pair
+//   gradients, odd row stride, pairs k -> (i, j) from a per-block table) and
+//   z staged, lane i computes dz_i = sum_j G_ij z_j (z_j float4 broadcasts).
+constexpr int kIxBlocksPerSM = 4;
+
+__device__ __forceinline__ void build_pairs(uint16_t* pij, int P, int LG) {
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    int i = 1;
+    while ((i + 1) * i / 2 <= k) ++i;
+    const int j = k - i * (i - 1) / 2;  // i <= 31, j <= 30: i*LG + j < 2^11, j < 2^5
+    pij[k] = (uint16_t)((i * LG + j) | (j << 11));
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(kIxWarps * 32) k_interact_fwd_reg(const void* __restrict__ x, int x_bf16,
                                                                     const float* __restrict__ emb, long long B,
@@ -173,40 +190,60 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
                                                                     const uint32_t* __restrict__ gemb_rows) {
   extern __shared__ float ix_smem[];
   constexpr int LG = 33;  // G row stride (odd)
-  const int n = T + 1;
+  constexpr int GR = 16;  // pairs per lane (P <= 496)
+  const int n = T + 1, P = n * (n - 1) / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* z = ix_smem + warp * (32 * D + 32 * LG);
   float* G = z + 32 * D;
-  // (i, j) of every lower-triangle pair k, once per block (not a sqrt and
-  // two search loops per pair and sample)
-  const int P = n * (n - 1) / 2;
   uint16_t* pij = reinterpret_cast<uint16_t*>(ix_smem + kIxWarps * (32 * D + 32 * LG));
-  for (int k = threadIdx.x; k < P; k += blockDim.x) {
-    int i = 1;
-    while ((i + 1) * i / 2 <= k) ++i;
-    const int j = k - i * (i - 1) / 2;  // i <= 31, j <= 30: i*LG + j < 2^11, j < 2^5
-    pij[k] = (uint16_t)((i * LG + j) | (j << 11));
-  }
+  build_pairs(pij, P, LG);
   __syncthreads();
-  for (long long b = (long long)blockIdx.x * kIxWarps + warp; b < B; b += (long long)gridDim.x * kIxWarps) {
-    const long long p = b * T + (lane - 1);  // this lane's embedding-gradient row (lanes 1..T)
-    const long long drow = (gemb_rows && lane >= 1 && lane < n) ? (long long)gemb_rows[p] : p;
-    for (int e = lane; e < n * D; e += 32)
-      z[e] = e < D ? ld_any(x, b * D + e, x_bf16) : emb[b * T * D + (e - D)];
-    const long long ob = b * out_stride;
-    if (lane < n) G[lane * LG + lane] = 0.f;
-    for (int k = lane; k < P; k += 32) {
-      const uint32_t e = pij[k];
-      const int ij = (int)(e & 0x7FFu), j = (int)(e >> 11), i = (ij - j) / LG;
-      const float g = ld_any(gout, ob + D + k, g_bf16);
-      G[ij] = g;
-      G[j * LG + i] = g;
-    }
-    __syncwarp();
-    if (lane < n) {
-      float acc[D];
+  float zr[D], gr[GR], go = 0.f;
+  long long dr = 0;
+  const long long stride = (long long)gridDim.x * kIxWarps;
+  long long b = (long long)blockIdx.x * kIxWarps + warp;
+  auto load = [&](long long bb) {
+    const long long ob = bb * out_stride;
 #pragma unroll
-      for (int d = 0; d < D; ++d) acc[d] = 0.f;
+    for (int r = 0; r < D; ++r) {
+      const int e = lane + 32 * r;
+      zr[r] = e < n * D ? (e < D ? ld_any(x, bb * D + e, x_bf16) : emb[bb * T * D + (e - D)]) : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < GR; ++r) {
+      const int k = lane + 32 * r;
+      gr[r] = k < P ? ld_any(gout, ob + D + k, g_bf16) : 0.f;
+    }
+    go = lane < D ? ld_any(gout, ob + lane, g_bf16) : 0.f;  // gx = gout[:, :D] + dz_0
+    const long long p = bb * T + (lane - 1);                  // this lane's embedding-gradient row
+    dr = (gemb_rows && lane >= 1 && lane < n) ? (long long)gemb_rows[p] : p;
+  };
+  if (b < B) load(b);
+  for (; b < B; b += stride) {
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      const int e = lane + 32 * r;
+      if (e < n * D) z[e] = zr[r];
+    }
+    if (lane < n) G[lane * LG + lane] = 0.f;
+#pragma unroll
+    for (int r = 0; r < GR; ++r) {
+      const int k = lane + 32 * r;
+      if (k < P) {
+        const uint32_t e = pij[k];
+        const int ij = (int)(e & 0x7FFu), j = (int)(e >> 11), i = (ij - j) / LG;
+        G[ij] = gr[r];
+        G[j * LG + i] = gr[r];
+      }
+    }
+    const float go_cur = go;
+    const long long drow = dr;
+    __syncwarp();
+    if (b + stride < B) load(b + stride);  // next sample in flight during this one's math
+    float acc[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc[d] = 0.f;
+    if (lane < n) {
       for (int j = 0; j < n; ++j) {
         const float g = G[lane * LG + j];
 #pragma unroll
@@ -218,14 +255,17 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
           acc[d + 3] = fmaf(g, v.w, acc[d + 3]);
         }
       }
-      if (lane == 0) {
+    }
+    // gx row: lane 0 holds dz_0; gout[:, :D] sits in lanes 0..D-1
 #pragma unroll
-        for (int d = 0; d < D; ++d) st_any(gx, b * D + d, acc[d] + ld_any(gout, ob + d, g_bf16), x_bf16);
-      } else {
-        float4* dst = reinterpret_cast<float4*>(gemb + drow * D);
+    for (int d = 0; d < D; ++d) {
+      const float gd = __shfl_sync(0xffffffffu, go_cur, d);
+      if (lane == 0) st_any(gx, b * D + d, acc[d] + gd, x_bf16);
+    }
+    if (lane >= 1 && lane < n) {
+      float4* dst = reinterpret_cast<float4*>(gemb + drow * D);
 #pragma unroll
-        for (int d = 0; d < D; d += 4) dst[d / 4] = make_float4(acc[d], acc[d + 1], acc[d + 2], acc[d + 3]);
-      }
+      for (int d = 0; d < D; d += 4) dst[d / 4] = make_float4(acc[d], acc[d + 1], acc[d + 2], acc[d + 3]);
     }
     __syncwarp();
   }
@@ -309,7 +349,7 @@ extern "C" int bp_dlrm_interact_backward_rows(const void* d_x, int32_t x_bf16, c
   const int rc = check_shape(B, T, D, out_stride);
   if (rc != BP_OK) return rc;
   if (B == 0) return BP_OK;
-  const long long nblk = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * 16);
+  const long long nblk = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * kIxBlocksPerSM);
   if (T + 1 <= 32 && (D == 4 || D == 8 || D == 16 || D == 32)) {
     const size_t sm = sizeof(float) * kIxWarps * (32 * D + 32 * 33) + sizeof(uint16_t) * 512;
 #define BP_IX_BWD(DD)                                                                                              \
