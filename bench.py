@@ -30,6 +30,7 @@ with EmbeddingBag fwd/bwd + SGD feeding PyTorch MLPs replayed as a CUDA graph.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 
 import numpy as np
@@ -94,6 +95,7 @@ class ClockSampler:
 
     REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
                ("sw_power_cap", 0x4))
+    PERIOD = float(os.environ.get("BAGPIPE_B200_CLOCK_PERIOD", "0.002"))  # seconds between NVML samples
 
     def __init__(self, index: int):
         self.index = index
@@ -125,7 +127,7 @@ class ClockSampler:
     def _loop(self):
         while not self._stop.is_set():
             self._sample()
-            self._stop.wait(0.002)
+            self._stop.wait(self.PERIOD)
 
     def start(self):
         if self.nvml is None:
@@ -186,16 +188,28 @@ def _timed_steps(pipe, first: int, steps: int, flush_buf, torch, exclusive: int 
             "bp_engine_set_l2_flush")
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    wall0 = time.perf_counter()
-    start.record(stream)
-    for i in range(steps):
-        # the last timed step must not enqueue step K+1 ahead of time
-        pipe.step(first + i, early=i < steps - 1)
-    L.check(pipe.lib.bp_engine_join(pipe.eng, L.stream_ptr(stream)), "bp_engine_join")
-    end.record(stream)
-    torch.cuda.synchronize()
-    wall = (time.perf_counter() - wall0) * 1e3
+    # no cyclic-GC pass (a multi-millisecond host stall) inside the short span
+    gc.collect()
+    gc.disable()
+    try:
+        torch.cuda.synchronize()
+        wall0 = time.perf_counter()
+        start.record(stream)
+        host_ts = []
+        for i in range(steps):
+            # the last timed step must not enqueue step K+1 ahead of time
+            pipe.step(first + i, early=i < steps - 1)
+            host_ts.append(time.perf_counter())
+        L.check(pipe.lib.bp_engine_join(pipe.eng, L.stream_ptr(stream)), "bp_engine_join")
+        end.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - wall0) * 1e3
+    finally:
+        gc.enable()
+    dump = os.environ.get("BAGPIPE_B200_BENCH_DUMP")  # debug: host time of every timed step
+    if dump:
+        with open(f"{dump}.steps.{os.environ.get('RANK', '0')}.{first}.json", "w") as fh:
+            json.dump([round((t - wall0) * 1e3, 3) for t in host_ts], fh)
     L.check(pipe.lib.bp_engine_set_l2_flush(pipe.eng, None, 0, 0), "bp_engine_set_l2_flush")
     return start.elapsed_time(end), wall
 

@@ -491,6 +491,18 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   BP_CUDA_TRY(cudaHostAlloc(&e->h_result, bp_engine::kStepRing * 16 * sizeof(int64_t), cudaHostAllocMapped));
   BP_CUDA_TRY(cudaHostGetDevicePointer((void**)&e->d_result, e->h_result, 0));
   BP_CUDA_TRY(cudaMalloc(&e->d_col_tables, sc->num_tables * sizeof(int32_t)));
+  // Reserve the stream-ordered pool's memory up front (its release threshold
+  // is infinite, bp_ctx_create): the per-batch prep arenas and scratch then
+  // never grow the pool inside the iteration loop -- a growth maps memory on
+  // the host thread and stalled a step for milliseconds.
+  {
+    const size_t reserve = std::min<size_t>((size_t)4 << 30, std::max<size_t>((size_t)512 << 20,
+                                             (size_t)(cfg->prep_slots > 0 ? cfg->prep_slots : 8) *
+                                                 (size_t)n * 160));
+    void* tmp = nullptr;
+    if (cudaMallocAsync(&tmp, reserve, e->prepq) == cudaSuccess) cudaFreeAsync(tmp, e->prepq);
+    else cudaGetLastError();
+  }
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
   BP_CUDA_TRY(cudaStreamSynchronize(e->planq));
   BP_CUDA_TRY(cudaStreamSynchronize(e->prepq));

@@ -502,6 +502,8 @@ extern "C" int bp_mark_ids(bp_prep* P, int64_t* d_mark, int64_t tag, bp_stream_t
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  float* parts = nullptr;  // rank partials of the long keys (grow-only; no per-step allocation)
+  size_t parts_cap = 0;
   SideStream() {
     int lo = 0, hi = 0;
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
@@ -555,7 +557,19 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   // stream-ordered scratch), combined in rank order by k_stub_long_combine
   const int T = P->num_ranks;
   float* parts = nullptr;
-  if (T > 1) BP_CUDA_TRY(pool_alloc(&parts, (size_t)P->long_cap * T * dim, ls));
+  if (T > 1) {
+    SideStream& side = side_stream();
+    const size_t need = (size_t)P->long_cap * T * dim;
+    if (need > side.parts_cap) {
+      BP_CUDA_TRY(cudaDeviceSynchronize());  // the old buffer may still be read
+      if (side.parts) BP_CUDA_TRY(cudaFree(side.parts));
+      side.parts = nullptr;
+      side.parts_cap = 0;
+      BP_CUDA_TRY(cudaMalloc(&side.parts, need * sizeof(float)));
+      side.parts_cap = need;
+    }
+    parts = side.parts;
+  }
   BP_DISPATCH_GD(G, dpl,
                  (long_attr<g_, d_>(), k_stub_step_long<g_, d_><<<kLongBlocks, 128, kLongSmemPad, ls>>>(
                      P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,
@@ -566,7 +580,6 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
                    (k_stub_long_combine<g_, d_><<<kNumSMs, 256, 0, ls>>>(
                        P->d_num_long, P->d_long, P->long_cap, T, parts, d_rows, d_row_index, d_dirty, dim, lr, mode,
                        d_grad_out, P->d_uniq_id_s, d_next_mark, next_tag, (unsigned long long*)d_stats)));
-    cudaFreeAsync(parts, ls);
   }
   BP_DISPATCH_GD(G, dpl,
                  (k_stub_step<g_, d_><<<blocks, threads, 0, s>>>(
