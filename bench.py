@@ -249,7 +249,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
 
     from paper_2202_12429_b200 import _lib as L
     from paper_2202_12429_b200.engine import EngineConfig, _Pipeline
-    from paper_2202_12429_b200.shard import shard_batches, table_shards
+    from paper_2202_12429_b200.shard import shard_batches, table_costs, table_shards
 
     L.lib()
     sc = schema()
@@ -261,9 +261,12 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     # every rank runs the whole pipeline for its tables of every example --
     # N x 16,384 x 26/N = the same 425,984 occurrences per step as one GPU --
     # with no data-path collective, and the same per-GPU HBM cache budget.
-    tables = table_shards(sc.num_tables, world)[rank]
     gbatch = BATCH * world
     full = make_batches(n_batches, args.seed, gbatch)
+    # tables dealt by their cost (occurrences + unique keys of the first
+    # batch), largest first to the least-loaded rank
+    shards = table_shards(sc.num_tables, world, table_costs(full[0])) if world > 1 else [list(range(sc.num_tables))]
+    tables = shards[rank]
     batches = full if world == 1 else shard_batches(full, tables)
     # N GPUs = the reference's N data-parallel trainers (rank r = examples
     # [r*B/N, (r+1)*B/N) of the global batch; gradients combined in rank order)
@@ -332,7 +335,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     # ---- DLRM mode (N=1): the same engine feeding PyTorch MLPs (bf16 autocast)
     dlrm = None
     if not args.no_dlrm:
-        dlrm = run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank, world, len(tables))
+        dlrm = run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank, world, len(tables), shards)
 
     t = torch.tensor([ms, e2e_ms], device="cuda", dtype=torch.float64)
     by_rank = [ms / steps]
@@ -416,7 +419,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     return out
 
 
-def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, local_tables=26) -> dict:
+def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, local_tables=26, shards=None) -> dict:
     """DLRM mode; N > 1 = hybrid parallel (hybrid.py): this rank's table shard
     through the engine over the global batch, all-to-all of pooled rows and
     their gradients, data-parallel MLPs with a mean all-reduce."""
@@ -436,9 +439,9 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
         # NVLink peer-memory exchange fused into the EmbeddingBag kernels
         # (default) or the NCCL all-to-all version
         if os.environ.get("BAGPIPE_B200_EXCHANGE", "peer") == "peer":
-            ex = PeerExchange(sc.num_tables, DIM, rank, world, BATCH)
+            ex = PeerExchange(sc.num_tables, DIM, rank, world, BATCH, shards=shards)
         else:
-            ex = EmbeddingExchange(sc.num_tables, DIM, rank, world)
+            ex = EmbeddingExchange(sc.num_tables, DIM, rank, world, shards=shards)
     trainer = DLRMTrainer(dcfg, sc.num_dense, sc.num_tables, DIM, exchange=ex)
     dev_inputs = {}
     for i, b in enumerate(batches):

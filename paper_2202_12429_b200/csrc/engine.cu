@@ -502,6 +502,10 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     void* tmp = nullptr;
     if (cudaMallocAsync(&tmp, reserve, e->prepq) == cudaSuccess) cudaFreeAsync(tmp, e->prepq);
     else cudaGetLastError();
+    // and a block freed on the compute stream for its own per-call scratch
+    // (reused on the same stream without a cross-stream dependency)
+    if (cudaMallocAsync(&tmp, (size_t)256 << 20, e->compute) == cudaSuccess) cudaFreeAsync(tmp, e->compute);
+    else cudaGetLastError();
   }
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
   BP_CUDA_TRY(cudaStreamSynchronize(e->planq));

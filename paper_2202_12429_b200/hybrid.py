@@ -31,9 +31,9 @@ from .shard import table_shards
 class EmbeddingExchange:
     """All-to-all of pooled embedding rows between table owners and example owners."""
 
-    def __init__(self, num_tables: int, dim: int, rank: int, world: int, group=None):
+    def __init__(self, num_tables: int, dim: int, rank: int, world: int, group=None, shards=None):
         self.num_tables, self.dim, self.rank, self.world, self.group = num_tables, dim, rank, world, group
-        self.shards = table_shards(num_tables, world)
+        self.shards = shards if shards is not None else table_shards(num_tables, world)
         self.local_tables = self.shards[rank]
         order = [t for s in self.shards for t in s]        # concatenation order of the received blocks
         self.to_global = torch.tensor([order.index(t) for t in range(num_tables)], dtype=torch.long)
@@ -109,14 +109,14 @@ class PeerExchange:
     phases and protect buffer reuse.  Same interface fields as
     EmbeddingExchange (shards, local_tables, world, rank, num_tables)."""
 
-    def __init__(self, num_tables: int, dim: int, rank: int, world: int, bl: int, group=None):
+    def __init__(self, num_tables: int, dim: int, rank: int, world: int, bl: int, group=None, shards=None):
         import ctypes as C
 
         from . import _lib as L
         from .device import _wrap_device
 
         self.num_tables, self.dim, self.rank, self.world, self.bl, self.group = num_tables, dim, rank, world, bl, group
-        self.shards = table_shards(num_tables, world)
+        self.shards = shards if shards is not None else table_shards(num_tables, world)
         self.local_tables = self.shards[rank]
         lib = L.lib()
         self._lib, self._L = lib, L

@@ -9,8 +9,11 @@ unchanged) partitions the work without any data-path collective, and the
 union of the shard stores equals the single-GPU store bit for bit
 (tests/test_shard_dist.py checks it with gloo on CPU ranks).
 
-Tables are dealt round-robin: every table contributes exactly one key per
-example, so ranks differ by at most one table's worth of occurrences.
+Tables are dealt round-robin by default: every table contributes exactly one
+key per example, so ranks differ by at most one table's worth of
+occurrences.  With a per-table cost (e.g. unique keys per batch, which drive
+prefetch, insertion, eviction and the trainer) the tables are instead dealt
+longest-processing-time first, each to the rank with the least cost so far.
 """
 
 from __future__ import annotations
@@ -20,9 +23,33 @@ import numpy as np
 from .traces import Batch
 
 
-def table_shards(num_tables: int, world: int) -> list:
-    """Tables owned by each rank (round-robin)."""
-    return [list(range(r, num_tables, world)) for r in range(world)]
+def table_shards(num_tables: int, world: int, cost=None) -> list:
+    """Tables owned by each rank, in increasing table order: round-robin, or
+    greedy by ``cost[t]`` (largest first, to the least-loaded rank; ties to
+    the lower rank) -- deterministic, so every rank computes the same split."""
+    if cost is None:
+        return [list(range(r, num_tables, world)) for r in range(world)]
+    cost = np.asarray(cost, dtype=np.float64)
+    if cost.shape != (num_tables,):
+        raise ValueError("cost needs one entry per table")
+    load = np.zeros(world)
+    out = [[] for _ in range(world)]
+    for t in sorted(range(num_tables), key=lambda t: (-cost[t], t)):
+        r = int(np.argmin(load))
+        out[r].append(t)
+        load[r] += cost[t]
+    return [sorted(ts) for ts in out]
+
+
+def table_costs(batch: Batch, unique_weight: float = 4.0) -> np.ndarray:
+    """Sharding cost per table of one columnar batch: its occurrences (one per
+    example: batch prep, trainer streams) plus ``unique_weight`` x its unique
+    keys (lookups, prefetches, insertions, evictions, write-back)."""
+    if not batch.is_columnar:
+        raise ValueError("table costs need a columnar batch")
+    n = batch.rows.shape[0]
+    return np.asarray([n + unique_weight * len(np.unique(batch.rows[:, c])) for c in range(batch.rows.shape[1])],
+                      dtype=np.float64)
 
 
 def shard_batches(batches: list, tables: list) -> list:
