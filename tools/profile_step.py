@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--nvtx", action="store_true")
     ap.add_argument("--torch-prof", action="store_true")
     ap.add_argument("--host-inputs", action="store_true")
+    ap.add_argument("--pin", action="store_true", help="host inputs in pinned memory (bench.py's e2e)")
     ap.add_argument("--cprofile", action="store_true")
     ap.add_argument("--trace", default=None, help="write a chrome trace (kernel timeline per stream) here")
     ap.add_argument("--flush", action="store_true", help="256 MiB L2 flush before each step, like bench.py")
@@ -59,6 +60,9 @@ def main():
     cfg = EngineConfig(cache_capacity=sc.total_rows // 100, batch_size=bench.BATCH, lookahead=0, num_shards=1,
                        seed=11)
     dev = None
+    if args.host_inputs and args.pin:
+        for b in batches:
+            b.pin_memory()
     if not args.host_inputs:
         dev = {}
         for i, b in enumerate(batches):
