@@ -544,6 +544,10 @@ int bp_engine_dlrm_forward_peer(bp_engine* engine, int64_t pos, int32_t plan_slo
 int bp_engine_dlrm_backward_peer(bp_engine* engine, int64_t pos, int32_t plan_slot, const bp_peer_xchg* grads,
                                  float scale, int32_t model_dim, int32_t opt, float lr, float eps,
                                  int32_t chunk_slot, int32_t drain_slot, bp_step_result* out);
+/* Asynchronous form: enqueue only; bp_engine_train_end reads the counters. */
+int bp_engine_dlrm_backward_peer_begin(bp_engine* engine, int64_t pos, int32_t plan_slot, const bp_peer_xchg* grads,
+                                       float scale, int32_t model_dim, int32_t opt, float lr, float eps,
+                                       int32_t chunk_slot, int32_t drain_slot);
 
 /* DLRM feature interaction (dense-model side of DLRM mode; the reference has
  * no model).  z = [x; emb_0..emb_{T-1}] per sample (T+1 vectors of D);

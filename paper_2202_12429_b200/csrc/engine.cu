@@ -1266,6 +1266,28 @@ extern "C" int bp_engine_dlrm_backward_peer(bp_engine* e, int64_t pos, int32_t p
   return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
 }
 
+// Asynchronous form of bp_engine_dlrm_backward_peer: enqueue only (the
+// device-side peer barriers order the ranks' buffer reuse across iterations);
+// bp_engine_train_end reads the counters.
+extern "C" int bp_engine_dlrm_backward_peer_begin(bp_engine* e, int64_t pos, int32_t plan_slot,
+                                                  const bp_peer_xchg* grads, float scale, int32_t model_dim,
+                                                  int32_t opt, float lr, float eps, int32_t chunk_slot,
+                                                  int32_t drain_slot) {
+  using namespace bp;
+  if (e->step_count == bp_engine::kStepRing) return BP_ERR_ENGINE;
+  bp_prep* P = e->preps[engine_prep_slot(e, pos)];
+  if (!P) return BP_ERR_ENGINE;
+  PlanSlot& ps = e->plans[plan_slot];
+  bp_cache_view cv;
+  bp_cache_get_view(e->cache, &cv);
+  stage_begin(e, kStageTrainer, e->compute);
+  int rc = bp_embbag_backward_peer(P, grads, scale, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim, opt,
+                                   lr, eps, e->stats, e->compute);
+  stage_end(e, kStageTrainer, e->compute);
+  if (rc) return rc;
+  return engine_finish_begin(e, P, ps, chunk_slot, drain_slot);
+}
+
 // Evicted keys of a chunk (device -> host), for event logs.
 extern "C" int bp_engine_chunk_keys(bp_engine* e, int32_t chunk_slot, uint64_t* h_out, int64_t n) {
   if (n <= 0) return BP_OK;

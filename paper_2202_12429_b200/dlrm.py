@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import copy
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -249,6 +250,7 @@ class DLRMTrainer:
             self.compute_model = self.model
             self.opt = torch.optim.SGD(self.model.parameters(), lr=dcfg.mlp_lr)
         self.losses: list = []
+        self.async_peer = os.environ.get("BAGPIPE_B200_ASYNC_PEER", "1") == "1"
         # single GPU, dims the sorted backward supports: gradients in key-sorted order
         self._sorted = dcfg.sorted_grad and (exchange is None or exchange.world <= 1) and dim in (4, 8, 16, 32)
         self._dense_dev: dict = {}
@@ -271,10 +273,13 @@ class DLRMTrainer:
         self._dense_dev[pos] = (self._pad_dense(dense), labels)
 
     def can_split(self) -> bool:
-        """Single GPU: the iteration is enqueued by train_begin and its counters
-        read later by the engine (bp_engine_train_end), so the host prepares
-        the next iteration while this one runs."""
-        return self.exchange is None or self.exchange.world <= 1
+        """Single GPU and the NVLink peer exchange: the iteration is enqueued by
+        train_begin and its counters read later by the engine
+        (bp_engine_train_end), so the host prepares the next iteration while
+        this one runs (the peer exchange's device barriers keep the ranks'
+        buffer reuse ordered across iterations)."""
+        ex = self.exchange
+        return ex is None or ex.world <= 1 or (hasattr(ex, "rows_x") and self.async_peer)
 
     def train(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, res) -> None:
         if self.exchange is not None and self.exchange.world > 1:
@@ -285,6 +290,8 @@ class DLRMTrainer:
         L.check(pipe.lib.bp_engine_train_end(pipe.eng, C.byref(res)), "bp_engine_train_end")
 
     def train_begin(self, pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain) -> None:
+        if self.exchange is not None and self.exchange.world > 1:
+            return self._train_peer(pipe, pos, plan, nxt, skip_key, has_skip, chunk, drain, None)
         lib = pipe.lib
         batch = pipe.batches[pos]
         n_occ = int(batch.packed_occurrences()[0].size)
@@ -425,11 +432,12 @@ class DLRMTrainer:
                 g["step"].replay()
             else:
                 self.opt.step()
-            L.check(lib.bp_engine_dlrm_backward_peer(pipe.eng, pos, plan.slot, C.byref(ex.grads_x),
-                                                     1.0 / ex.world, self.dim, self.dcfg.opt_code,
-                                                     float(np.float32(self.dcfg.emb_lr)),
-                                                     float(np.float32(self.dcfg.adagrad_eps)), chunk, drain,
-                                                     C.byref(res)), "bp_engine_dlrm_backward_peer")
+            args = (pipe.eng, pos, plan.slot, C.byref(ex.grads_x), 1.0 / ex.world, self.dim, self.dcfg.opt_code,
+                    float(np.float32(self.dcfg.emb_lr)), float(np.float32(self.dcfg.adagrad_eps)), chunk, drain)
+            if res is None:  # asynchronous: counters read by the engine later
+                L.check(lib.bp_engine_dlrm_backward_peer_begin(*args), "bp_engine_dlrm_backward_peer_begin")
+            else:
+                L.check(lib.bp_engine_dlrm_backward_peer(*args, C.byref(res)), "bp_engine_dlrm_backward_peer")
 
     def _loss(self, dense, emb, labels, grad_rows=None):
         logits = self.compute_model(dense, emb, grad_rows).float()
