@@ -414,6 +414,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         out["roofline"]["peak"] = hbm_peak
         out["roofline"]["frac"] = out["roofline"]["achieved"] / hbm_peak
         out["roofline"]["peak_source"] = peak_src
+        for part in (dlrm.get("roofline_parts") or {}).values():
+            part.update(peak=hbm_peak, frac=part["achieved"] / hbm_peak, peak_source=peak_src)
+        out["roofline_parts"] = dlrm.get("roofline_parts")
     else:
         out["roofline"] = dict(out["roofline_stub_trainer"], bound="hbm")
     return out
@@ -466,8 +469,10 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
     stages = _stage_breakdown(pipe, warm + steps, 8)
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     n_occ = BATCH * world * local_tables
-    # "trainer" spans: EmbeddingBag forward and backward (2 per step), per step
-    spans = stages["trainer"]
+    # "trainer" spans: the EmbeddingBag forward, "trainer_bwd": its backward
+    # + optimizer (one each per step); per step
+    fwd_span, bwd_span = stages["trainer"], stages["trainer_bwd"]
+    spans = (fwd_span[0] + bwd_span[0], fwd_span[1] + bwd_span[1])
     # forward N_occ*(64 row read + 64 pooled write + 4 index)
     fwd_bytes = n_occ * (8 * DIM + 4)
     losses = trainer.loss_history()
@@ -488,7 +493,28 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
                          if spans[0] else 0.0,
                          "traffic": _traffic(),
                          "note": "SURVEY 8(d) algorithmic bytes: forward N_occ*(64 row read + 64 pooled write + 4 "
-                                 "index) + backward N_occ*(64 gradient read + 4 index) + U*(64 read + 64 write)"}}
+                                 "index) + backward N_occ*(64 gradient read + 4 index) + U*(64 read + 64 write)"},
+            # the two halves of the pair above, each timed by its own stage
+            # events in the same steps
+            # (N > 1: the peer-exchange variants, their spans include the
+            # device-side barriers of the exchange)
+            "roofline_parts": None if world > 1 else {
+                "gather": _part("bp::k_embbag_fwd_rows_v4 (EmbeddingBag forward: gather + pooling)",
+                                fwd_bytes, fwd_span, "k_embbag_fwd_rows_v4"),
+                "scatter": _part("bp::k_embbag_bwd_staged (sorted-gradient segmented scatter-add + SGD in place)",
+                                 bwd_bytes(n_occ, int(u_mean)), bwd_span, "k_embbag_bwd_staged<4>")}}
+
+
+def _part(kernel: str, nbytes: int, span, ncu_name: str) -> dict:
+    ms = span[0]
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "round1", "traffic.json")))[
+            "dram_bytes_per_launch"][ncu_name]
+    except (OSError, KeyError, ValueError):
+        traffic = None
+    return {"kernel": kernel, "bound": "hbm", "bytes_per_launch": nbytes, "ms_per_launch": ms,
+            "launches_per_step": span[1], "unit": "GB/s", "achieved": nbytes / (ms * 1e-3) / 1e9 if ms else 0.0,
+            "traffic": traffic}
 
 
 def _traffic():

@@ -455,10 +455,11 @@ int bp_engine_set_timing(bp_engine* engine, int32_t on);
  * compute stream; exclusive != 0 fences the plan and host-link streams
  * around the write.  d_buf = NULL disables. */
 int bp_engine_set_l2_flush(bp_engine* engine, void* d_buf, int64_t bytes, int32_t exclusive);
-/* Per-stage device time since the last call, 7 stages: prep, planner, fetch
- * (link), apply (insert+TTL+lookup+mark), trainer, evict, flush (link).
- * Synchronises the device. */
-int bp_engine_stage_times(bp_engine* engine, double* h_ms7, int64_t* h_counts7);
+/* Per-stage device time since the last call, 8 stages: prep, planner, fetch
+ * (link), apply (insert+TTL+lookup+mark), trainer (stub trainer or DLRM
+ * EmbeddingBag forward), evict, flush (link), trainer_bwd (DLRM EmbeddingBag
+ * backward + optimizer).  Synchronises the device. */
+int bp_engine_stage_times(bp_engine* engine, double* h_ms8, int64_t* h_counts8);
 
 /* ------------------------------------------------------- EmbeddingBag (DLRM)
  * North-star piece 4 (no reference counterpart: parity vs a PyTorch fp32 CPU

@@ -284,8 +284,10 @@ struct UploadSlot {
 namespace bp {
 // Optional per-stage CUDA-event timing (cfg.timing): pairs recorded on the
 // stream that runs the stage, summed on demand by bp_engine_stage_times.
+// kStageTrainer: the stub trainer, or the DLRM EmbeddingBag forward;
+// kStageTrainerBwd: the DLRM EmbeddingBag backward + optimizer
 enum Stage { kStagePrep = 0, kStagePlanner, kStageFetch, kStageApply, kStageTrainer, kStageEvict, kStageFlush,
-             kNumStages };
+             kStageTrainerBwd, kNumStages };
 struct StageTimer {
   std::mutex mu;  // the planner thread (prep/planner stages) and the training thread record concurrently
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans[kNumStages];
@@ -1148,10 +1150,10 @@ extern "C" int bp_engine_dlrm_backward(bp_engine* e, int64_t pos, int32_t plan_s
   PlanSlot& ps = e->plans[plan_slot];
   bp_cache_view cv;
   bp_cache_get_view(e->cache, &cv);
-  stage_begin(e, kStageTrainer, e->compute);
+  stage_begin(e, kStageTrainerBwd, e->compute);
   int rc = bp_embbag_backward(P, d_grad, nullptr, nullptr, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty,
                               model_dim, opt, lr, eps, e->stats, e->compute);
-  stage_end(e, kStageTrainer, e->compute);
+  stage_end(e, kStageTrainerBwd, e->compute);
   if (rc) return rc;
   return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
 }
@@ -1177,10 +1179,10 @@ extern "C" int bp_engine_dlrm_backward_sorted(bp_engine* e, int64_t pos, int32_t
   PlanSlot& ps = e->plans[plan_slot];
   bp_cache_view cv;
   bp_cache_get_view(e->cache, &cv);
-  stage_begin(e, kStageTrainer, e->compute);
+  stage_begin(e, kStageTrainerBwd, e->compute);
   int rc = bp_embbag_backward_sorted(P, d_grad_sorted, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim,
                                      opt, lr, eps, e->stats, e->compute);
-  stage_end(e, kStageTrainer, e->compute);
+  stage_end(e, kStageTrainerBwd, e->compute);
   if (rc) return rc;
   return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
 }
@@ -1199,7 +1201,7 @@ extern "C" int bp_engine_dlrm_backward_begin(bp_engine* e, int64_t pos, int32_t 
   PlanSlot& ps = e->plans[plan_slot];
   bp_cache_view cv;
   bp_cache_get_view(e->cache, &cv);
-  stage_begin(e, kStageTrainer, e->compute);
+  stage_begin(e, kStageTrainerBwd, e->compute);
   if (grad_sorted) {
     const size_t need = (size_t)bp_embbag_bwd_scratch_bytes(P->n_occ, model_dim);
     if (need > e->bwd_scratch_bytes) {
@@ -1217,7 +1219,7 @@ extern "C" int bp_engine_dlrm_backward_begin(bp_engine* e, int64_t pos, int32_t 
                                                            e->bwd_scratch, (int64_t)e->bwd_scratch_bytes, e->compute)
                        : bp_embbag_backward(P, d_grad, nullptr, nullptr, cv.d_values, e->cfg.dim, e->slots_s,
                                             cv.d_dirty, model_dim, opt, lr, eps, e->stats, e->compute);
-  stage_end(e, kStageTrainer, e->compute);
+  stage_end(e, kStageTrainerBwd, e->compute);
   if (rc) return rc;
   return engine_finish_begin(e, P, ps, chunk_slot, drain_slot);
 }
@@ -1258,10 +1260,10 @@ extern "C" int bp_engine_dlrm_backward_peer(bp_engine* e, int64_t pos, int32_t p
   PlanSlot& ps = e->plans[plan_slot];
   bp_cache_view cv;
   bp_cache_get_view(e->cache, &cv);
-  stage_begin(e, kStageTrainer, e->compute);
+  stage_begin(e, kStageTrainerBwd, e->compute);
   int rc = bp_embbag_backward_peer(P, grads, scale, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim, opt,
                                    lr, eps, e->stats, e->compute);
-  stage_end(e, kStageTrainer, e->compute);
+  stage_end(e, kStageTrainerBwd, e->compute);
   if (rc) return rc;
   return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
 }
@@ -1280,10 +1282,10 @@ extern "C" int bp_engine_dlrm_backward_peer_begin(bp_engine* e, int64_t pos, int
   PlanSlot& ps = e->plans[plan_slot];
   bp_cache_view cv;
   bp_cache_get_view(e->cache, &cv);
-  stage_begin(e, kStageTrainer, e->compute);
+  stage_begin(e, kStageTrainerBwd, e->compute);
   int rc = bp_embbag_backward_peer(P, grads, scale, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim, opt,
                                    lr, eps, e->stats, e->compute);
-  stage_end(e, kStageTrainer, e->compute);
+  stage_end(e, kStageTrainerBwd, e->compute);
   if (rc) return rc;
   return engine_finish_begin(e, P, ps, chunk_slot, drain_slot);
 }

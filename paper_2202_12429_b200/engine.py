@@ -178,7 +178,7 @@ class _Pipeline:
     ``end`` split the reference's loop so a benchmark can time iterations.
     """
 
-    STAGES = ("prep", "planner", "fetch", "apply", "trainer", "evict", "flush")
+    STAGES = ("prep", "planner", "fetch", "apply", "trainer", "evict", "flush", "trainer_bwd")
 
     def __init__(self, cfg: EngineConfig, schema: Schema, batches: list, fingerprint, fault, device_inputs=None,
                  timing: bool = False, trainer=None, link_mode: int | None = None, threaded: bool | None = None):
@@ -294,8 +294,8 @@ class _Pipeline:
 
     def stage_times(self) -> dict:
         """{stage: (total ms, launches)} since the last call (timing=True)."""
-        ms = np.zeros(7, dtype=np.float64)
-        cnt = np.zeros(7, dtype=np.int64)
+        ms = np.zeros(len(self.STAGES), dtype=np.float64)
+        cnt = np.zeros(len(self.STAGES), dtype=np.int64)
         L.check(self.lib.bp_engine_stage_times(self.eng, ms.ctypes.data, cnt.ctypes.data), "bp_engine_stage_times")
         return {name: (float(m), int(c)) for name, m, c in zip(self.STAGES, ms, cnt)}
 
