@@ -112,15 +112,30 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd(const void* __re
 //   gradients, odd row stride, pairs k -> (i, j) from a per-block table) and
 //   z staged, lane i computes dz_i = sum_j G_ij z_j (z_j float4 broadcasts).
 constexpr int kIxBlocksPerSM = 4;
+// k_interact_bwd_reg: resident CTAs per SM (launch bounds and grid).  D = 16
+// takes 91 registers: 2 CTAs; a 3-CTA cap (80 registers) spilled and measured
+// slower (46 vs 43 us at the Criteo-Kaggle shape, tools/ix_bench.py)
+constexpr int ix_bwd_bps(int D) { return D >= 32 ? 1 : 2; }
 
-__device__ __forceinline__ void build_pairs(uint16_t* pij, int P, int LG) {
+// pair k = (i, j), i > j: both G offsets, i*LG + j (low half) and j*LG + i
+// (high half), so the scatter needs no index arithmetic
+__device__ __forceinline__ void build_pairs(uint32_t* pij, int P, int LG) {
   for (int k = threadIdx.x; k < P; k += blockDim.x) {
     int i = 1;
     while ((i + 1) * i / 2 <= k) ++i;
-    const int j = k - i * (i - 1) / 2;  // i <= 31, j <= 30: i*LG + j < 2^11, j < 2^5
-    pij[k] = (uint16_t)((i * LG + j) | (j << 11));
+    const int j = k - i * (i - 1) / 2;
+    pij[k] = (uint32_t)(i * LG + j) | ((uint32_t)(j * LG + i) << 16);
   }
 }
+
+// raw 32-bit image of element i (bf16 bits zero-extended, or the fp32 bits):
+// the prefetch keeps loads unconsumed until the next sample is computed (a
+// conversion at load time stalled the warp on the load right away)
+__device__ __forceinline__ uint32_t ld_raw(const void* p, long long i, int bf16) {
+  return bf16 ? (uint32_t)reinterpret_cast<const uint16_t*>(p)[i] : reinterpret_cast<const uint32_t*>(p)[i];
+}
+
+__device__ __forceinline__ float raw_f(uint32_t r, int bf16) { return __uint_as_float(bf16 ? r << 16 : r); }
 
 template <int D>
 __global__ void __launch_bounds__(kIxWarps * 32) k_interact_fwd_reg(const void* __restrict__ x, int x_bf16,
@@ -182,7 +197,7 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_fwd_reg(const void* 
 }
 
 template <int D>
-__global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* __restrict__ x, int x_bf16,
+__global__ void __launch_bounds__(kIxWarps * 32, ix_bwd_bps(D)) k_interact_bwd_reg(const void* __restrict__ x, int x_bf16,
                                                                     const float* __restrict__ emb,
                                                                     const void* __restrict__ gout, int g_bf16,
                                                                     long long B, int T, int out_stride,
@@ -195,10 +210,11 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* z = ix_smem + warp * (32 * D + 32 * LG);
   float* G = z + 32 * D;
-  uint16_t* pij = reinterpret_cast<uint16_t*>(ix_smem + kIxWarps * (32 * D + 32 * LG));
+  uint32_t* pij = reinterpret_cast<uint32_t*>(ix_smem + kIxWarps * (32 * D + 32 * LG));
   build_pairs(pij, P, LG);
   __syncthreads();
-  float zr[D], gr[GR], go = 0.f;
+  const uint32_t* emb_u = reinterpret_cast<const uint32_t*>(emb);
+  uint32_t zr[D], gr[GR], go = 0u;
   long long dr = 0;
   const long long stride = (long long)gridDim.x * kIxWarps;
   long long b = (long long)blockIdx.x * kIxWarps + warp;
@@ -207,14 +223,14 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       const int e = lane + 32 * r;
-      zr[r] = e < n * D ? (e < D ? ld_any(x, bb * D + e, x_bf16) : emb[bb * T * D + (e - D)]) : 0.f;
+      zr[r] = e < n * D ? (e < D ? ld_raw(x, bb * D + e, x_bf16) : emb_u[bb * T * D + (e - D)]) : 0u;
     }
 #pragma unroll
     for (int r = 0; r < GR; ++r) {
       const int k = lane + 32 * r;
-      gr[r] = k < P ? ld_any(gout, ob + D + k, g_bf16) : 0.f;
+      gr[r] = k < P ? ld_raw(gout, ob + D + k, g_bf16) : 0u;
     }
-    go = lane < D ? ld_any(gout, ob + lane, g_bf16) : 0.f;  // gx = gout[:, :D] + dz_0
+    go = lane < D ? ld_raw(gout, ob + lane, g_bf16) : 0u;  // gx = gout[:, :D] + dz_0
     const long long p = bb * T + (lane - 1);                  // this lane's embedding-gradient row
     dr = (gemb_rows && lane >= 1 && lane < n) ? (long long)gemb_rows[p] : p;
   };
@@ -223,7 +239,7 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       const int e = lane + 32 * r;
-      if (e < n * D) z[e] = zr[r];
+      if (e < n * D) z[e] = raw_f(zr[r], e < D ? x_bf16 : 0);
     }
     if (lane < n) G[lane * LG + lane] = 0.f;
 #pragma unroll
@@ -231,12 +247,12 @@ __global__ void __launch_bounds__(kIxWarps * 32) k_interact_bwd_reg(const void* 
       const int k = lane + 32 * r;
       if (k < P) {
         const uint32_t e = pij[k];
-        const int ij = (int)(e & 0x7FFu), j = (int)(e >> 11), i = (ij - j) / LG;
-        G[ij] = gr[r];
-        G[j * LG + i] = gr[r];
+        const float gv = raw_f(gr[r], g_bf16);
+        G[e & 0xFFFFu] = gv;
+        G[e >> 16] = gv;
       }
     }
-    const float go_cur = go;
+    const float go_cur = raw_f(go, g_bf16);
     const long long drow = dr;
     __syncwarp();
     if (b + stride < B) load(b + stride);  // next sample in flight during this one's math
@@ -349,12 +365,14 @@ extern "C" int bp_dlrm_interact_backward_rows(const void* d_x, int32_t x_bf16, c
   const int rc = check_shape(B, T, D, out_stride);
   if (rc != BP_OK) return rc;
   if (B == 0) return BP_OK;
-  const long long nblk = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * kIxBlocksPerSM);
+  const long long nblk = std::min<long long>((B + kIxWarps - 1) / kIxWarps, (long long)kNumSMs * ix_bwd_bps(D));
   if (T + 1 <= 32 && (D == 4 || D == 8 || D == 16 || D == 32)) {
-    const size_t sm = sizeof(float) * kIxWarps * (32 * D + 32 * 33) + sizeof(uint16_t) * 512;
+    const size_t sm = sizeof(float) * kIxWarps * (32 * D + 32 * 33) + sizeof(uint32_t) * 512;
 #define BP_IX_BWD(DD)                                                                                              \
   {                                                                                                                \
     BP_CUDA_TRY(cudaFuncSetAttribute(k_interact_bwd_reg<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    BP_CUDA_TRY(cudaFuncSetAttribute(k_interact_bwd_reg<DD>, cudaFuncAttributePreferredSharedMemoryCarveout,         \
+                                     cudaSharedmemCarveoutMaxShared));                                                 \
     k_interact_bwd_reg<DD><<<(unsigned)nblk, kIxWarps * 32, sm, (cudaStream_t)stream>>>(                          \
         d_x, x_bf16, d_emb, d_gout, g_bf16, B, T, out_stride, d_gx, d_gemb, d_gemb_rows);                                         \
   }
