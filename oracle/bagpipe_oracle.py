@@ -12,6 +12,8 @@ dictionary loops:
   hashing / init     reference hashing.py:42-79, store.py:29-42
   unique keys        reference traces.py:91-103, engine.py:142-182
   Algorithm 1        reference lookahead.py:64-123 (refill / pop / halving)
+  cache contents     reference cache.py:99-286 (insert / TTL / update /
+                     evict / drain, content_checksum, canonical_digest)
   stub trainer       reference trainer.py:37-53, 92-105, 140-146
   baseline engine    reference engine.py:688-769
   pipeline data path reference engine.py:302-452 (gate, forced flush,
@@ -100,6 +102,91 @@ def first_order_unique(keys: np.ndarray):
     rank = np.empty_like(order)
     rank[order] = np.arange(order.size)
     return sorted_u[order], rank[inv]
+
+
+# ----------------------------------------------------------- cache contents
+def content_checksum(keys, ttl, dirty, values) -> int:
+    """XOR over entries of a splitmix chain over (t<<44 ^ r), ttl, dirty<<63
+    and every f32 word of the value (cache.py:249-272); order-independent."""
+    keys = np.asarray(keys, dtype=np.uint64)
+    if keys.size == 0:
+        return 0
+    word = splitmix(keys)
+    word = splitmix(word ^ np.asarray(ttl, dtype=np.int64).astype(np.uint64))
+    word = splitmix(word ^ (np.asarray(dirty, dtype=np.uint64) << np.uint64(63)))
+    vals = np.ascontiguousarray(values, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    for j in range(vals.shape[1]):
+        word = splitmix(word ^ vals[:, j])
+    return int(np.bitwise_xor.reduce(word))
+
+
+def canonical_digest(keys, ttl, dirty, values) -> str:
+    """blake2b-128 over key-sorted records <i8 table, row, ttl, dirty> + <f4
+    value (cache.py:274-286); one update over the concatenated records equals
+    the reference's per-entry updates."""
+    keys = np.asarray(keys, dtype=np.uint64)
+    order = np.argsort(keys, kind="stable")
+    k = keys[order]
+    dim = np.shape(values)[1] if np.ndim(values) == 2 else 0
+    rec = np.zeros(k.size, dtype=[("h", "<i8", (4,)), ("v", "<f4", (dim,))])
+    rec["h"][:, 0] = (k >> SHIFT).astype(np.int64)
+    rec["h"][:, 1] = (k & ROWMASK).astype(np.int64)
+    rec["h"][:, 2] = np.asarray(ttl, dtype=np.int64)[order]
+    rec["h"][:, 3] = np.asarray(dirty, dtype=np.int64)[order]
+    if k.size:
+        rec["v"] = np.asarray(values, dtype=np.float32)[order]
+    h = hashlib.blake2b(digest_size=16)
+    h.update(rec.tobytes())
+    return h.hexdigest()
+
+
+class DictCache:
+    """The reference DynamicCache's contents as a dict key -> [value, ttl,
+    dirty] (cache.py:99-247): enough to replay an API scenario and checksum
+    it; capacity/ordering errors are exercised on the GPU object itself."""
+
+    def __init__(self):
+        self.ent = {}
+
+    def prefetch(self, keys, values, ttls):
+        for k, v, t in zip(keys, values, ttls):
+            assert k not in self.ent
+            self.ent[int(k)] = [np.asarray(v, dtype=np.float32).copy(), int(t), False]
+
+    def set_ttl(self, keys, ttls):
+        for k, t in zip(keys, ttls):
+            self.ent[int(k)][1] = int(t)
+
+    def update(self, keys, values, mask):
+        for k, v, m in zip(keys, values, mask):
+            e = self.ent[int(k)]
+            e[0] = np.asarray(v, dtype=np.float32).copy()
+            e[2] = e[2] or bool(m)
+
+    def release(self, pred):
+        gone = sorted(k for k, e in self.ent.items() if pred(e))
+        out = [(k, self.ent[k][0], self.ent[k][2]) for k in gone]
+        for k in gone:
+            del self.ent[k]
+        return out
+
+    def arrays(self):
+        ks = sorted(self.ent)
+        dim = len(next(iter(self.ent.values()))[0]) if ks else 0
+        vals = np.asarray([self.ent[k][0] for k in ks], dtype=np.float32).reshape(len(ks), dim)
+        return (np.asarray(ks, dtype=np.uint64), np.asarray([self.ent[k][1] for k in ks], dtype=np.int64),
+                np.asarray([self.ent[k][2] for k in ks], dtype=bool), vals)
+
+    def checksum(self) -> int:
+        return content_checksum(*self.arrays())
+
+    def digest(self) -> str:
+        return canonical_digest(*self.arrays())
+
+
+def shard_of(tables, rows, num_shards: int) -> np.ndarray:
+    """fnv1a64(t, r) mod num_shards (store.py:80-88, 100-104)."""
+    return (fnv_cols(tables, rows) % np.uint64(num_shards)).astype(np.int64)
 
 
 # ------------------------------------------------------------- Algorithm 1

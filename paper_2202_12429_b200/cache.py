@@ -18,7 +18,7 @@ import torch
 from . import _lib as L
 from .device import DeviceSchema, _wrap_device
 from .errors import CacheCapacityError, CacheOrderingError, ConfigurationError
-from .traces import EmbeddingKey, unpack_key, unpack_keys
+from .traces import EmbeddingKey, unpack_keys
 
 
 class DynamicCache:
@@ -240,18 +240,23 @@ class DynamicCache:
         return int(out.cpu().numpy()[0])
 
     def canonical_digest(self) -> str:
-        """blake2b over key-sorted (table, row, ttl, dirty, value) entries."""
+        """blake2b over key-sorted (table, row, ttl, dirty, value) entries
+        (reference cache.py:274-286): the records are laid out as one <i8 x 4 +
+        <f4 x D structured array, so a single update hashes the same bytes as
+        the reference's per-entry updates."""
         slots, keys = self._resident()
         order = np.argsort(keys, kind="stable")
-        slots, keys = slots[order], keys[order]
-        ttl = self.ttl.cpu().numpy()
-        dirty = self.dirty.cpu().numpy()
-        values = self.values.cpu().numpy()
+        slots, keys = slots[order], np.asarray(keys, dtype=np.uint64)[order]
+        rec = np.zeros(keys.size, dtype=[("h", "<i8", (4,)), ("v", "<f4", (self.emb_dim,))])
+        if keys.size:
+            d_slots = torch.from_numpy(np.asarray(slots, dtype=np.int64)).cuda()
+            rec["h"][:, 0] = (keys >> np.uint64(44)).astype(np.int64)
+            rec["h"][:, 1] = (keys & np.uint64((1 << 44) - 1)).astype(np.int64)
+            rec["h"][:, 2] = self.ttl[d_slots].cpu().numpy()
+            rec["h"][:, 3] = self.dirty[d_slots].cpu().numpy()
+            rec["v"] = self.values[d_slots].cpu().numpy()
         h = hashlib.blake2b(digest_size=16)
-        for s, k in zip(slots, keys):
-            key = unpack_key(int(k))
-            h.update(np.array([key.table_id, key.row_id, int(ttl[s]), int(dirty[s])], dtype="<i8").tobytes())
-            h.update(values[s].astype("<f4").tobytes())
+        h.update(rec.tobytes())
         return h.hexdigest()
 
 

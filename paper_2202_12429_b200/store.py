@@ -45,6 +45,14 @@ def initial_values(schema: Schema, seed: int, tables, rows) -> np.ndarray:
     return out.cpu().numpy()
 
 
+def shard_of_keys(tables, rows, num_shards: int) -> np.ndarray:
+    """Shard index of every (table, row): fnv1a64(t, r) mod num_shards
+    (reference store.py:80-88, 100-104).  Placement only -- it never changes
+    a value -- so it stays host arithmetic."""
+    h = fnv1a64_u64_arrays(np.asarray(tables, dtype=np.uint64), np.asarray(rows, dtype=np.uint64))
+    return (h % np.uint64(num_shards)).astype(np.int64)
+
+
 class ShardedStore:
     """All tables behind fetch / write-back; values in pinned host memory."""
 
@@ -85,8 +93,7 @@ class ShardedStore:
 
     # -- placement -----------------------------------------------------------
     def shard_of(self, key: EmbeddingKey) -> int:
-        h = fnv1a64_u64_arrays(np.asarray([key[0]], dtype=np.uint64), np.asarray([key[1]], dtype=np.uint64))
-        return int(h[0] % np.uint64(self.num_shards))
+        return int(shard_of_keys([key[0]], [key[1]], self.num_shards)[0])
 
     # -- key validation (reference store.py:90-98) ---------------------------
     def _ids(self, keys) -> np.ndarray:

@@ -253,6 +253,139 @@ def gen_ck(iterations=12):
     return batches
 
 
+def _bits(a) -> list:
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).tolist()
+
+
+def _b64(a, dtype) -> str:
+    import base64
+
+    return base64.b64encode(np.ascontiguousarray(a, dtype=dtype).tobytes()).decode()
+
+
+def gen_api():
+    """Pins of the remaining public API rows: DynamicCache
+    content_checksum / canonical_digest / evict_expired / drain
+    (cache.py:214-286), the trainer object wrappers (trainer.py:56-179),
+    ShardedStore.shard_of (store.py:80-88) and the plan text format with the
+    CLI's worked-example records (lookahead.py:162-189, tests/test_cli.py:97-103).
+    Every input of a scenario is recorded next to its outputs, so the tests
+    replay exactly these operations."""
+    from embcache.cache import DynamicCache
+    from embcache.lookahead import parse_plan
+    from embcache.store import ShardedStore
+    from embcache.trainer import (StubModelConfig, apply_updates, combine_gradients, local_gradients,
+                                  split_sync_sets)
+
+    out = {}
+    rng = np.random.default_rng(2024)
+
+    def cache_state(c, compact=False):
+        st = {"len": len(c), "checksum": c.content_checksum(), "digest": c.canonical_digest()}
+        if not compact:
+            keys = sorted(c.key_set())
+            st.update(ttl=[c.ttl_of(k) for k in keys], dirty=[c.is_dirty(k) for k in keys],
+                      keys=[packed(k) for k in keys])
+        return st
+
+    def released(items, compact):
+        if compact:  # large scenario: count + sha256 over (keys u64, value bits, dirty u8)
+            return {"n": len(items), "sha": sha(np.asarray([packed(k) for k, _, _ in items], dtype="<u8"),
+                                                 np.asarray([v for _, v, _ in items], dtype="<f4"),
+                                                 np.asarray([d for _, _, d in items], dtype=np.uint8))}
+        return [[packed(k), _bits(v), bool(d)] for k, v, d in items]
+
+    # -- cache scenarios: a small hand-sized one and a 3,000-entry one
+    for name, cap, dim, n, tables in (("small", 16, 4, 9, 3), ("large", 4096, 16, 2000, 5)):
+        c = DynamicCache(cap, dim)
+        keyset = set()
+        while len(keyset) < n:
+            keyset.add((int(rng.integers(0, tables)), int(rng.integers(0, 50 * n))))
+        keys = sorted(EmbeddingKey(t, r) for t, r in keyset)
+        vals = rng.standard_normal((n, dim)).astype(np.float32)
+        ttls = rng.integers(0, 6, size=n).tolist()
+        half = n // 2
+        ops = {"keys": [packed(k) for k in keys], "values": _b64(vals, "<f4"), "ttls": ttls, "half": half}
+        c.apply_prefetch(keys[:half], vals[:half], {k: t for k, t in zip(keys[:half], ttls[:half])})
+        c.apply_prefetch(keys[half:], vals[half:], {k: t for k, t in zip(keys[half:], ttls[half:])})
+        sc = {"capacity": cap, "dim": dim, "ops": ops, "after_prefetch": cache_state(c, name == "large")}
+        upd_idx = sorted(rng.choice(n, size=max(1, n // 3), replace=False).tolist())
+        new_ttl = rng.integers(2, 9, size=len(upd_idx)).tolist()
+        c.apply_ttl_updates([(keys[i], t) for i, t in zip(upd_idx, new_ttl)])
+        ops["ttl_updates"] = [upd_idx, new_ttl]
+        row_idx = sorted(rng.choice(n, size=max(1, n // 2), replace=False).tolist())
+        slots = c.resolve_slots([keys[i] for i in row_idx])
+        new_rows = rng.standard_normal((len(row_idx), dim)).astype(np.float32)
+        mask = rng.integers(0, 2, size=len(row_idx)).astype(bool)
+        c.update_rows(slots, new_rows, mask)
+        ops["update_rows"] = [row_idx, _b64(new_rows, "<f4"), mask.astype(int).tolist()]
+        wl = keys[n - 1]
+        wl_val = rng.standard_normal(dim).astype(np.float32)
+        c.write_local_update(wl, wl_val)
+        ops["write_local"] = [n - 1, _bits(wl_val)]
+        sc["after_update"] = cache_state(c, name == "large")
+        sc["evict_2"] = released(c.evict_expired(2), name == "large")
+        sc["after_evict"] = cache_state(c, name == "large")
+        sc["drain"] = released(c.drain(), name == "large")
+        sc["after_drain"] = cache_state(c, name == "large")
+        sc["counters"] = {"insertions": c.insertions, "evictions": c.evictions, "peak": c.peak_occupancy}
+        out[f"cache_{name}"] = sc
+
+    # -- trainer object wrappers (3 ranks, overlapping keys, one empty rank)
+    cfgm = StubModelConfig(lr=0.05, c_value=0.01, c_label=0.001)
+    dim = 4
+    universe = [EmbeddingKey(t, r) for t in range(2) for r in range(6)]
+    values = {k: rng.standard_normal(dim).astype(np.float32) for k in universe}
+    ranks = []
+    for r in range(3):
+        exs = []
+        for i in range(0 if r == 1 else 5):
+            sparse = tuple(universe[j] for j in rng.choice(len(universe), size=2, replace=False))
+            exs.append(Example(int(rng.integers(0, 2)), (), sparse))
+        ranks.append(exs)
+    per_trainer = [local_gradients(exs, values, cfgm) for exs in ranks]
+    combined = combine_gradients(per_trainer)
+    c = DynamicCache(32, dim)
+    ukeys = sorted(values)
+    c.apply_prefetch(ukeys, np.stack([values[k] for k in ukeys]), {k: 9 for k in ukeys})
+    # one zero-gradient key: must stay clean (trainer.py:149-165)
+    zero_key = next(k for k in ukeys if k not in combined)
+    combined_z = dict(combined)
+    combined_z[zero_key] = np.zeros(dim, dtype=np.float32)
+    updated = apply_updates(c, combined_z, cfgm)
+    nxt = set(universe[::3])
+    crit, bg = split_sync_sets(updated, nxt)
+    out["trainer"] = {
+        "cfg": [cfgm.lr, cfgm.c_value, cfgm.c_label], "dim": dim,
+        "values": [[packed(k), _bits(values[k])] for k in ukeys],
+        "ranks": [[[ex.label, [packed(k) for k in ex.sparse]] for ex in exs] for exs in ranks],
+        "local": [[[packed(k), _bits(v)] for k, v in g.items()] for g in per_trainer],
+        "combined": [[packed(k), _bits(v)] for k, v in combined.items()],
+        "zero_key": packed(zero_key), "updated": sorted(packed(k) for k in updated),
+        "after_apply": cache_state(c),
+        "next": sorted(packed(k) for k in nxt), "critical": [packed(k) for k in crit],
+        "background": [packed(k) for k in bg]}
+
+    # -- shard placement
+    schema = Schema(4, (1000, 50, 7, 100000), 0, 4)
+    tk = [(int(rng.integers(0, 4)), 0) for _ in range(40)]
+    tk = [(t, int(rng.integers(0, schema.rows_per_table[t]))) for t, _ in tk]
+    out["shard_of"] = {"schema": [4, list(schema.rows_per_table), 0, 4], "keys": [packed(EmbeddingKey(*x)) for x in tk],
+                       "shards": {str(ns): [ShardedStore(schema, ns, 3).shard_of(EmbeddingKey(*x)) for x in tk]
+                                  for ns in (1, 3, 4, 7, 16)}}
+
+    # -- plan text format: the CLI worked-example records and the small fixture
+    worked = [make_batch(1, [3, 9]), make_batch(2, [3, 4]), make_batch(3, [3, 6]), make_batch(4, [1, 6])]
+    wplans, _ = plan_stream(worked, 2, 100)
+    _, small = small_fixture()
+    splans, _ = plan_stream(small, 8, 5000)
+    lines = [format_plan(p) for p in splans[:12]]
+    parsed = [plan_record(parse_plan(ln)) for ln in lines]
+    out["plan_text"] = {"worked": [format_plan(p) for p in wplans], "small_L8": lines, "small_L8_parsed": parsed,
+                        "empty": format_plan(parse_plan("iter=7 prefetch= ttl="))}
+    dump("api.json", out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
@@ -263,6 +396,8 @@ def main():
         gen_hashing()
     if want("engine"):
         gen_planner_and_engine()
+    if want("api"):
+        gen_api()
     if want("acceptance"):
         gen_acceptance()
     ck = gen_ck() if want("ck") else None
