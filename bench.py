@@ -62,13 +62,14 @@ FLUSH_EXCLUSIVE = int(os.environ.get("BAGPIPE_B200_BENCH_FLUSH_EXCLUSIVE", "0"))
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=8, help="oracle steps timed for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dlrm", action="store_true")
+    ap.add_argument("--no-link-probe", action="store_true", help="skip the host-link-disabled comparison run")
     ap.add_argument("--seed", type=int, default=1)
     return ap.parse_args()
 
@@ -84,6 +85,19 @@ def make_batches(n_batches: int, seed: int, batch: int = BATCH):
 
     rows, labels, dense = generate_columns(ZipfSpec(schema(), ZIPF, n_batches * batch, seed))
     return batchify_columns(rows, labels, dense, batch)
+
+
+def bench_config(world: int) -> dict:
+    """The workload of one bench line, identical in both arms (ours and
+    --impl reference) for the same N."""
+    sc_rows = sum(CK_ROWS)
+    return {"workload": WORKLOAD, "global_batch": BATCH * world, "per_gpu_batch": BATCH, "tables": len(CK_ROWS),
+            "rows": sc_rows, "emb_dim": DIM, "cache_capacity_per_gpu": sc_rows // 100, "lookahead": "auto",
+            "parallelism": "single" if world == 1 else f"table-sharded x{world} (weak: {BATCH} examples/GPU)",
+            "num_trainers": world,
+            "l2": "flushed at the start of every timed iteration (256 MiB write inside the timed span)",
+            "timing": "one CUDA-event span over K steps, end event after joining the plan and host-link streams",
+            "mode": "stub-gradient (bit-exact)"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -171,6 +185,47 @@ def count_launches(pipe, pos: int) -> int:
     return n
 
 
+# Kernels of the batch prep and of the Oracle Cacher planner (roofline_planner)
+PREP_KERNELS = ("k_col_cluster_prep", "k_first_order", "k_occ_k_from_s", "k_prep_", "k_radix", "k_scan_onepass",
+                "k_set_rank_bounds")
+PLANNER_KERNELS = ("k_refill", "k_pop_fused")
+
+
+def kernel_times(pipe, first: int, k: int) -> dict:
+    """Device time per step of every kernel of our library over k engine
+    steps (CUPTI through the torch profiler): {kernel name: us per step}."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(k):
+            pipe.step(first + i, early=i < k - 1)
+        torch.cuda.synchronize()
+    out = {}
+    for ev in prof.events():
+        name = ev.name or ""
+        if ev.device_type == torch.autograd.DeviceType.CUDA and ("bp::" in name or name.startswith("k_")):
+            key = name.split("(")[0].replace("void ", "").replace("bp::", "")
+            out[key] = out.get(key, 0.0) + ev.device_time / k
+    return out
+
+
+def prep_bytes(n_occ: int, u: int) -> int:
+    """Algorithmic bytes of one batch prep: keys + labels
+    read (9 B/occurrence), sorted positions + label bytes written (5 B), per
+    unique key the sorted key, id, first-order key, both permutations and the
+    CSR offset (32 B)."""
+    return n_occ * 14 + u * 32
+
+
+def planner_bytes(u: int, p: int, e: int) -> int:
+    """Algorithmic bytes of refill + pop (SURVEY 8d planner row): tracker and
+    flag updates of the batch entering the window (13 B/unique), the pop's
+    tracker/flag reads + TTL and flag writes (21 B/unique), prefetch key/id/ttl
+    (20 B each) and evict key/id (12 B each)."""
+    return u * 34 + p * 20 + e * 12
+
+
 def _timed_steps(pipe, first: int, steps: int, flush_buf, torch, exclusive: int | None = None):
     """K steps as ONE span on the engine's compute stream, bracketed by
     device syncs: CUDA events, the end event recorded after the compute
@@ -255,7 +310,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     sc = schema()
     cap = sc.total_rows // 100
     steps, warm = args.steps, args.warmup
-    n_batches = warm + 2 * steps + 12
+    link_probe = not args.no_link_probe
+    n_batches = warm + (3 if link_probe else 2) * steps + 16
     # N>1 (weak scaling, the DLRM convention of a fixed per-GPU batch): the
     # global batch is N x 16,384 examples, its 26 tables dealt over the ranks;
     # every rank runs the whole pipeline for its tables of every example --
@@ -306,8 +362,22 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     # the same K steps with every engine stream drained around each flush
     # (no overlap across iterations): reported beside the value
     ms_excl, _ = _timed_steps(pipe, warm + steps + 9, steps, flush_buf, torch, exclusive=1)
+    nxt = warm + 2 * steps + 9
+    ktimes = kernel_times(pipe, nxt, 4)
+    nxt += 4
+    # host link: the same steps with the store's fetch and write-back kernels
+    # turned into no-ops (results become wrong; timing only).  The difference
+    # is the part of the host link NOT hidden behind the compute stream.
+    ms_nolink = None
+    if link_probe:
+        L.check(pipe.lib.bp_debug_skip_link(3), "bp_debug_skip_link")
+        try:
+            ms_nolink, _ = _timed_steps(pipe, nxt, steps, flush_buf, torch)
+        finally:
+            L.check(pipe.lib.bp_debug_skip_link(0), "bp_debug_skip_link")
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     pf_mean = statistics.mean(r.prefetch_count for r in records)
+    ev_mean = statistics.mean(r.evicted_count for r in records)
     n_occ = gbatch * len(tables)
     link_rows = np.zeros(2, dtype=np.int64)  # lazy prefetch over the run: host-link reads, GPU-computed inits
     pipe.lib.bp_store_link_counters(pipe.store.handle, link_rows.ctypes.data)
@@ -354,6 +424,24 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    pl_prep_us = sum(v for k, v in ktimes.items() if k.startswith(PREP_KERNELS))
+    pl_plan_us = sum(v for k, v in ktimes.items() if k.startswith(PLANNER_KERNELS))
+    pl_bytes = prep_bytes(n_occ, int(u_mean)) + planner_bytes(int(u_mean), int(pf_mean), int(ev_mean))
+    pl_ms = (pl_prep_us + pl_plan_us) * 1e-3
+    roofline_planner = {
+        "kernel": "batch prep (bp::k_col_cluster_prep + k_first_order) + Oracle Cacher (bp::k_refill + k_pop_fused)",
+        "bound": "hbm (latency-bound: sort, scans, dependent random reads of the per-key planner state)",
+        "bytes_per_step": pl_bytes, "ms_per_step": pl_ms, "unit": "GB/s",
+        "achieved": pl_bytes / (pl_ms * 1e-3) / 1e9 if pl_ms else 0.0, "peak": None,
+        "kernels_us_per_step": {k: round(v, 2) for k, v in ktimes.items()
+                                if k.startswith(PREP_KERNELS + PLANNER_KERNELS)},
+        "prep_us": pl_prep_us, "planner_us": pl_plan_us,
+        "stage_span_ms": {"prep": stages["prep"][0], "planner": stages["planner"][0]},
+        "timing": "CUPTI device time of the kernels over 4 engine steps; stage_span_ms = the engine's event "
+                  "spans around the enqueue (include host enqueue gaps)",
+        "note": "bytes: prep 14 B/occurrence + 32 B/unique, planner 34 B/unique + 20 B/prefetch + 12 B/evict "
+                "(DESIGN.md section 3)"}
+    roofline_planner.update(peak=hbm_peak, frac=roofline_planner["achieved"] / hbm_peak, peak_source=peak_src)
     stub_total, stub_launches = stages["trainer"]
     stub_ms = stub_total / max(stub_launches, 1e-9)
     stub_bytes = stub_step_bytes(n_occ, int(u_mean))
@@ -363,6 +451,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     out = {
         "metric": METRIC,
         "value": samples / (ms_max * 1e-3),
+        "value_kind": "stub-gradient engine samples/s (the reference's own run_pipeline arithmetic, bit-exact; "
+                      "the like-for-like comparison with the CPU reference, SURVEY 8d) -- DLRM-mode samples/s "
+                      "with MLPs is under 'dlrm'",
         "unit": "samples/s",
         "n_gpus": world,
         "steps": steps,
@@ -373,18 +464,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (reference Zipf generator stream, columnar)",
-        "config": {"workload": WORKLOAD, "global_batch": gbatch, "per_gpu_batch": BATCH, "tables": 26,
-                   "rows": sc.total_rows,
-                   "emb_dim": DIM, "cache_capacity_per_gpu": cap, "lookahead": lookahead0,
-                   "parallelism": "single" if world == 1 else f"table-sharded x{world} (weak: {BATCH} examples/GPU)",
-                   "num_trainers": trainers,
-                   "l2": "flushed at the start of every timed iteration by the engine (256 MiB memset on the compute "
-                         "stream, inside the timed span; " + ("plan and host-link streams fenced around it"
-                                                              if FLUSH_EXCLUSIVE else
-                                                              "plan and host-link streams keep running: the pipeline "
-                                                              "stays overlapped across iterations") + ")",
-                   "timing": "one CUDA-event span over K steps, end event after joining the plan and host-link streams",
-                   "mode": "stub-gradient (bit-exact)"},
+        "config": bench_config(world),
+        "lookahead_resolved": lookahead0,
         "e2e": None if args.no_e2e else {"value": samples / (e2e_max * 1e-3), "unit": "samples/s",
                                          "h2d_bytes_per_step": n_occ * 9, "d2h_bytes_per_step": 12 * 8 + 32},
         "roofline_stub_trainer": {"kernel": "bp::k_stub_step(+_long): fused gather + backward + rank-ordered combine"
@@ -393,10 +474,23 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                                   "frac": stub_achieved / hbm_peak, "bytes_per_launch": stub_bytes,
                                   "ms_per_launch": stub_ms, "peak_source": peak_src},
         "stages_ms_per_step": {k: v[0] for k, v in stages.items()},
+        "roofline_planner": roofline_planner,
         "host_link": {"prefetch_rows_per_step": pf_mean,
                       "prefetch_host_read_frac": host_frac,
                       "prefetch_link_gbs": pf_mean * host_frac * 64 / (fetch_total * 1e-3) / 1e9
                       if fetch_total else None,
+                      "prefetch_peak_gbs": 19.5, "prefetch_peak_note": "zero-copy random 64 B rows",
+                      "writeback_rows_per_step": ev_mean,
+                      "writeback_link_gbs": ev_mean * DIM * 4 / (stages["flush"][0] * 1e-3) / 1e9
+                      if stages["flush"][0] else None,
+                      "writeback_peak_gbs": 56.5, "writeback_peak_note": "pinned memcpy D2H (copy-engine log append)",
+                      "ms_per_step_link_disabled": None if ms_nolink is None else ms_nolink / steps,
+                      "link_ms_per_step": stages["fetch"][0] + stages["flush"][0],
+                      "hidden": None if ms_nolink is None else
+                      max(0.0, min(1.0, 1.0 - max(0.0, ms - ms_nolink) / steps /
+                                   max(stages["fetch"][0] + stages["flush"][0], 1e-9))),
+                      "hidden_note": "1 - (ms/step with the host link - ms/step with the store's fetch and "
+                                     "write-back kernels disabled) / (fetch + write-back stage ms/step)",
                       "prefetch_note": "rows never written back are computed on the GPU (functional init, "
                                        "store.py:106-129); only written rows are read over the host link",
                       "peak_note": "pinned memcpy 55.5 GB/s H2D, 56.5 D2H; zero-copy random 64 B rows 18.7-25 GB/s "
@@ -565,7 +659,7 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (reference Zipf generator stream, columnar)",
-                "config": {"workload": WORKLOAD, "global_batch": BATCH, "parallelism": "cpu"},
+                "config": bench_config(world if world > 1 else args.gpus),
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)

@@ -589,6 +589,16 @@ int bp_debug_long_trace(void* d_buf);
 int bp_debug_bwd_variant(int32_t variant);
 /* Debug: EmbeddingBag single-key forward shape (0 occurrence-order gather, 1 key-sorted scatter). */
 int bp_debug_fwd_variant(int32_t variant);
+/* Debug: columnar batch prep on thread-block clusters (1, default) or the
+ * per-column single-CTA sort (0); outputs are identical. */
+int bp_debug_prep_cluster(int32_t on);
+/* Tuning: smallest items per thread of the cluster prep (4, 8 default, 16). */
+int bp_debug_prep_shape(int32_t ipt_min);
+/* Debug: %globaltimer phase stamps of one kernel into d_buf (NULL disables):
+ * which 0 = the cluster prep [column][16 CTAs][16], 1 = the fused planner pop
+ * [tile][8] (tools/planner_bench.py --trace). */
+int bp_debug_phase_trace(int32_t which, void* d_buf);
+int bp_debug_pop_trace(void* d_buf);
 /* Debug: bit 0 turns the store's fetch kernels, bit 1 its write kernels into
  * no-ops (results become wrong; only for measuring the host link's share). */
 int bp_debug_skip_link(int32_t skip);

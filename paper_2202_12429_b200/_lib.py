@@ -232,6 +232,10 @@ _SIGS = {
                                                   c_vp, c_vp, c_i64, c_vp]),
     "bp_debug_bwd_variant": (c_i32, [c_i32]),
     "bp_debug_fwd_variant": (c_i32, [c_i32]),
+    "bp_debug_prep_cluster": (c_i32, [c_i32]),
+    "bp_debug_prep_shape": (c_i32, [c_i32]),
+    "bp_debug_phase_trace": (c_i32, [c_i32, c_vp]),
+    "bp_debug_pop_trace": (c_i32, [c_vp]),
     "bp_embbag_backward_sorted": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32, c_f32, c_vp,
                                           c_vp]),
     "bp_dlrm_interact_backward_rows": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp,
@@ -297,6 +301,12 @@ def lib() -> C.CDLL:
                 fv = os.environ.get("BAGPIPE_B200_FWD_VARIANT")  # tuning knob: EmbeddingBag forward shape
                 if fv:
                     check(lb.bp_debug_fwd_variant(int(fv)), "bp_debug_fwd_variant")
+                ps = os.environ.get("BAGPIPE_B200_PREP_IPT")  # tuning knob: cluster prep items per thread
+                if ps:
+                    check(lb.bp_debug_prep_shape(int(ps)), "bp_debug_prep_shape")
+                pc = os.environ.get("BAGPIPE_B200_PREP_CLUSTER")  # 0: single-CTA column sort
+                if pc:
+                    check(lb.bp_debug_prep_cluster(int(pc)), "bp_debug_prep_cluster")
                 bv = os.environ.get("BAGPIPE_B200_BWD_VARIANT")  # tuning knob: sorted backward launch shape
                 if bv:
                     check(lb.bp_debug_bwd_variant(int(bv)), "bp_debug_bwd_variant")

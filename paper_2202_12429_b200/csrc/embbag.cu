@@ -1088,6 +1088,259 @@ __global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
   }
 }
 
+// Persistent, pipelined form of k_embbag_bwd_staged (the default): a grid
+// of 2 CTAs per SM walks the tiles t = blockIdx.x + k * gridDim.x with
+// kPipeStages shared-memory stages.  Thread 0 keeps kPipeStages bulk copies
+// (TMA, one mbarrier per stage, phase parity per reuse) in flight, so tile
+// k+1..k+S-1 stream in while tile k is reduced and applied -- the one-shot
+// kernel left every CTA idle on its single copy.  The per-tile work (running
+// segmented sums in shared memory, two-level carry scan, in-place
+// SGD/Adagrad of the keys ending in the tile, partials + arrival counters for
+// spanning keys) is the same, so results are bit-identical.
+constexpr int kPipeStages = 3;
+
+template <int Q>
+__global__ void __launch_bounds__(256, 2) k_embbag_bwd_pipe(
+    const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start, uint32_t n, uint32_t n_tiles,
+    const float4* __restrict__ grad, float* __restrict__ values, int row_stride, const int32_t* __restrict__ slots_s,
+    uint8_t* __restrict__ dirty, int opt, float lr, float eps, float4* __restrict__ parts,
+    unsigned int* __restrict__ arrivals, unsigned long long* __restrict__ stats) {
+  constexpr int T = kStagedF4 / Q, NG = 256 / Q, RPG = T / NG, GW = 32 / Q;
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  float4* tiles_sm = reinterpret_cast<float4*>(st_smem);                          // [S][T][Q]
+  uint32_t* sgs_sm = reinterpret_cast<uint32_t*>(tiles_sm + kPipeStages * T * Q);  // [S][T]
+  int32_t* tslot = reinterpret_cast<int32_t*>(sgs_sm + kPipeStages * T);          // [T]
+  __shared__ __align__(8) uint64_t bar[kPipeStages];
+  __shared__ float4 gcarry[NG][Q];
+  __shared__ float4 wagg[8][Q];
+  __shared__ int wflag[8][Q];
+  __shared__ uint8_t ghead[NG];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t G = gridDim.x;
+  auto issue = [&](uint32_t tile, int st) {  // thread 0: bulk copies of one tile into stage st
+    const uint32_t t0 = tile * T;
+    const uint32_t rows = min((uint32_t)T, n - t0);
+    const uint32_t gbytes = rows * Q * 16, seg_bytes = (rows / 4) * 16;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[st])),
+                 "r"(gbytes + seg_bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(tiles_sm + (size_t)st * T * Q)),
+                 "l"(grad + (size_t)t0 * Q), "r"(gbytes), "r"(smem_u32(&bar[st]))
+                 : "memory");
+    if (seg_bytes)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(sgs_sm + (size_t)st * T)),
+                   "l"(seg_of + t0), "r"(seg_bytes), "r"(smem_u32(&bar[st]))
+                   : "memory");
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int st = 0; st < kPipeStages; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[st])));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (int st = 0; st < kPipeStages; ++st)
+      if (blockIdx.x + st * G < n_tiles) issue(blockIdx.x + st * G, st);
+  }
+  __syncthreads();
+  const int c = (int)(tid % Q), gi = (int)(tid / Q), w = (int)(tid >> 5), gw = (int)((tid & 31) / Q);
+  const uint32_t r0 = gi * RPG;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  unsigned my_nz = 0;
+  uint32_t k = 0;
+  for (uint32_t tile_id = blockIdx.x; tile_id < n_tiles; tile_id += G, ++k) {
+    const int st = (int)(k % kPipeStages);
+    const uint32_t phase = (k / kPipeStages) & 1u;
+    float4* tile = tiles_sm + (size_t)st * T * Q;
+    uint32_t* sgs = sgs_sm + (size_t)st * T;
+    const uint32_t t0 = tile_id * T;
+    const uint32_t rows = min((uint32_t)T, n - t0);
+    const uint32_t seg_bytes = (rows / 4) * 16;
+    // while the copy is in flight: run bounds, slots of the tile's keys (rows
+    // pulled into L2 for the update), the < 4 tail segment ids
+    const uint32_t tile_first = seg_of[t0], tile_last = seg_of[t0 + rows - 1];
+    const uint32_t fa = seg_start[tile_first], fb = seg_start[tile_first + 1];
+    const uint32_t la = seg_start[tile_last], lb = seg_start[tile_last + 1];
+    const uint32_t nu = tile_last - tile_first + 1;
+    for (uint32_t i = tid; i < nu; i += 256) {
+      const int32_t sl = slots_s[tile_first + i];
+      tslot[i] = sl;
+      if (sl >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(values + (size_t)sl * row_stride));
+    }
+    if (tid < rows - seg_bytes / 4) sgs[seg_bytes / 4 + tid] = seg_of[t0 + seg_bytes / 4 + tid];
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT%=;\n}\n" ::"r"(
+            smem_u32(&bar[st])),
+        "r"(phase)
+        : "memory");
+    __syncthreads();
+    // pass 1: running segmented sums of the group's rows, in place
+    float4 acc = zero;
+    bool flag = false;
+    if (r0 < rows) {
+      uint32_t ps = sgs[r0];
+      acc = tile[r0 * Q + c];
+      flag = r0 == 0 || sgs[r0 - 1] != ps;
+      if (c == 0) ghead[gi] = flag ? 1 : 0;
+      const uint32_t re = min(r0 + RPG, rows);
+      for (uint32_t r = r0 + 1; r < re; ++r) {
+        const uint32_t sr = sgs[r];
+        const float4 x = tile[r * Q + c];
+        if (sr == ps) {
+          acc = f4_add(acc, x);
+        } else {
+          acc = x;
+          flag = true;
+        }
+        tile[r * Q + c] = acc;
+        ps = sr;
+      }
+    } else if (c == 0) {
+      ghead[gi] = 1;
+    }
+    // pass 2: segmented scan of the group totals; warp level first
+    float4 inc = acc;
+    bool finc = flag;
+#pragma unroll
+    for (int off = 1; off < GW; off <<= 1) {
+      const bool fo = __shfl_up_sync(0xffffffffu, finc ? 1 : 0, off * Q) != 0;
+      float4 o;
+      o.x = __shfl_up_sync(0xffffffffu, inc.x, off * Q);
+      o.y = __shfl_up_sync(0xffffffffu, inc.y, off * Q);
+      o.z = __shfl_up_sync(0xffffffffu, inc.z, off * Q);
+      o.w = __shfl_up_sync(0xffffffffu, inc.w, off * Q);
+      if (gw >= off && !finc) inc = f4_add(o, inc);
+      if (gw >= off) finc = finc || fo;
+    }
+    if (gw == GW - 1) {
+      wagg[w][c] = inc;
+      wflag[w][c] = finc ? 1 : 0;
+    }
+    float4 ex;
+    ex.x = __shfl_up_sync(0xffffffffu, inc.x, Q);
+    ex.y = __shfl_up_sync(0xffffffffu, inc.y, Q);
+    ex.z = __shfl_up_sync(0xffffffffu, inc.z, Q);
+    ex.w = __shfl_up_sync(0xffffffffu, inc.w, Q);
+    const bool fex = __shfl_up_sync(0xffffffffu, finc ? 1 : 0, Q) != 0;
+    __syncthreads();
+    float4 cw = zero;
+    for (int kk = 0; kk < w; ++kk) cw = wflag[kk][c] ? wagg[kk][c] : f4_add(cw, wagg[kk][c]);
+    const float4 carry = gw == 0 ? cw : (fex ? ex : f4_add(cw, ex));
+    gcarry[gi][c] = carry;
+    __syncthreads();
+    const bool span1 = fa < t0 || fb > t0 + rows;
+    const bool span2 = tile_last != tile_first && lb > t0 + rows;
+    // pass 3: (row, column) items; a key's last row in the tile holds its sum
+    bool wrote = false;
+    constexpr int ITEMS = T * Q / 256, B = 4;
+#pragma unroll 1
+    for (int k0 = 0; k0 < ITEMS; k0 += B) {
+      int32_t sl[B];
+      float4 val[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const uint32_t r = (uint32_t)(tid / Q) + (uint32_t)(k0 + u) * NG;
+        sl[u] = -1;
+        if (r >= rows) continue;
+        const uint32_t sg = sgs[r];
+        if (r + 1 < rows && sgs[r + 1] == sg) continue;  // not the last row of its run
+        const int32_t slot = tslot[sg - tile_first];
+        if (slot < 0) continue;
+        const uint32_t g = r / RPG;
+        float4 x = tile[r * Q + c];
+        if (!ghead[g] && sg == sgs[g * RPG]) x = f4_add(gcarry[g][c], x);
+        if (sg == tile_first ? span1 : (sg == tile_last && span2)) {
+          parts[(size_t)(tile_id * 2 + (sg == tile_first ? 0 : 1)) * Q + c] = x;
+          wrote = true;
+          continue;
+        }
+        sl[u] = slot;
+        val[u] = x;
+      }
+      float4 wv[B], av[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const float4* row = reinterpret_cast<const float4*>(values + (size_t)(sl[u] >= 0 ? sl[u] : 0) * row_stride);
+        wv[u] = sl[u] >= 0 ? row[c] : zero;
+        av[u] = (sl[u] >= 0 && opt == BP_OPT_ADAGRAD) ? row[Q + c] : zero;
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        bool nz = false;
+        if (sl[u] >= 0) {
+          const float4 gg = val[u];
+          float4 x = wv[u], a = av[u];
+          x.x = upd1(x.x, a.x, gg.x, opt, lr, eps);
+          x.y = upd1(x.y, a.y, gg.y, opt, lr, eps);
+          x.z = upd1(x.z, a.z, gg.z, opt, lr, eps);
+          x.w = upd1(x.w, a.w, gg.w, opt, lr, eps);
+          float4* row = reinterpret_cast<float4*>(values + (size_t)sl[u] * row_stride);
+          row[c] = x;
+          if (opt == BP_OPT_ADAGRAD) row[Q + c] = a;
+          nz = gg.x != 0.f || gg.y != 0.f || gg.z != 0.f || gg.w != 0.f;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, nz);
+        const unsigned gm = (Q == 32 ? 0xffffffffu : ((1u << Q) - 1u)) << ((tid & 31) / Q * Q);
+        if (sl[u] >= 0 && c == 0 && (bal & gm)) {
+          if (dirty) dirty[sl[u]] = 1;
+          ++my_nz;
+        }
+      }
+    }
+    const int32_t slot_first = tslot[0], slot_last = tslot[nu - 1];
+    if (wrote) __threadfence();  // partials visible device-wide before the arrival count
+    __syncthreads();             // every thread is done with this stage and with tslot
+    if (tid == 0 && tile_id + kPipeStages * G < n_tiles) {
+      // the stage was read and written through the generic proxy: order that
+      // before the async-proxy (TMA) refill
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tile_id + kPipeStages * G, st);
+    }
+    if ((span1 || span2) && w == 0) {
+      // warp 0 counts the arrivals and, when it completed a spanning key,
+      // combines its partials in tile order; the other warps move on
+      unsigned lst = 0;
+      if (tid == 0) {
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          if (!(kk == 0 ? span1 : span2)) continue;
+          if ((kk == 0 ? slot_first : slot_last) < 0) continue;
+          const uint32_t a = kk == 0 ? fa : la, b = kk == 0 ? fb : lb;
+          const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
+          if (atomicAdd(arrivals + ft, 1u) == nt - 1) {
+            lst |= 1u << kk;
+            arrivals[ft] = 0;  // every arrival is in: the counter is free again (persistent scratch)
+          }
+        }
+      }
+      lst = __shfl_sync(0xffffffffu, lst, 0);
+      if (lst) {
+        __threadfence();
+        unsigned n_comb = 0;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          if (!((lst >> kk) & 1u)) continue;
+          const uint32_t a = kk == 0 ? fa : la, b = kk == 0 ? fb : lb;
+          const uint32_t ft = a / T, nt = (b - 1) / T - ft + 1;
+          const int32_t slot = kk == 0 ? slot_first : slot_last;
+          const bool nz = span_combine<Q>(parts, ft, nt, a != ft * T, (int)(tid / Q), c,
+                                          values + (size_t)slot * row_stride, opt, lr, eps);
+          if (__ballot_sync(0xffffffffu, nz) != 0 && tid == 0) {
+            if (dirty) dirty[slot] = 1;
+            ++n_comb;
+          }
+        }
+        if (tid == 0) my_nz += n_comb;
+      }
+    }
+  }
+  if (stats) {
+    for (int off = 16; off > 0; off >>= 1) my_nz += __shfl_down_sync(0xffffffffu, my_nz, off);
+    if ((tid & 31) == 0 && my_nz) atomicAdd(&stats[1], (unsigned long long)my_nz);
+  }
+}
+
 // Keys spanning several tiles, listed by the tile kernels at the key's first
 // tile: up to kSpanWarpTiles tiles (the many keys that merely cross a tile
 // boundary) one warp per key, longer ones (the Zipf-hot rows) one CTA per
@@ -1353,8 +1606,8 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
   return BP_OK;
 }
 
-// debug: the kernel behind bp_embbag_backward_sorted (0: k_embbag_bwd_staged,
-// the default -- measured fastest inside the DLRM step; warp tiles: 1: R=8 x 3
+// debug: the kernel behind bp_embbag_backward_sorted (0: k_embbag_bwd_pipe,
+// the default; 4: the one-shot k_embbag_bwd_staged; warp tiles: 1: R=8 x 3
 // CTAs/SM, 2: R=4 x 4, 3: R=8 x 2)
 static int g_bwd_variant = 0;
 
@@ -1437,7 +1690,8 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
   if (P->n_occ == 0) return BP_OK;
   cudaStream_t s = (cudaStream_t)stream;
   switch (g_bwd_variant) {
-    case 0: {
+    case 0:
+    case 4: {
       const int q = dim / 4, T = kStagedF4 / q;
       const unsigned tiles = (unsigned)((P->n_occ + T - 1) / T);
       const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
@@ -1447,6 +1701,34 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
       float4* parts = reinterpret_cast<float4*>(scratch);
       unsigned int* arrivals = reinterpret_cast<unsigned int*>(scratch + parts_bytes);
       if (!own) BP_CUDA_TRY(cudaMemsetAsync(arrivals, 0, tiles * sizeof(unsigned int), s));
+      if (g_bwd_variant == 0) {
+        const size_t psmem = (size_t)kPipeStages * ((size_t)T * q * sizeof(float4) + (size_t)T * sizeof(uint32_t)) +
+                             (size_t)T * sizeof(int32_t);
+        const unsigned grid = tiles < 2u * kNumSMs ? tiles : 2u * kNumSMs;
+#define BP_BWD_PIPE(QQ)                                                                                        \
+  {                                                                                                            \
+    static bool attr = false;                                                                                  \
+    if (!attr) {                                                                                               \
+      BP_CUDA_TRY(cudaFuncSetAttribute(k_embbag_bwd_pipe<QQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                       (int)psmem));                                                           \
+      attr = true;                                                                                             \
+    }                                                                                                          \
+    k_embbag_bwd_pipe<QQ><<<grid, 256, psmem, s>>>(P->d_seg_of, P->d_seg_start, (uint32_t)P->n_occ, tiles,      \
+                                                   reinterpret_cast<const float4*>(d_grad_sorted), d_values,    \
+                                                   row_stride, d_slots_s, d_dirty, opt, lr, eps, parts,         \
+                                                   arrivals, (unsigned long long*)d_stats);                     \
+  }
+        switch (q) {
+          case 1: BP_BWD_PIPE(1); break;
+          case 2: BP_BWD_PIPE(2); break;
+          case 4: BP_BWD_PIPE(4); break;
+          default: BP_BWD_PIPE(8); break;
+        }
+#undef BP_BWD_PIPE
+        BP_LAUNCH_CHECK();
+        if (!own) cudaFreeAsync(scratch, s);
+        return BP_OK;
+      }
       const size_t smem = (size_t)T * q * sizeof(float4) + 2 * (size_t)T * sizeof(uint32_t);
 #define BP_BWD_STAGED(QQ)                                                                                      \
   {                                                                                                            \

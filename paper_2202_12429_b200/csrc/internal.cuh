@@ -118,4 +118,9 @@ struct bp_prep {
   void* d_arena;
   void *t_ka, *t_kb;
   uint32_t *t_va, *t_vb, *t_hist, *t_head, *t_segx, *t_first_flag, *t_first_rank, *t_partials;
+  // cluster columnar path: per-example first-occurrence masks and look-back
+  // words, zeroed with d_num_long by one memset of zero_bytes
+  uint32_t* t_ex_mask;
+  unsigned long long *t_col_state, *t_tile_state;
+  size_t zero_bytes;
 };

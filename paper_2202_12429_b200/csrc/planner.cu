@@ -12,6 +12,7 @@
 //   pop(batch i):     projected = |tracker|  (recorded before popping)
 //                     ttl(e) = tracker[e]; prefetch iff e not mirrored;
 //                     erase e from tracker+mirror iff ttl == i     (lookahead.py:84-110)
+//                     -- one launch, k_pop_fused
 // Prefetch and evict lists are compactions over the batch's KEY-SORTED
 // uniques, so plan.prefetch comes out sorted without a sort; ttl_updates are
 // scattered to first-occurrence order through the prep permutation.
@@ -43,11 +44,8 @@ struct bp_planner {
   // scratch sized for the largest batch seen
   long long scratch_cap;
   uint32_t* d_ids;
-  uint32_t* d_pf_flag;
-  uint32_t* d_ev_flag;
-  uint32_t* d_pf_pos;
-  uint32_t* d_ev_pos;
-  uint32_t* d_partials;
+  unsigned long long* d_pop_state;  // [2][pop_state_tiles] look-back words of k_pop_fused
+  long long pop_state_tiles;
   cudaStream_t home;
 };
 
@@ -70,86 +68,131 @@ __global__ void k_refill(const uint32_t* __restrict__ ids, const long long* d_U,
   if (lane_id() == 0 && added) atomicAdd((unsigned long long*)&ctr->tracked, added);
 }
 
-__global__ void k_pop_begin(PlannerCounters* ctr, int64_t* counts) {
-  ctr->last_projected = ctr->tracked;
-  if (ctr->tracked > ctr->peak_projected) ctr->peak_projected = ctr->tracked;
-  ctr->resident_before = ctr->in_cache;
-  counts[2] = ctr->tracked;
-  counts[3] = ctr->in_cache;
+// The whole pop of one batch in ONE launch (reference lookahead.py:84-110):
+// per key-sorted unique s the TTL, prefetch and evict decisions, then the two
+// compactions by a block scan of the (prefetch, evict) flag pair plus one
+// decoupled look-back per list (prefetch comes out key-sorted, evict too).
+// The CTA owning the last tile reads the totals from its inclusive prefixes
+// and does the scalar bookkeeping (projected occupancy before the pop,
+// counters after it) -- no memset, no one-thread kernels, no flag arrays.
+constexpr int kPopThreads = 256;
+constexpr int kPopIpt = 4;
+constexpr int kPopTile = kPopThreads * kPopIpt;
+__device__ unsigned long long* g_pop_trace = nullptr;  // debug: [tile][8] %globaltimer stamps
+
+__device__ __forceinline__ unsigned long long pop_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
-__global__ void k_pop(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ perm_s2k,
-                      const long long* d_U, long long iteration, const long long* __restrict__ last,
-                      uint8_t* __restrict__ flags, int64_t* __restrict__ ttl_k, uint32_t* __restrict__ pf_flag,
-                      uint32_t* __restrict__ ev_flag) {
+__global__ void __launch_bounds__(kPopThreads) k_pop_fused(
+    const uint32_t* __restrict__ ids, const uint32_t* __restrict__ perm_s2k, const long long* d_U,
+    long long iteration, long long* __restrict__ last, uint8_t* __restrict__ flags, int64_t* __restrict__ ttl_k,
+    const uint64_t* __restrict__ keys_s, uint64_t* __restrict__ pf_keys, uint32_t* __restrict__ pf_ids,
+    int64_t* __restrict__ pf_ttls, uint64_t* __restrict__ ev_keys, uint32_t* __restrict__ ev_ids,
+    unsigned long long* st_pf, unsigned long long* st_ev, uint32_t epoch, PlannerCounters* ctr, int64_t* counts) {
+  __shared__ uint32_t sh_warp[kPopThreads / 32];
+  __shared__ uint32_t sh_pfx[2];
   const long long U = *d_U;
-  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < U; s += (long long)gridDim.x * blockDim.x) {
-    const uint32_t id = ids[s];
-    const long long ttl = last[id];
-    ttl_k[perm_s2k[s]] = ttl;
-    const uint8_t f = flags[id];
-    const bool pf = !(f & kMirrored);
-    const bool ev = ttl == iteration;
-    flags[id] = ev ? (uint8_t)0 : (uint8_t)(f | kMirrored);
-    pf_flag[s] = pf;
-    ev_flag[s] = ev;
+  const long long tile = blockIdx.x;
+  const long long base = tile * kPopTile;
+  const long long n_tiles = U > 0 ? (U + kPopTile - 1) / kPopTile : 1;
+  if (tile >= n_tiles) return;
+  unsigned long long* tr = g_pop_trace ? g_pop_trace + tile * 8 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = pop_timer();
+  uint32_t pf_bits = 0, ev_bits = 0;
+  long long ttl[kPopIpt];
+  uint32_t id[kPopIpt], k2[kPopIpt];
+  uint8_t f[kPopIpt];
+  // two dependent rounds of loads, each with every item in flight: the
+  // stores into flags below would otherwise order each item's loads after
+  // the previous item's store
+#pragma unroll
+  for (int q = 0; q < kPopIpt; ++q) {
+    const long long s = base + (long long)threadIdx.x * kPopIpt + q;
+    id[q] = s < U ? __ldg(ids + s) : 0u;
+    k2[q] = s < U ? __ldg(perm_s2k + s) : 0u;
   }
-}
-
-__global__ void k_pop_compact(const uint32_t* __restrict__ pf_flag, const uint32_t* __restrict__ ev_flag,
-                              const uint32_t* __restrict__ pf_pos, const uint32_t* __restrict__ ev_pos,
-                              const long long* d_U, const uint64_t* __restrict__ keys_s,
-                              const uint32_t* __restrict__ ids, const uint32_t* __restrict__ perm_s2k,
-                              const int64_t* __restrict__ ttl_k, uint64_t* __restrict__ pf_keys,
-                              uint32_t* __restrict__ pf_ids, int64_t* __restrict__ pf_ttls,
-                              uint64_t* __restrict__ ev_keys, uint32_t* __restrict__ ev_ids) {
-  const long long U = *d_U;
-  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < U; s += (long long)gridDim.x * blockDim.x) {
-    if (pf_flag[s]) {
-      const uint32_t p = pf_pos[s];
-      pf_keys[p] = keys_s[s];
-      pf_ids[p] = ids[s];
-      pf_ttls[p] = ttl_k[perm_s2k[s]];
-    }
-    if (ev_flag[s]) {
-      if (ev_keys) ev_keys[ev_pos[s]] = keys_s[s];
-      if (ev_ids) ev_ids[ev_pos[s]] = ids[s];
+#pragma unroll
+  for (int q = 0; q < kPopIpt; ++q) {
+    const long long s = base + (long long)threadIdx.x * kPopIpt + q;
+    ttl[q] = s < U ? last[id[q]] : 0;
+    f[q] = s < U ? flags[id[q]] : (uint8_t)0;
+  }
+#pragma unroll
+  for (int q = 0; q < kPopIpt; ++q) {
+    const long long s = base + (long long)threadIdx.x * kPopIpt + q;
+    if (s < U) {
+      ttl_k[k2[q]] = ttl[q];
+      const bool pf = !(f[q] & kMirrored);
+      const bool ev = ttl[q] == iteration;
+      flags[id[q]] = ev ? (uint8_t)0 : (uint8_t)(f[q] | kMirrored);
+      pf_bits |= (uint32_t)pf << q;
+      ev_bits |= (uint32_t)ev << q;
     }
   }
-}
-
-__global__ void k_pop_end(PlannerCounters* ctr, int64_t* counts) {
-  const long long npf = counts[0], nev = counts[1];
-  ctr->insertions += npf;
-  ctr->removals += nev;
-  ctr->tracked -= nev;
-  const long long occ = ctr->resident_before + npf;
-  if (occ > ctr->peak_occupancy) ctr->peak_occupancy = occ;
-  ctr->in_cache += npf - nev;
-  ctr->last_prefetch = npf;
-  ctr->last_evict = nev;
-  counts[4] = ctr->in_cache;  // mirror size after this batch: the cache's occupancy after its evictions
+  if (tr && threadIdx.x == 0) tr[1] = pop_timer();
+  // (prefetch count, evict count) of this thread packed as 16 | 16 bits
+  const uint32_t mine = (uint32_t)__popc(pf_bits) | ((uint32_t)__popc(ev_bits) << 16);
+  uint32_t tile_total;
+  const uint32_t excl = block_inclusive_scan_256(mine, sh_warp, &tile_total) - mine;
+  const uint32_t warp = threadIdx.x >> 5;
+  if (tr && threadIdx.x == 0) tr[2] = pop_timer();
+  if (warp < 2) {
+    const uint32_t agg = warp == 0 ? (tile_total & 0xFFFFu) : (tile_total >> 16);
+    const uint32_t pfx = warp_lookback(warp == 0 ? st_pf : st_ev, tile, epoch, agg);
+    if ((threadIdx.x & 31u) == 0) sh_pfx[warp] = pfx;
+  }
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[3] = pop_timer();
+  uint32_t pos_pf = sh_pfx[0] + (excl & 0xFFFFu);
+  uint32_t pos_ev = sh_pfx[1] + (excl >> 16);
+#pragma unroll
+  for (int q = 0; q < kPopIpt; ++q) {
+    const long long s = base + (long long)threadIdx.x * kPopIpt + q;
+    if ((pf_bits >> q) & 1u) {
+      pf_keys[pos_pf] = keys_s[s];
+      pf_ids[pos_pf] = id[q];
+      pf_ttls[pos_pf] = ttl[q];
+      ++pos_pf;
+    }
+    if ((ev_bits >> q) & 1u) {
+      if (ev_keys) ev_keys[pos_ev] = keys_s[s];
+      if (ev_ids) ev_ids[pos_ev] = id[q];
+      ++pos_ev;
+    }
+  }
+  if (tr && threadIdx.x == 0) tr[4] = pop_timer();
+  if (tile == n_tiles - 1 && threadIdx.x == 0) {
+    const long long npf = (long long)sh_pfx[0] + (tile_total & 0xFFFFu);
+    const long long nev = (long long)sh_pfx[1] + (tile_total >> 16);
+    // pop_begin: the projected occupancy is len(tracker) before popping
+    ctr->last_projected = ctr->tracked;
+    if (ctr->tracked > ctr->peak_projected) ctr->peak_projected = ctr->tracked;
+    counts[2] = ctr->tracked;
+    counts[3] = ctr->in_cache;
+    const long long occ = ctr->in_cache + npf;
+    if (occ > ctr->peak_occupancy) ctr->peak_occupancy = occ;
+    ctr->insertions += npf;
+    ctr->removals += nev;
+    ctr->tracked -= nev;
+    ctr->in_cache += npf - nev;
+    ctr->last_prefetch = npf;
+    ctr->last_evict = nev;
+    counts[0] = npf;
+    counts[1] = nev;
+    counts[4] = ctr->in_cache;  // mirror size after this batch
+  }
 }
 
 static int planner_scratch(bp_planner* p, long long n, cudaStream_t s) {
   if (p->scratch_cap >= n) return BP_OK;
-  if (p->scratch_cap) {
-    cudaFreeAsync(p->d_ids, s);
-    cudaFreeAsync(p->d_pf_flag, s);
-    cudaFreeAsync(p->d_ev_flag, s);
-    cudaFreeAsync(p->d_pf_pos, s);
-    cudaFreeAsync(p->d_ev_pos, s);
-    cudaFreeAsync(p->d_partials, s);
-  }
+  if (p->scratch_cap) cudaFreeAsync(p->d_ids, s);
   long long cap = 1024;
   while (cap < n) cap <<= 1;
   p->scratch_cap = cap;
   BP_CUDA_TRY(pool_alloc(&p->d_ids, cap, s));
-  BP_CUDA_TRY(pool_alloc(&p->d_pf_flag, cap, s));
-  BP_CUDA_TRY(pool_alloc(&p->d_ev_flag, cap, s));
-  BP_CUDA_TRY(pool_alloc(&p->d_pf_pos, cap, s));
-  BP_CUDA_TRY(pool_alloc(&p->d_ev_pos, cap, s));
-  BP_CUDA_TRY(pool_alloc(&p->d_partials, scan_state_words(cap), s));
   return BP_OK;
 }
 
@@ -227,15 +270,9 @@ extern "C" int bp_planner_destroy(bp_planner* p) {
   cudaStream_t s = 0;
   if (p->d_last) cudaFreeAsync(p->d_last, s);
   if (p->d_flags) cudaFreeAsync(p->d_flags, s);
-  if (p->scratch_cap) {
-    cudaFreeAsync(p->d_ids, s);
-    cudaFreeAsync(p->d_pf_flag, s);
-    cudaFreeAsync(p->d_ev_flag, s);
-    cudaFreeAsync(p->d_pf_pos, s);
-    cudaFreeAsync(p->d_ev_pos, s);
-    cudaFreeAsync(p->d_partials, s);
-  }
+  if (p->scratch_cap) cudaFreeAsync(p->d_ids, s);
   if (!p->sc) bp::registry_free(&p->reg, s);
+  if (p->d_pop_state) cudaFreeAsync(p->d_pop_state, s);
   cudaFree(p->d_ctr);
   cudaFreeHost(p->h_ctr);
   cudaStreamSynchronize(s);
@@ -259,28 +296,35 @@ extern "C" int bp_planner_refill(bp_planner* p, bp_prep* P, bp_stream_t stream) 
 extern "C" int bp_planner_pop(bp_planner* p, bp_prep* P, const bp_plan_buffers* b, bp_stream_t stream) {
   using namespace bp;
   cudaStream_t s = (cudaStream_t)stream;
-  BP_CUDA_TRY(cudaMemsetAsync(b->d_counts, 0, 2 * sizeof(int64_t), s));
-  k_pop_begin<<<1, 1, 0, s>>>(p->d_ctr, b->d_counts);
+  const uint32_t* ids = nullptr;
   if (P->n_occ > 0) {
-    const uint32_t* ids;
     int rc = planner_ids(p, P, 0, &ids, s);
     if (rc) return rc;
-    rc = planner_scratch(p, P->n_occ, s);
-    if (rc) return rc;
-    const long long n = P->n_occ;
-    const int g = grid_for(n, 256);
-    k_pop<<<g, 256, 0, s>>>(ids, P->d_perm_s2k, P->d_num_unique, P->iteration, p->d_last, p->d_flags, b->d_ttl_k,
-                            p->d_pf_flag, p->d_ev_flag);
-    BP_CUDA_TRY(exclusive_scan(p->d_pf_flag, p->d_pf_pos, n, P->d_num_unique, p->d_partials, nullptr,
-                               (long long*)&b->d_counts[0], s));
-    BP_CUDA_TRY(exclusive_scan(p->d_ev_flag, p->d_ev_pos, n, P->d_num_unique, p->d_partials, nullptr,
-                               (long long*)&b->d_counts[1], s));
-    k_pop_compact<<<g, 256, 0, s>>>(p->d_pf_flag, p->d_ev_flag, p->d_pf_pos, p->d_ev_pos, P->d_num_unique,
-                                    P->d_uniq_key_s, ids, P->d_perm_s2k, b->d_ttl_k, b->d_prefetch_keys,
-                                    b->d_prefetch_ids, b->d_prefetch_ttls, b->d_evict_keys, b->d_evict_ids);
   }
-  k_pop_end<<<1, 1, 0, s>>>(p->d_ctr, b->d_counts);
+  // look-back words of the two compactions: persistent, zeroed once, epoch-tagged
+  const long long nn = P->n_occ > 0 ? P->n_occ : 1;
+  const long long tiles = (nn + kPopTile - 1) / kPopTile;
+  if (p->pop_state_tiles < tiles) {
+    if (p->d_pop_state) cudaFreeAsync(p->d_pop_state, s);
+    long long cap = 64;
+    while (cap < tiles) cap <<= 1;
+    BP_CUDA_TRY(pool_alloc(&p->d_pop_state, 2 * cap * kLookbackStride, s));
+    BP_CUDA_TRY(cudaMemsetAsync(p->d_pop_state, 0, 2 * cap * kLookbackStride * sizeof(unsigned long long), s));
+    p->pop_state_tiles = cap;
+  }
+  k_pop_fused<<<(int)tiles, kPopThreads, 0, s>>>(ids, P->d_perm_s2k, P->d_num_unique, P->iteration, p->d_last,
+                                                 p->d_flags, b->d_ttl_k, P->d_uniq_key_s, b->d_prefetch_keys,
+                                                 b->d_prefetch_ids, b->d_prefetch_ttls, b->d_evict_keys,
+                                                 b->d_evict_ids, p->d_pop_state,
+                                                 p->d_pop_state + p->pop_state_tiles * kLookbackStride,
+                                                 next_scan_epoch(), p->d_ctr,
+                                                 b->d_counts);
   BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
+extern "C" int bp_debug_pop_trace(void* d_buf) {
+  BP_CUDA_TRY(cudaMemcpyToSymbol(bp::g_pop_trace, &d_buf, sizeof(void*)));
   return BP_OK;
 }
 

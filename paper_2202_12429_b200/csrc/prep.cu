@@ -15,13 +15,19 @@
 // bit ranges (rows: [0,row_bits), tables: [44, 44+table_bits)).
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
 
 namespace bp {
 
+// Debug switch (bp_debug_prep_cluster): 0 forces the single-CTA column sort.
+static int g_prep_cluster = 1;
+
 struct ColumnarInfo {
   int n_ex, n_cols, row_bits;
   const int32_t* d_tables;
+  bool cluster;  // k_col_cluster_prep applies (see cs_shape)
 };
 
 __global__ void k_prep_keys_schema(const uint64_t* __restrict__ keys, long long n, const int64_t* base,
@@ -281,8 +287,516 @@ struct RankBounds {
   long long v[kMax];
 };
 
+// ---------------------------------------------------------------------------
+// Columnar prep on thread-block clusters (the default for Criteo-layout
+// batches of up to 65,536 examples and 32 columns).
+//
+// One cluster of CS CTAs (CS = 1..16) sorts one column: CTA r of the cluster
+// owns the column's examples [r*M, (r+1)*M) (M = 256 x IPT).  Elements
+//   e = row << 27 | label << 20 | example
+// live in registers; each 8-bit LSD pass over the column's OWN row bits
+// ranks digits per warp with __match_any_sync (stable), publishes the CTA's
+// 256 digit counts in shared memory, reads every CTA's counts through
+// distributed shared memory (DSMEM) to get the column-wide digit offsets,
+// and scatters each element straight into the shared memory of the CTA that
+// owns its destination slot (st.shared::cluster).  After the last pass CTA r
+// holds sorted positions [r*M, (r+1)*M) of the column -- no global
+// temporaries, no merge pass, and every column occupies CS SMs instead of
+// one.  Small tables take fewer passes (a 3-row table: one; a 1-row table:
+// none).
+//
+// The same kernel then finds segment heads (row != previous row; the
+// neighbour CTA's last element via DSMEM), numbers them with a block scan, a
+// cluster prefix over the CTA totals and a decoupled look-back over the
+// columns (column c's first segment index = distinct keys of columns < c,
+// since dense ids of table t precede those of any later table), and writes
+// every per-occurrence and per-segment output of the prep directly:
+// key-sorted occurrence positions (column c's occurrences are sorted slots
+// [c*n_ex, (c+1)*n_ex): every column holds exactly n_ex occurrences), the
+// label byte with its rank-start bit, CSR offsets, sorted unique keys/ids,
+// and, per first occurrence, its segment index plus one bit in a per-example
+// mask from which k_first_order derives the first-occurrence order.
+// ---------------------------------------------------------------------------
+constexpr int kCsThreads = 256;
+constexpr int kCsWarps = kCsThreads / 32;
+constexpr int kCsRowShift = 27;  // row << 27 | label (7 bits) << 20 | example (20 bits)
+constexpr unsigned long long kCsExMask = (1ull << 20) - 1;
+constexpr int kCsMaxRowBits = 64 - kCsRowShift;
+constexpr int kCsMaxCols = 32;
+constexpr int kCsMaxCluster = 16;
+constexpr int kFirstThreads = 256;  // k_first_order: one example per thread
+
+struct ColPrepArgs {
+  const uint64_t* keys;
+  const uint8_t* labels;
+  int n_ex, n_cols;
+  const int32_t* col_tables;
+  const int64_t* base;
+  const int64_t* rows;
+  RankBounds rb;
+  int num_ranks;
+  long long iteration;
+  ErrorRecord* err;
+  // outputs
+  uint32_t* occ_pos;
+  uint8_t* occ_label;
+  uint32_t* seg_start;
+  uint64_t* uniq_key_s;
+  uint32_t* uniq_id_s;
+  uint32_t* first_s;   // [n_occ] segment index at each first occurrence (only those written)
+  uint32_t* ex_mask;   // [n_ex] bit c = column c's key is first seen at this example (zeroed)
+  unsigned long long* col_state;  // [n_cols] look-back words (zeroed)
+  uint32_t epoch;
+  long long* num_unique;
+  long long* rank_bounds;
+  uint32_t* occ_s;     // optional: occurrence -> key-sorted unique index
+  uint32_t* seg_of;    // optional: sorted position -> key-sorted unique index
+  uint32_t* occ_rank;  // optional: occurrence -> sorted position
+  uint32_t* long_list;
+  unsigned long long* num_long;
+  long long long_cap;
+};
+
+__device__ __forceinline__ int rank_of_rb(long long p, const RankBounds& rb, int num_ranks) {
+  int r = 0;
+  while (r + 1 < num_ranks && p >= rb.v[r + 1]) ++r;
+  return r;
+}
+
+// Debug (bp_debug_phase_trace 0): %globaltimer stamps of every CTA's phases,
+// [column][16 CTAs][16 stamps].
+__device__ unsigned long long* g_prep_trace = nullptr;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(kCsThreads, 2) k_col_cluster_prep(const __grid_constant__ ColPrepArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int M = kCsThreads * IPT;
+  extern __shared__ unsigned long long cs_smem[];
+  unsigned long long* recv = cs_smem;                           // [M] this CTA's slice of the column
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(recv + M);       // [warps][256]
+  uint32_t* hist = wcnt + kCsWarps * 256;                       // [256] published per-CTA counts
+  uint32_t* off = hist + 256;                                   // [256]
+  uint32_t* misc = off + 256;                                   // [32]
+  uint32_t* headpos = misc + 32;                                // [M] slice index of the CTA's h-th head
+  uint32_t* loff = headpos + M;                                 // [256] local digit offsets
+  unsigned long long* stage = reinterpret_cast<unsigned long long*>(loff + 256);  // [M] locally sorted
+  const int CS = (int)cluster.num_blocks();
+  const int me = (int)cluster.block_rank();
+  const int c = blockIdx.y;
+  const int t = a.col_tables[c];
+  const long long rows_t = a.rows[t];
+  const long long base_t = a.base[t];
+  const int bits = rows_t > 1 ? 64 - __clzll((unsigned long long)(rows_t - 1)) : 0;
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const int n_ex = a.n_ex, n_cols = a.n_cols;
+  unsigned long long* tr = g_prep_trace ? g_prep_trace + ((long long)c * 16 + me) * 16 : nullptr;
+#define BP_STAMP(k) \
+  if (tr && threadIdx.x == 0) tr[k] = gtimer()
+  BP_STAMP(0);
+
+  if (blockIdx.x == 0 && c == 0 && (int)threadIdx.x <= a.num_ranks) a.rank_bounds[threadIdx.x] = a.rb.v[threadIdx.x];
+
+  // every key and label load in flight at once (the checks below may call
+  // the error path, which would otherwise serialise the loads)
+  unsigned long long e[IPT];
+  uint32_t lab[IPT];
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const int ex = me * M + (int)(warp * (32 * IPT) + r * 32 + lane);
+    const long long p = (long long)(ex < n_ex ? ex : 0) * n_cols + c;
+    e[r] = __ldg(a.keys + p);
+    lab[r] = __ldg(a.labels + p);
+  }
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const int ex = me * M + (int)(warp * (32 * IPT) + r * 32 + lane);
+    if (ex < n_ex) {
+      const uint64_t key = e[r];
+      uint64_t row = key & kRowMask;
+      const bool bad_key = (int)(key >> kKeyTableShift) != t || (long long)row >= rows_t;
+      if (bad_key || lab[r] > 127) {
+        const long long p = (long long)ex * n_cols + c;
+        if (bad_key) raise_error(a.err, BP_ERR_STORE_KEY, a.iteration, p, key);
+        else raise_error(a.err, BP_ERR_CONFIG, a.iteration, p, 0);
+        if (bad_key) row = 0;
+      }
+      e[r] = (row << kCsRowShift) | ((unsigned long long)(lab[r] & 0x7f) << 20) | (unsigned long long)ex;
+    } else {
+      e[r] = ~0ull;  // padding sorts last (stable: after any real all-ones digit)
+    }
+  }
+  BP_STAMP(1);
+  int pass = 0;
+
+  for (int shift = kCsRowShift; shift < kCsRowShift + bits; shift += 8) {
+    for (int i = lane; i < 256; i += 32) wcnt[warp * 256 + i] = 0;
+    __syncwarp();
+    uint32_t rank[IPT];
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+      const uint32_t d = (uint32_t)((e[r] >> shift) & 0xFFull);
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const unsigned below = peers & ((1u << lane) - 1u);
+      const uint32_t prev = wcnt[warp * 256 + d];
+      rank[r] = prev + (uint32_t)__popc(below);
+      __syncwarp();
+      if (below == 0) wcnt[warp * 256 + d] = prev + (uint32_t)__popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // per digit: exclusive prefix over warps; the CTA's count is published
+      uint32_t run = 0;
+#pragma unroll
+      for (int w = 0; w < kCsWarps; ++w) {
+        const uint32_t x = wcnt[w * 256 + threadIdx.x];
+        wcnt[w * 256 + threadIdx.x] = run;
+        run += x;
+      }
+      hist[threadIdx.x] = run;
+    }
+    cluster.sync();
+    {  // column-wide offset of digit d in this CTA: all CTAs' smaller digits + lower CTAs' d
+      uint32_t h[kCsMaxCluster];
+#pragma unroll
+      for (int r = 0; r < kCsMaxCluster; ++r)  // independent remote loads
+        h[r] = r < CS ? *cluster.map_shared_rank(&hist[threadIdx.x], r) : 0u;
+      uint32_t tot = 0, before = 0;
+#pragma unroll
+      for (int r = 0; r < kCsMaxCluster; ++r) {
+        tot += h[r];
+        before += r < me ? h[r] : 0u;
+      }
+      uint32_t block_total;
+      const uint32_t incl = block_inclusive_scan_256(tot, misc, &block_total);
+      off[threadIdx.x] = incl - tot + before;
+      const uint32_t mine = hist[threadIdx.x];
+      loff[threadIdx.x] = block_inclusive_scan_256(mine, misc, &block_total) - mine;
+    }
+    __syncthreads();
+    // stable local sort by digit, then the slice is streamed out in local
+    // order: consecutive threads hold consecutive elements of one digit's run,
+    // whose destinations are consecutive too (coalesced DSMEM stores)
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+      const uint32_t d = (uint32_t)((e[r] >> shift) & 0xFFull);
+      stage[loff[d] + wcnt[warp * 256 + d] + rank[r]] = e[r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+      const uint32_t li = threadIdx.x + r * kCsThreads;
+      const unsigned long long x = stage[li];
+      const uint32_t d = (uint32_t)((x >> shift) & 0xFFull);
+      const uint32_t dest = off[d] + (li - loff[d]);
+      unsigned long long* rp = cluster.map_shared_rank(recv, (int)(dest / M));
+      rp[dest % M] = x;
+    }
+    cluster.sync();
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) e[r] = recv[warp * (32 * IPT) + r * 32 + lane];
+    BP_STAMP(2 + (pass < 4 ? pass : 3));
+    ++pass;
+  }
+  if (bits == 0) {
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) recv[warp * (32 * IPT) + r * 32 + lane] = e[r];
+  }
+  cluster.sync();  // final slices visible to the neighbours
+  BP_STAMP(6);
+
+  // ---- segment heads and their numbering
+  const unsigned long long left = me > 0 ? *cluster.map_shared_rank(&recv[M - 1], me - 1) : ~0ull;
+  bool head[IPT];
+  uint32_t pre[IPT];
+  uint32_t wsum = 0;
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const int i = (int)(warp * (32 * IPT) + r * 32 + lane);
+    const int j = me * M + i;
+    const unsigned long long prev = i > 0 ? recv[i - 1] : left;
+    head[r] = j < n_ex && (j == 0 || (prev >> kCsRowShift) != (e[r] >> kCsRowShift));
+    const unsigned b = __ballot_sync(0xffffffffu, head[r]);
+    pre[r] = wsum + (uint32_t)__popc(b & ((1u << lane) - 1u));
+    wsum += (uint32_t)__popc(b);
+  }
+  if (lane == 0) off[warp] = wsum;
+  if (threadIdx.x == 0) hist[1] = 0xFFFFFFFFu;  // column index of this CTA's first head (none yet)
+  __syncthreads();
+  uint32_t wbefore = 0, cta_heads = 0;
+#pragma unroll
+  for (int w = 0; w < kCsWarps; ++w) {
+    const uint32_t x = off[w];
+    wbefore += w < (int)warp ? x : 0u;
+    cta_heads += x;
+  }
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    if (!head[r]) continue;
+    const uint32_t i = warp * (32 * IPT) + r * 32 + lane;
+    headpos[wbefore + pre[r]] = i;
+    if (wbefore + pre[r] == 0) hist[1] = (uint32_t)(me * M) + i;
+  }
+  if (threadIdx.x == 0) hist[0] = cta_heads;
+  cluster.sync();
+  uint32_t cbefore = 0, col_heads = 0;
+  uint32_t next_first = (uint32_t)n_ex;  // first head after this CTA's slice: where its last segment ends
+  {
+    uint32_t h[kCsMaxCluster], f[kCsMaxCluster];
+#pragma unroll
+    for (int r = 0; r < kCsMaxCluster; ++r) {
+      h[r] = r < CS ? *cluster.map_shared_rank(&hist[0], r) : 0u;
+      f[r] = r < CS && r > me ? *cluster.map_shared_rank(&hist[1], r) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int r = 0; r < kCsMaxCluster; ++r) {
+      col_heads += h[r];
+      cbefore += r < me ? h[r] : 0u;
+      next_first = f[r] < next_first ? f[r] : next_first;
+    }
+  }
+  BP_STAMP(7);
+  if (me == 0 && warp == 0) {
+    // distinct keys of the columns before this one (decoupled look-back over
+    // columns, one warp), broadcast to the cluster's CTAs
+    const uint32_t colp = warp_lookback(a.col_state, c, a.epoch, col_heads);
+    if (lane < (unsigned)CS) *cluster.map_shared_rank(&misc[16], (int)lane) = colp;
+  }
+  // ---- position outputs (independent of the segment numbering: written
+  // while CTA 0 waits for the columns in front)
+  const long long col0 = (long long)c * n_ex;
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const int i = (int)(warp * (32 * IPT) + r * 32 + lane);
+    const int j = me * M + i;
+    if (j >= n_ex) continue;
+    const unsigned long long x = e[r];
+    const long long p = (long long)(x & kCsExMask) * n_cols + c;
+    const long long J = col0 + j;
+    bool rs = head[r];
+    if (!rs && a.num_ranks > 1) {
+      const unsigned long long px = i > 0 ? recv[i - 1] : left;
+      rs = rank_of_rb(p, a.rb, a.num_ranks) !=
+           rank_of_rb((long long)(px & kCsExMask) * n_cols + c, a.rb, a.num_ranks);
+    }
+    a.occ_pos[J] = (uint32_t)p;
+    a.occ_label[J] = (uint8_t)(((x >> 20) & 0x7f) | (rs ? 0x80 : 0));
+    if (a.occ_rank) a.occ_rank[p] = (uint32_t)J;
+  }
+  cluster.sync();
+  const uint32_t seg0 = misc[16] + cbefore + wbefore;
+  BP_STAMP(8);
+
+  // ---- segment outputs
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const int i = (int)(warp * (32 * IPT) + r * 32 + lane);
+    const int j = me * M + i;
+    if (j >= n_ex) continue;
+    const unsigned long long x = e[r];
+    const uint32_t ex = (uint32_t)(x & kCsExMask);
+    const long long p = (long long)ex * n_cols + c;
+    const long long J = col0 + j;
+    const uint32_t s = seg0 + pre[r] + (head[r] ? 0u : (uint32_t)-1);  // inclusive segment index
+    if (head[r]) {
+      const uint64_t row = x >> kCsRowShift;
+      a.seg_start[s] = (uint32_t)J;
+      a.uniq_key_s[s] = ((uint64_t)t << kKeyTableShift) | row;
+      a.uniq_id_s[s] = (uint32_t)(base_t + (long long)row);
+      a.first_s[p] = s;
+      atomicOr(&a.ex_mask[ex], 1u << c);
+      // segment length from the next head (this slice's, else the first
+      // head of a later slice of the column, else the column's end)
+      const uint32_t lh = wbefore + pre[r];
+      const uint32_t end = lh + 1 < cta_heads ? (uint32_t)(me * M) + headpos[lh + 1] : next_first;
+      const uint32_t len = end - (uint32_t)j;
+      if (len >= kVeryLongSeg) a.long_list[atomicAdd(&a.num_long[0], 1ull)] = s;
+      else if (len >= kLongSeg) a.long_list[a.long_cap - 1 - (long long)atomicAdd(&a.num_long[1], 1ull)] = s;
+    }
+    if (a.occ_s) a.occ_s[p] = s;
+    if (a.seg_of) a.seg_of[J] = s;
+    if (c == n_cols - 1 && j == n_ex - 1) {
+      const uint32_t U = misc[16] + col_heads;
+      *a.num_unique = U;
+      a.seg_start[U] = (uint32_t)((long long)n_cols * n_ex);
+    }
+  }
+  BP_STAMP(9);
+  BP_STAMP(10);
+#undef BP_STAMP
+}
+
+// First-occurrence order (reference traces.py:91-103: examples in order, an
+// example's keys in column order): k of the first occurrence at (ex, c) =
+// first occurrences in earlier examples (block scan of the per-example mask
+// popcounts + decoupled look-back over tiles of 256 examples) + set bits
+// below c.  The tile's positions are then walked in order by all threads
+// (coalesced, independent loads) to fill both permutations and the
+// first-order keys (read from the batch itself: the key at position p).
+__global__ void __launch_bounds__(kFirstThreads) k_first_order(const uint32_t* __restrict__ ex_mask,
+                                                               const uint32_t* __restrict__ first_s,
+                                                               const uint64_t* __restrict__ keys, int n_ex,
+                                                               int n_cols, unsigned long long* state, uint32_t epoch,
+                                                               uint32_t* __restrict__ perm_s2k,
+                                                               uint32_t* __restrict__ perm_k2s,
+                                                               uint64_t* __restrict__ uniq_key_k) {
+  __shared__ uint32_t sh_warp[kFirstThreads / 32];
+  __shared__ uint32_t sh_mask[kFirstThreads];
+  __shared__ uint32_t sh_pfx[kFirstThreads];
+  __shared__ uint32_t sh_prefix;
+  const int ex0 = blockIdx.x * kFirstThreads;
+  const int ex = ex0 + threadIdx.x;
+  const uint32_t m = ex < n_ex ? ex_mask[ex] : 0u;
+  const uint32_t cnt = (uint32_t)__popc(m);
+  uint32_t block_total;
+  const uint32_t excl = block_inclusive_scan_256(cnt, sh_warp, &block_total) - cnt;
+  if (threadIdx.x < 32) {
+    const uint32_t pfx = warp_lookback(state, blockIdx.x, epoch, block_total);
+    if (threadIdx.x == 0) sh_prefix = pfx;
+  }
+  sh_mask[threadIdx.x] = m;
+  sh_pfx[threadIdx.x] = excl;
+  __syncthreads();
+  const uint32_t tile_k0 = sh_prefix;
+  // warp w walks examples [32w, 32w+32) of the tile, lane c = column c: the
+  // loads of one example are consecutive positions, all issued up front
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const bool col_ok = (int)lane < n_cols;
+  uint32_t sv[32];
+  uint64_t kv[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int e = (int)warp * 32 + i;
+    const bool first = col_ok && ex0 + e < n_ex && ((sh_mask[e] >> lane) & 1u);
+    const long long p = (long long)(ex0 + e) * n_cols + lane;
+    sv[i] = first ? __ldg(first_s + p) : 0u;
+    kv[i] = first ? __ldg(keys + p) : 0ull;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int e = (int)warp * 32 + i;
+    const uint32_t mm = sh_mask[e];
+    if (!col_ok || ex0 + e >= n_ex || !((mm >> lane) & 1u)) continue;
+    const uint32_t k = tile_k0 + sh_pfx[e] + (uint32_t)__popc(mm & ((1u << lane) - 1u));
+    perm_s2k[sv[i]] = k;
+    perm_k2s[k] = sv[i];
+    uniq_key_k[k] = kv[i];
+  }
+}
+
+__global__ void k_occ_k_from_s(const uint32_t* __restrict__ occ_s, long long n, const uint32_t* __restrict__ perm_s2k,
+                               uint32_t* __restrict__ occ_k) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    occ_k[p] = perm_s2k[occ_s[p]];
+}
+
+static size_t cs_smem_bytes(int ipt) {
+  return 2 * sizeof(unsigned long long) * kCsThreads * ipt +
+         sizeof(uint32_t) * (kCsWarps * 256 + 256 + 256 + 32 + kCsThreads * ipt + 256);
+}
+
+// Cluster size and items per thread for n_ex examples per column; 0 if the
+// cluster path does not apply.
+static int g_prep_ipt_min = 8;  // debug knob (bp_debug_prep_shape): smallest items per thread tried
+
+static bool cs_shape(int n_ex, int* cs, int* ipt) {
+  for (int i : {4, 8, 16}) {
+    if (i < g_prep_ipt_min) continue;
+    for (int c = 1; c <= kCsMaxCluster; c <<= 1) {
+      if ((long long)c * kCsThreads * i >= n_ex && (i != 8 || c <= 8)) {
+        *cs = c;
+        *ipt = i;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+
 __global__ void k_set_rank_bounds(RankBounds rb, int n, long long* out) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = rb.v[i];
+}
+
+// Columnar prep on clusters: one memset (example masks, look-back words,
+// long-list counters), the cluster sort-and-number kernel, the
+// first-occurrence kernel (+ the occurrence -> first-order index on request).
+static int prep_build_cluster(bp_prep* P, const bp_schema* sc, const uint64_t* d_keys, const uint8_t* d_labels,
+                              const ColumnarInfo* col, const int64_t* h_rank_bounds, cudaStream_t s) {
+  int cs = 0, ipt = 0;
+  cs_shape(col->n_ex, &cs, &ipt);
+  ColPrepArgs a;
+  a.keys = d_keys;
+  a.labels = d_labels;
+  a.n_ex = col->n_ex;
+  a.n_cols = col->n_cols;
+  a.col_tables = col->d_tables;
+  a.base = sc->d_table_base;
+  a.rows = sc->d_rows;
+  for (int i = 0; i <= P->num_ranks; ++i) a.rb.v[i] = h_rank_bounds[i];
+  a.num_ranks = P->num_ranks;
+  a.iteration = P->iteration;
+  a.err = P->ctx ? P->ctx->d_err : nullptr;
+  a.occ_pos = P->d_occ_pos;
+  a.occ_label = P->d_occ_label;
+  a.seg_start = P->d_seg_start;
+  a.uniq_key_s = P->d_uniq_key_s;
+  a.uniq_id_s = P->d_uniq_id_s;
+  a.first_s = P->t_first_flag;
+  a.ex_mask = P->t_ex_mask;
+  a.col_state = P->t_col_state;
+  a.epoch = next_scan_epoch();
+  a.num_unique = P->d_num_unique;
+  a.rank_bounds = P->d_rank_bounds;
+  const bool occ_s_needed = (P->flags & (BP_PREP_OCC_INDEX | BP_PREP_OCC_SORTED)) != 0;
+  a.occ_s = occ_s_needed ? (P->d_occ_s ? P->d_occ_s : P->t_va) : nullptr;
+  a.seg_of = P->d_seg_of;
+  a.occ_rank = P->d_occ_rank;
+  a.long_list = P->d_long;
+  a.num_long = (unsigned long long*)P->d_num_long;
+  a.long_cap = P->long_cap;
+  BP_CUDA_TRY(cudaMemsetAsync(P->d_num_long, 0, P->zero_bytes, s));
+  const size_t smem = cs_smem_bytes(ipt);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, col->n_cols, 1);
+  cfg.blockDim = dim3(kCsThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BP_CUDA_TRY(cudaFuncSetAttribute(k_col_cluster_prep<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)cs_smem_bytes(8)));
+    BP_CUDA_TRY(cudaFuncSetAttribute(k_col_cluster_prep<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)cs_smem_bytes(16)));
+    BP_CUDA_TRY(cudaFuncSetAttribute(k_col_cluster_prep<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    BP_CUDA_TRY(cudaFuncSetAttribute(k_col_cluster_prep<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)cs_smem_bytes(4)));
+    BP_CUDA_TRY(cudaFuncSetAttribute(k_col_cluster_prep<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_set = true;
+  }
+  if (ipt == 4) BP_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_col_cluster_prep<4>, a));
+  else if (ipt == 8) BP_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_col_cluster_prep<8>, a));
+  else BP_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_col_cluster_prep<16>, a));
+  const int tiles = (col->n_ex + kFirstThreads - 1) / kFirstThreads;
+  k_first_order<<<tiles, kFirstThreads, 0, s>>>(P->t_ex_mask, P->t_first_flag, d_keys, col->n_ex, col->n_cols,
+                                                P->t_tile_state, next_scan_epoch(), P->d_perm_s2k, P->d_perm_k2s,
+                                                P->d_uniq_key_k);
+  if (P->flags & BP_PREP_OCC_INDEX)
+    k_occ_k_from_s<<<grid_for(P->n_occ, 256), 256, 0, s>>>(a.occ_s, P->n_occ, P->d_perm_s2k, P->d_occ_k);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
 }
 
 template <typename K>
@@ -365,7 +879,7 @@ struct Carve {
   }
 };
 
-static size_t prep_layout(bp_prep* P, char* base, long long n, int num_ranks, int flags) {
+static size_t prep_layout(bp_prep* P, char* base, long long n, int num_ranks, int flags, const ColumnarInfo* cl) {
   Carve c{base};
   P->d_num_unique = c.take<long long>(1);
   P->d_uniq_key_s = c.take<uint64_t>(n);
@@ -383,7 +897,28 @@ static size_t prep_layout(bp_prep* P, char* base, long long n, int num_ranks, in
   P->d_rank_bounds = c.take<long long>(num_ranks + 1);
   P->long_cap = n / kLongSeg + 1;
   P->d_long = c.take<uint32_t>(P->long_cap);
+  if (cl) {
+    // cluster path: the temporaries are one segment index per occurrence and
+    // a zeroed block (long-list counters, example masks, look-back words)
+    // cleared by ONE memset starting at d_num_long
+    const size_t zero0 = c.off = (c.off + 255) & ~size_t(255);
+    P->d_num_long = reinterpret_cast<long long*>(base ? base + c.off : nullptr);
+    c.off += 2 * sizeof(long long);
+    P->t_ex_mask = c.take<uint32_t>(cl->n_ex);
+    P->t_col_state = c.take<unsigned long long>((size_t)cl->n_cols * kLookbackStride);
+    P->t_tile_state = c.take<unsigned long long>((size_t)((cl->n_ex + kFirstThreads - 1) / kFirstThreads) *
+                                                 kLookbackStride);
+    P->zero_bytes = c.off - zero0;
+    P->t_first_flag = c.take<uint32_t>(n);
+    P->t_va = (flags & BP_PREP_OCC_INDEX) && !(flags & BP_PREP_OCC_SORTED) ? c.take<uint32_t>(n) : nullptr;
+    P->t_ka = P->t_kb = nullptr;
+    P->t_vb = P->t_hist = P->t_head = P->t_segx = P->t_first_rank = P->t_partials = nullptr;
+    return c.off;
+  }
   P->d_num_long = c.take<long long>(2);
+  P->t_ex_mask = nullptr;
+  P->t_col_state = P->t_tile_state = nullptr;
+  P->zero_bytes = 0;
   P->t_ka = c.take<uint64_t>(n);
   P->t_kb = c.take<uint64_t>(n);
   P->t_va = c.take<uint32_t>(n);
@@ -416,11 +951,18 @@ static int prep_create_impl(bp_ctx* ctx, const bp_schema* sc, const uint64_t* d_
   P->stream = s;
   P->h_num_unique = n_occ == 0 ? 0 : -1;
   const long long n = n_occ > 0 ? n_occ : 1;
-  const size_t bytes = prep_layout(P, nullptr, n, num_ranks, flags);
+  const ColumnarInfo* cl = (col && n_occ > 0 && col->cluster) ? col : nullptr;
+  const size_t bytes = prep_layout(P, nullptr, n, num_ranks, flags, cl);
   void* arena = nullptr;
   BP_CUDA_TRY(cudaMallocAsync(&arena, bytes, s));
   P->d_arena = arena;
-  prep_layout(P, static_cast<char*>(arena), n, num_ranks, flags);
+  prep_layout(P, static_cast<char*>(arena), n, num_ranks, flags, cl);
+  if (cl) {
+    const int rc = prep_build_cluster(P, sc, d_keys, d_labels, cl, h_rank_bounds, s);
+    if (rc != BP_OK) return rc;
+    *out = P;
+    return BP_OK;
+  }
   if (num_ranks + 1 <= RankBounds::kMax) {
     // by value as a kernel parameter: a pageable H2D copy would first wait
     // for the whole stream (host-blocking)
@@ -481,7 +1023,10 @@ extern "C" int bp_prep_create_columnar(bp_ctx* ctx, const bp_schema* sc, const u
     max_rows = std::max<int64_t>(max_rows, sc->h_table_base[t + 1] - sc->h_table_base[t]);
   const int row_bits = std::max(1, bit_width_u64((unsigned long long)(max_rows - 1)));
   if (row_bits > 44 - 14) return BP_ERR_INVALID;
-  const ColumnarInfo col{(int)n_ex, n_cols, row_bits, d_tables};
+  int cs = 0, ipt = 0;
+  const bool cluster = g_prep_cluster && n_cols <= kCsMaxCols && row_bits <= kCsMaxRowBits &&
+                       num_ranks + 1 <= RankBounds::kMax && cs_shape((int)n_ex, &cs, &ipt);
+  const ColumnarInfo col{(int)n_ex, n_cols, row_bits, d_tables, cluster};
   return prep_create_impl(ctx, sc, d_keys, d_labels, n_occ, h_rank_bounds, num_ranks, iteration, flags, 0, 0, stream,
                           out, &col);
 }
@@ -521,5 +1066,30 @@ extern "C" int bp_prep_num_unique(bp_prep* P, bp_stream_t stream, int64_t* h_out
     P->h_num_unique = u;
   }
   *h_out = P->h_num_unique;
+  return BP_OK;
+}
+
+// 1 (default): Criteo-layout batches use the cluster prep; 0: the per-column
+// single-CTA sort (kept as the reference implementation for tests).
+// Debug: phase timestamps (%globaltimer, ns) of kernel `which` into d_buf
+// (NULL disables): 0 = k_col_cluster_prep [column][16][16], 1 = k_pop_fused
+// [tile][8].
+extern "C" int bp_debug_phase_trace(int32_t which, void* d_buf) {
+  if (which == 0) BP_CUDA_TRY(cudaMemcpyToSymbol(bp::g_prep_trace, &d_buf, sizeof(void*)));
+  else if (which == 1) return bp_debug_pop_trace(d_buf);
+  else return BP_ERR_INVALID;
+  return BP_OK;
+}
+
+extern "C" int bp_debug_prep_cluster(int32_t on) {
+  bp::g_prep_cluster = on ? 1 : 0;
+  return BP_OK;
+}
+
+// Debug/tuning: smallest items per thread of the cluster prep (4, 8 or 16;
+// with 4 a 16,384-example column is spread over 16 CTAs instead of 8).
+extern "C" int bp_debug_prep_shape(int32_t ipt_min) {
+  if (ipt_min != 4 && ipt_min != 8 && ipt_min != 16) return BP_ERR_INVALID;
+  bp::g_prep_ipt_min = ipt_min;
   return BP_OK;
 }

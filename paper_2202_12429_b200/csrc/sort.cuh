@@ -153,6 +153,48 @@ static __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(const uint
   }
 }
 
+// Decoupled look-back for one tile, run by ONE full warp: publishes the
+// tile's aggregate, walks back over its predecessors (lane l inspects tile
+// j - l) until an inclusive prefix, publishes its own inclusive prefix and
+// returns the exclusive prefix on every lane.  Same epoch-tagged status
+// words as k_scan_onepass (the state needs no clearing between calls that
+// use distinct epochs, only once after allocation).
+// Status words sit kLookbackStride words apart (one 128-byte line each): the
+// pollers of a tile then never queue on a line shared with other tiles.
+constexpr int kLookbackStride = 16;
+
+__device__ __forceinline__ uint32_t warp_lookback(unsigned long long* state, long long tile, uint32_t epoch,
+                                                  uint32_t agg) {
+  struct Strided {
+    volatile unsigned long long* p;
+    __device__ volatile unsigned long long& operator[](long long i) const { return p[i * kLookbackStride]; }
+  } st{state};
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t ep = epoch & 0x3FFFFFFFu;
+  if (tile == 0) {
+    if (lane == 0) st[0] = scan_pack(epoch, kFlagPrefix, agg);
+    return 0;
+  }
+  if (lane == 0) st[tile] = scan_pack(epoch, kFlagAgg, agg);
+  uint32_t prefix = 0;
+  for (long long j = tile - 1;; j -= 32) {
+    const long long idx = j - (long long)lane;
+    unsigned long long w = 0;
+    if (idx >= 0) {
+      do {
+        w = st[idx];
+      } while ((uint32_t)(w >> 34) != ep || ((w >> 32) & 3ull) == 0);
+    }
+    const unsigned pm = __ballot_sync(0xffffffffu, idx >= 0 && ((w >> 32) & 3ull) == kFlagPrefix);
+    const unsigned stop = pm ? (unsigned)(__ffs(pm) - 1) : 31u;
+    const uint32_t v = (idx >= 0 && lane <= stop) ? (uint32_t)w : 0u;
+    prefix += warp_sum(v);
+    if (pm || j - 32 < 0) break;
+  }
+  if (lane == 0) st[tile] = scan_pack(epoch, kFlagPrefix, prefix + agg);
+  return prefix;
+}
+
 inline int scan_tiles(long long n) { return (int)((n + kScanTile - 1) / kScanTile); }
 // u32 words of tile state an exclusive_scan over n elements needs.
 inline long long scan_state_words(long long n) { return 2ll * (scan_tiles(n > 0 ? n : 1) + 1); }

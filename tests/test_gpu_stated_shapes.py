@@ -61,7 +61,7 @@ def _check(schema, batches, cfg, lookahead_plans):
     from paper_2202_12429_b200 import engine
 
     cap = cfg.cache_capacity
-    want_shas = [O.plan_sha(p) for p in O.plan_stream(batches, lookahead_plans, cap)]
+    want_shas = [O.plan_sha(p) for p in O.plan_stream(batches, lookahead_plans, cap)[0]]
     assert _plan_shas_gpu(batches, schema, lookahead_plans, cap) == want_shas
     pipe = engine.run_pipeline(cfg, schema, batches)
     digest = pipe.final_store_digest

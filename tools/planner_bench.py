@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--warm", type=int, default=10)
     ap.add_argument("--nvtx", action="store_true")
     ap.add_argument("--no-prof", action="store_true")
+    ap.add_argument("--trace", action="store_true", help="phase timestamps of the cluster prep and the fused pop")
     args = ap.parse_args()
     lib = L.lib()
     sc = bench.schema()
@@ -134,6 +135,39 @@ def main():
             if e.device_type == torch.autograd.DeviceType.CUDA:
                 name = (e.name or "").split("(")[0].replace("void ", "")
                 kernels[name] = round(kernels.get(name, 0.0) + e.device_time, 2)
+    trace = None
+    if args.trace:
+        tp = torch.zeros(64 * 16 * 16, dtype=torch.int64, device="cuda")
+        tq = torch.zeros(4096 * 8, dtype=torch.int64, device="cuda")
+        L.check(lib.bp_debug_phase_trace(0, L.ptr(tp)), "trace")
+        L.check(lib.bp_debug_phase_trace(1, L.ptr(tq)), "trace")
+        one(i, False)
+        i += 1
+        L.check(lib.bp_debug_phase_trace(0, None), "trace")
+        L.check(lib.bp_debug_phase_trace(1, None), "trace")
+        a = tp.view(64, 16, 16).cpu().numpy()
+        ncols = len(dev[0][4][1])
+        a = a[:ncols]
+        valid = a[:, :, 0] > 0
+        t0 = a[:, :, 0][valid].min()
+        cols = {}
+        for c in range(ncols):
+            v = a[c][valid[c]]
+            rel = np.where(v > 0, (v - t0) / 1e3, np.nan)
+            cols[c] = {"ctas": int(valid[c].sum()), "max_us": [None if np.isnan(x) else round(float(x), 2)
+                                                               for x in np.nanmax(rel, axis=0)[:11]],
+                       "min_us": [None if np.isnan(x) else round(float(x), 2) for x in np.nanmin(rel, axis=0)[:11]]}
+        q = tq.view(4096, 8).cpu().numpy()
+        qv = q[q[:, 0] > 0]
+        q0 = qv[:, 0].min()
+        qrel = (qv[:, :5] - q0) / 1e3
+        trace = {"prep_phases": "0 start, 1 loads, 2-5 after radix pass 1-4, 6 final sync, 7 heads counted, "
+                                "8 column look-back, 9 outputs, 10 long list",
+                 "prep_columns": cols,
+                 "pop_phases": "0 start, 1 loads+decisions, 2 block scan, 3 look-back, 4 compaction",
+                 "pop_tiles": int(len(qv)), "pop_max_us": [round(float(x), 2) for x in qrel.max(axis=0)],
+                 "pop_min_us": [round(float(x), 2) for x in qrel.min(axis=0)],
+                 "pop_median_us": [round(float(x), 2) for x in np.median(qrel, axis=0)]}
     u, p, e = float(np.mean(us)), float(np.mean(pfs)), float(np.mean(evs))
     prep_us, plan_us = float(np.median(t_prep)), float(np.median(t_plan))
     pb_, plb = prep_bytes(n_occ, int(u)), planner_bytes(int(u), int(p), int(e))
@@ -143,7 +177,7 @@ def main():
            "prep_gbs": pb_ / (prep_us * 1e-6) / 1e9, "planner_gbs": plb / (plan_us * 1e-6) / 1e9,
            "combined_gbs": (pb_ + plb) / ((prep_us + plan_us) * 1e-6) / 1e9,
            "prep_us_all": [round(x, 1) for x in t_prep], "planner_us_all": [round(x, 1) for x in t_plan],
-           "kernels_us": kernels}
+           "kernels_us": kernels, "trace": trace}
     print(json.dumps(out), flush=True)
     lib.bp_planner_destroy(h)
 
