@@ -863,21 +863,21 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 constexpr int kStagedF4 = 2048;  // float4 per k_embbag_bwd_staged tile (32 KB)
 
-template <int Q>
-__global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
+template <int Q, int NT = 256, int F4 = kStagedF4>
+__global__ void __launch_bounds__(NT, 3 * 256 / NT) k_embbag_bwd_staged(
     const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start, uint32_t n,
     const float4* __restrict__ grad, float* __restrict__ values, int row_stride, const int32_t* __restrict__ slots_s,
     uint8_t* __restrict__ dirty, int opt, float lr, float eps, float4* __restrict__ parts,
     unsigned int* __restrict__ arrivals, unsigned long long* __restrict__ stats) {
-  constexpr int T = kStagedF4 / Q, NG = 256 / Q, RPG = T / NG, GW = 32 / Q;
+  constexpr int T = F4 / Q, NG = NT / Q, RPG = T / NG, GW = 32 / Q, NW = NT / 32;
   extern __shared__ __align__(128) unsigned char st_smem[];
   float4* tile = reinterpret_cast<float4*>(st_smem);          // [T][Q]
   uint32_t* sgs = reinterpret_cast<uint32_t*>(tile + T * Q);  // [T]
   int32_t* tslot = reinterpret_cast<int32_t*>(sgs + T);          // [T] cache slots of the tile's keys
   __shared__ __align__(8) uint64_t bar;
   __shared__ float4 gcarry[NG][Q];
-  __shared__ float4 wagg[8][Q];
-  __shared__ int wflag[8][Q];
+  __shared__ float4 wagg[NW][Q];
+  __shared__ int wflag[NW][Q];
   __shared__ uint8_t ghead[NG];
   const uint32_t t0 = blockIdx.x * T;
   const uint32_t rows = min((uint32_t)T, n - t0);
@@ -910,7 +910,7 @@ __global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
   const uint32_t fa = seg_start[tile_first], fb = seg_start[tile_first + 1];
   const uint32_t la = seg_start[tile_last], lb = seg_start[tile_last + 1];
   const uint32_t nu = tile_last - tile_first + 1;
-  for (uint32_t i = tid; i < nu; i += 256) {
+  for (uint32_t i = tid; i < nu; i += NT) {
     const int32_t sl = slots_s[tile_first + i];
     tslot[i] = sl;
     if (sl >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(values + (size_t)sl * row_stride));
@@ -986,7 +986,7 @@ __global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
   // pass 3: (row, column) items; a key's last row in the tile holds its sum
   unsigned my_nz = 0;
   bool wrote = false;
-  constexpr int ITEMS = T * Q / 256, B = 4;
+  constexpr int ITEMS = T * Q / NT, B = 4;
 #pragma unroll 1
   for (int k0 = 0; k0 < ITEMS; k0 += B) {
     int32_t sl[B];
@@ -1088,7 +1088,7 @@ __global__ void __launch_bounds__(256, 3) k_embbag_bwd_staged(
   }
 }
 
-// Persistent, pipelined form of k_embbag_bwd_staged (the default): a grid
+// Persistent, pipelined form of k_embbag_bwd_staged (variant 5): a grid
 // of 2 CTAs per SM walks the tiles t = blockIdx.x + k * gridDim.x with
 // kPipeStages shared-memory stages.  Thread 0 keeps kPipeStages bulk copies
 // (TMA, one mbarrier per stage, phase parity per reuse) in flight, so tile
@@ -1338,6 +1338,225 @@ __global__ void __launch_bounds__(256, 2) k_embbag_bwd_pipe(
   if (stats) {
     for (int off = 16; off > 0; off >>= 1) my_nz += __shfl_down_sync(0xffffffffu, my_nz, off);
     if ((tid & 31) == 0 && my_nz) atomicAdd(&stats[1], (unsigned long long)my_nz);
+  }
+}
+
+// Two-kernel backward (variant 4; measured slower inside the step than the
+// fused one-shot kernel, kept for comparison): the reduction and the update
+// are split so neither waits on the other's latency.
+//
+// k_bwd_reduce: a streaming segmented reduction of the key-sorted gradient
+// rows.  Persistent CTAs (2 per SM) keep kPipeStages bulk copies (TMA +
+// mbarrier) of 16 KB tiles in flight; per tile the running segmented sums,
+// the two-level carry scan (fixed order) and, for every key ending in the
+// tile, ONE float4 store of its sum into gsum[s] (keys are consecutive, so
+// the stores are too) -- no cache-row access, no dependent global loads.  A
+// key that continues from the previous tile or into the next one leaves its
+// tile partial in parts[tile][0 | 1] (first | last key of the tile).
+//
+// k_bwd_apply: one Q-lane group per unique key (fully parallel, latency
+// hidden by occupancy): g = gsum[s], or for a key spanning tiles its
+// partials summed in tile order, then SGD/Adagrad in place on its cached row,
+// dirty mark and the non-zero count.
+constexpr int kRedF4 = 1024;  // float4 per k_bwd_reduce tile (16 KB): 4 CTAs x 3 stages per SM
+
+template <int Q>
+__global__ void __launch_bounds__(256, 4) k_bwd_reduce(const uint32_t* __restrict__ seg_of, uint32_t n,
+                                                       uint32_t n_tiles, const float4* __restrict__ grad,
+                                                       float4* __restrict__ gsum, float4* __restrict__ parts) {
+  constexpr int T = kRedF4 / Q, NG = 256 / Q, RPG = T / NG, GW = 32 / Q;
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  float4* tiles_sm = reinterpret_cast<float4*>(st_smem);                          // [S][T][Q]
+  uint32_t* sgs_sm = reinterpret_cast<uint32_t*>(tiles_sm + kPipeStages * T * Q);  // [S][T]
+  __shared__ __align__(8) uint64_t bar[kPipeStages];
+  __shared__ float4 gcarry[NG][Q];
+  __shared__ float4 wagg[8][Q];
+  __shared__ int wflag[8][Q];
+  __shared__ uint8_t ghead[NG];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t G = gridDim.x;
+  auto issue = [&](uint32_t tile, int st) {
+    const uint32_t t0 = tile * T;
+    const uint32_t rows = min((uint32_t)T, n - t0);
+    const uint32_t gbytes = rows * Q * 16, seg_bytes = (rows / 4) * 16;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[st])),
+                 "r"(gbytes + seg_bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(tiles_sm + (size_t)st * T * Q)),
+                 "l"(grad + (size_t)t0 * Q), "r"(gbytes), "r"(smem_u32(&bar[st]))
+                 : "memory");
+    if (seg_bytes)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(sgs_sm + (size_t)st * T)),
+                   "l"(seg_of + t0), "r"(seg_bytes), "r"(smem_u32(&bar[st]))
+                   : "memory");
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int st = 0; st < kPipeStages; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[st])));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (int st = 0; st < kPipeStages; ++st)
+      if (blockIdx.x + st * G < n_tiles) issue(blockIdx.x + st * G, st);
+  }
+  __syncthreads();
+  const int c = (int)(tid % Q), gi = (int)(tid / Q), w = (int)(tid >> 5), gw = (int)((tid & 31) / Q);
+  const uint32_t r0 = gi * RPG;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t k = 0;
+  for (uint32_t tile_id = blockIdx.x; tile_id < n_tiles; tile_id += G, ++k) {
+    const int st = (int)(k % kPipeStages);
+    const uint32_t phase = (k / kPipeStages) & 1u;
+    float4* tile = tiles_sm + (size_t)st * T * Q;
+    uint32_t* sgs = sgs_sm + (size_t)st * T;
+    const uint32_t t0 = tile_id * T;
+    const uint32_t rows = min((uint32_t)T, n - t0);
+    const uint32_t seg_bytes = (rows / 4) * 16;
+    // the neighbours' segment ids tell whether the tile's first / last key
+    // continues across its edges (independent loads, in flight with the copy)
+    const uint32_t prev_id = t0 > 0 ? seg_of[t0 - 1] : 0xFFFFFFFFu;
+    const uint32_t next_id = t0 + rows < n ? seg_of[t0 + rows] : 0xFFFFFFFFu;
+    if (tid < rows - seg_bytes / 4) sgs[seg_bytes / 4 + tid] = seg_of[t0 + seg_bytes / 4 + tid];
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT%=;\n}\n" ::"r"(
+            smem_u32(&bar[st])),
+        "r"(phase)
+        : "memory");
+    __syncthreads();
+    float4 acc = zero;
+    bool flag = false;
+    if (r0 < rows) {
+      uint32_t ps = sgs[r0];
+      acc = tile[r0 * Q + c];
+      flag = r0 == 0 || sgs[r0 - 1] != ps;
+      if (c == 0) ghead[gi] = flag ? 1 : 0;
+      const uint32_t re = min(r0 + RPG, rows);
+      for (uint32_t r = r0 + 1; r < re; ++r) {
+        const uint32_t sr = sgs[r];
+        const float4 x = tile[r * Q + c];
+        if (sr == ps) {
+          acc = f4_add(acc, x);
+        } else {
+          acc = x;
+          flag = true;
+        }
+        tile[r * Q + c] = acc;
+        ps = sr;
+      }
+    } else if (c == 0) {
+      ghead[gi] = 1;
+    }
+    float4 inc = acc;
+    bool finc = flag;
+#pragma unroll
+    for (int off = 1; off < GW; off <<= 1) {
+      const bool fo = __shfl_up_sync(0xffffffffu, finc ? 1 : 0, off * Q) != 0;
+      float4 o;
+      o.x = __shfl_up_sync(0xffffffffu, inc.x, off * Q);
+      o.y = __shfl_up_sync(0xffffffffu, inc.y, off * Q);
+      o.z = __shfl_up_sync(0xffffffffu, inc.z, off * Q);
+      o.w = __shfl_up_sync(0xffffffffu, inc.w, off * Q);
+      if (gw >= off && !finc) inc = f4_add(o, inc);
+      if (gw >= off) finc = finc || fo;
+    }
+    if (gw == GW - 1) {
+      wagg[w][c] = inc;
+      wflag[w][c] = finc ? 1 : 0;
+    }
+    float4 ex;
+    ex.x = __shfl_up_sync(0xffffffffu, inc.x, Q);
+    ex.y = __shfl_up_sync(0xffffffffu, inc.y, Q);
+    ex.z = __shfl_up_sync(0xffffffffu, inc.z, Q);
+    ex.w = __shfl_up_sync(0xffffffffu, inc.w, Q);
+    const bool fex = __shfl_up_sync(0xffffffffu, finc ? 1 : 0, Q) != 0;
+    __syncthreads();
+    float4 cw = zero;
+    for (int kk = 0; kk < w; ++kk) cw = wflag[kk][c] ? wagg[kk][c] : f4_add(cw, wagg[kk][c]);
+    const float4 carry = gw == 0 ? cw : (fex ? ex : f4_add(cw, ex));
+    gcarry[gi][c] = carry;
+    __syncthreads();
+    const uint32_t first = sgs[0], last = sgs[rows - 1];
+    const bool cont_in = prev_id == first, cont_out = next_id == last;
+    constexpr int ITEMS = T * Q / 256;
+#pragma unroll 4
+    for (int kk = 0; kk < ITEMS; ++kk) {
+      const uint32_t r = (uint32_t)(tid / Q) + (uint32_t)kk * NG;
+      if (r >= rows) continue;
+      const uint32_t sg = sgs[r];
+      if (r + 1 < rows && sgs[r + 1] == sg) continue;  // not the last row of its run
+      const uint32_t g = r / RPG;
+      float4 x = tile[r * Q + c];
+      if (!ghead[g] && sg == sgs[g * RPG]) x = f4_add(gcarry[g][c], x);
+      if (sg == first && cont_in) parts[(size_t)(tile_id * 2) * Q + c] = x;
+      else if (sg == last && cont_out) parts[(size_t)(tile_id * 2 + 1) * Q + c] = x;
+      else gsum[(size_t)sg * Q + c] = x;
+    }
+    __syncthreads();  // every thread is done with this stage
+    if (tid == 0 && tile_id + kPipeStages * G < n_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tile_id + kPipeStages * G, st);
+    }
+  }
+}
+
+template <int Q>
+__global__ void __launch_bounds__(256) k_bwd_apply(const uint32_t* __restrict__ seg_start, const long long* d_U,
+                                                   const float4* __restrict__ gsum, const float4* __restrict__ parts,
+                                                   float* __restrict__ values, int row_stride,
+                                                   const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty,
+                                                   int opt, float lr, float eps,
+                                                   unsigned long long* __restrict__ stats) {
+  constexpr int T = kRedF4 / Q;
+  const long long U = *d_U;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long s = i / Q;
+  const int c = (int)(i % Q);
+  bool nz = false;
+  if (s < U) {
+    // independent loads first: slot, CSR bounds, the in-tile sum
+    const int32_t slot = slots_s[s];
+    const uint32_t a = seg_start[s], b = seg_start[s + 1];
+    float4 g = __ldcg(gsum + (size_t)s * Q + c);
+    if (slot >= 0) {
+      float* row = values + (size_t)slot * row_stride;
+      float4 x = reinterpret_cast<const float4*>(row)[c];
+      float4 acc = opt == BP_OPT_ADAGRAD ? reinterpret_cast<const float4*>(row)[Q + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t ft = a / T, lt = (b - 1) / T;
+      if (ft != lt) {  // tile partials in tile order: the key continues out of
+                       // its first tile (slot 1 there) and into every later one (slot 0)
+        g = __ldcg(parts + (size_t)(ft * 2 + 1) * Q + c);
+        // 8 partial loads in flight per round (a Zipf-hot key spans dozens of
+        // tiles), summed in tile order
+        for (uint32_t t0 = ft + 1; t0 <= lt; t0 += 8) {
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            v[u] = t0 + u <= lt ? __ldcg(parts + (size_t)((t0 + u) * 2) * Q + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (t0 + u <= lt) g = f4_add(g, v[u]);
+        }
+      }
+      x.x = upd1(x.x, acc.x, g.x, opt, lr, eps);
+      x.y = upd1(x.y, acc.y, g.y, opt, lr, eps);
+      x.z = upd1(x.z, acc.z, g.z, opt, lr, eps);
+      x.w = upd1(x.w, acc.w, g.w, opt, lr, eps);
+      reinterpret_cast<float4*>(row)[c] = x;
+      if (opt == BP_OPT_ADAGRAD) reinterpret_cast<float4*>(row)[Q + c] = acc;
+      nz = g.x != 0.f || g.y != 0.f || g.z != 0.f || g.w != 0.f;
+    }
+  }
+  // a key is dirty if any of its Q lanes saw a non-zero component
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned bal = __ballot_sync(0xffffffffu, nz);
+  const unsigned gm = (Q == 32 ? 0xffffffffu : ((1u << Q) - 1u)) << (lane / Q * Q);
+  const bool key_nz = (bal & gm) != 0 && c == 0 && s < U;
+  if (key_nz && dirty) dirty[slots_s[s]] = 1;
+  if (stats) {
+    const unsigned cnt = __popc(__ballot_sync(0xffffffffu, key_nz));
+    if (lane == 0 && cnt) atomicAdd(&stats[1], (unsigned long long)cnt);
   }
 }
 
@@ -1606,9 +1825,13 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
   return BP_OK;
 }
 
-// debug: the kernel behind bp_embbag_backward_sorted (0: k_embbag_bwd_pipe,
-// the default; 4: the one-shot k_embbag_bwd_staged; warp tiles: 1: R=8 x 3
-// CTAs/SM, 2: R=4 x 4, 3: R=8 x 2)
+// debug: the kernels behind bp_embbag_backward_sorted (0: the one-shot fused
+// k_embbag_bwd_staged, 32 KB tiles -- the default, fastest inside the DLRM
+// step; 6: the same with 16 KB tiles x 128 threads; 4: the split
+// k_bwd_reduce + k_bwd_apply; 5: the persistent 3-stage k_embbag_bwd_pipe;
+// warp tiles: 1: R=8 x 3 CTAs/SM, 2: R=4 x 4, 3: R=8 x 2).  Measured at CK
+// shape (tools/embbag_instep.py, profiles/round2): in the step 0 = 6 = 30.7
+// us, 4: 35.8 us, 5: slower still; isolated 24-25 us for 0/6, 28-31 us for 4/5.
 static int g_bwd_variant = 0;
 
 extern "C" int bp_debug_bwd_variant(int32_t v) {
@@ -1652,9 +1875,13 @@ static int launch_bwd_sorted(bp_prep* P, const float* d_grad_sorted, float* d_va
 // the arrival counters (zero between calls: the last arriver resets them).
 extern "C" int64_t bp_embbag_bwd_scratch_bytes(int64_t n_occ, int32_t dim) {
   if (dim < 4 || (dim & 3) != 0) return 0;
-  const int q = dim / 4, T = bp::kStagedF4 / q;
+  const int q = dim / 4, T = bp::kStagedF4 / 2 / q;  // the smaller staged tiles (variant 6): most tiles
   const long long tiles = (n_occ + T - 1) / T;
-  return (((long long)tiles * 2 * q * 16 + 255) & ~255ll) + tiles * 4 + 256;
+  const long long rtiles = (n_occ + bp::kRedF4 / q - 1) / (bp::kRedF4 / q);
+  // parts [tiles][2][q] float4 | arrival counters | gsum [n_occ][q] float4 |
+  // k_bwd_reduce parts [rtiles][2][q] float4
+  return (((long long)tiles * 2 * q * 16 + 255) & ~255ll) + ((tiles * 4 + 255) & ~255ll) + n_occ * q * 16 +
+         rtiles * 2 * q * 16 + 256;
 }
 
 static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, float* d_values, int32_t row_stride,
@@ -1691,20 +1918,56 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
   cudaStream_t s = (cudaStream_t)stream;
   switch (g_bwd_variant) {
     case 0:
-    case 4: {
-      const int q = dim / 4, T = kStagedF4 / q;
+    case 4:
+    case 5:
+    case 6: {
+      const int q = dim / 4, T = kStagedF4 / 2 / q;  // scratch layout of the smallest tiles
       const unsigned tiles = (unsigned)((P->n_occ + T - 1) / T);
       const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
       const bool own = own_scratch && own_bytes >= (size_t)bp_embbag_bwd_scratch_bytes(P->n_occ, dim);
       char* scratch = own ? own_scratch : nullptr;
-      if (!own) BP_CUDA_TRY(pool_alloc(&scratch, parts_bytes + tiles * sizeof(unsigned int) + 256, s));
+      if (!own) BP_CUDA_TRY(pool_alloc(&scratch, (size_t)bp_embbag_bwd_scratch_bytes(P->n_occ, dim), s));
       float4* parts = reinterpret_cast<float4*>(scratch);
       unsigned int* arrivals = reinterpret_cast<unsigned int*>(scratch + parts_bytes);
       if (!own) BP_CUDA_TRY(cudaMemsetAsync(arrivals, 0, tiles * sizeof(unsigned int), s));
-      if (g_bwd_variant == 0) {
-        const size_t psmem = (size_t)kPipeStages * ((size_t)T * q * sizeof(float4) + (size_t)T * sizeof(uint32_t)) +
-                             (size_t)T * sizeof(int32_t);
-        const unsigned grid = tiles < 2u * kNumSMs ? tiles : 2u * kNumSMs;
+      if (g_bwd_variant == 4) {
+        float4* gsum = reinterpret_cast<float4*>(scratch + parts_bytes + ((tiles * sizeof(unsigned int) + 255) & ~size_t(255)));
+        const int Tr = kRedF4 / q;
+        const unsigned rtiles = (unsigned)((P->n_occ + Tr - 1) / Tr);
+        float4* rparts = gsum + (size_t)P->n_occ * q;  // [rtiles][2][q] after gsum
+        const size_t rsmem = (size_t)kPipeStages * ((size_t)Tr * q * sizeof(float4) + (size_t)Tr * sizeof(uint32_t));
+        const unsigned grid = rtiles < 4u * kNumSMs ? rtiles : 4u * kNumSMs;
+        const int agrid = grid_for(P->n_occ * q, 256, 1 << 30);
+#define BP_BWD_SPLIT(QQ)                                                                                       \
+  {                                                                                                            \
+    static bool attr = false;                                                                                  \
+    if (!attr) {                                                                                               \
+      BP_CUDA_TRY(cudaFuncSetAttribute(k_bwd_reduce<QQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                       (int)rsmem));                                                           \
+      attr = true;                                                                                             \
+    }                                                                                                          \
+    k_bwd_reduce<QQ><<<grid, 256, rsmem, s>>>(P->d_seg_of, (uint32_t)P->n_occ, rtiles,                          \
+                                              reinterpret_cast<const float4*>(d_grad_sorted), gsum, rparts);   \
+    k_bwd_apply<QQ><<<agrid, 256, 0, s>>>(P->d_seg_start, P->d_num_unique, gsum, rparts, d_values, row_stride, \
+                                          d_slots_s, d_dirty, opt, lr, eps, (unsigned long long*)d_stats);     \
+  }
+        switch (q) {
+          case 1: BP_BWD_SPLIT(1); break;
+          case 2: BP_BWD_SPLIT(2); break;
+          case 4: BP_BWD_SPLIT(4); break;
+          default: BP_BWD_SPLIT(8); break;
+        }
+#undef BP_BWD_SPLIT
+        BP_LAUNCH_CHECK();
+        if (!own) cudaFreeAsync(scratch, s);
+        return BP_OK;
+      }
+      if (g_bwd_variant == 5) {
+        const int Tp = kStagedF4 / q;
+        const size_t psmem = (size_t)kPipeStages * ((size_t)Tp * q * sizeof(float4) + (size_t)Tp * sizeof(uint32_t)) +
+                             (size_t)Tp * sizeof(int32_t);
+        const unsigned ptiles = (unsigned)((P->n_occ + kStagedF4 / q - 1) / (kStagedF4 / q));
+        const unsigned grid = ptiles < 2u * kNumSMs ? ptiles : 2u * kNumSMs;
 #define BP_BWD_PIPE(QQ)                                                                                        \
   {                                                                                                            \
     static bool attr = false;                                                                                  \
@@ -1713,7 +1976,7 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
                                        (int)psmem));                                                           \
       attr = true;                                                                                             \
     }                                                                                                          \
-    k_embbag_bwd_pipe<QQ><<<grid, 256, psmem, s>>>(P->d_seg_of, P->d_seg_start, (uint32_t)P->n_occ, tiles,      \
+    k_embbag_bwd_pipe<QQ><<<grid, 256, psmem, s>>>(P->d_seg_of, P->d_seg_start, (uint32_t)P->n_occ, ptiles,     \
                                                    reinterpret_cast<const float4*>(d_grad_sorted), d_values,    \
                                                    row_stride, d_slots_s, d_dirty, opt, lr, eps, parts,         \
                                                    arrivals, (unsigned long long*)d_stats);                     \
@@ -1729,25 +1992,39 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
         if (!own) cudaFreeAsync(scratch, s);
         return BP_OK;
       }
-      const size_t smem = (size_t)T * q * sizeof(float4) + 2 * (size_t)T * sizeof(uint32_t);
-#define BP_BWD_STAGED(QQ)                                                                                      \
+      // one-shot staged tiles: 32 KB x 256 threads (variant 4) or 16 KB x 128
+      // threads (variant 6: twice the CTAs resident per SM)
+      const bool small = g_bwd_variant == 6;
+      const int Ts = (small ? kStagedF4 / 2 : kStagedF4) / q;
+      const unsigned stiles = (unsigned)((P->n_occ + Ts - 1) / Ts);
+      const size_t smem = (size_t)Ts * q * sizeof(float4) + 2 * (size_t)Ts * sizeof(uint32_t);
+#define BP_BWD_STAGED(QQ, NT, F4)                                                                              \
   {                                                                                                            \
     static bool attr = false;                                                                                  \
     if (!attr) {                                                                                               \
-      BP_CUDA_TRY(cudaFuncSetAttribute(k_embbag_bwd_staged<QQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                       (int)smem));                                                            \
+      BP_CUDA_TRY(cudaFuncSetAttribute(k_embbag_bwd_staged<QQ, NT, F4>,                                        \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
       attr = true;                                                                                             \
     }                                                                                                          \
-    k_embbag_bwd_staged<QQ><<<tiles, 256, smem, s>>>(P->d_seg_of, P->d_seg_start, (uint32_t)P->n_occ,           \
-                                                     reinterpret_cast<const float4*>(d_grad_sorted), d_values,  \
-                                                     row_stride, d_slots_s, d_dirty, opt, lr, eps, parts,       \
-                                                     arrivals, (unsigned long long*)d_stats);                   \
+    k_embbag_bwd_staged<QQ, NT, F4><<<stiles, NT, smem, s>>>(                                                  \
+        P->d_seg_of, P->d_seg_start, (uint32_t)P->n_occ, reinterpret_cast<const float4*>(d_grad_sorted),       \
+        d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts, arrivals,                               \
+        (unsigned long long*)d_stats);                                                                         \
   }
-      switch (q) {
-        case 1: BP_BWD_STAGED(1); break;
-        case 2: BP_BWD_STAGED(2); break;
-        case 4: BP_BWD_STAGED(4); break;
-        default: BP_BWD_STAGED(8); break;
+      if (small) {
+        switch (q) {
+          case 1: BP_BWD_STAGED(1, 128, kStagedF4 / 2); break;
+          case 2: BP_BWD_STAGED(2, 128, kStagedF4 / 2); break;
+          case 4: BP_BWD_STAGED(4, 128, kStagedF4 / 2); break;
+          default: BP_BWD_STAGED(8, 128, kStagedF4 / 2); break;
+        }
+      } else {
+        switch (q) {
+          case 1: BP_BWD_STAGED(1, 256, kStagedF4); break;
+          case 2: BP_BWD_STAGED(2, 256, kStagedF4); break;
+          case 4: BP_BWD_STAGED(4, 256, kStagedF4); break;
+          default: BP_BWD_STAGED(8, 256, kStagedF4); break;
+        }
       }
 #undef BP_BWD_STAGED
       BP_LAUNCH_CHECK();

@@ -1,0 +1,4 @@
+set -u
+mkdir -p gpurun_out/p10
+timeout 600 python -m pytest tests/test_gpu_dlrm.py tests/test_gpu_ck_dlrm.py -x -q > gpurun_out/p10/dlrm.log 2>&1; echo "dlrm rc=$?"
+timeout 300 python tools/kernel_bench.py > gpurun_out/p10/kernel.json 2> gpurun_out/p10/kernel.err; echo "kernel rc=$?"
