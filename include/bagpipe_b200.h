@@ -581,6 +581,16 @@ typedef struct bp_sgd_tensors {
 } bp_sgd_tensors;
 int bp_dlrm_master_sgd(const bp_sgd_tensors* tensors, float lr, bp_stream_t stream);
 
+/* --------------------------------------------------------- trace ingest */
+/* EMTRC1 records -> device batch columns (replaces the per-record decode of
+ * reference traces.py:231-296, iter_trace / read_trace).  d_records holds n
+ * packed records "<B{num_dense}f{num_tables}Q" (the bytes after the
+ * header); outputs: d_keys[n*T] packed (t << 44 | row) in occurrence order,
+ * d_occ_labels[n*T] (the label of each occurrence), d_labels[n] and
+ * d_dense[n*D] (either may be NULL). */
+int bp_trace_decode(const uint8_t* d_records, int64_t n, int32_t num_dense, int32_t num_tables, uint64_t* d_keys,
+                    uint8_t* d_occ_labels, uint8_t* d_labels, float* d_dense, bp_stream_t stream);
+
 /* ------------------------------------------------------------ utilities */
 /* Debug: per-CTA phase clock64() stamps of the long-segment trainer kernel
  * into d_buf[148][8] (NULL disables; tools/kernel_bench.py --trace). */

@@ -201,6 +201,7 @@ _SIGS = {
     "bp_engine_dlrm_backward_peer_begin": (c_i32, [c_vp, c_i64, c_i32, P(PeerXchg), c_f32, c_i32, c_i32, c_f32,
                                                    c_f32, c_i32, c_i32]),
     "bp_host_rows_bench": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp]),
+    "bp_trace_decode": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bp_engine_set_link_mode": (c_i32, [c_vp, c_i32, c_i32]),
     "bp_engine_train_begin": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_u64, c_i32, c_i32, c_i32]),
     "bp_engine_train_end": (c_i32, [c_vp, P(StepResult)]),

@@ -32,6 +32,7 @@ import json
 import math
 import os
 import threading
+import time
 from bisect import bisect_right
 from collections import deque
 from dataclasses import asdict, dataclass, field
@@ -190,6 +191,7 @@ class _Pipeline:
         self.n = len(batches)
         self.T = cfg.num_trainers
         self.device_inputs = device_inputs  # optional {pos: (d_keys, d_labels)} already in HBM
+        self.timing = bool(timing)
         self.probe = None
         self.lib = L.lib()
         self.trainer = trainer  # None: the reference's stub trainer; else e.g. dlrm.DLRMTrainer
@@ -543,6 +545,8 @@ class _Pipeline:
             self._thread = None
 
     def begin(self) -> None:
+        self._wall0 = time.perf_counter()
+        self._wall_marks = []
         if self._threaded:
             self._device = torch.cuda.current_device()
             self._thread = threading.Thread(target=self._planner_loop, name="bagpipe-planner", daemon=True)
@@ -744,6 +748,8 @@ class _Pipeline:
                 if not np.array_equal(expect, got):
                     raise EngineError(f"planner mirror diverged at position {pos}: "
                                       f"{len(expect)} mirrored vs {len(got)} resident")
+        if getattr(self, "_wall_marks", None) is not None:
+            self._wall_marks.append(time.perf_counter())
         rec = IterationRecord(
             iteration=partial["iteration"], warmup=partial["warmup"], compute=partial["compute"],
             critical_sync=partial["critical_sync"], blocked_on_prefetch=partial["blocked_on_prefetch"],
@@ -773,19 +779,32 @@ class _Pipeline:
             "store_entries_written": self.store.entries_written,
             "store_write_calls": self.store.write_calls,
         })
+        marks = getattr(self, "_wall_marks", None) or []
+        t0 = getattr(self, "_wall0", None)
+        wall = [round((b - a) * 1e3, 6) for a, b in zip([t0] + marks[:-1], marks)] if t0 is not None else []
+        measured = {"clock": "measured (host perf_counter; device stage spans when the engine times stages)",
+                    "wall_ms_per_iteration": wall, "wall_ms_total": round(sum(wall), 6),
+                    "device": torch.cuda.get_device_name() if torch.cuda.is_available() else None}
+        if self.timing:
+            measured["stage_ms"] = {k: v[0] for k, v in self.stage_times().items()}
         return RunReport(
             kind="pipelined", config=self.cfg.to_dict(), schema=_schema_dict(self.schema), iterations_run=self.n,
             initial_lookahead=self.L0, final_lookahead=self.lookahead, flush_interval=self.flush_interval,
             totals=totals, metadata=dict(_METADATA), final_store_digest=digest, trace_fingerprint=self.fingerprint,
             flushes=self.flush_log, records=self.records, events=self.events, final_store=self.store,
+            measured=measured,
         )
 
 
 def run_pipeline(cfg: EngineConfig, schema: Schema, trace: Iterable[Batch], *, trace_fingerprint=None,
-                 fault=None) -> RunReport:
-    """Run the pipelined engine over a batch stream (reference run_bagpipe)."""
+                 fault=None, measure_stages: bool = False, device_inputs=None) -> RunReport:
+    """Run the pipelined engine over a batch stream (reference run_bagpipe).
+    measure_stages: also record per-stage device time (CUDA events) into the
+    report's measured-timing sidecar; device_inputs: {position: (d_keys,
+    d_labels)} of batches already in HBM (ingest.DeviceTrace.batch_inputs)."""
     batches = _materialize(trace, cfg.iterations)
-    return _Pipeline(cfg, schema, batches, trace_fingerprint, fault).run()
+    return _Pipeline(cfg, schema, batches, trace_fingerprint, fault, timing=measure_stages,
+                     device_inputs=device_inputs).run()
 
 
 run_bagpipe = run_pipeline

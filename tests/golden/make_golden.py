@@ -386,6 +386,59 @@ def gen_api():
     dump("api.json", out)
 
 
+def gen_cli():
+    """Outputs of the reference CLI itself (reference cli.py; fixtures of
+    tests/test_cli.py:22-51): gen-trace file bytes, plan records, run /
+    baseline report bytes and stdout, verify exit codes."""
+    import contextlib
+    import io
+    import tempfile
+
+    from embcache.cli import main as cli_main
+    from embcache.traces import write_trace
+
+    def call(argv):
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = cli_main(argv)
+        return rc, buf.getvalue()
+
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        gen = os.path.join(td, "gen.trace")
+        rc, so = call(["gen-trace", "--schema", "2:300,200:1:4", "--zipf", "1.05", "--examples", "500", "--seed", "3",
+                       "--out", gen])
+        out["gen_trace"] = {"rc": rc, "stdout": so, "sha256": hashlib.sha256(open(gen, "rb").read()).hexdigest()}
+        zipf = os.path.join(td, "zipf.trace")
+        schema = Schema(2, (600, 400), 2, 4)
+        write_trace(zipf, schema, generate_synthetic_trace(ZipfSpec(schema, 1.05, 30 * 64, seed=7)))
+        worked = os.path.join(td, "fig.trace")
+        wb = [make_batch(1, [3, 9]), make_batch(2, [3, 4]), make_batch(3, [3, 6]), make_batch(4, [1, 6])]
+        write_trace(worked, Schema(1, (10,), 0, 4), [ex for b in wb for ex in b.examples])
+        plans = os.path.join(td, "plans.txt")
+        rc, so = call(["plan", "--trace", worked, "--batch-size", "2", "--lookahead", "2", "--capacity", "100",
+                       "--first-iteration", "1", "--out", plans])
+        out["plan_worked"] = {"rc": rc, "stdout": so, "lines": open(plans).read().splitlines()}
+        rc, so = call(["plan", "--trace", zipf, "--batch-size", "64", "--lookahead", "8", "--capacity", "5000",
+                       "--out", plans])
+        out["plan_zipf"] = {"rc": rc, "stdout": so, "sha256": hashlib.sha256(open(plans, "rb").read()).hexdigest(),
+                            "first": open(plans).read().splitlines()[:3]}
+        cfg = os.path.join(td, "config.json")
+        with open(cfg, "w") as fh:
+            json.dump(dict(cache_capacity=5_000, batch_size=64, lookahead=8, num_trainers=2, seed=5), fh)
+        reports = {}
+        for cmd in ("run", "baseline"):
+            rep = os.path.join(td, f"{cmd}.json")
+            rc, so = call([cmd, "--config", cfg, "--trace", zipf, "--report", rep, "--dump-store"])
+            reports[cmd] = rep
+            out[cmd] = {"rc": rc, "stdout": so, "json": open(rep).read(),
+                        "csv": open(rep[:-5] + ".csv").read(),
+                        "store_sha256": hashlib.sha256(open(rep[:-5] + ".store", "rb").read()).hexdigest()}
+        rc, so = call(["verify", "--a", reports["run"], "--b", reports["baseline"]])
+        out["verify"] = {"rc": rc, "stdout": so}
+    dump("cli.json", out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
@@ -398,6 +451,8 @@ def main():
         gen_planner_and_engine()
     if want("api"):
         gen_api()
+    if want("cli"):
+        gen_cli()
     if want("acceptance"):
         gen_acceptance()
     ck = gen_ck() if want("ck") else None
