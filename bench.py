@@ -53,6 +53,10 @@ WORKLOAD = ("criteo-kaggle-shape 26 tables 33.76M rows D=16 fp32, batch 16384, z
             "lookahead auto(7), pinned-host table; stub-gradient engine iteration (reference run_pipeline)")
 
 
+# N>1 stub-mode sharding: "row" (keys placed by fnv1a64(table, row) mod N,
+# the reference store's placement) or "table" (whole tables per rank)
+SHARDING = os.environ.get("BAGPIPE_B200_SHARDING", "row")
+
 # L2 flush at every iteration start: 0 = the memset runs on the compute
 # stream while the plan / host-link streams keep working (the pipeline stays
 # overlapped across iterations), 1 = every engine stream drained around it
@@ -93,7 +97,7 @@ def bench_config(world: int) -> dict:
     sc_rows = sum(CK_ROWS)
     return {"workload": WORKLOAD, "global_batch": BATCH * world, "per_gpu_batch": BATCH, "tables": len(CK_ROWS),
             "rows": sc_rows, "emb_dim": DIM, "cache_capacity_per_gpu": sc_rows // 100, "lookahead": "auto",
-            "parallelism": "single" if world == 1 else f"table-sharded x{world} (weak: {BATCH} examples/GPU)",
+            "parallelism": "single" if world == 1 else f"{SHARDING}-sharded x{world} (weak: {BATCH} examples/GPU)",
             "num_trainers": world,
             "l2": "flushed at the start of every timed iteration (256 MiB write inside the timed span)",
             "timing": "one CUDA-event span over K steps, end event after joining the plan and host-link streams",
@@ -226,6 +230,29 @@ def planner_bytes(u: int, p: int, e: int) -> int:
     return u * 34 + p * 20 + e * 12
 
 
+def trace_ingest(batches) -> dict:
+    """EMTRC1 file -> decoded device columns: the bench's
+    batches written as a trace file, then streamed into pinned buffers, DMA'd
+    and decoded on the GPU (ingest.read_trace_device); bytes/s of the file."""
+    import tempfile
+
+    from paper_2202_12429_b200.ingest import read_trace_device
+    from paper_2202_12429_b200.traces import write_trace_columns
+
+    rows = np.concatenate([b.rows for b in batches])
+    labels = np.concatenate([b.labels for b in batches])
+    dense = np.concatenate([b.dense for b in batches])
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "ck.trace")
+        write_trace_columns(path, schema(), rows, labels, dense)
+        read_trace_device(path)  # warm: allocations, page cache
+        tr = read_trace_device(path)
+    st = dict(tr.stats)
+    st["note"] = (f"{len(batches)} CK batches ({st['records']} records x 261 B) from the page cache: readinto pinned "
+                  "chunks, H2D DMA, bp_trace_decode (packed keys, occurrence labels, labels, dense)")
+    return st
+
+
 def _timed_steps(pipe, first: int, steps: int, flush_buf, torch, exclusive: int | None = None):
     """K steps as ONE span on the engine's compute stream, bracketed by
     device syncs: CUDA events, the end event recorded after the compute
@@ -323,7 +350,17 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     # batch), largest first to the least-loaded rank
     shards = table_shards(sc.num_tables, world, table_costs(full[0])) if world > 1 else [list(range(sc.num_tables))]
     tables = shards[rank]
-    batches = full if world == 1 else shard_batches(full, tables)
+    if world == 1:
+        batches = full
+    elif SHARDING == "row":
+        from paper_2202_12429_b200.shard import row_shard_batches
+
+        batches = row_shard_batches(full, world, rank)
+    else:
+        batches = shard_batches(full, tables)
+    # DLRM mode (hybrid parallel) keeps whole tables per rank: its pooled-row
+    # exchange is by table
+    dlrm_batches = batches if (world == 1 or SHARDING != "row") else shard_batches(full, tables)
     # N GPUs = the reference's N data-parallel trainers (rank r = examples
     # [r*B/N, (r+1)*B/N) of the global batch; gradients combined in rank order)
     trainers = int(os.environ.get("BAGPIPE_B200_BENCH_TRAINERS", str(world)))
@@ -378,7 +415,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     pf_mean = statistics.mean(r.prefetch_count for r in records)
     ev_mean = statistics.mean(r.evicted_count for r in records)
-    n_occ = gbatch * len(tables)
+    n_occ = int(statistics.mean(b.packed_occurrences()[0].size for b in batches[warm:warm + steps]))
     link_rows = np.zeros(2, dtype=np.int64)  # lazy prefetch over the run: host-link reads, GPU-computed inits
     pipe.lib.bp_store_link_counters(pipe.store.handle, link_rows.ctypes.data)
     host_frac = float(link_rows[0]) / max(int(link_rows.sum()), 1)
@@ -405,7 +442,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     # ---- DLRM mode (N=1): the same engine feeding PyTorch MLPs (bf16 autocast)
     dlrm = None
     if not args.no_dlrm:
-        dlrm = run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank, world, len(tables), shards)
+        dlrm = run_dlrm_mode(args, sc, dlrm_batches, cfg, flush_buf, torch, rank, world, len(tables), shards)
+
+    ingest = None
+    if world == 1 and not args.no_e2e:
+        ingest = trace_ingest(full[:20])
 
     t = torch.tensor([ms, e2e_ms], device="cuda", dtype=torch.float64)
     by_rank = [ms / steps]
@@ -495,6 +536,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                                        "store.py:106-129); only written rows are read over the host link",
                       "peak_note": "pinned memcpy 55.5 GB/s H2D, 56.5 D2H; zero-copy random 64 B rows 18.7-25 GB/s "
                                    "(tools/hostlink_peak.py)"},
+        "trace_ingest": ingest,
         "gpu_launches": launches_per_step * steps,
         "clocks": clk,
         "wall_ms_timed_region": wall_ms,

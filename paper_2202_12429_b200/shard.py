@@ -1,4 +1,5 @@
-"""Table-wise sharding of the embedding path across GPUs (one process per GPU).
+"""Table-wise and row-wise sharding of the embedding path across GPUs (one
+process per GPU).
 
 Every key belongs to exactly one table, and every per-key decision of the
 path -- Algorithm 1's TTLs and prefetches, the cache, the stub gradient's
@@ -14,6 +15,15 @@ key per example, so ranks differ by at most one table's worth of
 occurrences.  With a per-table cost (e.g. unique keys per batch, which drive
 prefetch, insertion, eviction and the trainer) the tables are instead dealt
 longest-processing-time first, each to the rank with the least cost so far.
+
+Row-wise sharding (row_shard_batches) places every KEY by the reference
+store's own placement hash, fnv1a64(table, row) mod N (reference
+store.py:80-88, 100-104): a 10M-row table is spread over all ranks instead of
+landing on one.  A rank's batch holds, example by example, the occurrences of
+its keys (an occurrence-backed Batch: examples carry a variable number of
+keys), so each key keeps all of its occurrences in occurrence order and every
+trainer rank (example index / (B/T), engine.py:159-161) keeps its examples --
+the same per-key arithmetic as one GPU, exact by the same argument.
 """
 
 from __future__ import annotations
@@ -61,6 +71,32 @@ def shard_batches(batches: list, tables: list) -> list:
         cols = [int(np.flatnonzero(b.table_ids() == t)[0]) for t in tables]
         out.append(Batch.from_columns(b.iteration, np.ascontiguousarray(b.rows[:, cols]), b.labels, b.dense,
                                       tables=tables))
+    return out
+
+
+def row_owner(keys: np.ndarray, world: int) -> np.ndarray:
+    """Owning rank of every packed key: fnv1a64(table, row) mod world, the
+    reference store's shard placement (store.py:80-88)."""
+    from .store import shard_of_keys
+
+    keys = np.asarray(keys, dtype=np.uint64)
+    return shard_of_keys(keys >> np.uint64(44), keys & np.uint64((1 << 44) - 1), world)
+
+
+def row_shard_batches(batches: list, world: int, rank: int) -> list:
+    """The rank's occurrences of every batch (keys with row_owner == rank), in
+    occurrence order, as occurrence-backed batches with the original example
+    boundaries (so trainer ranks are unchanged)."""
+    out = []
+    for b in batches:
+        keys, labels, offsets = b.packed_occurrences()
+        mine = row_owner(keys, world) == rank
+        per_ex = np.add.reduceat(mine.astype(np.int64), offsets[:-1]) if keys.size else np.zeros(0, np.int64)
+        # reduceat repeats the value at empty examples: zero them
+        per_ex = np.where(offsets[1:] > offsets[:-1], per_ex, 0)
+        offs = np.zeros(offsets.size, dtype=np.int64)
+        np.cumsum(per_ex, out=offs[1:])
+        out.append(Batch.from_occurrences(b.iteration, keys[mine], labels[mine], offs))
     return out
 
 

@@ -117,7 +117,7 @@ class Batch:
     memo dict.
     """
 
-    __slots__ = ("iteration", "_examples", "rows", "labels", "dense", "tables", "_memo")
+    __slots__ = ("iteration", "_examples", "rows", "labels", "dense", "tables", "_memo", "_n_ex")
 
     def __init__(self, iteration: int, examples=None, *, rows=None, labels=None, dense=None, tables=None):
         self.iteration = int(iteration)
@@ -129,6 +129,7 @@ class Batch:
         # keeps the global ids of its tables (shard.py)
         self.tables = None if tables is None else np.asarray(tables, dtype=np.int64)
         self._memo: dict = {}
+        self._n_ex = None
         if examples is None and rows is None:
             self._examples = []
 
@@ -144,15 +145,40 @@ class Batch:
             raise ConfigurationError("one table id per column")
         return cls(iteration, None, rows=rows, labels=labels, dense=dense, tables=tables)
 
+    @classmethod
+    def from_occurrences(cls, iteration: int, keys: np.ndarray, labels: np.ndarray, offsets: np.ndarray) -> "Batch":
+        """Occurrence-backed batch: packed keys u64[n_occ] in occurrence order,
+        one label byte per occurrence and the example offsets i64[n+1] -- the
+        layout of a row-wise shard (shard.row_shard_batches), whose examples
+        carry a variable number of the rank's keys.  Examples are built only
+        when read."""
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        labels = np.ascontiguousarray(labels, dtype=np.uint8)
+        if offsets.ndim != 1 or offsets.size < 1 or offsets[0] != 0 or offsets[-1] != keys.size:
+            raise ConfigurationError("offsets must run from 0 to the occurrence count")
+        if labels.shape != keys.shape:
+            raise ConfigurationError("one label per occurrence")
+        b = cls(iteration, None, rows=None)
+        b._examples = None
+        b._n_ex = offsets.size - 1
+        b._memo["occ"] = (keys, labels, offsets)
+        return b
+
     def table_ids(self) -> np.ndarray:
         return self.tables if self.tables is not None else np.arange(self.rows.shape[1], dtype=np.int64)
 
     @property
     def is_columnar(self) -> bool:
-        return self._examples is None
+        return self._examples is None and self._n_ex is None
 
     @property
     def examples(self) -> list:
+        if self._examples is None and self._n_ex is not None:  # occurrence-backed
+            keys, labels, offsets = self._memo["occ"]
+            ks = unpack_keys(keys)
+            self._examples = [Example(int(labels[offsets[i]]) if offsets[i + 1] > offsets[i] else 0, (),
+                                      tuple(ks[offsets[i]:offsets[i + 1]])) for i in range(self._n_ex)]
         if self._examples is None:
             n, nt = self.rows.shape
             dense = self.dense
@@ -167,6 +193,8 @@ class Batch:
 
     @property
     def num_examples(self) -> int:
+        if self._n_ex is not None:
+            return self._n_ex
         return self.rows.shape[0] if self._examples is None else len(self._examples)
 
     def __len__(self) -> int:

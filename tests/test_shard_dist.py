@@ -1,4 +1,5 @@
-"""N>1 host logic on CPU with gloo (world_size 2): table-wise shards of the
+"""N>1 host logic on CPU with gloo (world_size 2 and 3): table-wise and
+row-wise (fnv1a64 key placement, reference store.py:80-88) shards of the
 pipelined path, each run by the CPU oracle on its rank, gathered to rank 0,
 reproduce the unsharded final store bit for bit."""
 
@@ -12,7 +13,9 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2202_12429_b200.shard import shard_batches, table_shards
+import pytest
+
+from paper_2202_12429_b200.shard import row_shard_batches, shard_batches, table_shards
 from paper_2202_12429_b200.traces import Schema, ZipfSpec, batchify_columns, generate_columns
 
 SCHEMA = Schema(3, (600, 400, 50), 2, 4)
@@ -29,13 +32,16 @@ def _trace():
     return batchify_columns(rows, labels, dense, 64)
 
 
-def _rank_main(rank, world, port, out):
+def _rank_main(rank, world, port, out, mode="table"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import bagpipe_oracle as O
 
-    tables = table_shards(SCHEMA.num_tables, world)[rank]
-    store, _ = O.pipeline(shard_batches(_trace(), tables), SCHEMA.rows_per_table, 4, 5, 2, 10_000, 6, 0.25)
+    if mode == "table":
+        mine = shard_batches(_trace(), table_shards(SCHEMA.num_tables, world)[rank])
+    else:
+        mine = row_shard_batches(_trace(), world, rank)
+    store, _ = O.pipeline(mine, SCHEMA.rows_per_table, 4, 5, 2, 10_000, 6, 0.25)
     gathered = [None] * world
     dist.all_gather_object(gathered, store.values)
     t = torch.tensor([float(rank + 1)])  # the bench's timing reduction: max over ranks
@@ -49,20 +55,21 @@ def _rank_main(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_table_sharding_is_exact_with_gloo():
+@pytest.mark.parametrize("mode,world", [("table", 2), ("row", 2), ("row", 3)])
+def test_sharding_is_exact_with_gloo(mode, world):
     from oracle import bagpipe_oracle as O
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     merged, tmax = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert tmax == 2.0
+    assert tmax == float(world)
     store, _ = O.pipeline(_trace(), SCHEMA.rows_per_table, 4, 5, 2, 10_000, 6, 0.25)
     assert set(merged) == set(store.values)
     for k, v in store.values.items():
