@@ -333,6 +333,12 @@ int bp_stub_step(bp_ctx* ctx, bp_prep* prep, float* d_rows, const int32_t* d_row
 /* bp_stub_step runs its long-segment kernel on a side stream of the calling
  * thread, concurrently with the short-segment kernel (1, default) or both on
  * `stream` in sequence (0). */
+/* Tuning: CTAs per SM of the short-segment stub trainer kernel (1..6,
+ * default 5: one slot per SM stays free for the long-segment kernel). */
+int bp_set_stub_short_ctas(int32_t per_sm);
+/* Tuning: preferred shared-memory carveout (%) of the short-segment kernel
+ * (default 100; -1 = driver default).  Set before the first bp_stub_step. */
+int bp_set_stub_carveout(int32_t percent);
 int bp_set_stub_fork(int32_t on);
 /* mark[id] = tag for every unique key of a schema-mode prep. */
 int bp_mark_ids(bp_prep* prep, int64_t* d_mark, int64_t tag, bp_stream_t stream);

@@ -209,6 +209,8 @@ _SIGS = {
     "bp_set_link_config": (c_i32, [c_i32, c_i32, c_i32]),
     "bp_set_write_blocks": (c_i32, [c_i32]),
     "bp_set_stub_fork": (c_i32, [c_i32]),
+    "bp_set_stub_short_ctas": (c_i32, [c_i32]),
+    "bp_set_stub_carveout": (c_i32, [c_i32]),
     "bp_dlrm_master_sgd": (c_i32, [P(SgdTensors), c_f32, c_vp]),
     "bp_engine_dlrm_backward_begin": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_i32, c_f32, c_f32, c_i32,
                                               c_i32]),
@@ -296,6 +298,12 @@ def lib() -> C.CDLL:
                 sk = os.environ.get("BAGPIPE_B200_DEBUG_SKIP_LINK")  # debug only: results become wrong
                 if sk:
                     check(lb.bp_debug_skip_link(int(sk)), "bp_debug_skip_link")
+                co = os.environ.get("BAGPIPE_B200_STUB_CARVEOUT")  # tuning knob: short kernel smem carveout %
+                if co:
+                    check(lb.bp_set_stub_carveout(int(co)), "bp_set_stub_carveout")
+                sc_ = os.environ.get("BAGPIPE_B200_STUB_SHORT_CTAS")  # tuning knob: short trainer CTAs per SM
+                if sc_:
+                    check(lb.bp_set_stub_short_ctas(int(sc_)), "bp_set_stub_short_ctas")
                 sf = os.environ.get("BAGPIPE_B200_STUB_FORK")  # tuning knob: long trainer kernel beside the short
                 if sf:
                     check(lb.bp_set_stub_fork(int(sf)), "bp_set_stub_fork")

@@ -520,12 +520,20 @@ static SideStream& side_stream() {
 }
 
 static bool g_fork_long = true;
+static int g_short_ctas = 5;  // tuning knob (bp_set_stub_short_ctas): short-kernel CTAs per SM
+
+static int g_short_carveout = 100;  // tuning knob: shared-memory carveout (%) of the short kernel
 
 template <int G, int DPL>
 static void long_attr() {
   static bool done = false;
   if (!done) {
     cudaFuncSetAttribute(bp::k_stub_step_long<G, DPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bp::kLongSmemPad);
+    // the short kernel's SMs keep the shared-memory carveout a long CTA
+    // needs: with a small carveout an SM running short CTAs would have to
+    // drain before it could take a long one (measured: the hot-key chains
+    // then started ~25 us after the short kernel instead of beside it)
+    cudaFuncSetAttribute(bp::k_stub_step<G, DPL>, cudaFuncAttributePreferredSharedMemoryCarveout, g_short_carveout);
     done = true;
   }
 }
@@ -542,7 +550,10 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   cudaStream_t s = (cudaStream_t)stream;
   const long long groups = P->n_occ;  // upper bound on U
   const int threads = 256;
-  const int blocks = grid_for(groups * G, threads, kNumSMs * 6);
+  // grid: g_short_ctas CTAs per SM (grid-stride).  5 (default) of the 6 that
+  // fit leave every SM room for one long-segment CTA, so the hot-key chains
+  // start when they are launched instead of after the whole short kernel
+  const int blocks = grid_for(groups * G, threads, kNumSMs * g_short_ctas);
   // the long-segment kernel (a few sequential hot-key chains) runs on a side
   // stream beside the short-segment kernel: the two touch disjoint keys
   cudaStream_t ls = s;
@@ -593,6 +604,18 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
     BP_CUDA_TRY(cudaEventRecord(side.join, ls));
     BP_CUDA_TRY(cudaStreamWaitEvent(s, side.join, 0));
   }
+  return BP_OK;
+}
+
+extern "C" int bp_set_stub_carveout(int32_t percent) {
+  if (percent < -1 || percent > 100) return BP_ERR_INVALID;
+  g_short_carveout = percent;
+  return BP_OK;
+}
+
+extern "C" int bp_set_stub_short_ctas(int32_t per_sm) {
+  if (per_sm < 1 || per_sm > 6) return BP_ERR_INVALID;
+  g_short_ctas = per_sm;
   return BP_OK;
 }
 
