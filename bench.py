@@ -53,9 +53,50 @@ WORKLOAD = ("criteo-kaggle-shape 26 tables 33.76M rows D=16 fp32, batch 16384, z
             "lookahead auto(7), pinned-host table; stub-gradient engine iteration (reference run_pipeline)")
 
 
+NUM_DENSE = 13
+SHAPE = "ck"
+
+# BASELINE.json configs 3 and 4 as alternative workloads (--shape): the
+# headline line (the driver's) is configs[1], the Criteo-Kaggle shape.
+# Avazu: 22 categorical tables summing to 9,449,206 rows ("9.4M"; the
+# split is ours, the reference ships none), D=16, batch 16,384.  tb10: the
+# Criteo-Terabyte cardinalities / 10 (88.3M rows, 22.6 GB pinned fp32 store),
+# D=64, batch 65,536.
+SHAPES = {
+    "ck": dict(rows=CK_ROWS, batch=16384, dim=16, dense=13, workload=WORKLOAD),
+    "avazu": dict(rows=(7, 7, 4737, 7745, 26, 8552, 559, 36, 2686408, 6729486, 8251, 5, 4, 2626, 8, 9, 435, 4, 68,
+                        172, 60, 1), batch=16384, dim=16, dense=1,
+                  workload="avazu-shape 22 tables 9.45M rows D=16 fp32, batch 16384, zipf 1.05, HBM cache 1% of "
+                           "rows, lookahead auto, pinned-host table; stub-gradient engine iteration"),
+    "tb10": dict(rows=tuple(max(1, r // 10) for r in (227605432, 39060, 17295, 7424, 20265, 3, 7122, 1543, 63,
+                                                       130229467, 3067956, 405282, 10, 2209, 11938, 155, 4, 976, 14,
+                                                       292775614, 40790948, 187188510, 590152, 12973, 108, 36)),
+                 batch=65536, dim=64, dense=13,
+                 workload="criteo-terabyte-shape / 10: 26 tables 88.3M rows D=64 fp32, batch 65536, zipf 1.05, HBM "
+                          "cache 1% of rows, lookahead auto, pinned-host table; stub-gradient engine iteration"),
+}
+
+
+def apply_shape(name: str) -> None:
+    """Rebind the workload constants to one of SHAPES."""
+    global CK_ROWS, BATCH, DIM, NUM_DENSE, WORKLOAD, SHAPE
+    sh = SHAPES[name]
+    CK_ROWS, BATCH, DIM, NUM_DENSE, WORKLOAD, SHAPE = (sh["rows"], sh["batch"], sh["dim"], sh["dense"],
+                                                       sh["workload"], name)
+
+
 # N>1 stub-mode sharding: "row" (keys placed by fnv1a64(table, row) mod N,
-# the reference store's placement) or "table" (whole tables per rank)
-SHARDING = os.environ.get("BAGPIPE_B200_SHARDING", "row")
+# the reference store's placement), "table" (whole tables per rank), or
+# "auto": tables up to N=4 (measured faster: 0.226 vs 0.281 ms/step at N=4,
+# the columnar cluster prep applies), rows from N=8 (26 tables cannot be
+# balanced over 8 ranks when one holds 10.1M rows)
+SHARDING_MODE = os.environ.get("BAGPIPE_B200_SHARDING", "auto")
+
+
+def sharding(world: int) -> str:
+    if SHARDING_MODE != "auto":
+        return SHARDING_MODE
+    return "table" if world <= 4 else "row"
 
 # L2 flush at every iteration start: 0 = the memset runs on the compute
 # stream while the plan / host-link streams keep working (the pipeline stays
@@ -75,13 +116,15 @@ def parse():
     ap.add_argument("--no-dlrm", action="store_true")
     ap.add_argument("--no-link-probe", action="store_true", help="skip the host-link-disabled comparison run")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--shape", default="ck", choices=sorted(SHAPES),
+                    help="workload: ck (BASELINE configs[1], the headline), avazu (configs[2]), tb10 (configs[3] / 10)")
     return ap.parse_args()
 
 
 def schema():
     from paper_2202_12429_b200.traces import Schema
 
-    return Schema(26, CK_ROWS, 13, DIM)
+    return Schema(len(CK_ROWS), CK_ROWS, NUM_DENSE, DIM)
 
 
 def make_batches(n_batches: int, seed: int, batch: int = BATCH):
@@ -97,7 +140,7 @@ def bench_config(world: int) -> dict:
     sc_rows = sum(CK_ROWS)
     return {"workload": WORKLOAD, "global_batch": BATCH * world, "per_gpu_batch": BATCH, "tables": len(CK_ROWS),
             "rows": sc_rows, "emb_dim": DIM, "cache_capacity_per_gpu": sc_rows // 100, "lookahead": "auto",
-            "parallelism": "single" if world == 1 else f"{SHARDING}-sharded x{world} (weak: {BATCH} examples/GPU)",
+            "parallelism": "single" if world == 1 else f"{sharding(world)}-sharded x{world} (weak: {BATCH} examples/GPU)",
             "num_trainers": world,
             "l2": "flushed at the start of every timed iteration (256 MiB write inside the timed span)",
             "timing": "one CUDA-event span over K steps, end event after joining the plan and host-link streams",
@@ -352,7 +395,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     tables = shards[rank]
     if world == 1:
         batches = full
-    elif SHARDING == "row":
+    elif sharding(world) == "row":
         from paper_2202_12429_b200.shard import row_shard_batches
 
         batches = row_shard_batches(full, world, rank)
@@ -360,7 +403,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         batches = shard_batches(full, tables)
     # DLRM mode (hybrid parallel) keeps whole tables per rank: its pooled-row
     # exchange is by table
-    dlrm_batches = batches if (world == 1 or SHARDING != "row") else shard_batches(full, tables)
+    dlrm_batches = batches if (world == 1 or sharding(world) != "row") else shard_batches(full, tables)
     # N GPUs = the reference's N data-parallel trainers (rank r = examples
     # [r*B/N, (r+1)*B/N) of the global batch; gradients combined in rank order)
     trainers = int(os.environ.get("BAGPIPE_B200_BENCH_TRAINERS", str(world)))
@@ -675,7 +718,7 @@ def cpu_oracle(steps: int, warmup: int, seed: int) -> dict:
     sc = schema()
     batches = make_batches(warmup + steps + 10, seed)
     cap = sc.total_rows // 100
-    run = O.OraclePipeline(batches, CK_ROWS, DIM, 11, 1, cap, 7, 0.25)
+    run = O.OraclePipeline(batches, CK_ROWS, DIM, 11, 1, cap, 7 if SHAPE == "ck" else 0, 0.25)
     run.begin()
     for pos in range(warmup):
         run.step(pos)
@@ -690,6 +733,9 @@ def cpu_oracle(steps: int, warmup: int, seed: int) -> dict:
 
 def main():
     args = parse()
+    apply_shape(args.shape)
+    if args.shape != "ck":
+        args.no_dlrm = True  # the DLRM-mode line is the Criteo-Kaggle model
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

@@ -339,6 +339,12 @@ int bp_set_stub_short_ctas(int32_t per_sm);
 /* Tuning: preferred shared-memory carveout (%) of the short-segment kernel
  * (default 100; -1 = driver default).  Set before the first bp_stub_step. */
 int bp_set_stub_carveout(int32_t percent);
+/* Tuning: green-context SM partition of engines created afterwards: the
+ * stub trainer's hot-key chains run on `sms` SMs of their own, every other
+ * engine stream on the rest (0 = off, the default). */
+int bp_set_green_sms(int32_t sms);
+/* {hot-partition SMs, rest SMs} of the partition in use ({0, 0} when off). */
+int bp_green_info(int32_t* out2);
 int bp_set_stub_fork(int32_t on);
 /* mark[id] = tag for every unique key of a schema-mode prep. */
 int bp_mark_ids(bp_prep* prep, int64_t* d_mark, int64_t tag, bp_stream_t stream);

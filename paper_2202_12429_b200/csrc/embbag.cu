@@ -31,13 +31,15 @@ constexpr int kSpanSmallBlocks = 148 * 2;  // CTAs of k_embbag_bwd_span on those
 // lane per (occurrence, 4 components): coalesced pooled writes in occurrence
 // order, row reads from the (L2-resident) cache arena, no per-key serial loop
 // (a Zipf-hot key has ~9K occurrences per Criteo-Kaggle batch).
+template <int QT>  // QT > 0: the float4s per row at compile time (shifts instead of divisions); 0: runtime q
 __global__ void __launch_bounds__(256) k_embbag_fwd_rows_v4(const uint32_t* __restrict__ occ_s,
                                                            const int32_t* __restrict__ slots_s,
-                                                           const float4* __restrict__ values, int q,
+                                                           const float4* __restrict__ values, int q_rt,
                                                            int row_q, long long n, float4* __restrict__ out) {
   // 4 elements per thread, their three dependent loads (unique index, slot,
   // row) issued as batches so the latency chain is paid once per 4 rows
   constexpr int U = 4;
+  const int q = QT > 0 ? QT : q_rt;
   const long long total = n * q;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += stride * U) {
@@ -47,14 +49,14 @@ __global__ void __launch_bounds__(256) k_embbag_fwd_rows_v4(const uint32_t* __re
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const long long i = i0 + k * stride;
-      u[k] = i < total ? occ_s[i / q] : 0u;
+      u[k] = i < total ? __ldg(occ_s + i / q) : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < U; ++k) sl[k] = i0 + k * stride < total ? slots_s[u[k]] : -1;
+    for (int k = 0; k < U; ++k) sl[k] = i0 + k * stride < total ? __ldg(slots_s + u[k]) : -1;
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const long long i = i0 + k * stride;
-      const int c = (int)(i - (i / q) * q);
+      const int c = (int)(i % q);
       v[k] = sl[k] >= 0 ? values[(long long)sl[k] * row_q + c] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
@@ -1727,9 +1729,17 @@ extern "C" int bp_embbag_forward(bp_prep* P, const float* d_values, int32_t row_
         P->n_occ, reinterpret_cast<float4*>(d_out));
   } else if (!d_bag_offsets && (dim & 3) == 0 && (row_stride & 3) == 0) {
     const int q = dim / 4;
-    k_embbag_fwd_rows_v4<<<grid_for(P->n_occ * q, 256 * 4, kNumSMs * 8), 256, 0, s>>>(
-        d_occ_s, d_slots_s, reinterpret_cast<const float4*>(d_values), q, row_stride / 4, P->n_occ,
-        reinterpret_cast<float4*>(d_out));
+    const int fg = grid_for(P->n_occ * q, 256 * 4, kNumSMs * 8);
+    const float4* vals4 = reinterpret_cast<const float4*>(d_values);
+    float4* out4 = reinterpret_cast<float4*>(d_out);
+    switch (q) {
+      case 1: k_embbag_fwd_rows_v4<1><<<fg, 256, 0, s>>>(d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, out4); break;
+      case 2: k_embbag_fwd_rows_v4<2><<<fg, 256, 0, s>>>(d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, out4); break;
+      case 4: k_embbag_fwd_rows_v4<4><<<fg, 256, 0, s>>>(d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, out4); break;
+      case 8: k_embbag_fwd_rows_v4<8><<<fg, 256, 0, s>>>(d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, out4); break;
+      case 16: k_embbag_fwd_rows_v4<16><<<fg, 256, 0, s>>>(d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, out4); break;
+      default: k_embbag_fwd_rows_v4<0><<<fg, 256, 0, s>>>(d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, out4); break;
+    }
   } else {
     if (!d_bag_offsets) return BP_ERR_INVALID;
     const int blocks = grid_for(n_bags * G, 256, kNumSMs * 8);

@@ -416,13 +416,31 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   BP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   // Compute at the highest priority: the host-link kernels only wait on PCIe
   // and must not delay the critical path's CTAs.
-  BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->compute, cudaStreamNonBlocking, hi));
-  BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->link, cudaStreamNonBlocking, lo));
-  // Batch prep and the planner window step of batches entering the window run
-  // on their own stream: they depend only on the trace, so they overlap the
-  // training of the iterations ahead of them.
-  BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->planq, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
-  BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->prepq, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
+  // With a green-context SM partition (bp_set_green_sms) every engine stream
+  // lives in the rest partition and the hot-key chains get the hot one.
+  cudaStream_t gs = nullptr;
+  {
+    int grc = green_stream(0, hi, &gs);
+    if (grc) return grc;
+  }
+  if (gs) {
+    e->compute = gs;
+    int grc = green_stream(0, lo, &e->link);
+    if (!grc) grc = green_stream(0, hi < lo ? hi + 1 : hi, &e->planq);
+    if (!grc) grc = green_stream(0, hi < lo ? hi + 1 : hi, &e->prepq);
+    cudaStream_t hs = nullptr;
+    if (!grc) grc = green_stream(1, hi, &hs);
+    if (grc) return grc;
+    set_long_stream(hs);
+  } else {
+    BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->compute, cudaStreamNonBlocking, hi));
+    BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->link, cudaStreamNonBlocking, lo));
+    // Batch prep and the planner window step of batches entering the window run
+    // on their own stream: they depend only on the trace, so they overlap the
+    // training of the iterations ahead of them.
+    BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->planq, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
+    BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->prepq, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
+  }
   int rc = bp_store_create_ex(ctx, sc, cfg->seed, cfg->init_dims > 0 ? cfg->init_dims : sc->emb_dim, e->compute,
                               &e->store);
   if (rc) return rc;

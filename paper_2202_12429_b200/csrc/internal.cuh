@@ -75,6 +75,12 @@ __device__ __forceinline__ uint32_t registry_find(const uint64_t* keys, const ui
   return kNoId;
 }
 
+// Green-context SM partition (green.cu): a stream of the hot (hot != 0) or
+// the rest partition, or nullptr when partitioning is off.
+int green_stream(int hot, int priority, cudaStream_t* out);
+// The stub trainer's hot-key chains go to this stream when set (trainer.cu).
+void set_long_stream(cudaStream_t s);
+
 // Dense id of a packed key in schema mode; kNoId if out of schema.
 __device__ __forceinline__ uint32_t schema_id(const int64_t* base, const int64_t* rows, int num_tables,
                                               uint64_t key) {

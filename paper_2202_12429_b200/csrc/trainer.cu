@@ -520,6 +520,7 @@ static SideStream& side_stream() {
 }
 
 static bool g_fork_long = true;
+static cudaStream_t g_long_stream = nullptr;  // engine-provided stream for the chains (green partition)
 static int g_short_ctas = 5;  // tuning knob (bp_set_stub_short_ctas): short-kernel CTAs per SM
 
 static int g_short_carveout = 100;  // tuning knob: shared-memory carveout (%) of the short kernel
@@ -560,9 +561,9 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   if (g_fork_long) {
     SideStream& side = side_stream();
     if (!side.s) return BP_ERR_CUDA;
+    ls = g_long_stream ? g_long_stream : side.s;
     BP_CUDA_TRY(cudaEventRecord(side.fork, s));
-    BP_CUDA_TRY(cudaStreamWaitEvent(side.s, side.fork, 0));
-    ls = side.s;
+    BP_CUDA_TRY(cudaStreamWaitEvent(ls, side.fork, 0));
   }
   // T > 1: the long keys' rank runs are separate chains (rank partials in a
   // stream-ordered scratch), combined in rank order by k_stub_long_combine
@@ -606,6 +607,10 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   }
   return BP_OK;
 }
+
+namespace bp {
+void set_long_stream(cudaStream_t s) { g_long_stream = s; }
+}  // namespace bp
 
 extern "C" int bp_set_stub_carveout(int32_t percent) {
   if (percent < -1 || percent > 100) return BP_ERR_INVALID;
