@@ -541,6 +541,17 @@ int bp_ipc_free(void* d_ptr);
 int bp_peer_barrier(bp_ctx* ctx, const bp_peer_xchg* x, uint32_t epoch, bp_stream_t stream);
 /* EmbeddingBag forward of single-key bags straight into the example owners'
  * row buffers (d_peer_rows of `rows`). */
+/* The peer backward through the key-sorted path: the rank's gradient rows
+ * pulled over NVLink into key-sorted order in d_sorted (n_occ * dim floats),
+ * then the staged sorted backward (d_scratch: bp_embbag_bwd_scratch_bytes,
+ * zeroed once). */
+int bp_embbag_backward_peer_sorted(bp_prep* prep, const bp_peer_xchg* grads, float scale, float* d_values,
+                                   int32_t row_stride, const int32_t* d_slots_s, uint8_t* d_dirty, int32_t dim,
+                                   int32_t opt, float lr, float eps, int64_t* d_stats, float* d_sorted,
+                                   void* d_scratch, int64_t scratch_bytes, bp_stream_t stream);
+/* Engine peer backward: 1 (default) = the key-sorted path above, 0 = the
+ * reduce-by-key gather straight from the peers' buffers. */
+int bp_set_peer_sorted(int32_t on);
 int bp_embbag_forward_peer(bp_prep* prep, const float* d_values, int32_t row_stride, const int32_t* d_slots_s,
                            int32_t dim, const bp_peer_xchg* rows, bp_stream_t stream);
 /* EmbeddingBag backward + optimizer reading each occurrence's gradient row

@@ -79,7 +79,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
             if ptxas_verbose and log:
                 print(log)
     if force or jobs or _stale(LIB_PATH, objs):
-        cmd = [nvcc] + ARCH_FLAGS + ["-shared", "-o", LIB_PATH] + objs + ["-lcudart", "-lcuda"]
+        cmd = [nvcc] + ARCH_FLAGS + ["-shared", "-o", LIB_PATH] + objs + ["-lcudart"]
         run(cmd)
     return LIB_PATH
 

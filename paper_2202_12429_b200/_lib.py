@@ -212,6 +212,9 @@ _SIGS = {
     "bp_set_stub_short_ctas": (c_i32, [c_i32]),
     "bp_set_stub_carveout": (c_i32, [c_i32]),
     "bp_set_green_sms": (c_i32, [c_i32]),
+    "bp_set_peer_sorted": (c_i32, [c_i32]),
+    "bp_embbag_backward_peer_sorted": (c_i32, [c_vp, c_vp, c_f32, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32,
+                                                c_f32, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "bp_green_info": (c_i32, [c_vp]),
     "bp_dlrm_master_sgd": (c_i32, [P(SgdTensors), c_f32, c_vp]),
     "bp_engine_dlrm_backward_begin": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_i32, c_f32, c_f32, c_i32,
@@ -300,6 +303,9 @@ def lib() -> C.CDLL:
                 sk = os.environ.get("BAGPIPE_B200_DEBUG_SKIP_LINK")  # debug only: results become wrong
                 if sk:
                     check(lb.bp_debug_skip_link(int(sk)), "bp_debug_skip_link")
+                psr = os.environ.get("BAGPIPE_B200_PEER_SORTED")  # 0: reduce-by-key peer backward
+                if psr:
+                    check(lb.bp_set_peer_sorted(int(psr)), "bp_set_peer_sorted")
                 gr = os.environ.get("BAGPIPE_B200_GREEN_SMS")  # tuning knob: SMs of the hot-key partition
                 if gr:
                     check(lb.bp_set_green_sms(int(gr)), "bp_set_green_sms")

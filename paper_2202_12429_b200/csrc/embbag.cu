@@ -2088,6 +2088,71 @@ extern "C" int bp_embbag_backward_peer(bp_prep* P, const bp_peer_xchg* x, float 
                               eps, d_stats, stream, &ps);
 }
 
+namespace bp {
+
+// Peer gradient rows pulled into key-sorted order: sorted position j (one
+// float4 lane per (j, 4 components): coalesced stores) takes the gradient
+// row of occurrence occ_pos[j] from its example owner's buffer over NVLink,
+// scaled.  The staged sorted backward then streams the local buffer.
+__global__ void __launch_bounds__(256) k_peer_gather_sorted(const uint32_t* __restrict__ occ_pos, int q, long long n,
+                                                           PeerSrc src, float4* __restrict__ out) {
+  constexpr int U = 4;
+  const long long total = n * q;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += stride * U) {
+    float4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < total) {
+        const long long j = i / q;
+        v[k] = peer_row(src, occ_pos[j], q)[i - j * q];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      if (i < total) {
+        float4 x = v[k];
+        if (src.scale != 1.f) {
+          x.x = __fmul_rn(x.x, src.scale);
+          x.y = __fmul_rn(x.y, src.scale);
+          x.z = __fmul_rn(x.z, src.scale);
+          x.w = __fmul_rn(x.w, src.scale);
+        }
+        out[i] = x;
+      }
+    }
+  }
+}
+
+}  // namespace bp
+
+// Peer backward through the key-sorted path: the gradient rows of the rank's
+// occurrences gathered from the example owners into d_sorted (n_occ x dim
+// floats, caller-owned) in key-sorted order, then the staged sorted backward
+// (d_scratch: bp_embbag_bwd_scratch_bytes, zeroed once).
+extern "C" int bp_embbag_backward_peer_sorted(bp_prep* P, const bp_peer_xchg* x, float scale, float* d_values,
+                                              int32_t row_stride, const int32_t* d_slots_s, uint8_t* d_dirty,
+                                              int32_t dim, int32_t opt, float lr, float eps, int64_t* d_stats,
+                                              float* d_sorted, void* d_scratch, int64_t scratch_bytes,
+                                              bp_stream_t stream) {
+  using namespace bp;
+  if (!x || !P->d_seg_of || (dim & 3) != 0 || dim > 32 || (32 % dim) != 0 || x->n_cols < 1 || x->bl < 1)
+    return BP_ERR_INVALID;
+  if (P->n_occ != x->bl * x->world * x->n_cols) return BP_ERR_INVALID;
+  if (P->n_occ == 0) return BP_OK;
+  const int q = dim / 4;
+  const PeerSrc ps{reinterpret_cast<float4* const*>(x->d_peer_rows), x->d_col_tables, x->bl, x->t_global, x->n_cols,
+                   scale};
+  k_peer_gather_sorted<<<grid_for(P->n_occ * q, 256 * 4, kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+      P->d_occ_pos, q, P->n_occ, ps, reinterpret_cast<float4*>(d_sorted));
+  BP_LAUNCH_CHECK();
+  return bp_embbag_backward_sorted_scratch(P, d_sorted, d_values, row_stride, d_slots_s, d_dirty, dim, opt, lr, eps,
+                                           d_stats, d_scratch, scratch_bytes, stream);
+}
+
 extern "C" int bp_embbag_forward_peer(bp_prep* P, const float* d_values, int32_t row_stride, const int32_t* d_slots_s,
                                       int32_t dim, const bp_peer_xchg* x, bp_stream_t stream) {
   using namespace bp;

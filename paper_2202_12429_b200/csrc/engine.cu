@@ -339,6 +339,8 @@ struct bp_engine {
   // persistent scratch of the sorted EmbeddingBag backward (zeroed once)
   void* bwd_scratch = nullptr;
   size_t bwd_scratch_bytes = 0;
+  float* peer_rows = nullptr;  // key-sorted peer gradient rows (sorted peer backward)
+  size_t peer_rows_bytes = 0;
   bool link_gate = false;
   bool side_gate = false;  // the same for batch preps and planner passes
   cudaEvent_t gate_ev = nullptr;
@@ -542,6 +544,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   if (e->flush_ev) cudaEventDestroy(e->flush_ev);
   if (e->gate_ev) cudaEventDestroy(e->gate_ev);
   if (e->bwd_scratch) cudaFree(e->bwd_scratch);
+  if (e->peer_rows) cudaFree(e->peer_rows);
   cudaFreeHost(e->h_fetch_ids);
   cudaFreeHost(e->h_fetch_rows);
   cudaFreeHost(e->h_flush_ids);
@@ -1269,6 +1272,52 @@ extern "C" int bp_engine_dlrm_forward_peer(bp_engine* e, int64_t pos, int32_t pl
   return rc;
 }
 
+namespace bp {
+
+static int g_peer_sorted = 1;  // bp_set_peer_sorted: 1 = gather into key order + staged backward
+
+// The peer backward: the key-sorted form (gradient rows pulled over NVLink
+// into key order, then the staged segmented reduce) or the reduce-by-key
+// gather straight from the peers' buffers.
+static int engine_backward_peer(bp_engine* e, bp_prep* P, const bp_peer_xchg* grads, float scale,
+                                const bp_cache_view& cv, int32_t model_dim, int32_t opt, float lr, float eps) {
+  const bool sorted = g_peer_sorted && P->d_seg_of && (model_dim == 4 || model_dim == 8 || model_dim == 16 ||
+                                                       model_dim == 32);
+  if (!sorted)
+    return bp_embbag_backward_peer(P, grads, scale, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim, opt,
+                                   lr, eps, e->stats, e->compute);
+  const size_t need = (size_t)bp_embbag_bwd_scratch_bytes(P->n_occ, model_dim);
+  const size_t rows = (size_t)P->n_occ * model_dim * sizeof(float);
+  if (need > e->bwd_scratch_bytes || rows > e->peer_rows_bytes) {
+    BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
+    if (need > e->bwd_scratch_bytes) {
+      if (e->bwd_scratch) BP_CUDA_TRY(cudaFree(e->bwd_scratch));
+      e->bwd_scratch = nullptr;
+      e->bwd_scratch_bytes = 0;
+      BP_CUDA_TRY(cudaMalloc(&e->bwd_scratch, need));
+      BP_CUDA_TRY(cudaMemset(e->bwd_scratch, 0, need));
+      e->bwd_scratch_bytes = need;
+    }
+    if (rows > e->peer_rows_bytes) {
+      if (e->peer_rows) BP_CUDA_TRY(cudaFree(e->peer_rows));
+      e->peer_rows = nullptr;
+      e->peer_rows_bytes = 0;
+      BP_CUDA_TRY(cudaMalloc(&e->peer_rows, rows));
+      e->peer_rows_bytes = rows;
+    }
+  }
+  return bp_embbag_backward_peer_sorted(P, grads, scale, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim,
+                                        opt, lr, eps, e->stats, e->peer_rows, e->bwd_scratch,
+                                        (int64_t)e->bwd_scratch_bytes, e->compute);
+}
+
+}  // namespace bp
+
+extern "C" int bp_set_peer_sorted(int32_t on) {
+  bp::g_peer_sorted = on ? 1 : 0;
+  return BP_OK;
+}
+
 extern "C" int bp_engine_dlrm_backward_peer(bp_engine* e, int64_t pos, int32_t plan_slot, const bp_peer_xchg* grads,
                                             float scale, int32_t model_dim, int32_t opt, float lr, float eps,
                                             int32_t chunk_slot, int32_t drain_slot, bp_step_result* out) {
@@ -1279,8 +1328,7 @@ extern "C" int bp_engine_dlrm_backward_peer(bp_engine* e, int64_t pos, int32_t p
   bp_cache_view cv;
   bp_cache_get_view(e->cache, &cv);
   stage_begin(e, kStageTrainerBwd, e->compute);
-  int rc = bp_embbag_backward_peer(P, grads, scale, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim, opt,
-                                   lr, eps, e->stats, e->compute);
+  int rc = engine_backward_peer(e, P, grads, scale, cv, model_dim, opt, lr, eps);
   stage_end(e, kStageTrainerBwd, e->compute);
   if (rc) return rc;
   return engine_finish(e, P, ps, chunk_slot, drain_slot, out);
@@ -1301,8 +1349,7 @@ extern "C" int bp_engine_dlrm_backward_peer_begin(bp_engine* e, int64_t pos, int
   bp_cache_view cv;
   bp_cache_get_view(e->cache, &cv);
   stage_begin(e, kStageTrainerBwd, e->compute);
-  int rc = bp_embbag_backward_peer(P, grads, scale, cv.d_values, e->cfg.dim, e->slots_s, cv.d_dirty, model_dim, opt,
-                                   lr, eps, e->stats, e->compute);
+  int rc = engine_backward_peer(e, P, grads, scale, cv, model_dim, opt, lr, eps);
   stage_end(e, kStageTrainerBwd, e->compute);
   if (rc) return rc;
   return engine_finish_begin(e, P, ps, chunk_slot, drain_slot);

@@ -4,12 +4,45 @@
 // stream lives in the complementary partition, so the chains never share an
 // SM with the short-segment kernel (measured in the step: the two kernels
 // slowed each other from 47 + 25 us isolated to ~55 us side by side).
-// Memory is the device's: green contexts partition SMs only.
+// Memory is the device's: green contexts partition SMs only.  The driver
+// entry points are fetched through the runtime (cudaGetDriverEntryPoint), so
+// the library does not link libcuda and still loads on a machine without a
+// GPU driver.
 #include <cuda.h>
 
 #include "internal.cuh"
 
 namespace bp {
+
+struct GreenApi {
+  CUresult (*ctxGetDevice)(CUdevice*);
+  CUresult (*getDevResource)(CUdevice, CUdevResource*, CUdevResourceType);
+  CUresult (*smSplit)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int, unsigned int);
+  CUresult (*genDesc)(CUdevResourceDesc*, CUdevResource*, unsigned int);
+  CUresult (*greenCreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int);
+  CUresult (*greenStream)(CUstream*, CUgreenCtx, unsigned int, int);
+};
+
+static int green_api(GreenApi* a) {
+  struct {
+    const char* name;
+    void** fn;
+  } entries[] = {{"cuCtxGetDevice", (void**)&a->ctxGetDevice},
+                 {"cuDeviceGetDevResource", (void**)&a->getDevResource},
+                 {"cuDevSmResourceSplitByCount", (void**)&a->smSplit},
+                 {"cuDevResourceGenerateDesc", (void**)&a->genDesc},
+                 {"cuGreenCtxCreate", (void**)&a->greenCreate},
+                 {"cuGreenCtxStreamCreate", (void**)&a->greenStream}};
+  for (auto& en : entries) {
+    cudaDriverEntryPointQueryResult q;
+    BP_CUDA_TRY(cudaGetDriverEntryPoint(en.name, en.fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !*en.fn) {
+      bp_set_last_error(en.name, __FILE__, __LINE__);
+      return BP_ERR_CUDA;
+    }
+  }
+  return BP_OK;
+}
 
 struct GreenPartition {
   CUgreenCtx hot = nullptr, rest = nullptr;
@@ -19,33 +52,35 @@ struct GreenPartition {
 static GreenPartition g_green;
 static int g_green_sms = 0;  // bp_set_green_sms: SMs of the hot partition (0 = off)
 
-#define BP_CU_TRY(expr)                                               \
-  do {                                                                \
-    CUresult _r = (expr);                                             \
-    if (_r != CUDA_SUCCESS) {                                         \
-      const char* _m = nullptr;                                       \
-      cuGetErrorString(_r, &_m);                                      \
-      bp_set_last_error(_m ? _m : "driver error", __FILE__, __LINE__); \
-      return BP_ERR_CUDA;                                             \
-    }                                                                 \
+#define BP_CU_TRY(expr)                                        \
+  do {                                                         \
+    CUresult _r = (expr);                                      \
+    if (_r != CUDA_SUCCESS) {                                  \
+      bp_set_last_error("CUDA driver call failed", __FILE__, __LINE__); \
+      return BP_ERR_CUDA;                                      \
+    }                                                          \
   } while (0)
+
+static GreenApi g_api;
 
 // Creates the partition once per process (green contexts are per device).
 static int green_init() {
   if (g_green.hot || g_green_sms <= 0) return BP_OK;
   BP_CUDA_TRY(cudaFree(nullptr));  // the runtime's primary context exists
+  const int rc = green_api(&g_api);
+  if (rc) return rc;
   CUdevice dev;
-  BP_CU_TRY(cuCtxGetDevice(&dev));
+  BP_CU_TRY(g_api.ctxGetDevice(&dev));
   CUdevResource all;
-  BP_CU_TRY(cuDeviceGetDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM));
+  BP_CU_TRY(g_api.getDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM));
   CUdevResource hot, rest;
   unsigned int n = 1;
-  BP_CU_TRY(cuDevSmResourceSplitByCount(&hot, &n, &all, &rest, 0, (unsigned)g_green_sms));
+  BP_CU_TRY(g_api.smSplit(&hot, &n, &all, &rest, 0, (unsigned)g_green_sms));
   CUdevResourceDesc dh, dr;
-  BP_CU_TRY(cuDevResourceGenerateDesc(&dh, &hot, 1));
-  BP_CU_TRY(cuDevResourceGenerateDesc(&dr, &rest, 1));
-  BP_CU_TRY(cuGreenCtxCreate(&g_green.hot, dh, dev, CU_GREEN_CTX_DEFAULT_STREAM));
-  BP_CU_TRY(cuGreenCtxCreate(&g_green.rest, dr, dev, CU_GREEN_CTX_DEFAULT_STREAM));
+  BP_CU_TRY(g_api.genDesc(&dh, &hot, 1));
+  BP_CU_TRY(g_api.genDesc(&dr, &rest, 1));
+  BP_CU_TRY(g_api.greenCreate(&g_green.hot, dh, dev, CU_GREEN_CTX_DEFAULT_STREAM));
+  BP_CU_TRY(g_api.greenCreate(&g_green.rest, dr, dev, CU_GREEN_CTX_DEFAULT_STREAM));
   g_green.hot_sms = (int)hot.sm.smCount;
   g_green.rest_sms = (int)rest.sm.smCount;
   return BP_OK;
@@ -58,7 +93,7 @@ int green_stream(int hot, int priority, cudaStream_t* out) {
   const int rc = green_init();
   if (rc || !g_green.hot) return rc;
   CUstream s;
-  BP_CU_TRY(cuGreenCtxStreamCreate(&s, hot ? g_green.hot : g_green.rest, CU_STREAM_NON_BLOCKING, priority));
+  BP_CU_TRY(g_api.greenStream(&s, hot ? g_green.hot : g_green.rest, CU_STREAM_NON_BLOCKING, priority));
   *out = (cudaStream_t)s;
   return BP_OK;
 }
