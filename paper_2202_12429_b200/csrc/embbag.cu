@@ -136,16 +136,33 @@ __device__ __forceinline__ float4* peer_row(const PeerSrc& ps, long long p, int 
 // Forward fused with the all-to-all: pooled row of occurrence p (example b,
 // local column j) stored straight into example owner b / bl's buffer at its
 // global-table column, over NVLink.
+template <int QT>  // QT > 0: float4s per row at compile time; 0: runtime q
 __global__ void __launch_bounds__(256) k_embbag_fwd_peer_v4(const uint32_t* __restrict__ occ_s,
                                                            const int32_t* __restrict__ slots_s,
-                                                           const float4* __restrict__ values, int q, int row_q,
+                                                           const float4* __restrict__ values, int q_rt, int row_q,
                                                            long long n, PeerSrc dst) {
+  constexpr int U = 4;  // four independent (index, slot, row) chains per thread
+  const int q = QT > 0 ? QT : q_rt;
   const long long total = n * q;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long p = i / q;
-    const int c = (int)(i - p * q);
-    const int32_t slot = slots_s[occ_s[p]];
-    peer_row(dst, p, q)[c] = slot >= 0 ? values[(long long)slot * row_q + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += stride * U) {
+    int32_t sl[U];
+    float4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      sl[k] = i < total ? __ldg(slots_s + __ldg(occ_s + i / q)) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      v[k] = sl[k] >= 0 ? values[(long long)sl[k] * row_q + (int)(i % q)] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = i0 + k * stride;
+      if (i < total) peer_row(dst, i / q, q)[i % q] = v[k];
+    }
   }
 }
 
@@ -2094,9 +2111,11 @@ namespace bp {
 // float4 lane per (j, 4 components): coalesced stores) takes the gradient
 // row of occurrence occ_pos[j] from its example owner's buffer over NVLink,
 // scaled.  The staged sorted backward then streams the local buffer.
-__global__ void __launch_bounds__(256) k_peer_gather_sorted(const uint32_t* __restrict__ occ_pos, int q, long long n,
-                                                           PeerSrc src, float4* __restrict__ out) {
+template <int QT>
+__global__ void __launch_bounds__(256) k_peer_gather_sorted(const uint32_t* __restrict__ occ_pos, int q_rt,
+                                                           long long n, PeerSrc src, float4* __restrict__ out) {
   constexpr int U = 4;
+  const int q = QT > 0 ? QT : q_rt;
   const long long total = n * q;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += stride * U) {
@@ -2105,10 +2124,7 @@ __global__ void __launch_bounds__(256) k_peer_gather_sorted(const uint32_t* __re
     for (int k = 0; k < U; ++k) {
       const long long i = i0 + k * stride;
       v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i < total) {
-        const long long j = i / q;
-        v[k] = peer_row(src, occ_pos[j], q)[i - j * q];
-      }
+      if (i < total) v[k] = peer_row(src, __ldg(occ_pos + i / q), q)[i % q];
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -2146,8 +2162,15 @@ extern "C" int bp_embbag_backward_peer_sorted(bp_prep* P, const bp_peer_xchg* x,
   const int q = dim / 4;
   const PeerSrc ps{reinterpret_cast<float4* const*>(x->d_peer_rows), x->d_col_tables, x->bl, x->t_global, x->n_cols,
                    scale};
-  k_peer_gather_sorted<<<grid_for(P->n_occ * q, 256 * 4, kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(
-      P->d_occ_pos, q, P->n_occ, ps, reinterpret_cast<float4*>(d_sorted));
+  const int gg = grid_for(P->n_occ * q, 256 * 4, kNumSMs * 8);
+  float4* out4 = reinterpret_cast<float4*>(d_sorted);
+  cudaStream_t gs = (cudaStream_t)stream;
+  switch (q) {
+    case 1: k_peer_gather_sorted<1><<<gg, 256, 0, gs>>>(P->d_occ_pos, q, P->n_occ, ps, out4); break;
+    case 2: k_peer_gather_sorted<2><<<gg, 256, 0, gs>>>(P->d_occ_pos, q, P->n_occ, ps, out4); break;
+    case 4: k_peer_gather_sorted<4><<<gg, 256, 0, gs>>>(P->d_occ_pos, q, P->n_occ, ps, out4); break;
+    default: k_peer_gather_sorted<8><<<gg, 256, 0, gs>>>(P->d_occ_pos, q, P->n_occ, ps, out4); break;
+  }
   BP_LAUNCH_CHECK();
   return bp_embbag_backward_sorted_scratch(P, d_sorted, d_values, row_stride, d_slots_s, d_dirty, dim, opt, lr, eps,
                                            d_stats, d_scratch, scratch_bytes, stream);
@@ -2163,8 +2186,16 @@ extern "C" int bp_embbag_forward_peer(bp_prep* P, const float* d_values, int32_t
   const int q = dim / 4;
   const PeerSrc dst{reinterpret_cast<float4* const*>(x->d_peer_rows), x->d_col_tables, x->bl, x->t_global, x->n_cols,
                     1.f};
-  k_embbag_fwd_peer_v4<<<grid_for(P->n_occ * q, 256, kNumSMs * 16), 256, 0, (cudaStream_t)stream>>>(
-      P->d_occ_s, d_slots_s, reinterpret_cast<const float4*>(d_values), q, row_stride / 4, P->n_occ, dst);
+  const int fg = grid_for(P->n_occ * q, 256 * 4, kNumSMs * 8);
+  const float4* vals4 = reinterpret_cast<const float4*>(d_values);
+  cudaStream_t fs = (cudaStream_t)stream;
+  switch (q) {
+    case 1: k_embbag_fwd_peer_v4<1><<<fg, 256, 0, fs>>>(P->d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, dst); break;
+    case 2: k_embbag_fwd_peer_v4<2><<<fg, 256, 0, fs>>>(P->d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, dst); break;
+    case 4: k_embbag_fwd_peer_v4<4><<<fg, 256, 0, fs>>>(P->d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, dst); break;
+    case 8: k_embbag_fwd_peer_v4<8><<<fg, 256, 0, fs>>>(P->d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, dst); break;
+    default: k_embbag_fwd_peer_v4<0><<<fg, 256, 0, fs>>>(P->d_occ_s, d_slots_s, vals4, q, row_stride / 4, P->n_occ, dst); break;
+  }
   BP_LAUNCH_CHECK();
   return BP_OK;
 }
