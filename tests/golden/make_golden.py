@@ -439,6 +439,30 @@ def gen_cli():
     dump("cli.json", out)
 
 
+def gen_wire():
+    """Frames of the reference store protocol (reference wire.py) and a served
+    session transcript against a fresh store (schema 2:(1000,300):0:4, 3
+    shards, seed 11): request bytes in, response bytes out."""
+    import io
+
+    from embcache import wire as W
+
+    keys = [EmbeddingKey(0, 3), EmbeddingKey(1, 299), EmbeddingKey(0, 999), EmbeddingKey(1, 0)]
+    vals = (np.arange(16, dtype=np.float32).reshape(4, 4) * 0.25 - 1.0)
+    out = {"fetch": W.encode_fetch(keys).hex(), "fetch_resp": W.encode_fetch_resp(vals).hex(),
+           "write": W.encode_write(keys, vals).hex(), "ack": W.encode_ack(7).hex(),
+           "keys": [[k.table_id, k.row_id] for k in keys], "values": _bits(vals)}
+    schema = Schema(2, (1000, 300), 0, 4)
+    store = ShardedStore(schema, 3, 11)
+    reqs = (W.encode_fetch(keys) + W.encode_write(keys[:2], vals[:2]) + W.encode_fetch(keys)
+            + W.encode_fetch([EmbeddingKey(1, 5)]))
+    wbuf = io.BytesIO()
+    served = W.serve_connection(store, io.BytesIO(reqs), wbuf)
+    out["session"] = {"schema": [2, [1000, 300], 0, 4], "num_shards": 3, "seed": 11, "requests": reqs.hex(),
+                      "responses": wbuf.getvalue().hex(), "served": served}
+    dump("wire.json", out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
@@ -453,6 +477,8 @@ def main():
         gen_api()
     if want("cli"):
         gen_cli()
+    if want("wire"):
+        gen_wire()
     if want("acceptance"):
         gen_acceptance()
     ck = gen_ck() if want("ck") else None
