@@ -519,7 +519,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "achieved": pl_bytes / (pl_ms * 1e-3) / 1e9 if pl_ms else 0.0, "peak": None,
         "kernels_us_per_step": {k: round(v, 2) for k, v in ktimes.items()
                                 if k.startswith(PREP_KERNELS + PLANNER_KERNELS)},
-        "prep_us": pl_prep_us, "planner_us": pl_plan_us,
+        "prep_us": pl_prep_us, "planner_us": pl_plan_us, "traffic": _planner_traffic(),
         "stage_span_ms": {"prep": stages["prep"][0], "planner": stages["planner"][0]},
         "timing": "CUPTI device time of the kernels over 4 engine steps; stage_span_ms = the engine's event "
                   "spans around the enqueue (include host enqueue gaps)",
@@ -594,7 +594,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         out["roofline"]["frac"] = out["roofline"]["achieved"] / hbm_peak
         out["roofline"]["peak_source"] = peak_src
         for part in (dlrm.get("roofline_parts") or {}).values():
-            part.update(peak=hbm_peak, frac=part["achieved"] / hbm_peak, peak_source=peak_src)
+            part.update(peak=hbm_peak, frac=part["achieved"] / hbm_peak, peak_source=peak_src,
+                        frac_cupti=part["achieved_cupti"] / hbm_peak if part.get("achieved_cupti") else None)
         out["roofline_parts"] = dlrm.get("roofline_parts")
     else:
         out["roofline"] = dict(out["roofline_stub_trainer"], bound="hbm")
@@ -646,6 +647,9 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
         ms = float(t[0])
     records = pipe.records[warm:warm + steps]
     stages = _stage_breakdown(pipe, warm + steps, 8)
+    # CUPTI device time of the same kernels inside 4 more steps (no event
+    # brackets: the kernel alone, still beside the step's other streams)
+    ktimes = kernel_times(pipe, warm + steps + 8, 4)
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     n_occ = BATCH * world * local_tables
     # "trainer" spans: the EmbeddingBag forward, "trainer_bwd": its backward
@@ -679,29 +683,53 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
             # device-side barriers of the exchange)
             "roofline_parts": None if world > 1 else {
                 "gather": _part("bp::k_embbag_fwd_rows_v4 (EmbeddingBag forward: gather + pooling)",
-                                fwd_bytes, fwd_span, "k_embbag_fwd_rows_v4"),
+                                fwd_bytes, fwd_span, "k_embbag_fwd_rows_v4", ktimes),
                 "scatter": _part("bp::k_embbag_bwd_staged (sorted-gradient segmented scatter-add + SGD in place)",
-                                 bwd_bytes(n_occ, int(u_mean)), bwd_span, "k_embbag_bwd_staged<4>")}}
+                                 bwd_bytes(n_occ, int(u_mean)), bwd_span, "k_embbag_bwd_staged", ktimes)}}
 
 
-def _part(kernel: str, nbytes: int, span, ncu_name: str) -> dict:
+def _part(kernel: str, nbytes: int, span, ncu_name: str, ktimes: dict | None = None) -> dict:
+    """One half of the EmbeddingBag pair: achieved = algorithmic bytes / the
+    launch's CUDA-event span on the compute stream (the spec's measure; the
+    span includes the launch gap behind the begin event), plus the CUPTI
+    kernel duration inside the step for comparison."""
     ms = span[0]
-    try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "round1", "traffic.json")))[
-            "dram_bytes_per_launch"][ncu_name]
-    except (OSError, KeyError, ValueError):
-        traffic = None
+    traffic = None
+    for rnd in ("round2", "round1"):
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", rnd, "traffic.json")))["dram_bytes_per_launch"]
+            traffic = next((v for k, v in tr.items() if k.startswith(ncu_name)), None)
+        except (OSError, KeyError, ValueError):
+            continue
+        if traffic is not None:
+            break
+    kus = None
+    if ktimes:
+        kus = sum(v for k, v in ktimes.items() if k.startswith(ncu_name)) or None
     return {"kernel": kernel, "bound": "hbm", "bytes_per_launch": nbytes, "ms_per_launch": ms,
             "launches_per_step": span[1], "unit": "GB/s", "achieved": nbytes / (ms * 1e-3) / 1e9 if ms else 0.0,
-            "traffic": traffic}
+            "traffic": traffic, "kernel_us_cupti_in_step": kus,
+            "achieved_cupti": nbytes / (kus * 1e-6) / 1e9 if kus else None}
 
 
 def _traffic():
     """DRAM bytes (read + write) per step of the EmbeddingBag kernels from the
-    committed ncu --set full capture (profiles/round1/traffic.json)."""
+    committed ncu --set full capture (profiles/round2/traffic.json)."""
+    for rnd in ("round2", "round1"):
+        try:
+            return json.load(open(os.path.join(ROOT, "profiles", rnd, "traffic.json")))[
+                "embbag_fwd_bwd_dram_bytes_per_step"]
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
+
+
+def _planner_traffic():
+    """DRAM bytes per step of the prep + planner kernels (ncu --set full of
+    tools/planner_bench.py, profiles/round2/traffic.json)."""
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "round1", "traffic.json")))[
-            "embbag_fwd_bwd_dram_bytes_per_step"]
+        return json.load(open(os.path.join(ROOT, "profiles", "round2", "traffic.json")))[
+            "prep_planner_dram_bytes_per_step"]
     except (OSError, KeyError, ValueError):
         return None
 

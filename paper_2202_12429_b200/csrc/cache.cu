@@ -19,6 +19,8 @@ namespace bp {
 struct CacheCounters {
   long long occupancy, free_top, insertions, evictions, peak_occupancy, abort;
   unsigned int ticket;  // k_insert: blocks finished (the last one commits the counters)
+  unsigned int evict_ticket;  // k_evict_planned: blocks finished
+  unsigned long long evict_dirty;  // k_evict_planned: dirty rows so far (reset by the last block)
 };
 
 }  // namespace bp
@@ -70,8 +72,14 @@ __global__ void k_insert(const uint64_t* __restrict__ keys, const uint32_t* __re
                          int32_t* __restrict__ slot_of, uint64_t* __restrict__ slot_key,
                          uint32_t* __restrict__ slot_id, long long* __restrict__ ttl, uint8_t* __restrict__ dirty,
                          uint8_t* __restrict__ used, float* __restrict__ values, const uint32_t* __restrict__ free_list,
-                         ErrorRecord* err, long long iteration) {
-  n = load_count(n, d_n);
+                         ErrorRecord* err, long long iteration, long long sub, long long* n_out) {
+  // d_n - sub rows (the engine skips a dropped first key this way), written
+  // back to n_out for the step counters
+  if (d_n) {
+    const long long m = *d_n - sub;
+    n = m < 0 ? 0 : (m < n ? m : n);
+  }
+  if (n_out && blockIdx.x == 0 && threadIdx.x == 0) *n_out = n;
   const long long occ = ctr->occupancy, top = ctr->free_top;
   const bool abort = occ + n > capacity;
   if (abort) {
@@ -247,10 +255,11 @@ __global__ void k_evict_planned(const uint64_t* __restrict__ keys, const uint32_
                                 const long long* __restrict__ d_n, long long n_max, int dim,
                                 const float* __restrict__ values, uint8_t* __restrict__ dirty,
                                 uint8_t* __restrict__ used, int32_t* __restrict__ slot_of,
-                                const CacheCounters* __restrict__ ctr, uint32_t* __restrict__ free_list,
+                                CacheCounters* __restrict__ ctr, uint32_t* __restrict__ free_list,
                                 uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_ids,
                                 float* __restrict__ out_rows, uint8_t* __restrict__ out_dirty,
-                                long long* __restrict__ out_count, ErrorRecord* err, long long iteration) {
+                                long long* __restrict__ out_count, ErrorRecord* err, long long iteration,
+                                const int64_t* __restrict__ d_expect, StepRecord rec) {
   const long long n = load_count(n_max, d_n);
   const long long top = ctr->free_top;
   unsigned long long nd = 0;
@@ -278,19 +287,28 @@ __global__ void k_evict_planned(const uint64_t* __restrict__ keys, const uint32_
     dirty[slot] = 0;
     free_list[top + i] = (uint32_t)slot;
   }
+  // the last block to finish commits the counters (no separate end kernel,
+  // no memset of the output counts) and, for the engine, the step record
+  __shared__ unsigned long long sh_nd;
+  if (threadIdx.x == 0) sh_nd = 0;
+  __syncthreads();
   nd = warp_sum(nd);
-  if (lane_id() == 0 && nd) atomicAdd((unsigned long long*)&out_count[1], nd);
-}
-
-__global__ void k_evict_planned_end(CacheCounters* ctr, const long long* d_n, long long n_max,
-                                    const int64_t* d_expect, long long* out_count, ErrorRecord* err,
-                                    long long iteration) {
-  const long long n = load_count(n_max, d_n);
+  if (lane_id() == 0 && nd) atomicAdd(&sh_nd, nd);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (sh_nd) atomicAdd(&ctr->evict_dirty, sh_nd);
+  __threadfence();
+  if (atomicAdd(&ctr->evict_ticket, 1u) != gridDim.x - 1) return;
+  __threadfence();
+  const unsigned long long n_dirty = atomicExch(&ctr->evict_dirty, 0ull);
+  ctr->evict_ticket = 0;
   ctr->free_top += n;
   ctr->occupancy -= n;
   ctr->evictions += n;
   out_count[0] = n;
+  out_count[1] = (long long)n_dirty;
   if (d_expect && ctr->occupancy != *d_expect) raise_error(err, BP_ERR_ENGINE, iteration, 1ll << 41, 0);
+  if (rec.out) write_step_record(rec, n, (long long)n_dirty, err);
 }
 
 __global__ void k_evict_end(CacheCounters* ctr, const long long* d_count, long long out_cap) {
@@ -472,19 +490,37 @@ extern "C" int bp_cache_get_stats(bp_cache* c, bp_stream_t stream, bp_cache_stat
   return BP_OK;
 }
 
+namespace bp {
+// bp_cache_insert of (*d_n - sub) rows that also stores that count in n_out
+// (the engine's plan-slot insert: no separate count kernel).
+int cache_insert_sub(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids, const float* d_rows,
+                     const int64_t* d_ttls, int64_t n, const int64_t* d_n, int64_t sub, int64_t* n_out,
+                     int64_t iteration, cudaStream_t s);
+}  // namespace bp
+
 extern "C" int bp_cache_insert(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids, const float* d_rows,
                                const int64_t* d_ttls, int64_t n, const int64_t* d_n, int64_t iteration,
                                bp_stream_t stream) {
+  return bp::cache_insert_sub(c, d_keys, d_ids, d_rows, d_ttls, n, d_n, 0, nullptr, iteration, (cudaStream_t)stream);
+}
+
+int bp::cache_insert_sub(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids, const float* d_rows,
+                         const int64_t* d_ttls, int64_t n, const int64_t* d_n, int64_t sub, int64_t* n_out_,
+                         int64_t iteration, cudaStream_t s) {
   using namespace bp;
-  if (n <= 0) return BP_OK;
-  cudaStream_t s = (cudaStream_t)stream;
+  long long* n_out = (long long*)n_out_;
+  if (n <= 0) {
+    if (n_out) BP_CUDA_TRY(cudaMemsetAsync(n_out, 0, sizeof(long long), s));
+    return BP_OK;
+  }
   const uint32_t* ids;
   int rc = cache_ids(c, d_keys, d_ids, n, (const long long*)d_n, 1, &ids, s);
   if (rc) return rc;
   ErrorRecord* err = c->ctx ? c->ctx->d_err : nullptr;
   k_insert<<<grid_for(n, 256), 256, 0, s>>>(d_keys, ids, d_rows, d_ttls, n, (const long long*)d_n, c->dim, c->d_ctr,
                                             c->capacity, c->d_slot_of, c->d_slot_key, c->d_slot_id, c->d_ttl,
-                                            c->d_dirty, c->d_used, c->d_values, c->d_free, err, iteration);
+                                            c->d_dirty, c->d_used, c->d_values, c->d_free, err, iteration, sub,
+                                            n_out);
   BP_LAUNCH_CHECK();
   return BP_OK;
 }
@@ -567,20 +603,23 @@ extern "C" int bp_cache_evict(bp_cache* c, int64_t completed, int32_t drain, con
   return BP_OK;
 }
 
-extern "C" int bp_cache_evict_planned(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids, const int64_t* d_n,
-                                      int64_t n_max, const int64_t* d_expect, int64_t iteration,
-                                      const bp_evict_buffers* o, bp_stream_t stream) {
+int bp::cache_evict_planned_rec(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids, const int64_t* d_n,
+                                int64_t n_max, const int64_t* d_expect, int64_t iteration, const bp_evict_buffers* o,
+                                const StepRecord& rec, cudaStream_t s) {
   using namespace bp;
-  cudaStream_t s = (cudaStream_t)stream;
-  BP_CUDA_TRY(cudaMemsetAsync(o->d_count, 0, 2 * sizeof(int64_t), s));
   ErrorRecord* err = c->ctx ? c->ctx->d_err : nullptr;
   k_evict_planned<<<grid_for(n_max, 256, kNumSMs * 4), 256, 0, s>>>(
       d_keys, d_ids, (const long long*)d_n, n_max, c->dim, c->d_values, c->d_dirty, c->d_used, c->d_slot_of, c->d_ctr,
-      c->d_free, o->d_keys, o->d_ids, o->d_rows, o->d_dirty, (long long*)o->d_count, err, iteration);
-  k_evict_planned_end<<<1, 1, 0, s>>>(c->d_ctr, (const long long*)d_n, n_max, d_expect, (long long*)o->d_count, err,
-                                      iteration);
+      c->d_free, o->d_keys, o->d_ids, o->d_rows, o->d_dirty, (long long*)o->d_count, err, iteration, d_expect, rec);
   BP_LAUNCH_CHECK();
   return BP_OK;
+}
+
+extern "C" int bp_cache_evict_planned(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids, const int64_t* d_n,
+                                      int64_t n_max, const int64_t* d_expect, int64_t iteration,
+                                      const bp_evict_buffers* o, bp_stream_t stream) {
+  return bp::cache_evict_planned_rec(c, d_keys, d_ids, d_n, n_max, d_expect, iteration, o, bp::StepRecord{},
+                                     (cudaStream_t)stream);
 }
 
 extern "C" int bp_cache_checksum(bp_cache* c, uint64_t* d_out, bp_stream_t stream) {

@@ -73,11 +73,6 @@ int bp_embbag_backward(bp_prep*, const float*, const int64_t*, const float*, flo
 
 namespace bp {
 
-__global__ void k_offset_count(const int64_t* src, int64_t off, int64_t* dst) {
-  const int64_t v = *src - off;
-  *dst = v < 0 ? 0 : v;
-}
-
 struct PlanSlot {
   uint64_t* keys;
   uint32_t* ids;
@@ -974,19 +969,20 @@ static int engine_apply(bp_engine* e, bp_prep* P, PlanSlot& ps, int64_t next_pos
   BP_CUDA_TRY(cudaStreamWaitEvent(s, ps.fetched, 0));
   stage_begin(e, kStageApply, s);
   const int off = has_skip ? 1 : 0;
-  k_offset_count<<<1, 1, 0, s>>>(ps.counts, off, ps.n_ins);
-  int rc = bp_cache_insert(e->cache, ps.keys + off, ps.ids + off, ps.staging + (size_t)off * dim, ps.ttls + off,
-                           e->cfg.max_occ - off, ps.n_ins, P->iteration, s);
+  // insert counts[0] - off rows; the count lands in ps.n_ins for the step record
+  int rc = cache_insert_sub(e->cache, ps.keys + off, ps.ids + off, ps.staging + (size_t)off * dim, ps.ttls + off,
+                            e->cfg.max_occ - off, ps.counts, off, ps.n_ins, P->iteration, s);
   if (rc) return rc;
   rc = bp_cache_apply_resolve(e->cache, P, ps.ttl_k, skip_key, has_skip, e->slots_s, s);
   if (rc) return rc;
   bp_prep* N = next_pos >= 0 ? e->preps[engine_prep_slot(e, next_pos)] : nullptr;
   if (N) {
     BP_CUDA_TRY(cudaStreamWaitEvent(s, e->prep_ready[engine_prep_slot(e, next_pos)], 0));
-    rc = bp_mark_ids(N, e->mark, N->iteration, s);
+    rc = mark_ids_zero(N, e->mark, N->iteration, e->stats, s);  // also zeroes the step stats
     if (rc) return rc;
+  } else {
+    BP_CUDA_TRY(cudaMemsetAsync(e->stats, 0, 2 * sizeof(int64_t), s));
   }
-  BP_CUDA_TRY(cudaMemsetAsync(e->stats, 0, 2 * sizeof(int64_t), s));
   stage_end(e, kStageApply, s);
   *next_out = N;
   return BP_OK;
@@ -1037,12 +1033,20 @@ static int engine_finish_begin(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t c
   // The planner's key-sorted evict set is exactly {ttl <= iteration}
   // (checked: the occupancy must then equal the mirror size after the pop);
   // key order makes the later write-back walk the host table ascending.
-  int rc = bp_cache_evict_planned(e->cache, ps.evict_keys, ps.evict_ids, ps.counts + 1, e->chunk_cap, ps.counts + 4,
-                                  P->iteration, &eb, s);
+  // Without a drain, the eviction kernel's last block also writes the step
+  // record (all counters + the error record) into mapped pinned memory.
+  StepRecord rec;
+  if (drain_slot < 0) {
+    rec.num_unique = (const unsigned long long*)P->d_num_unique;
+    rec.n_ins = (const long long*)ps.n_ins;
+    rec.stats = (const unsigned long long*)e->stats;
+    rec.out = (uint64_t*)(e->d_result + 16 * rs);
+  }
+  int rc = cache_evict_planned_rec(e->cache, ps.evict_keys, ps.evict_ids, ps.counts + 1, e->chunk_cap, ps.counts + 4,
+                                   P->iteration, &eb, rec, s);
   stage_end(e, kStageEvict, s);
   if (rc) return rc;
   c.pending = true;
-  const uint64_t* d_drain_count = nullptr;
   if (drain_slot >= 0) {
     ChunkSlot& d = e->chunks[drain_slot];
     BP_CUDA_TRY(cudaStreamWaitEvent(s, d.flushed, 0));
@@ -1050,14 +1054,13 @@ static int engine_finish_begin(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t c
     rc = bp_cache_evict(e->cache, P->iteration, 1, &db, e->cfg.capacity, s);
     if (rc) return rc;
     d.pending = true;
-    d_drain_count = (const uint64_t*)d.count;
+    // all step counters + the error record in ONE kernel writing mapped
+    // pinned memory, then one synchronisation
+    k_step_counters<<<1, 32, 0, s>>>((const uint64_t*)P->d_num_unique, (const uint64_t*)ps.n_ins,
+                                     (const uint64_t*)e->stats, (const uint64_t*)c.count, (const uint64_t*)d.count,
+                                     (const uint64_t*)e->ctx->d_err, (uint64_t*)(e->d_result + 16 * rs));
+    BP_LAUNCH_CHECK();
   }
-  // all step counters + the error record in ONE kernel writing mapped pinned
-  // memory, then one synchronisation (instead of 5 small D2H copies)
-  k_step_counters<<<1, 32, 0, s>>>((const uint64_t*)P->d_num_unique, (const uint64_t*)ps.n_ins,
-                                   (const uint64_t*)e->stats, (const uint64_t*)c.count, d_drain_count,
-                                   (const uint64_t*)e->ctx->d_err, (uint64_t*)(e->d_result + 16 * rs));
-  BP_LAUNCH_CHECK();
   BP_CUDA_TRY(cudaEventRecord(e->step_done[rs], s));
   ++e->step_count;
   return BP_OK;

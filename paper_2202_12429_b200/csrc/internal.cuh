@@ -75,6 +75,41 @@ __device__ __forceinline__ uint32_t registry_find(const uint64_t* keys, const ui
   return kNoId;
 }
 
+// The engine's per-step counter record in mapped pinned memory (engine.cu
+// layout: unique, inserted, critical, dirty keys, evicted, evicted dirty,
+// drained, drained dirty, then the error record), written by the last block
+// of the step's eviction kernel; out == nullptr: none.
+struct StepRecord {
+  const unsigned long long* num_unique = nullptr;
+  const long long* n_ins = nullptr;
+  const unsigned long long* stats = nullptr;
+  uint64_t* out = nullptr;
+};
+
+__device__ __forceinline__ void write_step_record(const StepRecord& r, long long evicted, long long evicted_dirty,
+                                                  const ErrorRecord* err) {
+  r.out[0] = *r.num_unique;
+  r.out[1] = (uint64_t)*r.n_ins;
+  r.out[2] = r.stats[0];
+  r.out[3] = r.stats[1];
+  r.out[4] = (uint64_t)evicted;
+  r.out[5] = (uint64_t)evicted_dirty;
+  r.out[6] = 0;
+  r.out[7] = 0;
+  constexpr int kErrWords = sizeof(ErrorRecord) / sizeof(uint64_t);
+  const volatile uint64_t* ew = reinterpret_cast<const volatile uint64_t*>(err);
+  for (int k = 0; k < kErrWords; ++k) r.out[8 + k] = ew ? ew[k] : 0;
+  __threadfence_system();
+}
+
+int cache_evict_planned_rec(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids, const int64_t* d_n,
+                            int64_t n_max, const int64_t* d_expect, int64_t iteration, const bp_evict_buffers* o,
+                            const StepRecord& rec, cudaStream_t s);
+int cache_insert_sub(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids, const float* d_rows,
+                     const int64_t* d_ttls, int64_t n, const int64_t* d_n, int64_t sub, int64_t* n_out,
+                     int64_t iteration, cudaStream_t s);
+int mark_ids_zero(bp_prep* P, int64_t* d_mark, int64_t tag, int64_t* d_zero2, cudaStream_t s);
+
 // Green-context SM partition (green.cu): a stream of the hot (hot != 0) or
 // the rest partition, or nullptr when partitioning is off.
 int green_stream(int hot, int priority, cudaStream_t* out);

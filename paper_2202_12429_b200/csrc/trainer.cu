@@ -459,7 +459,8 @@ __global__ void k_key_rows(const uint64_t* __restrict__ keys, const long long* d
 }
 
 __global__ void k_mark_ids(const uint32_t* __restrict__ ids, const long long* __restrict__ d_U, int64_t* mark,
-                           long long tag) {
+                           long long tag, int64_t* zero2) {
+  if (zero2 && blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0;  // the step's stats (no memset)
   const long long U = *d_U;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < U; i += (long long)gridDim.x * blockDim.x)
     mark[ids[i]] = tag;
@@ -489,10 +490,19 @@ static inline void group_shape(int dim, int* G, int* dpl) {
   }
 
 extern "C" int bp_mark_ids(bp_prep* P, int64_t* d_mark, int64_t tag, bp_stream_t stream) {
+  return bp::mark_ids_zero(P, d_mark, tag, nullptr, (cudaStream_t)stream);
+}
+
+// bp_mark_ids that also zeroes two counters (the engine's step stats).
+int bp::mark_ids_zero(bp_prep* P, int64_t* d_mark, int64_t tag, int64_t* d_zero2, cudaStream_t stream) {
   using namespace bp;
-  if (P->n_occ == 0 || !P->schema_mode) return P->schema_mode ? BP_OK : BP_ERR_INVALID;
+  if (!P->schema_mode) return BP_ERR_INVALID;
+  if (P->n_occ == 0) {
+    if (d_zero2) BP_CUDA_TRY(cudaMemsetAsync(d_zero2, 0, 2 * sizeof(int64_t), stream));
+    return BP_OK;
+  }
   k_mark_ids<<<grid_for(P->n_occ, 256), 256, 0, (cudaStream_t)stream>>>(P->d_uniq_id_s, P->d_num_unique, d_mark,
-                                                                         tag);
+                                                                         tag, d_zero2);
   BP_LAUNCH_CHECK();
   return BP_OK;
 }
