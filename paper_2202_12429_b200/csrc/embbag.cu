@@ -882,7 +882,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 constexpr int kStagedF4 = 2048;  // float4 per k_embbag_bwd_staged tile (32 KB)
 
-template <int Q, int NT = 256, int F4 = kStagedF4>
+template <int Q, int NT = 256, int F4 = kStagedF4, bool ENDS = true>
 __global__ void __launch_bounds__(NT, 3 * 256 / NT) k_embbag_bwd_staged(
     const uint32_t* __restrict__ seg_of, const uint32_t* __restrict__ seg_start, uint32_t n,
     const float4* __restrict__ grad, float* __restrict__ values, int row_stride, const int32_t* __restrict__ slots_s,
@@ -898,10 +898,15 @@ __global__ void __launch_bounds__(NT, 3 * 256 / NT) k_embbag_bwd_staged(
   __shared__ float4 wagg[NW][Q];
   __shared__ int wflag[NW][Q];
   __shared__ uint8_t ghead[NG];
+  // rows that end a key's run inside the tile (pass 1 records them, pass 3
+  // walks only those: ~T/6 at Criteo-Kaggle shape instead of every row)
+  __shared__ uint16_t ends[ENDS ? T : 1];
+  __shared__ uint32_t n_ends;
   const uint32_t t0 = blockIdx.x * T;
   const uint32_t rows = min((uint32_t)T, n - t0);
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
+    if (ENDS) n_ends = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -958,12 +963,14 @@ __global__ void __launch_bounds__(NT, 3 * 256 / NT) k_embbag_bwd_staged(
       if (sr == ps) {
         acc = f4_add(acc, x);
       } else {
+        if (ENDS && c == 0) ends[atomicAdd(&n_ends, 1u)] = (uint16_t)(r - 1);  // row r-1 ends its run
         acc = x;
         flag = true;
       }
       tile[r * Q + c] = acc;
       ps = sr;
     }
+    if (ENDS && c == 0 && (re == rows || sgs[re] != ps)) ends[atomicAdd(&n_ends, 1u)] = (uint16_t)(re - 1);
   } else if (c == 0) {
     ghead[gi] = 1;
   }
@@ -1006,17 +1013,25 @@ __global__ void __launch_bounds__(NT, 3 * 256 / NT) k_embbag_bwd_staged(
   unsigned my_nz = 0;
   bool wrote = false;
   constexpr int ITEMS = T * Q / NT, B = 4;
+  const int n_items = ENDS ? (int)((n_ends + NG - 1) / NG) : ITEMS;
 #pragma unroll 1
-  for (int k0 = 0; k0 < ITEMS; k0 += B) {
+  for (int k0 = 0; k0 < n_items; k0 += B) {
     int32_t sl[B];
     float4 val[B];
 #pragma unroll
     for (int u = 0; u < B; ++u) {
-      const uint32_t r = (uint32_t)(tid / Q) + (uint32_t)(k0 + u) * NG;
       sl[u] = -1;
+      uint32_t r;
+      if (ENDS) {
+        const uint32_t e = (uint32_t)(tid / Q) + (uint32_t)(k0 + u) * NG;
+        if (e >= n_ends) continue;
+        r = ends[e];
+      } else {
+        r = (uint32_t)(tid / Q) + (uint32_t)(k0 + u) * NG;
+      }
       if (r >= rows) continue;
       const uint32_t s = sgs[r];
-      if (r + 1 < rows && sgs[r + 1] == s) continue;  // not the last row of its run
+      if (!ENDS && r + 1 < rows && sgs[r + 1] == s) continue;  // not the last row of its run
       const int32_t slot = tslot[s - tile_first];
       if (slot < 0) continue;
       const uint32_t g = r / RPG;
@@ -1947,7 +1962,8 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
     case 0:
     case 4:
     case 5:
-    case 6: {
+    case 6:
+    case 7: {
       const int q = dim / 4, T = kStagedF4 / 2 / q;  // scratch layout of the smallest tiles
       const unsigned tiles = (unsigned)((P->n_occ + T - 1) / T);
       const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
@@ -2022,23 +2038,31 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
       // one-shot staged tiles: 32 KB x 256 threads (variant 4) or 16 KB x 128
       // threads (variant 6: twice the CTAs resident per SM)
       const bool small = g_bwd_variant == 6;
+      const bool no_ends = g_bwd_variant == 7;  // the round-1 pass 3 over every row
       const int Ts = (small ? kStagedF4 / 2 : kStagedF4) / q;
       const unsigned stiles = (unsigned)((P->n_occ + Ts - 1) / Ts);
       const size_t smem = (size_t)Ts * q * sizeof(float4) + 2 * (size_t)Ts * sizeof(uint32_t);
-#define BP_BWD_STAGED(QQ, NT, F4)                                                                              \
+#define BP_BWD_STAGED(QQ, NT, F4, ...)                                                                         \
   {                                                                                                            \
     static bool attr = false;                                                                                  \
     if (!attr) {                                                                                               \
-      BP_CUDA_TRY(cudaFuncSetAttribute(k_embbag_bwd_staged<QQ, NT, F4>,                                        \
+      BP_CUDA_TRY(cudaFuncSetAttribute(k_embbag_bwd_staged<QQ, NT, F4, ##__VA_ARGS__>,                         \
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
       attr = true;                                                                                             \
     }                                                                                                          \
-    k_embbag_bwd_staged<QQ, NT, F4><<<stiles, NT, smem, s>>>(                                                  \
+    k_embbag_bwd_staged<QQ, NT, F4, ##__VA_ARGS__><<<stiles, NT, smem, s>>>(                                   \
         P->d_seg_of, P->d_seg_start, (uint32_t)P->n_occ, reinterpret_cast<const float4*>(d_grad_sorted),       \
         d_values, row_stride, d_slots_s, d_dirty, opt, lr, eps, parts, arrivals,                               \
         (unsigned long long*)d_stats);                                                                         \
   }
-      if (small) {
+      if (no_ends) {
+        switch (q) {
+          case 1: BP_BWD_STAGED(1, 256, kStagedF4, false); break;
+          case 2: BP_BWD_STAGED(2, 256, kStagedF4, false); break;
+          case 4: BP_BWD_STAGED(4, 256, kStagedF4, false); break;
+          default: BP_BWD_STAGED(8, 256, kStagedF4, false); break;
+        }
+      } else if (small) {
         switch (q) {
           case 1: BP_BWD_STAGED(1, 128, kStagedF4 / 2); break;
           case 2: BP_BWD_STAGED(2, 128, kStagedF4 / 2); break;

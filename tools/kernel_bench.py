@@ -130,7 +130,7 @@ def main():
         return float(np.median(times))
 
     out["embbag_bwd_warm_us"] = timed_warm(bwd, args.reps)
-    for var in (0, 1, 2, 3, 4, 5, 6):
+    for var in (0, 1, 2, 3, 4, 5, 6, 7):
         lib.bp_debug_bwd_variant(var)
         out[f"embbag_bwd_sorted_v{var}_warm_us"] = timed_warm(bwd_sorted, args.reps)
     lib.bp_debug_bwd_variant(0)
@@ -143,7 +143,7 @@ def main():
     out["embbag_fwd_variants_equal"] = bool(torch.equal(ref, pooled))
     out["embbag_bwd_us"] = timed(bwd, args.reps, flush)
     out["embbag_bwd_sorted_us"] = timed(bwd_sorted, args.reps, flush)
-    for var in (1, 2, 3, 4, 5, 6):  # other launch shapes (4: one-shot staged, 5: persistent fused, 6: small staged)
+    for var in (1, 2, 3, 4, 5, 6, 7):  # other launch shapes (4: split, 5: persistent, 6: small staged, 7: no end list)
         lib.bp_debug_bwd_variant(var)
         out[f"embbag_bwd_sorted_v{var}_us"] = timed(bwd_sorted, args.reps, flush)
     lib.bp_debug_bwd_variant(0)
@@ -173,7 +173,7 @@ def main():
         fwd()
         lib.bp_debug_fwd_variant(0)
 
-    for fn in (stub, fwd, fwd_sorted, bwd, bwd_sorted, variant(1), variant(2), variant(3), variant(4), variant(5), variant(6)):
+    for fn in (stub, fwd, fwd_sorted, bwd, bwd_sorted, variant(1), variant(2), variant(3), variant(4), variant(5), variant(6), variant(7)):
         flush.zero_()
         torch.cuda.synchronize()
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
