@@ -339,6 +339,8 @@ int bp_set_stub_short_ctas(int32_t per_sm);
 /* Tuning: preferred shared-memory carveout (%) of the short-segment kernel
  * (default 100; -1 = driver default).  Set before the first bp_stub_step. */
 int bp_set_stub_carveout(int32_t percent);
+/* Tuning: threads per long-segment (hot-key chain) CTA, 64..1024 (default 1024). */
+int bp_set_stub_long_threads(int32_t threads);
 /* Tuning: green-context SM partition of engines created afterwards: the
  * stub trainer's hot-key chains run on `sms` SMs of their own, every other
  * engine stream on the rest (0 = off, the default). */

@@ -211,6 +211,7 @@ _SIGS = {
     "bp_set_stub_fork": (c_i32, [c_i32]),
     "bp_set_stub_short_ctas": (c_i32, [c_i32]),
     "bp_set_stub_carveout": (c_i32, [c_i32]),
+    "bp_set_stub_long_threads": (c_i32, [c_i32]),
     "bp_set_green_sms": (c_i32, [c_i32]),
     "bp_set_peer_sorted": (c_i32, [c_i32]),
     "bp_embbag_backward_peer_sorted": (c_i32, [c_vp, c_vp, c_f32, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32,
@@ -309,6 +310,9 @@ def lib() -> C.CDLL:
                 gr = os.environ.get("BAGPIPE_B200_GREEN_SMS")  # tuning knob: SMs of the hot-key partition
                 if gr:
                     check(lb.bp_set_green_sms(int(gr)), "bp_set_green_sms")
+                lt = os.environ.get("BAGPIPE_B200_STUB_LONG_THREADS")  # tuning knob: hot-key chain CTA width
+                if lt:
+                    check(lb.bp_set_stub_long_threads(int(lt)), "bp_set_stub_long_threads")
                 co = os.environ.get("BAGPIPE_B200_STUB_CARVEOUT")  # tuning knob: short kernel smem carveout %
                 if co:
                     check(lb.bp_set_stub_carveout(int(co)), "bp_set_stub_carveout")

@@ -287,6 +287,19 @@ struct StageTimer {
   std::mutex mu;  // the planner thread (prep/planner stages) and the training thread record concurrently
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans[kNumStages];
   cudaEvent_t open[kNumStages] = {};
+  // recycled events: a span's begin event is recorded right before the
+  // stage's first launch, with no event creation on the host in between
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t take() {
+    if (pool.empty()) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      return ev;
+    }
+    cudaEvent_t ev = pool.back();
+    pool.pop_back();
+    return ev;
+  }
 };
 }  // namespace bp
 
@@ -360,8 +373,7 @@ static int engine_prep_slot(bp_engine* e, long long pos) { return (int)(pos % (l
 static void stage_begin(bp_engine* e, int stage, cudaStream_t s) {
   if (!e->cfg.timing) return;
   std::lock_guard<std::mutex> lk(e->timer.mu);
-  cudaEvent_t ev;
-  cudaEventCreate(&ev);
+  cudaEvent_t ev = e->timer.take();
   cudaEventRecord(ev, s);
   e->timer.open[stage] = ev;
 }
@@ -370,8 +382,7 @@ static void stage_end(bp_engine* e, int stage, cudaStream_t s) {
   if (!e->cfg.timing) return;
   std::lock_guard<std::mutex> lk(e->timer.mu);
   if (!e->timer.open[stage]) return;
-  cudaEvent_t ev;
-  cudaEventCreate(&ev);
+  cudaEvent_t ev = e->timer.take();
   cudaEventRecord(ev, s);
   e->timer.spans[stage].emplace_back(e->timer.open[stage], ev);
   e->timer.open[stage] = nullptr;
@@ -390,8 +401,8 @@ extern "C" int bp_engine_stage_times(bp_engine* e, double* h_ms, int64_t* h_coun
       float ms = 0;
       cudaEventElapsedTime(&ms, pr.first, pr.second);
       total += ms;
-      cudaEventDestroy(pr.first);
-      cudaEventDestroy(pr.second);
+      e->timer.pool.push_back(pr.first);
+      e->timer.pool.push_back(pr.second);
     }
     h_ms[st] = total;
     h_counts[st] = (int64_t)e->timer.spans[st].size();
@@ -540,6 +551,14 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   if (e->gate_ev) cudaEventDestroy(e->gate_ev);
   if (e->bwd_scratch) cudaFree(e->bwd_scratch);
   if (e->peer_rows) cudaFree(e->peer_rows);
+  for (auto& spans : e->timer.spans)
+    for (auto& pr : spans) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  for (auto ev : e->timer.open)
+    if (ev) cudaEventDestroy(ev);
+  for (auto ev : e->timer.pool) cudaEventDestroy(ev);
   cudaFreeHost(e->h_fetch_ids);
   cudaFreeHost(e->h_fetch_rows);
   cudaFreeHost(e->h_flush_ids);
@@ -1377,7 +1396,10 @@ extern "C" int bp_engine_chunk_view(bp_engine* e, int32_t chunk_slot, bp_evict_b
 extern "C" int bp_engine_set_timing(bp_engine* e, int32_t on) {
   std::lock_guard<std::mutex> lk(e->timer.mu);
   e->cfg.timing = on ? 1 : 0;
-  for (auto& ev : e->timer.open) ev = nullptr;
+  for (auto& ev : e->timer.open) {
+    if (ev) e->timer.pool.push_back(ev);
+    ev = nullptr;
+  }
   return BP_OK;
 }
 

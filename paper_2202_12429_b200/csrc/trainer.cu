@@ -96,7 +96,7 @@ constexpr int kLongWindowChunks = 1024;  // 16 KB of occurrence bytes staged in 
 // per-key load that does not depend on another is issued up front, and the
 // label chunks are prefetched two rounds ahead.
 template <int G, int DPL>
-__global__ void __launch_bounds__(128) k_stub_step_long(
+__global__ void __launch_bounds__(1024) k_stub_step_long(
     const uint32_t* __restrict__ seg_start, const uint8_t* __restrict__ occ_label,
     const long long* __restrict__ d_U, const uint32_t* __restrict__ long_list,
     const long long* __restrict__ d_num_long, long long long_cap, float* __restrict__ rows, const int32_t* __restrict__ row_index,
@@ -532,6 +532,10 @@ static SideStream& side_stream() {
 static bool g_fork_long = true;
 static cudaStream_t g_long_stream = nullptr;  // engine-provided stream for the chains (green partition)
 static int g_short_ctas = 5;  // tuning knob (bp_set_stub_short_ctas): short-kernel CTAs per SM
+// threads of a long-segment CTA (bp_set_stub_long_threads): one warp runs the
+// chain, the others stage occurrence bytes; a wider CTA also leaves fewer
+// thread slots on its SM for short-kernel warps competing with the chain
+static int g_long_threads = 1024;
 
 static int g_short_carveout = 100;  // tuning knob: shared-memory carveout (%) of the short kernel
 
@@ -593,7 +597,7 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
     parts = side.parts;
   }
   BP_DISPATCH_GD(G, dpl,
-                 (long_attr<g_, d_>(), k_stub_step_long<g_, d_><<<kLongBlocks, 128, kLongSmemPad, ls>>>(
+                 (long_attr<g_, d_>(), k_stub_step_long<g_, d_><<<kLongBlocks, g_long_threads, kLongSmemPad, ls>>>(
                      P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,
                      d_row_index, d_dirty, dim, c_value, c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark,
                      next_tag, (unsigned long long*)d_stats, P->d_occ_pos, P->d_rank_bounds, T, parts)));
@@ -621,6 +625,12 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
 namespace bp {
 void set_long_stream(cudaStream_t s) { g_long_stream = s; }
 }  // namespace bp
+
+extern "C" int bp_set_stub_long_threads(int32_t threads) {
+  if (threads < 64 || threads > 1024 || (threads & 31)) return BP_ERR_INVALID;
+  g_long_threads = threads;
+  return BP_OK;
+}
 
 extern "C" int bp_set_stub_carveout(int32_t percent) {
   if (percent < -1 || percent > 100) return BP_ERR_INVALID;
