@@ -347,7 +347,10 @@ int bp_set_stub_long_threads(int32_t threads);
 int bp_set_green_sms(int32_t sms);
 /* {hot-partition SMs, rest SMs} of the partition in use ({0, 0} when off). */
 int bp_green_info(int32_t* out2);
-int bp_set_stub_fork(int32_t on);
+/* Trainer stub stream layout: 0 = one stream; 1 = hot-key chains on a side
+ * stream; 2 (default) = chains first on the caller's stream, short kernel on
+ * the side stream. */
+int bp_set_stub_fork(int32_t mode);
 /* mark[id] = tag for every unique key of a schema-mode prep. */
 int bp_mark_ids(bp_prep* prep, int64_t* d_mark, int64_t tag, bp_stream_t stream);
 /* np.add.at(out, idx, vals) row-wise in input order, over a registry-mode

@@ -247,8 +247,7 @@ __global__ void k_evict_out(const uint32_t* __restrict__ flag, const uint32_t* _
     dirty[i] = 0;
     free_list[top + (cnt - 1 - p)] = (uint32_t)i;
   }
-  nd = warp_sum(nd);
-  if (lane_id() == 0 && nd) atomicAdd(n_dirty, nd);
+  cta_add(n_dirty, nd);
 }
 
 __global__ void k_evict_planned(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ids,

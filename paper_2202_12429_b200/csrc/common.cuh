@@ -91,6 +91,20 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// CTA-aggregated atomicAdd: every thread of the CTA must call it (it holds
+// two barriers); one global atomic per CTA.  Same-address atomics serialise
+// in the L2's atomic unit (~0.65 ns each on B200: tools/mb/atomic_probe.cu),
+// so one per warp of a 1,664-CTA grid alone costs ~9 us.
+__device__ __forceinline__ void cta_add(unsigned long long* ctr, unsigned long long v) {
+  __shared__ unsigned long long s_acc;
+  if (threadIdx.x == 0) s_acc = 0;
+  __syncthreads();
+  v = warp_sum(v);
+  if (lane_id() == 0 && v) atomicAdd(&s_acc, v);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_acc) atomicAdd(ctr, s_acc);
+}
+
 // Warp-aggregated atomicAdd of a predicate count.
 __device__ __forceinline__ void warp_count_add(unsigned long long* ctr, bool pred) {
   const unsigned mask = __ballot_sync(0xffffffffu, pred);

@@ -1075,11 +1075,8 @@ __global__ void __launch_bounds__(NT, 3 * 256 / NT) k_embbag_bwd_staged(
       }
     }
   }
-  // stats: one atomic per warp (no CTA-wide reduction barrier)
-  if (stats) {
-    for (int off = 16; off > 0; off >>= 1) my_nz += __shfl_down_sync(0xffffffffu, my_nz, off);
-    if ((tid & 31) == 0 && my_nz) atomicAdd(&stats[1], (unsigned long long)my_nz);
-  }
+  // stats: one atomic per CTA (same-address atomics serialise in L2)
+  if (stats) cta_add(&stats[1], my_nz);
   if (span1 || span2) {
     // partials visible device-wide, then warp 0 alone counts the arrivals and
     // (if it completed a key) combines; the other warps are done
@@ -1369,10 +1366,7 @@ __global__ void __launch_bounds__(256, 2) k_embbag_bwd_pipe(
       }
     }
   }
-  if (stats) {
-    for (int off = 16; off > 0; off >>= 1) my_nz += __shfl_down_sync(0xffffffffu, my_nz, off);
-    if ((tid & 31) == 0 && my_nz) atomicAdd(&stats[1], (unsigned long long)my_nz);
-  }
+  if (stats) cta_add(&stats[1], my_nz);
 }
 
 // Two-kernel backward (variant 4; measured slower inside the step than the
@@ -1588,10 +1582,7 @@ __global__ void __launch_bounds__(256) k_bwd_apply(const uint32_t* __restrict__ 
   const unsigned gm = (Q == 32 ? 0xffffffffu : ((1u << Q) - 1u)) << (lane / Q * Q);
   const bool key_nz = (bal & gm) != 0 && c == 0 && s < U;
   if (key_nz && dirty) dirty[slots_s[s]] = 1;
-  if (stats) {
-    const unsigned cnt = __popc(__ballot_sync(0xffffffffu, key_nz));
-    if (lane == 0 && cnt) atomicAdd(&stats[1], (unsigned long long)cnt);
-  }
+  if (stats) cta_add(&stats[1], key_nz ? 1ull : 0ull);
 }
 
 // Keys spanning several tiles, listed by the tile kernels at the key's first

@@ -1032,8 +1032,7 @@ __global__ void k_count_critical(const uint32_t* __restrict__ ids, const long lo
   unsigned long long c = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < U; i += (long long)gridDim.x * blockDim.x)
     c += mark[ids[i]] == tag;
-  c = warp_sum(c);
-  if (lane_id() == 0 && c) atomicAdd(stats, c);
+  cta_add(stats, c);
 }
 
 // Eviction of ttl <= iteration into chunk_slot (+ full drain into drain_slot

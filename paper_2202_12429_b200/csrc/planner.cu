@@ -64,8 +64,7 @@ __global__ void k_refill(const uint32_t* __restrict__ ids, const long long* d_U,
     }
     last[id] = iteration;  // appended iterations increase: plain store == tracker[e] = j
   }
-  added = warp_sum(added);
-  if (lane_id() == 0 && added) atomicAdd((unsigned long long*)&ctr->tracked, added);
+  cta_add((unsigned long long*)&ctr->tracked, added);
 }
 
 // The whole pop of one batch in ONE launch (reference lookahead.py:84-110):

@@ -290,6 +290,11 @@ __global__ void __launch_bounds__(256, 6) k_stub_step(
   const long long groups_per_block = blockDim.x / G;
   const long long groups_total = (long long)gridDim.x * groups_per_block;
   const long long warp_first = (long long)blockIdx.x * groups_per_block + (threadIdx.x >> 5) * (32 / G);
+  // the counters are summed per CTA in shared memory: one global atomic per
+  // CTA instead of one per warp and key round on the same two addresses
+  __shared__ unsigned int cta_stats[2];
+  if (threadIdx.x < 2) cta_stats[threadIdx.x] = 0u;
+  __syncthreads();
 
   for (long long base = warp_first; base < U; base += groups_total) {
     const long long s = base + (long long)(lane / G);
@@ -361,10 +366,14 @@ __global__ void __launch_bounds__(256, 6) k_stub_step(
       const unsigned cm = __ballot_sync(0xffffffffu, crit);
       const unsigned dm = __ballot_sync(0xffffffffu, active && lane_g == 0 && nz != 0);
       if (lane == 0) {
-        if (cm) atomicAdd(&stats[0], (unsigned long long)__popc(cm));
-        if (dm) atomicAdd(&stats[1], (unsigned long long)__popc(dm));
+        if (cm) atomicAdd(&cta_stats[0], (unsigned)__popc(cm));
+        if (dm) atomicAdd(&cta_stats[1], (unsigned)__popc(dm));
       }
     }
+  }
+  if (stats) {
+    __syncthreads();
+    if (threadIdx.x < 2 && cta_stats[threadIdx.x]) atomicAdd(&stats[threadIdx.x], (unsigned long long)cta_stats[threadIdx.x]);
   }
 }
 
@@ -529,7 +538,11 @@ static SideStream& side_stream() {
   return side;
 }
 
-static bool g_fork_long = true;
+// 0: both kernels on the caller's stream; 1: hot-key chains on a side stream;
+// 2 (default): chains on the caller's stream, launched first, and the short
+// kernel on the side stream -- the chain CTAs then reach their SMs before the
+// short kernel's grid fills them, instead of racing a cross-stream event
+static int g_fork_long = 2;
 static cudaStream_t g_long_stream = nullptr;  // engine-provided stream for the chains (green partition)
 static int g_short_ctas = 5;  // tuning knob (bp_set_stub_short_ctas): short-kernel CTAs per SM
 // threads of a long-segment CTA (bp_set_stub_long_threads): one warp runs the
@@ -571,13 +584,15 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
   const int blocks = grid_for(groups * G, threads, kNumSMs * g_short_ctas);
   // the long-segment kernel (a few sequential hot-key chains) runs on a side
   // stream beside the short-segment kernel: the two touch disjoint keys
-  cudaStream_t ls = s;
+  cudaStream_t ls = s, ss = s;
   if (g_fork_long) {
     SideStream& side = side_stream();
     if (!side.s) return BP_ERR_CUDA;
-    ls = g_long_stream ? g_long_stream : side.s;
+    if (g_fork_long == 2 && !g_long_stream) ss = side.s;
+    else ls = g_long_stream ? g_long_stream : side.s;
+    cudaStream_t forked = ls != s ? ls : ss;
     BP_CUDA_TRY(cudaEventRecord(side.fork, s));
-    BP_CUDA_TRY(cudaStreamWaitEvent(ls, side.fork, 0));
+    BP_CUDA_TRY(cudaStreamWaitEvent(forked, side.fork, 0));
   }
   // T > 1: the long keys' rank runs are separate chains (rank partials in a
   // stream-ordered scratch), combined in rank order by k_stub_long_combine
@@ -608,15 +623,15 @@ extern "C" int bp_stub_step(bp_ctx* ctx, bp_prep* P, float* d_rows, const int32_
                        d_grad_out, P->d_uniq_id_s, d_next_mark, next_tag, (unsigned long long*)d_stats)));
   }
   BP_DISPATCH_GD(G, dpl,
-                 (k_stub_step<g_, d_><<<blocks, threads, 0, s>>>(
+                 (k_stub_step<g_, d_><<<blocks, threads, 0, ss>>>(
                      P->d_seg_start, P->d_occ_label, P->d_num_unique, P->d_long, P->d_num_long, P->long_cap, d_rows,
                      d_row_index, d_dirty, dim, c_value,
                      c_label, lr, mode, d_grad_out, P->d_uniq_id_s, d_next_mark, next_tag,
                      (unsigned long long*)d_stats)));
   BP_LAUNCH_CHECK();
-  if (ls != s) {
+  if (ls != s || ss != s) {
     SideStream& side = side_stream();
-    BP_CUDA_TRY(cudaEventRecord(side.join, ls));
+    BP_CUDA_TRY(cudaEventRecord(side.join, ls != s ? ls : ss));
     BP_CUDA_TRY(cudaStreamWaitEvent(s, side.join, 0));
   }
   return BP_OK;
@@ -644,8 +659,9 @@ extern "C" int bp_set_stub_short_ctas(int32_t per_sm) {
   return BP_OK;
 }
 
-extern "C" int bp_set_stub_fork(int32_t on) {
-  g_fork_long = on != 0;
+extern "C" int bp_set_stub_fork(int32_t mode) {
+  if (mode < 0 || mode > 2) return BP_ERR_INVALID;
+  g_fork_long = mode;
   return BP_OK;
 }
 
