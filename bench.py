@@ -319,6 +319,7 @@ def _timed_steps(pipe, first: int, steps: int, flush_buf, torch, exclusive: int 
     try:
         torch.cuda.synchronize()
         wall0 = time.perf_counter()
+        wait0 = pipe.host_wait_s
         start.record(stream)
         host_ts = []
         for i in range(steps):
@@ -329,6 +330,7 @@ def _timed_steps(pipe, first: int, steps: int, flush_buf, torch, exclusive: int 
         end.record(stream)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - wall0) * 1e3
+        pipe.timed_host_wait_ms = (pipe.host_wait_s - wait0) * 1e3
     finally:
         gc.enable()
     dump = os.environ.get("BAGPIPE_B200_BENCH_DUMP")  # debug: host time of every timed step
@@ -429,6 +431,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     pipe.lib.bp_engine_set_timing(pipe.eng, 0)
     clocks.start()
     ms, wall_ms = _timed_steps(pipe, warm, steps, flush_buf, torch)
+    host_wait_ms = pipe.timed_host_wait_ms
     flush_ms = _flush_ms(flush_buf, steps, torch)
     clk = clocks.stop()
     records = pipe.records[warm:warm + steps]
@@ -583,6 +586,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "gpu_launches": launches_per_step * steps,
         "clocks": clk,
         "wall_ms_timed_region": wall_ms,
+        # host time blocked waiting for step results inside the span: near 0
+        # means the host loop, not the device, paces the steps
+        "host_wait_ms_timed_region": round(host_wait_ms, 3),
         "l2_flush_ms_per_step": flush_ms / steps,
         "ms_per_step_exclusive_flush": ms_excl / steps,
         "ms_per_step_by_rank": by_rank,

@@ -341,6 +341,9 @@ int bp_set_stub_short_ctas(int32_t per_sm);
 int bp_set_stub_carveout(int32_t percent);
 /* Tuning: threads per long-segment (hot-key chain) CTA, 64..1024 (default 1024). */
 int bp_set_stub_long_threads(int32_t threads);
+/* Dynamic shared memory of a hot-key chain CTA (its SM's room for short-kernel
+ * CTAs): bytes, default 120 KB. */
+int bp_set_stub_long_smem(int32_t bytes);
 /* Tuning: green-context SM partition of engines created afterwards: the
  * stub trainer's hot-key chains run on `sms` SMs of their own, every other
  * engine stream on the rest (0 = off, the default). */
@@ -351,6 +354,9 @@ int bp_green_info(int32_t* out2);
  * stream; 2 (default) = chains first on the caller's stream, short kernel on
  * the side stream. */
 int bp_set_stub_fork(int32_t mode);
+/* Engine write-back (link mode 0, log): 1 (default) = row DMA on its own
+ * stream, overlapping the prefetch reads; 0 = on the link stream. */
+int bp_set_split_writeback(int32_t on);
 /* mark[id] = tag for every unique key of a schema-mode prep. */
 int bp_mark_ids(bp_prep* prep, int64_t* d_mark, int64_t tag, bp_stream_t stream);
 /* np.add.at(out, idx, vals) row-wise in input order, over a registry-mode

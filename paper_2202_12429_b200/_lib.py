@@ -209,9 +209,11 @@ _SIGS = {
     "bp_set_link_config": (c_i32, [c_i32, c_i32, c_i32]),
     "bp_set_write_blocks": (c_i32, [c_i32]),
     "bp_set_stub_fork": (c_i32, [c_i32]),
+    "bp_set_split_writeback": (c_i32, [c_i32]),
     "bp_set_stub_short_ctas": (c_i32, [c_i32]),
     "bp_set_stub_carveout": (c_i32, [c_i32]),
     "bp_set_stub_long_threads": (c_i32, [c_i32]),
+    "bp_set_stub_long_smem": (c_i32, [c_i32]),
     "bp_set_green_sms": (c_i32, [c_i32]),
     "bp_set_peer_sorted": (c_i32, [c_i32]),
     "bp_embbag_backward_peer_sorted": (c_i32, [c_vp, c_vp, c_f32, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_f32,
@@ -310,6 +312,9 @@ def lib() -> C.CDLL:
                 gr = os.environ.get("BAGPIPE_B200_GREEN_SMS")  # tuning knob: SMs of the hot-key partition
                 if gr:
                     check(lb.bp_set_green_sms(int(gr)), "bp_set_green_sms")
+                ls_ = os.environ.get("BAGPIPE_B200_STUB_LONG_SMEM")  # tuning knob: chain CTA smem pad (bytes)
+                if ls_:
+                    check(lb.bp_set_stub_long_smem(int(ls_)), "bp_set_stub_long_smem")
                 lt = os.environ.get("BAGPIPE_B200_STUB_LONG_THREADS")  # tuning knob: hot-key chain CTA width
                 if lt:
                     check(lb.bp_set_stub_long_threads(int(lt)), "bp_set_stub_long_threads")
@@ -319,6 +324,9 @@ def lib() -> C.CDLL:
                 sc_ = os.environ.get("BAGPIPE_B200_STUB_SHORT_CTAS")  # tuning knob: short trainer CTAs per SM
                 if sc_:
                     check(lb.bp_set_stub_short_ctas(int(sc_)), "bp_set_stub_short_ctas")
+                sw = os.environ.get("BAGPIPE_B200_SPLIT_WB")  # A/B switch: write-back on its own stream
+                if sw:
+                    check(lb.bp_set_split_writeback(int(sw)), "bp_set_split_writeback")
                 sf = os.environ.get("BAGPIPE_B200_STUB_FORK")  # tuning knob: long trainer kernel beside the short
                 if sf:
                     check(lb.bp_set_stub_fork(int(sf)), "bp_set_stub_fork")

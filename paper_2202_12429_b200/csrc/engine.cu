@@ -312,6 +312,14 @@ struct bp_engine {
   bp_cache* cache;
   bp_planner* planner;
   cudaStream_t compute, link, planq;
+  // write-back appends (link mode 0) on their own stream: the copy-engine
+  // D2H of evicted rows overlaps the prefetch's zero-copy reads (opposite
+  // link directions).  Fetches wait for the latest commit (wb_done); a
+  // commit, a compaction or a direct table write waits for the latest fetch
+  // (fetch_done) -- every fetch reads exactly what it reads in stream order.
+  cudaStream_t wb = nullptr;
+  cudaEvent_t wb_done = nullptr, fetch_done = nullptr;
+  bool wb_pending = false, fetch_pending = false;
   cudaStream_t prepq;  // batch uploads + preps, ahead of and apart from the planner
   std::vector<bp_prep*> preps;  // ring indexed by position
   std::vector<cudaEvent_t> prep_ready;  // per prep slot, recorded on planq
@@ -434,6 +442,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   if (gs) {
     e->compute = gs;
     int grc = green_stream(0, lo, &e->link);
+    if (!grc) grc = green_stream(0, lo, &e->wb);
     if (!grc) grc = green_stream(0, hi < lo ? hi + 1 : hi, &e->planq);
     if (!grc) grc = green_stream(0, hi < lo ? hi + 1 : hi, &e->prepq);
     cudaStream_t hs = nullptr;
@@ -443,6 +452,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   } else {
     BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->compute, cudaStreamNonBlocking, hi));
     BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->link, cudaStreamNonBlocking, lo));
+    BP_CUDA_TRY(cudaStreamCreateWithPriority(&e->wb, cudaStreamNonBlocking, lo));
     // Batch prep and the planner window step of batches entering the window run
     // on their own stream: they depend only on the trace, so they overlap the
     // training of the iterations ahead of them.
@@ -505,6 +515,8 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     BP_CUDA_TRY(cudaMalloc(&e->d_labels_staging[i], n + 16));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->staging_free[i], cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->join_ev[i], cudaEventDisableTiming));
+    if (i == 0) BP_CUDA_TRY(cudaEventCreateWithFlags(&e->wb_done, cudaEventDisableTiming));
+    if (i == 0) BP_CUDA_TRY(cudaEventCreateWithFlags(&e->fetch_done, cudaEventDisableTiming));
     if (i == 0) BP_CUDA_TRY(cudaEventCreateWithFlags(&e->join_ev[2], cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventCreateWithFlags(&e->step_done[i], cudaEventDisableTiming));
     BP_CUDA_TRY(cudaEventRecord(e->staging_free[i], e->prepq));
@@ -612,6 +624,9 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   for (auto& ev : e->prep_ready) cudaEventDestroy(ev);
   cudaStreamDestroy(e->compute);
   cudaStreamDestroy(e->link);
+  if (e->wb) cudaStreamDestroy(e->wb);
+  if (e->wb_done) cudaEventDestroy(e->wb_done);
+  if (e->fetch_done) cudaEventDestroy(e->fetch_done);
   cudaStreamDestroy(e->planq);
   cudaStreamDestroy(e->prepq);
   delete e;
@@ -840,6 +855,7 @@ extern "C" int bp_engine_plan_view(bp_engine* e, int32_t slot, bp_plan_buffers* 
 // (zero-copy scatters are the worst interferers: tools/mb/interfere.cu).
 extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threads) {
   if (mode < 0 || mode > 2) return BP_ERR_INVALID;
+  BP_CUDA_TRY(cudaStreamSynchronize(e->wb));
   BP_CUDA_TRY(cudaStreamSynchronize(e->link));
   if (mode != 0) {  // the host worker paths read / write the table itself
     const int rc = bp_store_compact(e->store, e->link);
@@ -878,6 +894,7 @@ extern "C" int bp_engine_set_link_mode(bp_engine* e, int32_t mode, int32_t threa
 // flushes append to by DMA (0: zero-copy scatter into the table).
 extern "C" int bp_engine_set_write_log(bp_engine* e, int64_t log_rows) {
   if (log_rows <= 0) return BP_OK;
+  BP_CUDA_TRY(cudaStreamSynchronize(e->wb));
   return bp_store_enable_log(e->store, log_rows, e->link);
 }
 
@@ -894,6 +911,8 @@ extern "C" int bp_engine_set_link_gate(bp_engine* e, int32_t on) {
 extern "C" int bp_engine_fetch(bp_engine* e, int32_t slot) {
   bp::PlanSlot& ps = e->plans[slot];
   BP_CUDA_TRY(cudaStreamWaitEvent(e->link, ps.popped, 0));
+  // rows written back by every flush enqueued before this fetch are visible
+  if (e->wb_pending) BP_CUDA_TRY(cudaStreamWaitEvent(e->link, e->wb_done, 0));
   // the waited-for forward was enqueued before this fetch and everything
   // that waits on the fetch (the plan's apply) is enqueued after it: no cycle
   if (e->link_gate) BP_CUDA_TRY(cudaStreamWaitEvent(e->link, e->gate_ev, 0));
@@ -918,12 +937,24 @@ extern "C" int bp_engine_fetch(bp_engine* e, int32_t slot) {
   }
   bp::stage_end(e, bp::kStageFetch, e->link);
   BP_CUDA_TRY(cudaEventRecord(ps.fetched, e->link));
+  BP_CUDA_TRY(cudaEventRecord(e->fetch_done, e->link));
+  e->fetch_pending = true;
+  return BP_OK;
+}
+
+static int g_split_wb = 1;  // bp_set_split_writeback
+
+extern "C" int bp_set_split_writeback(int32_t on) {
+  g_split_wb = on != 0;
   return BP_OK;
 }
 
 // Dirty write-back of chunk slots, in order (last write wins), on the link stream.
 extern "C" int bp_engine_flush(bp_engine* e, const int32_t* chunk_slots, int32_t n) {
-  bp::stage_begin(e, bp::kStageFlush, e->link);
+  // link mode 0: the write-back stream (see bp_engine.wb); host-worker modes
+  // keep everything on the link stream
+  cudaStream_t ws = (g_split_wb && e->link_mode == 0) ? e->wb : e->link;
+  bp::stage_begin(e, bp::kStageFlush, ws);
   for (int i = 0; i < n; ++i) {
     bp::ChunkSlot& c = e->chunks[chunk_slots[i]];
     if (e->link_mode >= 1 && c.h_count >= 0) {
@@ -945,16 +976,24 @@ extern "C" int bp_engine_flush(bp_engine* e, const int32_t* chunk_slots, int32_t
     } else if (e->link_mode == 0 && c.h_count >= 0 && c.h_count <= bp_store_log_rows(e->store)) {
       // write-back log: one copy-engine append of the chunk + a commit kernel
       // (no zero-copy scatter stalling the compute stream)
-      int rc = bp_store_log_append(e->store, c.ids, c.rows, c.dirty, c.h_count, e->link);
+      // split stream: the DMA overlaps the fetch enqueued before this flush,
+      // the commit (or a compaction) waits for it
+      int rc = bp::store_log_append_fenced(e->store, c.ids, c.rows, c.dirty, c.h_count, ws,
+                                           (ws != e->link && e->fetch_pending) ? e->fetch_done : nullptr);
       if (rc) return rc;
     } else {
-      int rc = bp_store_write_masked(e->store, c.ids, c.rows, c.dirty, e->cfg.capacity, c.count, e->link);
+      if (ws != e->link && e->fetch_pending) BP_CUDA_TRY(cudaStreamWaitEvent(ws, e->fetch_done, 0));
+      int rc = bp_store_write_masked(e->store, c.ids, c.rows, c.dirty, e->cfg.capacity, c.count, ws);
       if (rc) return rc;
     }
-    BP_CUDA_TRY(cudaEventRecord(c.flushed, e->link));
+    BP_CUDA_TRY(cudaEventRecord(c.flushed, ws));
     c.pending = false;
   }
-  bp::stage_end(e, bp::kStageFlush, e->link);
+  bp::stage_end(e, bp::kStageFlush, ws);
+  if (ws != e->link && n > 0) {
+    BP_CUDA_TRY(cudaEventRecord(e->wb_done, ws));
+    e->wb_pending = true;
+  }
   return BP_OK;
 }
 
@@ -976,12 +1015,15 @@ static int engine_apply(bp_engine* e, bp_prep* P, PlanSlot& ps, int64_t next_pos
       BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[0], 0));
       BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[1], 0));
       BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[2], 0));
+      BP_CUDA_TRY(cudaEventRecord(e->join_ev[1], e->wb));
+      BP_CUDA_TRY(cudaStreamWaitEvent(s, e->join_ev[1], 0));
     }
     BP_CUDA_TRY(cudaMemsetAsync(e->l2_flush_buf, 0, e->l2_flush_bytes, s));
     if (e->l2_flush_exclusive) {
       BP_CUDA_TRY(cudaEventRecord(e->flush_ev, s));
       BP_CUDA_TRY(cudaStreamWaitEvent(e->planq, e->flush_ev, 0));
       BP_CUDA_TRY(cudaStreamWaitEvent(e->link, e->flush_ev, 0));
+      BP_CUDA_TRY(cudaStreamWaitEvent(e->wb, e->flush_ev, 0));
       BP_CUDA_TRY(cudaStreamWaitEvent(e->prepq, e->flush_ev, 0));
     }
   }
@@ -1416,6 +1458,9 @@ extern "C" int bp_engine_set_l2_flush(bp_engine* e, void* d_buf, int64_t bytes, 
 
 extern "C" int bp_engine_join(bp_engine* e, bp_stream_t stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  // the write-back stream first folds into the link stream
+  BP_CUDA_TRY(cudaEventRecord(e->join_ev[1], e->wb));
+  BP_CUDA_TRY(cudaStreamWaitEvent(e->link, e->join_ev[1], 0));
   BP_CUDA_TRY(cudaEventRecord(e->join_ev[0], e->planq));
   BP_CUDA_TRY(cudaEventRecord(e->join_ev[1], e->link));
   BP_CUDA_TRY(cudaEventRecord(e->join_ev[2], e->prepq));
@@ -1434,6 +1479,7 @@ extern "C" int bp_engine_sync(bp_engine* e) {
   BP_CUDA_TRY(cudaStreamSynchronize(e->compute));
   BP_CUDA_TRY(cudaStreamSynchronize(e->planq));
   BP_CUDA_TRY(cudaStreamSynchronize(e->prepq));
+  BP_CUDA_TRY(cudaStreamSynchronize(e->wb));
   BP_CUDA_TRY(cudaStreamSynchronize(e->link));
   return BP_OK;
 }

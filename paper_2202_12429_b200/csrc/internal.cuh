@@ -115,6 +115,8 @@ int mark_ids_zero(bp_prep* P, int64_t* d_mark, int64_t tag, int64_t* d_zero2, cu
 int green_stream(int hot, int priority, cudaStream_t* out);
 // The stub trainer's hot-key chains go to this stream when set (trainer.cu).
 void set_long_stream(cudaStream_t s);
+int store_log_append_fenced(bp_store* st, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_dirty,
+                            int64_t m, cudaStream_t s, cudaEvent_t before_commit);
 
 // Dense id of a packed key in schema mode; kNoId if out of schema.
 __device__ __forceinline__ uint32_t schema_id(const int64_t* base, const int64_t* rows, int num_tables,

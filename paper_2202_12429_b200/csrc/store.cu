@@ -478,27 +478,42 @@ extern "C" int bp_store_compact(bp_store* st, bp_stream_t stream) {
   return BP_OK;
 }
 
-extern "C" int bp_store_log_append(bp_store* st, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_dirty,
-                                   int64_t m, bp_stream_t stream) {
-  using namespace bp;
+namespace bp {
+// The append with an optional event waited for between the row DMA and the
+// commit: the engine's write-back stream DMAs into fresh log rows while an
+// earlier-enqueued fetch still reads the store, and publishes the rows only
+// after that fetch (so it reads exactly what it would have in stream order).
+int store_log_append_fenced(bp_store* st, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_dirty,
+                            int64_t m, cudaStream_t s, cudaEvent_t before_commit) {
   if (!st->log_rows || m > st->log_rows) return BP_ERR_INVALID;
   if (m <= 0) return BP_OK;
-  cudaStream_t s = (cudaStream_t)stream;
   if (st->log_pos + m > st->log_rows) {
-    const int rc = bp_store_compact(st, stream);
+    // compaction rewrites the table and recycles log rows: fenced as a whole
+    if (before_commit) BP_CUDA_TRY(cudaStreamWaitEvent(s, before_commit, 0));
+    before_commit = nullptr;
+    const int rc = bp_store_compact(st, s);
     if (rc) return rc;
   }
   const size_t rb = (size_t)st->dim * sizeof(float);
   BP_CUDA_TRY(cudaMemcpyAsync(st->h_log + (size_t)st->log_pos * st->dim, d_rows, (size_t)m * rb,
                               cudaMemcpyDeviceToHost, s));
+  if (before_commit) BP_CUDA_TRY(cudaStreamWaitEvent(s, before_commit, 0));
   k_log_commit<<<grid_for(m, 256), 256, 0, s>>>(d_ids, d_dirty, m, st->log_pos, st->d_loc, st->d_log_ids,
                                                 st->d_written);
   BP_LAUNCH_CHECK();
   st->log_pos += m;
   return BP_OK;
 }
+}  // namespace bp
+
+extern "C" int bp_store_log_append(bp_store* st, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_dirty,
+                                   int64_t m, bp_stream_t stream) {
+  return bp::store_log_append_fenced(st, d_ids, d_rows, d_dirty, m, (cudaStream_t)stream, nullptr);
+}
 
 extern "C" int64_t bp_store_log_rows(bp_store* st) { return st->log_rows; }
+
+
 
 extern "C" int bp_set_write_blocks(int32_t blocks) {
   if (blocks < 0 || blocks > 4096) return BP_ERR_INVALID;

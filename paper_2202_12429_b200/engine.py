@@ -272,6 +272,7 @@ class _Pipeline:
         self.drop_done = False
         self.result = L.StepResult()
         self._inflight: dict = {}
+        self.host_wait_s = 0.0  # host time blocked in bp_engine_train_end (device-bound steps)
         self._host_refs: dict = {}
         # planner thread (see _planner_loop); fault injection and event logs
         # keep the single-thread order
@@ -546,6 +547,7 @@ class _Pipeline:
 
     def begin(self) -> None:
         self._wall0 = time.perf_counter()
+        self.host_wait_s = 0.0
         self._wall_marks = []
         if self._threaded:
             self._device = torch.cuda.current_device()
@@ -610,7 +612,9 @@ class _Pipeline:
         plan, arrival, skip_key, has_skip, nxt, chunk, drain = self._inflight.pop(pos)
         res = self.result
         if self._split:
+            t0 = time.perf_counter()
             L.check(lib.bp_engine_train_end(self.eng, C.byref(res)), "bp_engine_train_end")
+            self.host_wait_s += time.perf_counter() - t0  # host blocked on the device
         else:
             self.trainer.train(self, pos, plan, nxt, skip_key, has_skip, chunk, drain, res)
         if res.err.code:

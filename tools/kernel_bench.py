@@ -90,6 +90,20 @@ def main():
                            "cta_total_cyc": int(t[4] - t[0])}
     starts = tr[:, 0]
     out["long_cta_start_spread_cyc"] = int(starts.max() - starts.min())
+    # the same chain with the short-segment kernel serialised after it (no
+    # co-resident warps competing for the chain warp's issue slots)
+    L.check(lib.bp_set_stub_fork(0), "bp_set_stub_fork")
+    trace.zero_()
+    L.check(lib.bp_debug_long_trace(L.ptr(trace)), "bp_debug_long_trace")
+    flush.zero_()
+    stub()
+    torch.cuda.synchronize()
+    L.check(lib.bp_debug_long_trace(None), "bp_debug_long_trace")
+    out["stub_step_serial_us"] = timed(stub, args.reps, flush)
+    L.check(lib.bp_set_stub_fork(2), "bp_set_stub_fork")
+    t = trace.view(148, 8).cpu().numpy()[hot]
+    out["long_hot_cta_alone"] = {"occurrences": int(t[5]), "chain_cyc": int(t[3] - t[2]),
+                                 "cyc_per_occurrence": round(float(t[3] - t[2]) / max(int(t[5]), 1), 2)}
 
     # EmbeddingBag forward / backward (DLRM prep: occurrence->unique maps)
     prep2 = make_prep(2)
