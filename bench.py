@@ -690,11 +690,17 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
             "roofline_parts": None if world > 1 else {
                 "gather": _part("bp::k_embbag_fwd_rows_v4 (EmbeddingBag forward: gather + pooling)",
                                 fwd_bytes, fwd_span, "k_embbag_fwd_rows_v4", ktimes),
-                "scatter": _part("bp::k_embbag_bwd_staged (sorted-gradient segmented scatter-add + SGD in place)",
-                                 bwd_bytes(n_occ, int(u_mean)), bwd_span, "k_embbag_bwd_staged", ktimes)}}
+                "scatter": _part(SCATTER_LABEL, bwd_bytes(n_occ, int(u_mean)), bwd_span,
+                                 ("k_embbag_bwd_staged", "k_bwd_reduce_reg", "k_bwd_apply"), ktimes)}}
 
 
-def _part(kernel: str, nbytes: int, span, ncu_name: str, ktimes: dict | None = None) -> dict:
+# the sorted-gradient backward kernels of the default variant (CUPTI times
+# of every listed kernel are summed)
+SCATTER_LABEL = ("bp::k_embbag_bwd_staged (sorted-gradient segmented scatter-add + SGD in place); "
+                 "variants 8/9: bp::k_bwd_reduce_reg + bp::k_bwd_apply")
+
+
+def _part(kernel: str, nbytes: int, span, ncu_name, ktimes: dict | None = None) -> dict:
     """One half of the EmbeddingBag pair: achieved = algorithmic bytes / the
     launch's CUDA-event span on the compute stream (the spec's measure; the
     span includes the launch gap behind the begin event), plus the CUPTI

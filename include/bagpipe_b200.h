@@ -629,7 +629,9 @@ int bp_trace_decode(const uint8_t* d_records, int64_t n, int32_t num_dense, int3
 /* Debug: per-CTA phase clock64() stamps of the long-segment trainer kernel
  * into d_buf[148][8] (NULL disables; tools/kernel_bench.py --trace). */
 int bp_debug_long_trace(void* d_buf);
-/* Debug: launch shape of bp_embbag_backward_sorted (0 default; tools/kernel_bench.py). */
+/* Debug: launch shape of bp_embbag_backward_sorted (-1 = default = 9, the
+ * register-resident reduce + update; 0 = the staged one-kernel form; 1-8 the
+ * other measured shapes, tools/kernel_bench.py). */
 int bp_debug_bwd_variant(int32_t variant);
 /* Debug: EmbeddingBag single-key forward shape (0 occurrence-order gather, 1 key-sorted scatter). */
 int bp_debug_fwd_variant(int32_t variant);

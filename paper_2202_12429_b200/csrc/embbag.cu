@@ -1529,16 +1529,201 @@ __global__ void __launch_bounds__(256, 4) k_bwd_reduce(const uint32_t* __restric
   }
 }
 
-template <int Q>
+// Register-resident reduce of the key-sorted gradient rows (variant 8, the
+// first half of the split backward; k_bwd_apply is the second).  A CTA owns
+// kRegTileF4 / Q sorted rows, each of its 8 warps 16 rows per lane group
+// (Q lanes, one float4 column each; the 16 loads of a lane are issued
+// together).  A group sums its rows in order, branch-free, and stores every
+// key that starts and ends inside them straight to gsum.  Two left-to-right
+// chains in fixed order complete the keys crossing group boundaries (through
+// shuffles) and warp boundaries (through shared memory); a key crossing the
+// CTA tile boundary leaves its partial in the tile's parts slot (1 at the
+// key's first tile, 0 at every later one) for k_bwd_apply.  No atomics,
+// one barrier; ncu on the staged and split kernels: 6.9M warp instructions
+// per CK batch, most of them in shared-memory passes and per-thread carry
+// loops.
+constexpr int kRegTileF4 = 4096;  // float4 per k_bwd_reduce_reg CTA tile (64 KB of gradient rows)
+
+// one segment of a chain: its first key (+ that key's sum, complete when the
+// segment holds more than one key) and its last key (+ sum); nk = keys seen
+struct ChainSeg {
+  uint32_t fk, lk;
+  int nk;
+  float4 fv, lv;
+};
+
+// Left-to-right merge of the open key (ok, ov) with the next segment:
+// returns through emit the keys it completes.  first: the open key is the
+// chain's first key.
+template <typename Emit>
+__device__ __forceinline__ void chain_step(uint32_t& ok, float4& ov, bool& first, const ChainSeg& sg, Emit&& emit) {
+  if (sg.nk == 0) return;
+  if (sg.fk == ok) {
+    if (sg.nk == 1) {
+      ov = f4_add(ov, sg.lv);
+      return;
+    }
+    emit(ok, f4_add(ov, sg.fv), first);
+  } else {
+    emit(ok, ov, first);
+    if (sg.nk >= 2) emit(sg.fk, sg.fv, false);
+  }
+  first = false;
+  ok = sg.lk;
+  ov = sg.lv;
+}
+
+template <int Q, int R = 16, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, (R == 16 ? 2 : 3) * 8 / NW) k_bwd_reduce_reg(
+    const uint32_t* __restrict__ seg_of, uint32_t n, const float4* __restrict__ grad, float4* __restrict__ gsum,
+    float4* __restrict__ parts) {
+  constexpr int G = 32 / Q, WT = G * R, T = NW * WT;
+  static_assert(T * Q == 32 * NW * R, "tile of k_bwd_apply");
+  const unsigned lane = threadIdx.x & 31u;
+  const int w = (int)(threadIdx.x >> 5), g = (int)(lane / Q), c = (int)(lane % Q);
+  const long long t0 = (long long)blockIdx.x * T;
+  const long long w0 = t0 + (long long)w * WT;
+  const long long r0 = w0 + (long long)g * R;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  const long long t_end = t0 + T < (long long)n ? t0 + T : (long long)n;
+  // neighbours of the CTA tile: does its first key come from the previous
+  // tile, does its last key go on into the next one
+  const uint32_t before = t0 > 0 ? seg_of[t0 - 1] : 0xFFFFFFFFu;
+  const uint32_t after = t_end < (long long)n ? seg_of[t_end] : 0xFFFFFFFEu;
+  // the lane's 16 rows, all loads in flight together
+  uint32_t sg[R];
+  float4 x[R];
+  if (r0 + R <= (long long)n) {
+#pragma unroll
+    for (int j = 0; j < R; j += 4) {
+      const uint4 q4 = *reinterpret_cast<const uint4*>(seg_of + r0 + j);
+      sg[j] = q4.x;
+      sg[j + 1] = q4.y;
+      sg[j + 2] = q4.z;
+      sg[j + 3] = q4.w;
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) x[j] = __ldcs(grad + (r0 + j) * Q + c);
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const bool ok = r0 + j < (long long)n;
+      sg[j] = ok ? seg_of[r0 + j] : 0xFFFFFFFFu;
+      x[j] = ok ? __ldcs(grad + (r0 + j) * Q + c) : zero;
+    }
+  }
+  // in-order segmented sum, branch-free: a key that closes as the group's
+  // second or later key started and ended here -> gsum
+  ChainSeg me;
+  me.fk = 0xFFFFFFFFu;
+  me.nk = 0;
+  me.fv = zero;
+  uint32_t cur = 0xFFFFFFFFu;
+  float4 acc = zero;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const bool valid = sg[j] != 0xFFFFFFFFu;
+    const bool same = sg[j] == cur;
+    const bool opens = valid && !same;
+    if (opens && me.nk >= 2) gsum[(size_t)cur * Q + c] = acc;
+    if (opens && me.nk == 1) me.fv = acc;
+    if (opens && me.nk == 0) me.fk = sg[j];
+    me.nk += opens ? 1 : 0;
+    const float4 sum = f4_add(acc, x[j]);
+    acc = !valid ? acc : (same ? sum : x[j]);
+    cur = valid ? sg[j] : cur;
+  }
+  me.lk = cur;
+  me.lv = acc;
+  // chain 1: the warp's groups, left to right (every lane runs it for its
+  // column; group 0's lanes store).  The warp's first and last keys stay
+  // open for chain 2.
+  ChainSeg ws;
+  {
+    ChainSeg s0;
+    s0.nk = __shfl_sync(0xffffffffu, me.nk, c);
+    s0.fk = __shfl_sync(0xffffffffu, me.fk, c);
+    s0.lk = __shfl_sync(0xffffffffu, me.lk, c);
+    s0.fv.x = __shfl_sync(0xffffffffu, me.fv.x, c);
+    s0.fv.y = __shfl_sync(0xffffffffu, me.fv.y, c);
+    s0.fv.z = __shfl_sync(0xffffffffu, me.fv.z, c);
+    s0.fv.w = __shfl_sync(0xffffffffu, me.fv.w, c);
+    s0.lv.x = __shfl_sync(0xffffffffu, me.lv.x, c);
+    s0.lv.y = __shfl_sync(0xffffffffu, me.lv.y, c);
+    s0.lv.z = __shfl_sync(0xffffffffu, me.lv.z, c);
+    s0.lv.w = __shfl_sync(0xffffffffu, me.lv.w, c);
+    ws = s0;  // fk / fv / nk describe the warp's first key until it closes
+    uint32_t ok_ = s0.lk;
+    float4 ov = s0.lv;
+    bool first = s0.nk <= 1;
+    int keys = s0.nk;
+    const bool leader = g == 0;
+#pragma unroll
+    for (int k = 1; k < G; ++k) {
+      const int src = k * Q + c;
+      ChainSeg sk;
+      sk.nk = __shfl_sync(0xffffffffu, me.nk, src);
+      sk.fk = __shfl_sync(0xffffffffu, me.fk, src);
+      sk.lk = __shfl_sync(0xffffffffu, me.lk, src);
+      sk.fv.x = __shfl_sync(0xffffffffu, me.fv.x, src);
+      sk.fv.y = __shfl_sync(0xffffffffu, me.fv.y, src);
+      sk.fv.z = __shfl_sync(0xffffffffu, me.fv.z, src);
+      sk.fv.w = __shfl_sync(0xffffffffu, me.fv.w, src);
+      sk.lv.x = __shfl_sync(0xffffffffu, me.lv.x, src);
+      sk.lv.y = __shfl_sync(0xffffffffu, me.lv.y, src);
+      sk.lv.z = __shfl_sync(0xffffffffu, me.lv.z, src);
+      sk.lv.w = __shfl_sync(0xffffffffu, me.lv.w, src);
+      keys += sk.nk > 0 ? sk.nk - (sk.fk == ok_ ? 1 : 0) : 0;
+      chain_step(ok_, ov, first, sk, [&](uint32_t key, float4 val, bool is_first) {
+        if (is_first) {
+          ws.fv = val;  // the warp's first key closes: chain 2 decides
+        } else if (leader) {
+          gsum[(size_t)key * Q + c] = val;
+        }
+      });
+    }
+    ws.nk = keys;
+    ws.lk = ok_;
+    ws.lv = ov;
+    if (keys <= 1) ws.fv = ov;
+  }
+  // chain 2: the CTA's warps, left to right, in shared memory
+  __shared__ ChainSeg wseg[NW][Q];
+  if (g == 0) wseg[w][c] = ws;
+  __syncthreads();
+  if (w != 0 || g != 0) return;
+  const ChainSeg s0 = wseg[0][c];
+  if (s0.nk == 0) return;
+  const bool cont_in = before == s0.fk;
+  const auto emit = [&](uint32_t key, float4 val, bool is_first) {
+    if (is_first && cont_in) parts[(size_t)(blockIdx.x * 2) * Q + c] = val;
+    else gsum[(size_t)key * Q + c] = val;
+  };
+  uint32_t ok_ = s0.lk;
+  float4 ov = s0.lv;
+  bool first = s0.nk <= 1;
+  if (s0.nk >= 2) emit(s0.fk, s0.fv, true);
+#pragma unroll 1
+  for (int k = 1; k < NW; ++k) chain_step(ok_, ov, first, wseg[k][c], emit);
+  // the tile's last key
+  if (after == ok_) parts[(size_t)(blockIdx.x * 2 + ((first && cont_in) ? 0 : 1)) * Q + c] = ov;
+  else emit(ok_, ov, first);
+}
+
+template <int Q, int TF4 = kRedF4>
 __global__ void __launch_bounds__(256) k_bwd_apply(const uint32_t* __restrict__ seg_start, const long long* d_U,
                                                    const float4* __restrict__ gsum, const float4* __restrict__ parts,
                                                    float* __restrict__ values, int row_stride,
                                                    const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty,
                                                    int opt, float lr, float eps,
                                                    unsigned long long* __restrict__ stats) {
-  constexpr int T = kRedF4 / Q;
+  constexpr int T = TF4 / Q;
   const long long U = *d_U;
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // grid-stride over (key, column) items: the grid is sized for the
+  // machine, not for the n_occ bound on U
+  unsigned long long my_nz = 0;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < U * Q; base += (long long)gridDim.x * blockDim.x) {
+  const long long i = base + threadIdx.x;
   const long long s = i / Q;
   const int c = (int)(i % Q);
   bool nz = false;
@@ -1582,7 +1767,9 @@ __global__ void __launch_bounds__(256) k_bwd_apply(const uint32_t* __restrict__ 
   const unsigned gm = (Q == 32 ? 0xffffffffu : ((1u << Q) - 1u)) << (lane / Q * Q);
   const bool key_nz = (bal & gm) != 0 && c == 0 && s < U;
   if (key_nz && dirty) dirty[slots_s[s]] = 1;
-  if (stats) cta_add(&stats[1], key_nz ? 1ull : 0ull);
+  my_nz += key_nz ? 1ull : 0ull;
+  }
+  if (stats) cta_add(&stats[1], my_nz);
 }
 
 // Keys spanning several tiles, listed by the tile kernels at the key's first
@@ -1865,10 +2052,16 @@ static int embbag_backward_impl(bp_prep* P, const float* d_grad, const int64_t* 
 // warp tiles: 1: R=8 x 3 CTAs/SM, 2: R=4 x 4, 3: R=8 x 2).  Measured at CK
 // shape (tools/embbag_instep.py, profiles/round2): in the step 0 = 6 = 30.7
 // us, 4: 35.8 us, 5: slower still; isolated 24-25 us for 0/6, 28-31 us for 4/5.
-static int g_bwd_variant = 0;
+// Sorted-gradient backward launch shape (bp_debug_bwd_variant; -1 = the
+// default).  9 (default): register-resident reduce in 512-row CTA tiles +
+// the per-key update (in-step CUPTI 19.5 us at CK shape against 26.7 us for
+// the staged one-kernel form, variant 0).
+constexpr int kBwdDefault = 9;
+static int g_bwd_variant = kBwdDefault;
 
 extern "C" int bp_debug_bwd_variant(int32_t v) {
-  g_bwd_variant = v;
+  if (v < -1 || v > 9) return BP_ERR_INVALID;
+  g_bwd_variant = v < 0 ? kBwdDefault : v;
   return BP_OK;
 }
 
@@ -1954,7 +2147,9 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
     case 4:
     case 5:
     case 6:
-    case 7: {
+    case 7:
+    case 8:
+    case 9: {
       const int q = dim / 4, T = kStagedF4 / 2 / q;  // scratch layout of the smallest tiles
       const unsigned tiles = (unsigned)((P->n_occ + T - 1) / T);
       const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
@@ -1964,6 +2159,39 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
       float4* parts = reinterpret_cast<float4*>(scratch);
       unsigned int* arrivals = reinterpret_cast<unsigned int*>(scratch + parts_bytes);
       if (!own) BP_CUDA_TRY(cudaMemsetAsync(arrivals, 0, tiles * sizeof(unsigned int), s));
+      if ((g_bwd_variant == 8 || g_bwd_variant == 9) && (reinterpret_cast<uintptr_t>(P->d_seg_of) & 15) == 0) {
+        // register-resident reduce + apply (k_bwd_reduce_reg, k_bwd_apply)
+        float4* gsum = reinterpret_cast<float4*>(scratch + parts_bytes + ((tiles * sizeof(unsigned int) + 255) & ~size_t(255)));
+        const bool r8 = g_bwd_variant == 9;  // 4-warp CTAs: 2 KB tiles, more CTAs per SM
+        const int Tr = (r8 ? kRegTileF4 / 2 : kRegTileF4) / q;
+        const unsigned rgrid = (unsigned)((P->n_occ + Tr - 1) / Tr);
+        float4* rparts = gsum + (size_t)P->n_occ * q;
+        const int agrid = grid_for(P->n_occ * q, 256, kNumSMs * 8);
+#define BP_BWD_REG(QQ)                                                                                        \
+  if (r8) {                                                                                                   \
+    k_bwd_reduce_reg<QQ, 16, 4><<<rgrid, 128, 0, s>>>(P->d_seg_of, (uint32_t)P->n_occ,                          \
+                                                  reinterpret_cast<const float4*>(d_grad_sorted), gsum, rparts);\
+    k_bwd_apply<QQ, kRegTileF4 / 2><<<agrid, 256, 0, s>>>(P->d_seg_start, P->d_num_unique, gsum, rparts,       \
+                                                          d_values, row_stride, d_slots_s, d_dirty, opt, lr,   \
+                                                          eps, (unsigned long long*)d_stats);                  \
+  } else {                                                                                                    \
+    k_bwd_reduce_reg<QQ><<<rgrid, 256, 0, s>>>(P->d_seg_of, (uint32_t)P->n_occ,                                 \
+                                               reinterpret_cast<const float4*>(d_grad_sorted), gsum, rparts);  \
+    k_bwd_apply<QQ, kRegTileF4><<<agrid, 256, 0, s>>>(P->d_seg_start, P->d_num_unique, gsum, rparts, d_values, \
+                                                      row_stride, d_slots_s, d_dirty, opt, lr, eps,            \
+                                                      (unsigned long long*)d_stats);                           \
+  }
+        switch (q) {
+          case 1: BP_BWD_REG(1); break;
+          case 2: BP_BWD_REG(2); break;
+          case 4: BP_BWD_REG(4); break;
+          default: BP_BWD_REG(8); break;
+        }
+#undef BP_BWD_REG
+        BP_LAUNCH_CHECK();
+        if (!own) cudaFreeAsync(scratch, s);
+        return BP_OK;
+      }
       if (g_bwd_variant == 4) {
         float4* gsum = reinterpret_cast<float4*>(scratch + parts_bytes + ((tiles * sizeof(unsigned int) + 255) & ~size_t(255)));
         const int Tr = kRedF4 / q;
@@ -1971,7 +2199,7 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
         float4* rparts = gsum + (size_t)P->n_occ * q;  // [rtiles][2][q] after gsum
         const size_t rsmem = (size_t)kPipeStages * ((size_t)Tr * q * sizeof(float4) + (size_t)Tr * sizeof(uint32_t));
         const unsigned grid = rtiles < 4u * kNumSMs ? rtiles : 4u * kNumSMs;
-        const int agrid = grid_for(P->n_occ * q, 256, 1 << 30);
+        const int agrid = grid_for(P->n_occ * q, 256, kNumSMs * 8);
 #define BP_BWD_SPLIT(QQ)                                                                                       \
   {                                                                                                            \
     static bool attr = false;                                                                                  \
