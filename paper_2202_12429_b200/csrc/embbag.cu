@@ -1576,7 +1576,7 @@ __device__ __forceinline__ void chain_step(uint32_t& ok, float4& ov, bool& first
 template <int Q, int R = 16, int NW = 8>
 __global__ void __launch_bounds__(NW * 32, (R == 16 ? 2 : 3) * 8 / NW) k_bwd_reduce_reg(
     const uint32_t* __restrict__ seg_of, uint32_t n, const float4* __restrict__ grad, float4* __restrict__ gsum,
-    float4* __restrict__ parts) {
+    float4* __restrict__ parts, uint32_t* __restrict__ span_list, unsigned* __restrict__ span_count) {
   constexpr int G = 32 / Q, WT = G * R, T = NW * WT;
   static_assert(T * Q == 32 * NW * R, "tile of k_bwd_apply");
   const unsigned lane = threadIdx.x & 31u;
@@ -1706,7 +1706,11 @@ __global__ void __launch_bounds__(NW * 32, (R == 16 ? 2 : 3) * 8 / NW) k_bwd_red
 #pragma unroll 1
   for (int k = 1; k < NW; ++k) chain_step(ok_, ov, first, wseg[k][c], emit);
   // the tile's last key
-  if (after == ok_) parts[(size_t)(blockIdx.x * 2 + ((first && cont_in) ? 0 : 1)) * Q + c] = ov;
+  if (after == ok_) {
+    parts[(size_t)(blockIdx.x * 2 + ((first && cont_in) ? 0 : 1)) * Q + c] = ov;
+    // the key's first tile lists it: k_bwd_apply gives it a whole warp
+    if (span_list && c == 0 && !(first && cont_in)) span_list[atomicAdd(span_count, 1u)] = ok_;
+  }
   else emit(ok_, ov, first);
 }
 
@@ -1716,12 +1720,67 @@ __global__ void __launch_bounds__(256) k_bwd_apply(const uint32_t* __restrict__ 
                                                    float* __restrict__ values, int row_stride,
                                                    const int32_t* __restrict__ slots_s, uint8_t* __restrict__ dirty,
                                                    int opt, float lr, float eps,
-                                                   unsigned long long* __restrict__ stats) {
+                                                   unsigned long long* __restrict__ stats,
+                                                   const uint32_t* __restrict__ span_list = nullptr,
+                                                   const unsigned* __restrict__ span_count = nullptr) {
   constexpr int T = TF4 / Q;
   const long long U = *d_U;
+  unsigned long long my_nz = 0;
+  if (span_count) {
+    // keys spanning tiles (listed by k_bwd_reduce_reg): a warp each, one
+    // lane per tile partial (all loaded at once), a fixed xor tree over the
+    // lanes, then the update by the first Q lanes
+    const unsigned nspan = *span_count;
+    const unsigned lane = threadIdx.x & 31u;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long wi = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); wi < nspan; wi += warps) {
+      const uint32_t key = span_list[wi];
+      const uint32_t ft = seg_start[key] / T, lt = (seg_start[key + 1] - 1) / T;
+      float4 part[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) part[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t t = ft + lane; t <= lt; t += 32) {  // lanes: ascending tiles; rounds: in order
+        const float4* pt = parts + (size_t)(t * 2 + (t == ft ? 1 : 0)) * Q;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) part[q] = f4_add(part[q], __ldcg(pt + q));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          float4 y;
+          y.x = __shfl_xor_sync(0xffffffffu, part[q].x, o);
+          y.y = __shfl_xor_sync(0xffffffffu, part[q].y, o);
+          y.z = __shfl_xor_sync(0xffffffffu, part[q].z, o);
+          y.w = __shfl_xor_sync(0xffffffffu, part[q].w, o);
+          part[q] = (lane & o) ? f4_add(y, part[q]) : f4_add(part[q], y);  // same order on both lanes
+        }
+      const int32_t slot = slots_s[key];
+      bool nz = false;
+      if (slot >= 0 && lane < (unsigned)Q) {
+        float4 gv = part[0];
+#pragma unroll
+        for (int q = 1; q < Q; ++q)
+          if (lane == (unsigned)q) gv = part[q];
+        float* row = values + (size_t)slot * row_stride;
+        float4 x = reinterpret_cast<const float4*>(row)[lane];
+        float4 a = opt == BP_OPT_ADAGRAD ? reinterpret_cast<const float4*>(row)[Q + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        x.x = upd1(x.x, a.x, gv.x, opt, lr, eps);
+        x.y = upd1(x.y, a.y, gv.y, opt, lr, eps);
+        x.z = upd1(x.z, a.z, gv.z, opt, lr, eps);
+        x.w = upd1(x.w, a.w, gv.w, opt, lr, eps);
+        reinterpret_cast<float4*>(row)[lane] = x;
+        if (opt == BP_OPT_ADAGRAD) reinterpret_cast<float4*>(row)[Q + lane] = a;
+        nz = gv.x != 0.f || gv.y != 0.f || gv.z != 0.f || gv.w != 0.f;
+      }
+      if (__ballot_sync(0xffffffffu, nz) && lane == 0) {
+        if (dirty) dirty[slot] = 1;
+        ++my_nz;
+      }
+    }
+  }
   // grid-stride over (key, column) items: the grid is sized for the
   // machine, not for the n_occ bound on U
-  unsigned long long my_nz = 0;
   for (long long base = (long long)blockIdx.x * blockDim.x; base < U * Q; base += (long long)gridDim.x * blockDim.x) {
   const long long i = base + threadIdx.x;
   const long long s = i / Q;
@@ -1732,11 +1791,12 @@ __global__ void __launch_bounds__(256) k_bwd_apply(const uint32_t* __restrict__ 
     const int32_t slot = slots_s[s];
     const uint32_t a = seg_start[s], b = seg_start[s + 1];
     float4 g = __ldcg(gsum + (size_t)s * Q + c);
-    if (slot >= 0) {
+    const uint32_t ft = a / T, lt = (b - 1) / T;
+    // a listed spanning key is done by its warp above
+    if (slot >= 0 && !(ft != lt && span_count)) {
       float* row = values + (size_t)slot * row_stride;
       float4 x = reinterpret_cast<const float4*>(row)[c];
       float4 acc = opt == BP_OPT_ADAGRAD ? reinterpret_cast<const float4*>(row)[Q + c] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const uint32_t ft = a / T, lt = (b - 1) / T;
       if (ft != lt) {  // tile partials in tile order: the key continues out of
                        // its first tile (slot 1 there) and into every later one (slot 0)
         g = __ldcg(parts + (size_t)(ft * 2 + 1) * Q + c);
@@ -2106,8 +2166,9 @@ extern "C" int64_t bp_embbag_bwd_scratch_bytes(int64_t n_occ, int32_t dim) {
   const long long rtiles = (n_occ + bp::kRedF4 / q - 1) / (bp::kRedF4 / q);
   // parts [tiles][2][q] float4 | arrival counters | gsum [n_occ][q] float4 |
   // k_bwd_reduce parts [rtiles][2][q] float4
+  // ... | spanning-key count + list of the register-resident reduce
   return (((long long)tiles * 2 * q * 16 + 255) & ~255ll) + ((tiles * 4 + 255) & ~255ll) + n_occ * q * 16 +
-         rtiles * 2 * q * 16 + 256;
+         rtiles * 2 * q * 16 + ((64 + rtiles) * 4 + 255) / 256 * 256 + 256;
 }
 
 static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, float* d_values, int32_t row_stride,
@@ -2166,20 +2227,28 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
         const int Tr = (r8 ? kRegTileF4 / 2 : kRegTileF4) / q;
         const unsigned rgrid = (unsigned)((P->n_occ + Tr - 1) / Tr);
         float4* rparts = gsum + (size_t)P->n_occ * q;
+        // spanning-key list after the k_bwd_reduce tile partials
+        const long long rtiles_max = (P->n_occ + kRedF4 / q - 1) / (kRedF4 / q);
+        unsigned* span_count = reinterpret_cast<unsigned*>(rparts + (size_t)rtiles_max * 2 * q);
+        uint32_t* span_list = span_count + 64;
+        BP_CUDA_TRY(cudaMemsetAsync(span_count, 0, sizeof(unsigned), s));
         const int agrid = grid_for(P->n_occ * q, 256, kNumSMs * 8);
 #define BP_BWD_REG(QQ)                                                                                        \
   if (r8) {                                                                                                   \
     k_bwd_reduce_reg<QQ, 16, 4><<<rgrid, 128, 0, s>>>(P->d_seg_of, (uint32_t)P->n_occ,                          \
-                                                  reinterpret_cast<const float4*>(d_grad_sorted), gsum, rparts);\
+                                                  reinterpret_cast<const float4*>(d_grad_sorted), gsum, rparts, \
+                                                  span_list, span_count);                                      \
     k_bwd_apply<QQ, kRegTileF4 / 2><<<agrid, 256, 0, s>>>(P->d_seg_start, P->d_num_unique, gsum, rparts,       \
                                                           d_values, row_stride, d_slots_s, d_dirty, opt, lr,   \
-                                                          eps, (unsigned long long*)d_stats);                  \
+                                                          eps, (unsigned long long*)d_stats, span_list,        \
+                                                          span_count);                                         \
   } else {                                                                                                    \
     k_bwd_reduce_reg<QQ><<<rgrid, 256, 0, s>>>(P->d_seg_of, (uint32_t)P->n_occ,                                 \
-                                               reinterpret_cast<const float4*>(d_grad_sorted), gsum, rparts);  \
+                                               reinterpret_cast<const float4*>(d_grad_sorted), gsum, rparts,   \
+                                               span_list, span_count);                                         \
     k_bwd_apply<QQ, kRegTileF4><<<agrid, 256, 0, s>>>(P->d_seg_start, P->d_num_unique, gsum, rparts, d_values, \
                                                       row_stride, d_slots_s, d_dirty, opt, lr, eps,            \
-                                                      (unsigned long long*)d_stats);                           \
+                                                      (unsigned long long*)d_stats, span_list, span_count);    \
   }
         switch (q) {
           case 1: BP_BWD_REG(1); break;
