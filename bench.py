@@ -674,7 +674,7 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
                         "mlp": "PyTorch, bf16 compute copy + fp32 master SGD, one CUDA graph per step (13-512-256-64-16 / 367-1024-1024-512-256-1)",
                         "embedding_optimizer": "sgd", "final_loss": losses[-1] if losses else None,
                         "embedding_stage_ms_per_step": spans[0]},
-            "roofline": {"kernel": "bp::k_embbag_fwd_rows_v4 + k_embbag_bwd_staged (EmbeddingBag fwd + sorted-gradient "
+            "roofline": {"kernel": "bp::k_embbag_fwd_rows_v4 + k_bwd_reduce_reg + k_bwd_apply (EmbeddingBag fwd + sorted-gradient "
                                    "bwd+SGD on cached rows)",
                          "bound": "hbm", "bytes_per_step": fwd_bytes + bwd_bytes(n_occ, int(u_mean)),
                          "ms_per_step": spans[0], "launches_per_step": 2, "unit": "GB/s",

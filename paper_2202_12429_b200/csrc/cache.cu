@@ -177,6 +177,53 @@ __global__ void k_apply_resolve(const uint32_t* __restrict__ ids_s, const uint64
   }
 }
 
+// k_apply_resolve of this batch and the next batch's id stamp (k_mark_ids)
+// in one launch: independent work on the same stream, one launch gap less
+// on the engine's compute stream.
+__global__ void k_apply_resolve_mark(const uint32_t* __restrict__ ids_s, const uint64_t* __restrict__ keys_s,
+                                     const uint32_t* __restrict__ perm_s2k, const int64_t* __restrict__ ttl_k,
+                                     const long long* d_U, uint64_t skip_key, int has_skip,
+                                     const int32_t* __restrict__ slot_of, long long* __restrict__ ttl,
+                                     int32_t* __restrict__ slots_s, ErrorRecord* err, long long iteration,
+                                     const uint32_t* __restrict__ next_ids, const long long* d_next_U,
+                                     int64_t* __restrict__ mark, long long tag, int64_t* zero2) {
+  if (zero2 && blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0;  // the step's stats (no memset)
+  const long long U = *d_U, NU = *d_next_U;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < U; s += stride) {
+    const uint32_t id = ids_s[s];
+    const uint64_t key = keys_s[s];
+    const long long k = perm_s2k[s];
+    const int32_t slot = id == kNoId ? -1 : slot_of[id];
+    const bool skipped = has_skip && key == skip_key;
+    if (slot < 0) {
+      raise_error(err, skipped ? BP_ERR_CACHE_MISS : BP_ERR_CACHE_ORDERING, iteration,
+                  skipped ? (k | (1ll << 40)) : k, key);
+    } else if (!skipped) {
+      ttl[slot] = ttl_k[k];
+    }
+    slots_s[s] = slot;
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < NU; i += stride) mark[next_ids[i]] = tag;
+}
+
+int apply_resolve_mark(bp_cache* c, bp_prep* P, const int64_t* d_ttl_k, uint64_t skip_key, int32_t has_skip,
+                       int32_t* d_slots_s, bp_prep* N, int64_t* d_mark, int64_t tag, int64_t* d_zero2,
+                       cudaStream_t s) {
+  if (!c->sc || !P->schema_mode || !N->schema_mode) return BP_ERR_INVALID;
+  if (P->n_occ == 0 || N->n_occ == 0) {  // the separate launches handle the empty cases
+    int rc = bp_cache_apply_resolve(c, P, d_ttl_k, skip_key, has_skip, d_slots_s, s);
+    return rc ? rc : mark_ids_zero(N, d_mark, tag, d_zero2, s);
+  }
+  const long long n = P->n_occ > N->n_occ ? P->n_occ : N->n_occ;
+  k_apply_resolve_mark<<<grid_for(n, 256), 256, 0, s>>>(
+      P->d_uniq_id_s, P->d_uniq_key_s, P->d_perm_s2k, d_ttl_k, P->d_num_unique, skip_key, has_skip, c->d_slot_of,
+      c->d_ttl, d_slots_s, c->ctx ? c->ctx->d_err : nullptr, P->iteration, N->d_uniq_id_s, N->d_num_unique, d_mark,
+      tag, d_zero2);
+  BP_LAUNCH_CHECK();
+  return BP_OK;
+}
+
 __global__ void k_gather(const float* __restrict__ values, const int32_t* __restrict__ slots, long long n,
                          const long long* d_n, int dim, float* __restrict__ out) {
   n = load_count(n, d_n);

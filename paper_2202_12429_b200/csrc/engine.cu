@@ -1001,6 +1001,17 @@ namespace bp {
 
 // Apply plan x (insert of its staged rows minus an optional dropped first
 // key), TTL updates + lookup into slots_s, and stamp the next batch's keys.
+// A cross-stream dependency the host has already seen complete needs no
+// device-side wait: everything before the event is finished and visible to
+// work enqueued after the query.  (The fetch, the next batch's prep and the
+// chunk's previous write-back normally finished steps ago.)
+static cudaError_t wait_pending(cudaStream_t s, cudaEvent_t ev) {
+  const cudaError_t q = cudaEventQuery(ev);
+  if (q == cudaSuccess) return cudaSuccess;
+  if (q != cudaErrorNotReady) return q;
+  return cudaStreamWaitEvent(s, ev, 0);
+}
+
 static int engine_apply(bp_engine* e, bp_prep* P, PlanSlot& ps, int64_t next_pos, uint64_t skip_key,
                         int32_t has_skip, bp_prep** next_out) {
   cudaStream_t s = e->compute;
@@ -1027,21 +1038,24 @@ static int engine_apply(bp_engine* e, bp_prep* P, PlanSlot& ps, int64_t next_pos
       BP_CUDA_TRY(cudaStreamWaitEvent(e->prepq, e->flush_ev, 0));
     }
   }
-  BP_CUDA_TRY(cudaStreamWaitEvent(s, ps.fetched, 0));
+  BP_CUDA_TRY(wait_pending(s, ps.fetched));
   stage_begin(e, kStageApply, s);
   const int off = has_skip ? 1 : 0;
   // insert counts[0] - off rows; the count lands in ps.n_ins for the step record
   int rc = cache_insert_sub(e->cache, ps.keys + off, ps.ids + off, ps.staging + (size_t)off * dim, ps.ttls + off,
                             e->cfg.max_occ - off, ps.counts, off, ps.n_ins, P->iteration, s);
   if (rc) return rc;
-  rc = bp_cache_apply_resolve(e->cache, P, ps.ttl_k, skip_key, has_skip, e->slots_s, s);
-  if (rc) return rc;
   bp_prep* N = next_pos >= 0 ? e->preps[engine_prep_slot(e, next_pos)] : nullptr;
   if (N) {
-    BP_CUDA_TRY(cudaStreamWaitEvent(s, e->prep_ready[engine_prep_slot(e, next_pos)], 0));
-    rc = mark_ids_zero(N, e->mark, N->iteration, e->stats, s);  // also zeroes the step stats
+    // this batch's TTL + lookup and the next batch's id stamp in one launch
+    // (it also zeroes the step stats)
+    BP_CUDA_TRY(wait_pending(s, e->prep_ready[engine_prep_slot(e, next_pos)]));
+    rc = apply_resolve_mark(e->cache, P, ps.ttl_k, skip_key, has_skip, e->slots_s, N, e->mark, N->iteration,
+                            e->stats, s);
     if (rc) return rc;
   } else {
+    rc = bp_cache_apply_resolve(e->cache, P, ps.ttl_k, skip_key, has_skip, e->slots_s, s);
+    if (rc) return rc;
     BP_CUDA_TRY(cudaMemsetAsync(e->stats, 0, 2 * sizeof(int64_t), s));
   }
   stage_end(e, kStageApply, s);
@@ -1087,7 +1101,7 @@ static int engine_finish_begin(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t c
   cudaStream_t s = e->compute;
   BP_CUDA_TRY(cudaEventRecord(ps.consumed, s));
   ChunkSlot& c = e->chunks[chunk_slot];
-  BP_CUDA_TRY(cudaStreamWaitEvent(s, c.flushed, 0));  // its previous contents are durable
+  BP_CUDA_TRY(wait_pending(s, c.flushed));  // its previous contents are durable
   bp_evict_buffers eb{e->cfg.record_keys ? c.keys : nullptr, c.ids, c.rows, c.dirty, c.count};
   stage_begin(e, kStageEvict, s);
   // The planner's key-sorted evict set is exactly {ttl <= iteration}
@@ -1109,7 +1123,7 @@ static int engine_finish_begin(bp_engine* e, bp_prep* P, PlanSlot& ps, int32_t c
   c.pending = true;
   if (drain_slot >= 0) {
     ChunkSlot& d = e->chunks[drain_slot];
-    BP_CUDA_TRY(cudaStreamWaitEvent(s, d.flushed, 0));
+    BP_CUDA_TRY(wait_pending(s, d.flushed));
     bp_evict_buffers db{e->cfg.record_keys ? d.keys : nullptr, d.ids, d.rows, d.dirty, d.count};
     rc = bp_cache_evict(e->cache, P->iteration, 1, &db, e->cfg.capacity, s);
     if (rc) return rc;

@@ -109,6 +109,9 @@ int cache_insert_sub(bp_cache* c, const uint64_t* d_keys, const uint32_t* d_ids,
                      const int64_t* d_ttls, int64_t n, const int64_t* d_n, int64_t sub, int64_t* n_out,
                      int64_t iteration, cudaStream_t s);
 int mark_ids_zero(bp_prep* P, int64_t* d_mark, int64_t tag, int64_t* d_zero2, cudaStream_t s);
+int apply_resolve_mark(bp_cache* c, bp_prep* P, const int64_t* d_ttl_k, uint64_t skip_key, int32_t has_skip,
+                       int32_t* d_slots_s, bp_prep* N, int64_t* d_mark, int64_t tag, int64_t* d_zero2,
+                       cudaStream_t s);
 
 // Green-context SM partition (green.cu): a stream of the hot (hot != 0) or
 // the rest partition, or nullptr when partitioning is off.

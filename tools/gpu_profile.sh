@@ -20,7 +20,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --n
   > "$OUT/ncu_l3.log" 2>&1
 # full captures of the roofline kernels and the prep / planner kernels
 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed_step/" \
-  -k regex:"k_embbag|k_interact" -c 6 -f -o "$OUT/full_dlrm" python tools/profile_step.py --steps 1 --nvtx \
+  -k regex:"k_embbag|k_interact|k_bwd_reduce_reg|k_bwd_apply" -c 8 -f -o "$OUT/full_dlrm" python tools/profile_step.py --steps 1 --nvtx \
   --engine-flush 0 --dlrm > "$OUT/ncu_f1.log" 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "planner_batch/" \
   -k regex:"k_col_cluster|k_first_order|k_pop_fused|k_refill" -c 4 -f -o "$OUT/full_planner" \

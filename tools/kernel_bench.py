@@ -60,7 +60,11 @@ def main():
 
     prep = make_prep()
     keep = []
-    out["prep_columnar_us"] = timed(lambda: keep.append(make_prep()), args.reps, flush)
+    # event span around the whole Python-level DevicePrep construction (host
+    # argument marshalling, arena allocation and launches included); the
+    # prep kernels' own device time is in kernels_us (k_col_cluster_prep,
+    # k_first_order) and in tools/planner_bench.py
+    out["prep_construct_span_us"] = timed(lambda: keep.append(make_prep()), args.reps, flush)
     keep.clear()
 
     u = prep.num_unique
@@ -187,7 +191,7 @@ def main():
         fwd()
         lib.bp_debug_fwd_variant(0)
 
-    for fn in (stub, fwd, fwd_sorted, bwd, bwd_sorted, variant(0), variant(1), variant(2), variant(3), variant(4), variant(5), variant(6), variant(7), variant(8), variant(9)):
+    for fn in (lambda: keep.append(make_prep()), stub, fwd, fwd_sorted, bwd, bwd_sorted, variant(0), variant(1), variant(2), variant(3), variant(4), variant(5), variant(6), variant(7), variant(8)):  # (variant 9 is the default bwd_sorted)
         flush.zero_()
         torch.cuda.synchronize()
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
