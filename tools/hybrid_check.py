@@ -60,7 +60,7 @@ def main() -> int:
     dist.all_gather_object(gathered, mine)
     ok = True
     if rank == 0:
-        want_losses, want_tables, want_model = cpu_reference(batches, model, opt_name, lr, eps, seed)
+        want_losses, want_tables, want_model, want_ill = cpu_reference(batches, model, opt_name, lr, eps, seed)
         np.testing.assert_allclose(losses.cpu().numpy(), want_losses, rtol=1e-4)
         atol = 1e-4 if opt_name == "adagrad" else 1e-6
         got = {}
@@ -68,7 +68,11 @@ def main() -> int:
             got.update(part)
         assert sorted(got) == list(range(SCHEMA.num_tables))
         for t in range(SCHEMA.num_tables):
-            np.testing.assert_allclose(got[t], want_tables[t], rtol=1e-5, atol=atol, err_msg=f"table {t}")
+            # Adagrad: components the reference stepped on a near-zero
+            # accumulated gradient are order-sensitive (test_gpu_dlrm.py)
+            well = np.ones(want_tables[t].shape, bool) if want_ill is None else ~want_ill[t]
+            np.testing.assert_allclose(got[t][well], want_tables[t][well], rtol=1e-5, atol=atol, err_msg=f"table {t}")
+            assert np.all(np.abs(got[t][~well] - want_tables[t][~well]) <= lr * len(batches) + 1e-6)
         for (name, p), (_, q) in zip(trainer.model.named_parameters(), want_model.named_parameters()):
             np.testing.assert_allclose(p.detach().cpu().numpy(), q.detach().numpy(), rtol=1e-4, atol=1e-6,
                                        err_msg=name)
