@@ -691,7 +691,8 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
                 "gather": _part("bp::k_embbag_fwd_rows_v4 (EmbeddingBag forward: gather + pooling)",
                                 fwd_bytes, fwd_span, "k_embbag_fwd_rows_v4", ktimes),
                 "scatter": _part(SCATTER_LABEL, bwd_bytes(n_occ, int(u_mean)), bwd_span,
-                                 ("k_embbag_bwd_staged", "k_bwd_reduce_reg", "k_bwd_apply"), ktimes)}}
+                                 ("k_embbag_bwd_staged", "k_bwd_reduce_reg", "k_bwd_apply"), ktimes,
+                                 traffic_names=("k_bwd_reduce_reg", "k_bwd_apply"))}}
 
 
 # the sorted-gradient backward kernels of the default variant (CUPTI times
@@ -700,7 +701,7 @@ SCATTER_LABEL = ("bp::k_embbag_bwd_staged (sorted-gradient segmented scatter-add
                  "variants 8/9: bp::k_bwd_reduce_reg + bp::k_bwd_apply")
 
 
-def _part(kernel: str, nbytes: int, span, ncu_name, ktimes: dict | None = None) -> dict:
+def _part(kernel: str, nbytes: int, span, ncu_name, ktimes: dict | None = None, traffic_names=None) -> dict:
     """One half of the EmbeddingBag pair: achieved = algorithmic bytes / the
     launch's CUDA-event span on the compute stream (the spec's measure; the
     span includes the launch gap behind the begin event), plus the CUPTI
@@ -710,7 +711,9 @@ def _part(kernel: str, nbytes: int, span, ncu_name, ktimes: dict | None = None) 
     for rnd in ("round2", "round1"):
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", rnd, "traffic.json")))["dram_bytes_per_launch"]
-            traffic = next((v for k, v in tr.items() if k.startswith(ncu_name)), None)
+            # the default launch shape's kernels (all of them, summed)
+            names = traffic_names or ncu_name
+            traffic = sum(v for k, v in tr.items() if k.startswith(names)) or None
         except (OSError, KeyError, ValueError):
             continue
         if traffic is not None:
