@@ -1573,8 +1573,12 @@ __device__ __forceinline__ void chain_step(uint32_t& ok, float4& ov, bool& first
   ov = sg.lv;
 }
 
-template <int Q, int R = 16, int NW = 8>
-__global__ void __launch_bounds__(NW * 32, (R == 16 ? 2 : 3) * 8 / NW) k_bwd_reduce_reg(
+// TMA = true (variant 10): the CTA's tile of gradient rows and segment ids
+// arrives by one bulk async copy (TMA engine, mbarrier completion) into
+// shared memory instead of per-lane loads: the bytes in flight no longer
+// cost registers, so ~6 CTAs per SM stream their tiles at once.
+template <int Q, int R = 16, int NW = 8, bool TMA = false>
+__global__ void __launch_bounds__(NW * 32, TMA ? 6 : (R == 16 ? 2 : 3) * 8 / NW) k_bwd_reduce_reg(
     const uint32_t* __restrict__ seg_of, uint32_t n, const float4* __restrict__ grad, float4* __restrict__ gsum,
     float4* __restrict__ parts, uint32_t* __restrict__ span_list, unsigned* __restrict__ span_count) {
   constexpr int G = 32 / Q, WT = G * R, T = NW * WT;
@@ -1593,7 +1597,43 @@ __global__ void __launch_bounds__(NW * 32, (R == 16 ? 2 : 3) * 8 / NW) k_bwd_red
   // the lane's 16 rows, all loads in flight together
   uint32_t sg[R];
   float4 x[R];
-  if (r0 + R <= (long long)n) {
+  if constexpr (TMA) {
+    extern __shared__ __align__(128) unsigned char rt_smem[];
+    float4* tile = reinterpret_cast<float4*>(rt_smem);            // [T][Q]
+    uint32_t* sgs = reinterpret_cast<uint32_t*>(tile + T * Q);     // [T]
+    __shared__ __align__(8) uint64_t bar;
+    const uint32_t rows = (uint32_t)(t_end - t0);
+    const uint32_t seg_bytes = (rows / 4) * 16;
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
+                   "r"(rows * Q * 16 + seg_bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(tile)),
+                   "l"(grad + t0 * Q), "r"(rows * Q * 16), "r"(smem_u32(&bar))
+                   : "memory");
+      if (seg_bytes)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(sgs)),
+                     "l"(seg_of + t0), "r"(seg_bytes), "r"(smem_u32(&bar))
+                     : "memory");
+    }
+    if (threadIdx.x < rows - seg_bytes / 4) sgs[seg_bytes / 4 + threadIdx.x] = seg_of[t0 + seg_bytes / 4 + threadIdx.x];
+    __syncthreads();  // the barrier is initialised, the tail ids are in
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT%=;\n}\n" ::"r"(
+            smem_u32(&bar))
+        : "memory");
+    const int lr0 = (int)(r0 - t0);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const bool ok = (uint32_t)(lr0 + j) < rows;
+      sg[j] = ok ? sgs[lr0 + j] : 0xFFFFFFFFu;
+      x[j] = ok ? tile[(lr0 + j) * Q + c] : zero;
+    }
+  } else if (r0 + R <= (long long)n) {
 #pragma unroll
     for (int j = 0; j < R; j += 4) {
       const uint4 q4 = *reinterpret_cast<const uint4*>(seg_of + r0 + j);
@@ -2120,7 +2160,7 @@ constexpr int kBwdDefault = 9;
 static int g_bwd_variant = kBwdDefault;
 
 extern "C" int bp_debug_bwd_variant(int32_t v) {
-  if (v < -1 || v > 9) return BP_ERR_INVALID;
+  if (v < -1 || v > 10) return BP_ERR_INVALID;
   g_bwd_variant = v < 0 ? kBwdDefault : v;
   return BP_OK;
 }
@@ -2210,7 +2250,8 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
     case 6:
     case 7:
     case 8:
-    case 9: {
+    case 9:
+    case 10: {
       const int q = dim / 4, T = kStagedF4 / 2 / q;  // scratch layout of the smallest tiles
       const unsigned tiles = (unsigned)((P->n_occ + T - 1) / T);
       const size_t parts_bytes = ((size_t)tiles * 2 * q * sizeof(float4) + 255) & ~size_t(255);
@@ -2220,11 +2261,15 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
       float4* parts = reinterpret_cast<float4*>(scratch);
       unsigned int* arrivals = reinterpret_cast<unsigned int*>(scratch + parts_bytes);
       if (!own) BP_CUDA_TRY(cudaMemsetAsync(arrivals, 0, tiles * sizeof(unsigned int), s));
-      if ((g_bwd_variant == 8 || g_bwd_variant == 9) && (reinterpret_cast<uintptr_t>(P->d_seg_of) & 15) == 0) {
+      if ((g_bwd_variant == 8 || g_bwd_variant == 9 || g_bwd_variant == 10) &&
+          (reinterpret_cast<uintptr_t>(P->d_seg_of) & 15) == 0 &&
+          (reinterpret_cast<uintptr_t>(d_grad_sorted) & 15) == 0) {
         // register-resident reduce + apply (k_bwd_reduce_reg, k_bwd_apply)
         float4* gsum = reinterpret_cast<float4*>(scratch + parts_bytes + ((tiles * sizeof(unsigned int) + 255) & ~size_t(255)));
-        const bool r8 = g_bwd_variant == 9;  // 4-warp CTAs: 2 KB tiles, more CTAs per SM
+        const bool r8 = g_bwd_variant == 9 || g_bwd_variant == 10;  // 4-warp CTAs: 2 KB tiles, more CTAs per SM
+        const bool tma = g_bwd_variant == 10;
         const int Tr = (r8 ? kRegTileF4 / 2 : kRegTileF4) / q;
+        const size_t tsmem = (size_t)Tr * q * sizeof(float4) + (size_t)Tr * sizeof(uint32_t);
         const unsigned rgrid = (unsigned)((P->n_occ + Tr - 1) / Tr);
         float4* rparts = gsum + (size_t)P->n_occ * q;
         // spanning-key list after the k_bwd_reduce tile partials
@@ -2234,7 +2279,21 @@ static int embbag_backward_sorted_impl(bp_prep* P, const float* d_grad_sorted, f
         BP_CUDA_TRY(cudaMemsetAsync(span_count, 0, sizeof(unsigned), s));
         const int agrid = grid_for(P->n_occ * q, 256, kNumSMs * 8);
 #define BP_BWD_REG(QQ)                                                                                        \
-  if (r8) {                                                                                                   \
+  if (tma) {                                                                                                  \
+    static bool attr = false;                                                                                 \
+    if (!attr) {                                                                                              \
+      BP_CUDA_TRY(cudaFuncSetAttribute(k_bwd_reduce_reg<QQ, 16, 4, true>,                                     \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));             \
+      attr = true;                                                                                            \
+    }                                                                                                         \
+    k_bwd_reduce_reg<QQ, 16, 4, true><<<rgrid, 128, tsmem, s>>>(P->d_seg_of, (uint32_t)P->n_occ,               \
+                                                  reinterpret_cast<const float4*>(d_grad_sorted), gsum, rparts, \
+                                                  span_list, span_count);                                      \
+    k_bwd_apply<QQ, kRegTileF4 / 2><<<agrid, 256, 0, s>>>(P->d_seg_start, P->d_num_unique, gsum, rparts,       \
+                                                          d_values, row_stride, d_slots_s, d_dirty, opt, lr,   \
+                                                          eps, (unsigned long long*)d_stats, span_list,        \
+                                                          span_count);                                         \
+  } else if (r8) {                                                                                            \
     k_bwd_reduce_reg<QQ, 16, 4><<<rgrid, 128, 0, s>>>(P->d_seg_of, (uint32_t)P->n_occ,                          \
                                                   reinterpret_cast<const float4*>(d_grad_sorted), gsum, rparts, \
                                                   span_list, span_count);                                      \

@@ -267,7 +267,7 @@ def test_bf16_mixed_precision_tracks_fp32():
     np.testing.assert_allclose(out["bf16"][1], out["fp32"][1], rtol=0, atol=2e-3)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10])
 @pytest.mark.parametrize("dim", [4, 8, 16, 32])
 @pytest.mark.parametrize("opt_name", ["sgd", "adagrad"])
 def test_sorted_gradient_backward(dim, opt_name, variant):
