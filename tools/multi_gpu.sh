@@ -1,3 +1,5 @@
+# N-GPU bench lines (table- and row-sharded), the reference arm and the
+# multi-GPU tests on one box:  gpurun --gpus N -- 'bash tools/multi_gpu.sh N'
 set -u
 N=$1
 mkdir -p gpurun_out/m$N
