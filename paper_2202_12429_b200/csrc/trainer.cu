@@ -571,9 +571,10 @@ static int g_fork_long = 2;
 static cudaStream_t g_long_stream = nullptr;  // engine-provided stream for the chains (green partition)
 static int g_short_ctas = 5;  // tuning knob (bp_set_stub_short_ctas): short-kernel CTAs per SM
 // threads of a long-segment CTA (bp_set_stub_long_threads): one warp runs the
-// chain, the others stage occurrence bytes; a wider CTA also leaves fewer
-// thread slots on its SM for short-kernel warps competing with the chain
-static int g_long_threads = 1024;
+// chain, the others stage occurrence bytes.  With the chains launched first
+// (fork mode 2) 128 measured best (0.1699 vs 0.171 ms/step for 1024 over 6
+// runs each, profiles/round2/stub_knobs2/)
+static int g_long_threads = 128;
 
 static int g_short_carveout = 100;  // tuning knob: shared-memory carveout (%) of the short kernel
 
