@@ -603,6 +603,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
             part.update(peak=hbm_peak, frac=part["achieved"] / hbm_peak, peak_source=peak_src,
                         frac_cupti=part["achieved_cupti"] / hbm_peak if part.get("achieved_cupti") else None)
         out["roofline_parts"] = dlrm.get("roofline_parts")
+        if dlrm.get("event_span_null_kernel_us"):
+            out["event_span_null_kernel_us"] = dlrm["event_span_null_kernel_us"]
     else:
         out["roofline"] = dict(out["roofline_stub_trainer"], bound="hbm")
     return out
@@ -656,6 +658,7 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
     # CUPTI device time of the same kernels inside 4 more steps (no event
     # brackets: the kernel alone, still beside the step's other streams)
     ktimes = kernel_times(pipe, warm + steps + 8, 4)
+    ev_over = event_overhead_us(pipe.stream, torch) if world == 1 else None
     u_mean = statistics.mean(r.critical_size + r.background_size for r in records)
     n_occ = BATCH * world * local_tables
     # "trainer" spans: the EmbeddingBag forward, "trainer_bwd": its backward
@@ -687,6 +690,9 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
             # events in the same steps
             # (N > 1: the peer-exchange variants, their spans include the
             # device-side barriers of the exchange)
+            # span of a trivial kernel between two events on the same stream
+            # (idle / busy): the part of each span above that is not kernel time
+            "event_span_null_kernel_us": ev_over,
             "roofline_parts": None if world > 1 else {
                 "gather": _part("bp::k_embbag_fwd_rows_v4 (EmbeddingBag forward: gather + pooling)",
                                 fwd_bytes, fwd_span, "k_embbag_fwd_rows_v4", ktimes),
@@ -699,6 +705,35 @@ def run_dlrm_mode(args, sc, batches, cfg, flush_buf, torch, rank=0, world=1, loc
 # of every listed kernel are summed)
 SCATTER_LABEL = ("bp::k_embbag_bwd_staged (sorted-gradient segmented scatter-add + SGD in place); "
                  "variants 8/9: bp::k_bwd_reduce_reg + bp::k_bwd_apply")
+
+
+def event_overhead_us(stream, torch) -> dict:
+    """CUDA-event span of a trivial kernel on `stream`: begin event, one
+    tiny kernel, end event, back to back from the host -- with the stream
+    idle (as at a host-paced stage start) and busy behind a 256 MiB memset
+    (the stream ahead of the host).  What a stage span adds to a kernel's
+    own duration (tools/mb/event_overhead.py)."""
+    import statistics
+
+    x = torch.zeros(1, device="cuda")
+    big = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    out = {}
+    for mode in ("idle", "busy"):
+        spans = []
+        for _ in range(30):
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                if mode == "busy":
+                    big.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                x.add_(1.0)
+                b.record(stream)
+            b.synchronize()
+            spans.append(a.elapsed_time(b) * 1e3)
+        out[mode] = round(statistics.median(spans), 2)
+    del big
+    return out
 
 
 def _part(kernel: str, nbytes: int, span, ncu_name, ktimes: dict | None = None, traffic_names=None) -> dict:
