@@ -330,9 +330,23 @@ class _Pipeline:
         if pos in self.added:
             return
         b = self.batches[pos]
-        keys, labels, _ = b.packed_occurrences()
         rb = np.ascontiguousarray(b.rank_bounds(self.T), dtype=np.int64)
         dev = self.device_inputs.get(pos) if self.device_inputs else None
+        pinned32 = b._memo.get("pinned_rows32") if dev is None else None
+        tables = b.table_ids() if b.is_columnar else None
+        if pinned32 is not None and tables is not None and len(tables) and bool(np.all(np.diff(tables) > 0)):
+            # compact columnar upload from pinned memory: u32 row ids + one
+            # label per example, expanded on the GPU
+            pr, pl = pinned32
+            t32 = np.ascontiguousarray(tables, dtype=np.int32)
+            rc = self.lib.bp_engine_add_batch_rows32(self.eng, pos, b.iteration, pr.data_ptr(), pl.data_ptr(),
+                                                     b.num_examples, len(t32), t32.ctypes.data, rb.ctypes.data,
+                                                     self.T, 1)
+            L.check(rc, "bp_engine_add_batch_rows32")
+            self._host_refs[pos] = (pr, pl)
+            self.added.add(pos)
+            return
+        keys, labels, _ = b.packed_occurrences()
         if dev is not None:
             kptr, lptr, on_host, n = L.ptr(dev[0]), L.ptr(dev[1]), 0, dev[0].numel()
         else:

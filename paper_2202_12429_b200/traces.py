@@ -204,10 +204,21 @@ class Batch:
         return f"Batch(iteration={self.iteration}, examples={self.num_examples})"
 
     def pin_memory(self) -> "Batch":
-        """Keep the packed occurrences (keys, labels) in pinned host memory, so
-        the engine DMAs them straight to the GPU (no staging copy)."""
+        """Keep the batch in pinned host memory, so the engine DMAs it straight
+        to the GPU (no staging copy): a columnar batch whose row ids fit in 32
+        bits as its row ids + per-example labels (the compact upload:
+        4 B per key + 1 B per example), any other batch as its packed
+        occurrences (keys, labels)."""
         import torch
 
+        if self._examples is None and self.rows is not None and self.rows.size and \
+                0 <= int(self.rows.min()) and int(self.rows.max()) < (1 << 32):
+            pr = torch.empty(self.rows.shape, dtype=torch.int32, pin_memory=True)
+            pr.numpy().view(np.uint32)[:] = self.rows
+            pl = torch.empty(self.labels.shape[0], dtype=torch.uint8, pin_memory=True)
+            pl.numpy()[:] = self.labels
+            self._memo["pinned_rows32"] = (pr, pl)
+            return self
         keys, labels, offsets = self.packed_occurrences()
         pk = torch.empty(keys.size, dtype=torch.uint64, pin_memory=True)
         pl = torch.empty(labels.size, dtype=torch.uint8, pin_memory=True)

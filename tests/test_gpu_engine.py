@@ -10,7 +10,7 @@ import pytest
 
 from conftest import golden, unpack
 from oracle import bagpipe_oracle as O
-from paper_2202_12429_b200.traces import Schema, ZipfSpec, batchify_columns, generate_columns
+from paper_2202_12429_b200.traces import Batch, Schema, ZipfSpec, batchify_columns, generate_columns
 
 pytestmark = pytest.mark.gpu
 
@@ -205,3 +205,21 @@ def test_threaded_mode_equals_serial(small_schema, small_batches):
     a["config"].pop("mode"), b["config"].pop("mode")
     assert a == b
     assert threaded.final_store_digest == serial.final_store_digest
+
+
+@pytest.mark.parametrize("case", ["L8_T1", "L16_T2", "L32_cap550_halving"])
+def test_pinned_host_batches_byte_identical(small_schema, case):
+    """Batches in pinned host memory reproduce the reference reports: columnar
+    batches through the compact upload (u32 row ids + one label per example,
+    expanded to packed keys on the GPU: bp_engine_add_batch_rows32),
+    object-backed ones through the pinned packed-occurrence DMA."""
+    eng = _engine()
+    blob = golden("reports_small.json")[case]
+    cfg = _cfg(blob["config"])
+    rows, labels, dense = generate_columns(ZipfSpec(small_schema, 1.05, 60 * 64, seed=7))
+    columnar = [b.pin_memory() for b in batchify_columns(rows, labels, dense, 64)]
+    assert all("pinned_rows32" in b._memo for b in columnar)
+    _assert_report(eng.run_pipeline(cfg, small_schema, columnar), blob)
+    objects = [Batch(b.iteration, list(b.examples)).pin_memory() for b in batchify_columns(rows, labels, dense, 64)]
+    assert all("pinned" in b._memo for b in objects)
+    _assert_report(eng.run_pipeline(cfg, small_schema, objects), blob)
