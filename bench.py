@@ -475,12 +475,12 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     if not args.no_e2e:
         for b in batches:
             b.pin_memory()
-        # bytes DMA'd per step: the compact columnar upload (u32 row id per
-        # key + one label per example) where the batch has one, else packed
-        # u64 keys + a label per occurrence
+        # bytes DMA'd per step: the compact columnar upload (row ids at 1, 2
+        # or 4 bytes per column + one label per example) where the batch has
+        # one, else packed u64 keys + a label per occurrence
         def _h2d(b):
-            p32 = b._memo.get("pinned_rows32")
-            return p32[0].numel() * 4 + p32[1].numel() if p32 is not None else b.packed_occurrences()[0].size * 9
+            pp = b._memo.get("pinned_planes")
+            return pp[0].numel() + pp[1].numel() if pp is not None else b.packed_occurrences()[0].size * 9
 
         e2e_h2d = int(statistics.mean(_h2d(b) for b in batches[warm:warm + steps]))
         pipe2 = _Pipeline(cfg, sc, batches, None, None)

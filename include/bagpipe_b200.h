@@ -414,13 +414,16 @@ int bp_engine_add_batch_columnar(bp_engine* engine, int64_t pos, int64_t iterati
                                  const uint8_t* labels, int64_t n_ex, int32_t n_cols, const int32_t* h_tables,
                                  const int64_t* h_rank_bounds, int32_t num_ranks, int32_t keys_on_host);
 /* Compact columnar batch entering the window (reference Batch.rows /
- * Batch.labels of a Criteo-layout batch, traces.py): row ids rows[n_ex][n_cols]
- * (u32) of the tables h_tables[n_cols] and one label per example; expanded
- * to packed keys + occurrence labels on the prep stream.  on_host: rows and
- * ex_labels are pinned host memory (DMA'd), else device memory. */
-int bp_engine_add_batch_rows32(bp_engine* e, int64_t pos, int64_t iteration, const uint32_t* rows,
+ * Batch.labels of a Criteo-layout batch, traces.py): the row ids of the
+ * tables h_tables[n_cols] as planes of u32, u16 and u8 columns (h_widths[c]
+ * = 4, 2 or 1; planes [n_ex][n_w] in that order in one buffer) and one label
+ * per example; expanded to packed keys + occurrence labels on the prep
+ * stream.  on_host: planes and ex_labels are pinned host memory (DMA'd),
+ * else device memory.  n_cols <= 64. */
+int bp_engine_add_batch_packed(bp_engine* e, int64_t pos, int64_t iteration, const void* planes,
                                const uint8_t* ex_labels, int64_t n_ex, int32_t n_cols, const int32_t* h_tables,
-                               const int64_t* h_rank_bounds, int32_t num_ranks, int32_t on_host);
+                               const int8_t* h_widths, const int64_t* h_rank_bounds, int32_t num_ranks,
+                               int32_t on_host);
 int bp_engine_prep(bp_engine* engine, int64_t pos, bp_prep** out);
 int bp_engine_release_batch(bp_engine* engine, int64_t pos);
 int bp_engine_refill(bp_engine* engine, int64_t pos);

@@ -168,7 +168,8 @@ _SIGS = {
     "bp_engine_destroy": (c_i32, [c_vp]),
     "bp_engine_parts": (c_i32, [c_vp, P(EngineParts)]),
     "bp_engine_add_batch": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32]),
-    "bp_engine_add_batch_rows32": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_i32]),
+    "bp_engine_add_batch_packed": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32,
+                                           c_i32]),
     "bp_engine_add_batch_columnar": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32,
                                              c_i32]),
     "bp_prep_create_columnar": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_i64, c_i32, c_vp,

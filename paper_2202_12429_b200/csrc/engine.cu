@@ -337,8 +337,8 @@ struct bp_engine {
   std::vector<int32_t> h_col_tables;
   uint64_t* d_keys_staging[2];
   uint8_t* d_labels_staging[2];
-  // compact columnar uploads (bp_engine_add_batch_rows32), allocated on first use
-  uint32_t* d_rows32_staging[2] = {nullptr, nullptr};
+  // compact columnar uploads (bp_engine_add_batch_packed), allocated on first use
+  uint32_t* d_planes_staging[2] = {nullptr, nullptr};  // row-id planes (u32 | u16 | u8)
   uint8_t* d_exlab_staging[2] = {nullptr, nullptr};
   cudaEvent_t staging_free[2];
   cudaEvent_t join_ev[3];  // bp_engine_join: planq, link, prepq
@@ -611,7 +611,7 @@ extern "C" int bp_engine_destroy(bp_engine* e) {
   for (int i = 0; i < 2; ++i) {
     cudaFree(e->d_keys_staging[i]);
     cudaFree(e->d_labels_staging[i]);
-    if (e->d_rows32_staging[i]) cudaFree(e->d_rows32_staging[i]);
+    if (e->d_planes_staging[i]) cudaFree(e->d_planes_staging[i]);
     if (e->d_exlab_staging[i]) cudaFree(e->d_exlab_staging[i]);
     cudaEventDestroy(e->staging_free[i]);
     cudaEventDestroy(e->join_ev[i]);
@@ -749,58 +749,77 @@ static int engine_add(bp_engine* e, int64_t pos, int64_t iteration, const uint64
 }
 
 namespace bp {
+// Column map of a packed columnar upload: table id and (plane, index) of
+// every column (plane 0: u32 rows, 1: u16, 2: u8).
+struct PackedCols {
+  int32_t table[64];
+  int32_t where[64];  // plane << 16 | index within the plane
+  int32_t n[3];       // columns per plane
+};
+
 // Packed keys (table << 44 | row) and per-occurrence labels of a columnar
-// batch from its row ids [n_ex][n_cols] and per-example labels.
-__global__ void k_expand_rows32(const uint32_t* __restrict__ rows, const uint8_t* __restrict__ ex_labels,
-                                long long n_ex, int n_cols, const int32_t* __restrict__ col_tables,
-                                uint64_t* __restrict__ keys, uint8_t* __restrict__ labels) {
+// batch from its row-id planes and per-example labels.
+__global__ void k_expand_packed(const uint8_t* __restrict__ planes, long long n_ex, int n_cols, PackedCols m,
+                                const uint8_t* __restrict__ ex_labels, uint64_t* __restrict__ keys,
+                                uint8_t* __restrict__ labels) {
+  const uint32_t* r32 = reinterpret_cast<const uint32_t*>(planes);
+  const uint16_t* r16 = reinterpret_cast<const uint16_t*>(planes + (size_t)n_ex * m.n[0] * 4);
+  const uint8_t* r8 = planes + (size_t)n_ex * (m.n[0] * 4 + m.n[1] * 2);
   const long long n = n_ex * n_cols;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long ex = i / n_cols;
     const int c = (int)(i - ex * n_cols);
-    keys[i] = ((uint64_t)(uint32_t)col_tables[c] << kKeyTableShift) | (uint64_t)rows[i];
+    const int w = m.where[c], plane = w >> 16, j = w & 0xFFFF;
+    const uint32_t row = plane == 0 ? r32[ex * m.n[0] + j] : plane == 1 ? (uint32_t)r16[ex * m.n[1] + j]
+                                                                        : (uint32_t)r8[ex * m.n[2] + j];
+    keys[i] = ((uint64_t)(uint32_t)m.table[c] << kKeyTableShift) | (uint64_t)row;
     labels[i] = ex_labels[ex];
   }
 }
 }  // namespace bp
 
-// Compact columnar upload: row ids (u32) and one label per example instead
-// of packed u64 keys and a label per occurrence (a CK batch: 1.72 MB over the
-// link instead of 3.83 MB); expanded on the prep stream, then the columnar
-// prep.  rows / ex_labels: pinned host (DMA'd) or device memory.
-extern "C" int bp_engine_add_batch_rows32(bp_engine* e, int64_t pos, int64_t iteration, const uint32_t* rows,
+// Compact columnar upload (reference Batch.rows / Batch.labels of a
+// Criteo-layout batch, traces.py): the row ids as planes of u32, u16 and u8
+// columns ([n_ex][n] each, in that order, one buffer) and one label per
+// example -- a CK batch is 1.0 MB over the link instead of 3.83 MB of packed
+// u64 keys + per-occurrence labels -- expanded to packed keys + occurrence
+// labels by one kernel on the prep stream, then the columnar prep.
+// planes / ex_labels: pinned host memory (DMA'd) or device memory.
+extern "C" int bp_engine_add_batch_packed(bp_engine* e, int64_t pos, int64_t iteration, const void* planes,
                                           const uint8_t* ex_labels, int64_t n_ex, int32_t n_cols,
-                                          const int32_t* h_tables, const int64_t* h_rank_bounds, int32_t num_ranks,
-                                          int32_t on_host) {
+                                          const int32_t* h_tables, const int8_t* h_widths,
+                                          const int64_t* h_rank_bounds, int32_t num_ranks, int32_t on_host) {
   using namespace bp;
   const long long n_occ = n_ex * n_cols;
-  if (n_occ > e->cfg.max_occ || n_cols < 1 || n_cols > e->sc->num_tables) return BP_ERR_INVALID;
+  if (n_occ > e->cfg.max_occ || n_cols < 1 || n_cols > e->sc->num_tables || n_cols > 64) return BP_ERR_INVALID;
+  PackedCols m{};
+  for (int c = 0; c < n_cols; ++c) {
+    const int plane = h_widths[c] == 4 ? 0 : h_widths[c] == 2 ? 1 : h_widths[c] == 1 ? 2 : -1;
+    if (plane < 0) return BP_ERR_INVALID;
+    m.table[c] = h_tables[c];
+    m.where[c] = (plane << 16) | m.n[plane]++;
+  }
+  const size_t plane_bytes = (size_t)n_ex * (m.n[0] * 4 + m.n[1] * 2 + m.n[2]);
   cudaStream_t q = e->prepq;
   const int si = e->staging_i;
   e->staging_i ^= 1;
   BP_CUDA_TRY(cudaStreamWaitEvent(q, e->staging_free[si], 0));
-  if ((int)e->h_col_tables.size() != n_cols ||
-      std::memcmp(e->h_col_tables.data(), h_tables, n_cols * sizeof(int32_t)) != 0) {
-    e->h_col_tables.assign(h_tables, h_tables + n_cols);
-    BP_CUDA_TRY(cudaStreamSynchronize(q));  // previous preps may still read the old ids
-    BP_CUDA_TRY(cudaMemcpy(e->d_col_tables, h_tables, n_cols * sizeof(int32_t), cudaMemcpyHostToDevice));
-  }
-  const uint32_t* d_rows = rows;
+  const uint8_t* d_planes = static_cast<const uint8_t*>(planes);
   const uint8_t* d_lab = ex_labels;
   if (on_host) {
-    if (!e->d_rows32_staging[si]) {
+    if (!e->d_planes_staging[si]) {
       BP_CUDA_TRY(cudaStreamSynchronize(q));
-      BP_CUDA_TRY(cudaMalloc(&e->d_rows32_staging[si], (size_t)e->cfg.max_occ * sizeof(uint32_t)));
+      BP_CUDA_TRY(cudaMalloc(&e->d_planes_staging[si], (size_t)e->cfg.max_occ * sizeof(uint32_t)));
       BP_CUDA_TRY(cudaMalloc(&e->d_exlab_staging[si], (size_t)e->cfg.max_occ + 16));
     }
-    BP_CUDA_TRY(cudaMemcpyAsync(e->d_rows32_staging[si], rows, n_occ * sizeof(uint32_t), cudaMemcpyHostToDevice, q));
+    BP_CUDA_TRY(cudaMemcpyAsync(e->d_planes_staging[si], planes, plane_bytes, cudaMemcpyHostToDevice, q));
     BP_CUDA_TRY(cudaMemcpyAsync(e->d_exlab_staging[si], ex_labels, n_ex, cudaMemcpyHostToDevice, q));
-    d_rows = e->d_rows32_staging[si];
+    d_planes = reinterpret_cast<const uint8_t*>(e->d_planes_staging[si]);
     d_lab = e->d_exlab_staging[si];
   }
   if (n_occ > 0) {
-    k_expand_rows32<<<grid_for(n_occ, 256), 256, 0, q>>>(d_rows, d_lab, n_ex, n_cols, e->d_col_tables,
-                                                         e->d_keys_staging[si], e->d_labels_staging[si]);
+    k_expand_packed<<<grid_for(n_occ, 256), 256, 0, q>>>(d_planes, n_ex, n_cols, m, d_lab, e->d_keys_staging[si],
+                                                         e->d_labels_staging[si]);
     BP_LAUNCH_CHECK();
   }
   const int rc = engine_add(e, pos, iteration, e->d_keys_staging[si], e->d_labels_staging[si], n_occ, n_ex, n_cols,

@@ -281,7 +281,7 @@ class _Pipeline:
         # training thread -- so by default only with device inputs)
         # batches in pinned memory are DMA'd straight from there (no upload
         # copy on a host thread), so they take the planner thread as well --
-        # except the compact columnar uploads ("pinned_rows32"), measured
+        # except the compact columnar uploads ("pinned_planes"), measured
         # faster and steadier single-threaded (e2e 85.6-87.3M vs 70.2-85.8M)
         default_threaded = bool(self.device_inputs) or (
             bool(batches) and all("pinned" in getattr(b, "_memo", {}) for b in batches))
@@ -334,18 +334,20 @@ class _Pipeline:
         b = self.batches[pos]
         rb = np.ascontiguousarray(b.rank_bounds(self.T), dtype=np.int64)
         dev = self.device_inputs.get(pos) if self.device_inputs else None
-        pinned32 = b._memo.get("pinned_rows32") if dev is None else None
+        packed = b._memo.get("pinned_planes") if dev is None else None
         tables = b.table_ids() if b.is_columnar else None
-        if pinned32 is not None and tables is not None and len(tables) and bool(np.all(np.diff(tables) > 0)):
-            # compact columnar upload from pinned memory: u32 row ids + one
-            # label per example, expanded on the GPU
-            pr, pl = pinned32
+        if packed is not None and tables is not None and 0 < len(tables) <= 64 and \
+                bool(np.all(np.diff(tables) > 0)):
+            # compact columnar upload from pinned memory: row-id planes of
+            # 4/2/1-byte columns + one label per example, expanded on the GPU
+            buf, pl, widths = packed
             t32 = np.ascontiguousarray(tables, dtype=np.int32)
-            rc = self.lib.bp_engine_add_batch_rows32(self.eng, pos, b.iteration, pr.data_ptr(), pl.data_ptr(),
-                                                     b.num_examples, len(t32), t32.ctypes.data, rb.ctypes.data,
-                                                     self.T, 1)
-            L.check(rc, "bp_engine_add_batch_rows32")
-            self._host_refs[pos] = (pr, pl)
+            w8 = np.ascontiguousarray(widths, dtype=np.int8)
+            rc = self.lib.bp_engine_add_batch_packed(self.eng, pos, b.iteration, buf.data_ptr(), pl.data_ptr(),
+                                                     b.num_examples, len(t32), t32.ctypes.data, w8.ctypes.data,
+                                                     rb.ctypes.data, self.T, 1)
+            L.check(rc, "bp_engine_add_batch_packed")
+            self._host_refs[pos] = (buf, pl)
             self.added.add(pos)
             return
         keys, labels, _ = b.packed_occurrences()

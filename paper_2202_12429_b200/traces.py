@@ -206,18 +206,29 @@ class Batch:
     def pin_memory(self) -> "Batch":
         """Keep the batch in pinned host memory, so the engine DMAs it straight
         to the GPU (no staging copy): a columnar batch whose row ids fit in 32
-        bits as its row ids + per-example labels (the compact upload:
-        4 B per key + 1 B per example), any other batch as its packed
+        bits as its row ids, each column at 1, 2 or 4 bytes, + per-example
+        labels (the compact upload), any other batch as its packed
         occurrences (keys, labels)."""
         import torch
 
         if self._examples is None and self.rows is not None and self.rows.size and \
                 0 <= int(self.rows.min()) and int(self.rows.max()) < (1 << 32):
-            pr = torch.empty(self.rows.shape, dtype=torch.int32, pin_memory=True)
-            pr.numpy().view(np.uint32)[:] = self.rows
-            pl = torch.empty(self.labels.shape[0], dtype=torch.uint8, pin_memory=True)
+            # each column at the narrowest width its row ids fit (u32 / u16 /
+            # u8), the planes in that order in one pinned buffer
+            mx = self.rows.max(axis=0)
+            widths = np.where(mx < (1 << 8), 1, np.where(mx < (1 << 16), 2, 4)).astype(np.int8)
+            n = self.rows.shape[0]
+            planes = [np.ascontiguousarray(self.rows[:, widths == w], dtype=dt)
+                      for w, dt in ((4, np.uint32), (2, np.uint16), (1, np.uint8))]
+            nbytes = sum(p.nbytes for p in planes)
+            buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+            off = 0
+            for p in planes:
+                buf.numpy()[off:off + p.nbytes] = p.reshape(-1).view(np.uint8)
+                off += p.nbytes
+            pl = torch.empty(n, dtype=torch.uint8, pin_memory=True)
             pl.numpy()[:] = self.labels
-            self._memo["pinned_rows32"] = (pr, pl)
+            self._memo["pinned_planes"] = (buf, pl, widths)
             return self
         keys, labels, offsets = self.packed_occurrences()
         pk = torch.empty(keys.size, dtype=torch.uint64, pin_memory=True)

@@ -210,16 +210,33 @@ def test_threaded_mode_equals_serial(small_schema, small_batches):
 @pytest.mark.parametrize("case", ["L8_T1", "L16_T2", "L32_cap550_halving"])
 def test_pinned_host_batches_byte_identical(small_schema, case):
     """Batches in pinned host memory reproduce the reference reports: columnar
-    batches through the compact upload (u32 row ids + one label per example,
-    expanded to packed keys on the GPU: bp_engine_add_batch_rows32),
+    batches through the compact upload (row-id planes of 4/2/1-byte columns
+    + one label per example, expanded to packed keys on the GPU:
+    bp_engine_add_batch_packed),
     object-backed ones through the pinned packed-occurrence DMA."""
     eng = _engine()
     blob = golden("reports_small.json")[case]
     cfg = _cfg(blob["config"])
     rows, labels, dense = generate_columns(ZipfSpec(small_schema, 1.05, 60 * 64, seed=7))
     columnar = [b.pin_memory() for b in batchify_columns(rows, labels, dense, 64)]
-    assert all("pinned_rows32" in b._memo for b in columnar)
+    assert all("pinned_planes" in b._memo for b in columnar)
     _assert_report(eng.run_pipeline(cfg, small_schema, columnar), blob)
     objects = [Batch(b.iteration, list(b.examples)).pin_memory() for b in batchify_columns(rows, labels, dense, 64)]
     assert all("pinned" in b._memo for b in objects)
     _assert_report(eng.run_pipeline(cfg, small_schema, objects), blob)
+
+
+def test_pinned_planes_all_widths_equal_plain_run():
+    """The compact upload with u8, u16 and u32 columns (tables of 200, 3,000
+    and 100,000 rows): the same report bytes and store digest as the same
+    batches uploaded as packed keys."""
+    eng = _engine()
+    schema = Schema(3, (200, 3000, 100000), 2, 8)
+    rows, labels, dense = generate_columns(ZipfSpec(schema, 1.05, 40 * 256, seed=5))
+    cfg = eng.EngineConfig(cache_capacity=2000, batch_size=256, lookahead=4, num_shards=1, seed=3)
+    plain = eng.run_pipeline(cfg, schema, batchify_columns(rows, labels, dense, 256))
+    pinned = [b.pin_memory() for b in batchify_columns(rows, labels, dense, 256)]
+    assert sorted(set(int(w) for b in pinned for w in b._memo["pinned_planes"][2])) == [1, 2, 4]
+    rep = eng.run_pipeline(cfg, schema, pinned)
+    assert rep.to_json_bytes() == plain.to_json_bytes()
+    assert rep.final_store_digest == plain.final_store_digest
