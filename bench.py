@@ -134,6 +134,34 @@ def make_batches(n_batches: int, seed: int, batch: int = BATCH):
     return batchify_columns(rows, labels, dense, batch)
 
 
+def make_batches_shared(n_batches: int, seed: int, batch: int, rank: int, world: int):
+    """make_batches, generated once per box at N > 1: rank 0 writes the trace
+    columns to /dev/shm, the other ranks map them (instead of N processes
+    each drawing the whole global trace on the same host cores)."""
+    if world == 1:
+        return make_batches(n_batches, seed, batch)
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_2202_12429_b200.traces import ZipfSpec, batchify_columns, generate_columns
+
+    tag = f"/dev/shm/bp_bench_{os.environ.get('MASTER_PORT', '0')}_{seed}_{n_batches}_{batch}"
+    names = ("rows", "labels", "dense")
+    if rank == 0:
+        cols = generate_columns(ZipfSpec(schema(), ZIPF, n_batches * batch, seed))
+        for name, arr in zip(names, cols):
+            np.save(f"{tag}_{name}.npy", arr)
+    dist.barrier()
+    if rank != 0:
+        cols = tuple(np.load(f"{tag}_{name}.npy", mmap_mode="r") for name in names)
+    dist.barrier()  # every rank mapped the files: they can go (the mappings stay)
+    if rank == 0:
+        for name in names:
+            os.unlink(f"{tag}_{name}.npy")
+    rows, labels, dense = cols
+    return batchify_columns(rows, labels, dense, batch)
+
+
 def bench_config(world: int) -> dict:
     """The workload of one bench line, identical in both arms (ours and
     --impl reference) for the same N."""
@@ -390,7 +418,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     # N x 16,384 x 26/N = the same 425,984 occurrences per step as one GPU --
     # with no data-path collective, and the same per-GPU HBM cache budget.
     gbatch = BATCH * world
-    full = make_batches(n_batches, args.seed, gbatch)
+    full = make_batches_shared(n_batches, args.seed, gbatch, rank, world)
     # tables dealt by their cost (occurrences + unique keys of the first
     # batch), largest first to the least-loaded rank
     shards = table_shards(sc.num_tables, world, table_costs(full[0])) if world > 1 else [list(range(sc.num_tables))]
