@@ -350,6 +350,9 @@ int bp_set_stub_long_smem(int32_t bytes);
 int bp_set_green_sms(int32_t sms);
 /* {hot-partition SMs, rest SMs} of the partition in use ({0, 0} when off). */
 int bp_green_info(int32_t* out2);
+/* With a green partition (bp_set_green_sms): 1 = its small part runs the
+ * engine's host-link streams instead of the hot-key chains. */
+int bp_set_green_link(int32_t on);
 /* Trainer stub stream layout: 0 = one stream; 1 = hot-key chains on a side
  * stream; 2 (default) = chains first on the caller's stream, short kernel on
  * the side stream. */

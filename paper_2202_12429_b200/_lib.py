@@ -212,6 +212,7 @@ _SIGS = {
     "bp_set_write_blocks": (c_i32, [c_i32]),
     "bp_set_stub_fork": (c_i32, [c_i32]),
     "bp_set_split_writeback": (c_i32, [c_i32]),
+    "bp_set_green_link": (c_i32, [c_i32]),
     "bp_set_stub_short_ctas": (c_i32, [c_i32]),
     "bp_set_stub_carveout": (c_i32, [c_i32]),
     "bp_set_stub_long_threads": (c_i32, [c_i32]),
@@ -311,6 +312,9 @@ def lib() -> C.CDLL:
                 psr = os.environ.get("BAGPIPE_B200_PEER_SORTED")  # 0: reduce-by-key peer backward
                 if psr:
                     check(lb.bp_set_peer_sorted(int(psr)), "bp_set_peer_sorted")
+                gl = os.environ.get("BAGPIPE_B200_GREEN_LINK")  # the green partition's small part: link streams
+                if gl:
+                    check(lb.bp_set_green_link(int(gl)), "bp_set_green_link")
                 gr = os.environ.get("BAGPIPE_B200_GREEN_SMS")  # tuning knob: SMs of the hot-key partition
                 if gr:
                     check(lb.bp_set_green_sms(int(gr)), "bp_set_green_sms")

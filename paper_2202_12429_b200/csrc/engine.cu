@@ -442,7 +442,15 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
     int grc = green_stream(0, hi, &gs);
     if (grc) return grc;
   }
-  if (gs) {
+  if (gs && green_link_mode()) {
+    // the small partition runs the host-link streams, everything else the rest
+    e->compute = gs;
+    int grc = green_stream(1, lo, &e->link);
+    if (!grc) grc = green_stream(1, lo, &e->wb);
+    if (!grc) grc = green_stream(0, hi < lo ? hi + 1 : hi, &e->planq);
+    if (!grc) grc = green_stream(0, hi < lo ? hi + 1 : hi, &e->prepq);
+    if (grc) return grc;
+  } else if (gs) {
     e->compute = gs;
     int grc = green_stream(0, lo, &e->link);
     if (!grc) grc = green_stream(0, lo, &e->wb);

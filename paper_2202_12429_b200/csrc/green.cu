@@ -51,6 +51,10 @@ struct GreenPartition {
 
 static GreenPartition g_green;
 static int g_green_sms = 0;  // bp_set_green_sms: SMs of the hot partition (0 = off)
+// bp_set_green_link: 1 = the small partition runs the host-link streams
+// (zero-copy prefetch, write-back) instead of the hot-key chains, so the
+// SMs whose load queues fill with microsecond host reads run nothing else
+static int g_green_link = 0;
 
 #define BP_CU_TRY(expr)                                        \
   do {                                                         \
@@ -98,7 +102,14 @@ int green_stream(int hot, int priority, cudaStream_t* out) {
   return BP_OK;
 }
 
+bool green_link_mode() { return g_green_link != 0; }
+
 }  // namespace bp
+
+extern "C" int bp_set_green_link(int32_t on) {
+  bp::g_green_link = on != 0;
+  return BP_OK;
+}
 
 // Tuning: SMs of the hot-key partition (0 = off, the default; on B200 a
 // multiple of 8).  Takes effect for engines created afterwards.

@@ -550,8 +550,15 @@ struct SideStream {
   size_t parts_cap = 0;
   SideStream() {
     int lo = 0, hi = 0;
+    cudaStream_t gs = nullptr;
+    // with the host-link green partition the side stream stays out of it
+    if (bp::green_link_mode() && bp::green_stream(0, 0, &gs) == BP_OK && gs) {
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStreamDestroy(gs);
+      if (bp::green_stream(0, hi, &gs) == BP_OK && gs) s = gs;
+    }
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        (!s && cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi) != cudaSuccess) ||
         cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess)
       s = nullptr;
