@@ -280,11 +280,12 @@ class _Pipeline:
         # and slows host batches, whose uploads then contend with the
         # training thread -- so by default only with device inputs)
         # batches in pinned memory are DMA'd straight from there (no upload
-        # copy on a host thread), so they take the planner thread as well --
-        # except the compact columnar uploads ("pinned_planes"), measured
-        # faster and steadier single-threaded (e2e 85.6-87.3M vs 70.2-85.8M)
+        # copy on a host thread), so they take the planner thread as well
+        # (compact columnar uploads: e2e 87.4-90.6M vs 84.4-88.3M
+        # single-threaded over 5 runs each)
         default_threaded = bool(self.device_inputs) or (
-            bool(batches) and all("pinned" in getattr(b, "_memo", {}) for b in batches))
+            bool(batches) and all("pinned" in getattr(b, "_memo", {}) or "pinned_planes" in getattr(b, "_memo", {})
+                                  for b in batches))
         env = os.environ.get("BAGPIPE_B200_PLANNER_THREAD")
         if env is not None:
             default_threaded = env == "1"
