@@ -1,9 +1,9 @@
-// Optional SM partition of the engine with green contexts (CUDA driver API):
-// a "hot" partition of a few SMs runs the stub trainer's hot-key chains
-// (k_stub_step_long, sequential per-key f32 adds) and every other engine
-// stream lives in the complementary partition, so the chains never share an
-// SM with the short-segment kernel (measured in the step: the two kernels
-// slowed each other from 47 + 25 us isolated to ~55 us side by side).
+// SM partition of the engine with green contexts (CUDA driver API): a small
+// partition of a few SMs runs either the engine's host-link streams (the
+// default: the zero-copy prefetch fills its SMs' load queues with
+// microsecond host reads, which slowed every kernel sharing those SMs) or
+// the stub trainer's hot-key chains (measured slower, off), and every other
+// engine stream lives in the complementary partition.
 // Memory is the device's: green contexts partition SMs only.  The driver
 // entry points are fetched through the runtime (cudaGetDriverEntryPoint), so
 // the library does not link libcuda and still loads on a machine without a
@@ -50,11 +50,15 @@ struct GreenPartition {
 };
 
 static GreenPartition g_green;
-static int g_green_sms = 0;  // bp_set_green_sms: SMs of the hot partition (0 = off)
+// bp_set_green_sms: SMs of the small partition (0 = off).  Default: 4 SMs
+// for the engine's host-link streams (bp_set_green_link), measured on the CK
+// step with the planner thread: value 99.0-100.6M vs 89.3-97.1M samples/s,
+// e2e 92.5-95.3M vs 82.0-89.8M (profiles/round2/green_link_threaded/)
+static int g_green_sms = 4;
 // bp_set_green_link: 1 = the small partition runs the host-link streams
 // (zero-copy prefetch, write-back) instead of the hot-key chains, so the
 // SMs whose load queues fill with microsecond host reads run nothing else
-static int g_green_link = 0;
+static int g_green_link = 1;
 
 #define BP_CU_TRY(expr)                                        \
   do {                                                         \
@@ -111,8 +115,8 @@ extern "C" int bp_set_green_link(int32_t on) {
   return BP_OK;
 }
 
-// Tuning: SMs of the hot-key partition (0 = off, the default; on B200 a
-// multiple of 8).  Takes effect for engines created afterwards.
+// Tuning: SMs of the small partition (0 = off; default 4, for the host-link
+// streams).  Takes effect for engines created afterwards.
 extern "C" int bp_set_green_sms(int32_t sms) {
   if (sms < 0) return BP_ERR_INVALID;
   bp::g_green_sms = sms;
