@@ -406,6 +406,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     from paper_2202_12429_b200.engine import EngineConfig, _Pipeline
     from paper_2202_12429_b200.shard import shard_batches, table_costs, table_shards
 
+    if world > 1:
+        # the host-link green partition (on by default) measured 4 % slower
+        # at N=4 (tables per rank: the generic chunked prep keeps the SMs
+        # busier) and equal at N=2, +5 % at N=1: the N>1 lines run without
+        os.environ.setdefault("BAGPIPE_B200_GREEN_SMS", "0")
     L.lib()
     sc = schema()
     cap = sc.total_rows // 100
