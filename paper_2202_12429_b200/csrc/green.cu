@@ -98,8 +98,13 @@ static int green_init() {
 // when partitioning is off.
 int green_stream(int hot, int priority, cudaStream_t* out) {
   *out = nullptr;
-  const int rc = green_init();
-  if (rc || !g_green.hot) return rc;
+  if (green_init() != BP_OK || !g_green.rest) {
+    // the partition is a performance feature: without green-context support
+    // the engine runs unpartitioned
+    g_green = GreenPartition{};
+    g_green_sms = 0;
+    return BP_OK;
+  }
   CUstream s;
   BP_CU_TRY(g_api.greenStream(&s, hot ? g_green.hot : g_green.rest, CU_STREAM_NON_BLOCKING, priority));
   *out = (cudaStream_t)s;
