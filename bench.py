@@ -147,17 +147,29 @@ def make_batches_shared(n_batches: int, seed: int, batch: int, rank: int, world:
 
     tag = f"/dev/shm/bp_bench_{os.environ.get('MASTER_PORT', '0')}_{seed}_{n_batches}_{batch}"
     names = ("rows", "labels", "dense")
+    ok = [True]
     if rank == 0:
         cols = generate_columns(ZipfSpec(schema(), ZIPF, n_batches * batch, seed))
-        for name, arr in zip(names, cols):
-            np.save(f"{tag}_{name}.npy", arr)
-    dist.barrier()
-    if rank != 0:
-        cols = tuple(np.load(f"{tag}_{name}.npy", mmap_mode="r") for name in names)
-    dist.barrier()  # every rank mapped the files: they can go (the mappings stay)
-    if rank == 0:
-        for name in names:
-            os.unlink(f"{tag}_{name}.npy")
+        try:
+            for name, arr in zip(names, cols):
+                np.save(f"{tag}_{name}.npy", arr)
+        except OSError:  # /dev/shm too small: every rank draws the trace itself
+            ok[0] = False
+    dist.broadcast_object_list(ok, src=0)
+    if not ok[0]:
+        if rank == 0:
+            for name in names:
+                if os.path.exists(f"{tag}_{name}.npy"):
+                    os.unlink(f"{tag}_{name}.npy")
+        else:
+            cols = generate_columns(ZipfSpec(schema(), ZIPF, n_batches * batch, seed))
+    else:
+        if rank != 0:
+            cols = tuple(np.load(f"{tag}_{name}.npy", mmap_mode="r") for name in names)
+        dist.barrier()  # every rank mapped the files: they can go (the mappings stay)
+        if rank == 0:
+            for name in names:
+                os.unlink(f"{tag}_{name}.npy")
     rows, labels, dense = cols
     return batchify_columns(rows, labels, dense, batch)
 
