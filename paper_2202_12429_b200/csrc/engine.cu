@@ -438,6 +438,7 @@ extern "C" int bp_engine_create(bp_ctx* ctx, const bp_schema* sc, const bp_engin
   // With a green-context SM partition (bp_set_green_sms) every engine stream
   // lives in the rest partition and the hot-key chains get the hot one.
   cudaStream_t gs = nullptr;
+  green_auto(cfg->dim);  // the partition's size by the row width (unless set)
   {
     int grc = green_stream(0, hi, &gs);
     if (grc) return grc;

@@ -54,7 +54,11 @@ static GreenPartition g_green;
 // for the engine's host-link streams (bp_set_green_link), measured on the CK
 // step with the planner thread: value 99.0-100.6M vs 89.3-97.1M samples/s,
 // e2e 92.5-95.3M vs 82.0-89.8M (profiles/round2/green_link_threaded/)
-static int g_green_sms = 4;
+// -1 (default) = auto at the first engine: 4 SMs per 16 row components
+// (the host-link bytes per row), at most 16 -- CK / Avazu (D=16) 4 SMs,
+// Terabyte (D=64) 16 (measured there: 71.1M samples/s with 16 SMs, 63.2M
+// with 4, 64.9M unpartitioned; profiles/round2/green_link_tb10/)
+static int g_green_sms = -1;
 // bp_set_green_link: 1 = the small partition runs the host-link streams
 // (zero-copy prefetch, write-back) instead of the hot-key chains, so the
 // SMs whose load queues fill with microsecond host reads run nothing else
@@ -113,6 +117,13 @@ int green_stream(int hot, int priority, cudaStream_t* out) {
 
 bool green_link_mode() { return g_green_link != 0; }
 
+void green_auto(int dim) {
+  if (g_green_sms < 0) {
+    const int s = 4 * ((dim + 15) / 16);
+    g_green_sms = s < 4 ? 4 : (s > 16 ? 16 : s);
+  }
+}
+
 }  // namespace bp
 
 extern "C" int bp_set_green_link(int32_t on) {
@@ -120,10 +131,11 @@ extern "C" int bp_set_green_link(int32_t on) {
   return BP_OK;
 }
 
-// Tuning: SMs of the small partition (0 = off; default 4, for the host-link
-// streams).  Takes effect for engines created afterwards.
+// Tuning: SMs of the small partition (0 = off; -1 = auto by the row width,
+// the default).  Takes effect for engines created afterwards (the partition
+// is made once per process).
 extern "C" int bp_set_green_sms(int32_t sms) {
-  if (sms < 0) return BP_ERR_INVALID;
+  if (sms < -1) return BP_ERR_INVALID;
   bp::g_green_sms = sms;
   return BP_OK;
 }

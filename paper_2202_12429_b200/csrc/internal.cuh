@@ -117,6 +117,7 @@ int apply_resolve_mark(bp_cache* c, bp_prep* P, const int64_t* d_ttl_k, uint64_t
 // the rest partition, or nullptr when partitioning is off.
 int green_stream(int hot, int priority, cudaStream_t* out);
 bool green_link_mode();
+void green_auto(int dim);
 // The stub trainer's hot-key chains go to this stream when set (trainer.cu).
 void set_long_stream(cudaStream_t s);
 int store_log_append_fenced(bp_store* st, const uint32_t* d_ids, const float* d_rows, const uint8_t* d_dirty,
