@@ -510,6 +510,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     link_rows = np.zeros(2, dtype=np.int64)  # lazy prefetch over the run: host-link reads, GPU-computed inits
     pipe.lib.bp_store_link_counters(pipe.store.handle, link_rows.ctypes.data)
     host_frac = float(link_rows[0]) / max(int(link_rows.sum()), 1)
+    green = np.zeros(2, dtype=np.int32)  # the host-link SM partition the driver made
+    pipe.lib.bp_green_info(green.ctypes.data)
     pipe.close()
     del pipe
 
@@ -635,7 +637,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                       "prefetch_note": "rows never written back are computed on the GPU (functional init, "
                                        "store.py:106-129); only written rows are read over the host link",
                       "peak_note": "pinned memcpy 55.5 GB/s H2D, 56.5 D2H; zero-copy random 64 B rows 18.7-25 GB/s "
-                                   "(tools/hostlink_peak.py)"},
+                                   "(tools/hostlink_peak.py)",
+                      "green_partition_sms": {"link": int(green[0]), "rest": int(green[1])}},
         "trace_ingest": ingest,
         "gpu_launches": launches_per_step * steps,
         "clocks": clk,

@@ -345,10 +345,11 @@ int bp_set_stub_long_threads(int32_t threads);
  * CTAs): bytes, default 120 KB. */
 int bp_set_stub_long_smem(int32_t bytes);
 /* Tuning: green-context SM partition of engines created afterwards: its
- * small part of `sms` SMs runs the host-link streams (bp_set_green_link 1,
- * the default) or the stub trainer's hot-key chains (0), every other engine
- * stream the rest.  0 = off; -1 (default) = 4 SMs per 16 row components, at
- * most 16. */
+ * small part of `sms` SMs (rounded up by the driver to its split
+ * granularity, 8 on B200; bp_green_info reports the result) runs the
+ * host-link streams (bp_set_green_link 1, the default) or the stub trainer's
+ * hot-key chains (0), every other engine stream the rest.  0 = off; -1
+ * (default) = 8 SMs per 32 row components, at most 16. */
 int bp_set_green_sms(int32_t sms);
 /* {hot-partition SMs, rest SMs} of the partition in use ({0, 0} when off). */
 int bp_green_info(int32_t* out2);

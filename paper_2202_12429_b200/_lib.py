@@ -315,7 +315,7 @@ def lib() -> C.CDLL:
                 gl = os.environ.get("BAGPIPE_B200_GREEN_LINK")  # the green partition's small part: link streams
                 if gl:
                     check(lb.bp_set_green_link(int(gl)), "bp_set_green_link")
-                gr = os.environ.get("BAGPIPE_B200_GREEN_SMS")  # tuning knob: SMs of the hot-key partition
+                gr = os.environ.get("BAGPIPE_B200_GREEN_SMS")  # tuning knob: SMs requested for the small partition (-1 auto, 0 off)
                 if gr:
                     check(lb.bp_set_green_sms(int(gr)), "bp_set_green_sms")
                 ls_ = os.environ.get("BAGPIPE_B200_STUB_LONG_SMEM")  # tuning knob: chain CTA smem pad (bytes)

@@ -50,14 +50,16 @@ struct GreenPartition {
 };
 
 static GreenPartition g_green;
-// bp_set_green_sms: SMs of the small partition (0 = off).  Default: 4 SMs
-// for the engine's host-link streams (bp_set_green_link), measured on the CK
-// step with the planner thread: value 99.0-100.6M vs 89.3-97.1M samples/s,
-// e2e 92.5-95.3M vs 82.0-89.8M (profiles/round2/green_link_threaded/)
-// -1 (default) = auto at the first engine: 4 SMs per 16 row components
-// (the host-link bytes per row), at most 16 -- CK / Avazu (D=16) 4 SMs,
-// Terabyte (D=64) 16 (measured there: 71.1M samples/s with 16 SMs, 63.2M
-// with 4, 64.9M unpartitioned; profiles/round2/green_link_tb10/)
+// bp_set_green_sms: SMs requested for the small partition (0 = off); the
+// driver rounds a request up to its split granularity -- on B200 8 SMs
+// (bp_green_info reports the partition made).  Used for the engine's
+// host-link streams (bp_set_green_link), measured on the CK step with the
+// planner thread (8 SMs): value 99.0-100.6M vs 89.3-97.1M samples/s, e2e
+// 92.5-95.3M vs 82.0-89.8M (profiles/round2/green_link_threaded/).
+// -1 (default) = auto at the first engine: 8 SMs per 32 row components (the
+// host-link bytes per row), at most 16 -- CK / Avazu (D=16) 8 SMs, Terabyte
+// (D=64) 16 (measured there: 71.1M samples/s with 16 SMs, 63.2M with 8,
+// 64.9M unpartitioned; profiles/round2/green_link_tb10/)
 static int g_green_sms = -1;
 // bp_set_green_link: 1 = the small partition runs the host-link streams
 // (zero-copy prefetch, write-back) instead of the hot-key chains, so the
@@ -119,8 +121,8 @@ bool green_link_mode() { return g_green_link != 0; }
 
 void green_auto(int dim) {
   if (g_green_sms < 0) {
-    const int s = 4 * ((dim + 15) / 16);
-    g_green_sms = s < 4 ? 4 : (s > 16 ? 16 : s);
+    const int s = 8 * ((dim + 31) / 32);
+    g_green_sms = s < 8 ? 8 : (s > 16 ? 16 : s);
   }
 }
 
